@@ -1,0 +1,246 @@
+/*
+ * lbx.h -- C ABI of the B200-native in-situ cost assessment + load-balancing
+ * path (libLBX, built from paper_2104_11385_b200/csrc/).
+ *
+ * Every entry point returns 0 on success or a nonzero LBX_E* code; the
+ * message of the most recent failure on the calling thread is available from
+ * lbx_last_error().  The Python host layer maps LBX_EINVAL to ValueError
+ * (same message substrings the reference raises: "cap", "permutation",
+ * "curve", "length", ...), LBX_ECUDA to RuntimeError and LBX_EOOM to
+ * MemoryError.
+ *
+ * Ownership: the caller allocates every buffer (host or device) and keeps it
+ * alive for the duration of the call (for stream-ordered device calls: until
+ * the stream has drained).  The library never frees caller memory.  Opaque
+ * contexts are created and destroyed by explicit calls.  Host functions are
+ * reentrant; device functions are asynchronous on the caller's stream
+ * (`stream` is a cudaStream_t passed as void*; NULL = legacy default stream).
+ *
+ * Reference interface each entry replaces is cited as file:line under
+ * /root/reference/pkg/src/lbsim/.
+ */
+#ifndef LBX_H_
+#define LBX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LBX_OK 0
+#define LBX_EINVAL 1   /* contract violation -> ValueError              */
+#define LBX_ECUDA 2    /* CUDA runtime failure -> RuntimeError          */
+#define LBX_EOOM 3     /* device allocation failure -> MemoryError      */
+#define LBX_ERANGE 4   /* particle outside the box grid -> ValueError   */
+
+/* Last error message of the calling thread ("" if none). */
+const char* lbx_last_error(void);
+/* Library version string and the compute capability it was built for. */
+const char* lbx_version(void);
+
+/* ------------------------------------------------------------------------
+ * Device context: the look-back workspace and the device-resident step
+ * state (tile ticket, finished-CTA counter, look-back epoch, live particle
+ * count).  One context per device and stream of work.
+ * ---------------------------------------------------------------------- */
+typedef struct lbx_ctx lbx_ctx;
+
+/* capacity = max particles any call on this context will process. */
+int lbx_ctx_create(lbx_ctx** out, int device, int64_t capacity);
+int lbx_ctx_destroy(lbx_ctx* ctx);
+/* Grow the look-back workspace to at least `capacity` particles. */
+int lbx_ctx_reserve(lbx_ctx* ctx, int64_t capacity);
+/* Stream-ordered: set / read the device-resident live particle count. */
+int lbx_ctx_set_count(lbx_ctx* ctx, int64_t n, void* stream);
+int lbx_ctx_get_count(lbx_ctx* ctx, int64_t* n_host, void* stream); /* syncs */
+/* Persistent-grid size the step kernels launch with (0 = auto: resident
+ * CTAs per SM x SMs). */
+int lbx_ctx_set_grid(lbx_ctx* ctx, int ctas);
+
+/* ------------------------------------------------------------------------
+ * Drop-in kernels (reference plugin point 1, kernels.py:10-25).
+ * Array-of-structs [n][2] float64 device buffers, exactly the reference's
+ * argument layout.
+ * ---------------------------------------------------------------------- */
+
+/* Replaces _kernels.pyx:12-35 advance_particles (fallback
+ * _kernels_py.py:13-22): out_pos[m] = pos+vel of survivors (0 <= p < extent
+ * on both axes), out_vel[m] = their velocities, order preserved.  Single
+ * pass (decoupled look-back stable compaction).  *m_dev (device int64)
+ * receives m.  Buffers must not overlap. */
+int lbx_advance_particles(lbx_ctx* ctx, const double* pos, const double* vel,
+                          int64_t n, double extent_z, double extent_x,
+                          double* out_pos, double* out_vel, int64_t* m_dev,
+                          void* stream);
+
+/* Replaces _kernels.pyx:38-47 bin_particles: counts[nbz*nbx] (device int64,
+ * overwritten) of (int)(z/M)*nbx + (int)(x/M).  A position outside the grid
+ * (UB in the reference) sets *err_dev (device int64, may be NULL) nonzero. */
+int lbx_bin_particles(const double* pos, int64_t n, double box_size,
+                      int32_t nbz, int32_t nbx, int64_t* counts,
+                      int64_t* err_dev, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Fused device step (the hot path; replaces workload.py:286-300 advance +
+ * workload.py:303-311 true_work counts + cost.py:83-95 heuristic_cost, and
+ * adds the GpuClock tally of PAPER.md:170-173).
+ *
+ * Structure-of-arrays particle state z,x,vz,vx (float64, 16-byte aligned,
+ * capacity >= n + 2), updated IN PLACE: push, absorb, stable compaction,
+ * per-box counts of the survivors, heuristic cost, optional per-box clock64
+ * tally -- one kernel launch.  n is the context's device-resident count and
+ * is replaced by the survivor count.
+ *
+ * Outputs (device or mapped-pinned host pointers, any may be NULL):
+ *   counts_out[nb] int64   survivors per box (== bin_particles of result)
+ *   cost_out[nb]   double  wp*count + wc*cells, no FMA (cost.py:94)
+ *   clk_out[nb]    uint64  GpuClock tally (SM cycles attributed per box);
+ *                          requires flags & LBX_STEP_CLOCK
+ *   n_out          int64   survivor count
+ * ---------------------------------------------------------------------- */
+#define LBX_STEP_CLOCK 1u   /* fused GpuClock instrumentation             */
+
+typedef struct lbx_step_args {
+  double* z;
+  double* x;
+  double* vz;
+  double* vx;
+  double extent_z, extent_x;
+  double box_size;
+  int32_t nbz, nbx;
+  double w_particle, w_cell;   /* heuristic weights (cost.py:52-63)     */
+  double cells_per_box;        /* BoxArray.cells_per_box (M*M)          */
+  uint32_t flags;
+  int64_t* counts_out;
+  double* cost_out;
+  uint64_t* clk_out;
+  int64_t* n_out;
+  int64_t* err_out;            /* out-of-grid survivors (should be 0)   */
+} lbx_step_args;
+
+int lbx_push_step(lbx_ctx* ctx, const lbx_step_args* args, void* stream);
+
+/* Heuristic cost from counts on the device (cost.py:83-95), no FMA. */
+int lbx_heuristic_cost(const int64_t* counts, int32_t nboxes, double w_particle,
+                       double w_cell, double cells_per_box, double* cost,
+                       void* stream);
+
+/* ------------------------------------------------------------------------
+ * Host balancer (pure, reentrant, bit-exact with the reference's numpy
+ * arithmetic: sequential bincount sums, numpy pairwise sum for means and
+ * the SFC target, lexsort/argmin tie rules, exact swap expressions).
+ * owner/curve arrays are int64 box-indexed.
+ * ---------------------------------------------------------------------- */
+
+/* balancer.py:73-79 rank_loads: loads[R] = bincount(owner, weights=cost). */
+int lbx_rank_loads(const double* cost, const int64_t* owner, int64_t n,
+                   int32_t n_ranks, double* loads);
+/* balancer.py:82-99 efficiency_flagged: mean/max; all-zero -> 1.0 + flag. */
+int lbx_efficiency(const double* cost, const int64_t* owner, int64_t n,
+                   int32_t n_ranks, double* eff, int32_t* degenerate);
+/* balancer.py:102-179 knapsack_assign (LPT + cap + swap refinement). */
+int lbx_knapsack(const double* cost, int64_t n, int32_t n_ranks,
+                 double cap_factor, int64_t* owner);
+/* balancer.py:182-219 sfc_assign (greedy split of the curve). */
+int lbx_sfc(const double* cost, const int64_t* curve, int64_t n,
+            int32_t n_ranks, int64_t* owner);
+/* decomposition.py:137-168 morton_order (2D: axis 0 on even bits). */
+int lbx_morton_order(int32_t nbz, int32_t nbx, int64_t* curve);
+/* 3D extension (config C4; parity unpinned): axis 0 on bits 0,3,6,... */
+int lbx_morton_order_3d(int32_t nb0, int32_t nb1, int32_t nb2, int64_t* curve);
+/* decomposition.py:176-181 slab_mapping. */
+int lbx_slab_mapping(int64_t n_boxes, int32_t n_ranks, int64_t* owner);
+/* numpy pairwise float64 sum (used by .sum()/.mean(), balancer.py:93,199). */
+double lbx_pairwise_sum(const double* a, int64_t n);
+/* cost.py:98-113 measured_cost noise stream: out[i] = work[i]*(1+eps_i),
+ * eps from numpy PCG64(SeedSequence((seed, 0x6D656173, step))).uniform. */
+int lbx_measured_cost(const double* work, int64_t n, double amplitude,
+                      uint64_t seed, uint64_t step, double* out);
+
+/* ------------------------------------------------------------------------
+ * Native stepping runtime (replaces workload.py:388-470 run_simulation's
+ * per-step loop: advance -> assess -> should_attempt/attempt_rebalance ->
+ * step_walltime).  The Python layer builds the scenario (numpy init,
+ * kick velocities) and hands device buffers in; the loop then runs without
+ * Python in it.  Results are left in caller-provided host arrays.
+ * ---------------------------------------------------------------------- */
+typedef struct lbx_sim lbx_sim;
+
+#define LBX_COST_HEURISTIC 0     /* device counts -> heuristic cost          */
+#define LBX_COST_MEASURED 1      /* modeled timer: true work x PCG64 noise   */
+#define LBX_COST_INSTRUMENTED 2  /* same stream, overhead factor applied    */
+#define LBX_COST_GPUCLOCK 3      /* fused clock64 tally (real device cost)   */
+
+#define LBX_STRATEGY_KNAPSACK 0
+#define LBX_STRATEGY_SFC 1
+
+typedef struct lbx_sim_config {
+  /* geometry */
+  int32_t extent_z, extent_x, box_size, n_ranks;
+  /* per-step scheduling */
+  int64_t total_steps;
+  int64_t kick_step;           /* step whose advance uses the kick velocity */
+  /* balance policy (balancer.py:31-59) */
+  int32_t strategy;            /* LBX_STRATEGY_*                              */
+  int64_t interval;
+  double improvement_threshold;
+  int32_t threshold_relative;  /* 1 relative, 0 absolute                      */
+  double cap_factor;
+  int64_t static_step;         /* -1 = none                                   */
+  /* cost provider (cost.py:153-215) */
+  int32_t cost_kind;           /* LBX_COST_*                                  */
+  double w_particle, w_cell;   /* provider heuristic weights                  */
+  double noise_amplitude;
+  uint64_t noise_seed;
+  double overhead_factor;
+  /* ground-truth work weights (workload.py:100) */
+  double work_wp, work_wc;
+  /* walltime model (workload.py:72-86, resolved) */
+  double comm_per_face, gather, redistribute_per_particle, redistribute_latency;
+  int64_t capacity_particles;  /* -1 = unlimited                              */
+} lbx_sim_config;
+
+/* Per-step outputs, host arrays of length total_steps (caller-owned). */
+typedef struct lbx_sim_outputs {
+  double* eff_before;
+  double* eff_after;
+  uint8_t* adopted;
+  uint8_t* attempted;
+  double* compute_max;
+  double* comm_max;
+  double* gather;
+  double* redistribute;
+  double* walltime;
+  int64_t* max_rank_particles;
+  uint8_t* oom;
+  int64_t* n_alive;            /* survivors after the step                  */
+  double* cost_trace;          /* [total_steps][n_boxes]                    */
+  int64_t* count_trace;        /* [total_steps][n_boxes] or NULL            */
+  uint64_t* clock_trace;       /* [total_steps][n_boxes] or NULL            */
+  int64_t* owner;              /* [n_boxes] in: initial mapping; out: final */
+  /* adoption snapshots: step index per adoption and owner rows */
+  int64_t* adopt_steps;        /* [total_steps]                              */
+  int64_t* adopt_owners;       /* [total_steps][n_boxes] or NULL            */
+  int64_t n_adoptions;         /* out                                        */
+  int64_t n_attempts;          /* out                                        */
+  int64_t completed_steps;     /* out                                        */
+} lbx_sim_outputs;
+
+int lbx_sim_create(lbx_sim** out, lbx_ctx* ctx, const lbx_sim_config* cfg);
+int lbx_sim_destroy(lbx_sim* sim);
+/* Particle buffers (device SoA, capacity >= n + 2); kick_vz/kick_vx replace
+ * the velocity buffers at kick_step (pointer swap, no copy). */
+int lbx_sim_set_particles(lbx_sim* sim, double* z, double* x, double* vz,
+                          double* vx, double* kick_vz, double* kick_vx,
+                          int64_t n, void* stream);
+/* Run steps [first, last) of the loop; outputs indexed by absolute step. */
+int lbx_sim_run(lbx_sim* sim, int64_t first, int64_t last,
+                lbx_sim_outputs* out, void* stream);
+/* Current device live count (syncs the stream). */
+int lbx_sim_particles(lbx_sim* sim, int64_t* n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LBX_H_ */

@@ -1,0 +1,426 @@
+// libLBX host balancer: distribution-mapping policies and load-balance
+// efficiency, bit-exact with the reference's numpy arithmetic.
+//
+// Why C++ and not numpy: the reference knapsack costs 5-56 ms per call at 900
+// boxes ("Where time goes"), which would dwarf a microsecond
+// device step.  Bit-exactness rules followed here (compiled with
+// -ffp-contract=off so no FMA is formed):
+//   * np.bincount(weights=) accumulates sequentially in input order;
+//   * ndarray.sum()/.mean() use numpy's pairwise summation (8 accumulators,
+//     blocks of 128, recursive split at n/2 rounded down to a multiple of 8);
+//   * np.lexsort((arange, -cost)) == sort by cost descending, id ascending;
+//   * np.argmin returns the first minimum;
+//   * the swap search evaluates (load_max - c_a) + c_b and
+//     (load_other - c_b) + c_a exactly as balancer.py:163-164 does.
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <numeric>
+#include <vector>
+
+#include "lbx_internal.h"
+
+namespace lbx {
+
+double pairwise_sum(const double* a, int64_t n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; ++i) r += a[i];
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i];
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return pairwise_sum(a, n2) + pairwise_sum(a + n2, n - n2);
+}
+
+namespace {
+
+int check_owner(const int64_t* owner, int64_t n, int32_t R) {
+  for (int64_t i = 0; i < n; ++i)
+    if (owner[i] < 0 || owner[i] >= R)
+      return set_error(LBX_EINVAL, "owner entries must lie in [0, %d), got %lld at box %lld", R,
+                       (long long)owner[i], (long long)i);
+  return LBX_OK;
+}
+
+void loads_of(const double* cost, const int64_t* owner, int64_t n, int32_t R, double* loads) {
+  std::fill(loads, loads + R, 0.0);
+  for (int64_t i = 0; i < n; ++i) loads[owner[i]] += cost[i];
+}
+
+// balancer.py:137-179.  Only swaps that involve the unique most-loaded rank
+// can lower the maximum; best strict improvement wins, ties to the lowest
+// own box id, then the lowest partner box id.
+void refine_by_swaps(int64_t* owner, double* loads, const double* v, int64_t n, int32_t R) {
+  if (R < 2 || n < 2) return;
+  std::vector<int64_t> mine, others;
+  std::vector<double> other_load;
+  mine.reserve(n);
+  others.reserve(n);
+  other_load.reserve(n);
+  while (true) {
+    double top = loads[0];
+    for (int32_t r = 1; r < R; ++r) top = std::max(top, loads[r]);
+    int32_t rmax = -1, at_top = 0;
+    for (int32_t r = 0; r < R; ++r)
+      if (loads[r] == top) {
+        if (at_top == 0) rmax = r;
+        ++at_top;
+      }
+    if (at_top != 1) return;
+    mine.clear();
+    others.clear();
+    other_load.clear();
+    for (int64_t b = 0; b < n; ++b) {
+      if (owner[b] == rmax) {
+        mine.push_back(b);
+      } else {
+        others.push_back(b);
+        other_load.push_back(loads[owner[b]]);
+      }
+    }
+    if (mine.empty() || others.empty()) return;
+    bool have = false;
+    double best_pm = 0.0;
+    int64_t best_a = -1, best_b = -1;
+    const int64_t no = (int64_t)others.size();
+    for (int64_t a : mine) {
+      const double ca = v[a];
+      const double here0 = top - ca;
+      int64_t jbest = -1;
+      double pm_best = 0.0;
+      for (int64_t j = 0; j < no; ++j) {
+        const double cb = v[others[j]];
+        const double here = here0 + cb;
+        const double there = (other_load[j] - cb) + ca;
+        const double pm = here >= there ? here : there;
+        if (pm < top && (jbest < 0 || pm < pm_best)) {
+          jbest = j;
+          pm_best = pm;
+        }
+      }
+      if (jbest < 0) continue;
+      if (!have || pm_best < best_pm) {
+        have = true;
+        best_pm = pm_best;
+        best_a = a;
+        best_b = others[jbest];
+      }
+    }
+    if (!have) return;
+    const int64_t rb = owner[best_b];
+    loads[rmax] += v[best_b] - v[best_a];
+    loads[rb] += v[best_a] - v[best_b];
+    owner[best_a] = rb;
+    owner[best_b] = rmax;
+  }
+}
+
+uint64_t spread2(uint64_t v) {
+  uint64_t out = 0;
+  for (int s = 0; v; ++s, v >>= 1) out |= (v & 1ull) << (2 * s);
+  return out;
+}
+
+uint64_t spread3(uint64_t v) {
+  uint64_t out = 0;
+  for (int s = 0; v; ++s, v >>= 1) out |= (v & 1ull) << (3 * s);
+  return out;
+}
+
+void stable_argsort(const std::vector<uint64_t>& codes, int64_t* out) {
+  std::vector<int64_t> idx(codes.size());
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(),
+                   [&](int64_t a, int64_t b) { return codes[a] < codes[b]; });
+  std::copy(idx.begin(), idx.end(), out);
+}
+
+// ---- numpy SeedSequence + PCG64 (XSL-RR 128/64) --------------------------
+constexpr uint32_t kInitA = 0x43b0d7e5u, kMultA = 0x931e8875u;
+constexpr uint32_t kInitB = 0x8b51f9ddu, kMultB = 0x58f38dedu;
+constexpr uint32_t kMixL = 0xca01f9ddu, kMixR = 0x4973f715u;
+
+uint32_t hashmix(uint32_t value, uint32_t& h) {
+  value ^= h;
+  h *= kMultA;
+  value *= h;
+  value ^= value >> 16;
+  return value;
+}
+
+uint32_t mix(uint32_t x, uint32_t y) {
+  uint32_t r = kMixL * x - kMixR * y;
+  r ^= r >> 16;
+  return r;
+}
+
+void int_words(uint64_t v, std::vector<uint32_t>& out) {
+  if (v == 0) {
+    out.push_back(0u);
+    return;
+  }
+  while (v) {
+    out.push_back((uint32_t)v);
+    v >>= 32;
+  }
+}
+
+struct Pcg64 {
+  unsigned __int128 state, inc;
+  static unsigned __int128 mult() {
+    return ((unsigned __int128)2549297995355413924ull << 64) | 4865540595714422341ull;
+  }
+  void step() { state = state * mult() + inc; }
+  uint64_t next64() {
+    step();
+    const uint64_t x = (uint64_t)(state >> 64) ^ (uint64_t)state;
+    const unsigned rot = (unsigned)(state >> 122);
+    return (x >> rot) | (x << ((64 - rot) & 63));
+  }
+  double next_double() { return (double)(next64() >> 11) * (1.0 / 9007199254740992.0); }
+};
+
+// np.random.default_rng(entropy words) -> PCG64.
+Pcg64 make_pcg64(const std::vector<uint32_t>& entropy) {
+  uint32_t pool[4];
+  uint32_t h = kInitA;
+  for (size_t i = 0; i < 4; ++i) pool[i] = hashmix(i < entropy.size() ? entropy[i] : 0u, h);
+  for (int s = 0; s < 4; ++s)
+    for (int d = 0; d < 4; ++d)
+      if (s != d) pool[d] = mix(pool[d], hashmix(pool[s], h));
+  for (size_t s = 4; s < entropy.size(); ++s)
+    for (int d = 0; d < 4; ++d) pool[d] = mix(pool[d], hashmix(entropy[s], h));
+  uint32_t words[8];
+  uint32_t hb = kInitB;
+  for (int i = 0; i < 8; ++i) {
+    uint32_t v = pool[i % 4];
+    v ^= hb;
+    hb *= kMultB;
+    v *= hb;
+    v ^= v >> 16;
+    words[i] = v;
+  }
+  uint64_t val[4];
+  for (int i = 0; i < 4; ++i) val[i] = (uint64_t)words[2 * i] | ((uint64_t)words[2 * i + 1] << 32);
+  const unsigned __int128 initstate = ((unsigned __int128)val[0] << 64) | val[1];
+  const unsigned __int128 initseq = ((unsigned __int128)val[2] << 64) | val[3];
+  Pcg64 g;
+  g.state = 0;
+  g.inc = (initseq << 1) | 1u;
+  g.step();
+  g.state += initstate;
+  g.step();
+  return g;
+}
+
+}  // namespace
+
+// cost.py:98-113 (work * (1 + U[-a, a]) per box, stream keyed by step).
+int measured_cost(const double* work, int64_t n, double amplitude, uint64_t seed, uint64_t step,
+                  double* out) {
+  if (amplitude == 0.0) {
+    std::memcpy(out, work, (size_t)n * sizeof(double));
+    return LBX_OK;
+  }
+  std::vector<uint32_t> ent;
+  int_words(seed, ent);
+  int_words(0x6D656173ull, ent);
+  int_words(step, ent);
+  Pcg64 g = make_pcg64(ent);
+  const double lo = -amplitude;
+  const double scale = amplitude - lo;
+  for (int64_t i = 0; i < n; ++i) {
+    const double eps = lo + scale * g.next_double();
+    out[i] = work[i] * (1.0 + eps);
+  }
+  return LBX_OK;
+}
+
+int efficiency(const double* cost, const int64_t* owner, int64_t n, int32_t R, double* eff,
+               int32_t* degenerate, std::vector<double>& scratch) {
+  scratch.resize(R);
+  loads_of(cost, owner, n, R, scratch.data());
+  double top = scratch[0];
+  for (int32_t r = 1; r < R; ++r) top = std::max(top, scratch[r]);
+  if (top == 0.0) {
+    *eff = 1.0;
+    if (degenerate) *degenerate = 1;
+    return LBX_OK;
+  }
+  const double mean = pairwise_sum(scratch.data(), R) / (double)R;
+  *eff = mean / top;
+  if (degenerate) *degenerate = 0;
+  return LBX_OK;
+}
+
+int knapsack(const double* v, int64_t n, int32_t R, double cap_factor, int64_t* owner) {
+  if (R < 1) return set_error(LBX_EINVAL, "n_ranks must be >= 1, got %d", R);
+  const int64_t cap = n ? (int64_t)std::ceil(cap_factor * (double)n / (double)R) : 0;
+  if (cap * R < n)
+    return set_error(LBX_EINVAL,
+                     "box cap %lld per rank cannot place %lld boxes on %d ranks "
+                     "(cap_factor %g too tight)",
+                     (long long)cap, (long long)n, R, cap_factor);
+  std::vector<int64_t> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+    if (v[a] > v[b]) return true;
+    if (v[b] > v[a]) return false;
+    return a < b;
+  });
+  std::vector<double> loads(R, 0.0);
+  std::vector<int64_t> count(R, 0);
+  const double inf = std::numeric_limits<double>::infinity();
+  for (int64_t b : order) {
+    int32_t r = 0;
+    double best = count[0] < cap ? loads[0] : inf;
+    for (int32_t k = 1; k < R; ++k) {
+      const double m = count[k] < cap ? loads[k] : inf;
+      if (m < best) {
+        best = m;
+        r = k;
+      }
+    }
+    owner[b] = r;
+    loads[r] += v[b];
+    count[r] += 1;
+  }
+  refine_by_swaps(owner, loads.data(), v, n, R);
+  return LBX_OK;
+}
+
+int sfc(const double* cost, const int64_t* curve, int64_t n, int32_t R, int64_t* owner) {
+  if (R < 1) return set_error(LBX_EINVAL, "n_ranks must be >= 1, got %d", R);
+  if (n == 0) return set_error(LBX_EINVAL, "cannot partition an empty cost vector");
+  std::vector<char> seen(n, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    if (curve[i] < 0 || curve[i] >= n || seen[curve[i]])
+      return set_error(LBX_EINVAL, "curve must be a permutation of box indices");
+    seen[curve[i]] = 1;
+  }
+  std::vector<double> along(n);
+  for (int64_t i = 0; i < n; ++i) along[i] = cost[curve[i]];
+  const double target = pairwise_sum(along.data(), n) / (double)R;
+  int64_t i = 0;
+  for (int32_t r = 0; r < R; ++r) {
+    if (i == n) break;
+    if (r == R - 1) {
+      for (int64_t k = i; k < n; ++k) owner[curve[k]] = r;
+      break;
+    }
+    const int64_t start = i;
+    double seg = along[i];
+    ++i;
+    const int64_t reserve = R - r - 1;
+    while (i < n - reserve) {
+      const double nxt = along[i];
+      if (std::fabs(seg + nxt - target) > std::fabs(seg - target)) break;
+      seg += nxt;
+      ++i;
+    }
+    for (int64_t k = start; k < i; ++k) owner[curve[k]] = r;
+  }
+  return LBX_OK;
+}
+
+}  // namespace lbx
+
+using namespace lbx;
+
+extern "C" {
+
+double lbx_pairwise_sum(const double* a, int64_t n) { return n > 0 ? pairwise_sum(a, n) : 0.0; }
+
+int lbx_rank_loads(const double* cost, const int64_t* owner, int64_t n, int32_t R, double* loads) {
+  clear_error();
+  if (R < 1) return set_error(LBX_EINVAL, "n_ranks must be >= 1, got %d", R);
+  int rc = check_owner(owner, n, R);
+  if (rc) return rc;
+  loads_of(cost, owner, n, R, loads);
+  return LBX_OK;
+}
+
+int lbx_efficiency(const double* cost, const int64_t* owner, int64_t n, int32_t R, double* eff,
+                   int32_t* degenerate) {
+  clear_error();
+  if (R < 1) return set_error(LBX_EINVAL, "n_ranks must be >= 1, got %d", R);
+  int rc = check_owner(owner, n, R);
+  if (rc) return rc;
+  std::vector<double> scratch;
+  return efficiency(cost, owner, n, R, eff, degenerate, scratch);
+}
+
+int lbx_knapsack(const double* cost, int64_t n, int32_t R, double cap_factor, int64_t* owner) {
+  clear_error();
+  return knapsack(cost, n, R, cap_factor, owner);
+}
+
+int lbx_sfc(const double* cost, const int64_t* curve, int64_t n, int32_t R, int64_t* owner) {
+  clear_error();
+  return sfc(cost, curve, n, R, owner);
+}
+
+int lbx_morton_order(int32_t nbz, int32_t nbx, int64_t* curve) {
+  clear_error();
+  if (nbz < 0 || nbx < 0) return set_error(LBX_EINVAL, "box grid must be nonnegative");
+  const int64_t n = (int64_t)nbz * nbx;
+  std::vector<uint64_t> codes(n);
+  for (int64_t i = 0; i < n; ++i) codes[i] = spread2(i / nbx) | (spread2(i % nbx) << 1);
+  stable_argsort(codes, curve);
+  return LBX_OK;
+}
+
+int lbx_morton_order_3d(int32_t nb0, int32_t nb1, int32_t nb2, int64_t* curve) {
+  clear_error();
+  if (nb0 < 0 || nb1 < 0 || nb2 < 0) return set_error(LBX_EINVAL, "box grid must be nonnegative");
+  const int64_t n = (int64_t)nb0 * nb1 * nb2;
+  std::vector<uint64_t> codes(n);
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t a = i / ((int64_t)nb1 * nb2), b = (i / nb2) % nb1, c = i % nb2;
+    codes[i] = spread3(a) | (spread3(b) << 1) | (spread3(c) << 2);
+  }
+  stable_argsort(codes, curve);
+  return LBX_OK;
+}
+
+int lbx_slab_mapping(int64_t n_boxes, int32_t R, int64_t* owner) {
+  clear_error();
+  if (R < 1) return set_error(LBX_EINVAL, "n_ranks must be >= 1, got %d", R);
+  if (n_boxes <= 0) return LBX_OK;
+  // np.linspace(0, n_boxes, R + 1): edge_i = i * (n/R), last edge = n exactly.
+  std::vector<double> edges(R + 1);
+  const double step = (double)n_boxes / (double)R;
+  for (int32_t i = 0; i <= R; ++i) edges[i] = (double)i * step + 0.0;
+  edges[R] = (double)n_boxes;
+  for (int64_t j = 0; j < n_boxes; ++j) {
+    // searchsorted(edges, j, side='right') - 1, clipped to [0, R-1]
+    const double x = (double)j;
+    const int64_t pos = std::upper_bound(edges.begin(), edges.end(), x) - edges.begin();
+    owner[j] = std::min<int64_t>(std::max<int64_t>(pos - 1, 0), R - 1);
+  }
+  return LBX_OK;
+}
+
+int lbx_measured_cost(const double* work, int64_t n, double amplitude, uint64_t seed,
+                      uint64_t step, double* out) {
+  clear_error();
+  if (n < 0) return set_error(LBX_EINVAL, "length must be >= 0");
+  for (int64_t i = 0; i < n; ++i)
+    if (work[i] < 0) return set_error(LBX_EINVAL, "true work must be nonnegative");
+  return measured_cost(work, n, amplitude, seed, step, out);
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// Internal declarations shared by the libLBX translation units.
+#pragma once
+
+#include <cstdarg>
+#include <cstdint>
+#include <string>
+
+#include "lbx.h"
+
+namespace lbx {
+
+// Thread-local last-error slot behind lbx_last_error().
+int set_error(int code, const char* fmt, ...);
+void clear_error();
+
+// Device-resident step state (one per context).  Written only by the
+// kernels' last CTA (epilogue) and by stream-ordered host memcpys.
+struct DevState {
+  unsigned long long ticket;  // next tile ticket (reset to 0 by the epilogue)
+  unsigned int done;          // CTAs finished (reset to 0 by the epilogue)
+  unsigned int epoch;         // look-back epoch tag, 1..2^22-1
+  long long n;                // live particles (input count of the next step)
+  long long err;              // cumulative out-of-grid survivors
+};
+
+// Host-side model of the particle state's pushed-and-binned step.
+struct StepLaunch {
+  double *z, *x, *vz, *vx;
+  double ez, ex, m;
+  int nbz, nbx;
+  double wp, wc, cells;
+  bool clock;
+  long long* counts_out;
+  double* cost_out;
+  unsigned long long* clk_out;
+  long long* n_out;
+  long long* err_out;
+};
+
+}  // namespace lbx
+
+struct lbx_ctx {
+  int device = 0;
+  int num_sms = 0;
+  lbx::DevState* st = nullptr;        // device
+  unsigned long long* status = nullptr;  // look-back tile status words
+  int64_t status_tiles = 0;
+  unsigned long long* acc = nullptr;  // per-box accumulators [2][acc_boxes]
+  int32_t acc_boxes = 0;
+  int64_t n_upper = 0;                // host upper bound on the live count
+  int grid_override = 0;
+  int64_t* host_scratch = nullptr;    // pinned
+};
+
+#include <vector>
+
+namespace lbx {
+// Implemented in lbx_balancer.cpp.
+double pairwise_sum(const double* a, int64_t n);
+int efficiency(const double* cost, const int64_t* owner, int64_t n, int32_t R, double* eff,
+               int32_t* degenerate, std::vector<double>& scratch);
+int knapsack(const double* v, int64_t n, int32_t R, double cap_factor, int64_t* owner);
+int sfc(const double* cost, const int64_t* curve, int64_t n, int32_t R, int64_t* owner);
+int measured_cost(const double* work, int64_t n, double amplitude, uint64_t seed, uint64_t step,
+                  double* out);
+// Implemented in lbx_kernels.cu.
+int launch_push_step(lbx_ctx* ctx, const StepLaunch& a, void* stream);
+int ensure_accumulators(lbx_ctx* ctx, int32_t nboxes);
+}  // namespace lbx

@@ -1,0 +1,819 @@
+// libLBX device kernels for sm_100a.
+//
+// The hot path of the reference is two CPU loops per step:
+//   advance_particles  (_kernels.pyx:12-35): x += v, absorb, stable compaction
+//   bin_particles      (_kernels.pyx:38-47): per-box survivor counts
+// followed by heuristic_cost (cost.py:83-95) and, for the paper's GpuClock
+// strategy, an on-device per-box cycle tally.
+//
+// B200 design: ONE persistent kernel per step does all of it in a single pass
+// over HBM.  Particles are SoA float64 (z, x, vz, vx), updated in place.
+//   * tiles of 2048 particles are claimed in order from a device ticket;
+//   * each thread loads 4 x (2 particles) with 16-byte vector loads;
+//   * push + absorbing test in registers;
+//   * per-box counts and GpuClock cycles are run-length aggregated per
+//     thread, warp-reduced with redux.sync when the warp sits in one box, and
+//     accumulated in a shared-memory histogram that each CTA flushes once
+//     (one atomicAdd per box per CTA);
+//   * stable compaction uses a decoupled look-back scan over tile survivor
+//     counts; a tile with no absorbed particles at or before it rewrites only
+//     z and x in place (48 B/particle total traffic), otherwise survivors are
+//     written to their compacted slots (safe in place: every predecessor has
+//     loaded its tile before it publishes its status);
+//   * the last CTA to finish forms the cost vector (wp*count + wc*cells with
+//     separately rounded products, cost.py:94), writes the step outputs
+//     (optionally into mapped pinned host memory), zeroes the accumulators
+//     and advances the device-resident count/epoch -- so consecutive steps
+//     need no host round trip.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "lbx_internal.h"
+
+namespace lbx {
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kWarps = kBlock / 32;
+constexpr int kItems = 8;                 // particles per thread per tile
+constexpr int kTile = kBlock * kItems;    // 2048 particles per tile
+constexpr int kSmemBoxesMax = 8192;       // shared-memory histogram limit
+constexpr unsigned kFull = 0xffffffffu;
+
+constexpr int kEpochShift = 42;
+constexpr int kFlagShift = 40;
+constexpr unsigned long long kValueMask = (1ull << kFlagShift) - 1;
+constexpr unsigned long long kFlagAgg = 1ull;
+constexpr unsigned long long kFlagPfx = 2ull;
+constexpr unsigned kEpochMask = (1u << 22) - 1;
+
+enum Layout { kSoAInPlace = 0, kAoSOutOfPlace = 1 };
+
+struct PushParams {
+  // SoA (in place)
+  double* z;
+  double* x;
+  double* vz;
+  double* vx;
+  // AoS (drop-in, out of place)
+  const double2* in_pos;
+  const double2* in_vel;
+  double2* out_pos;
+  double2* out_vel;
+  double ez, ex, m;
+  int nbz, nbx, nb;
+  int smem_hist;
+  long long n_override;        // >= 0: particle count given by the host
+  DevState* st;
+  unsigned long long* status;
+  unsigned long long* g_cnt;
+  unsigned long long* g_clk;
+  long long* counts_out;
+  double* cost_out;
+  unsigned long long* clk_out;
+  long long* n_out;
+  long long* err_out;
+  double wp, wc, cells;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long pack_status(unsigned epoch,
+                                                          unsigned long long flag,
+                                                          unsigned long long value) {
+  return ((unsigned long long)epoch << kEpochShift) | (flag << kFlagShift) | value;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// Exclusive prefix of survivors over all tiles before `tile` (warp 0 only).
+// Reads a window of 32 predecessors per iteration; stops at the nearest one
+// that has published its inclusive prefix.
+__device__ long long lookback(unsigned long long* status, long long tile, unsigned epoch) {
+  const int lane = threadIdx.x & 31;
+  long long acc = 0;
+  long long top = tile - 1;
+  while (true) {
+    const long long idx = top - lane;
+    unsigned long long s = 0;
+    unsigned long long flag = kFlagPfx;  // virtual predecessor of tile 0
+    if (idx >= 0) {
+      do {
+        s = ld_acquire(status + idx);
+        flag = ((unsigned)(s >> kEpochShift) == epoch) ? ((s >> kFlagShift) & 3ull) : 0ull;
+      } while (flag == 0ull);
+    }
+    const long long val = (long long)(s & kValueMask);
+    const unsigned pfx = __ballot_sync(kFull, flag == kFlagPfx);
+    if (pfx) {
+      const int first = __ffs(pfx) - 1;  // nearest predecessor with a prefix
+      acc += warp_sum_ll(lane <= first ? val : 0ll);
+      return acc;
+    }
+    acc += warp_sum_ll(val);
+    top -= 32;
+  }
+}
+
+template <bool kClock>
+__device__ __forceinline__ void hist_add(const PushParams& p, unsigned* s_cnt,
+                                         unsigned long long* s_clk, int b, unsigned cnt,
+                                         unsigned clk) {
+  if (p.smem_hist) {
+    atomicAdd(s_cnt + b, cnt);
+    if (kClock) atomicAdd(s_clk + b, (unsigned long long)clk);
+  } else {
+    atomicAdd(p.g_cnt + b, (unsigned long long)cnt);
+    if (kClock) atomicAdd(p.g_clk + b, (unsigned long long)clk);
+  }
+}
+
+template <int kLayout, bool kHist, bool kClock>
+__global__ void __launch_bounds__(kBlock, 2) push_kernel(PushParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned long long* s_clk = reinterpret_cast<unsigned long long*>(smem_raw);
+  unsigned* s_cnt = reinterpret_cast<unsigned*>(smem_raw + (kClock ? 8 * p.nb : 0));
+
+  __shared__ long long s_tile;
+  __shared__ long long s_prefix;
+  __shared__ int s_last;
+  __shared__ long long s_n;
+  __shared__ unsigned s_epoch;
+  constexpr int kRows = (kLayout == kSoAInPlace) ? kItems / 2 : kItems;
+  __shared__ int s_row[kRows * kWarps];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+
+  if (tid == 0) {
+    s_n = p.n_override >= 0 ? p.n_override : *((volatile long long*)&p.st->n);
+    s_epoch = *((volatile unsigned*)&p.st->epoch);
+  }
+  if (kHist && p.smem_hist) {
+    for (int b = tid; b < p.nb; b += kBlock) {
+      s_cnt[b] = 0u;
+      if (kClock) s_clk[b] = 0ull;
+    }
+  }
+  __syncthreads();
+  const long long n = s_n;
+  const unsigned epoch = s_epoch;
+  const long long ntiles = (n + kTile - 1) / kTile;
+  long long err = 0;
+
+  while (true) {
+    if (tid == 0) s_tile = (long long)atomicAdd(&p.st->ticket, 1ull);
+    __syncthreads();
+    const long long tile = s_tile;
+    if (tile >= ntiles) break;
+    const long long base = tile * kTile;
+    const long long valid = min((long long)kTile, n - base);
+
+    long long t0 = 0;
+    if (kClock) t0 = clock64();
+
+    double pz[kItems], px[kItems], pvz[kItems], pvx[kItems];
+    bool keep[kItems];
+
+    if (kLayout == kSoAInPlace) {
+      const double2* z2 = reinterpret_cast<const double2*>(p.z);
+      const double2* x2 = reinterpret_cast<const double2*>(p.x);
+      const double2* vz2 = reinterpret_cast<const double2*>(p.vz);
+      const double2* vx2 = reinterpret_cast<const double2*>(p.vx);
+#pragma unroll
+      for (int r = 0; r < kItems / 2; ++r) {
+        const long long q = (base >> 1) + r * kBlock + tid;  // pair index
+        const long long i0 = 2 * q;
+        double2 a = make_double2(0.0, 0.0), b = a, c = a, d = a;
+        if (i0 < n) {
+          a = __ldcs(z2 + q);
+          b = __ldcs(x2 + q);
+          c = __ldcs(vz2 + q);
+          d = __ldcs(vx2 + q);
+        }
+        pvz[2 * r] = c.x;
+        pvz[2 * r + 1] = c.y;
+        pvx[2 * r] = d.x;
+        pvx[2 * r + 1] = d.y;
+        pz[2 * r] = __dadd_rn(a.x, c.x);
+        pz[2 * r + 1] = __dadd_rn(a.y, c.y);
+        px[2 * r] = __dadd_rn(b.x, d.x);
+        px[2 * r + 1] = __dadd_rn(b.y, d.y);
+        keep[2 * r] = i0 < n;
+        keep[2 * r + 1] = i0 + 1 < n;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < kItems; ++r) {
+        const long long i = base + r * kBlock + tid;
+        double2 a = make_double2(0.0, 0.0), c = a;
+        if (i < n) {
+          a = __ldcs(p.in_pos + i);
+          c = __ldcs(p.in_vel + i);
+        }
+        pvz[r] = c.x;
+        pvx[r] = c.y;
+        pz[r] = __dadd_rn(a.x, c.x);
+        px[r] = __dadd_rn(a.y, c.y);
+        keep[r] = i < n;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      keep[k] = keep[k] && pz[k] >= 0.0 && pz[k] < p.ez && px[k] >= 0.0 && px[k] < p.ex;
+    }
+
+    // ---- per-box counts + GpuClock tally (survivors, new positions) ----
+    if (kHist) {
+      int box[kItems];
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        box[k] = -1;
+        if (keep[k]) {
+          const int bz = (int)__ddiv_rn(pz[k], p.m);
+          const int bx = (int)__ddiv_rn(px[k], p.m);
+          if (bz < p.nbz && bx < p.nbx) {
+            box[k] = bz * p.nbx + bx;
+          } else {
+            ++err;
+          }
+        }
+      }
+      unsigned dt = 0;
+      if (kClock) {
+        const long long t1 = clock64();
+        dt = (unsigned)min(t1 - t0, (long long)(1 << 22));
+      }
+      int cur = -1;
+      unsigned run = 0;
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        if (box[k] != cur) {
+          if (cur >= 0) hist_add<kClock>(p, s_cnt, s_clk, cur, run, dt * run);
+          cur = box[k];
+          run = 0;
+        }
+        run += (box[k] >= 0) ? 1u : 0u;
+      }
+      const int cur0 = __shfl_sync(kFull, cur, 0);
+      if (__all_sync(kFull, cur == cur0)) {
+        const unsigned tot = __reduce_add_sync(kFull, run);
+        const unsigned clk = kClock ? __reduce_add_sync(kFull, dt * run) : 0u;
+        if (lane == 0 && cur0 >= 0 && tot) hist_add<kClock>(p, s_cnt, s_clk, cur0, tot, clk);
+      } else if (cur >= 0 && run) {
+        hist_add<kClock>(p, s_cnt, s_clk, cur, run, dt * run);
+      }
+    }
+
+    // ---- tile-local ranks of survivors (tile order = index order) ----
+    int pre[kItems];
+    const unsigned lt = lanemask_lt();
+    if (kLayout == kSoAInPlace) {
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) {
+        const unsigned b0 = __ballot_sync(kFull, keep[2 * r]);
+        const unsigned b1 = __ballot_sync(kFull, keep[2 * r + 1]);
+        pre[2 * r] = __popc(b0 & lt) + __popc(b1 & lt);
+        pre[2 * r + 1] = pre[2 * r] + (keep[2 * r] ? 1 : 0);
+        if (lane == 0) s_row[r * kWarps + warp] = __popc(b0) + __popc(b1);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) {
+        const unsigned b0 = __ballot_sync(kFull, keep[r]);
+        pre[r] = __popc(b0 & lt);
+        if (lane == 0) s_row[r * kWarps + warp] = __popc(b0);
+      }
+    }
+    __syncthreads();
+
+    // ---- warp 0: scan row counts, publish, look back ----
+    if (warp == 0) {
+      constexpr int kPer = (kRows * kWarps) / 32;
+      int v[kPer];
+      int sum = 0;
+#pragma unroll
+      for (int e = 0; e < kPer; ++e) {
+        v[e] = s_row[lane * kPer + e];
+        sum += v[e];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int total = __shfl_sync(kFull, incl, 31);
+      int run_off = incl - sum;
+#pragma unroll
+      for (int e = 0; e < kPer; ++e) {
+        s_row[lane * kPer + e] = run_off;
+        run_off += v[e];
+      }
+      long long prefix = 0;
+      if (tile == 0) {
+        if (lane == 0) {
+          __threadfence();
+          st_release(p.status, pack_status(epoch, kFlagPfx, (unsigned long long)total));
+        }
+      } else {
+        if (lane == 0) {
+          __threadfence();
+          st_release(p.status + tile, pack_status(epoch, kFlagAgg, (unsigned long long)total));
+        }
+        prefix = lookback(p.status, tile, epoch);
+        if (lane == 0) {
+          st_release(p.status + tile,
+                     pack_status(epoch, kFlagPfx, (unsigned long long)(prefix + total)));
+        }
+      }
+      if (lane == 0) {
+        s_prefix = prefix;
+        s_last = total;  // reuse as tile survivor count for the fast-path test
+      }
+    }
+    __syncthreads();
+    const long long prefix = s_prefix;
+    const bool fast = (prefix == base) && ((long long)s_last == valid);
+
+    // ---- stores ----
+    if (kLayout == kSoAInPlace) {
+      if (fast) {
+        double2* z2 = reinterpret_cast<double2*>(p.z);
+        double2* x2 = reinterpret_cast<double2*>(p.x);
+#pragma unroll
+        for (int r = 0; r < kItems / 2; ++r) {
+          const long long q = (base >> 1) + r * kBlock + tid;
+          if (2 * q < n) {
+            __stcs(z2 + q, make_double2(pz[2 * r], pz[2 * r + 1]));
+            __stcs(x2 + q, make_double2(px[2 * r], px[2 * r + 1]));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          if (keep[k]) {
+            const long long d = prefix + s_row[(k >> 1) * kWarps + warp] + pre[k];
+            p.z[d] = pz[k];
+            p.x[d] = px[k];
+            p.vz[d] = pvz[k];
+            p.vx[d] = pvx[k];
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        if (keep[k]) {
+          const long long d = prefix + s_row[k * kWarps + warp] + pre[k];
+          __stcs(p.out_pos + d, make_double2(pz[k], px[k]));
+          __stcs(p.out_vel + d, make_double2(pvz[k], pvx[k]));
+        }
+      }
+    }
+    __syncthreads();  // s_row / s_tile reuse
+  }
+
+  // ---- CTA exit: flush the shared histogram (one atomic per box) ----
+  if (kHist) {
+    if (err) atomicAdd((unsigned long long*)&p.st->err, (unsigned long long)err);
+    if (p.smem_hist) {
+      for (int b = tid; b < p.nb; b += kBlock) {
+        const unsigned c = s_cnt[b];
+        if (c) atomicAdd(p.g_cnt + b, (unsigned long long)c);
+        if (kClock) {
+          const unsigned long long k = s_clk[b];
+          if (k) atomicAdd(p.g_clk + b, k);
+        }
+      }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(&p.st->done, 1u) == gridDim.x - 1) ? 1 : 0;
+  __syncthreads();
+  if (!s_last) return;
+
+  // ---- last CTA: step epilogue ----
+  __threadfence();
+  long long n_new = 0;
+  if (ntiles > 0) n_new = (long long)(ld_acquire(p.status + (ntiles - 1)) & kValueMask);
+  if (kHist) {
+    for (int b = tid; b < p.nb; b += kBlock) {
+      const unsigned long long c = atomicExch(p.g_cnt + b, 0ull);
+      if (p.counts_out) p.counts_out[b] = (long long)c;
+      if (p.cost_out) {
+        p.cost_out[b] = __dadd_rn(__dmul_rn(p.wp, (double)(long long)c),
+                                  __dmul_rn(p.wc, p.cells));
+      }
+      if (kClock) {
+        const unsigned long long k = atomicExch(p.g_clk + b, 0ull);
+        if (p.clk_out) p.clk_out[b] = k;
+      }
+    }
+  }
+  if (tid == 0) {
+    if (p.n_out) *p.n_out = n_new;
+    const long long e = *((volatile long long*)&p.st->err);
+    if (p.err_out) *p.err_out = e;
+    p.st->n = n_new;
+    p.st->ticket = 0ull;
+    p.st->done = 0u;
+    unsigned ne = (epoch + 1u) & kEpochMask;
+    p.st->epoch = ne ? ne : 1u;
+    __threadfence_system();
+  }
+}
+
+// Histogram of AoS positions (drop-in bin_particles).
+__global__ void __launch_bounds__(kBlock) bin_kernel(const double2* __restrict__ pos,
+                                                     long long n, double m, int nbz, int nbx,
+                                                     int smem_hist,
+                                                     unsigned long long* __restrict__ counts,
+                                                     unsigned long long* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned* s_cnt = reinterpret_cast<unsigned*>(smem_raw);
+  const int nb = nbz * nbx;
+  if (smem_hist) {
+    for (int b = threadIdx.x; b < nb; b += kBlock) s_cnt[b] = 0u;
+    __syncthreads();
+  }
+  long long bad = 0;
+  const long long stride = (long long)gridDim.x * kBlock;
+  int cur = -1;
+  unsigned run = 0;
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += stride) {
+    const double2 q = __ldcs(pos + i);
+    const double fz = __ddiv_rn(q.x, m);
+    const double fx = __ddiv_rn(q.y, m);
+    int b = -1;
+    if (fz >= 0.0 && fx >= 0.0 && fz < (double)nbz && fx < (double)nbx) {
+      b = (int)fz * nbx + (int)fx;
+    } else {
+      ++bad;
+    }
+    if (b != cur) {
+      if (cur >= 0) {
+        if (smem_hist) atomicAdd(s_cnt + cur, run);
+        else atomicAdd(counts + cur, (unsigned long long)run);
+      }
+      cur = b;
+      run = 0;
+    }
+    run += (b >= 0) ? 1u : 0u;
+  }
+  if (cur >= 0 && run) {
+    if (smem_hist) atomicAdd(s_cnt + cur, run);
+    else atomicAdd(counts + cur, (unsigned long long)run);
+  }
+  if (bad && err) atomicAdd(err, (unsigned long long)bad);
+  if (smem_hist) {
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += kBlock) {
+      const unsigned c = s_cnt[b];
+      if (c) atomicAdd(counts + b, (unsigned long long)c);
+    }
+  }
+}
+
+__global__ void heuristic_kernel(const long long* __restrict__ counts, int nb, double wp,
+                                 double wc, double cells, double* __restrict__ cost) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nb) cost[b] = __dadd_rn(__dmul_rn(wp, (double)counts[b]), __dmul_rn(wc, cells));
+}
+
+__global__ void init_state_kernel(DevState* st, long long n) {
+  st->ticket = 0ull;
+  st->done = 0u;
+  if (st->epoch == 0u) st->epoch = 1u;
+  st->n = n;
+}
+
+inline int cuda_fail(cudaError_t e, const char* what) {
+  return set_error(LBX_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+template <int kLayout, bool kHist, bool kClock>
+int launch_push(lbx_ctx* ctx, PushParams& p, long long n_upper, cudaStream_t s) {
+  auto kern = push_kernel<kLayout, kHist, kClock>;
+  const size_t smem =
+      (kHist && p.smem_hist) ? (size_t)p.nb * (4 + (kClock ? 8 : 0)) : (size_t)0;
+  static thread_local size_t configured[2][2][2] = {};
+  size_t& cfg = configured[kLayout][kHist][kClock];
+  if (smem > 48 * 1024 && smem > cfg) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    cfg = smem;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
+  if (per_sm < 1) per_sm = 1;
+  long long grid = (long long)per_sm * ctx->num_sms;
+  if (ctx->grid_override > 0) grid = ctx->grid_override;
+  const long long tiles = (n_upper + kTile - 1) / kTile;
+  grid = std::max(1ll, std::min(grid, tiles));
+  kern<<<(unsigned)grid, kBlock, smem, s>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "push_kernel launch");
+  return LBX_OK;
+}
+
+int reserve_status(lbx_ctx* ctx, int64_t capacity) {
+  const int64_t tiles = (capacity + kTile - 1) / kTile + 1;
+  if (tiles <= ctx->status_tiles) return LBX_OK;
+  unsigned long long* s = nullptr;
+  cudaError_t e = cudaMalloc(&s, (size_t)tiles * sizeof(unsigned long long));
+  if (e != cudaSuccess) return set_error(LBX_EOOM, "look-back workspace: %s", cudaGetErrorString(e));
+  // Epoch 0 is never current, so zeroed words read as "not yet published".
+  e = cudaMemset(s, 0, (size_t)tiles * sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    cudaFree(s);
+    return cuda_fail(e, "cudaMemset");
+  }
+  if (ctx->status) {
+    cudaDeviceSynchronize();
+    cudaFree(ctx->status);
+  }
+  ctx->status = s;
+  ctx->status_tiles = tiles;
+  return LBX_OK;
+}
+
+}  // namespace
+
+int ensure_accumulators(lbx_ctx* ctx, int32_t nboxes) {
+  if (nboxes <= ctx->acc_boxes) return LBX_OK;
+  unsigned long long* a = nullptr;
+  cudaError_t e = cudaMalloc(&a, (size_t)2 * nboxes * sizeof(unsigned long long));
+  if (e != cudaSuccess) return set_error(LBX_EOOM, "accumulators: %s", cudaGetErrorString(e));
+  e = cudaMemset(a, 0, (size_t)2 * nboxes * sizeof(unsigned long long));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemset");
+  if (ctx->acc) {
+    cudaDeviceSynchronize();
+    cudaFree(ctx->acc);
+  }
+  ctx->acc = a;
+  ctx->acc_boxes = nboxes;
+  return LBX_OK;
+}
+
+int launch_push_step(lbx_ctx* ctx, const StepLaunch& a, void* stream) {
+  if (a.nbz < 1 || a.nbx < 1) return set_error(LBX_EINVAL, "box grid must be at least 1x1");
+  if (!(a.m > 0.0)) return set_error(LBX_EINVAL, "box_size must be positive");
+  const long long nb = (long long)a.nbz * a.nbx;
+  if (nb > (1ll << 30)) return set_error(LBX_EINVAL, "too many boxes");
+  if (((uintptr_t)a.z | (uintptr_t)a.x | (uintptr_t)a.vz | (uintptr_t)a.vx) & 15u)
+    return set_error(LBX_EINVAL, "particle arrays must be 16-byte aligned");
+  int rc = ensure_accumulators(ctx, (int32_t)nb);
+  if (rc) return rc;
+  rc = reserve_status(ctx, ctx->n_upper);
+  if (rc) return rc;
+  PushParams p{};
+  p.z = a.z;
+  p.x = a.x;
+  p.vz = a.vz;
+  p.vx = a.vx;
+  p.ez = a.ez;
+  p.ex = a.ex;
+  p.m = a.m;
+  p.nbz = a.nbz;
+  p.nbx = a.nbx;
+  p.nb = (int)nb;
+  p.smem_hist = nb <= kSmemBoxesMax ? 1 : 0;
+  p.n_override = -1;
+  p.st = ctx->st;
+  p.status = ctx->status;
+  p.g_cnt = ctx->acc;
+  p.g_clk = ctx->acc + ctx->acc_boxes;
+  p.counts_out = a.counts_out;
+  p.cost_out = a.cost_out;
+  p.clk_out = a.clk_out;
+  p.n_out = a.n_out;
+  p.err_out = a.err_out;
+  p.wp = a.wp;
+  p.wc = a.wc;
+  p.cells = a.cells;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (a.clock) return launch_push<kSoAInPlace, true, true>(ctx, p, ctx->n_upper, s);
+  return launch_push<kSoAInPlace, true, false>(ctx, p, ctx->n_upper, s);
+}
+
+}  // namespace lbx
+
+using namespace lbx;
+
+extern "C" {
+
+int lbx_ctx_create(lbx_ctx** out, int device, int64_t capacity) {
+  clear_error();
+  if (!out) return set_error(LBX_EINVAL, "out pointer is NULL");
+  if (capacity < 0) return set_error(LBX_EINVAL, "capacity must be >= 0");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  lbx_ctx* c = new lbx_ctx();
+  c->device = device;
+  e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "device query");
+  }
+  e = cudaMalloc(&c->st, sizeof(DevState));
+  if (e != cudaSuccess) {
+    delete c;
+    return set_error(LBX_EOOM, "device state: %s", cudaGetErrorString(e));
+  }
+  cudaMemset(c->st, 0, sizeof(DevState));
+  e = cudaHostAlloc(&c->host_scratch, 64, cudaHostAllocDefault);
+  if (e != cudaSuccess) {
+    cudaFree(c->st);
+    delete c;
+    return cuda_fail(e, "cudaHostAlloc");
+  }
+  init_state_kernel<<<1, 1>>>(c->st, 0);
+  int rc = reserve_status(c, capacity);
+  if (rc) {
+    lbx_ctx_destroy(c);
+    return rc;
+  }
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    lbx_ctx_destroy(c);
+    return cuda_fail(e, "context init");
+  }
+  *out = c;
+  return LBX_OK;
+}
+
+int lbx_ctx_destroy(lbx_ctx* ctx) {
+  clear_error();
+  if (!ctx) return LBX_OK;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  if (ctx->st) cudaFree(ctx->st);
+  if (ctx->status) cudaFree(ctx->status);
+  if (ctx->acc) cudaFree(ctx->acc);
+  if (ctx->host_scratch) cudaFreeHost(ctx->host_scratch);
+  delete ctx;
+  return LBX_OK;
+}
+
+int lbx_ctx_reserve(lbx_ctx* ctx, int64_t capacity) {
+  clear_error();
+  if (!ctx) return set_error(LBX_EINVAL, "context is NULL");
+  return reserve_status(ctx, capacity);
+}
+
+int lbx_ctx_set_count(lbx_ctx* ctx, int64_t n, void* stream) {
+  clear_error();
+  if (!ctx) return set_error(LBX_EINVAL, "context is NULL");
+  if (n < 0) return set_error(LBX_EINVAL, "count must be >= 0");
+  int rc = reserve_status(ctx, n);
+  if (rc) return rc;
+  init_state_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(ctx->st, n);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "set_count");
+  ctx->n_upper = n;
+  return LBX_OK;
+}
+
+int lbx_ctx_get_count(lbx_ctx* ctx, int64_t* n_host, void* stream) {
+  clear_error();
+  if (!ctx || !n_host) return set_error(LBX_EINVAL, "NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(ctx->host_scratch, &ctx->st->n, sizeof(long long),
+                                  cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "get_count");
+  *n_host = ctx->host_scratch[0];
+  ctx->n_upper = *n_host;
+  return LBX_OK;
+}
+
+int lbx_ctx_set_grid(lbx_ctx* ctx, int ctas) {
+  clear_error();
+  if (!ctx) return set_error(LBX_EINVAL, "context is NULL");
+  ctx->grid_override = ctas > 0 ? ctas : 0;
+  return LBX_OK;
+}
+
+int lbx_advance_particles(lbx_ctx* ctx, const double* pos, const double* vel, int64_t n,
+                          double extent_z, double extent_x, double* out_pos, double* out_vel,
+                          int64_t* m_dev, void* stream) {
+  clear_error();
+  if (!ctx) return set_error(LBX_EINVAL, "context is NULL");
+  if (n < 0) return set_error(LBX_EINVAL, "n must be >= 0");
+  if (n > 0 && (!pos || !vel || !out_pos || !out_vel))
+    return set_error(LBX_EINVAL, "NULL particle buffer");
+  if (((uintptr_t)pos | (uintptr_t)vel | (uintptr_t)out_pos | (uintptr_t)out_vel) & 15u)
+    return set_error(LBX_EINVAL, "particle arrays must be 16-byte aligned");
+  int rc = reserve_status(ctx, n);
+  if (rc) return rc;
+  PushParams p{};
+  p.in_pos = reinterpret_cast<const double2*>(pos);
+  p.in_vel = reinterpret_cast<const double2*>(vel);
+  p.out_pos = reinterpret_cast<double2*>(out_pos);
+  p.out_vel = reinterpret_cast<double2*>(out_vel);
+  p.ez = extent_z;
+  p.ex = extent_x;
+  p.m = 1.0;
+  p.nbz = p.nbx = p.nb = 1;
+  p.n_override = n;
+  p.st = ctx->st;
+  p.status = ctx->status;
+  p.n_out = reinterpret_cast<long long*>(m_dev);
+  return launch_push<kAoSOutOfPlace, false, false>(ctx, p, n, (cudaStream_t)stream);
+}
+
+int lbx_bin_particles(const double* pos, int64_t n, double box_size, int32_t nbz, int32_t nbx,
+                      int64_t* counts, int64_t* err_dev, void* stream) {
+  clear_error();
+  if (nbz < 0 || nbx < 0) return set_error(LBX_EINVAL, "box grid must be nonnegative");
+  if (n < 0) return set_error(LBX_EINVAL, "n must be >= 0");
+  const long long nb = (long long)nbz * nbx;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nb > 0) {
+    cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)nb * sizeof(int64_t), s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  }
+  if (n == 0) return LBX_OK;
+  if (nb == 0) return set_error(LBX_ERANGE, "particles present but the box grid is empty");
+  if ((uintptr_t)pos & 15u) return set_error(LBX_EINVAL, "positions must be 16-byte aligned");
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int smem_hist = nb <= kSmemBoxesMax ? 1 : 0;
+  const size_t smem = smem_hist ? (size_t)nb * 4 : 0;
+  long long grid = std::min((long long)sms * 8, (long long)((n + kBlock * 8 - 1) / (kBlock * 8)));
+  grid = std::max(1ll, grid);
+  bin_kernel<<<(unsigned)grid, kBlock, smem, s>>>(
+      reinterpret_cast<const double2*>(pos), n, box_size, nbz, nbx, smem_hist,
+      reinterpret_cast<unsigned long long*>(counts),
+      reinterpret_cast<unsigned long long*>(err_dev));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bin_kernel launch");
+  return LBX_OK;
+}
+
+int lbx_push_step(lbx_ctx* ctx, const lbx_step_args* a, void* stream) {
+  clear_error();
+  if (!ctx || !a) return set_error(LBX_EINVAL, "NULL argument");
+  StepLaunch l{};
+  l.z = a->z;
+  l.x = a->x;
+  l.vz = a->vz;
+  l.vx = a->vx;
+  l.ez = a->extent_z;
+  l.ex = a->extent_x;
+  l.m = a->box_size;
+  l.nbz = a->nbz;
+  l.nbx = a->nbx;
+  l.wp = a->w_particle;
+  l.wc = a->w_cell;
+  l.cells = a->cells_per_box;
+  l.clock = (a->flags & LBX_STEP_CLOCK) != 0;
+  l.counts_out = reinterpret_cast<long long*>(a->counts_out);
+  l.cost_out = a->cost_out;
+  l.clk_out = reinterpret_cast<unsigned long long*>(a->clk_out);
+  l.n_out = reinterpret_cast<long long*>(a->n_out);
+  l.err_out = reinterpret_cast<long long*>(a->err_out);
+  return launch_push_step(ctx, l, stream);
+}
+
+int lbx_heuristic_cost(const int64_t* counts, int32_t nboxes, double w_particle, double w_cell,
+                       double cells_per_box, double* cost, void* stream) {
+  clear_error();
+  if (nboxes < 0) return set_error(LBX_EINVAL, "nboxes must be >= 0");
+  if (nboxes == 0) return LBX_OK;
+  heuristic_kernel<<<(nboxes + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const long long*>(counts), nboxes, w_particle, w_cell, cells_per_box,
+      cost);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "heuristic launch");
+  return LBX_OK;
+}
+
+}  // extern "C"

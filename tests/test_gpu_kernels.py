@@ -1,0 +1,116 @@
+"""GPU parity of libLBX kernels against the oracle and reference fixtures."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import lbsim_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+G = Path(__file__).resolve().parent / "golden"
+
+
+@pytest.fixture(scope="module")
+def K():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test without a CUDA device")
+    from paper_2104_11385_b200 import kernels
+    return kernels
+
+
+def test_backend_is_cuda(K):
+    assert K.BACKEND == "cuda"
+
+
+def test_fixture_advance_and_bin(K):
+    f = np.load(G / "kernels.npz")
+    for tag in "abcd":
+        e = float(f[f"{tag}_extent"])
+        p, v = K.advance_particles(f[f"{tag}_pos"], f[f"{tag}_vel"], e, e)
+        assert np.array_equal(p, f[f"{tag}_out_pos"])
+        assert np.array_equal(v, f[f"{tag}_out_vel"])
+        assert np.array_equal(K.bin_particles(p, e / 8, 8, 8), f[f"{tag}_bins"])
+    p, v = f["chain_pos"], f["chain_vel"]
+    for _ in range(25):
+        p, v = K.advance_particles(p, v, 64.0, 64.0)
+    assert np.array_equal(p, f["chain_out_pos"]) and np.array_equal(v, f["chain_out_vel"])
+
+
+def test_known_answer_order_preserved(K):
+    pos = np.array([[1.0, 1.0], [2.0, 2.0], [63.5, 63.5], [3.0, 3.0]])
+    vel = np.array([[0.1, 0.0], [0.0, 0.0], [1.0, 1.0], [0.0, -0.5]])
+    p, _ = K.advance_particles(pos, vel, 64.0, 64.0)
+    assert np.array_equal(p, [[1.1, 1.0], [2.0, 2.0], [3.0, 2.5]])
+
+
+def test_empty(K):
+    p, v = K.advance_particles(np.empty((0, 2)), np.empty((0, 2)), 8.0, 8.0)
+    assert p.shape == (0, 2)
+    assert np.array_equal(K.bin_particles(np.empty((0, 2)), 4.0, 2, 2), np.zeros(4, np.int64))
+
+
+@pytest.mark.parametrize("n,spill", [(1, 0.5), (2047, 0.3), (2048, 0.0), (2049, 0.3),
+                                     (100_003, 0.05), (1_000_000, 0.01), (777_777, 2.0)])
+def test_random_advance_bin(K, n, spill):
+    rng = np.random.default_rng(n)
+    pos = rng.uniform(0, 64.0, size=(n, 2))
+    vel = rng.normal(0, spill * 64.0, size=(n, 2))
+    p, v = K.advance_particles(pos, vel, 64.0, 64.0)
+    p2, v2 = O.advance_particles(pos, vel, 64.0, 64.0)
+    assert np.array_equal(p, p2) and np.array_equal(v, v2)
+    assert np.array_equal(K.bin_particles(p, 8.0, 8, 8), O.bin_particles(p2, 8.0, 8, 8))
+
+
+def test_bin_out_of_grid_raises(K):
+    with pytest.raises(ValueError):
+        K.bin_particles(np.array([[1.0, 100.0]]), 8.0, 2, 2)
+
+
+def _fused_case(n, ext, m, spill, seed, clock, steps=1, sort=False):
+    from paper_2104_11385_b200 import device
+    rng = np.random.default_rng(seed)
+    pos = rng.uniform(0, ext, size=(n, 2))
+    if sort:  # blob-like spatial coherence
+        pos = pos[np.lexsort((pos[:, 1], np.floor(pos[:, 0])))]
+    vel = rng.normal(0, spill, size=(n, 2))
+    nb1 = int(ext // m)
+    st = device.ParticleState.from_numpy(pos, vel)
+    ctx = device.Context(capacity=n)
+    p2, v2 = pos, vel
+    for _ in range(steps):
+        out = device.push_step(ctx, st, ext, ext, m, nb1, nb1, (0.75, 0.25), clock=clock)
+        p2, v2 = O.advance_particles(p2, v2, ext, ext)
+        c2 = O.bin_particles(p2, m, nb1, nb1)
+        assert out["n"] == p2.shape[0]
+        assert np.array_equal(out["counts"], c2)
+        assert np.array_equal(out["cost"], O.heuristic_cost(c2, np.full(nb1 * nb1, m * m), 0.75, 0.25))
+        if clock:
+            assert ((out["clock"] > 0) == (c2 > 0)).all()
+    gp, gv = st.to_numpy()
+    assert np.array_equal(gp, p2) and np.array_equal(gv, v2)
+
+
+@pytest.mark.parametrize("clock", [False, True])
+@pytest.mark.parametrize("n,spill,sort", [(5, 1.0, False), (4096, 0.0, False),
+                                          (300_001, 0.5, False), (2_000_000, 0.05, True),
+                                          (1_500_000, 3.0, True)])
+def test_fused_step_matches_oracle(n, spill, sort, clock):
+    _fused_case(n, 96.0, 16.0, spill, seed=n, clock=clock, steps=3, sort=sort)
+
+
+def test_fused_many_boxes_global_hist():
+    # 128x128 boxes > shared-memory histogram limit -> global atomics path
+    _fused_case(400_000, 512.0, 4.0, 0.7, seed=9, clock=True, steps=2)
+
+
+def test_fused_sfc_weights_no_fma():
+    # (0.02, 0.98) preset is where an FMA would change 16.5% of costs
+    from paper_2104_11385_b200 import device
+    rng = np.random.default_rng(3)
+    pos = rng.uniform(0, 96.0, size=(200_000, 2))
+    st = device.ParticleState.from_numpy(pos, np.zeros_like(pos))
+    ctx = device.Context(capacity=200_000)
+    out = device.push_step(ctx, st, 96.0, 96.0, 16.0, 6, 6, (0.02, 0.98))
+    c2 = O.bin_particles(pos, 16.0, 6, 6)
+    assert np.array_equal(out["cost"], O.heuristic_cost(c2, np.full(36, 256), 0.02, 0.98))
