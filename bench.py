@@ -1,0 +1,444 @@
+#!/usr/bin/env python
+"""Benchmark: particle-pushes/s including in-situ cost assessment, plus LB
+efficiency, on B200 (BASELINE.json metric; workload = config C2).
+
+Workload (config C2, "2D laser-ion dense-slab target, GpuClock costs,
+dynamic LB every 10 steps"): the reference's default.yaml geometry -- 960x960
+cells, 32-cell boxes (900 boxes), dense blob (core 64, skirt 4, 55 ppc)
+sampled with the reference's own PCG64 stream -- from the kick step onward
+(radial kick, speed 0.035, drift 0.01), GpuClock costs, knapsack remap
+attempted every 10 steps with a 10% relative threshold.  To fill a B200 the
+801,499-particle set is tiled R times (default R=128 -> 102.6 M particles,
+3.3 GB of particle state): every replica evolves identically, so per-box
+counts are exactly R x the reference's (checked by tests/test_gpu_bench_parity).
+
+One step = the fused sm_100a kernel (push + absorb + stable compaction +
+per-box counts + heuristic cost + GpuClock tally) + the step record written
+to mapped host memory + the native host loop (cost vector, efficiency,
+knapsack attempt every 10 steps).  Inputs (3.3 GB) are larger than L2
+(126 MB), so no flush is needed between steps.
+
+--impl reference: the reference's own CPU implementation (its compiled
+Cython kernels from oracle/_ref, with the oracle port of its numpy cost and
+balancer code) on the same workload, one process per host core, each on a
+bounded sample; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "particle-pushes/s incl. in-situ cost assessment; LB efficiency at 1-8 B200"
+UNIT = "particle-pushes/s"
+BYTES_PER_PUSH = 48  # read z,x,vz,vx + write z,x (fp64), SURVEY 8(d)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="lbx", choices=["lbx", "reference"])
+    ap.add_argument("--replicas", type=int, default=128)
+    ap.add_argument("--cost", default="gpuclock")
+    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+
+def c2_spec(n_ranks: int, steps: int, cost: str):
+    from dataclasses import replace
+
+    from paper_2104_11385_b200.scenarios import apply_overrides, load_spec
+
+    spec = apply_overrides(load_spec("default"), cost=cost, ranks=n_ranks, steps=steps)
+    sc = spec.scenario
+    # bench starts at the kick (step 150 of the preset): kick applies at step 0
+    return spec, replace(sc, kick=replace(sc.kick, step=0))
+
+
+def base_particles(spec):
+    from paper_2104_11385_b200.workload import kick_velocities, sample_blob
+
+    pos = sample_blob(spec.scenario)
+    return pos, kick_velocities(pos, spec.scenario)
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *a):
+        time.sleep(0.15)
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        self.f.flush()
+        rows = [r.split(",") for r in Path(self.f.name).read_text().splitlines() if r.strip()]
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def traffic_per_push():
+    """dram read+write bytes per particle from the committed ncu capture."""
+    p = ROOT / "profiles" / "ncu_push_kernel.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return float(d["dram_bytes_per_particle"])
+    except (KeyError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference's own kernels (oracle/_ref) + oracle port
+# ---------------------------------------------------------------------------
+
+def _ref_kernels():
+    import importlib.util
+
+    cands = sorted((ROOT / "oracle" / "_ref").glob("_kernels*.so"))
+    if cands:
+        spec = importlib.util.spec_from_file_location("_kernels", cands[0])
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        return mod, "reference"
+    from oracle import lbsim_oracle as O
+    return O, "port"
+
+
+def _cpu_worker(args):
+    """One single-threaded reference loop on the base (1-replica) workload,
+    running whole steps until `seconds` elapse.  Returns (pushes, secs)."""
+    seconds, cost_kind = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import lbsim_oracle as O
+    K, _ = _ref_kernels()
+    spec, sc = c2_spec(1, 10 ** 6, "measured")
+    pos, vel = base_particles(spec)
+    m = float(sc.box_size)
+    nbz = nbx = sc.domain_extent[0] // sc.box_size
+    cells = np.full(nbz * nbx, sc.box_size ** 2, dtype=np.int64)
+    owner = O.slab_mapping(nbz * nbx, 8)
+    pushes, step = 0, 0
+    t0 = time.perf_counter()
+    while True:
+        n = pos.shape[0]
+        pos, vel = K.advance_particles(pos, vel, float(sc.domain_extent[0]),
+                                       float(sc.domain_extent[1]))
+        counts = K.bin_particles(pos, m, nbz, nbx)
+        work = O.true_work(counts, sc.box_size, sc.work_weights)
+        if cost_kind == "heuristic":
+            cost = O.heuristic_cost(counts, cells, 0.75, 0.25)
+        else:
+            cost = O.measured_cost(work, 0.05, sc.seed, step)
+        e, _ = O.efficiency_flagged(cost, owner, 8)
+        if step % 10 == 0:
+            prop = O.knapsack_assign(cost, 8)
+            if O.gate(e, O.efficiency_flagged(cost, prop, 8)[0], 0.10, "relative"):
+                owner = prop
+        pushes += n
+        step += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            return pushes, el, step
+
+
+def cpu_baseline(seconds: float, processes: int):
+    import multiprocessing as mp
+
+    _, kind = _ref_kernels()
+    if processes <= 1:
+        res = [_cpu_worker((seconds, "measured"))]
+    else:
+        with mp.get_context("spawn").Pool(processes) as pool:
+            res = pool.map(_cpu_worker, [(seconds, "measured")] * processes)
+    value = sum(p / s for p, s, _ in res)
+    steps = sum(k for _, _, k in res)
+    return {"value": value, "unit": UNIT, "cores": processes, "kind": kind,
+            "sample": (f"C2 base set (801,499 particles, from the kick) x {processes} "
+                       f"independent single-threaded processes, {steps} steps total in "
+                       f"~{seconds:.0f} s each: reference Cython advance_particles + "
+                       "bin_particles (oracle/_ref) + measured_cost / efficiency / "
+                       "knapsack every 10 (oracle numpy port)")}
+
+
+# ---------------------------------------------------------------------------
+# arms
+# ---------------------------------------------------------------------------
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    procs = os.cpu_count() or 1
+    cb = cpu_baseline(args.cpu_seconds, procs)
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "impl": "reference",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C2 default.yaml geometry from the kick, x"
+                                   f"{args.replicas} replicas (sampled: see cpu_baseline)",
+                       "cost": "measured (reference timer model)", "parallelism": "cpu"},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_lbx(args, rank, world, local_rank):
+    import torch
+
+    from paper_2104_11385_b200 import _lib
+    from paper_2104_11385_b200 import device as D
+    from paper_2104_11385_b200.workload import Simulation
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    total = args.warmup + args.steps
+    spec, sc = c2_spec(world, total, args.cost)
+    pos0, kick0 = base_particles(spec)
+    R = args.replicas
+    pos = torch.from_numpy(pos0).to(dev).repeat(R, 1)
+    kick = torch.from_numpy(kick0).to(dev).repeat(R, 1)
+    sim = Simulation(sc, spec.policy, spec.build_provider(), device=dev, positions=pos,
+                     kick=kick, time_kernels=True)
+    del pos, kick
+    n0 = sim.n_init
+    sim.run(0, args.warmup)
+    torch.cuda.synchronize(dev)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    barrier()
+    torch.cuda.synchronize(dev)
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        e0.record(stream)
+        sim.run(args.warmup, total)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    ms = e0.elapsed_time(e1)
+    n_alive = sim.out["n_alive"]
+    n_before = np.concatenate(([n0], n_alive[:-1]))
+    pushed = float(n_before[args.warmup:total].sum())
+    kms = sim.out["kernel_ms"][args.warmup:total]
+    res = sim.result()
+    if world > 1:
+        t = torch.tensor([ms, pushed], dtype=torch.float64, device=dev)
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        torch.distributed.all_gather(allt, t)
+        ms = max(float(x[0]) for x in allt)
+        pushed = sum(float(x[1]) for x in allt)
+    value = pushed / (ms / 1e3)
+    kernel_s = float(np.mean(kms)) / 1e3
+    per_launch = float(np.mean(n_before[args.warmup:total]))
+    achieved = BYTES_PER_PUSH * per_launch / kernel_s / 1e9
+    peak, peak_src = peaks()
+    tpp = traffic_per_push()
+    effs = [m.efficiency_after for m in res.metrics]
+
+    # ---- e2e through the reference-facing C-ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_plugin(args, dev, pos0, kick0, R, sc)
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": (f"C2: default.yaml geometry (960x960 cells, 32-cell boxes, "
+                                f"900 boxes, blob core 64 / skirt 4 / 55 ppc, seed 7) from "
+                                f"the kick, particle set x{R} replicas = {n0} particles per "
+                                "GPU"),
+                   "cost": spec.build_provider().kind, "lb": "knapsack every 10, 10% rel",
+                   "ranks": world, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "inputs larger than L2 (3.3 GB particle state vs 126 MB L2)"},
+        "gpu_launches": int(args.steps),
+        "lb": {"ranks": world, "e_first": effs[0] if effs else None,
+               "e_mean": float(np.mean(effs)) if effs else None,
+               "adoptions": res.summary["adoption_count"]},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_source": peak_src,
+                     "kernel": "lbx push_kernel<SoA,hist,clock>",
+                     "bytes_per_launch": BYTES_PER_PUSH * per_launch,
+                     "kernel_ms": kernel_s * 1e3,
+                     "traffic": None if tpp is None else tpp * per_launch},
+        "clocks": clocks.summary(),
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.cpu_seconds, 1)
+    print(json.dumps(line), flush=True)
+    _lib.lib.lbx_sim_destroy(sim.handle)
+    sim.handle = None
+    del D
+
+
+def e2e_plugin(args, dev, pos0, kick0, R, sc):
+    """Same workload through the reference-facing plugin boundary
+    (kernels.advance_particles / bin_particles + heuristic cost, C ABI) with
+    HOST buffers: every step copies the particles in from pinned host memory
+    and the survivors, counts and costs back out."""
+    import torch
+
+    from paper_2104_11385_b200 import _lib
+    from paper_2104_11385_b200.device import Context, _stream
+
+    n = pos0.shape[0] * R
+    nbz = nbx = sc.domain_extent[0] // sc.box_size
+    nb = nbz * nbx
+    hp = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
+    hv = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
+    hp.numpy()[:] = np.tile(pos0, (R, 1))
+    hv.numpy()[:] = np.tile(kick0, (R, 1))
+    op = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
+    ov = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
+    hc = torch.empty(nb, dtype=torch.int64, pin_memory=True)
+    hcost = torch.empty(nb, dtype=torch.float64, pin_memory=True)
+    dp = torch.empty((n + 1, 2), dtype=torch.float64, device=dev)
+    dv = torch.empty_like(dp)
+    dpo = torch.empty_like(dp)
+    dvo = torch.empty_like(dp)
+    dc = torch.empty(nb, dtype=torch.int64, device=dev)
+    dcf = torch.empty(nb, dtype=torch.float64, device=dev)
+    dcells = torch.full((nb,), float(sc.box_size ** 2), dtype=torch.float64, device=dev)
+    dcost = torch.empty(nb, dtype=torch.float64, device=dev)
+    m = torch.empty(1, dtype=torch.int64, device=dev)
+    hm = torch.empty(1, dtype=torch.int64, pin_memory=True)
+    ctx = Context(dev, capacity=n)
+    s = _stream(dev)
+    stream = torch.cuda.current_stream(dev)
+    ez, ex, M = float(sc.domain_extent[0]), float(sc.domain_extent[1]), float(sc.box_size)
+    state = {"n": n, "inp": (hp, hv), "out": (op, ov)}
+    h2d = d2h = 0
+
+    def step():
+        nonlocal h2d, d2h
+        k = state["n"]
+        ip, iv = state["inp"]
+        dp[:k].copy_(ip[:k], non_blocking=True)
+        dv[:k].copy_(iv[:k], non_blocking=True)
+        _lib.check(_lib.lib.lbx_advance_particles(ctx.handle, _lib.ptr(dp), _lib.ptr(dv), k,
+                                                  ez, ex, _lib.ptr(dpo), _lib.ptr(dvo),
+                                                  _lib.ptr(m), s))
+        hm.copy_(m, non_blocking=True)
+        stream.synchronize()
+        mm = int(hm[0])
+        _lib.check(_lib.lib.lbx_bin_particles(_lib.ptr(dpo), mm, M, nbz, nbx, _lib.ptr(dc),
+                                              None, s))
+        dcf.copy_(dc)
+        _lib.check(_lib.lib.lbx_heuristic_cost(_lib.ptr(dcf), _lib.ptr(dcells), nb, 0.75,
+                                               0.25, _lib.ptr(dcost), s))
+        opp, ovv = state["out"]
+        opp[:mm].copy_(dpo[:mm], non_blocking=True)
+        ovv[:mm].copy_(dvo[:mm], non_blocking=True)
+        hc.copy_(dc, non_blocking=True)
+        hcost.copy_(dcost, non_blocking=True)
+        stream.synchronize()
+        h2d += 32 * k
+        d2h += 32 * mm + 16 * nb + 8
+        state["n"] = mm
+        state["inp"], state["out"] = state["out"], state["inp"]
+        return k
+
+    for _ in range(2):
+        step()
+    h2d = d2h = 0
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    pushed = sum(step() for _ in range(args.e2e_steps))
+    el = time.perf_counter() - t0
+    ctx.close()
+    return {"value": pushed / el, "unit": UNIT,
+            "h2d_bytes_per_step": h2d // args.e2e_steps,
+            "d2h_bytes_per_step": d2h // args.e2e_steps,
+            "steps": args.e2e_steps,
+            "path": "lbx_advance_particles + lbx_bin_particles + lbx_heuristic_cost "
+                    "(reference AoS layout), pinned host buffers, copies in the timed region"}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    run_lbx(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -121,9 +121,11 @@ typedef struct lbx_step_args {
 
 int lbx_push_step(lbx_ctx* ctx, const lbx_step_args* args, void* stream);
 
-/* Heuristic cost from counts on the device (cost.py:83-95), no FMA. */
-int lbx_heuristic_cost(const int64_t* counts, int32_t nboxes, double w_particle,
-                       double w_cell, double cells_per_box, double* cost,
+/* Replaces cost.py:83-95 heuristic_cost on device vectors:
+ * cost[i] = w_particle*particles[i] + w_cell*cells[i], two separately
+ * rounded products then one add (no FMA). */
+int lbx_heuristic_cost(const double* particles, const double* cells, int64_t n,
+                       double w_particle, double w_cell, double* cost,
                        void* stream);
 
 /* ------------------------------------------------------------------------
@@ -222,6 +224,8 @@ typedef struct lbx_sim_outputs {
   /* adoption snapshots: step index per adoption and owner rows */
   int64_t* adopt_steps;        /* [total_steps]                              */
   int64_t* adopt_owners;       /* [total_steps][n_boxes] or NULL            */
+  double* kernel_ms;           /* [total_steps] fused-kernel time (CUDA events
+                                  on the launch stream) or NULL             */
   int64_t n_adoptions;         /* out                                        */
   int64_t n_attempts;          /* out                                        */
   int64_t completed_steps;     /* out                                        */

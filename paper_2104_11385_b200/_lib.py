@@ -54,7 +54,7 @@ class SimOutputs(C.Structure):
                 ("redistribute", vp), ("walltime", vp), ("max_rank_particles", vp),
                 ("oom", vp), ("n_alive", vp), ("cost_trace", vp), ("count_trace", vp),
                 ("clock_trace", vp), ("owner", vp), ("adopt_steps", vp),
-                ("adopt_owners", vp), ("n_adoptions", i64), ("n_attempts", i64),
+                ("adopt_owners", vp), ("kernel_ms", vp), ("n_adoptions", i64), ("n_attempts", i64),
                 ("completed_steps", i64)]
 
 
@@ -71,7 +71,7 @@ SIGNATURES = {
     "lbx_advance_particles": (i32, [vp, vp, vp, i64, f64, f64, vp, vp, vp, vp]),
     "lbx_bin_particles": (i32, [vp, i64, f64, i32, i32, vp, vp, vp]),
     "lbx_push_step": (i32, [vp, P(StepArgs), vp]),
-    "lbx_heuristic_cost": (i32, [vp, i32, f64, f64, f64, vp, vp]),
+    "lbx_heuristic_cost": (i32, [vp, vp, i64, f64, f64, vp, vp]),
     "lbx_rank_loads": (i32, [vp, vp, i64, i32, vp]),
     "lbx_efficiency": (i32, [vp, vp, i64, i32, P(f64), P(i32)]),
     "lbx_knapsack": (i32, [vp, i64, i32, f64, vp]),

@@ -498,10 +498,11 @@ __global__ void __launch_bounds__(kBlock) bin_kernel(const double2* __restrict__
   }
 }
 
-__global__ void heuristic_kernel(const long long* __restrict__ counts, int nb, double wp,
-                                 double wc, double cells, double* __restrict__ cost) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b < nb) cost[b] = __dadd_rn(__dmul_rn(wp, (double)counts[b]), __dmul_rn(wc, cells));
+__global__ void heuristic_kernel(const double* __restrict__ particles,
+                                 const double* __restrict__ cells, long long n, double wp,
+                                 double wc, double* __restrict__ cost) {
+  const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < n) cost[b] = __dadd_rn(__dmul_rn(wp, particles[b]), __dmul_rn(wc, cells[b]));
 }
 
 __global__ void init_state_kernel(DevState* st, long long n) {
@@ -803,14 +804,13 @@ int lbx_push_step(lbx_ctx* ctx, const lbx_step_args* a, void* stream) {
   return launch_push_step(ctx, l, stream);
 }
 
-int lbx_heuristic_cost(const int64_t* counts, int32_t nboxes, double w_particle, double w_cell,
-                       double cells_per_box, double* cost, void* stream) {
+int lbx_heuristic_cost(const double* particles, const double* cells, int64_t n,
+                       double w_particle, double w_cell, double* cost, void* stream) {
   clear_error();
-  if (nboxes < 0) return set_error(LBX_EINVAL, "nboxes must be >= 0");
-  if (nboxes == 0) return LBX_OK;
-  heuristic_kernel<<<(nboxes + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
-      reinterpret_cast<const long long*>(counts), nboxes, w_particle, w_cell, cells_per_box,
-      cost);
+  if (n < 0) return set_error(LBX_EINVAL, "length must be >= 0");
+  if (n == 0) return LBX_OK;
+  heuristic_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      particles, cells, n, w_particle, w_cell, cost);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "heuristic launch");
   return LBX_OK;

@@ -38,7 +38,8 @@ struct lbx_sim {
   size_t rec_bytes = 0;
   unsigned char* ring_h = nullptr;
   unsigned char* ring_d = nullptr;
-  std::vector<cudaEvent_t> ev;
+  std::vector<cudaEvent_t> ev, t0, t1;  // completion / kernel timing events
+  bool timing = false;
   std::vector<int64_t> owner, prop, prev;
   std::vector<double> work, cost, scratch, rank_acc;
   std::vector<int64_t> faces_per_rank;
@@ -75,6 +76,8 @@ int cuda_fail(cudaError_t e, const char* what) {
 }
 
 int launch_step(lbx_sim* s, int64_t step, cudaStream_t st) {
+  const int tslot = (int)(step % s->ring);
+  if (s->timing) cudaEventRecord(s->t0[tslot], st);
   const int slot = (int)(step % s->ring);
   Rec d = rec_at(s->ring_d, s->rec_bytes, slot, s->nb);
   const bool kicked = step >= s->cfg.kick_step && s->kvz != nullptr;
@@ -99,6 +102,7 @@ int launch_step(lbx_sim* s, int64_t step, cudaStream_t st) {
   a.err_out = reinterpret_cast<long long*>(d.err);
   int rc = launch_push_step(s->ctx, a, st);
   if (rc) return rc;
+  if (s->timing) cudaEventRecord(s->t1[tslot], st);
   cudaError_t e = cudaEventRecord(s->ev[slot], st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
   return LBX_OK;
@@ -113,6 +117,11 @@ int process_step(lbx_sim* s, int64_t step, lbx_sim_outputs* o, int* halt) {
   cudaError_t e = cudaEventSynchronize(s->ev[slot]);
   if (e != cudaSuccess) return cuda_fail(e, "step kernel");
   Rec h = rec_at(s->ring_h, s->rec_bytes, slot, nb);
+  if (s->timing && o->kernel_ms) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, s->t0[slot], s->t1[slot]);
+    o->kernel_ms[step] = ms;
+  }
   if (*h.err != 0)
     return set_error(LBX_ERANGE, "step %lld: %lld survivors fall outside the box grid",
                      (long long)step, (long long)*h.err);
@@ -274,6 +283,12 @@ int lbx_sim_create(lbx_sim** out, lbx_ctx* ctx, const lbx_sim_config* cfg) {
   }
   s->ev.resize(s->ring);
   for (auto& ev : s->ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  s->t0.resize(s->ring);
+  s->t1.resize(s->ring);
+  for (int i = 0; i < s->ring; ++i) {
+    cudaEventCreate(&s->t0[i]);
+    cudaEventCreate(&s->t1[i]);
+  }
   int rc = ensure_accumulators(ctx, nb);
   if (rc) {
     lbx_sim_destroy(s);
@@ -287,6 +302,8 @@ int lbx_sim_destroy(lbx_sim* s) {
   clear_error();
   if (!s) return LBX_OK;
   for (auto& ev : s->ev) cudaEventSynchronize(ev), cudaEventDestroy(ev);
+  for (auto& ev : s->t0) cudaEventDestroy(ev);
+  for (auto& ev : s->t1) cudaEventDestroy(ev);
   if (s->ring_h) cudaFreeHost(s->ring_h);
   delete s;
   return LBX_OK;
@@ -320,6 +337,7 @@ int lbx_sim_run(lbx_sim* s, int64_t first, int64_t last, lbx_sim_outputs* o, voi
     if (s->owner[b] < 0 || s->owner[b] >= s->cfg.n_ranks)
       return set_error(LBX_EINVAL, "owner entries must lie in [0, %d)", s->cfg.n_ranks);
   cudaStream_t st = (cudaStream_t)stream;
+  s->timing = o->kernel_ms != nullptr;
   int64_t launched = first, processed = first;
   int halt = 0;
   while (processed < last && !halt) {

@@ -1,0 +1,87 @@
+"""Whole-run parity on the GPU: libLBX's native loop vs the reference's own
+results (golden fixtures made by tests/golden/make_golden.py)."""
+import hashlib
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+G = Path(__file__).resolve().parent / "golden"
+
+CASES = ["mini", "mini_none", "mini_static", "mini_sfc", "mini_measured",
+         "mini_instrumented", "tight", "tight_none", "c1", "small", "leaky",
+         "default_short"]
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def runs():
+    return json.loads((G / "runs.json").read_text())
+
+
+def spec_for(runs, name):
+    from paper_2104_11385_b200 import scenarios as S
+    base = {"mini": "mini", "tight": "tight-memory", "default": "default"}
+    if name in runs["_docs"]:
+        spec = S.spec_from_dict(runs["_docs"][name])
+    else:
+        spec = S.load_spec(base[name.split("_")[0]])
+    return S.apply_overrides(spec, **runs[name]["overrides"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_run_matches_reference(runs, name):
+    from paper_2104_11385_b200.workload import run_simulation
+    spec = spec_for(runs, name)
+    res = run_simulation(spec.scenario, spec.policy, spec.build_provider(),
+                         record_counts=True)
+    ref = runs[name]
+    got = {
+        "eff_before": [m.efficiency_before for m in res.metrics],
+        "eff_after": [m.efficiency_after for m in res.metrics],
+        "adopted": [m.adopted for m in res.metrics],
+        "compute_max": [m.compute_max for m in res.metrics],
+        "comm_max": [m.comm_max for m in res.metrics],
+        "gather": [m.gather for m in res.metrics],
+        "redistribute": [m.redistribute for m in res.metrics],
+        "walltime": [m.walltime for m in res.metrics],
+        "max_rank_particles": [m.max_rank_particles for m in res.metrics],
+        "oom": [m.oom for m in res.metrics],
+    }
+    for k, v in ref["metrics"].items():
+        assert got[k] == v, (name, k)
+    assert sha(res.cost_trace) == ref["cost_trace_sha"], name
+    assert sha(res.count_trace.astype(np.int64)) == ref["count_trace_sha"], name
+    assert res.initial_owner.tolist() == ref["initial_owner"]
+    assert [[s, o.tolist()] for s, o in res.adoption_snapshots] == ref["snapshots"]
+    for k, v in ref["summary"].items():
+        assert res.summary[k] == v, (name, k)
+    pos, vel = res.final_state.to_numpy()
+    assert sha(pos) == ref["final_pos_sha"], name
+    assert sha(vel) == ref["final_vel_sha"], name
+
+
+def test_gpuclock_run_rank_correlates_with_true_work(runs):
+    """GpuClock costs (real clock64 tallies) vs the reference's timer model:
+    Spearman rank correlation with true work on every attempt step."""
+    from paper_2104_11385_b200 import scenarios as S
+    from paper_2104_11385_b200.workload import run_simulation
+    spec = S.apply_overrides(S.load_spec("mini"), cost="gpuclock", steps=60)
+    res = run_simulation(spec.scenario, spec.policy, spec.build_provider(),
+                         record_counts=True)
+    assert res.summary["provider"] == "gpuclock"
+    for s in range(0, 60, 10):
+        counts = res.count_trace[s]
+        clk = res.cost_trace[s]
+        occ = counts > 0
+        assert ((clk > 0) == occ).all()
+        rc = np.argsort(np.argsort(clk[occ]))
+        rw = np.argsort(np.argsort(counts[occ]))
+        rho = np.corrcoef(rc, rw)[0, 1]
+        assert rho > 0.9, (s, rho)
