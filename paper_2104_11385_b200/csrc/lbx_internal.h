@@ -21,6 +21,9 @@ struct DevState {
   unsigned int epoch;         // look-back epoch tag, 1..2^22-1
   long long n;                // live particles (input count of the next step)
   long long err;              // cumulative out-of-grid survivors
+  unsigned long long leavers; // absorbed this step (push -> compaction handoff)
+  long long first_leaver;     // lowest index absorbed this step (LLONG_MAX: none)
+  long long n_old;            // count before this step's push (compaction input)
 };
 
 // Host-side model of the particle state's pushed-and-binned step.

@@ -1,34 +1,42 @@
 // libLBX device kernels for sm_100a.
 //
-// The hot path of the reference is two CPU loops per step:
+// The reference's hot path is two CPU loops per step:
 //   advance_particles  (_kernels.pyx:12-35): x += v, absorb, stable compaction
 //   bin_particles      (_kernels.pyx:38-47): per-box survivor counts
 // followed by heuristic_cost (cost.py:83-95) and, for the paper's GpuClock
 // strategy, an on-device per-box cycle tally.
 //
-// B200 design: ONE persistent kernel per step does all of it in a single pass
-// over HBM.  Particles are SoA float64 (z, x, vz, vx), updated in place.
-//   * tiles of 2048 particles are claimed in order from a device ticket;
-//   * each thread loads 4 x (2 particles) with 16-byte vector loads;
-//   * push + absorbing test in registers;
-//   * per-box counts and GpuClock cycles are run-length aggregated per
-//     thread, warp-reduced with redux.sync when the warp sits in one box, and
-//     accumulated in a shared-memory histogram that each CTA flushes once
-//     (one atomicAdd per box per CTA);
-//   * stable compaction uses a decoupled look-back scan over tile survivor
-//     counts; a tile with no absorbed particles at or before it rewrites only
-//     z and x in place (48 B/particle total traffic), otherwise survivors are
-//     written to their compacted slots (safe in place: every predecessor has
-//     loaded its tile before it publishes its status);
-//   * the last CTA to finish forms the cost vector (wp*count + wc*cells with
-//     separately rounded products, cost.py:94), writes the step outputs
-//     (optionally into mapped pinned host memory), zeroes the accumulators
-//     and advances the device-resident count/epoch -- so consecutive steps
-//     need no host round trip.
+// B200 design (particle state SoA float64 z, x, vz, vx in HBM, in place):
+//
+//  push_bin_kernel   one streaming pass, no inter-CTA ordering: 16-byte
+//                    vector loads of two particles per array, push, absorbing
+//                    test, z/x written back in place, per-box survivor counts
+//                    and GpuClock cycles run-length aggregated per thread,
+//                    warp-reduced with redux.sync and accumulated in a 32-bit
+//                    shared-memory histogram flushed with one atomicAdd per
+//                    box per CTA.  Absorbed particles are only counted (and
+//                    the lowest absorbed index recorded).  The last CTA forms
+//                    the cost vector (wp*count + wc*cells, separately rounded
+//                    products: cost.py:94), writes the step record (can be
+//                    mapped pinned host memory) and hands the survivor count
+//                    to the next step on the device.  48 B/particle of HBM.
+//
+//  scan_kernel       stable compaction with a decoupled look-back scan over
+//                    2048-particle tiles claimed from an in-order ticket.
+//    COMPACT_SOA     after a push that absorbed particles: starts at the tile
+//                    of the first absorbed index (everything before it is
+//                    already in place), exits at once when nothing was
+//                    absorbed.  In place is safe: a tile publishes its status
+//                    only after it has loaded its input, and it writes only
+//                    below its own end.
+//    ADVANCE_AOS     the drop-in advance_particles: push + absorb + compaction
+//                    from the reference's [n][2] layout into fresh buffers.
 
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
+#include <cmath>
 #include <cstdio>
 
 #include "lbx_internal.h"
@@ -38,10 +46,13 @@ namespace {
 
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
-constexpr int kItems = 8;                 // particles per thread per tile
-constexpr int kTile = kBlock * kItems;    // 2048 particles per tile
-constexpr int kSmemBoxesMax = 8192;       // shared-memory histogram limit
+constexpr int kItems = 8;                 // particles per thread per scan tile
+constexpr int kTile = kBlock * kItems;    // 2048 particles per scan tile
+constexpr int kPairs = 2;                 // 16-byte pairs per thread per push iteration
+constexpr int kSmemBoxesMax = 12288;      // shared-memory histogram limit (96 KB)
+constexpr int kFlushIters = 128;          // push iterations between histogram flushes
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kClockShift = 4;            // GpuClock tally unit: 16 SM cycles
 
 constexpr int kEpochShift = 42;
 constexpr int kFlagShift = 40;
@@ -50,25 +61,17 @@ constexpr unsigned long long kFlagAgg = 1ull;
 constexpr unsigned long long kFlagPfx = 2ull;
 constexpr unsigned kEpochMask = (1u << 22) - 1;
 
-enum Layout { kSoAInPlace = 0, kAoSOutOfPlace = 1 };
+enum ScanMode { kAdvanceAoS = 0, kCompactSoA = 1 };
 
-struct PushParams {
-  // SoA (in place)
+struct StepParams {
   double* z;
   double* x;
-  double* vz;
-  double* vx;
-  // AoS (drop-in, out of place)
-  const double2* in_pos;
-  const double2* in_vel;
-  double2* out_pos;
-  double2* out_vel;
-  double ez, ex, m;
+  const double* vz;
+  const double* vx;
+  double ez, ex, m, inv_m;
   int nbz, nbx, nb;
   int smem_hist;
-  long long n_override;        // >= 0: particle count given by the host
   DevState* st;
-  unsigned long long* status;
   unsigned long long* g_cnt;
   unsigned long long* g_clk;
   long long* counts_out;
@@ -77,6 +80,24 @@ struct PushParams {
   long long* n_out;
   long long* err_out;
   double wp, wc, cells;
+};
+
+struct ScanParams {
+  // COMPACT_SOA (in place)
+  double* z;
+  double* x;
+  double* vz;
+  double* vx;
+  // ADVANCE_AOS (out of place)
+  const double2* in_pos;
+  const double2* in_vel;
+  double2* out_pos;
+  double2* out_vel;
+  double ez, ex;
+  long long n_host;  // ADVANCE_AOS: particle count
+  DevState* st;
+  unsigned long long* status;
+  long long* n_out;
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
@@ -107,18 +128,245 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
   return v;
 }
 
+__device__ __forceinline__ long long warp_min_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+__device__ __forceinline__ bool inside(double z, double x, double ez, double ex) {
+  return z >= 0.0 && z < ez && x >= 0.0 && x < ex;
+}
+
+// ---------------------------------------------------------------------------
+// push_bin_kernel
+// ---------------------------------------------------------------------------
+
+template <bool kClock>
+__device__ __forceinline__ void hist_add(const StepParams& p, unsigned* s_cnt, unsigned* s_clk,
+                                         int b, unsigned cnt, unsigned clk) {
+  if (p.smem_hist) {
+    atomicAdd(s_cnt + b, cnt);
+    if (kClock) atomicAdd(s_clk + b, clk);
+  } else {
+    atomicAdd(p.g_cnt + b, (unsigned long long)cnt);
+    if (kClock) atomicAdd(p.g_clk + b, (unsigned long long)clk);
+  }
+}
+
+template <bool kClock>
+__device__ __forceinline__ void hist_flush(const StepParams& p, unsigned* s_cnt, unsigned* s_clk) {
+  for (int b = threadIdx.x; b < p.nb; b += kBlock) {
+    const unsigned c = s_cnt[b];
+    if (c) {
+      atomicAdd(p.g_cnt + b, (unsigned long long)c);
+      s_cnt[b] = 0u;
+    }
+    if (kClock) {
+      const unsigned k = s_clk[b];
+      if (k) {
+        atomicAdd(p.g_clk + b, (unsigned long long)k);
+        s_clk[b] = 0u;
+      }
+    }
+  }
+}
+
+template <bool kClock, bool kPow2>
+__global__ void __launch_bounds__(kBlock, 4) push_bin_kernel(StepParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned* s_cnt = reinterpret_cast<unsigned*>(smem_raw);
+  unsigned* s_clk = s_cnt + p.nb;
+  __shared__ long long s_n;
+  __shared__ int s_last;
+  __shared__ unsigned long long s_red[kWarps];
+  __shared__ long long s_min[kWarps];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  if (tid == 0) s_n = *((volatile long long*)&p.st->n);
+  if (p.smem_hist) {
+    for (int b = tid; b < p.nb; b += kBlock) {
+      s_cnt[b] = 0u;
+      if (kClock) s_clk[b] = 0u;
+    }
+  }
+  __syncthreads();
+  const long long n = s_n;
+  const long long npairs = (n + 1) >> 1;
+  const long long stride = (long long)gridDim.x * kBlock * kPairs;
+  double2* z2 = reinterpret_cast<double2*>(p.z);
+  double2* x2 = reinterpret_cast<double2*>(p.x);
+  const double2* vz2 = reinterpret_cast<const double2*>(p.vz);
+  const double2* vx2 = reinterpret_cast<const double2*>(p.vx);
+
+  unsigned long long absorbed = 0;
+  long long first_out = LLONG_MAX;
+  long long err = 0;
+  int iter = 0;
+  // The loop trip count is uniform across the CTA (grid-stride over
+  // CTA-sized chunks), so the periodic histogram flush can use barriers.
+  for (long long q0 = (long long)blockIdx.x * kBlock * kPairs; q0 < npairs; q0 += stride) {
+    long long t0 = 0;
+    if (kClock) t0 = clock64();
+    double pz[2 * kPairs], px[2 * kPairs];
+    bool keep[2 * kPairs];
+#pragma unroll
+    for (int r = 0; r < kPairs; ++r) {
+      const long long q = q0 + r * kBlock + tid;
+      double2 a = make_double2(-1.0, -1.0), b = a, c = make_double2(0.0, 0.0), d = c;
+      const bool any = q < npairs;
+      if (any) {
+        a = __ldcs(z2 + q);
+        b = __ldcs(x2 + q);
+        c = __ldcs(vz2 + q);
+        d = __ldcs(vx2 + q);
+      }
+      pz[2 * r] = __dadd_rn(a.x, c.x);
+      pz[2 * r + 1] = __dadd_rn(a.y, c.y);
+      px[2 * r] = __dadd_rn(b.x, d.x);
+      px[2 * r + 1] = __dadd_rn(b.y, d.y);
+      const long long i0 = 2 * q;
+      keep[2 * r] = any && inside(pz[2 * r], px[2 * r], p.ez, p.ex);
+      keep[2 * r + 1] = i0 + 1 < n && inside(pz[2 * r + 1], px[2 * r + 1], p.ez, p.ex);
+      if (any) {
+        __stcs(z2 + q, make_double2(pz[2 * r], pz[2 * r + 1]));
+        __stcs(x2 + q, make_double2(px[2 * r], px[2 * r + 1]));
+        if (!keep[2 * r]) {
+          ++absorbed;
+          first_out = min(first_out, i0);
+        }
+        if (i0 + 1 < n && !keep[2 * r + 1]) {
+          ++absorbed;
+          first_out = min(first_out, i0 + 1);
+        }
+      }
+    }
+    int box[2 * kPairs];
+#pragma unroll
+    for (int k = 0; k < 2 * kPairs; ++k) {
+      box[k] = -1;
+      if (keep[k]) {
+        int bz, bx;
+        if (kPow2) {
+          bz = (int)__dmul_rn(pz[k], p.inv_m);  // exact: M is a power of two
+          bx = (int)__dmul_rn(px[k], p.inv_m);
+        } else {
+          bz = (int)__ddiv_rn(pz[k], p.m);
+          bx = (int)__ddiv_rn(px[k], p.m);
+        }
+        if (bz < p.nbz && bx < p.nbx) {
+          box[k] = bz * p.nbx + bx;
+        } else {
+          ++err;
+        }
+      }
+    }
+    unsigned dt = 0;
+    if (kClock) {
+      const long long t1 = clock64();
+      dt = (unsigned)min(t1 - t0, (long long)(1 << 20)) >> kClockShift;
+    }
+    int cur = -1;
+    unsigned run = 0;
+#pragma unroll
+    for (int k = 0; k < 2 * kPairs; ++k) {
+      if (box[k] != cur) {
+        if (cur >= 0) hist_add<kClock>(p, s_cnt, s_clk, cur, run, dt * run);
+        cur = box[k];
+        run = 0;
+      }
+      run += (box[k] >= 0) ? 1u : 0u;
+    }
+    const int cur0 = __shfl_sync(kFull, cur, 0);
+    if (__all_sync(kFull, cur == cur0)) {
+      const unsigned tot = __reduce_add_sync(kFull, run);
+      const unsigned clk = kClock ? __reduce_add_sync(kFull, dt * run) : 0u;
+      if (lane == 0 && cur0 >= 0 && tot) hist_add<kClock>(p, s_cnt, s_clk, cur0, tot, clk);
+    } else if (cur >= 0 && run) {
+      hist_add<kClock>(p, s_cnt, s_clk, cur, run, dt * run);
+    }
+    if (p.smem_hist && ++iter == kFlushIters) {  // keep 32-bit accumulators bounded
+      iter = 0;
+      __syncthreads();
+      hist_flush<kClock>(p, s_cnt, s_clk);
+      __syncthreads();
+    }
+  }
+
+  // ---- CTA totals: absorbed count, first absorbed index, errors ----
+  unsigned long long wa = (unsigned long long)warp_sum_ll((long long)absorbed);
+  long long wm = warp_min_ll(first_out);
+  long long we = warp_sum_ll(err);
+  if (lane == 0) {
+    s_red[warp] = wa;
+    s_min[warp] = wm;
+  }
+  if (we && lane == 0) atomicAdd((unsigned long long*)&p.st->err, (unsigned long long)we);
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long ta = 0;
+    long long tm = LLONG_MAX;
+    for (int w = 0; w < kWarps; ++w) {
+      ta += s_red[w];
+      tm = min(tm, s_min[w]);
+    }
+    if (ta) {
+      atomicAdd(&p.st->leavers, ta);
+      atomicMin(&p.st->first_leaver, tm);
+    }
+  }
+  if (p.smem_hist) hist_flush<kClock>(p, s_cnt, s_clk);
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(&p.st->done, 1u) == gridDim.x - 1) ? 1 : 0;
+  __syncthreads();
+  if (!s_last) return;
+
+  // ---- last CTA: step epilogue ----
+  __threadfence();
+  for (int b = tid; b < p.nb; b += kBlock) {
+    const unsigned long long c = atomicExch(p.g_cnt + b, 0ull);
+    if (p.counts_out) p.counts_out[b] = (long long)c;
+    if (p.cost_out) {
+      p.cost_out[b] =
+          __dadd_rn(__dmul_rn(p.wp, (double)(long long)c), __dmul_rn(p.wc, p.cells));
+    }
+    if (kClock) {
+      const unsigned long long k = atomicExch(p.g_clk + b, 0ull);
+      if (p.clk_out) p.clk_out[b] = k << kClockShift;
+    }
+  }
+  if (tid == 0) {
+    const unsigned long long lv = *((volatile unsigned long long*)&p.st->leavers);
+    const long long n_new = n - (long long)lv;
+    if (p.n_out) *p.n_out = n_new;
+    if (p.err_out) *p.err_out = *((volatile long long*)&p.st->err);
+    p.st->n_old = n;
+    p.st->n = n_new;
+    p.st->done = 0u;
+    __threadfence_system();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// scan_kernel (decoupled look-back stable compaction)
+// ---------------------------------------------------------------------------
+
 // Exclusive prefix of survivors over all tiles before `tile` (warp 0 only).
-// Reads a window of 32 predecessors per iteration; stops at the nearest one
-// that has published its inclusive prefix.
-__device__ long long lookback(unsigned long long* status, long long tile, unsigned epoch) {
+// Tile tile0 publishes an inclusive prefix that already includes everything
+// before it, so the walk never goes below tile0.
+__device__ long long lookback(unsigned long long* status, long long tile, long long tile0,
+                              unsigned epoch) {
   const int lane = threadIdx.x & 31;
   long long acc = 0;
   long long top = tile - 1;
   while (true) {
     const long long idx = top - lane;
     unsigned long long s = 0;
-    unsigned long long flag = kFlagPfx;  // virtual predecessor of tile 0
-    if (idx >= 0) {
+    unsigned long long flag = kFlagPfx;  // below tile0: virtual, never reached first
+    if (idx >= tile0) {
       do {
         s = ld_acquire(status + idx);
         flag = ((unsigned)(s >> kEpochShift) == epoch) ? ((s >> kFlagShift) & 3ull) : 0ull;
@@ -136,31 +384,16 @@ __device__ long long lookback(unsigned long long* status, long long tile, unsign
   }
 }
 
-template <bool kClock>
-__device__ __forceinline__ void hist_add(const PushParams& p, unsigned* s_cnt,
-                                         unsigned long long* s_clk, int b, unsigned cnt,
-                                         unsigned clk) {
-  if (p.smem_hist) {
-    atomicAdd(s_cnt + b, cnt);
-    if (kClock) atomicAdd(s_clk + b, (unsigned long long)clk);
-  } else {
-    atomicAdd(p.g_cnt + b, (unsigned long long)cnt);
-    if (kClock) atomicAdd(p.g_clk + b, (unsigned long long)clk);
-  }
-}
-
-template <int kLayout, bool kHist, bool kClock>
-__global__ void __launch_bounds__(kBlock, 2) push_kernel(PushParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  unsigned long long* s_clk = reinterpret_cast<unsigned long long*>(smem_raw);
-  unsigned* s_cnt = reinterpret_cast<unsigned*>(smem_raw + (kClock ? 8 * p.nb : 0));
-
+template <int kMode>
+__global__ void __launch_bounds__(kBlock, 3) scan_kernel(ScanParams p) {
   __shared__ long long s_tile;
   __shared__ long long s_prefix;
+  __shared__ int s_total;
   __shared__ int s_last;
   __shared__ long long s_n;
+  __shared__ long long s_tile0;
   __shared__ unsigned s_epoch;
-  constexpr int kRows = (kLayout == kSoAInPlace) ? kItems / 2 : kItems;
+  constexpr int kRows = (kMode == kCompactSoA) ? kItems / 2 : kItems;
   __shared__ int s_row[kRows * kWarps];
 
   const int tid = threadIdx.x;
@@ -168,65 +401,63 @@ __global__ void __launch_bounds__(kBlock, 2) push_kernel(PushParams p) {
   const int warp = tid >> 5;
 
   if (tid == 0) {
-    s_n = p.n_override >= 0 ? p.n_override : *((volatile long long*)&p.st->n);
-    s_epoch = *((volatile unsigned*)&p.st->epoch);
-  }
-  if (kHist && p.smem_hist) {
-    for (int b = tid; b < p.nb; b += kBlock) {
-      s_cnt[b] = 0u;
-      if (kClock) s_clk[b] = 0ull;
+    if (kMode == kCompactSoA) {
+      const unsigned long long lv = *((volatile unsigned long long*)&p.st->leavers);
+      s_n = lv ? *((volatile long long*)&p.st->n_old) : 0;
+      s_tile0 = lv ? (*((volatile long long*)&p.st->first_leaver)) / kTile : 0;
+    } else {
+      s_n = p.n_host;
+      s_tile0 = 0;
     }
+    s_epoch = *((volatile unsigned*)&p.st->epoch);
   }
   __syncthreads();
   const long long n = s_n;
+  const long long tile0 = s_tile0;
   const unsigned epoch = s_epoch;
   const long long ntiles = (n + kTile - 1) / kTile;
-  long long err = 0;
+  if (kMode == kCompactSoA && n == 0) return;  // nothing absorbed: data already final
 
   while (true) {
-    if (tid == 0) s_tile = (long long)atomicAdd(&p.st->ticket, 1ull);
+    if (tid == 0) s_tile = tile0 + (long long)atomicAdd(&p.st->ticket, 1ull);
     __syncthreads();
     const long long tile = s_tile;
     if (tile >= ntiles) break;
     const long long base = tile * kTile;
     const long long valid = min((long long)kTile, n - base);
 
-    long long t0 = 0;
-    if (kClock) t0 = clock64();
-
     double pz[kItems], px[kItems], pvz[kItems], pvx[kItems];
     bool keep[kItems];
-
-    if (kLayout == kSoAInPlace) {
+    if (kMode == kCompactSoA) {
       const double2* z2 = reinterpret_cast<const double2*>(p.z);
       const double2* x2 = reinterpret_cast<const double2*>(p.x);
       const double2* vz2 = reinterpret_cast<const double2*>(p.vz);
       const double2* vx2 = reinterpret_cast<const double2*>(p.vx);
 #pragma unroll
-      for (int r = 0; r < kItems / 2; ++r) {
-        const long long q = (base >> 1) + r * kBlock + tid;  // pair index
+      for (int r = 0; r < kRows; ++r) {
+        const long long q = (base >> 1) + r * kBlock + tid;
         const long long i0 = 2 * q;
-        double2 a = make_double2(0.0, 0.0), b = a, c = a, d = a;
+        double2 a = make_double2(-1.0, -1.0), b = a, c = make_double2(0.0, 0.0), d = c;
         if (i0 < n) {
           a = __ldcs(z2 + q);
           b = __ldcs(x2 + q);
           c = __ldcs(vz2 + q);
           d = __ldcs(vx2 + q);
         }
+        pz[2 * r] = a.x;
+        pz[2 * r + 1] = a.y;
+        px[2 * r] = b.x;
+        px[2 * r + 1] = b.y;
         pvz[2 * r] = c.x;
         pvz[2 * r + 1] = c.y;
         pvx[2 * r] = d.x;
         pvx[2 * r + 1] = d.y;
-        pz[2 * r] = __dadd_rn(a.x, c.x);
-        pz[2 * r + 1] = __dadd_rn(a.y, c.y);
-        px[2 * r] = __dadd_rn(b.x, d.x);
-        px[2 * r + 1] = __dadd_rn(b.y, d.y);
-        keep[2 * r] = i0 < n;
-        keep[2 * r + 1] = i0 + 1 < n;
+        keep[2 * r] = i0 < n && inside(a.x, b.x, p.ez, p.ex);
+        keep[2 * r + 1] = i0 + 1 < n && inside(a.y, b.y, p.ez, p.ex);
       }
     } else {
 #pragma unroll
-      for (int r = 0; r < kItems; ++r) {
+      for (int r = 0; r < kRows; ++r) {
         const long long i = base + r * kBlock + tid;
         double2 a = make_double2(0.0, 0.0), c = a;
         if (i < n) {
@@ -237,60 +468,14 @@ __global__ void __launch_bounds__(kBlock, 2) push_kernel(PushParams p) {
         pvx[r] = c.y;
         pz[r] = __dadd_rn(a.x, c.x);
         px[r] = __dadd_rn(a.y, c.y);
-        keep[r] = i < n;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-      keep[k] = keep[k] && pz[k] >= 0.0 && pz[k] < p.ez && px[k] >= 0.0 && px[k] < p.ex;
-    }
-
-    // ---- per-box counts + GpuClock tally (survivors, new positions) ----
-    if (kHist) {
-      int box[kItems];
-#pragma unroll
-      for (int k = 0; k < kItems; ++k) {
-        box[k] = -1;
-        if (keep[k]) {
-          const int bz = (int)__ddiv_rn(pz[k], p.m);
-          const int bx = (int)__ddiv_rn(px[k], p.m);
-          if (bz < p.nbz && bx < p.nbx) {
-            box[k] = bz * p.nbx + bx;
-          } else {
-            ++err;
-          }
-        }
-      }
-      unsigned dt = 0;
-      if (kClock) {
-        const long long t1 = clock64();
-        dt = (unsigned)min(t1 - t0, (long long)(1 << 22));
-      }
-      int cur = -1;
-      unsigned run = 0;
-#pragma unroll
-      for (int k = 0; k < kItems; ++k) {
-        if (box[k] != cur) {
-          if (cur >= 0) hist_add<kClock>(p, s_cnt, s_clk, cur, run, dt * run);
-          cur = box[k];
-          run = 0;
-        }
-        run += (box[k] >= 0) ? 1u : 0u;
-      }
-      const int cur0 = __shfl_sync(kFull, cur, 0);
-      if (__all_sync(kFull, cur == cur0)) {
-        const unsigned tot = __reduce_add_sync(kFull, run);
-        const unsigned clk = kClock ? __reduce_add_sync(kFull, dt * run) : 0u;
-        if (lane == 0 && cur0 >= 0 && tot) hist_add<kClock>(p, s_cnt, s_clk, cur0, tot, clk);
-      } else if (cur >= 0 && run) {
-        hist_add<kClock>(p, s_cnt, s_clk, cur, run, dt * run);
+        keep[r] = i < n && inside(pz[r], px[r], p.ez, p.ex);
       }
     }
 
-    // ---- tile-local ranks of survivors (tile order = index order) ----
+    // tile-local ranks of survivors (tile order == index order)
     int pre[kItems];
     const unsigned lt = lanemask_lt();
-    if (kLayout == kSoAInPlace) {
+    if (kMode == kCompactSoA) {
 #pragma unroll
       for (int r = 0; r < kRows; ++r) {
         const unsigned b0 = __ballot_sync(kFull, keep[2 * r]);
@@ -309,7 +494,6 @@ __global__ void __launch_bounds__(kBlock, 2) push_kernel(PushParams p) {
     }
     __syncthreads();
 
-    // ---- warp 0: scan row counts, publish, look back ----
     if (warp == 0) {
       constexpr int kPer = (kRows * kWarps) / 32;
       int v[kPer];
@@ -326,24 +510,25 @@ __global__ void __launch_bounds__(kBlock, 2) push_kernel(PushParams p) {
         if (lane >= o) incl += y;
       }
       const int total = __shfl_sync(kFull, incl, 31);
-      int run_off = incl - sum;
+      int off = incl - sum;
 #pragma unroll
       for (int e = 0; e < kPer; ++e) {
-        s_row[lane * kPer + e] = run_off;
-        run_off += v[e];
+        s_row[lane * kPer + e] = off;
+        off += v[e];
       }
-      long long prefix = 0;
-      if (tile == 0) {
+      long long prefix = tile0 * kTile;  // everything before tile0 stays put
+      if (tile == tile0) {
         if (lane == 0) {
           __threadfence();
-          st_release(p.status, pack_status(epoch, kFlagPfx, (unsigned long long)total));
+          st_release(p.status + tile,
+                     pack_status(epoch, kFlagPfx, (unsigned long long)(prefix + total)));
         }
       } else {
         if (lane == 0) {
           __threadfence();
           st_release(p.status + tile, pack_status(epoch, kFlagAgg, (unsigned long long)total));
         }
-        prefix = lookback(p.status, tile, epoch);
+        prefix = lookback(p.status, tile, tile0, epoch);
         if (lane == 0) {
           st_release(p.status + tile,
                      pack_status(epoch, kFlagPfx, (unsigned long long)(prefix + total)));
@@ -351,27 +536,15 @@ __global__ void __launch_bounds__(kBlock, 2) push_kernel(PushParams p) {
       }
       if (lane == 0) {
         s_prefix = prefix;
-        s_last = total;  // reuse as tile survivor count for the fast-path test
+        s_total = total;
       }
     }
     __syncthreads();
     const long long prefix = s_prefix;
-    const bool fast = (prefix == base) && ((long long)s_last == valid);
+    const bool in_place = (prefix == base) && ((long long)s_total == valid);
 
-    // ---- stores ----
-    if (kLayout == kSoAInPlace) {
-      if (fast) {
-        double2* z2 = reinterpret_cast<double2*>(p.z);
-        double2* x2 = reinterpret_cast<double2*>(p.x);
-#pragma unroll
-        for (int r = 0; r < kItems / 2; ++r) {
-          const long long q = (base >> 1) + r * kBlock + tid;
-          if (2 * q < n) {
-            __stcs(z2 + q, make_double2(pz[2 * r], pz[2 * r + 1]));
-            __stcs(x2 + q, make_double2(px[2 * r], px[2 * r + 1]));
-          }
-        }
-      } else {
+    if (kMode == kCompactSoA) {
+      if (!in_place) {
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
           if (keep[k]) {
@@ -396,58 +569,31 @@ __global__ void __launch_bounds__(kBlock, 2) push_kernel(PushParams p) {
     __syncthreads();  // s_row / s_tile reuse
   }
 
-  // ---- CTA exit: flush the shared histogram (one atomic per box) ----
-  if (kHist) {
-    if (err) atomicAdd((unsigned long long*)&p.st->err, (unsigned long long)err);
-    if (p.smem_hist) {
-      for (int b = tid; b < p.nb; b += kBlock) {
-        const unsigned c = s_cnt[b];
-        if (c) atomicAdd(p.g_cnt + b, (unsigned long long)c);
-        if (kClock) {
-          const unsigned long long k = s_clk[b];
-          if (k) atomicAdd(p.g_clk + b, k);
-        }
-      }
-    }
-  }
   __threadfence();
   __syncthreads();
   if (tid == 0) s_last = (atomicAdd(&p.st->done, 1u) == gridDim.x - 1) ? 1 : 0;
   __syncthreads();
-  if (!s_last) return;
-
-  // ---- last CTA: step epilogue ----
+  if (!s_last || tid != 0) return;
   __threadfence();
-  long long n_new = 0;
-  if (ntiles > 0) n_new = (long long)(ld_acquire(p.status + (ntiles - 1)) & kValueMask);
-  if (kHist) {
-    for (int b = tid; b < p.nb; b += kBlock) {
-      const unsigned long long c = atomicExch(p.g_cnt + b, 0ull);
-      if (p.counts_out) p.counts_out[b] = (long long)c;
-      if (p.cost_out) {
-        p.cost_out[b] = __dadd_rn(__dmul_rn(p.wp, (double)(long long)c),
-                                  __dmul_rn(p.wc, p.cells));
-      }
-      if (kClock) {
-        const unsigned long long k = atomicExch(p.g_clk + b, 0ull);
-        if (p.clk_out) p.clk_out[b] = k;
-      }
-    }
+  long long n_new = tile0 * kTile;
+  if (ntiles > tile0) n_new = (long long)(ld_acquire(p.status + (ntiles - 1)) & kValueMask);
+  if (kMode == kAdvanceAoS && p.n_out) *p.n_out = n_new;
+  if (kMode == kCompactSoA) {
+    p.st->leavers = 0ull;
+    p.st->first_leaver = LLONG_MAX;
+    if (*((volatile long long*)&p.st->n) != n_new) p.st->err += 1ll << 40;  // invariant
   }
-  if (tid == 0) {
-    if (p.n_out) *p.n_out = n_new;
-    const long long e = *((volatile long long*)&p.st->err);
-    if (p.err_out) *p.err_out = e;
-    p.st->n = n_new;
-    p.st->ticket = 0ull;
-    p.st->done = 0u;
-    unsigned ne = (epoch + 1u) & kEpochMask;
-    p.st->epoch = ne ? ne : 1u;
-    __threadfence_system();
-  }
+  p.st->ticket = 0ull;
+  p.st->done = 0u;
+  const unsigned ne = (epoch + 1u) & kEpochMask;
+  p.st->epoch = ne ? ne : 1u;
+  __threadfence();
 }
 
-// Histogram of AoS positions (drop-in bin_particles).
+// ---------------------------------------------------------------------------
+// drop-in bin_particles, heuristic cost, state init
+// ---------------------------------------------------------------------------
+
 __global__ void __launch_bounds__(kBlock) bin_kernel(const double2* __restrict__ pos,
                                                      long long n, double m, int nbz, int nbx,
                                                      int smem_hist,
@@ -510,36 +656,56 @@ __global__ void init_state_kernel(DevState* st, long long n) {
   st->done = 0u;
   if (st->epoch == 0u) st->epoch = 1u;
   st->n = n;
+  st->n_old = n;
+  st->leavers = 0ull;
+  st->first_leaver = LLONG_MAX;
 }
 
 inline int cuda_fail(cudaError_t e, const char* what) {
   return set_error(LBX_ECUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
-template <int kLayout, bool kHist, bool kClock>
-int launch_push(lbx_ctx* ctx, PushParams& p, long long n_upper, cudaStream_t s) {
-  auto kern = push_kernel<kLayout, kHist, kClock>;
-  const size_t smem =
-      (kHist && p.smem_hist) ? (size_t)p.nb * (4 + (kClock ? 8 : 0)) : (size_t)0;
-  static thread_local size_t configured[2][2][2] = {};
-  size_t& cfg = configured[kLayout][kHist][kClock];
-  if (smem > 48 * 1024 && smem > cfg) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    cfg = smem;
-  }
+template <typename K>
+int occupancy_grid(lbx_ctx* ctx, K kern, size_t smem, long long work_ctas, int* grid_out) {
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem);
   if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
-  if (per_sm < 1) per_sm = 1;
-  long long grid = (long long)per_sm * ctx->num_sms;
+  long long grid = (long long)std::max(per_sm, 1) * ctx->num_sms;
   if (ctx->grid_override > 0) grid = ctx->grid_override;
-  const long long tiles = (n_upper + kTile - 1) / kTile;
-  grid = std::max(1ll, std::min(grid, tiles));
-  kern<<<(unsigned)grid, kBlock, smem, s>>>(p);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "push_kernel launch");
+  *grid_out = (int)std::max(1ll, std::min(grid, work_ctas));
+  return LBX_OK;
+}
+
+template <bool kClock, bool kPow2>
+int launch_push_bin(lbx_ctx* ctx, const StepParams& p, cudaStream_t s) {
+  auto kern = push_bin_kernel<kClock, kPow2>;
+  const size_t smem = p.smem_hist ? (size_t)p.nb * 4 * (kClock ? 2 : 1) : 0;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    configured = smem;
+  }
+  int grid = 0;
+  const long long work = (ctx->n_upper + 2ll * kBlock * kPairs - 1) / (2ll * kBlock * kPairs);
+  int rc = occupancy_grid(ctx, kern, smem, std::max(1ll, work), &grid);
+  if (rc) return rc;
+  kern<<<grid, kBlock, smem, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "push_bin_kernel launch");
+  return LBX_OK;
+}
+
+template <int kMode>
+int launch_scan(lbx_ctx* ctx, const ScanParams& p, long long n_upper, cudaStream_t s) {
+  auto kern = scan_kernel<kMode>;
+  int grid = 0;
+  int rc = occupancy_grid(ctx, kern, 0, std::max(1ll, (n_upper + kTile - 1) / kTile), &grid);
+  if (rc) return rc;
+  kern<<<grid, kBlock, 0, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "scan_kernel launch");
   return LBX_OK;
 }
 
@@ -548,7 +714,8 @@ int reserve_status(lbx_ctx* ctx, int64_t capacity) {
   if (tiles <= ctx->status_tiles) return LBX_OK;
   unsigned long long* s = nullptr;
   cudaError_t e = cudaMalloc(&s, (size_t)tiles * sizeof(unsigned long long));
-  if (e != cudaSuccess) return set_error(LBX_EOOM, "look-back workspace: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess)
+    return set_error(LBX_EOOM, "look-back workspace: %s", cudaGetErrorString(e));
   // Epoch 0 is never current, so zeroed words read as "not yet published".
   e = cudaMemset(s, 0, (size_t)tiles * sizeof(unsigned long long));
   if (e != cudaSuccess) {
@@ -562,6 +729,12 @@ int reserve_status(lbx_ctx* ctx, int64_t capacity) {
   ctx->status = s;
   ctx->status_tiles = tiles;
   return LBX_OK;
+}
+
+bool is_pow2(double m) {
+  int e = 0;
+  const double f = std::frexp(m, &e);
+  return f == 0.5;
 }
 
 }  // namespace
@@ -593,7 +766,7 @@ int launch_push_step(lbx_ctx* ctx, const StepLaunch& a, void* stream) {
   if (rc) return rc;
   rc = reserve_status(ctx, ctx->n_upper);
   if (rc) return rc;
-  PushParams p{};
+  StepParams p{};
   p.z = a.z;
   p.x = a.x;
   p.vz = a.vz;
@@ -601,13 +774,12 @@ int launch_push_step(lbx_ctx* ctx, const StepLaunch& a, void* stream) {
   p.ez = a.ez;
   p.ex = a.ex;
   p.m = a.m;
+  p.inv_m = 1.0 / a.m;
   p.nbz = a.nbz;
   p.nbx = a.nbx;
   p.nb = (int)nb;
   p.smem_hist = nb <= kSmemBoxesMax ? 1 : 0;
-  p.n_override = -1;
   p.st = ctx->st;
-  p.status = ctx->status;
   p.g_cnt = ctx->acc;
   p.g_clk = ctx->acc + ctx->acc_boxes;
   p.counts_out = a.counts_out;
@@ -619,8 +791,25 @@ int launch_push_step(lbx_ctx* ctx, const StepLaunch& a, void* stream) {
   p.wc = a.wc;
   p.cells = a.cells;
   cudaStream_t s = (cudaStream_t)stream;
-  if (a.clock) return launch_push<kSoAInPlace, true, true>(ctx, p, ctx->n_upper, s);
-  return launch_push<kSoAInPlace, true, false>(ctx, p, ctx->n_upper, s);
+  const bool pow2 = is_pow2(a.m);
+  if (a.clock) {
+    rc = pow2 ? launch_push_bin<true, true>(ctx, p, s) : launch_push_bin<true, false>(ctx, p, s);
+  } else {
+    rc = pow2 ? launch_push_bin<false, true>(ctx, p, s)
+              : launch_push_bin<false, false>(ctx, p, s);
+  }
+  if (rc) return rc;
+  // Stable compaction of the survivors; returns at once when none was absorbed.
+  ScanParams c{};
+  c.z = a.z;
+  c.x = a.x;
+  c.vz = const_cast<double*>(a.vz);
+  c.vx = const_cast<double*>(a.vx);
+  c.ez = a.ez;
+  c.ex = a.ex;
+  c.st = ctx->st;
+  c.status = ctx->status;
+  return launch_scan<kCompactSoA>(ctx, c, ctx->n_upper, s);
 }
 
 }  // namespace lbx
@@ -733,20 +922,18 @@ int lbx_advance_particles(lbx_ctx* ctx, const double* pos, const double* vel, in
     return set_error(LBX_EINVAL, "particle arrays must be 16-byte aligned");
   int rc = reserve_status(ctx, n);
   if (rc) return rc;
-  PushParams p{};
+  ScanParams p{};
   p.in_pos = reinterpret_cast<const double2*>(pos);
   p.in_vel = reinterpret_cast<const double2*>(vel);
   p.out_pos = reinterpret_cast<double2*>(out_pos);
   p.out_vel = reinterpret_cast<double2*>(out_vel);
   p.ez = extent_z;
   p.ex = extent_x;
-  p.m = 1.0;
-  p.nbz = p.nbx = p.nb = 1;
-  p.n_override = n;
+  p.n_host = n;
   p.st = ctx->st;
   p.status = ctx->status;
   p.n_out = reinterpret_cast<long long*>(m_dev);
-  return launch_push<kAoSOutOfPlace, false, false>(ctx, p, n, (cudaStream_t)stream);
+  return launch_scan<kAdvanceAoS>(ctx, p, n, (cudaStream_t)stream);
 }
 
 int lbx_bin_particles(const double* pos, int64_t n, double box_size, int32_t nbz, int32_t nbx,
@@ -768,6 +955,8 @@ int lbx_bin_particles(const double* pos, int64_t n, double box_size, int32_t nbz
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int smem_hist = nb <= kSmemBoxesMax ? 1 : 0;
   const size_t smem = smem_hist ? (size_t)nb * 4 : 0;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   long long grid = std::min((long long)sms * 8, (long long)((n + kBlock * 8 - 1) / (kBlock * 8)));
   grid = std::max(1ll, grid);
   bin_kernel<<<(unsigned)grid, kBlock, smem, s>>>(

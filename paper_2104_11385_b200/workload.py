@@ -466,6 +466,11 @@ class Simulation:
         eff = np.array([m.efficiency_after for m in metrics])
         oom = bool(done and metrics[-1].oom)
         final = int(o["n_alive"][done - 1]) if done else self.n_init
+        from .device import ParticleState
+        kicked = self.kvz is not None and done > cfg.kick.step
+        st = self.state
+        final_state = ParticleState(st.z, st.x, self.kvz if kicked else st.vz,
+                                    self.kvx if kicked else st.vx, final)
         summary = {
             "scenario_id": cfg.scenario_id, "n_ranks": cfg.n_ranks,
             "n_boxes": self.ba.n_boxes, "box_grid": list(self.ba.grid_shape),
@@ -489,7 +494,7 @@ class Simulation:
             count_trace=None if o["count_trace"] is None else o["count_trace"][:done].copy(),
             clock_trace=None if o["clock_trace"] is None else o["clock_trace"][:done].copy(),
             kernel_ms=o["kernel_ms"][:done].copy() if self.time_kernels else None,
-            final_state=self.state)
+            final_state=final_state)
 
 
 def run_simulation(cfg: ScenarioConfig, policy: BalancePolicy, provider: CostProvider,
@@ -499,8 +504,6 @@ def run_simulation(cfg: ScenarioConfig, policy: BalancePolicy, provider: CostPro
     sim = Simulation(cfg, policy, provider, **kw)
     try:
         sim.run()
-        res = sim.result()
-        res.final_state.n = res.summary["final_particles"]
-        return res
+        return sim.result()
     finally:
         sim.close()
