@@ -231,6 +231,18 @@ typedef struct lbx_sim_outputs {
   int64_t completed_steps;     /* out                                        */
 } lbx_sim_outputs;
 
+/* Host half of the loop alone (no device needed): provider cost, efficiency,
+ * attempt/adopt, walltime-model columns for one step, given the step's GLOBAL
+ * per-box survivor counts (and GpuClock tally).  The multi-GPU driver calls
+ * it on every rank after all-reducing the tallies, so every rank takes the
+ * same decision with no broadcast.  `out` arrays as for lbx_sim_run. */
+typedef struct lbx_lb lbx_lb;
+int lbx_lb_create(lbx_lb** out, const lbx_sim_config* cfg, const int64_t* initial_owner);
+int lbx_lb_destroy(lbx_lb* lb);
+int lbx_lb_step(lbx_lb* lb, int64_t step, const int64_t* counts, const uint64_t* clk,
+                int64_t n_alive, lbx_sim_outputs* out, int32_t* adopted, int32_t* halt);
+int lbx_lb_owner(lbx_lb* lb, int64_t* owner);
+
 int lbx_sim_create(lbx_sim** out, lbx_ctx* ctx, const lbx_sim_config* cfg);
 int lbx_sim_destroy(lbx_sim* sim);
 /* Particle buffers (device SoA, capacity >= n + 2); kick_vz/kick_vx replace
@@ -243,6 +255,50 @@ int lbx_sim_run(lbx_sim* sim, int64_t first, int64_t last,
                 lbx_sim_outputs* out, void* stream);
 /* Current device live count (syncs the stream). */
 int lbx_sim_particles(lbx_sim* sim, int64_t* n, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Multi-GPU: box ownership -> GPU.  Each rank holds the particles
+ * of the boxes it owns.  A particle whose new box belongs to another rank is
+ * copied into the staging buffer as a 6-double record (z, x, vz, vx, kick_vz,
+ * kick_vx) tagged with its destination and removed locally (in-place
+ * compaction).  Every rank still bins ALL particles it pushed into the full
+ * per-box vector, so an all-reduce(sum) of counts / clock tallies is exact.
+ * Replaces the analytic comm/redistribution model of workload.py:324-337
+ * with real traffic.
+ * ---------------------------------------------------------------------- */
+#define LBX_RECORD_DOUBLES 6
+
+typedef struct lbx_exchange_args {
+  const int32_t* owner;     /* device [nbz*nbx]: owning rank of each box       */
+  int32_t rank, world;      /* this rank, number of ranks (<= 64)              */
+  double* stage;            /* device [stage_cap][6] emigrant records          */
+  int32_t* stage_dest;      /* device [stage_cap] destination rank             */
+  int64_t stage_cap;
+  int64_t* send_counts;     /* device [world] emigrants per destination; the
+                               caller zeroes it before the call              */
+  double* kick_vz;          /* pending kick velocities travelling with the
+                               particles (NULL once the kick has happened)   */
+  double* kick_vx;
+} lbx_exchange_args;
+
+/* lbx_push_step + emigrant staging (per-step box-crossing exchange). */
+int lbx_push_step_exchange(lbx_ctx* ctx, const lbx_step_args* args,
+                           const lbx_exchange_args* ex, void* stream);
+/* Adoption-time migration: stage every local particle whose box is owned
+ * elsewhere under ex->owner (no push), compact the rest; *n_out (device) gets
+ * the local count left. */
+int lbx_partition(lbx_ctx* ctx, double* z, double* x, double* vz, double* vx,
+                  double extent_z, double extent_x, double box_size, int32_t nbz,
+                  int32_t nbx, const lbx_exchange_args* ex, int64_t* n_out,
+                  void* stream);
+/* Group `count` staged records by destination into `send` ([count][6]);
+ * cursors[world] (device) holds each destination's first slot on entry. */
+int lbx_group_by_dest(const double* stage, const int32_t* stage_dest, int64_t count,
+                      int32_t world, int64_t* cursors, double* send, void* stream);
+/* Append n_recv received records at index `offset` of the SoA arrays
+ * (kick_vz/kick_vx may be NULL). */
+int lbx_unpack(const double* recv, int64_t n_recv, int64_t offset, double* z, double* x,
+               double* vz, double* vx, double* kick_vz, double* kick_vx, void* stream);
 
 #ifdef __cplusplus
 }

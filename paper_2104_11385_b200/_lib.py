@@ -89,6 +89,27 @@ SIGNATURES = {
 }
 
 
+class ExchangeArgs(C.Structure):
+    """lbx_exchange_args (include/lbx.h)."""
+    _fields_ = [("owner", vp), ("rank", i32), ("world", i32), ("stage", vp),
+                ("stage_dest", vp), ("stage_cap", i64), ("send_counts", vp),
+                ("kick_vz", vp), ("kick_vx", vp)]
+
+
+SIGNATURES.update({
+    "lbx_lb_create": (i32, [P(vp), P(SimConfig), vp]),
+    "lbx_lb_destroy": (i32, [vp]),
+    "lbx_lb_step": (i32, [vp, i64, vp, vp, i64, P(SimOutputs), P(i32), P(i32)]),
+    "lbx_lb_owner": (i32, [vp, vp]),
+    "lbx_push_step_exchange": (i32, [vp, P(StepArgs), P(ExchangeArgs), vp]),
+    "lbx_partition": (i32, [vp, vp, vp, vp, vp, f64, f64, f64, i32, i32, P(ExchangeArgs),
+                            vp, vp]),
+    "lbx_group_by_dest": (i32, [vp, vp, i64, i32, vp, vp, vp]),
+    "lbx_unpack": (i32, [vp, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
+})
+RECORD_DOUBLES = 6
+
+
 class LBXError(RuntimeError):
     pass
 

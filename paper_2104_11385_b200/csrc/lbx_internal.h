@@ -24,6 +24,7 @@ struct DevState {
   unsigned long long leavers; // absorbed this step (push -> compaction handoff)
   long long first_leaver;     // lowest index absorbed this step (LLONG_MAX: none)
   long long n_old;            // count before this step's push (compaction input)
+  unsigned long long staged;  // emigrant records staged this call
 };
 
 // Host-side model of the particle state's pushed-and-binned step.
@@ -67,6 +68,7 @@ int sfc(const double* cost, const int64_t* curve, int64_t n, int32_t R, int64_t*
 int measured_cost(const double* work, int64_t n, double amplitude, uint64_t seed, uint64_t step,
                   double* out);
 // Implemented in lbx_kernels.cu.
-int launch_push_step(lbx_ctx* ctx, const StepLaunch& a, void* stream);
+int launch_push_step(lbx_ctx* ctx, const StepLaunch& a, void* stream,
+                     const lbx_exchange_args* ex = nullptr, bool push = true);
 int ensure_accumulators(lbx_ctx* ctx, int32_t nboxes);
 }  // namespace lbx

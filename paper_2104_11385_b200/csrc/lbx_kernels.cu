@@ -80,6 +80,15 @@ struct StepParams {
   long long* n_out;
   long long* err_out;
   double wp, wc, cells;
+  // exchange (multi-GPU)
+  const int* owner;
+  int me;
+  double* stage;
+  int* stage_dest;
+  long long stage_cap;
+  long long* send_counts;
+  const double* kvz;
+  const double* kvx;
 };
 
 struct ScanParams {
@@ -93,6 +102,8 @@ struct ScanParams {
   const double2* in_vel;
   double2* out_pos;
   double2* out_vel;
+  double* kvz;       // COMPACT_SOA: pending kick velocities (may be NULL)
+  double* kvx;
   double ez, ex;
   long long n_host;  // ADVANCE_AOS: particle count
   DevState* st;
@@ -139,7 +150,7 @@ __device__ __forceinline__ bool inside(double z, double x, double ez, double ex)
 }
 
 // ---------------------------------------------------------------------------
-// push_bin_kernel
+// stream_kernel: push_bin (kPush) and partition (!kPush), optional exchange
 // ---------------------------------------------------------------------------
 
 template <bool kClock>
@@ -172,11 +183,40 @@ __device__ __forceinline__ void hist_flush(const StepParams& p, unsigned* s_cnt,
   }
 }
 
-template <bool kClock, bool kPow2>
-__global__ void __launch_bounds__(kBlock, 4) push_bin_kernel(StepParams p) {
+// Stage one emigrant record (warp-aggregated slot reservation).
+__device__ __forceinline__ void stage_emigrant(const StepParams& p, bool em, long long i,
+                                               double z, double x, double vz, double vx,
+                                               int dest) {
+  const unsigned mask = __ballot_sync(kFull, em);
+  if (!mask) return;
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == __ffs(mask) - 1) base = atomicAdd(&p.st->staged, (unsigned long long)__popc(mask));
+  base = __shfl_sync(kFull, base, __ffs(mask) - 1);
+  if (!em) return;
+  const long long slot = (long long)base + __popc(mask & lanemask_lt());
+  if (slot >= p.stage_cap) {
+    atomicOr((unsigned long long*)&p.st->err, 1ull << 62);  // staging overflow
+    return;
+  }
+  double* r = p.stage + slot * 6;
+  r[0] = z;
+  r[1] = x;
+  r[2] = vz;
+  r[3] = vx;
+  r[4] = p.kvz ? p.kvz[i] : 0.0;
+  r[5] = p.kvx ? p.kvx[i] : 0.0;
+  p.stage_dest[slot] = dest;
+  atomicAdd((unsigned long long*)(p.send_counts + dest), 1ull);
+}
+
+template <bool kClock, bool kPow2, bool kExch, bool kPush>
+__global__ void __launch_bounds__(kBlock, 4) stream_kernel(StepParams p) {
+  constexpr bool kHist = kPush;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned* s_cnt = reinterpret_cast<unsigned*>(smem_raw);
   unsigned* s_clk = s_cnt + p.nb;
+  int* s_owner = reinterpret_cast<int*>(s_cnt + (kClock ? 2 : 1) * p.nb);
   __shared__ long long s_n;
   __shared__ int s_last;
   __shared__ unsigned long long s_red[kWarps];
@@ -188,11 +228,13 @@ __global__ void __launch_bounds__(kBlock, 4) push_bin_kernel(StepParams p) {
   if (tid == 0) s_n = *((volatile long long*)&p.st->n);
   if (p.smem_hist) {
     for (int b = tid; b < p.nb; b += kBlock) {
-      s_cnt[b] = 0u;
+      if (kHist) s_cnt[b] = 0u;
       if (kClock) s_clk[b] = 0u;
+      if (kExch) s_owner[b] = p.owner[b];
     }
   }
   __syncthreads();
+  const int* owner = p.smem_hist ? s_owner : p.owner;
   const long long n = s_n;
   const long long npairs = (n + 1) >> 1;
   const long long stride = (long long)gridDim.x * kBlock * kPairs;
@@ -201,7 +243,7 @@ __global__ void __launch_bounds__(kBlock, 4) push_bin_kernel(StepParams p) {
   const double2* vz2 = reinterpret_cast<const double2*>(p.vz);
   const double2* vx2 = reinterpret_cast<const double2*>(p.vx);
 
-  unsigned long long absorbed = 0;
+  unsigned long long removed = 0;
   long long first_out = LLONG_MAX;
   long long err = 0;
   int iter = 0;
@@ -210,8 +252,8 @@ __global__ void __launch_bounds__(kBlock, 4) push_bin_kernel(StepParams p) {
   for (long long q0 = (long long)blockIdx.x * kBlock * kPairs; q0 < npairs; q0 += stride) {
     long long t0 = 0;
     if (kClock) t0 = clock64();
-    double pz[2 * kPairs], px[2 * kPairs];
-    bool keep[2 * kPairs];
+    double pz[2 * kPairs], px[2 * kPairs], pvz[2 * kPairs], pvx[2 * kPairs];
+    bool keep[2 * kPairs], valid[2 * kPairs];
 #pragma unroll
     for (int r = 0; r < kPairs; ++r) {
       const long long q = q0 + r * kBlock + tid;
@@ -220,33 +262,38 @@ __global__ void __launch_bounds__(kBlock, 4) push_bin_kernel(StepParams p) {
       if (any) {
         a = __ldcs(z2 + q);
         b = __ldcs(x2 + q);
-        c = __ldcs(vz2 + q);
-        d = __ldcs(vx2 + q);
-      }
-      pz[2 * r] = __dadd_rn(a.x, c.x);
-      pz[2 * r + 1] = __dadd_rn(a.y, c.y);
-      px[2 * r] = __dadd_rn(b.x, d.x);
-      px[2 * r + 1] = __dadd_rn(b.y, d.y);
-      const long long i0 = 2 * q;
-      keep[2 * r] = any && inside(pz[2 * r], px[2 * r], p.ez, p.ex);
-      keep[2 * r + 1] = i0 + 1 < n && inside(pz[2 * r + 1], px[2 * r + 1], p.ez, p.ex);
-      if (any) {
-        __stcs(z2 + q, make_double2(pz[2 * r], pz[2 * r + 1]));
-        __stcs(x2 + q, make_double2(px[2 * r], px[2 * r + 1]));
-        if (!keep[2 * r]) {
-          ++absorbed;
-          first_out = min(first_out, i0);
-        }
-        if (i0 + 1 < n && !keep[2 * r + 1]) {
-          ++absorbed;
-          first_out = min(first_out, i0 + 1);
+        if (kPush || kExch) {
+          c = __ldcs(vz2 + q);
+          d = __ldcs(vx2 + q);
         }
       }
+      pvz[2 * r] = c.x;
+      pvz[2 * r + 1] = c.y;
+      pvx[2 * r] = d.x;
+      pvx[2 * r + 1] = d.y;
+      if (kPush) {
+        pz[2 * r] = __dadd_rn(a.x, c.x);
+        pz[2 * r + 1] = __dadd_rn(a.y, c.y);
+        px[2 * r] = __dadd_rn(b.x, d.x);
+        px[2 * r + 1] = __dadd_rn(b.y, d.y);
+      } else {
+        pz[2 * r] = a.x;
+        pz[2 * r + 1] = a.y;
+        px[2 * r] = b.x;
+        px[2 * r + 1] = b.y;
+      }
+      valid[2 * r] = any;
+      valid[2 * r + 1] = 2 * q + 1 < n;
     }
+#pragma unroll
+    for (int k = 0; k < 2 * kPairs; ++k) keep[k] = valid[k] && inside(pz[k], px[k], p.ez, p.ex);
+
     int box[2 * kPairs];
+    bool emig[2 * kPairs];
 #pragma unroll
     for (int k = 0; k < 2 * kPairs; ++k) {
       box[k] = -1;
+      emig[k] = false;
       if (keep[k]) {
         int bz, bx;
         if (kPow2) {
@@ -258,45 +305,80 @@ __global__ void __launch_bounds__(kBlock, 4) push_bin_kernel(StepParams p) {
         }
         if (bz < p.nbz && bx < p.nbx) {
           box[k] = bz * p.nbx + bx;
+          if (kExch) emig[k] = owner[box[k]] != p.me;
         } else {
           ++err;
         }
       }
     }
-    unsigned dt = 0;
-    if (kClock) {
-      const long long t1 = clock64();
-      dt = (unsigned)min(t1 - t0, (long long)(1 << 20)) >> kClockShift;
-    }
-    int cur = -1;
-    unsigned run = 0;
+    // stores: pushed positions in place, removal sentinel (z = -1) for
+    // emigrants so the compaction drops them like absorbed particles
 #pragma unroll
-    for (int k = 0; k < 2 * kPairs; ++k) {
-      if (box[k] != cur) {
-        if (cur >= 0) hist_add<kClock>(p, s_cnt, s_clk, cur, run, dt * run);
-        cur = box[k];
-        run = 0;
+    for (int r = 0; r < kPairs; ++r) {
+      const long long q = q0 + r * kBlock + tid;
+      if (!valid[2 * r]) continue;
+      const double z0 = emig[2 * r] ? -1.0 : pz[2 * r];
+      const double z1 = emig[2 * r + 1] ? -1.0 : pz[2 * r + 1];
+      if (kPush) {
+        __stcs(z2 + q, make_double2(z0, z1));
+        __stcs(x2 + q, make_double2(px[2 * r], px[2 * r + 1]));
+      } else if (emig[2 * r] || emig[2 * r + 1]) {
+        __stcs(z2 + q, make_double2(z0, z1));
       }
-      run += (box[k] >= 0) ? 1u : 0u;
+      const long long i0 = 2 * q;
+      if (!keep[2 * r] || emig[2 * r]) {
+        ++removed;
+        first_out = min(first_out, i0);
+      }
+      if (valid[2 * r + 1] && (!keep[2 * r + 1] || emig[2 * r + 1])) {
+        ++removed;
+        first_out = min(first_out, i0 + 1);
+      }
     }
-    const int cur0 = __shfl_sync(kFull, cur, 0);
-    if (__all_sync(kFull, cur == cur0)) {
-      const unsigned tot = __reduce_add_sync(kFull, run);
-      const unsigned clk = kClock ? __reduce_add_sync(kFull, dt * run) : 0u;
-      if (lane == 0 && cur0 >= 0 && tot) hist_add<kClock>(p, s_cnt, s_clk, cur0, tot, clk);
-    } else if (cur >= 0 && run) {
-      hist_add<kClock>(p, s_cnt, s_clk, cur, run, dt * run);
+    if (kExch) {
+#pragma unroll
+      for (int k = 0; k < 2 * kPairs; ++k) {
+        const long long i = 2 * (q0 + (k >> 1) * kBlock + tid) + (k & 1);
+        stage_emigrant(p, emig[k], i, pz[k], px[k], pvz[k], pvx[k],
+                       emig[k] ? owner[box[k]] : 0);
+      }
     }
-    if (p.smem_hist && ++iter == kFlushIters) {  // keep 32-bit accumulators bounded
-      iter = 0;
-      __syncthreads();
-      hist_flush<kClock>(p, s_cnt, s_clk);
-      __syncthreads();
+    if (kHist) {
+      unsigned dt = 0;
+      if (kClock) {
+        const long long t1 = clock64();
+        dt = (unsigned)min(t1 - t0, (long long)(1 << 20)) >> kClockShift;
+      }
+      int cur = -1;
+      unsigned run = 0;
+#pragma unroll
+      for (int k = 0; k < 2 * kPairs; ++k) {
+        if (box[k] != cur) {
+          if (cur >= 0) hist_add<kClock>(p, s_cnt, s_clk, cur, run, dt * run);
+          cur = box[k];
+          run = 0;
+        }
+        run += (box[k] >= 0) ? 1u : 0u;
+      }
+      const int cur0 = __shfl_sync(kFull, cur, 0);
+      if (__all_sync(kFull, cur == cur0)) {
+        const unsigned tot = __reduce_add_sync(kFull, run);
+        const unsigned clk = kClock ? __reduce_add_sync(kFull, dt * run) : 0u;
+        if (lane == 0 && cur0 >= 0 && tot) hist_add<kClock>(p, s_cnt, s_clk, cur0, tot, clk);
+      } else if (cur >= 0 && run) {
+        hist_add<kClock>(p, s_cnt, s_clk, cur, run, dt * run);
+      }
+      if (p.smem_hist && ++iter == kFlushIters) {  // keep 32-bit accumulators bounded
+        iter = 0;
+        __syncthreads();
+        hist_flush<kClock>(p, s_cnt, s_clk);
+        __syncthreads();
+      }
     }
   }
 
-  // ---- CTA totals: absorbed count, first absorbed index, errors ----
-  unsigned long long wa = (unsigned long long)warp_sum_ll((long long)absorbed);
+  // ---- CTA totals: removed count, first removed index, errors ----
+  unsigned long long wa = (unsigned long long)warp_sum_ll((long long)removed);
   long long wm = warp_min_ll(first_out);
   long long we = warp_sum_ll(err);
   if (lane == 0) {
@@ -317,7 +399,7 @@ __global__ void __launch_bounds__(kBlock, 4) push_bin_kernel(StepParams p) {
       atomicMin(&p.st->first_leaver, tm);
     }
   }
-  if (p.smem_hist) hist_flush<kClock>(p, s_cnt, s_clk);
+  if (kHist && p.smem_hist) hist_flush<kClock>(p, s_cnt, s_clk);
   __threadfence();
   __syncthreads();
   if (tid == 0) s_last = (atomicAdd(&p.st->done, 1u) == gridDim.x - 1) ? 1 : 0;
@@ -326,16 +408,18 @@ __global__ void __launch_bounds__(kBlock, 4) push_bin_kernel(StepParams p) {
 
   // ---- last CTA: step epilogue ----
   __threadfence();
-  for (int b = tid; b < p.nb; b += kBlock) {
-    const unsigned long long c = atomicExch(p.g_cnt + b, 0ull);
-    if (p.counts_out) p.counts_out[b] = (long long)c;
-    if (p.cost_out) {
-      p.cost_out[b] =
-          __dadd_rn(__dmul_rn(p.wp, (double)(long long)c), __dmul_rn(p.wc, p.cells));
-    }
-    if (kClock) {
-      const unsigned long long k = atomicExch(p.g_clk + b, 0ull);
-      if (p.clk_out) p.clk_out[b] = k << kClockShift;
+  if (kHist) {
+    for (int b = tid; b < p.nb; b += kBlock) {
+      const unsigned long long c = atomicExch(p.g_cnt + b, 0ull);
+      if (p.counts_out) p.counts_out[b] = (long long)c;
+      if (p.cost_out) {
+        p.cost_out[b] =
+            __dadd_rn(__dmul_rn(p.wp, (double)(long long)c), __dmul_rn(p.wc, p.cells));
+      }
+      if (kClock) {
+        const unsigned long long k = atomicExch(p.g_clk + b, 0ull);
+        if (p.clk_out) p.clk_out[b] = k << kClockShift;
+      }
     }
   }
   if (tid == 0) {
@@ -346,6 +430,7 @@ __global__ void __launch_bounds__(kBlock, 4) push_bin_kernel(StepParams p) {
     p.st->n_old = n;
     p.st->n = n_new;
     p.st->done = 0u;
+    p.st->staged = 0ull;
     __threadfence_system();
   }
 }
@@ -385,7 +470,7 @@ __device__ long long lookback(unsigned long long* status, long long tile, long l
 }
 
 template <int kMode>
-__global__ void __launch_bounds__(kBlock, 3) scan_kernel(ScanParams p) {
+__global__ void __launch_bounds__(kBlock, kMode == kCompactSoA ? 2 : 3) scan_kernel(ScanParams p) {
   __shared__ long long s_tile;
   __shared__ long long s_prefix;
   __shared__ int s_total;
@@ -427,6 +512,7 @@ __global__ void __launch_bounds__(kBlock, 3) scan_kernel(ScanParams p) {
     const long long valid = min((long long)kTile, n - base);
 
     double pz[kItems], px[kItems], pvz[kItems], pvx[kItems];
+    double pkz[kMode == kCompactSoA ? kItems : 1], pkx[kMode == kCompactSoA ? kItems : 1];
     bool keep[kItems];
     if (kMode == kCompactSoA) {
       const double2* z2 = reinterpret_cast<const double2*>(p.z);
@@ -452,6 +538,17 @@ __global__ void __launch_bounds__(kBlock, 3) scan_kernel(ScanParams p) {
         pvz[2 * r + 1] = c.y;
         pvx[2 * r] = d.x;
         pvx[2 * r + 1] = d.y;
+        if (p.kvz) {
+          double2 e = make_double2(0.0, 0.0), f = e;
+          if (i0 < n) {
+            e = __ldcs(reinterpret_cast<const double2*>(p.kvz) + q);
+            f = __ldcs(reinterpret_cast<const double2*>(p.kvx) + q);
+          }
+          pkz[2 * r] = e.x;
+          pkz[2 * r + 1] = e.y;
+          pkx[2 * r] = f.x;
+          pkx[2 * r + 1] = f.y;
+        }
         keep[2 * r] = i0 < n && inside(a.x, b.x, p.ez, p.ex);
         keep[2 * r + 1] = i0 + 1 < n && inside(a.y, b.y, p.ez, p.ex);
       }
@@ -553,6 +650,10 @@ __global__ void __launch_bounds__(kBlock, 3) scan_kernel(ScanParams p) {
             p.x[d] = px[k];
             p.vz[d] = pvz[k];
             p.vx[d] = pvx[k];
+            if (p.kvz) {
+              p.kvz[d] = pkz[k];
+              p.kvx[d] = pkx[k];
+            }
           }
         }
       }
@@ -659,6 +760,35 @@ __global__ void init_state_kernel(DevState* st, long long n) {
   st->n_old = n;
   st->leavers = 0ull;
   st->first_leaver = LLONG_MAX;
+  st->staged = 0ull;
+}
+
+__global__ void group_kernel(const double* __restrict__ stage, const int* __restrict__ dest,
+                             long long count, unsigned long long* cursors,
+                             double* __restrict__ send) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const long long slot = (long long)atomicAdd(cursors + dest[i], 1ull);
+#pragma unroll
+    for (int j = 0; j < 6; ++j) send[slot * 6 + j] = stage[i * 6 + j];
+  }
+}
+
+__global__ void unpack_kernel(const double* __restrict__ recv, long long n_recv, long long off,
+                              double* z, double* x, double* vz, double* vx, double* kvz,
+                              double* kvx) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_recv; i += stride) {
+    const double* r = recv + i * 6;
+    z[off + i] = r[0];
+    x[off + i] = r[1];
+    vz[off + i] = r[2];
+    vx[off + i] = r[3];
+    if (kvz) {
+      kvz[off + i] = r[4];
+      kvx[off + i] = r[5];
+    }
+  }
 }
 
 inline int cuda_fail(cudaError_t e, const char* what) {
@@ -676,10 +806,10 @@ int occupancy_grid(lbx_ctx* ctx, K kern, size_t smem, long long work_ctas, int* 
   return LBX_OK;
 }
 
-template <bool kClock, bool kPow2>
-int launch_push_bin(lbx_ctx* ctx, const StepParams& p, cudaStream_t s) {
-  auto kern = push_bin_kernel<kClock, kPow2>;
-  const size_t smem = p.smem_hist ? (size_t)p.nb * 4 * (kClock ? 2 : 1) : 0;
+template <bool kClock, bool kPow2, bool kExch, bool kPush>
+int launch_stream(lbx_ctx* ctx, const StepParams& p, cudaStream_t s) {
+  auto kern = stream_kernel<kClock, kPow2, kExch, kPush>;
+  const size_t smem = p.smem_hist ? (size_t)p.nb * 4 * (1 + (kClock ? 1 : 0) + (kExch ? 1 : 0)) : 0;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     cudaError_t e =
@@ -693,8 +823,18 @@ int launch_push_bin(lbx_ctx* ctx, const StepParams& p, cudaStream_t s) {
   if (rc) return rc;
   kern<<<grid, kBlock, smem, s>>>(p);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "push_bin_kernel launch");
+  if (e != cudaSuccess) return cuda_fail(e, "stream_kernel launch");
   return LBX_OK;
+}
+
+template <bool kExch, bool kPush>
+int launch_stream_any(lbx_ctx* ctx, const StepParams& p, bool clock, bool pow2, cudaStream_t s) {
+  if (clock) {
+    return pow2 ? launch_stream<true, true, kExch, kPush>(ctx, p, s)
+                : launch_stream<true, false, kExch, kPush>(ctx, p, s);
+  }
+  return pow2 ? launch_stream<false, true, kExch, kPush>(ctx, p, s)
+              : launch_stream<false, false, kExch, kPush>(ctx, p, s);
 }
 
 template <int kMode>
@@ -755,7 +895,8 @@ int ensure_accumulators(lbx_ctx* ctx, int32_t nboxes) {
   return LBX_OK;
 }
 
-int launch_push_step(lbx_ctx* ctx, const StepLaunch& a, void* stream) {
+int launch_push_step(lbx_ctx* ctx, const StepLaunch& a, void* stream,
+                     const lbx_exchange_args* ex, bool push) {
   if (a.nbz < 1 || a.nbx < 1) return set_error(LBX_EINVAL, "box grid must be at least 1x1");
   if (!(a.m > 0.0)) return set_error(LBX_EINVAL, "box_size must be positive");
   const long long nb = (long long)a.nbz * a.nbx;
@@ -792,19 +933,29 @@ int launch_push_step(lbx_ctx* ctx, const StepLaunch& a, void* stream) {
   p.cells = a.cells;
   cudaStream_t s = (cudaStream_t)stream;
   const bool pow2 = is_pow2(a.m);
-  if (a.clock) {
-    rc = pow2 ? launch_push_bin<true, true>(ctx, p, s) : launch_push_bin<true, false>(ctx, p, s);
+  if (ex) {
+    p.owner = ex->owner;
+    p.me = ex->rank;
+    p.stage = ex->stage;
+    p.stage_dest = ex->stage_dest;
+    p.stage_cap = ex->stage_cap;
+    p.send_counts = reinterpret_cast<long long*>(ex->send_counts);
+    p.kvz = ex->kick_vz;
+    p.kvx = ex->kick_vx;
+    rc = push ? launch_stream_any<true, true>(ctx, p, a.clock, pow2, s)
+              : launch_stream_any<true, false>(ctx, p, false, pow2, s);
   } else {
-    rc = pow2 ? launch_push_bin<false, true>(ctx, p, s)
-              : launch_push_bin<false, false>(ctx, p, s);
+    rc = launch_stream_any<false, true>(ctx, p, a.clock, pow2, s);
   }
   if (rc) return rc;
-  // Stable compaction of the survivors; returns at once when none was absorbed.
+  // Stable compaction of the survivors; returns at once when none was removed.
   ScanParams c{};
   c.z = a.z;
   c.x = a.x;
   c.vz = const_cast<double*>(a.vz);
   c.vx = const_cast<double*>(a.vx);
+  c.kvz = ex ? ex->kick_vz : nullptr;
+  c.kvx = ex ? ex->kick_vx : nullptr;
   c.ez = a.ez;
   c.ex = a.ex;
   c.st = ctx->st;
@@ -990,7 +1141,7 @@ int lbx_push_step(lbx_ctx* ctx, const lbx_step_args* a, void* stream) {
   l.clk_out = reinterpret_cast<unsigned long long*>(a->clk_out);
   l.n_out = reinterpret_cast<long long*>(a->n_out);
   l.err_out = reinterpret_cast<long long*>(a->err_out);
-  return launch_push_step(ctx, l, stream);
+  return launch_push_step(ctx, l, stream, nullptr, true);
 }
 
 int lbx_heuristic_cost(const double* particles, const double* cells, int64_t n,
@@ -1002,6 +1153,85 @@ int lbx_heuristic_cost(const double* particles, const double* cells, int64_t n,
       particles, cells, n, w_particle, w_cell, cost);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "heuristic launch");
+  return LBX_OK;
+}
+
+int lbx_push_step_exchange(lbx_ctx* ctx, const lbx_step_args* a, const lbx_exchange_args* ex,
+                           void* stream) {
+  clear_error();
+  if (!ctx || !a || !ex) return set_error(LBX_EINVAL, "NULL argument");
+  if (ex->world < 1 || ex->world > 64 || ex->rank < 0 || ex->rank >= ex->world)
+    return set_error(LBX_EINVAL, "rank %d / world %d out of range", ex->rank, ex->world);
+  if (!ex->owner || !ex->stage || !ex->stage_dest || !ex->send_counts)
+    return set_error(LBX_EINVAL, "NULL exchange buffer");
+  StepLaunch l{};
+  l.z = a->z;
+  l.x = a->x;
+  l.vz = a->vz;
+  l.vx = a->vx;
+  l.ez = a->extent_z;
+  l.ex = a->extent_x;
+  l.m = a->box_size;
+  l.nbz = a->nbz;
+  l.nbx = a->nbx;
+  l.wp = a->w_particle;
+  l.wc = a->w_cell;
+  l.cells = a->cells_per_box;
+  l.clock = (a->flags & LBX_STEP_CLOCK) != 0;
+  l.counts_out = reinterpret_cast<long long*>(a->counts_out);
+  l.cost_out = a->cost_out;
+  l.clk_out = reinterpret_cast<unsigned long long*>(a->clk_out);
+  l.n_out = reinterpret_cast<long long*>(a->n_out);
+  l.err_out = reinterpret_cast<long long*>(a->err_out);
+  return launch_push_step(ctx, l, stream, ex, true);
+}
+
+int lbx_partition(lbx_ctx* ctx, double* z, double* x, double* vz, double* vx, double extent_z,
+                  double extent_x, double box_size, int32_t nbz, int32_t nbx,
+                  const lbx_exchange_args* ex, int64_t* n_out, void* stream) {
+  clear_error();
+  if (!ctx || !ex) return set_error(LBX_EINVAL, "NULL argument");
+  if (ex->world < 1 || ex->world > 64 || ex->rank < 0 || ex->rank >= ex->world)
+    return set_error(LBX_EINVAL, "rank %d / world %d out of range", ex->rank, ex->world);
+  StepLaunch l{};
+  l.z = z;
+  l.x = x;
+  l.vz = vz;
+  l.vx = vx;
+  l.ez = extent_z;
+  l.ex = extent_x;
+  l.m = box_size;
+  l.nbz = nbz;
+  l.nbx = nbx;
+  l.n_out = reinterpret_cast<long long*>(n_out);
+  return launch_push_step(ctx, l, stream, ex, false);
+}
+
+int lbx_group_by_dest(const double* stage, const int32_t* stage_dest, int64_t count,
+                      int32_t world, int64_t* cursors, double* send, void* stream) {
+  clear_error();
+  if (count < 0 || world < 1) return set_error(LBX_EINVAL, "bad count/world");
+  if (count == 0) return LBX_OK;
+  const unsigned grid = (unsigned)std::min<long long>(4096, (count + 255) / 256);
+  group_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      stage, stage_dest, count, reinterpret_cast<unsigned long long*>(cursors), send);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "group_kernel launch");
+  return LBX_OK;
+}
+
+int lbx_unpack(const double* recv, int64_t n_recv, int64_t offset, double* z, double* x,
+               double* vz, double* vx, double* kick_vz, double* kick_vx, void* stream) {
+  clear_error();
+  if (n_recv < 0 || offset < 0) return set_error(LBX_EINVAL, "bad count/offset");
+  if ((kick_vz == nullptr) != (kick_vx == nullptr))
+    return set_error(LBX_EINVAL, "kick velocity buffers must be given together");
+  if (n_recv == 0) return LBX_OK;
+  const unsigned grid = (unsigned)std::min<long long>(4096, (n_recv + 255) / 256);
+  unpack_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(recv, n_recv, offset, z, x, vz, vx,
+                                                         kick_vz, kick_vx);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "unpack_kernel launch");
   return LBX_OK;
 }
 

@@ -1,19 +1,20 @@
 // libLBX native stepping runtime: the per-step loop of workload.py:388-470
 // (run_simulation) without Python in it.
 //
-// Per step s:
-//   device  fused push/absorb/compact/bin/heuristic/clock kernel (one launch);
-//           its last CTA writes the step record (counts, heuristic cost,
-//           clock tally, survivor count) straight into a mapped pinned ring
-//           slot, so no memcpy is enqueued;
-//   host    once slot s is complete: provider cost (workload.py:414), trace,
-//           efficiency, should_attempt/attempt_rebalance (balancer.py:258-304),
-//           adoption, and the walltime-model columns of step_walltime
-//           (workload.py:314-363), all bit-exact with the reference.
-// The host runs up to `ring` steps behind the device: on one GPU the mapping
-// never feeds back into particle data, so nothing but the ring depth limits
-// the overlap.  Runs with a particle capacity (OOM can stop the run) use a
-// depth of 1 so the device never advances past the halting step.
+// Two layers:
+//   lbx_lb   host half of a step, given the step's global per-box counts
+//            (and GpuClock tally / device heuristic cost): provider cost
+//            (workload.py:414), efficiency, should_attempt/attempt_rebalance
+//            (balancer.py:258-304), adoption, and the walltime-model columns
+//            of step_walltime (workload.py:314-363) -- all bit-exact with the
+//            reference.  Used by lbx_sim below and by the multi-GPU driver
+//            (parallel.py) after the per-box tallies are all-reduced.
+//   lbx_sim  single-GPU loop: one fused kernel launch per step whose last CTA
+//            writes the step record straight into a mapped pinned ring slot
+//            (no memcpy enqueued); the host consumes records up to `ring`
+//            steps behind the device (on one GPU the mapping never feeds
+//            back into particle data).  Capacity runs (OOM can halt the run)
+//            use a depth of 1 so the device never passes the halting step.
 
 #include <cuda_runtime.h>
 
@@ -26,23 +27,26 @@
 
 using namespace lbx;
 
-struct lbx_sim {
-  lbx_ctx* ctx = nullptr;
+struct lbx_lb {
   lbx_sim_config cfg{};
   int32_t nbz = 0, nbx = 0, nb = 0;
   std::vector<int64_t> curve, face_a, face_b;
+  std::vector<int64_t> owner, prop, prev;
+  std::vector<double> work, scratch, rank_acc;
+  std::vector<int64_t> faces_per_rank;
+};
+
+struct lbx_sim {
+  lbx_ctx* ctx = nullptr;
+  lbx_lb* lb = nullptr;
   double *z = nullptr, *x = nullptr, *vz = nullptr, *vx = nullptr;
   double *kvz = nullptr, *kvx = nullptr;
-  // mapped pinned ring of step records
   int ring = 0;
   size_t rec_bytes = 0;
   unsigned char* ring_h = nullptr;
   unsigned char* ring_d = nullptr;
   std::vector<cudaEvent_t> ev, t0, t1;  // completion / kernel timing events
   bool timing = false;
-  std::vector<int64_t> owner, prop, prev;
-  std::vector<double> work, cost, scratch, rank_acc;
-  std::vector<int64_t> faces_per_rank;
 };
 
 namespace {
@@ -75,83 +79,61 @@ int cuda_fail(cudaError_t e, const char* what) {
   return set_error(LBX_ECUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
-int launch_step(lbx_sim* s, int64_t step, cudaStream_t st) {
-  const int tslot = (int)(step % s->ring);
-  if (s->timing) cudaEventRecord(s->t0[tslot], st);
-  const int slot = (int)(step % s->ring);
-  Rec d = rec_at(s->ring_d, s->rec_bytes, slot, s->nb);
-  const bool kicked = step >= s->cfg.kick_step && s->kvz != nullptr;
-  StepLaunch a{};
-  a.z = s->z;
-  a.x = s->x;
-  a.vz = kicked ? s->kvz : s->vz;
-  a.vx = kicked ? s->kvx : s->vx;
-  a.ez = (double)s->cfg.extent_z;
-  a.ex = (double)s->cfg.extent_x;
-  a.m = (double)s->cfg.box_size;
-  a.nbz = s->nbz;
-  a.nbx = s->nbx;
-  a.wp = s->cfg.w_particle;
-  a.wc = s->cfg.w_cell;
-  a.cells = (double)s->cfg.box_size * (double)s->cfg.box_size;
-  a.clock = s->cfg.cost_kind == LBX_COST_GPUCLOCK;
-  a.counts_out = reinterpret_cast<long long*>(d.counts);
-  a.cost_out = d.cost;
-  a.clk_out = a.clock ? reinterpret_cast<unsigned long long*>(d.clk) : nullptr;
-  a.n_out = reinterpret_cast<long long*>(d.n);
-  a.err_out = reinterpret_cast<long long*>(d.err);
-  int rc = launch_push_step(s->ctx, a, st);
-  if (rc) return rc;
-  if (s->timing) cudaEventRecord(s->t1[tslot], st);
-  cudaError_t e = cudaEventRecord(s->ev[slot], st);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+int validate(const lbx_sim_config& c) {
+  if (c.box_size < 1 || c.extent_z % c.box_size || c.extent_x % c.box_size)
+    return set_error(LBX_EINVAL, "box_size %d must divide the extents", c.box_size);
+  if (c.n_ranks < 1) return set_error(LBX_EINVAL, "n_ranks must be >= 1");
+  if (c.total_steps < 1) return set_error(LBX_EINVAL, "total_steps must be >= 1");
+  if (c.interval < 1) return set_error(LBX_EINVAL, "interval must be >= 1");
+  if (c.cost_kind < 0 || c.cost_kind > LBX_COST_GPUCLOCK)
+    return set_error(LBX_EINVAL, "unknown cost kind %d", c.cost_kind);
   return LBX_OK;
 }
 
-// Host half of one step.  Returns 1 if the step hit OOM (run halts).
-int process_step(lbx_sim* s, int64_t step, lbx_sim_outputs* o, int* halt) {
+}  // namespace
+
+namespace lbx {
+
+// Host half of one step (see file comment).  `device_cost` is the heuristic
+// cost formed on the device (NULL: form it here from counts -- same
+// separately rounded products).  `clk` is the GpuClock tally (NULL unless
+// cost_kind is GPUCLOCK).
+int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device_cost,
+            const uint64_t* clk, int64_t n_alive, lbx_sim_outputs* o, int* adopted_out,
+            int* halt) {
   const lbx_sim_config& c = s->cfg;
   const int nb = s->nb;
   const int32_t R = c.n_ranks;
-  const int slot = (int)(step % s->ring);
-  cudaError_t e = cudaEventSynchronize(s->ev[slot]);
-  if (e != cudaSuccess) return cuda_fail(e, "step kernel");
-  Rec h = rec_at(s->ring_h, s->rec_bytes, slot, nb);
-  if (s->timing && o->kernel_ms) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, s->t0[slot], s->t1[slot]);
-    o->kernel_ms[step] = ms;
-  }
-  if (*h.err != 0)
-    return set_error(LBX_ERANGE, "step %lld: %lld survivors fall outside the box grid",
-                     (long long)step, (long long)*h.err);
-
-  // true work (workload.py:303-311) and provider cost (workload.py:414)
   const double cells = (double)((int64_t)c.box_size * c.box_size);
-  for (int b = 0; b < nb; ++b) s->work[b] = c.work_wp * (double)h.counts[b] + c.work_wc * cells;
+  for (int b = 0; b < nb; ++b) s->work[b] = c.work_wp * (double)counts[b] + c.work_wc * cells;
   double* cost = o->cost_trace + (size_t)step * nb;
   switch (c.cost_kind) {
     case LBX_COST_HEURISTIC:
-      std::memcpy(cost, h.cost, sizeof(double) * nb);
+      if (device_cost) {
+        std::memcpy(cost, device_cost, sizeof(double) * nb);
+      } else {
+        for (int b = 0; b < nb; ++b) cost[b] = c.w_particle * (double)counts[b] + c.w_cell * cells;
+      }
       break;
     case LBX_COST_MEASURED:
     case LBX_COST_INSTRUMENTED:
       measured_cost(s->work.data(), nb, c.noise_amplitude, c.noise_seed, (uint64_t)step, cost);
       break;
     case LBX_COST_GPUCLOCK:
-      for (int b = 0; b < nb; ++b) cost[b] = (double)h.clk[b];
+      if (!clk) return set_error(LBX_EINVAL, "GpuClock costs need the clock tally");
+      for (int b = 0; b < nb; ++b) cost[b] = (double)clk[b];
       break;
     default:
       return set_error(LBX_EINVAL, "unknown cost kind %d", c.cost_kind);
   }
-  if (o->count_trace) std::memcpy(o->count_trace + (size_t)step * nb, h.counts, 8 * (size_t)nb);
-  if (o->clock_trace) std::memcpy(o->clock_trace + (size_t)step * nb, h.clk, 8 * (size_t)nb);
-  o->n_alive[step] = *h.n;
+  if (o->count_trace) std::memcpy(o->count_trace + (size_t)step * nb, counts, 8 * (size_t)nb);
+  if (o->clock_trace && clk) std::memcpy(o->clock_trace + (size_t)step * nb, clk, 8 * (size_t)nb);
+  if (o->n_alive) o->n_alive[step] = n_alive;
 
   // balance (balancer.py:258-304)
-  double e_cur = 1.0, e_after;
+  double e_cur = 1.0;
   efficiency(cost, s->owner.data(), nb, R, &e_cur, nullptr, s->scratch);
-  e_after = e_cur;
+  double e_after = e_cur;
   const bool attempted = should_attempt(c, step);
   bool adopted = false;
   s->prev = s->owner;
@@ -169,7 +151,7 @@ int process_step(lbx_sim* s, int64_t step, lbx_sim_outputs* o, int* halt) {
     if (adopted) {
       s->owner = s->prop;
       e_after = e_prop;
-      o->adopt_steps[o->n_adoptions] = step;
+      if (o->adopt_steps) o->adopt_steps[o->n_adoptions] = step;
       if (o->adopt_owners)
         std::memcpy(o->adopt_owners + (size_t)o->n_adoptions * nb, s->owner.data(),
                     8 * (size_t)nb);
@@ -198,11 +180,11 @@ int process_step(lbx_sim* s, int64_t step, lbx_sim_outputs* o, int* halt) {
   if (adopted) {
     int64_t moved = 0;
     for (int b = 0; b < nb; ++b)
-      if (s->owner[b] != s->prev[b]) moved += h.counts[b];
+      if (s->owner[b] != s->prev[b]) moved += counts[b];
     redis = c.redistribute_latency + c.redistribute_per_particle * (double)moved;
   }
   std::fill(s->rank_acc.begin(), s->rank_acc.end(), 0.0);
-  for (int b = 0; b < nb; ++b) s->rank_acc[s->owner[b]] += (double)h.counts[b];
+  for (int b = 0; b < nb; ++b) s->rank_acc[s->owner[b]] += (double)counts[b];
   double occ = s->rank_acc[0];
   for (int r = 1; r < R; ++r) occ = std::max(occ, s->rank_acc[r]);
   const int64_t mrp = (int64_t)occ;
@@ -224,27 +206,76 @@ int process_step(lbx_sim* s, int64_t step, lbx_sim_outputs* o, int* halt) {
   o->max_rank_particles[step] = mrp;
   o->oom[step] = oom;
   o->completed_steps = step + 1;
+  if (adopted_out) *adopted_out = adopted ? 1 : 0;
   *halt = oom ? 1 : 0;
   return LBX_OK;
+}
+
+}  // namespace lbx
+
+namespace {
+
+int launch_step(lbx_sim* s, int64_t step, cudaStream_t st) {
+  const int slot = (int)(step % s->ring);
+  if (s->timing) cudaEventRecord(s->t0[slot], st);
+  Rec d = rec_at(s->ring_d, s->rec_bytes, slot, s->lb->nb);
+  const lbx_sim_config& c = s->lb->cfg;
+  const bool kicked = step >= c.kick_step && s->kvz != nullptr;
+  StepLaunch a{};
+  a.z = s->z;
+  a.x = s->x;
+  a.vz = kicked ? s->kvz : s->vz;
+  a.vx = kicked ? s->kvx : s->vx;
+  a.ez = (double)c.extent_z;
+  a.ex = (double)c.extent_x;
+  a.m = (double)c.box_size;
+  a.nbz = s->lb->nbz;
+  a.nbx = s->lb->nbx;
+  a.wp = c.w_particle;
+  a.wc = c.w_cell;
+  a.cells = (double)c.box_size * (double)c.box_size;
+  a.clock = c.cost_kind == LBX_COST_GPUCLOCK;
+  a.counts_out = reinterpret_cast<long long*>(d.counts);
+  a.cost_out = d.cost;
+  a.clk_out = a.clock ? reinterpret_cast<unsigned long long*>(d.clk) : nullptr;
+  a.n_out = reinterpret_cast<long long*>(d.n);
+  a.err_out = reinterpret_cast<long long*>(d.err);
+  int rc = launch_push_step(s->ctx, a, st);
+  if (rc) return rc;
+  if (s->timing) cudaEventRecord(s->t1[slot], st);
+  cudaError_t e = cudaEventRecord(s->ev[slot], st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+  return LBX_OK;
+}
+
+int process_step(lbx_sim* s, int64_t step, lbx_sim_outputs* o, int* halt) {
+  const int slot = (int)(step % s->ring);
+  cudaError_t e = cudaEventSynchronize(s->ev[slot]);
+  if (e != cudaSuccess) return cuda_fail(e, "step kernel");
+  Rec h = rec_at(s->ring_h, s->rec_bytes, slot, s->lb->nb);
+  if (s->timing && o->kernel_ms) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, s->t0[slot], s->t1[slot]);
+    o->kernel_ms[step] = ms;
+  }
+  if (*h.err != 0)
+    return set_error(LBX_ERANGE, "step %lld: %lld survivors fall outside the box grid",
+                     (long long)step, (long long)*h.err);
+  const bool clock = s->lb->cfg.cost_kind == LBX_COST_GPUCLOCK;
+  return lb_step(s->lb, step, h.counts, h.cost, clock ? h.clk : nullptr, *h.n, o, nullptr, halt);
 }
 
 }  // namespace
 
 extern "C" {
 
-int lbx_sim_create(lbx_sim** out, lbx_ctx* ctx, const lbx_sim_config* cfg) {
+int lbx_lb_create(lbx_lb** out, const lbx_sim_config* cfg, const int64_t* initial_owner) {
   clear_error();
-  if (!out || !ctx || !cfg) return set_error(LBX_EINVAL, "NULL argument");
+  if (!out || !cfg) return set_error(LBX_EINVAL, "NULL argument");
+  int rc = validate(*cfg);
+  if (rc) return rc;
   const lbx_sim_config& c = *cfg;
-  if (c.box_size < 1 || c.extent_z % c.box_size || c.extent_x % c.box_size)
-    return set_error(LBX_EINVAL, "box_size %d must divide the extents", c.box_size);
-  if (c.n_ranks < 1) return set_error(LBX_EINVAL, "n_ranks must be >= 1");
-  if (c.total_steps < 1) return set_error(LBX_EINVAL, "total_steps must be >= 1");
-  if (c.interval < 1) return set_error(LBX_EINVAL, "interval must be >= 1");
-  if (c.cost_kind < 0 || c.cost_kind > LBX_COST_GPUCLOCK)
-    return set_error(LBX_EINVAL, "unknown cost kind %d", c.cost_kind);
-  lbx_sim* s = new lbx_sim();
-  s->ctx = ctx;
+  lbx_lb* s = new lbx_lb();
   s->cfg = c;
   s->nbz = c.extent_z / c.box_size;
   s->nbx = c.extent_x / c.box_size;
@@ -263,16 +294,65 @@ int lbx_sim_create(lbx_sim** out, lbx_ctx* ctx, const lbx_sim_config* cfg) {
       s->face_b.push_back(bz * s->nbx + bx + 1);
     }
   s->owner.assign(nb, 0);
+  if (initial_owner) {
+    for (int b = 0; b < nb; ++b) {
+      if (initial_owner[b] < 0 || initial_owner[b] >= c.n_ranks) {
+        delete s;
+        return set_error(LBX_EINVAL, "owner entries must lie in [0, %d)", c.n_ranks);
+      }
+      s->owner[b] = initial_owner[b];
+    }
+  }
   s->prop.assign(nb, 0);
   s->prev.assign(nb, 0);
   s->work.assign(nb, 0.0);
   s->rank_acc.assign(c.n_ranks, 0.0);
   s->faces_per_rank.assign(c.n_ranks, 0);
-  s->ring = c.capacity_particles >= 0 ? 1 : 16;
+  *out = s;
+  return LBX_OK;
+}
+
+int lbx_lb_destroy(lbx_lb* lb) {
+  delete lb;
+  return LBX_OK;
+}
+
+int lbx_lb_step(lbx_lb* lb, int64_t step, const int64_t* counts, const uint64_t* clk,
+                int64_t n_alive, lbx_sim_outputs* out, int32_t* adopted, int32_t* halt) {
+  clear_error();
+  if (!lb || !counts || !out || !halt) return set_error(LBX_EINVAL, "NULL argument");
+  if (step < 0 || step >= lb->cfg.total_steps)
+    return set_error(LBX_EINVAL, "step %lld outside [0, %lld)", (long long)step,
+                     (long long)lb->cfg.total_steps);
+  int a = 0, h = 0;
+  int rc = lb_step(lb, step, counts, nullptr, clk, n_alive, out, &a, &h);
+  if (adopted) *adopted = a;
+  *halt = h;
+  return rc;
+}
+
+int lbx_lb_owner(lbx_lb* lb, int64_t* owner) {
+  clear_error();
+  if (!lb || !owner) return set_error(LBX_EINVAL, "NULL argument");
+  std::memcpy(owner, lb->owner.data(), 8 * (size_t)lb->nb);
+  return LBX_OK;
+}
+
+int lbx_sim_create(lbx_sim** out, lbx_ctx* ctx, const lbx_sim_config* cfg) {
+  clear_error();
+  if (!out || !ctx || !cfg) return set_error(LBX_EINVAL, "NULL argument");
+  lbx_lb* lb = nullptr;
+  int rc = lbx_lb_create(&lb, cfg, nullptr);
+  if (rc) return rc;
+  lbx_sim* s = new lbx_sim();
+  s->ctx = ctx;
+  s->lb = lb;
+  const int nb = lb->nb;
+  s->ring = cfg->capacity_particles >= 0 ? 1 : 16;
   s->rec_bytes = ((size_t)24 * nb + 16 + 255) & ~(size_t)255;
   cudaError_t e = cudaHostAlloc(&s->ring_h, s->rec_bytes * s->ring, cudaHostAllocMapped);
   if (e != cudaSuccess) {
-    delete s;
+    lbx_sim_destroy(s);
     return cuda_fail(e, "cudaHostAlloc(ring)");
   }
   std::memset(s->ring_h, 0, s->rec_bytes * s->ring);
@@ -282,14 +362,14 @@ int lbx_sim_create(lbx_sim** out, lbx_ctx* ctx, const lbx_sim_config* cfg) {
     return cuda_fail(e, "cudaHostGetDevicePointer");
   }
   s->ev.resize(s->ring);
-  for (auto& ev : s->ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   s->t0.resize(s->ring);
   s->t1.resize(s->ring);
   for (int i = 0; i < s->ring; ++i) {
+    cudaEventCreateWithFlags(&s->ev[i], cudaEventDisableTiming);
     cudaEventCreate(&s->t0[i]);
     cudaEventCreate(&s->t1[i]);
   }
-  int rc = ensure_accumulators(ctx, nb);
+  rc = ensure_accumulators(ctx, nb);
   if (rc) {
     lbx_sim_destroy(s);
     return rc;
@@ -305,6 +385,7 @@ int lbx_sim_destroy(lbx_sim* s) {
   for (auto& ev : s->t0) cudaEventDestroy(ev);
   for (auto& ev : s->t1) cudaEventDestroy(ev);
   if (s->ring_h) cudaFreeHost(s->ring_h);
+  delete s->lb;
   delete s;
   return LBX_OK;
 }
@@ -328,14 +409,15 @@ int lbx_sim_set_particles(lbx_sim* s, double* z, double* x, double* vz, double* 
 int lbx_sim_run(lbx_sim* s, int64_t first, int64_t last, lbx_sim_outputs* o, void* stream) {
   clear_error();
   if (!s || !o) return set_error(LBX_EINVAL, "NULL argument");
-  if (first < 0 || last > s->cfg.total_steps || first > last)
+  const lbx_sim_config& c = s->lb->cfg;
+  if (first < 0 || last > c.total_steps || first > last)
     return set_error(LBX_EINVAL, "step range [%lld, %lld) outside [0, %lld)", (long long)first,
-                     (long long)last, (long long)s->cfg.total_steps);
+                     (long long)last, (long long)c.total_steps);
   if (!s->z) return set_error(LBX_EINVAL, "particles not set");
-  if (first == 0) std::memcpy(s->owner.data(), o->owner, 8 * (size_t)s->nb);
-  for (int b = 0; b < s->nb; ++b)
-    if (s->owner[b] < 0 || s->owner[b] >= s->cfg.n_ranks)
-      return set_error(LBX_EINVAL, "owner entries must lie in [0, %d)", s->cfg.n_ranks);
+  if (first == 0) std::memcpy(s->lb->owner.data(), o->owner, 8 * (size_t)s->lb->nb);
+  for (int b = 0; b < s->lb->nb; ++b)
+    if (s->lb->owner[b] < 0 || s->lb->owner[b] >= c.n_ranks)
+      return set_error(LBX_EINVAL, "owner entries must lie in [0, %d)", c.n_ranks);
   cudaStream_t st = (cudaStream_t)stream;
   s->timing = o->kernel_ms != nullptr;
   int64_t launched = first, processed = first;
@@ -353,7 +435,7 @@ int lbx_sim_run(lbx_sim* s, int64_t first, int64_t last, lbx_sim_outputs* o, voi
   // Capacity runs use ring=1, so no step past a halting step was launched.
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "stream sync");
-  std::memcpy(o->owner, s->owner.data(), 8 * (size_t)s->nb);
+  std::memcpy(o->owner, s->lb->owner.data(), 8 * (size_t)s->lb->nb);
   return LBX_OK;
 }
 

@@ -1,0 +1,397 @@
+"""Multi-GPU runtime: box ownership -> GPU.
+
+One process per GPU.  Rank r holds the particles of the boxes it owns
+(``owner[b] == r``).  Per step, on every rank:
+
+  1. libLBX exchange step: push + absorb + per-box counts / GpuClock tally of
+     everything this rank pushed; a survivor whose box is owned elsewhere is
+     staged as a 6-double record for its owner and compacted out locally.
+  2. all-reduce(sum) of the per-box counts (and clock tally): every box's
+     particles were pushed by exactly one rank, so the sum is the exact
+     global vector -- bit-identical to a single-process run.
+  3. box-crossing exchange: all-to-all of per-destination counts, then of the
+     records (NCCL over NVLink on B200; gloo in the CPU tests), unpack.
+  4. every rank runs the same host step (lbx_lb_step: cost vector,
+     efficiency, knapsack/SFC attempt, adoption gate, walltime columns) on
+     the same vector, so all ranks agree with no broadcast (PAPER.md:146,155
+     gathers to a root and broadcasts; replicated deterministic remapping
+     replaces that).
+  5. on adoption: every rank stages the particles of the boxes it lost
+     (lbx_partition) and the same all-to-all migrates them -- the
+     redistribution the reference only models (workload.py:332-337).
+
+Parity: metrics, cost trace and mappings equal the reference run with
+ranks = world size; the particle multiset equals it (local order differs).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ConfigError
+from .workload import (RunResult, StepMetrics, box_array_for, initial_mapping,
+                       kick_velocities, policy_kind, sample_blob, sim_config)
+
+REC = _lib.RECORD_DOUBLES
+
+
+# ---------------------------------------------------------------------------
+# communicators
+# ---------------------------------------------------------------------------
+
+class TorchComm:
+    """torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_reduce_sum(self, t: torch.Tensor):
+        self.dist.all_reduce(t, group=self.group)
+
+    def exchange_counts(self, send_counts: torch.Tensor) -> torch.Tensor:
+        recv = torch.empty_like(send_counts)
+        self.dist.all_to_all_single(recv, send_counts, group=self.group)
+        return recv
+
+    def exchange_records(self, send: torch.Tensor, sc: list, rc: list) -> torch.Tensor:
+        recv = torch.empty((sum(rc), REC), dtype=send.dtype, device=send.device)
+        self.dist.all_to_all_single(recv, send, rc, sc, group=self.group)
+        return recv
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+
+class ThreadComm:
+    """In-process communicator for `world` ranks run as threads (tests on a
+    single GPU).  Create one shared state with ThreadComm.shared(world)."""
+
+    @staticmethod
+    def shared(world: int) -> dict:
+        return {"world": world, "bar": threading.Barrier(world), "slot": [None] * world}
+
+    def __init__(self, shared: dict, rank: int):
+        self.s = shared
+        self.rank = rank
+        self.world = shared["world"]
+
+    def _swap(self, value):
+        self.s["slot"][self.rank] = value
+        self.s["bar"].wait()
+        vals = list(self.s["slot"])
+        self.s["bar"].wait()
+        return vals
+
+    def all_reduce_sum(self, t: torch.Tensor):
+        vals = self._swap(t.detach().cpu().clone())
+        total = vals[0].clone()
+        for v in vals[1:]:
+            total += v
+        t.copy_(total.to(t.device))
+
+    def exchange_counts(self, send_counts: torch.Tensor) -> torch.Tensor:
+        vals = self._swap(send_counts.detach().cpu().clone())
+        return torch.stack([v[self.rank] for v in vals]).to(send_counts.device)
+
+    def exchange_records(self, send: torch.Tensor, sc: list, rc: list) -> torch.Tensor:
+        chunks = list(torch.split(send.detach().cpu(), sc))
+        vals = self._swap(chunks)
+        out = torch.cat([v[self.rank] for v in vals]) if vals else send[:0].cpu()
+        return out.reshape(-1, REC).to(send.device)
+
+    def barrier(self):
+        self.s["bar"].wait()
+
+
+# ---------------------------------------------------------------------------
+# device engine (libLBX)
+# ---------------------------------------------------------------------------
+
+class DeviceEngine:
+    """This rank's particles in HBM and the libLBX exchange kernels."""
+
+    def __init__(self, cfg, rank, world, device, pos, kick, capacity, clock):
+        from . import device as D
+
+        self.dev = D.require_cuda(device)
+        self.D = D
+        self.rank, self.world = rank, world
+        self.nbz, self.nbx = box_array_for(cfg).grid_shape
+        self.nb = self.nbz * self.nbx
+        self.ez, self.ex = float(cfg.domain_extent[0]), float(cfg.domain_extent[1])
+        self.m = float(cfg.box_size)
+        self.clock = clock
+        cap = int(capacity) + 2
+        f64 = dict(dtype=torch.float64, device=self.dev)
+        self.z, self.x = torch.zeros(cap, **f64), torch.zeros(cap, **f64)
+        self.vz, self.vx = torch.zeros(cap, **f64), torch.zeros(cap, **f64)
+        self.kvz = self.kvx = None
+        n = int(pos.shape[0])
+        p = torch.as_tensor(pos).to(self.dev)
+        self.z[:n].copy_(p[:, 0])
+        self.x[:n].copy_(p[:, 1])
+        if kick is not None:
+            k = torch.as_tensor(kick).to(self.dev)
+            self.kvz, self.kvx = torch.zeros(cap, **f64), torch.zeros(cap, **f64)
+            self.kvz[:n].copy_(k[:, 0])
+            self.kvx[:n].copy_(k[:, 1])
+        self.n = n
+        self.capacity = int(capacity)
+        self.stage = torch.empty((cap, REC), **f64)
+        self.stage_dest = torch.empty(cap, dtype=torch.int32, device=self.dev)
+        self.send_counts = torch.zeros(world, dtype=torch.int64, device=self.dev)
+        self.owner = torch.zeros(self.nb, dtype=torch.int32, device=self.dev)
+        self.counts = torch.zeros(self.nb, dtype=torch.int64, device=self.dev)
+        self.cost = torch.zeros(self.nb, **f64)
+        self.clk = torch.zeros(self.nb, dtype=torch.int64, device=self.dev)
+        self.nout = torch.zeros(2, dtype=torch.int64, device=self.dev)
+        self.ctx = D.Context(self.dev, capacity=cap)
+
+    def _ex(self):
+        return _lib.ExchangeArgs(
+            _lib.ptr(self.owner), self.rank, self.world, _lib.ptr(self.stage),
+            _lib.ptr(self.stage_dest), self.capacity + 2, _lib.ptr(self.send_counts),
+            _lib.ptr(self.kvz), _lib.ptr(self.kvx))
+
+    def set_owner(self, owner: np.ndarray):
+        self.owner.copy_(torch.from_numpy(np.asarray(owner, dtype=np.int32)))
+
+    def kick(self):
+        if self.kvz is not None:
+            self.vz, self.vx, self.kvz, self.kvx = self.kvz, self.kvx, None, None
+
+    def push(self, wp, wc):
+        self.send_counts.zero_()
+        self.ctx.set_count(self.n)
+        args = _lib.StepArgs(
+            _lib.ptr(self.z), _lib.ptr(self.x), _lib.ptr(self.vz), _lib.ptr(self.vx),
+            self.ez, self.ex, self.m, self.nbz, self.nbx, float(wp), float(wc),
+            self.m * self.m, _lib.LBX_STEP_CLOCK if self.clock else 0,
+            _lib.ptr(self.counts), _lib.ptr(self.cost), _lib.ptr(self.clk),
+            _lib.ptr(self.nout), _lib.ptr(self.nout[1:]))
+        ex = self._ex()
+        _lib.check(_lib.lib.lbx_push_step_exchange(self.ctx.handle, C.byref(args), C.byref(ex),
+                                                   self.D._stream(self.dev)))
+        self._after()
+        return self.counts, self.clk, self.send_counts
+
+    def partition(self):
+        self.send_counts.zero_()
+        self.ctx.set_count(self.n)
+        ex = self._ex()
+        _lib.check(_lib.lib.lbx_partition(
+            self.ctx.handle, _lib.ptr(self.z), _lib.ptr(self.x), _lib.ptr(self.vz),
+            _lib.ptr(self.vx), self.ez, self.ex, self.m, self.nbz, self.nbx, C.byref(ex),
+            _lib.ptr(self.nout), self.D._stream(self.dev)))
+        self._after()
+        return self.send_counts
+
+    def _after(self):
+        h = self.nout.cpu().numpy()
+        if h[1] != 0:
+            raise ValueError("particles outside the box grid or staging overflow "
+                             f"(code {int(h[1])})")
+        self.n = int(h[0])
+
+    def pack(self, sc: list) -> torch.Tensor:
+        total = int(sum(sc))
+        send = torch.empty((total, REC), dtype=torch.float64, device=self.dev)
+        if total:
+            cur = torch.tensor(np.concatenate(([0], np.cumsum(sc)[:-1])), dtype=torch.int64,
+                               device=self.dev)
+            _lib.check(_lib.lib.lbx_group_by_dest(_lib.ptr(self.stage), _lib.ptr(self.stage_dest),
+                                                  total, self.world, _lib.ptr(cur), _lib.ptr(send),
+                                                  self.D._stream(self.dev)))
+        return send
+
+    def unpack(self, recv: torch.Tensor):
+        m = int(recv.shape[0])
+        if self.n + m > self.capacity:
+            raise MemoryError(f"rank {self.rank}: {self.n + m} particles exceed capacity "
+                              f"{self.capacity}")
+        if m:
+            recv = recv.contiguous()
+            _lib.check(_lib.lib.lbx_unpack(_lib.ptr(recv), m, self.n, _lib.ptr(self.z),
+                                           _lib.ptr(self.x), _lib.ptr(self.vz), _lib.ptr(self.vx),
+                                           _lib.ptr(self.kvz), _lib.ptr(self.kvx),
+                                           self.D._stream(self.dev)))
+        self.n += m
+
+    def state(self):
+        n = self.n
+        pos = torch.stack([self.z[:n], self.x[:n]], 1).cpu().numpy()
+        vel = torch.stack([self.vz[:n], self.vx[:n]], 1).cpu().numpy()
+        return pos, vel
+
+
+# ---------------------------------------------------------------------------
+# driver
+# ---------------------------------------------------------------------------
+
+def box_ids_host(pos: np.ndarray, box_size: int, nbx: int) -> np.ndarray:
+    """(int)(z/M)*nbx + (int)(x/M) on the host (setup only: selecting each
+    rank's initial particles), IEEE division then truncation."""
+    return (np.trunc(pos[:, 0] / float(box_size)).astype(np.int64) * nbx
+            + np.trunc(pos[:, 1] / float(box_size)).astype(np.int64))
+
+
+class DistributedSimulation:
+    """One rank of a box-decomposed run (see module docstring)."""
+
+    def __init__(self, cfg, policy, provider, *, comm=None, engine_factory=None,
+                 positions=None, kick=None, device=None, capacity=None,
+                 record_counts=False):
+        self.comm = comm or TorchComm()
+        self.rank, self.world = self.comm.rank, self.comm.world
+        if cfg.n_ranks != self.world:
+            raise ConfigError(f"scenario has {cfg.n_ranks} ranks but the job has {self.world}")
+        if provider.device_kind < 0 or provider.device_kind > 3:
+            raise ConfigError(f"provider {provider.kind!r} is not supported by the native loop")
+        self.cfg, self.policy, self.provider = cfg, policy, provider
+        self.ba = box_array_for(cfg)
+        nbz, nbx = self.ba.grid_shape
+        pos = sample_blob(cfg) if positions is None else np.asarray(positions)
+        self.n_init = int(pos.shape[0])
+        ids = box_ids_host(pos, cfg.box_size, nbx)
+        counts0 = np.bincount(ids, minlength=nbz * nbx).astype(np.int64)
+        self.initial_owner = np.array(initial_mapping(cfg, self.ba, counts0).owner)
+        mine = self.initial_owner[ids] == self.rank
+        if cfg.kick.step < cfg.total_steps and kick is None:
+            kick = kick_velocities(pos, cfg)
+        kick_local = None if kick is None or cfg.kick.step >= cfg.total_steps else kick[mine]
+        cap = capacity if capacity is not None else self.n_init
+        factory = engine_factory or DeviceEngine
+        self.engine = factory(cfg, self.rank, self.world, device, pos[mine], kick_local, cap,
+                              provider.device_kind == 3)
+        self.engine.set_owner(self.initial_owner)
+        self.conf = sim_config(cfg, policy, provider)
+        h = C.c_void_p()
+        own = np.ascontiguousarray(self.initial_owner, dtype=np.int64)
+        _lib.check(_lib.lib.lbx_lb_create(C.byref(h), C.byref(self.conf), _lib.ptr(own)))
+        self.lb = h
+        T, nb = cfg.total_steps, self.ba.n_boxes
+        o = {k: np.zeros(T) for k in ("eff_before", "eff_after", "compute_max", "comm_max",
+                                      "gather", "redistribute", "walltime")}
+        for k in ("adopted", "attempted", "oom"):
+            o[k] = np.zeros(T, dtype=np.uint8)
+        o["max_rank_particles"] = np.zeros(T, dtype=np.int64)
+        o["n_alive"] = np.zeros(T, dtype=np.int64)
+        o["cost_trace"] = np.zeros((T, nb))
+        o["count_trace"] = np.zeros((T, nb), dtype=np.int64) if record_counts else None
+        o["adopt_steps"] = np.zeros(T, dtype=np.int64)
+        o["adopt_owners"] = np.zeros((T, nb), dtype=np.int64)
+        o["owner"] = own.copy()
+        self.out = o
+        self.souts = _lib.SimOutputs(
+            *(_lib.ptr(o.get(k)) for k in ("eff_before", "eff_after", "adopted", "attempted",
+                                           "compute_max", "comm_max", "gather", "redistribute",
+                                           "walltime", "max_rank_particles", "oom", "n_alive",
+                                           "cost_trace", "count_trace", "clock_trace", "owner",
+                                           "adopt_steps", "adopt_owners")),
+            None, 0, 0, 0)
+        self.done = 0
+        self.halted = False
+        self.moved = np.zeros(T, dtype=np.int64)   # particles migrated on adoption
+
+    def close(self):
+        if getattr(self, "lb", None):
+            _lib.lib.lbx_lb_destroy(self.lb)
+            self.lb = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _exchange(self, send_counts) -> int:
+        recv_counts = self.comm.exchange_counts(send_counts)
+        sc = [int(v) for v in send_counts.cpu().tolist()]
+        rc = [int(v) for v in recv_counts.cpu().tolist()]
+        send = self.engine.pack(sc)
+        recv = self.comm.exchange_records(send, sc, rc)
+        self.engine.unpack(recv)
+        return sum(sc)
+
+    def run(self, first=None, last=None):
+        cfg = self.cfg
+        first = self.done if first is None else first
+        last = cfg.total_steps if last is None else last
+        w = getattr(self.provider, "weights", None)
+        wp, wc = (w.w_particle, w.w_cell) if w else (0.75, 0.25)
+        clock = self.provider.device_kind == 3
+        adopted, halt = C.c_int32(), C.c_int32()
+        for step in range(first, last):
+            if self.halted:
+                break
+            if step == cfg.kick.step:
+                self.engine.kick()
+            counts, clk, send_counts = self.engine.push(wp, wc)
+            self.comm.all_reduce_sum(counts)
+            if clock:
+                self.comm.all_reduce_sum(clk)
+            self._exchange(send_counts)
+            ch = np.ascontiguousarray(counts.cpu().numpy(), dtype=np.int64)
+            kh = np.ascontiguousarray(clk.cpu().numpy()).view(np.uint64) if clock else None
+            _lib.check(_lib.lib.lbx_lb_step(self.lb, step, _lib.ptr(ch), _lib.ptr(kh),
+                                            int(ch.sum()), C.byref(self.souts),
+                                            C.byref(adopted), C.byref(halt)))
+            if adopted.value:
+                owner = np.empty(self.ba.n_boxes, dtype=np.int64)
+                _lib.check(_lib.lib.lbx_lb_owner(self.lb, _lib.ptr(owner)))
+                self.engine.set_owner(owner)
+                self.moved[step] = self._exchange(self.engine.partition())
+            self.done = step + 1
+            if halt.value:
+                self.halted = True
+        return self
+
+    def local_state(self):
+        return self.engine.state()
+
+    def result(self) -> RunResult:
+        o, cfg, done = self.out, self.cfg, int(self.souts.completed_steps)
+        metrics = [StepMetrics(step=s, efficiency_before=float(o["eff_before"][s]),
+                               efficiency_after=float(o["eff_after"][s]),
+                               adopted=bool(o["adopted"][s]),
+                               compute_max=float(o["compute_max"][s]),
+                               comm_max=float(o["comm_max"][s]), gather=float(o["gather"][s]),
+                               redistribute=float(o["redistribute"][s]),
+                               walltime=float(o["walltime"][s]),
+                               max_rank_particles=int(o["max_rank_particles"][s]),
+                               oom=bool(o["oom"][s])) for s in range(done)]
+        na = int(self.souts.n_adoptions)
+        eff = np.array([m.efficiency_after for m in metrics])
+        summary = {
+            "scenario_id": cfg.scenario_id, "n_ranks": cfg.n_ranks,
+            "n_boxes": self.ba.n_boxes, "box_grid": list(self.ba.grid_shape),
+            "seed": cfg.seed, "policy": policy_kind(self.policy, cfg.total_steps),
+            "strategy": self.policy.strategy.value, "interval": self.policy.interval,
+            "improvement_threshold": self.policy.improvement_threshold,
+            "threshold_mode": self.policy.threshold_mode,
+            "static_step": self.policy.static_step, "provider": self.provider.kind,
+            "overhead_factor": self.provider.overhead_factor,
+            "total_steps": cfg.total_steps, "completed_steps": done,
+            "completion_fraction": done / cfg.total_steps,
+            "total_walltime": float(sum(m.walltime for m in metrics)),
+            "mean_efficiency": float(eff.mean()) if done else 0.0,
+            "adoption_count": na, "attempt_count": int(self.souts.n_attempts),
+            "oom": bool(done and metrics[-1].oom),
+            "final_particles": int(o["n_alive"][done - 1]) if done else self.n_init,
+        }
+        return RunResult(
+            metrics=metrics, summary=summary, cost_trace=o["cost_trace"][:done].copy(),
+            initial_owner=self.initial_owner.copy(),
+            adoption_snapshots=[(int(o["adopt_steps"][i]), o["adopt_owners"][i].copy())
+                                for i in range(na)],
+            n_alive=o["n_alive"][:done].copy(),
+            count_trace=None if o["count_trace"] is None else o["count_trace"][:done].copy())

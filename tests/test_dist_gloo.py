@@ -1,0 +1,85 @@
+"""Multi-rank protocol of parallel.DistributedSimulation on CPU (gloo,
+world size 2 and 3): per-rank particles, box-crossing exchange, exact
+all-reduced cost vectors, replicated remap and adoption-time migration must
+reproduce the single-process oracle run with ranks = world size exactly
+(metrics, cost trace, mappings) and its particle multiset."""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from oracle import lbsim_oracle as O
+from tests.dist_util import free_port, run_rank
+from tests.scenario_util import preset_doc
+
+G = Path(__file__).resolve().parent / "golden"
+
+CASES = [
+    ("mini", 2, {"steps": 40}),
+    ("mini", 3, {"steps": 40, "policy": "sfc"}),
+    ("leaky", 3, {}),
+    ("tight-memory", 2, {"steps": 60, "cost": "measured"}),
+]
+
+
+def oracle_cfg(base, world, kw):
+    if base == "leaky":
+        doc = json.loads((G / "runs.json").read_text())["_docs"]["leaky"]
+    else:
+        doc = preset_doc(base)
+    cfg = O.config_from_doc(doc)
+    cfg["ranks"] = world
+    if "steps" in kw:
+        cfg["steps"] = kw["steps"]
+    if "policy" in kw:
+        cfg = O.apply_policy(cfg, kw["policy"])
+    if "cost" in kw:
+        cfg["provider"] = kw["cost"]
+    return cfg, doc
+
+
+def sorted_rows(a):
+    a = np.asarray(a).reshape(-1, a.shape[-1] if a.ndim > 1 else 1)
+    return a[np.lexsort(a.T[::-1])]
+
+
+@pytest.mark.parametrize("base,world,kw", CASES)
+def test_distributed_matches_single_process_oracle(tmp_path, base, world, kw):
+    cfg, doc = oracle_cfg(base, world, kw)
+    spec_kw = dict(kw)
+    spec_kw["_base"] = doc if base == "leaky" else base
+    mp.spawn(run_rank, args=(world, free_port(), spec_kw, str(tmp_path)), nprocs=world)
+    ref = O.run_simulation(cfg, record_counts=True)
+    outs = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
+    for o in outs:   # every rank took the same decisions
+        assert o["eff_before"].tolist() == ref["metrics"]["eff_before"].tolist()
+        assert o["eff_after"].tolist() == ref["metrics"]["eff_after"].tolist()
+        assert o["adopted"].tolist() == ref["metrics"]["adopted"].tolist()
+        assert o["walltime"].tolist() == ref["metrics"]["walltime"].tolist()
+        assert o["redistribute"].tolist() == ref["metrics"]["redistribute"].tolist()
+        assert o["mrp"].tolist() == ref["metrics"]["max_rank_particles"].tolist()
+        assert np.array_equal(o["cost_trace"], ref["cost_trace"])
+        assert np.array_equal(o["count_trace"], ref["count_trace"])
+        assert o["initial_owner"].tolist() == ref["initial_owner"].tolist()
+        assert o["snap_steps"].tolist() == [s for s, _ in ref["snapshots"]]
+        for row, (_, own) in zip(o["snap_owner"], ref["snapshots"]):
+            assert row.tolist() == own.tolist()
+    # particle multiset equals the reference's final state
+    pos = np.concatenate([o["pos"] for o in outs])
+    vel = np.concatenate([o["vel"] for o in outs])
+    got = sorted_rows(np.column_stack([pos, vel]))
+    want = sorted_rows(np.column_stack([ref["final_pos"], ref["final_vel"]]))
+    assert np.array_equal(got, want)
+    # each rank holds exactly the particles of the boxes it owns at the end
+    final_owner = (ref["snapshots"][-1][1] if ref["snapshots"] else ref["initial_owner"])
+    M = cfg["box_size"]
+    nbx = cfg["extent"][1] // M
+    for r, o in enumerate(outs):
+        if o["pos"].size:
+            b = (np.trunc(o["pos"][:, 0] / M).astype(int) * nbx
+                 + np.trunc(o["pos"][:, 1] / M).astype(int))
+            assert (final_owner[b] == r).all()
+    if any(ref["metrics"]["adopted"]):
+        assert sum(o["moved"].sum() for o in outs) > 0

@@ -1,0 +1,85 @@
+"""The multi-GPU path's device kernels (exchange push, partition, group,
+unpack, compaction with kick buffers) on a real GPU: `world` ranks run as
+threads sharing cuda:0 through parallel.ThreadComm; results must equal the
+single-process oracle with ranks = world (metrics, cost trace, mappings,
+particle multiset)."""
+import json
+import threading
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import lbsim_oracle as O
+from tests.test_dist_gloo import oracle_cfg, sorted_rows
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def run_threads(base, world, kw, doc):
+    from paper_2104_11385_b200 import scenarios as S
+    from paper_2104_11385_b200.parallel import DeviceEngine, DistributedSimulation, ThreadComm
+    shared = ThreadComm.shared(world)
+    spec = S.spec_from_dict(doc) if base == "leaky" else S.load_spec(base)
+    spec = S.apply_overrides(spec, ranks=world, **kw)
+    outs, errs = [None] * world, []
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            sim = DistributedSimulation(spec.scenario, spec.policy, spec.build_provider(),
+                                        comm=ThreadComm(shared, r), engine_factory=DeviceEngine,
+                                        device="cuda:0", record_counts=True)
+            sim.run()
+            outs[r] = (sim.result(), sim.local_state(), sim.moved.copy())
+            sim.close()
+        except Exception as e:  # surface in the main thread
+            errs.append(e)
+            shared["bar"].abort()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    return outs
+
+
+@pytest.mark.parametrize("base,world,kw", [("mini", 2, {"steps": 40}),
+                                           ("mini", 3, {"steps": 40, "policy": "sfc"}),
+                                           ("leaky", 3, {}),
+                                           ("tight-memory", 2, {"steps": 60, "cost": "measured"})])
+def test_gpu_distributed_matches_oracle(base, world, kw):
+    cfg, doc = oracle_cfg(base, world, kw)
+    outs = run_threads(base, world, kw, doc)
+    ref = O.run_simulation(cfg, record_counts=True)
+    for res, _, _ in outs:
+        m = res.metrics
+        assert [x.efficiency_before for x in m] == ref["metrics"]["eff_before"].tolist()
+        assert [x.adopted for x in m] == ref["metrics"]["adopted"].tolist()
+        assert [x.walltime for x in m] == ref["metrics"]["walltime"].tolist()
+        assert np.array_equal(res.cost_trace, ref["cost_trace"])
+        assert np.array_equal(res.count_trace, ref["count_trace"])
+        assert [s for s, _ in res.adoption_snapshots] == [s for s, _ in ref["snapshots"]]
+    pos = np.concatenate([st[0] for _, st, _ in outs])
+    vel = np.concatenate([st[1] for _, st, _ in outs])
+    assert np.array_equal(sorted_rows(np.column_stack([pos, vel])),
+                          sorted_rows(np.column_stack([ref["final_pos"], ref["final_vel"]])))
+    if any(ref["metrics"]["adopted"]):
+        assert sum(mv.sum() for _, _, mv in outs) > 0
+
+
+def test_gpu_distributed_gpuclock_runs():
+    """GpuClock costs across ranks: every rank's clock tally is all-reduced,
+    so all ranks see the same cost vector and take the same decisions."""
+    cfg, doc = oracle_cfg("mini", 2, {"steps": 30})
+    outs = run_threads("mini", 2, {"steps": 30, "cost": "gpuclock"}, doc)
+    a, b = outs[0][0], outs[1][0]
+    assert np.array_equal(a.cost_trace, b.cost_trace)
+    assert [m.adopted for m in a.metrics] == [m.adopted for m in b.metrics]
+    ref = O.run_simulation(cfg, record_counts=True)
+    assert np.array_equal(a.count_trace, ref["count_trace"])
+    assert ((a.cost_trace > 0) == (ref["count_trace"] > 0)).all()
