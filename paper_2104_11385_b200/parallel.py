@@ -155,6 +155,7 @@ class DeviceEngine:
         self.clk = torch.zeros(self.nb, dtype=torch.int64, device=self.dev)
         self.nout = torch.zeros(2, dtype=torch.int64, device=self.dev)
         self.ctx = D.Context(self.dev, capacity=cap)
+        self.launches = 0   # libLBX kernel launches issued (for gpu_launches)
 
     def _ex(self):
         return _lib.ExchangeArgs(
@@ -181,6 +182,7 @@ class DeviceEngine:
         ex = self._ex()
         _lib.check(_lib.lib.lbx_push_step_exchange(self.ctx.handle, C.byref(args), C.byref(ex),
                                                    self.D._stream(self.dev)))
+        self.launches += 3   # set_count, stream kernel, compaction
         self._after()
         return self.counts, self.clk, self.send_counts
 
@@ -192,6 +194,7 @@ class DeviceEngine:
             self.ctx.handle, _lib.ptr(self.z), _lib.ptr(self.x), _lib.ptr(self.vz),
             _lib.ptr(self.vx), self.ez, self.ex, self.m, self.nbz, self.nbx, C.byref(ex),
             _lib.ptr(self.nout), self.D._stream(self.dev)))
+        self.launches += 3
         self._after()
         return self.send_counts
 
@@ -211,6 +214,7 @@ class DeviceEngine:
             _lib.check(_lib.lib.lbx_group_by_dest(_lib.ptr(self.stage), _lib.ptr(self.stage_dest),
                                                   total, self.world, _lib.ptr(cur), _lib.ptr(send),
                                                   self.D._stream(self.dev)))
+            self.launches += 1
         return send
 
     def unpack(self, recv: torch.Tensor):
@@ -224,6 +228,7 @@ class DeviceEngine:
                                            _lib.ptr(self.x), _lib.ptr(self.vz), _lib.ptr(self.vx),
                                            _lib.ptr(self.kvz), _lib.ptr(self.kvx),
                                            self.D._stream(self.dev)))
+            self.launches += 1
         self.n += m
 
     def state(self):
@@ -249,7 +254,7 @@ class DistributedSimulation:
 
     def __init__(self, cfg, policy, provider, *, comm=None, engine_factory=None,
                  positions=None, kick=None, device=None, capacity=None,
-                 record_counts=False):
+                 record_counts=False, replicas=1):
         self.comm = comm or TorchComm()
         self.rank, self.world = self.comm.rank, self.comm.world
         if cfg.n_ranks != self.world:
@@ -259,18 +264,24 @@ class DistributedSimulation:
         self.cfg, self.policy, self.provider = cfg, policy, provider
         self.ba = box_array_for(cfg)
         nbz, nbx = self.ba.grid_shape
+        # `replicas`: the particle set is tiled that many times (identical
+        # copies evolve identically; used to fill a B200 with the C2 set).
         pos = sample_blob(cfg) if positions is None else np.asarray(positions)
-        self.n_init = int(pos.shape[0])
+        self.n_init = int(pos.shape[0]) * replicas
         ids = box_ids_host(pos, cfg.box_size, nbx)
-        counts0 = np.bincount(ids, minlength=nbz * nbx).astype(np.int64)
+        counts0 = replicas * np.bincount(ids, minlength=nbz * nbx).astype(np.int64)
         self.initial_owner = np.array(initial_mapping(cfg, self.ba, counts0).owner)
         mine = self.initial_owner[ids] == self.rank
         if cfg.kick.step < cfg.total_steps and kick is None:
             kick = kick_velocities(pos, cfg)
         kick_local = None if kick is None or cfg.kick.step >= cfg.total_steps else kick[mine]
+        local = pos[mine]
+        if replicas > 1:
+            local = np.tile(local, (replicas, 1))
+            kick_local = None if kick_local is None else np.tile(kick_local, (replicas, 1))
         cap = capacity if capacity is not None else self.n_init
         factory = engine_factory or DeviceEngine
-        self.engine = factory(cfg, self.rank, self.world, device, pos[mine], kick_local, cap,
+        self.engine = factory(cfg, self.rank, self.world, device, local, kick_local, cap,
                               provider.device_kind == 3)
         self.engine.set_owner(self.initial_owner)
         self.conf = sim_config(cfg, policy, provider)
