@@ -425,86 +425,52 @@ def run_lbx_dist(args, rank, world, dev):
 
 
 def e2e_plugin(args, dev, pos0, kick0, R, sc):
-    """Same workload through the reference-facing plugin boundary
-    (kernels.advance_particles / bin_particles + heuristic cost, C ABI) with
-    HOST buffers: every step copies the particles in from pinned host memory
-    and the survivors, counts and costs back out."""
+    """Same workload through the reference-facing plugin boundary with HOST
+    buffers: every step calls lbx_advance_bin_host (the C-ABI behind
+    kernels.advance_particles / bin_particles for host arrays) on the
+    particles in pinned host memory -- host->device copy of all particles,
+    push + absorb + compaction + per-box counts + heuristic cost, and the
+    survivors, counts and costs copied back -- chunked over two streams so
+    both PCIe directions overlap the kernels."""
     import torch
 
-    from paper_2104_11385_b200 import _lib
-    from paper_2104_11385_b200.device import Context, _stream
+    from paper_2104_11385_b200.kernels import advance_bin_host
 
     n = pos0.shape[0] * R
     nbz = nbx = sc.domain_extent[0] // sc.box_size
-    nb = nbz * nbx
-    hp = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
-    hv = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
-    hp.numpy()[:] = np.tile(pos0, (R, 1))
-    hv.numpy()[:] = np.tile(kick0, (R, 1))
-    op = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
-    ov = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
-    hc = torch.empty(nb, dtype=torch.int64, pin_memory=True)
-    hcost = torch.empty(nb, dtype=torch.float64, pin_memory=True)
-    dp = torch.empty((n + 1, 2), dtype=torch.float64, device=dev)
-    dv = torch.empty_like(dp)
-    dpo = torch.empty_like(dp)
-    dvo = torch.empty_like(dp)
-    dc = torch.empty(nb, dtype=torch.int64, device=dev)
-    dcf = torch.empty(nb, dtype=torch.float64, device=dev)
-    dcells = torch.full((nb,), float(sc.box_size ** 2), dtype=torch.float64, device=dev)
-    dcost = torch.empty(nb, dtype=torch.float64, device=dev)
-    m = torch.empty(1, dtype=torch.int64, device=dev)
-    hm = torch.empty(1, dtype=torch.int64, pin_memory=True)
-    ctx = Context(dev, capacity=n)
-    s = _stream(dev)
-    stream = torch.cuda.current_stream(dev)
-    ez, ex, M = float(sc.domain_extent[0]), float(sc.domain_extent[1]), float(sc.box_size)
-    state = {"n": n, "inp": (hp, hv), "out": (op, ov)}
-    h2d = d2h = 0
+    bufs = [torch.empty((n, 2), dtype=torch.float64, pin_memory=True).numpy() for _ in range(4)]
+    bufs[0][:] = np.tile(pos0, (R, 1))
+    bufs[1][:] = np.tile(kick0, (R, 1))
+    state = {"n": n, "inp": (bufs[0], bufs[1]), "out": (bufs[2], bufs[3])}
+    ez, ex = float(sc.domain_extent[0]), float(sc.domain_extent[1])
+    io = {"h2d": 0, "d2h": 0}
 
     def step():
-        nonlocal h2d, d2h
         k = state["n"]
         ip, iv = state["inp"]
-        dp[:k].copy_(ip[:k], non_blocking=True)
-        dv[:k].copy_(iv[:k], non_blocking=True)
-        _lib.check(_lib.lib.lbx_advance_particles(ctx.handle, _lib.ptr(dp), _lib.ptr(dv), k,
-                                                  ez, ex, _lib.ptr(dpo), _lib.ptr(dvo),
-                                                  _lib.ptr(m), s))
-        hm.copy_(m, non_blocking=True)
-        stream.synchronize()
-        mm = int(hm[0])
-        _lib.check(_lib.lib.lbx_bin_particles(_lib.ptr(dpo), mm, M, nbz, nbx, _lib.ptr(dc),
-                                              None, s))
-        dcf.copy_(dc)
-        _lib.check(_lib.lib.lbx_heuristic_cost(_lib.ptr(dcf), _lib.ptr(dcells), nb, 0.75,
-                                               0.25, _lib.ptr(dcost), s))
-        opp, ovv = state["out"]
-        opp[:mm].copy_(dpo[:mm], non_blocking=True)
-        ovv[:mm].copy_(dvo[:mm], non_blocking=True)
-        hc.copy_(dc, non_blocking=True)
-        hcost.copy_(dcost, non_blocking=True)
-        stream.synchronize()
-        h2d += 32 * k
-        d2h += 32 * mm + 16 * nb + 8
-        state["n"] = mm
+        op, ov = state["out"]
+        p, v, counts, cost = advance_bin_host(ip[:k], iv[:k], ez, ex, float(sc.box_size),
+                                              nbz, nbx, out=(op, ov), dev=dev)
+        m = p.shape[0]
+        io["h2d"] += 32 * k
+        io["d2h"] += 32 * m + 16 * nbz * nbx
+        state["n"] = m
         state["inp"], state["out"] = state["out"], state["inp"]
         return k
 
     for _ in range(2):
         step()
-    h2d = d2h = 0
+    io["h2d"] = io["d2h"] = 0
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     pushed = sum(step() for _ in range(args.e2e_steps))
     el = time.perf_counter() - t0
-    ctx.close()
     return {"value": pushed / el, "unit": UNIT,
-            "h2d_bytes_per_step": h2d // args.e2e_steps,
-            "d2h_bytes_per_step": d2h // args.e2e_steps,
+            "h2d_bytes_per_step": io["h2d"] // args.e2e_steps,
+            "d2h_bytes_per_step": io["d2h"] // args.e2e_steps,
             "steps": args.e2e_steps,
-            "path": "lbx_advance_particles + lbx_bin_particles + lbx_heuristic_cost "
-                    "(reference AoS layout), pinned host buffers, copies in the timed region"}
+            "path": "lbx_advance_bin_host (reference AoS layout, pinned host buffers, "
+                    "4 Mi-particle chunks over 2 streams), copies in the timed region"}
 
 
 def main():

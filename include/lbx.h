@@ -81,6 +81,20 @@ int lbx_bin_particles(const double* pos, int64_t n, double box_size,
                       int32_t nbz, int32_t nbx, int64_t* counts,
                       int64_t* err_dev, void* stream);
 
+/* The plugin path for HOST arrays (the reference calls advance_particles and
+ * bin_particles on numpy arrays every step, workload.py:293-298): advance
+ * [n][2] host pos/vel (pinned for full PCIe speed) into host out_pos/out_vel
+ * (survivors, order kept, *m_out of them) and, when counts != NULL, the
+ * per-box counts of the survivors and their heuristic cost (cost may be
+ * NULL).  Chunks alternate over two streams with separate look-back state,
+ * so host->device copies, kernels and device->host copies overlap (PCIe is
+ * full duplex).  Synchronous. */
+int lbx_advance_bin_host(lbx_ctx* ctx, const double* pos, const double* vel, int64_t n,
+                         double extent_z, double extent_x, double box_size,
+                         int32_t nbz, int32_t nbx, double w_particle, double w_cell,
+                         double* out_pos, double* out_vel, int64_t* counts,
+                         double* cost, int64_t* m_out);
+
 /* ------------------------------------------------------------------------
  * Fused device step (the hot path; replaces workload.py:286-300 advance +
  * workload.py:303-311 true_work counts + cost.py:83-95 heuristic_cost, and

@@ -106,6 +106,8 @@ SIGNATURES.update({
                             vp, vp]),
     "lbx_group_by_dest": (i32, [vp, vp, i64, i32, vp, vp, vp]),
     "lbx_unpack": (i32, [vp, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
+    "lbx_advance_bin_host": (i32, [vp, vp, vp, i64, f64, f64, f64, i32, i32, f64, f64, vp, vp,
+                                   vp, vp, P(i64)]),
 })
 RECORD_DOUBLES = 6
 

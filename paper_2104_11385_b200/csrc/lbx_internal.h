@@ -43,6 +43,11 @@ struct StepLaunch {
 
 }  // namespace lbx
 
+namespace lbx {
+struct HostPipe;
+void destroy_pipe(HostPipe* hp);
+}  // namespace lbx
+
 struct lbx_ctx {
   int device = 0;
   int num_sms = 0;
@@ -54,6 +59,7 @@ struct lbx_ctx {
   int64_t n_upper = 0;                // host upper bound on the live count
   int grid_override = 0;
   int64_t* host_scratch = nullptr;    // pinned
+  lbx::HostPipe* pipe = nullptr;      // lbx_advance_bin_host lanes (lazy)
 };
 
 #include <vector>

@@ -699,7 +699,9 @@ __global__ void __launch_bounds__(kBlock) bin_kernel(const double2* __restrict__
                                                      long long n, double m, int nbz, int nbx,
                                                      int smem_hist,
                                                      unsigned long long* __restrict__ counts,
-                                                     unsigned long long* __restrict__ err) {
+                                                     unsigned long long* __restrict__ err,
+                                                     const long long* __restrict__ n_dev) {
+  if (n_dev) n = *n_dev;  // count produced by a preceding kernel on the stream
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned* s_cnt = reinterpret_cast<unsigned*>(smem_raw);
   const int nb = nbz * nbx;
@@ -750,6 +752,12 @@ __global__ void heuristic_kernel(const double* __restrict__ particles,
                                  double wc, double* __restrict__ cost) {
   const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (b < n) cost[b] = __dadd_rn(__dmul_rn(wp, particles[b]), __dmul_rn(wc, cells[b]));
+}
+
+__global__ void counts_cost_kernel(const long long* __restrict__ counts, int nb, double wp,
+                                   double wc, double cells, double* __restrict__ cost) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nb) cost[b] = __dadd_rn(__dmul_rn(wp, (double)counts[b]), __dmul_rn(wc, cells));
 }
 
 __global__ void init_state_kernel(DevState* st, long long n) {
@@ -868,6 +876,87 @@ int reserve_status(lbx_ctx* ctx, int64_t capacity) {
   }
   ctx->status = s;
   ctx->status_tiles = tiles;
+  return LBX_OK;
+}
+
+}  // namespace
+
+// Two-lane host-buffer pipeline state (lbx_advance_bin_host), cached in ctx.
+struct HostPipe {
+  static constexpr long long kChunk = 1ll << 22;  // 4 Mi particles per chunk
+  cudaStream_t s[2] = {};
+  cudaEvent_t done[2] = {}, ready = {};
+  DevState* st[2] = {};
+  unsigned long long* status[2] = {};
+  double *d_in_pos[2] = {}, *d_in_vel[2] = {}, *d_out_pos[2] = {}, *d_out_vel[2] = {};
+  long long* d_m[2] = {};
+  long long* h_m = nullptr;  // pinned [2]
+  long long* d_counts = nullptr;
+  double* d_cost = nullptr;
+  long long* d_err = nullptr;
+  long long nb = 0;
+};
+
+void destroy_pipe(HostPipe* hp) {
+  if (!hp) return;
+  for (int l = 0; l < 2; ++l) {
+    if (hp->s[l]) cudaStreamSynchronize(hp->s[l]), cudaStreamDestroy(hp->s[l]);
+    if (hp->done[l]) cudaEventDestroy(hp->done[l]);
+    cudaFree(hp->st[l]);
+    cudaFree(hp->status[l]);
+    cudaFree(hp->d_in_pos[l]);
+    cudaFree(hp->d_in_vel[l]);
+    cudaFree(hp->d_out_pos[l]);
+    cudaFree(hp->d_out_vel[l]);
+    cudaFree(hp->d_m[l]);
+  }
+  if (hp->ready) cudaEventDestroy(hp->ready);
+  cudaFreeHost(hp->h_m);
+  cudaFree(hp->d_counts);
+  cudaFree(hp->d_cost);
+  cudaFree(hp->d_err);
+  delete hp;
+}
+
+namespace {
+
+int ensure_pipe(lbx_ctx* ctx, long long nb) {
+  if (ctx->pipe && ctx->pipe->nb >= nb) return LBX_OK;
+  if (ctx->pipe) {
+    destroy_pipe(ctx->pipe);
+    ctx->pipe = nullptr;
+  }
+  HostPipe* hp = new HostPipe();
+  const long long C = HostPipe::kChunk;
+  const size_t tiles = (size_t)((C + kTile - 1) / kTile + 1);
+  bool ok = cudaHostAlloc(&hp->h_m, 16, cudaHostAllocDefault) == cudaSuccess;
+  for (int l = 0; l < 2 && ok; ++l) {
+    ok = cudaStreamCreateWithFlags(&hp->s[l], cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&hp->done[l], cudaEventDisableTiming) == cudaSuccess &&
+         cudaMalloc(&hp->st[l], sizeof(DevState)) == cudaSuccess &&
+         cudaMalloc(&hp->status[l], tiles * 8) == cudaSuccess &&
+         cudaMalloc(&hp->d_in_pos[l], (size_t)C * 16) == cudaSuccess &&
+         cudaMalloc(&hp->d_in_vel[l], (size_t)C * 16) == cudaSuccess &&
+         cudaMalloc(&hp->d_out_pos[l], (size_t)C * 16) == cudaSuccess &&
+         cudaMalloc(&hp->d_out_vel[l], (size_t)C * 16) == cudaSuccess &&
+         cudaMalloc(&hp->d_m[l], 8) == cudaSuccess;
+    if (ok) {
+      cudaMemset(hp->status[l], 0, tiles * 8);
+      cudaMemset(hp->st[l], 0, sizeof(DevState));
+      init_state_kernel<<<1, 1>>>(hp->st[l], 0);
+    }
+  }
+  ok = ok && cudaEventCreateWithFlags(&hp->ready, cudaEventDisableTiming) == cudaSuccess &&
+       cudaMalloc(&hp->d_counts, (size_t)std::max(nb, 1ll) * 8) == cudaSuccess &&
+       cudaMalloc(&hp->d_cost, (size_t)std::max(nb, 1ll) * 8) == cudaSuccess &&
+       cudaMalloc(&hp->d_err, 8) == cudaSuccess;
+  if (ok) ok = cudaMemset(hp->d_err, 0, 8) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess;
+  if (!ok) {
+    destroy_pipe(hp);
+    return set_error(LBX_EOOM, "host pipeline buffers: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  hp->nb = nb;
+  ctx->pipe = hp;
   return LBX_OK;
 }
 
@@ -1018,6 +1107,7 @@ int lbx_ctx_destroy(lbx_ctx* ctx) {
   if (ctx->status) cudaFree(ctx->status);
   if (ctx->acc) cudaFree(ctx->acc);
   if (ctx->host_scratch) cudaFreeHost(ctx->host_scratch);
+  destroy_pipe(ctx->pipe);
   delete ctx;
   return LBX_OK;
 }
@@ -1113,7 +1203,7 @@ int lbx_bin_particles(const double* pos, int64_t n, double box_size, int32_t nbz
   bin_kernel<<<(unsigned)grid, kBlock, smem, s>>>(
       reinterpret_cast<const double2*>(pos), n, box_size, nbz, nbx, smem_hist,
       reinterpret_cast<unsigned long long*>(counts),
-      reinterpret_cast<unsigned long long*>(err_dev));
+      reinterpret_cast<unsigned long long*>(err_dev), nullptr);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "bin_kernel launch");
   return LBX_OK;
@@ -1153,6 +1243,106 @@ int lbx_heuristic_cost(const double* particles, const double* cells, int64_t n,
       particles, cells, n, w_particle, w_cell, cost);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "heuristic launch");
+  return LBX_OK;
+}
+
+int lbx_advance_bin_host(lbx_ctx* ctx, const double* pos, const double* vel, int64_t n,
+                         double extent_z, double extent_x, double box_size, int32_t nbz,
+                         int32_t nbx, double w_particle, double w_cell, double* out_pos,
+                         double* out_vel, int64_t* counts, double* cost, int64_t* m_out) {
+  clear_error();
+  if (!ctx || !m_out) return set_error(LBX_EINVAL, "NULL argument");
+  if (n < 0) return set_error(LBX_EINVAL, "n must be >= 0");
+  const bool bin = counts != nullptr;
+  const long long nb = (long long)nbz * nbx;
+  if (bin && nb < 1) return set_error(LBX_EINVAL, "box grid must be at least 1x1");
+  cudaSetDevice(ctx->device);
+  int rc = ensure_pipe(ctx, bin ? nb : 0);
+  if (rc) return rc;
+  HostPipe& hp = *ctx->pipe;
+  cudaError_t e = cudaSuccess;
+  if (bin) e = cudaMemsetAsync(hp.d_counts, 0, (size_t)nb * 8, hp.s[0]);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  cudaEventRecord(hp.ready, hp.s[0]);
+  cudaStreamWaitEvent(hp.s[1], hp.ready, 0);
+  const long long C = HostPipe::kChunk;
+  const long long nchunks = (n + C - 1) / C;
+  const int smem_hist = (bin && nb <= kSmemBoxesMax) ? 1 : 0;
+  const size_t bsmem = smem_hist ? (size_t)nb * 4 : 0;
+  if (bsmem > 48 * 1024)
+    cudaFuncSetAttribute(bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
+  long long written = 0;
+  auto drain = [&](long long i) -> int {
+    const int l = (int)(i & 1);
+    cudaError_t ee = cudaEventSynchronize(hp.done[l]);
+    if (ee != cudaSuccess) return cuda_fail(ee, "advance chunk");
+    const long long m = hp.h_m[l];
+    if (m > 0) {
+      cudaMemcpyAsync(out_pos + 2 * written, hp.d_out_pos[l], (size_t)m * 16,
+                      cudaMemcpyDeviceToHost, hp.s[l]);
+      cudaMemcpyAsync(out_vel + 2 * written, hp.d_out_vel[l], (size_t)m * 16,
+                      cudaMemcpyDeviceToHost, hp.s[l]);
+    }
+    written += m;
+    return LBX_OK;
+  };
+  for (long long i = 0; i < nchunks; ++i) {
+    const int l = (int)(i & 1);
+    if (i >= 2) {  // lane l is reused: its previous chunk must be drained first
+      rc = drain(i - 2);
+      if (rc) return rc;
+    }
+    const long long k = std::min(C, n - i * C);
+    cudaStream_t s = hp.s[l];
+    cudaMemcpyAsync(hp.d_in_pos[l], pos + 2 * i * C, (size_t)k * 16, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(hp.d_in_vel[l], vel + 2 * i * C, (size_t)k * 16, cudaMemcpyHostToDevice, s);
+    ScanParams p{};
+    p.in_pos = reinterpret_cast<const double2*>(hp.d_in_pos[l]);
+    p.in_vel = reinterpret_cast<const double2*>(hp.d_in_vel[l]);
+    p.out_pos = reinterpret_cast<double2*>(hp.d_out_pos[l]);
+    p.out_vel = reinterpret_cast<double2*>(hp.d_out_vel[l]);
+    p.ez = extent_z;
+    p.ex = extent_x;
+    p.n_host = k;
+    p.st = hp.st[l];
+    p.status = hp.status[l];
+    p.n_out = hp.d_m[l];
+    rc = launch_scan<kAdvanceAoS>(ctx, p, k, s);
+    if (rc) return rc;
+    if (bin) {
+      const long long grid =
+          std::max(1ll, std::min((long long)ctx->num_sms * 8, (k + kBlock * 8 - 1) / (kBlock * 8)));
+      bin_kernel<<<(unsigned)grid, kBlock, bsmem, s>>>(
+          reinterpret_cast<const double2*>(hp.d_out_pos[l]), k, box_size, nbz, nbx, smem_hist,
+          reinterpret_cast<unsigned long long*>(hp.d_counts),
+          reinterpret_cast<unsigned long long*>(hp.d_err), hp.d_m[l]);
+    }
+    cudaMemcpyAsync(&hp.h_m[l], hp.d_m[l], 8, cudaMemcpyDeviceToHost, s);
+    cudaEventRecord(hp.done[l], s);
+  }
+  for (long long i = std::max(0ll, nchunks - 2); i < nchunks; ++i) {
+    rc = drain(i);
+    if (rc) return rc;
+  }
+  cudaEventRecord(hp.ready, hp.s[1]);
+  cudaStreamWaitEvent(hp.s[0], hp.ready, 0);
+  if (bin) {
+    counts_cost_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, hp.s[0]>>>(
+        hp.d_counts, (int)nb, w_particle, w_cell, box_size * box_size, hp.d_cost);
+    cudaMemcpyAsync(counts, hp.d_counts, (size_t)nb * 8, cudaMemcpyDeviceToHost, hp.s[0]);
+    if (cost) cudaMemcpyAsync(cost, hp.d_cost, (size_t)nb * 8, cudaMemcpyDeviceToHost, hp.s[0]);
+    cudaMemcpyAsync(&hp.h_m[0], hp.d_err, 8, cudaMemcpyDeviceToHost, hp.s[0]);
+  }
+  e = cudaStreamSynchronize(hp.s[0]);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(hp.s[1]);
+  if (e != cudaSuccess) return cuda_fail(e, "host pipeline");
+  if (bin && hp.h_m[0] != 0) {
+    cudaMemsetAsync(hp.d_err, 0, 8, hp.s[0]);
+    cudaStreamSynchronize(hp.s[0]);
+    return set_error(LBX_ERANGE, "%lld survivors fall outside the box grid",
+                     (long long)hp.h_m[0]);
+  }
+  *m_out = written;
   return LBX_OK;
 }
 

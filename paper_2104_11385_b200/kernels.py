@@ -47,13 +47,38 @@ def advance_particles(positions, velocities, extent_z, extent_x):
     vel = _as_pairs(velocities, "velocities")
     if pos.shape != vel.shape:
         raise ValueError("positions and velocities differ in shape")
-    dev = _dev.require_cuda("cuda")
+    _dev.require_cuda("cuda")
     dev = torch.device("cuda", torch.cuda.current_device())
-    if pos.shape[0] == 0:
+    n = pos.shape[0]
+    if n == 0:
         return np.empty((0, 2)), np.empty((0, 2))
-    p, v = _dev.advance_aos(_ctx(dev), torch.from_numpy(pos).to(dev),
-                            torch.from_numpy(vel).to(dev), extent_z, extent_x)
-    return p.cpu().numpy(), v.cpu().numpy()
+    return advance_bin_host(pos, vel, extent_z, extent_x, dev=dev)[:2]
+
+
+def advance_bin_host(pos, vel, extent_z, extent_x, box_size=None, nbz=0, nbx=0,
+                     weights=(0.75, 0.25), out=None, dev=None):
+    """Host arrays in, host arrays out, through lbx_advance_bin_host (chunked,
+    both PCIe directions and the kernels overlapped).  With box_size also
+    returns the survivors' per-box counts and heuristic cost.  `out` may
+    supply (out_pos, out_vel) host buffers of shape (n, 2) (pinned = full
+    speed)."""
+    import ctypes as C
+
+    from . import _lib
+
+    dev = dev or torch.device("cuda", torch.cuda.current_device())
+    n = pos.shape[0]
+    op, ov = out if out is not None else (np.empty((n, 2)), np.empty((n, 2)))
+    bin_ = box_size is not None
+    counts = np.empty(int(nbz) * int(nbx), dtype=np.int64) if bin_ else None
+    cost = np.empty(int(nbz) * int(nbx)) if bin_ else None
+    m = C.c_int64()
+    _lib.check(_lib.lib.lbx_advance_bin_host(
+        _ctx(dev).handle, _lib.ptr(pos), _lib.ptr(vel), n, float(extent_z), float(extent_x),
+        float(box_size or 1.0), int(nbz), int(nbx), float(weights[0]), float(weights[1]),
+        _lib.ptr(op), _lib.ptr(ov), _lib.ptr(counts), _lib.ptr(cost), C.byref(m)))
+    k = m.value
+    return op[:k], ov[:k], counts, cost
 
 
 def bin_particles(positions, box_size, nbz, nbx):

@@ -114,3 +114,17 @@ def test_fused_sfc_weights_no_fma():
     out = device.push_step(ctx, st, 96.0, 96.0, 16.0, 6, 6, (0.02, 0.98))
     c2 = O.bin_particles(pos, 16.0, 6, 6)
     assert np.array_equal(out["cost"], O.heuristic_cost(c2, np.full(36, 256), 0.02, 0.98))
+
+
+@pytest.mark.parametrize("n", [0, 1, 5000, (1 << 22) + 17, 9_000_001])
+def test_host_pipeline_matches_oracle(K, n):
+    """lbx_advance_bin_host: chunked two-lane pipeline, host buffers."""
+    rng = np.random.default_rng(n + 7)
+    pos = rng.uniform(0, 96.0, size=(n, 2))
+    vel = rng.normal(0, 1.5, size=(n, 2))
+    p, v, counts, cost = K.advance_bin_host(pos, vel, 96.0, 96.0, 16.0, 6, 6)
+    p2, v2 = O.advance_particles(pos, vel, 96.0, 96.0)
+    assert np.array_equal(p, p2) and np.array_equal(v, v2)
+    c2 = O.bin_particles(p2, 16.0, 6, 6)
+    assert np.array_equal(counts, c2)
+    assert np.array_equal(cost, O.heuristic_cost(c2, np.full(36, 256), 0.75, 0.25))
