@@ -196,11 +196,41 @@ def run_fixture():
     (OUT / "runs.json").write_text(json.dumps(out, indent=0, sort_keys=True))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--cli" not in sys.argv:
     print("reference lbsim", lbsim.__version__, "backend", lbsim.KERNEL_BACKEND)
     kernels_fixture()
     balancer_fixture()
     measured_fixture()
     run_fixture()
+    cli_fixture()
     for p in sorted(OUT.iterdir()):
         print(p.name, p.stat().st_size)
+
+
+def cli_fixture():
+    """sha256 of the reference CLI's own output files (lbsim/cli.py:65-101)."""
+    import tempfile
+
+    from lbsim import cli
+    cases = {"mini": ["--scenario", "mini"],
+             "mini_sfc": ["--scenario", "mini", "--policy", "sfc"],
+             "mini_measured": ["--scenario", "mini", "--cost", "measured", "--steps", "120"],
+             "tight_none": ["--scenario", "tight-memory", "--policy", "none"],
+             "tight": ["--scenario", "tight-memory", "--steps", "200"]}
+    out = {}
+    for name, argv in cases.items():
+        with tempfile.TemporaryDirectory() as d:
+            rc = cli.main(["run", *argv, "--out", d])
+            out[name] = {"argv": argv, "rc": rc,
+                         **{f: hashlib.sha256((Path(d) / f).read_bytes()).hexdigest()
+                            for f in ("metrics.csv", "cost_trace.csv", "mappings.csv",
+                                      "summary.json")}}
+            rd = Path(d) / "replay"
+            cli.main(["replay", "--run-dir", d, "--out", str(rd)])
+            out[name]["replay_metrics.csv"] = hashlib.sha256(
+                (rd / "replay_metrics.csv").read_bytes()).hexdigest()
+    (OUT / "cli.json").write_text(json.dumps(out, indent=1, sort_keys=True))
+
+
+if __name__ == "__main__" and "--cli" in sys.argv:
+    cli_fixture()
