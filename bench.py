@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="use the multi-GPU box-ownership path even at N=1 (testing)")
     return ap.parse_args()
 
 
@@ -169,14 +171,18 @@ def _ref_kernels():
 
 
 def _cpu_worker(args):
-    """One single-threaded reference loop on the base (1-replica) workload,
-    running whole steps until `seconds` elapse.  Returns (pushes, secs)."""
-    seconds, cost_kind = args
+    """One single-threaded reference loop over `reps` replicas of the base
+    set (its share of the benchmark workload), whole steps until `seconds`
+    elapse.  Returns (pushes, secs, steps)."""
+    seconds, cost_kind, reps = args
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     from oracle import lbsim_oracle as O
     K, _ = _ref_kernels()
     spec, sc = c2_spec(1, 10 ** 6, "measured")
     pos, vel = base_particles(spec)
+    if reps > 1:
+        pos = np.ascontiguousarray(np.tile(pos, (reps, 1)))
+        vel = np.ascontiguousarray(np.tile(vel, (reps, 1)))
     m = float(sc.box_size)
     nbz = nbx = sc.domain_extent[0] // sc.box_size
     cells = np.full(nbz * nbx, sc.box_size ** 2, dtype=np.int64)
@@ -205,21 +211,28 @@ def _cpu_worker(args):
             return pushes, el, step
 
 
-def cpu_baseline(seconds: float, processes: int):
+def cpu_baseline(seconds: float, processes: int, replicas: int):
+    """The reference's CPU path on the benchmark workload: the R replicas of
+    the C2 set are split over `processes` single-threaded processes (the
+    reference itself is single-threaded), each running whole steps of its
+    share for ~`seconds`; value = sum of per-process particle-pushes/s."""
     import multiprocessing as mp
 
     _, kind = _ref_kernels()
+    processes = max(1, min(processes, replicas))
+    reps = max(1, replicas // processes)
     if processes <= 1:
-        res = [_cpu_worker((seconds, "measured"))]
+        res = [_cpu_worker((seconds, "measured", reps))]
     else:
         with mp.get_context("spawn").Pool(processes) as pool:
-            res = pool.map(_cpu_worker, [(seconds, "measured")] * processes)
+            res = pool.map(_cpu_worker, [(seconds, "measured", reps)] * processes)
     value = sum(p / s for p, s, _ in res)
     steps = sum(k for _, _, k in res)
     return {"value": value, "unit": UNIT, "cores": processes, "kind": kind,
-            "sample": (f"C2 base set (801,499 particles, from the kick) x {processes} "
-                       f"independent single-threaded processes, {steps} steps total in "
-                       f"~{seconds:.0f} s each: reference Cython advance_particles + "
+            "sample": (f"C2 set (801,499 particles, from the kick) x {reps} replicas per "
+                       f"process x {processes} single-threaded processes = "
+                       f"{801499 * reps * processes} particles; {steps} whole steps in "
+                       f"~{seconds:.0f} s: reference Cython advance_particles + "
                        "bin_particles (oracle/_ref) + measured_cost / efficiency / "
                        "knapsack every 10 (oracle numpy port)")}
 
@@ -231,8 +244,8 @@ def cpu_baseline(seconds: float, processes: int):
 def run_reference(args, rank):
     if rank != 0:
         return
-    procs = os.cpu_count() or 1
-    cb = cpu_baseline(args.cpu_seconds, procs)
+    procs = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    cb = cpu_baseline(args.cpu_seconds, procs or 1, args.replicas)
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "impl": "reference",
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -255,9 +268,12 @@ def run_lbx(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
+    if world > 1 or args.force_dist:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29571")
+            dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
         return run_lbx_dist(args, rank, world, dev)
     total = args.warmup + args.steps
     spec, sc = c2_spec(world, total, args.cost)
@@ -340,7 +356,7 @@ def run_lbx(args, rank, world, local_rank):
     if e2e is not None:
         line["e2e"] = e2e
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.cpu_seconds, 1)
+        line["cpu_baseline"] = cpu_baseline(args.cpu_seconds, 1, args.replicas)
     print(json.dumps(line), flush=True)
     _lib.lib.lbx_sim_destroy(sim.handle)
     sim.handle = None
