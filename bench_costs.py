@@ -7,6 +7,8 @@ R-rank job, computed on one GPU).  For each strategy:
 
   heuristic  uninstrumented fused kernel (counts -> w_p*count + w_c*cells)
   gpuclock   the same kernel instantiated with the clock64 tally
+  timers     per-box push launches timed with CUDA events (the paper's
+             CUPTI-style strategy): box-sort + one launch per box
   measured   the reference's simulated timer (true work x PCG64 jitter)
 
 Reported per strategy: mean fused-kernel time (CUDA events around each
@@ -42,7 +44,7 @@ def main():
     ap.add_argument("--ranks", type=int, default=8)
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--strategies", default="heuristic,gpuclock,measured")
+    ap.add_argument("--strategies", default="heuristic,gpuclock,timers,measured")
     args = ap.parse_args()
 
     import torch
@@ -66,7 +68,14 @@ def main():
         sim = Simulation(sc, spec.policy, spec.build_provider(), device=dev, positions=pos,
                          kick=kick, record_counts=True, time_kernels=True)
         del pos, kick
-        sim.run()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sim.run(0, args.warmup)
+        torch.cuda.synchronize()
+        ev0.record()
+        sim.run(args.warmup, args.steps)
+        ev1.record()
+        torch.cuda.synchronize()
+        step_ms = ev0.elapsed_time(ev1) / (args.steps - args.warmup)
         res = sim.result()
         kms = res.kernel_ms[args.warmup:]
         owner = res.initial_owner.copy()
@@ -79,10 +88,11 @@ def main():
             work = true_work(res.count_trace[s], sc)
             e_true.append(efficiency(CostVector(values=work),
                                      DistributionMapping(owner=owner, n_ranks=args.ranks)))
-            if kind == "gpuclock" and s % 10 == 0:
+            if kind in ("gpuclock", "timers") and s % 10 == 0:
                 occ = res.count_trace[s] > 0
                 rho.append(spearman(res.cost_trace[s][occ], work[occ]))
-        entry = {"kernel_ms_mean": float(np.mean(kms)), "kernel_ms_min": float(np.min(kms)),
+        entry = {"step_ms_mean": step_ms,
+                 "kernel_ms_mean": float(np.mean(kms)), "kernel_ms_min": float(np.min(kms)),
                  "mean_eff_true_work": float(np.mean(e_true)),
                  "mean_eff_own_costs": res.summary["mean_efficiency"],
                  "e_true_first": float(e_true[0]), "adoptions": res.summary["adoption_count"],
@@ -97,6 +107,9 @@ def main():
     st = out["strategies"]
     if "heuristic" in st and "gpuclock" in st:
         out["gpuclock_overhead"] = st["gpuclock"]["kernel_ms_mean"] / st["heuristic"]["kernel_ms_mean"] - 1
+        out["gpuclock_step_overhead"] = st["gpuclock"]["step_ms_mean"] / st["heuristic"]["step_ms_mean"] - 1
+    if "heuristic" in st and "timers" in st:
+        out["timers_step_overhead"] = st["timers"]["step_ms_mean"] / st["heuristic"]["step_ms_mean"] - 1
     print(json.dumps(out))
 
 

@@ -187,6 +187,9 @@ typedef struct lbx_sim lbx_sim;
 #define LBX_COST_MEASURED 1      /* modeled timer: true work x PCG64 noise   */
 #define LBX_COST_INSTRUMENTED 2  /* same stream, overhead factor applied    */
 #define LBX_COST_GPUCLOCK 3      /* fused clock64 tally (real device cost)   */
+#define LBX_COST_TIMERS 4        /* per-box launches timed with CUDA events
+                                    (the paper's CUPTI-style Timers); cost =
+                                    microseconds per box                      */
 
 #define LBX_STRATEGY_KNAPSACK 0
 #define LBX_STRATEGY_SFC 1

@@ -77,4 +77,12 @@ int measured_cost(const double* work, int64_t n, double amplitude, uint64_t seed
 int launch_push_step(lbx_ctx* ctx, const StepLaunch& a, void* stream,
                      const lbx_exchange_args* ex = nullptr, bool push = true);
 int ensure_accumulators(lbx_ctx* ctx, int32_t nboxes);
+// Timers strategy helpers (lbx_kernels.cu): phase 0 = box ids + counts,
+// phase 1 = scatter indices into per-box segments (offsets from the host).
+int launch_timers_sort(const double* z, const double* x, long long n, double m, int nbz, int nbx,
+                       int* box, unsigned long long* counts, unsigned long long* cursors,
+                       int* perm, const unsigned long long* offsets_host, void* stream,
+                       int phase);
+int launch_timers_push(double* z, double* x, const double* vz, const double* vx, const int* idx,
+                       long long cnt, void* stream);
 }  // namespace lbx

@@ -754,6 +754,41 @@ __global__ void heuristic_kernel(const double* __restrict__ particles,
   if (b < n) cost[b] = __dadd_rn(__dmul_rn(wp, particles[b]), __dmul_rn(wc, cells[b]));
 }
 
+// ---- Timers strategy (per-box launches) ----
+__global__ void timers_box_kernel(const double* __restrict__ z, const double* __restrict__ x,
+                                  long long n, double m, int nbz, int nbx,
+                                  int* __restrict__ box, unsigned long long* __restrict__ counts) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    int bz = (int)__ddiv_rn(z[i], m), bx = (int)__ddiv_rn(x[i], m);
+    bz = min(max(bz, 0), nbz - 1);  // live particles are in the domain
+    bx = min(max(bx, 0), nbx - 1);
+    const int b = bz * nbx + bx;
+    box[i] = b;
+    atomicAdd(counts + b, 1ull);
+  }
+}
+
+__global__ void timers_scatter_kernel(const int* __restrict__ box, long long n,
+                                      unsigned long long* cursors, int* __restrict__ perm) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    perm[atomicAdd(cursors + box[i], 1ull)] = (int)i;
+}
+
+// Push the particles of one box (gather by index); absorbed ones are left
+// out of the domain for the compaction pass.
+__global__ void timers_push_kernel(double* z, double* x, const double* __restrict__ vz,
+                                   const double* __restrict__ vx, const int* __restrict__ idx,
+                                   long long cnt) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += stride) {
+    const int i = idx[j];
+    z[i] = __dadd_rn(z[i], vz[i]);
+    x[i] = __dadd_rn(x[i], vx[i]);
+  }
+}
+
 __global__ void counts_cost_kernel(const long long* __restrict__ counts, int nb, double wp,
                                    double wc, double cells, double* __restrict__ cost) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -967,6 +1002,33 @@ bool is_pow2(double m) {
 }
 
 }  // namespace
+
+int launch_timers_sort(const double* z, const double* x, long long n, double m, int nbz, int nbx,
+                       int* box, unsigned long long* counts, unsigned long long* cursors,
+                       int* perm, const unsigned long long* offsets_host, void* stream,
+                       int phase) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned grid = (unsigned)std::max(1ll, std::min(4096ll, (n + 255) / 256));
+  if (phase == 0) {
+    cudaMemsetAsync(counts, 0, (size_t)nbz * nbx * 8, s);
+    if (n) timers_box_kernel<<<grid, 256, 0, s>>>(z, x, n, m, nbz, nbx, box, counts);
+  } else {
+    cudaMemcpyAsync(cursors, offsets_host, (size_t)nbz * nbx * 8, cudaMemcpyHostToDevice, s);
+    if (n) timers_scatter_kernel<<<grid, 256, 0, s>>>(box, n, cursors, perm);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "timers sort launch");
+  return LBX_OK;
+}
+
+int launch_timers_push(double* z, double* x, const double* vz, const double* vx, const int* idx,
+                       long long cnt, void* stream) {
+  const unsigned grid = (unsigned)std::max(1ll, std::min(1184ll, (cnt + 255) / 256));
+  timers_push_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(z, x, vz, vx, idx, cnt);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "timers push launch");
+  return LBX_OK;
+}
 
 int ensure_accumulators(lbx_ctx* ctx, int32_t nboxes) {
   if (nboxes <= ctx->acc_boxes) return LBX_OK;

@@ -47,6 +47,17 @@ struct lbx_sim {
   unsigned char* ring_d = nullptr;
   std::vector<cudaEvent_t> ev, t0, t1;  // completion / kernel timing events
   bool timing = false;
+  // Timers strategy (cost_kind == LBX_COST_TIMERS)
+  int64_t n_host = 0;
+  int* box = nullptr;
+  int* perm = nullptr;
+  double* zero_v = nullptr;
+  unsigned long long* d_counts = nullptr;
+  unsigned long long* d_cursors = nullptr;
+  unsigned long long* h_counts = nullptr;   // pinned
+  unsigned long long* h_offsets = nullptr;  // pinned
+  std::vector<cudaEvent_t> tb0, tb1;
+  std::vector<double> timers;
 };
 
 namespace {
@@ -85,7 +96,7 @@ int validate(const lbx_sim_config& c) {
   if (c.n_ranks < 1) return set_error(LBX_EINVAL, "n_ranks must be >= 1");
   if (c.total_steps < 1) return set_error(LBX_EINVAL, "total_steps must be >= 1");
   if (c.interval < 1) return set_error(LBX_EINVAL, "interval must be >= 1");
-  if (c.cost_kind < 0 || c.cost_kind > LBX_COST_GPUCLOCK)
+  if (c.cost_kind < 0 || c.cost_kind > LBX_COST_TIMERS)
     return set_error(LBX_EINVAL, "unknown cost kind %d", c.cost_kind);
   return LBX_OK;
 }
@@ -100,7 +111,7 @@ namespace lbx {
 // cost_kind is GPUCLOCK).
 int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device_cost,
             const uint64_t* clk, int64_t n_alive, lbx_sim_outputs* o, int* adopted_out,
-            int* halt) {
+            int* halt, const double* timers = nullptr) {
   const lbx_sim_config& c = s->cfg;
   const int nb = s->nb;
   const int32_t R = c.n_ranks;
@@ -122,6 +133,10 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
     case LBX_COST_GPUCLOCK:
       if (!clk) return set_error(LBX_EINVAL, "GpuClock costs need the clock tally");
       for (int b = 0; b < nb; ++b) cost[b] = (double)clk[b];
+      break;
+    case LBX_COST_TIMERS:
+      if (!timers) return set_error(LBX_EINVAL, "Timers costs need per-box event timings");
+      std::memcpy(cost, timers, sizeof(double) * nb);
       break;
     default:
       return set_error(LBX_EINVAL, "unknown cost kind %d", c.cost_kind);
@@ -215,17 +230,56 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
 
 namespace {
 
+// Timers strategy: per-box push launches bracketed by CUDA events (the
+// paper's CUPTI-style per-kernel timing).  Box-sorts the
+// particle indices first (needs the per-box counts on the host), then the
+// fused kernel runs with zero velocity to count survivors, form the
+// heuristic record and compact the absorbed particles.
+int timers_prepare(lbx_sim* s, const double* vz, const double* vx, cudaStream_t st) {
+  const lbx_sim_config& c = s->lb->cfg;
+  const int nb = s->lb->nb;
+  const long long n = s->n_host;
+  int rc = launch_timers_sort(s->z, s->x, n, (double)c.box_size, s->lb->nbz, s->lb->nbx, s->box,
+                              s->d_counts, s->d_cursors, s->perm, nullptr, st, 0);
+  if (rc) return rc;
+  cudaMemcpyAsync(s->h_counts, s->d_counts, (size_t)nb * 8, cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "timers histogram");
+  unsigned long long acc = 0;
+  for (int b = 0; b < nb; ++b) {
+    s->h_offsets[b] = acc;
+    acc += s->h_counts[b];
+  }
+  rc = launch_timers_sort(s->z, s->x, n, (double)c.box_size, s->lb->nbz, s->lb->nbx, s->box,
+                          s->d_counts, s->d_cursors, s->perm, s->h_offsets, st, 1);
+  if (rc) return rc;
+  for (int b = 0; b < nb; ++b) {
+    const long long cnt = (long long)s->h_counts[b];
+    if (!cnt) continue;
+    cudaEventRecord(s->tb0[b], st);
+    rc = launch_timers_push(s->z, s->x, vz, vx, s->perm + s->h_offsets[b], cnt, st);
+    if (rc) return rc;
+    cudaEventRecord(s->tb1[b], st);
+  }
+  return LBX_OK;
+}
+
 int launch_step(lbx_sim* s, int64_t step, cudaStream_t st) {
   const int slot = (int)(step % s->ring);
   if (s->timing) cudaEventRecord(s->t0[slot], st);
   Rec d = rec_at(s->ring_d, s->rec_bytes, slot, s->lb->nb);
   const lbx_sim_config& c = s->lb->cfg;
   const bool kicked = step >= c.kick_step && s->kvz != nullptr;
+  const bool timers = c.cost_kind == LBX_COST_TIMERS;
+  if (timers) {
+    int rc = timers_prepare(s, kicked ? s->kvz : s->vz, kicked ? s->kvx : s->vx, st);
+    if (rc) return rc;
+  }
   StepLaunch a{};
   a.z = s->z;
   a.x = s->x;
-  a.vz = kicked ? s->kvz : s->vz;
-  a.vx = kicked ? s->kvx : s->vx;
+  a.vz = timers ? s->zero_v : kicked ? s->kvz : s->vz;
+  a.vx = timers ? s->zero_v : kicked ? s->kvx : s->vx;
   a.ez = (double)c.extent_z;
   a.ex = (double)c.extent_x;
   a.m = (double)c.box_size;
@@ -262,7 +316,21 @@ int process_step(lbx_sim* s, int64_t step, lbx_sim_outputs* o, int* halt) {
     return set_error(LBX_ERANGE, "step %lld: %lld survivors fall outside the box grid",
                      (long long)step, (long long)*h.err);
   const bool clock = s->lb->cfg.cost_kind == LBX_COST_GPUCLOCK;
-  return lb_step(s->lb, step, h.counts, h.cost, clock ? h.clk : nullptr, *h.n, o, nullptr, halt);
+  const double* timers = nullptr;
+  if (s->lb->cfg.cost_kind == LBX_COST_TIMERS) {
+    for (int b = 0; b < s->lb->nb; ++b) {
+      float ms = 0.f;
+      if (s->h_counts[b]) cudaEventElapsedTime(&ms, s->tb0[b], s->tb1[b]);
+      s->timers[b] = 1000.0 * (double)ms;  // microseconds
+    }
+    timers = s->timers.data();
+    if (o->clock_trace)  // record the per-box launch times (ns) in the clock trace slot
+      for (int b = 0; b < s->lb->nb; ++b)
+        o->clock_trace[(size_t)step * s->lb->nb + b] = (uint64_t)(s->timers[b] * 1000.0);
+  }
+  s->n_host = *h.n;
+  return lb_step(s->lb, step, h.counts, h.cost, clock ? h.clk : nullptr, *h.n, o, nullptr, halt,
+                 timers);
 }
 
 }  // namespace
@@ -348,7 +416,7 @@ int lbx_sim_create(lbx_sim** out, lbx_ctx* ctx, const lbx_sim_config* cfg) {
   s->ctx = ctx;
   s->lb = lb;
   const int nb = lb->nb;
-  s->ring = cfg->capacity_particles >= 0 ? 1 : 16;
+  s->ring = (cfg->capacity_particles >= 0 || cfg->cost_kind == LBX_COST_TIMERS) ? 1 : 16;
   s->rec_bytes = ((size_t)24 * nb + 16 + 255) & ~(size_t)255;
   cudaError_t e = cudaHostAlloc(&s->ring_h, s->rec_bytes * s->ring, cudaHostAllocMapped);
   if (e != cudaSuccess) {
@@ -385,6 +453,15 @@ int lbx_sim_destroy(lbx_sim* s) {
   for (auto& ev : s->t0) cudaEventDestroy(ev);
   for (auto& ev : s->t1) cudaEventDestroy(ev);
   if (s->ring_h) cudaFreeHost(s->ring_h);
+  for (auto& ev : s->tb0) cudaEventDestroy(ev);
+  for (auto& ev : s->tb1) cudaEventDestroy(ev);
+  cudaFree(s->box);
+  cudaFree(s->perm);
+  cudaFree(s->zero_v);
+  cudaFree(s->d_counts);
+  cudaFree(s->d_cursors);
+  cudaFreeHost(s->h_counts);
+  cudaFreeHost(s->h_offsets);
   delete s->lb;
   delete s;
   return LBX_OK;
@@ -403,6 +480,34 @@ int lbx_sim_set_particles(lbx_sim* s, double* z, double* x, double* vz, double* 
   s->vx = vx;
   s->kvz = kick_vz;
   s->kvx = kick_vx;
+  s->n_host = n;
+  if (s->lb->cfg.cost_kind == LBX_COST_TIMERS) {
+    if (n >= (1ll << 31)) return set_error(LBX_EINVAL, "Timers strategy supports < 2^31 particles");
+    const int nb = s->lb->nb;
+    cudaFree(s->box);
+    cudaFree(s->perm);
+    cudaFree(s->zero_v);
+    s->box = s->perm = nullptr;
+    s->zero_v = nullptr;
+    bool ok = cudaMalloc(&s->box, (size_t)(n + 1) * 4) == cudaSuccess &&
+              cudaMalloc(&s->perm, (size_t)(n + 1) * 4) == cudaSuccess &&
+              cudaMalloc(&s->zero_v, (size_t)(n + 2) * 8) == cudaSuccess;
+    if (ok && !s->d_counts) {
+      ok = cudaMalloc(&s->d_counts, (size_t)nb * 8) == cudaSuccess &&
+           cudaMalloc(&s->d_cursors, (size_t)nb * 8) == cudaSuccess &&
+           cudaHostAlloc(&s->h_counts, (size_t)nb * 8, cudaHostAllocDefault) == cudaSuccess &&
+           cudaHostAlloc(&s->h_offsets, (size_t)nb * 8, cudaHostAllocDefault) == cudaSuccess;
+      s->tb0.resize(nb);
+      s->tb1.resize(nb);
+      for (int b = 0; b < nb; ++b) {
+        cudaEventCreate(&s->tb0[b]);
+        cudaEventCreate(&s->tb1[b]);
+      }
+      s->timers.assign(nb, 0.0);
+    }
+    if (!ok) return set_error(LBX_EOOM, "Timers buffers");
+    cudaMemset(s->zero_v, 0, (size_t)(n + 2) * 8);
+  }
   return lbx_ctx_set_count(s->ctx, n, stream);
 }
 

@@ -325,7 +325,7 @@ def policy_kind(policy: BalancePolicy, total_steps: int) -> str:
 
 def sim_config(cfg: ScenarioConfig, policy: BalancePolicy, provider: CostProvider):
     """Flatten (scenario, policy, provider) into lbx_sim_config."""
-    if provider.device_kind < 0 or provider.device_kind > 3:
+    if provider.device_kind < 0 or provider.device_kind > 4:
         raise ConfigError(f"provider {provider.kind!r} is not supported by the native loop")
     model = resolve_costs(cfg)
     w = getattr(provider, "weights", None)

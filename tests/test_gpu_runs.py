@@ -85,3 +85,24 @@ def test_gpuclock_run_rank_correlates_with_true_work(runs):
         rw = np.argsort(np.argsort(counts[occ]))
         rho = np.corrcoef(rc, rw)[0, 1]
         assert rho > 0.9, (s, rho)
+
+
+def test_timers_run_keeps_reference_state(runs):
+    """Timers strategy (per-box launches + events): particle state and counts
+    stay bit-exact with the reference (in-place push by index + stable
+    compaction); costs are positive exactly on occupied boxes."""
+    from paper_2104_11385_b200 import scenarios as S
+    from paper_2104_11385_b200.workload import run_simulation
+    spec = S.apply_overrides(S.load_spec("tight-memory"), cost="timers", steps=80)
+    res = run_simulation(spec.scenario, spec.policy, spec.build_provider(),
+                         record_counts=True)
+    from oracle import lbsim_oracle as O
+    from tests.scenario_util import preset_doc
+    cfg = O.config_from_doc(preset_doc("tight-memory"))
+    cfg["steps"] = 80
+    ref = O.run_simulation(cfg, record_counts=True)
+    assert np.array_equal(res.count_trace, ref["count_trace"][:len(res.count_trace)])
+    assert ((res.cost_trace > 0) == (ref["count_trace"][:len(res.cost_trace)] > 0)).all()
+    if res.summary["completed_steps"] == 80:
+        pos, vel = res.final_state.to_numpy()
+        assert np.array_equal(pos, ref["final_pos"]) and np.array_equal(vel, ref["final_vel"])
