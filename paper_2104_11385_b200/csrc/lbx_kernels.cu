@@ -755,25 +755,72 @@ __global__ void heuristic_kernel(const double* __restrict__ particles,
 }
 
 // ---- Timers strategy (per-box launches) ----
-__global__ void timers_box_kernel(const double* __restrict__ z, const double* __restrict__ x,
-                                  long long n, double m, int nbz, int nbx,
-                                  int* __restrict__ box, unsigned long long* __restrict__ counts) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    int bz = (int)__ddiv_rn(z[i], m), bx = (int)__ddiv_rn(x[i], m);
-    bz = min(max(bz, 0), nbz - 1);  // live particles are in the domain
-    bx = min(max(bx, 0), nbx - 1);
-    const int b = bz * nbx + bx;
-    box[i] = b;
-    atomicAdd(counts + b, 1ull);
-  }
+// Box sort of particle indices.  Particles are spatially coherent, so most
+// warps sit in one box: counts use a shared histogram with warp-aggregated
+// updates (__match_any_sync), and the scatter reserves each box's range once
+// per CTA chunk, then hands out slots with shared-memory atomics.
+constexpr int kSortChunk = kBlock * 16;
+
+__device__ __forceinline__ int box_of(double z, double x, double m, int nbz, int nbx) {
+  int bz = (int)__ddiv_rn(z, m), bx = (int)__ddiv_rn(x, m);
+  bz = min(max(bz, 0), nbz - 1);  // live particles are in the domain
+  bx = min(max(bx, 0), nbx - 1);
+  return bz * nbx + bx;
 }
 
-__global__ void timers_scatter_kernel(const int* __restrict__ box, long long n,
-                                      unsigned long long* cursors, int* __restrict__ perm) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    perm[atomicAdd(cursors + box[i], 1ull)] = (int)i;
+__global__ void __launch_bounds__(kBlock) timers_box_kernel(
+    const double* __restrict__ z, const double* __restrict__ x, long long n, double m, int nbz,
+    int nbx, int* __restrict__ box, unsigned long long* __restrict__ counts) {
+  extern __shared__ unsigned s_hist[];
+  const int nb = nbz * nbx;
+  for (int b = threadIdx.x; b < nb; b += kBlock) s_hist[b] = 0u;
+  __syncthreads();
+  const long long stride = (long long)gridDim.x * kBlock;
+  const long long n_up = (n + kBlock - 1) / kBlock * kBlock;
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n_up; i += stride) {
+    const bool ok = i < n;
+    const int b = ok ? box_of(z[i], x[i], m, nbz, nbx) : -1;
+    if (ok) box[i] = b;
+    const unsigned grp = __match_any_sync(kFull, b);
+    if (ok && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(s_hist + b, (unsigned)__popc(grp));
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += kBlock)
+    if (s_hist[b]) atomicAdd(counts + b, (unsigned long long)s_hist[b]);
+}
+
+__global__ void __launch_bounds__(kBlock) timers_scatter_kernel(
+    const int* __restrict__ box, long long n, int nb, unsigned long long* cursors,
+    int* __restrict__ perm) {
+  extern __shared__ unsigned long long s_base[];
+  const int lane = threadIdx.x & 31;
+  for (long long c0 = (long long)blockIdx.x * kSortChunk; c0 < n;
+       c0 += (long long)gridDim.x * kSortChunk) {
+    for (int b = threadIdx.x; b < nb; b += kBlock) s_base[b] = 0ull;
+    __syncthreads();
+    const long long c1 = min(n, c0 + kSortChunk);
+    for (long long i = c0 + threadIdx.x; i < c0 + kSortChunk; i += kBlock) {
+      const int b = i < c1 ? box[i] : -1;
+      const unsigned grp = __match_any_sync(kFull, b);
+      if (b >= 0 && lane == __ffs(grp) - 1) atomicAdd(s_base + b, (unsigned long long)__popc(grp));
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += kBlock) {
+      const unsigned long long c = s_base[b];
+      if (c) s_base[b] = atomicAdd(cursors + b, c);  // reserve this chunk's range
+    }
+    __syncthreads();
+    for (long long i = c0 + threadIdx.x; i < c0 + kSortChunk; i += kBlock) {
+      const int b = i < c1 ? box[i] : -1;
+      const unsigned grp = __match_any_sync(kFull, b);
+      const int leader = __ffs(grp) - 1;
+      unsigned long long base = 0;
+      if (b >= 0 && lane == leader) base = atomicAdd(s_base + b, (unsigned long long)__popc(grp));
+      base = __shfl_sync(kFull, base, leader);
+      if (b >= 0) perm[base + __popc(grp & lanemask_lt())] = (int)i;
+    }
+    __syncthreads();
+  }
 }
 
 // Push the particles of one box (gather by index); absorbed ones are left
@@ -1008,13 +1055,28 @@ int launch_timers_sort(const double* z, const double* x, long long n, double m, 
                        int* perm, const unsigned long long* offsets_host, void* stream,
                        int phase) {
   cudaStream_t s = (cudaStream_t)stream;
-  const unsigned grid = (unsigned)std::max(1ll, std::min(4096ll, (n + 255) / 256));
+  const int nb = nbz * nbx;
+  if (nb > kSmemBoxesMax / 2) return set_error(LBX_EINVAL, "Timers strategy supports <= %d boxes",
+                                               kSmemBoxesMax / 2);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (phase == 0) {
-    cudaMemsetAsync(counts, 0, (size_t)nbz * nbx * 8, s);
-    if (n) timers_box_kernel<<<grid, 256, 0, s>>>(z, x, n, m, nbz, nbx, box, counts);
+    cudaMemsetAsync(counts, 0, (size_t)nb * 8, s);
+    const size_t smem = (size_t)nb * 4;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(timers_box_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const unsigned grid = (unsigned)std::max(1ll, std::min((long long)sms * 4, (n + kBlock - 1) / kBlock));
+    if (n) timers_box_kernel<<<grid, kBlock, smem, s>>>(z, x, n, m, nbz, nbx, box, counts);
   } else {
-    cudaMemcpyAsync(cursors, offsets_host, (size_t)nbz * nbx * 8, cudaMemcpyHostToDevice, s);
-    if (n) timers_scatter_kernel<<<grid, 256, 0, s>>>(box, n, cursors, perm);
+    cudaMemcpyAsync(cursors, offsets_host, (size_t)nb * 8, cudaMemcpyHostToDevice, s);
+    const size_t smem = (size_t)nb * 8;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(timers_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+    const unsigned grid =
+        (unsigned)std::max(1ll, std::min((long long)sms * 4, (n + kSortChunk - 1) / kSortChunk));
+    if (n) timers_scatter_kernel<<<grid, kBlock, smem, s>>>(box, n, nb, cursors, perm);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "timers sort launch");

@@ -183,8 +183,7 @@ class DeviceEngine:
         _lib.check(_lib.lib.lbx_push_step_exchange(self.ctx.handle, C.byref(args), C.byref(ex),
                                                    self.D._stream(self.dev)))
         self.launches += 3   # set_count, stream kernel, compaction
-        self._after()
-        return self.counts, self.clk, self.send_counts
+        return self.counts, self.clk, self.send_counts, self.nout
 
     def partition(self):
         self.send_counts.zero_()
@@ -195,15 +194,14 @@ class DeviceEngine:
             _lib.ptr(self.vx), self.ez, self.ex, self.m, self.nbz, self.nbx, C.byref(ex),
             _lib.ptr(self.nout), self.D._stream(self.dev)))
         self.launches += 3
-        self._after()
-        return self.send_counts
+        return self.send_counts, self.nout
 
-    def _after(self):
-        h = self.nout.cpu().numpy()
-        if h[1] != 0:
+    def commit(self, nout_host):
+        """Adopt the local count left by push/partition (host copy of nout)."""
+        if int(nout_host[1]) != 0:
             raise ValueError("particles outside the box grid or staging overflow "
-                             f"(code {int(h[1])})")
-        self.n = int(h[0])
+                             f"(code {int(nout_host[1])})")
+        self.n = int(nout_host[0])
 
     def pack(self, sc: list) -> torch.Tensor:
         total = int(sum(sc))
@@ -324,43 +322,68 @@ class DistributedSimulation:
         except Exception:
             pass
 
-    def _exchange(self, send_counts) -> int:
-        recv_counts = self.comm.exchange_counts(send_counts)
-        sc = [int(v) for v in send_counts.cpu().tolist()]
-        rc = [int(v) for v in recv_counts.cpu().tolist()]
+    def _records(self, sc, rc):
+        """All-to-all of the staged records given host split sizes."""
         send = self.engine.pack(sc)
         recv = self.comm.exchange_records(send, sc, rc)
         self.engine.unpack(recv)
+
+    def _migrate(self):
+        """Adoption-time redistribution: stage the particles of lost boxes,
+        one counts exchange + one host copy, then the record all-to-all."""
+        send_counts, nout = self.engine.partition()
+        total = send_counts.sum().reshape(1)
+        self.comm.all_reduce_sum(total)
+        recv_counts = self.comm.exchange_counts(send_counts)
+        h = torch.cat([nout, total, send_counts, recv_counts]).cpu().numpy()
+        self.engine.commit(h[:2])
+        w = self.world
+        sc, rc = [int(v) for v in h[3:3 + w]], [int(v) for v in h[3 + w:3 + 2 * w]]
+        if int(h[2]):
+            self._records(sc, rc)
         return sum(sc)
 
     def run(self, first=None, last=None):
+        """Steps [first, last).  Per step: push (no host sync), one all-reduce
+        of [counts, clock tally, global emigrant count], one all-to-all of
+        per-destination counts, ONE device->host copy, then the record
+        all-to-all only if some rank has emigrants, then the host LB step."""
         cfg = self.cfg
         first = self.done if first is None else first
         last = cfg.total_steps if last is None else last
         w = getattr(self.provider, "weights", None)
         wp, wc = (w.w_particle, w.w_cell) if w else (0.75, 0.25)
         clock = self.provider.device_kind == 3
+        nb, W = self.ba.n_boxes, self.world
         adopted, halt = C.c_int32(), C.c_int32()
         for step in range(first, last):
             if self.halted:
                 break
             if step == cfg.kick.step:
                 self.engine.kick()
-            counts, clk, send_counts = self.engine.push(wp, wc)
-            self.comm.all_reduce_sum(counts)
-            if clock:
-                self.comm.all_reduce_sum(clk)
-            self._exchange(send_counts)
-            ch = np.ascontiguousarray(counts.cpu().numpy(), dtype=np.int64)
-            kh = np.ascontiguousarray(clk.cpu().numpy()).view(np.uint64) if clock else None
+            counts, clk, send_counts, nout = self.engine.push(wp, wc)
+            parts = [counts, clk] if clock else [counts]
+            red = torch.cat(parts + [send_counts.sum().reshape(1)])
+            self.comm.all_reduce_sum(red)
+            recv_counts = self.comm.exchange_counts(send_counts)
+            h = torch.cat([red, nout, send_counts, recv_counts]).cpu().numpy()
+            k = len(parts) * nb
+            ch = np.ascontiguousarray(h[:nb], dtype=np.int64)
+            kh = np.ascontiguousarray(h[nb:2 * nb]).view(np.uint64) if clock else None
+            emigrants = int(h[k])
+            self.engine.commit(h[k + 1:k + 3])
+            sc = [int(v) for v in h[k + 3:k + 3 + W]]
+            rc = [int(v) for v in h[k + 3 + W:k + 3 + 2 * W]]
+            if emigrants:
+                self._records(sc, rc)
             _lib.check(_lib.lib.lbx_lb_step(self.lb, step, _lib.ptr(ch), _lib.ptr(kh),
                                             int(ch.sum()), C.byref(self.souts),
                                             C.byref(adopted), C.byref(halt)))
             if adopted.value:
-                owner = np.empty(self.ba.n_boxes, dtype=np.int64)
+                owner = np.empty(nb, dtype=np.int64)
                 _lib.check(_lib.lib.lbx_lb_owner(self.lb, _lib.ptr(owner)))
                 self.engine.set_owner(owner)
-                self.moved[step] = self._exchange(self.engine.partition())
+                self.moved[step] = self._migrate()
             self.done = step + 1
             if halt.value:
                 self.halted = True

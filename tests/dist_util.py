@@ -64,11 +64,15 @@ class NumpyEngine:
         counts = np.bincount(box[alive], minlength=self.nbz * self.nbx).astype(np.int64)
         send = np.bincount(self.dest, minlength=self.world).astype(np.int64)
         return (torch.from_numpy(counts), torch.zeros(counts.size, dtype=torch.int64),
-                torch.from_numpy(send))
+                torch.from_numpy(send), torch.tensor([self.n, 0], dtype=torch.int64))
 
     def partition(self):
         self._split(self.pos.copy(), np.ones(self.n, dtype=bool))
-        return torch.from_numpy(np.bincount(self.dest, minlength=self.world).astype(np.int64))
+        return (torch.from_numpy(np.bincount(self.dest, minlength=self.world).astype(np.int64)),
+                torch.tensor([self.n, 0], dtype=torch.int64))
+
+    def commit(self, nout_host):
+        assert int(nout_host[0]) == self.n
 
     def pack(self, sc):
         order = np.argsort(self.dest, kind="stable")
