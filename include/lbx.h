@@ -274,6 +274,43 @@ int lbx_sim_run(lbx_sim* sim, int64_t first, int64_t last,
 int lbx_sim_particles(lbx_sim* sim, int64_t* n, void* stream);
 
 /* ------------------------------------------------------------------------
+ * 2D3V electromagnetic PIC step (SURVEY 8a row a15 / north-star item 1; not
+ * in the reference, parity unpinned -- checked against oracle/pic_oracle.py
+ * at a stated tolerance).  Particles SoA float64 z, x, uz, ux, uy (u = gamma
+ * v, c = 1, unit cells), 16-byte aligned, capacity >= n + 2, count in the
+ * context as for lbx_push_step.  Fields float32 on a Yee grid with one zero
+ * guard layer: arrays of (nz+2) x (nx+2), cell (i, j) at [(i+1)*(nx+2) + j+1];
+ * fields[] = {Ex, Ey, Ez, Bx, By, Bz}, current[] = {Jx, Jy, Jz} (zero on
+ * entry, consumed).  One call: field gather + Boris push + absorb + current
+ * deposition (shared-memory staged per 1024-particle tile) + per-box counts /
+ * heuristic cost / GpuClock tally + stable compaction + Yee field update.
+ * ---------------------------------------------------------------------- */
+#define LBX_PIC_NO_FIELD_SOLVE 2u  /* skip the Yee update (tests)         */
+
+typedef struct lbx_pic_args {
+  double* z;
+  double* x;
+  double* uz;
+  double* ux;
+  double* uy;
+  float* fields[6];
+  float* current[3];
+  int32_t nz, nx;             /* grid (cells) == particle domain            */
+  int32_t box_size;           /* power of two dividing nz and nx            */
+  double q_over_m, q_times_w; /* species charge/mass, charge x macro weight */
+  double dt;                  /* < 1/sqrt(2)                                */
+  double w_particle, w_cell;  /* heuristic weights for cost_out             */
+  uint32_t flags;             /* LBX_STEP_CLOCK | LBX_PIC_NO_FIELD_SOLVE    */
+  int64_t* counts_out;
+  double* cost_out;
+  uint64_t* clk_out;
+  int64_t* n_out;
+  int64_t* err_out;
+} lbx_pic_args;
+
+int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* args, void* stream);
+
+/* ------------------------------------------------------------------------
  * Multi-GPU: box ownership -> GPU.  Each rank holds the particles
  * of the boxes it owns.  A particle whose new box belongs to another rank is
  * copied into the staging buffer as a 6-double record (z, x, vz, vx, kick_vz,

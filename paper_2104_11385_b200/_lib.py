@@ -110,6 +110,20 @@ SIGNATURES.update({
                                    vp, vp, P(i64)]),
 })
 RECORD_DOUBLES = 6
+LBX_PIC_NO_FIELD_SOLVE = 2
+
+
+class PicArgs(C.Structure):
+    """lbx_pic_args (include/lbx.h)."""
+    _fields_ = [("z", vp), ("x", vp), ("uz", vp), ("ux", vp), ("uy", vp),
+                ("fields", vp * 6), ("current", vp * 3), ("nz", i32), ("nx", i32),
+                ("box_size", i32), ("q_over_m", f64), ("q_times_w", f64), ("dt", f64),
+                ("w_particle", f64), ("w_cell", f64), ("flags", u32),
+                ("counts_out", vp), ("cost_out", vp), ("clk_out", vp), ("n_out", vp),
+                ("err_out", vp)]
+
+
+SIGNATURES["lbx_pic_step"] = (i32, [vp, P(PicArgs), vp])
 
 
 class LBXError(RuntimeError):

@@ -77,6 +77,12 @@ int measured_cost(const double* work, int64_t n, double amplitude, uint64_t seed
 int launch_push_step(lbx_ctx* ctx, const StepLaunch& a, void* stream,
                      const lbx_exchange_args* ex = nullptr, bool push = true);
 int ensure_accumulators(lbx_ctx* ctx, int32_t nboxes);
+// In-place stable compaction of particles whose (z, x) left the domain, as
+// recorded by the preceding push (st->leavers / first_leaver); carries up to
+// four more per-particle arrays (a..d, each may be NULL).
+int launch_compact(lbx_ctx* ctx, double* z, double* x, double* a, double* b, double* c,
+                   double* d, double ez, double ex, void* stream);
+int reserve_status(lbx_ctx* ctx, int64_t capacity);
 // Timers strategy helpers (lbx_kernels.cu): phase 0 = box ids + counts,
 // phase 1 = scatter indices into per-box segments (offsets from the host).
 int launch_timers_sort(const double* z, const double* x, long long n, double m, int nbz, int nbx,

@@ -539,13 +539,14 @@ __global__ void __launch_bounds__(kBlock, kMode == kCompactSoA ? 2 : 3) scan_ker
         pvx[2 * r] = d.x;
         pvx[2 * r + 1] = d.y;
         if (p.kvz) {
-          double2 e = make_double2(0.0, 0.0), f = e;
-          if (i0 < n) {
-            e = __ldcs(reinterpret_cast<const double2*>(p.kvz) + q);
-            f = __ldcs(reinterpret_cast<const double2*>(p.kvx) + q);
-          }
+          double2 e = make_double2(0.0, 0.0);
+          if (i0 < n) e = __ldcs(reinterpret_cast<const double2*>(p.kvz) + q);
           pkz[2 * r] = e.x;
           pkz[2 * r + 1] = e.y;
+        }
+        if (p.kvx) {
+          double2 f = make_double2(0.0, 0.0);
+          if (i0 < n) f = __ldcs(reinterpret_cast<const double2*>(p.kvx) + q);
           pkx[2 * r] = f.x;
           pkx[2 * r + 1] = f.y;
         }
@@ -650,10 +651,8 @@ __global__ void __launch_bounds__(kBlock, kMode == kCompactSoA ? 2 : 3) scan_ker
             p.x[d] = px[k];
             p.vz[d] = pvz[k];
             p.vx[d] = pvx[k];
-            if (p.kvz) {
-              p.kvz[d] = pkz[k];
-              p.kvx[d] = pkx[k];
-            }
+            if (p.kvz) p.kvz[d] = pkz[k];
+            if (p.kvx) p.kvx[d] = pkx[k];
           }
         }
       }
@@ -939,6 +938,8 @@ int launch_scan(lbx_ctx* ctx, const ScanParams& p, long long n_upper, cudaStream
   return LBX_OK;
 }
 
+}  // namespace
+
 int reserve_status(lbx_ctx* ctx, int64_t capacity) {
   const int64_t tiles = (capacity + kTile - 1) / kTile + 1;
   if (tiles <= ctx->status_tiles) return LBX_OK;
@@ -960,6 +961,8 @@ int reserve_status(lbx_ctx* ctx, int64_t capacity) {
   ctx->status_tiles = tiles;
   return LBX_OK;
 }
+
+namespace {
 
 }  // namespace
 
@@ -1049,6 +1052,24 @@ bool is_pow2(double m) {
 }
 
 }  // namespace
+
+int launch_compact(lbx_ctx* ctx, double* z, double* x, double* a, double* b, double* c,
+                   double* d, double ez, double ex, void* stream) {
+  int rc = reserve_status(ctx, ctx->n_upper);
+  if (rc) return rc;
+  ScanParams p{};
+  p.z = z;
+  p.x = x;
+  p.vz = a;
+  p.vx = b;
+  p.kvz = c;
+  p.kvx = d;
+  p.ez = ez;
+  p.ex = ex;
+  p.st = ctx->st;
+  p.status = ctx->status;
+  return launch_scan<kCompactSoA>(ctx, p, ctx->n_upper, (cudaStream_t)stream);
+}
 
 int launch_timers_sort(const double* z, const double* x, long long n, double m, int nbz, int nbx,
                        int* box, unsigned long long* counts, unsigned long long* cursors,

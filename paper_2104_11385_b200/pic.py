@@ -1,0 +1,91 @@
+"""2D3V electromagnetic PIC step on the device.
+
+The paper's per-box work is a WarpX PIC step: field gather, Lorentz (Boris)
+push, current deposition, field solve.  The
+reference only models it as ballistic motion, so this physics is the
+builder's own (checked against oracle/pic_oracle.py, parity unpinned).  The
+per-box counts / GpuClock tallies it produces feed the same balancer.
+See include/lbx.h (lbx_pic_step) for conventions.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import Context, _stream, require_cuda
+
+FIELD_NAMES = ("Ex", "Ey", "Ez", "Bx", "By", "Bz")
+CURRENT_NAMES = ("Jx", "Jy", "Jz")
+
+
+@dataclass
+class PicState:
+    z: torch.Tensor
+    x: torch.Tensor
+    uz: torch.Tensor
+    ux: torch.Tensor
+    uy: torch.Tensor
+    n: int
+    fields: dict
+    nz: int
+    nx: int
+
+    @classmethod
+    def create(cls, pos, u, nz, nx, device="cuda:0"):
+        dev = require_cuda(device)
+        pos = np.asarray(pos, dtype=np.float64).reshape(-1, 2)
+        u = np.asarray(u, dtype=np.float64).reshape(-1, 3)   # (uz, ux, uy)
+        n = pos.shape[0]
+        arrs = []
+        for col in (pos[:, 0], pos[:, 1], u[:, 0], u[:, 1], u[:, 2]):
+            t = torch.zeros(n + 2, dtype=torch.float64, device=dev)
+            t[:n].copy_(torch.from_numpy(np.ascontiguousarray(col)))
+            arrs.append(t)
+        fields = {k: torch.zeros((nz + 2, nx + 2), dtype=torch.float32, device=dev)
+                  for k in FIELD_NAMES + CURRENT_NAMES}
+        return cls(*arrs, n=n, fields=fields, nz=nz, nx=nx)
+
+    def particles(self):
+        n = self.n
+        return {k: getattr(self, k)[:n].cpu().numpy() for k in ("z", "x", "uz", "ux", "uy")}
+
+    def field_arrays(self):
+        return {k: v.cpu().numpy() for k, v in self.fields.items()}
+
+
+def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times_w: float,
+             dt: float, weights=(0.75, 0.25), clock=False, field_solve=True):
+    """One PIC step in place; returns per-box counts / cost / clock and n."""
+    dev = ctx.device
+    nbz, nbx = st.nz // box_size, st.nx // box_size
+    nb = nbz * nbx
+    counts = torch.empty(nb, dtype=torch.int64, device=dev)
+    cost = torch.empty(nb, dtype=torch.float64, device=dev)
+    clk = torch.zeros(nb, dtype=torch.int64, device=dev)
+    nout = torch.zeros(2, dtype=torch.int64, device=dev)
+    ctx.set_count(st.n)
+    a = _lib.PicArgs()
+    a.z, a.x, a.uz, a.ux, a.uy = (_lib.ptr(getattr(st, k)) for k in ("z", "x", "uz", "ux", "uy"))
+    for i, k in enumerate(FIELD_NAMES):
+        a.fields[i] = _lib.ptr(st.fields[k])
+    for i, k in enumerate(CURRENT_NAMES):
+        a.current[i] = _lib.ptr(st.fields[k])
+    a.nz, a.nx, a.box_size = st.nz, st.nx, int(box_size)
+    a.q_over_m, a.q_times_w, a.dt = float(q_over_m), float(q_times_w), float(dt)
+    a.w_particle, a.w_cell = float(weights[0]), float(weights[1])
+    a.flags = (_lib.LBX_STEP_CLOCK if clock else 0) | (0 if field_solve else
+                                                        _lib.LBX_PIC_NO_FIELD_SOLVE)
+    a.counts_out, a.cost_out, a.clk_out = _lib.ptr(counts), _lib.ptr(cost), _lib.ptr(clk)
+    a.n_out, a.err_out = _lib.ptr(nout), _lib.ptr(nout[1:])
+    _lib.check(_lib.lib.lbx_pic_step(ctx.handle, C.byref(a), _stream(dev)))
+    h = nout.cpu().numpy()
+    if h[1]:
+        raise ValueError(f"{int(h[1])} particles fell outside the box grid")
+    st.n = int(h[0])
+    return dict(counts=counts.cpu().numpy(), cost=cost.cpu().numpy(),
+                clock=clk.cpu().numpy().view(np.uint64), n=st.n)
