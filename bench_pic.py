@@ -1,0 +1,88 @@
+#!/usr/bin/env python
+"""PIC push + deposit benchmark (north-star item 1; SURVEY 8d "PIC extension").
+
+Workload: the C2 blob (default.yaml geometry: 960x960 cells, 32-cell boxes,
+801,499 particles sampled with the reference's stream) tiled R times
+(default 128 -> 102.6 M macro-particles), momenta from the C2 kick velocity
+(u = v/dt), electrons (q/m = -1), dt = 0.5, GpuClock tally on.  Timed with
+CUDA events on the launch stream:
+  push_deposit  lbx_pic_step with LBX_PIC_NO_FIELD_SOLVE (gather + Boris +
+                deposit + counts/clock + compaction), and
+  full_step     the same plus the Yee update.
+Roofline: HBM, algorithmic bytes = 80 B per particle (read z,x,uz,ux,uy +
+write them, float64) -- field patch and current flush traffic is counted
+separately from ncu (profiles/).  Prints one JSON object.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BYTES_PER_PARTICLE = 80
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--replicas", type=int, default=128)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    args = ap.parse_args()
+
+    import torch
+
+    import bench
+    from paper_2104_11385_b200 import device, pic
+
+    dev = torch.device("cuda:0")
+    spec, sc = bench.c2_spec(1, 10, "gpuclock")
+    pos0, kick0 = bench.base_particles(spec)
+    dt = 0.5
+    u0 = np.column_stack([kick0[:, 0] / dt, kick0[:, 1] / dt, np.zeros(len(kick0))])
+    R = args.replicas
+    n = pos0.shape[0] * R
+    nz, nx = sc.domain_extent
+    st = pic.PicState.create(pos0[:1], u0[:1], nz, nx, device=dev)
+    # tile on the device (host arrays of 100 M particles are not needed)
+    for name, col in (("z", pos0[:, 0]), ("x", pos0[:, 1]), ("uz", u0[:, 0]), ("ux", u0[:, 1]),
+                      ("uy", u0[:, 2])):
+        t = torch.zeros(n + 2, dtype=torch.float64, device=dev)
+        t[:n].copy_(torch.from_numpy(np.ascontiguousarray(col)).to(dev).repeat(R))
+        setattr(st, name, t)
+    st.n = n
+    ctx = device.Context(dev, capacity=n)
+    peak, peak_src = bench.peaks()
+    out = {"workload": f"C2 blob x{R} replicas = {n} particles, 960x960 Yee grid, "
+                       f"box 32, dt {dt}, q/m -1, GpuClock on", "particles": n}
+    stream = torch.cuda.current_stream(dev)
+    for mode, solve in (("push_deposit", False), ("full_step", True)):
+        for _ in range(args.warmup):
+            pic.pic_step(ctx, st, sc.box_size, -1.0, -1e-4, dt, clock=True, field_solve=solve)
+        times = []
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            n_before = st.n
+            e0.record(stream)
+            pic.pic_step(ctx, st, sc.box_size, -1.0, -1e-4, dt, clock=True, field_solve=solve)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            times.append((e0.elapsed_time(e1), n_before))
+        ms = float(np.mean([t for t, _ in times]))
+        nb = float(np.mean([k for _, k in times]))
+        achieved = BYTES_PER_PARTICLE * nb / (ms / 1e3) / 1e9
+        out[mode] = {"ms": ms, "pushes_per_s": nb / (ms / 1e3), "achieved_gbs": achieved,
+                     "frac_of_hbm_peak": achieved / peak}
+    out["peak_gbs"] = peak
+    out["peak_source"] = peak_src
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -83,7 +83,7 @@ def test_multi_step_with_field_solve(clustered):
 
 
 def test_absorption_and_compaction_keep_order():
-    pos, u = setup(30_000, 32, 32, seed=3, speed=2.0)
+    pos, u = setup(30_000, 32, 32, seed=3, speed=2.0, clustered=False)
     st, f, p, outs = run_both(pos, u, 32, 32, steps=4, field_solve=False)
     g = st.particles()
     assert st.n == p["z"].size < 30_000
