@@ -218,7 +218,14 @@ typedef struct lbx_sim_config {
   /* walltime model (workload.py:72-86, resolved) */
   double comm_per_face, gather, redistribute_per_particle, redistribute_latency;
   int64_t capacity_particles;  /* -1 = unlimited                              */
+  /* per-step physics: LBX_PHYSICS_SURROGATE (the reference's ballistic
+   * advance) or LBX_PHYSICS_PIC (lbx_pic_step; needs lbx_sim_set_fields) */
+  int32_t physics;
+  double pic_dt, pic_q_over_m, pic_q_times_w;
 } lbx_sim_config;
+
+#define LBX_PHYSICS_SURROGATE 0
+#define LBX_PHYSICS_PIC 1
 
 /* Per-step outputs, host arrays of length total_steps (caller-owned). */
 typedef struct lbx_sim_outputs {
@@ -267,6 +274,9 @@ int lbx_sim_destroy(lbx_sim* sim);
 int lbx_sim_set_particles(lbx_sim* sim, double* z, double* x, double* vz,
                           double* vx, double* kick_vz, double* kick_vx,
                           int64_t n, void* stream);
+/* PIC physics: Yee field arrays (as lbx_pic_args) and the uy momentum array;
+ * the velocity / kick buffers of lbx_sim_set_particles hold uz, ux. */
+int lbx_sim_set_fields(lbx_sim* sim, float* const* fields, float* const* current, double* uy);
 /* Run steps [first, last) of the loop; outputs indexed by absolute step. */
 int lbx_sim_run(lbx_sim* sim, int64_t first, int64_t last,
                 lbx_sim_outputs* out, void* stream);

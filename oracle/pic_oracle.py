@@ -15,7 +15,11 @@ macro weight w):
   gather  linear (CIC) interpolation of every component at its own stagger.
   push    relativistic Boris rotation, then z += dt uz/gamma, x += dt ux/gamma.
   absorb  particles leaving [0, Nz) x [0, Nx) are removed (as in lbsim).
-  deposit direct: J_c += q w v_c S(new position) at the component's stagger.
+  deposit direct: J_c += q w v_c S(new position) at the component's stagger;
+          every node contribution is quantised to fixed point with a
+          power-of-two scale (exact scaling, round half to even) and summed as
+          integers -- order-independent, so the GPU's atomics reproduce it
+          bit for bit; J = float32(sum / scale).
   field   B -= dt curl E ; E += dt (curl B - J) on interior nodes.
 """
 
@@ -54,26 +58,35 @@ def gather(f, comp, z, x):
             + fz * ((1 - fx) * g(1, 0) + fx * g(1, 1)))
 
 
+def current_scale(qw):
+    """Power-of-two fixed-point scale: a single particle's largest node
+    contribution (|qw|) maps to <= 2^20, so 1024-particle tile sums fit int32."""
+    _, e = np.frexp(2.0 ** 20 / abs(qw))     # exact floor(log2(.)) = e - 1
+    return float(2.0 ** (int(e) - 1))
+
+
 def boris(uz, ux, uy, E, B, qm, dt):
     """E, B dicts of per-particle float64 values; returns new (uz, ux, uy)."""
     h = 0.5 * qm * dt
     mx, my, mz = ux + h * E["Ex"], uy + h * E["Ey"], uz + h * E["Ez"]
     g = np.sqrt(1.0 + mx * mx + my * my + mz * mz)
-    tx, ty, tz = h * B["Bx"] / g, h * B["By"] / g, h * B["Bz"] / g
+    ig = 1.0 / g
+    tx, ty, tz = h * B["Bx"] * ig, h * B["By"] * ig, h * B["Bz"] * ig
     s = 2.0 / (1.0 + tx * tx + ty * ty + tz * tz)
     px, py, pz = mx + (my * tz - mz * ty), my + (mz * tx - mx * tz), mz + (mx * ty - my * tx)
     qx, qy, qz = mx + s * (py * tz - pz * ty), my + s * (pz * tx - px * tz), mz + s * (px * ty - py * tx)
     return qz + h * E["Ez"], qx + h * E["Ex"], qy + h * E["Ey"]
 
 
-def deposit(f, comp, z, x, val):
+def deposit(f, comp, z, x, val, scale):
     oz, ox = {"Jx": OFFSETS["Ex"], "Jy": OFFSETS["Ey"], "Jz": OFFSETS["Ez"]}[comp]
     i0, j0, fz, fx = _stencil(z, x, oz, ox)
-    acc = np.zeros(f[comp].shape, dtype=np.float64)
+    acc = np.zeros(f[comp].shape, dtype=np.int64)
     for di, wz in ((0, 1 - fz), (1, fz)):
         for dj, wx in ((0, 1 - fx), (1, fx)):
-            np.add.at(acc, (i0 + 1 + di, j0 + 1 + dj), val * wz * wx)
-    f[comp] += acc.astype(np.float32)
+            q = np.rint((val * wz * wx) * scale).astype(np.int64)
+            np.add.at(acc, (i0 + 1 + di, j0 + 1 + dj), q)
+    f[comp] += (acc.astype(np.float64) / scale).astype(np.float32)
 
 
 def particle_step(f, p, nz, nx, qm, qw, dt):
@@ -84,13 +97,15 @@ def particle_step(f, p, nz, nx, qm, qw, dt):
     B = {k: gather(f, k, z, x) for k in B_COMPS}
     uz, ux, uy = boris(p["uz"], p["ux"], p["uy"], E, B, qm, dt)
     gam = np.sqrt(1.0 + ux * ux + uy * uy + uz * uz)
-    zn, xn = z + dt * uz / gam, x + dt * ux / gam
+    ig = 1.0 / gam
+    zn, xn = z + dt * uz * ig, x + dt * ux * ig
     keep = (zn >= 0) & (zn < nz) & (xn >= 0) & (xn < nx)
     for k, v in (("z", zn), ("x", xn), ("uz", uz), ("ux", ux), ("uy", uy)):
         p[k] = v[keep]
-    g = gam[keep]
+    g = ig[keep]
+    sc = current_scale(qw)
     for comp, u in (("Jx", p["ux"]), ("Jy", p["uy"]), ("Jz", p["uz"])):
-        deposit(f, comp, p["z"], p["x"], qw * u / g)
+        deposit(f, comp, p["z"], p["x"], qw * u * g, sc)
     return keep
 
 

@@ -44,7 +44,8 @@ class SimConfig(C.Structure):
                 ("work_wp", f64), ("work_wc", f64),
                 ("comm_per_face", f64), ("gather", f64),
                 ("redistribute_per_particle", f64), ("redistribute_latency", f64),
-                ("capacity_particles", i64)]
+                ("capacity_particles", i64), ("physics", i32), ("pic_dt", f64),
+                ("pic_q_over_m", f64), ("pic_q_times_w", f64)]
 
 
 class SimOutputs(C.Structure):
@@ -124,6 +125,7 @@ class PicArgs(C.Structure):
 
 
 SIGNATURES["lbx_pic_step"] = (i32, [vp, P(PicArgs), vp])
+SIGNATURES["lbx_sim_set_fields"] = (i32, [vp, vp, vp, vp])
 
 
 class LBXError(RuntimeError):

@@ -60,6 +60,8 @@ struct lbx_ctx {
   int grid_override = 0;
   int64_t* host_scratch = nullptr;    // pinned
   lbx::HostPipe* pipe = nullptr;      // lbx_advance_bin_host lanes (lazy)
+  unsigned long long* pic_acc = nullptr;  // PIC fixed-point current [3][cells]
+  int64_t pic_cells = 0;
 };
 
 #include <vector>

@@ -1253,6 +1253,7 @@ int lbx_ctx_destroy(lbx_ctx* ctx) {
   if (ctx->acc) cudaFree(ctx->acc);
   if (ctx->host_scratch) cudaFreeHost(ctx->host_scratch);
   destroy_pipe(ctx->pipe);
+  if (ctx->pic_acc) cudaFree(ctx->pic_acc);
   delete ctx;
   return LBX_OK;
 }

@@ -33,6 +33,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 
 #include "lbx_internal.h"
 
@@ -50,7 +51,8 @@ constexpr unsigned kAll = 0xffffffffu;
 struct PicParams {
   double *z, *x, *uz, *ux, *uy;
   float* F[6];   // Ex Ey Ez Bx By Bz
-  float* J[3];   // Jx Jy Jz
+  unsigned long long* Jacc[3];  // fixed-point current accumulators (int64)
+  double jscale;                // power-of-two fixed-point scale
   int nz, nx, pitch;
   double qm, qw, dt;
   double inv_m;  // box binning: power-of-two box size (checked on host)
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(kPB, 2) pic_push_kernel(PicParams p) {
   unsigned* s_cnt = reinterpret_cast<unsigned*>(smem_raw);          // nb
   unsigned* s_clk = s_cnt + p.nb;                                    // nb
   float* s_F = reinterpret_cast<float*>(s_clk + p.nb);               // 6 * kPatchMax
-  float* s_J = s_F + 6 * kPatchMax;                                  // 3 * kPatchMax
+  int* s_J = reinterpret_cast<int*>(s_F + 6 * kPatchMax);            // 3 * kPatchMax
   __shared__ long long s_n;
   __shared__ int s_box[4];  // imin, imax, jmin, jmax
   __shared__ int s_last;
@@ -213,12 +215,12 @@ __global__ void __launch_bounds__(kPB, 2) pic_push_kernel(PicParams p) {
 #pragma unroll
         for (int c = 0; c < 6; ++c) s_F[c * kPatchMax + idx] = __ldg(p.F[c] + g);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) s_J[c * kPatchMax + idx] = 0.f;
+        for (int c = 0; c < 3; ++c) s_J[c * kPatchMax + idx] = 0;
       }
     }
     __syncthreads();
 
-    // ---- gather, push, move, absorb, deposit ----
+    // ---- gather, push, move, absorb (per lane), deposit (warp-collective) ----
     double nz_[kPItems], nx_[kPItems];
     bool keep[kPItems];
 #pragma unroll
@@ -226,82 +228,109 @@ __global__ void __launch_bounds__(kPB, 2) pic_push_kernel(PicParams p) {
       keep[k] = false;
       nz_[k] = pz[k];
       nx_[k] = px[k];
-      if (!valid[k]) continue;
-      double f6[6];
+      double vel[3] = {0.0, 0.0, 0.0};
+      if (valid[k]) {
+        double f6[6];
 #pragma unroll
-      for (int c = 0; c < 6; ++c) {
-        const Stencil s = stencil(pz[k], px[k], (double)c_oz[c], (double)c_ox[c]);
-        double a, b, cc, d;
-        if (staged) {
-          const float* F = s_F + c * kPatchMax;
-          const int o = (s.i0 - pi0) * W + (s.j0 - pj0);
-          a = F[o];
-          b = F[o + 1];
-          cc = F[o + W];
-          d = F[o + W + 1];
-        } else {
-          const float* F = p.F[c];
-          const long long o = (long long)(s.i0 + 1) * p.pitch + (s.j0 + 1);
-          a = __ldg(F + o);
-          b = __ldg(F + o + 1);
-          cc = __ldg(F + o + p.pitch);
-          d = __ldg(F + o + p.pitch + 1);
+        for (int c = 0; c < 6; ++c) {
+          const Stencil s = stencil(pz[k], px[k], (double)c_oz[c], (double)c_ox[c]);
+          double a, b, cc, d;
+          if (staged) {
+            const float* F = s_F + c * kPatchMax;
+            const int o = (s.i0 - pi0) * W + (s.j0 - pj0);
+            a = F[o];
+            b = F[o + 1];
+            cc = F[o + W];
+            d = F[o + W + 1];
+          } else {
+            const float* F = p.F[c];
+            const long long o = (long long)(s.i0 + 1) * p.pitch + (s.j0 + 1);
+            a = __ldg(F + o);
+            b = __ldg(F + o + 1);
+            cc = __ldg(F + o + p.pitch);
+            d = __ldg(F + o + p.pitch + 1);
+          }
+          f6[c] = cic(s, a, b, cc, d);
         }
-        f6[c] = cic(s, a, b, cc, d);
+        // relativistic Boris (x, y, z order; E = f6[0..2], B = f6[3..5])
+        const double mx = __dadd_rn(pux[k], __dmul_rn(h, f6[0]));
+        const double my = __dadd_rn(puy[k], __dmul_rn(h, f6[1]));
+        const double mz = __dadd_rn(puz[k], __dmul_rn(h, f6[2]));
+        const double g = sqrt(__dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(mx, mx)),
+                                                  __dmul_rn(my, my)), __dmul_rn(mz, mz)));
+        const double ig = __ddiv_rn(1.0, g);
+        const double tx = __dmul_rn(__dmul_rn(h, f6[3]), ig);
+        const double ty = __dmul_rn(__dmul_rn(h, f6[4]), ig);
+        const double tz = __dmul_rn(__dmul_rn(h, f6[5]), ig);
+        const double s2 = __ddiv_rn(2.0, __dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(tx, tx)),
+                                                             __dmul_rn(ty, ty)),
+                                                   __dmul_rn(tz, tz)));
+        const double qx = __dadd_rn(mx, __dsub_rn(__dmul_rn(my, tz), __dmul_rn(mz, ty)));
+        const double qy = __dadd_rn(my, __dsub_rn(__dmul_rn(mz, tx), __dmul_rn(mx, tz)));
+        const double qz = __dadd_rn(mz, __dsub_rn(__dmul_rn(mx, ty), __dmul_rn(my, tx)));
+        const double rx = __dadd_rn(mx, __dmul_rn(s2, __dsub_rn(__dmul_rn(qy, tz), __dmul_rn(qz, ty))));
+        const double ry = __dadd_rn(my, __dmul_rn(s2, __dsub_rn(__dmul_rn(qz, tx), __dmul_rn(qx, tz))));
+        const double rz = __dadd_rn(mz, __dmul_rn(s2, __dsub_rn(__dmul_rn(qx, ty), __dmul_rn(qy, tx))));
+        pux[k] = __dadd_rn(rx, __dmul_rn(h, f6[0]));
+        puy[k] = __dadd_rn(ry, __dmul_rn(h, f6[1]));
+        puz[k] = __dadd_rn(rz, __dmul_rn(h, f6[2]));
+        const double gam = sqrt(__dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(pux[k], pux[k])),
+                                                    __dmul_rn(puy[k], puy[k])),
+                                          __dmul_rn(puz[k], puz[k])));
+        const double igam = __ddiv_rn(1.0, gam);
+        nz_[k] = __dadd_rn(pz[k], __dmul_rn(__dmul_rn(p.dt, puz[k]), igam));
+        nx_[k] = __dadd_rn(px[k], __dmul_rn(__dmul_rn(p.dt, pux[k]), igam));
+        keep[k] = nz_[k] >= 0.0 && nz_[k] < ez && nx_[k] >= 0.0 && nx_[k] < ex;
+        vel[0] = __dmul_rn(__dmul_rn(p.qw, pux[k]), igam);
+        vel[1] = __dmul_rn(__dmul_rn(p.qw, puy[k]), igam);
+        vel[2] = __dmul_rn(__dmul_rn(p.qw, puz[k]), igam);
       }
-      // Boris (component order x, y, z; E = f6[0..2], B = f6[3..5])
-      const double mx = __dadd_rn(pux[k], __dmul_rn(h, f6[0]));
-      const double my = __dadd_rn(puy[k], __dmul_rn(h, f6[1]));
-      const double mz = __dadd_rn(puz[k], __dmul_rn(h, f6[2]));
-      const double g = sqrt(__dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(mx, mx)), __dmul_rn(my, my)),
-                                      __dmul_rn(mz, mz)));
-      const double tx = __ddiv_rn(__dmul_rn(h, f6[3]), g);
-      const double ty = __ddiv_rn(__dmul_rn(h, f6[4]), g);
-      const double tz = __ddiv_rn(__dmul_rn(h, f6[5]), g);
-      const double s2 = __ddiv_rn(2.0, __dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(tx, tx)),
-                                                           __dmul_rn(ty, ty)),
-                                                 __dmul_rn(tz, tz)));
-      const double qx = __dadd_rn(mx, __dsub_rn(__dmul_rn(my, tz), __dmul_rn(mz, ty)));
-      const double qy = __dadd_rn(my, __dsub_rn(__dmul_rn(mz, tx), __dmul_rn(mx, tz)));
-      const double qz = __dadd_rn(mz, __dsub_rn(__dmul_rn(mx, ty), __dmul_rn(my, tx)));
-      const double rx = __dadd_rn(mx, __dmul_rn(s2, __dsub_rn(__dmul_rn(qy, tz), __dmul_rn(qz, ty))));
-      const double ry = __dadd_rn(my, __dmul_rn(s2, __dsub_rn(__dmul_rn(qz, tx), __dmul_rn(qx, tz))));
-      const double rz = __dadd_rn(mz, __dmul_rn(s2, __dsub_rn(__dmul_rn(qx, ty), __dmul_rn(qy, tx))));
-      pux[k] = __dadd_rn(rx, __dmul_rn(h, f6[0]));
-      puy[k] = __dadd_rn(ry, __dmul_rn(h, f6[1]));
-      puz[k] = __dadd_rn(rz, __dmul_rn(h, f6[2]));
-      const double gam = sqrt(__dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(pux[k], pux[k])),
-                                                  __dmul_rn(puy[k], puy[k])),
-                                        __dmul_rn(puz[k], puz[k])));
-      nz_[k] = __dadd_rn(pz[k], __ddiv_rn(__dmul_rn(p.dt, puz[k]), gam));
-      nx_[k] = __dadd_rn(px[k], __ddiv_rn(__dmul_rn(p.dt, pux[k]), gam));
-      keep[k] = nz_[k] >= 0.0 && nz_[k] < ez && nx_[k] >= 0.0 && nx_[k] < ex;
-      if (!keep[k]) continue;
-      const double vel[3] = {__ddiv_rn(__dmul_rn(p.qw, pux[k]), gam),
-                             __ddiv_rn(__dmul_rn(p.qw, puy[k]), gam),
-                             __ddiv_rn(__dmul_rn(p.qw, puz[k]), gam)};
+      // Deposition: node contributions quantised to fixed point (exact
+      // power-of-two scaling, round-to-nearest-even), pre-summed over lanes
+      // that share a stencil (__match_any_sync + redux.sync) and added with
+      // native 32-bit shared atomics -- order-independent, deterministic.
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const Stencil s = stencil(nz_[k], nx_[k], (double)c_oz[c], (double)c_ox[c]);
-        const double gz = __dsub_rn(1.0, s.fz), gx = __dsub_rn(1.0, s.fx);
-        const float w00 = (float)__dmul_rn(__dmul_rn(vel[c], gz), gx);
-        const float w01 = (float)__dmul_rn(__dmul_rn(vel[c], gz), s.fx);
-        const float w10 = (float)__dmul_rn(__dmul_rn(vel[c], s.fz), gx);
-        const float w11 = (float)__dmul_rn(__dmul_rn(vel[c], s.fz), s.fx);
+        const Stencil s = stencil(keep[k] ? nz_[k] : 0.5, keep[k] ? nx_[k] : 0.5,
+                                  (double)c_oz[c], (double)c_ox[c]);
+        int q[4] = {0, 0, 0, 0};
+        if (keep[k]) {
+          const double gz = __dsub_rn(1.0, s.fz), gx = __dsub_rn(1.0, s.fx);
+          const double vz = __dmul_rn(vel[c], gz), vf = __dmul_rn(vel[c], s.fz);
+          q[0] = (int)__double2ll_rn(__dmul_rn(__dmul_rn(vz, gx), p.jscale));
+          q[1] = (int)__double2ll_rn(__dmul_rn(__dmul_rn(vz, s.fx), p.jscale));
+          q[2] = (int)__double2ll_rn(__dmul_rn(__dmul_rn(vf, gx), p.jscale));
+          q[3] = (int)__double2ll_rn(__dmul_rn(__dmul_rn(vf, s.fx), p.jscale));
+        }
+        long long off;
+        int row;
         if (staged) {
-          float* J = s_J + c * kPatchMax;
-          const int o = (s.i0 - pi0) * W + (s.j0 - pj0);
-          atomicAdd(J + o, w00);
-          atomicAdd(J + o + 1, w01);
-          atomicAdd(J + o + W, w10);
-          atomicAdd(J + o + W + 1, w11);
+          off = (long long)(s.i0 - pi0) * W + (s.j0 - pj0);
+          row = W;
         } else {
-          float* J = p.J[c];
-          const long long o = (long long)(s.i0 + 1) * p.pitch + (s.j0 + 1);
-          atomicAdd(J + o, w00);
-          atomicAdd(J + o + 1, w01);
-          atomicAdd(J + o + p.pitch, w10);
-          atomicAdd(J + o + p.pitch + 1, w11);
+          off = (long long)(s.i0 + 1) * p.pitch + (s.j0 + 1);
+          row = p.pitch;
+        }
+        const long long key = keep[k] ? off : -1 - lane;
+        const unsigned grp = __match_any_sync(kAll, key);
+        const int t0s = __reduce_add_sync(grp, q[0]);
+        const int t1s = __reduce_add_sync(grp, q[1]);
+        const int t2s = __reduce_add_sync(grp, q[2]);
+        const int t3s = __reduce_add_sync(grp, q[3]);
+        if (keep[k] && lane == __ffs(grp) - 1) {
+          if (staged) {
+            int* J = s_J + c * kPatchMax + off;
+            if (t0s) atomicAdd(J, t0s);
+            if (t1s) atomicAdd(J + 1, t1s);
+            if (t2s) atomicAdd(J + row, t2s);
+            if (t3s) atomicAdd(J + row + 1, t3s);
+          } else {
+            unsigned long long* J = p.Jacc[c] + off;
+            if (t0s) atomicAdd(J, (unsigned long long)(long long)t0s);
+            if (t1s) atomicAdd(J + 1, (unsigned long long)(long long)t1s);
+            if (t2s) atomicAdd(J + row, (unsigned long long)(long long)t2s);
+            if (t3s) atomicAdd(J + row + 1, (unsigned long long)(long long)t3s);
+          }
         }
       }
     }
@@ -314,8 +343,8 @@ __global__ void __launch_bounds__(kPB, 2) pic_push_kernel(PicParams p) {
         const long long g = (long long)(pi0 + li + 1) * p.pitch + (pj0 + lj + 1);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const float v = s_J[c * kPatchMax + idx];
-          if (v != 0.f) atomicAdd(p.J[c] + g, v);
+          const int v = s_J[c * kPatchMax + idx];
+          if (v) atomicAdd(p.Jacc[c] + g, (unsigned long long)(long long)v);
         }
       }
     }
@@ -423,6 +452,25 @@ __global__ void __launch_bounds__(kPB, 2) pic_push_kernel(PicParams p) {
   }
 }
 
+// Fixed-point current -> float32 J (J += sum / scale), accumulators zeroed.
+__global__ void pic_current_kernel(unsigned long long* acc0, unsigned long long* acc1,
+                                   unsigned long long* acc2, float* J0, float* J1, float* J2,
+                                   long long cells, double inv_scale) {
+  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < cells;
+       o += (long long)gridDim.x * blockDim.x) {
+    unsigned long long* acc[3] = {acc0, acc1, acc2};
+    float* J[3] = {J0, J1, J2};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const long long v = (long long)acc[c][o];
+      if (v) {
+        J[c][o] = __fadd_rn(J[c][o], (float)__dmul_rn((double)v, inv_scale));
+        acc[c][o] = 0ull;
+      }
+    }
+  }
+}
+
 // Yee update, interior cells; float32 storage, float64 arithmetic in the
 // oracle's evaluation order.
 __global__ void pic_b_kernel(const float* __restrict__ Ex, const float* __restrict__ Ey,
@@ -508,7 +556,23 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   p.ux = a->ux;
   p.uy = a->uy;
   for (int c = 0; c < 6; ++c) p.F[c] = a->fields[c];
-  for (int c = 0; c < 3; ++c) p.J[c] = a->current[c];
+  const long long padded = (long long)(a->nz + 2) * (a->nx + 2);
+  if (!ctx->pic_acc || ctx->pic_cells < padded) {
+    if (ctx->pic_acc) {
+      cudaDeviceSynchronize();
+      cudaFree(ctx->pic_acc);
+    }
+    ctx->pic_acc = nullptr;
+    if (cudaMalloc(&ctx->pic_acc, (size_t)padded * 3 * 8) != cudaSuccess)
+      return set_error(LBX_EOOM, "PIC current accumulators");
+    cudaMemset(ctx->pic_acc, 0, (size_t)padded * 3 * 8);
+    ctx->pic_cells = padded;
+  }
+  for (int c = 0; c < 3; ++c) p.Jacc[c] = ctx->pic_acc + c * padded;
+  if (!(a->q_times_w != 0.0)) return set_error(LBX_EINVAL, "q_times_w must be nonzero");
+  int e2 = 0;
+  std::frexp(1048576.0 / std::fabs(a->q_times_w), &e2);  // scale = 2^floor(log2(2^20/|qw|))
+  p.jscale = std::ldexp(1.0, e2 - 1);
   p.nz = a->nz;
   p.nx = a->nx;
   p.pitch = a->nx + 2;
@@ -543,6 +607,9 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   kern<<<(unsigned)grid, kPB, smem, s>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "pic_push_kernel launch");
+  const unsigned cg = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 8, (padded + 255) / 256));
+  pic_current_kernel<<<cg, 256, 0, s>>>(p.Jacc[0], p.Jacc[1], p.Jacc[2], a->current[0],
+                                        a->current[1], a->current[2], padded, 1.0 / p.jscale);
   rc = launch_compact(ctx, a->z, a->x, a->uz, a->ux, a->uy, nullptr, (double)a->nz,
                       (double)a->nx, stream);
   if (rc) return rc;

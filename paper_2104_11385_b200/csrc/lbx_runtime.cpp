@@ -58,6 +58,10 @@ struct lbx_sim {
   unsigned long long* h_offsets = nullptr;  // pinned
   std::vector<cudaEvent_t> tb0, tb1;
   std::vector<double> timers;
+  // PIC physics
+  float* fields[6] = {};
+  float* current[3] = {};
+  double* uy = nullptr;
 };
 
 namespace {
@@ -98,6 +102,10 @@ int validate(const lbx_sim_config& c) {
   if (c.interval < 1) return set_error(LBX_EINVAL, "interval must be >= 1");
   if (c.cost_kind < 0 || c.cost_kind > LBX_COST_TIMERS)
     return set_error(LBX_EINVAL, "unknown cost kind %d", c.cost_kind);
+  if (c.physics != LBX_PHYSICS_SURROGATE && c.physics != LBX_PHYSICS_PIC)
+    return set_error(LBX_EINVAL, "unknown physics %d", c.physics);
+  if (c.physics == LBX_PHYSICS_PIC && c.cost_kind == LBX_COST_TIMERS)
+    return set_error(LBX_EINVAL, "Timers strategy is implemented for the surrogate push only");
   return LBX_OK;
 }
 
@@ -271,6 +279,36 @@ int launch_step(lbx_sim* s, int64_t step, cudaStream_t st) {
   const lbx_sim_config& c = s->lb->cfg;
   const bool kicked = step >= c.kick_step && s->kvz != nullptr;
   const bool timers = c.cost_kind == LBX_COST_TIMERS;
+  if (c.physics == LBX_PHYSICS_PIC) {
+    lbx_pic_args pa{};
+    pa.z = s->z;
+    pa.x = s->x;
+    pa.uz = kicked ? s->kvz : s->vz;
+    pa.ux = kicked ? s->kvx : s->vx;
+    pa.uy = s->uy;
+    for (int k = 0; k < 6; ++k) pa.fields[k] = s->fields[k];
+    for (int k = 0; k < 3; ++k) pa.current[k] = s->current[k];
+    pa.nz = c.extent_z;
+    pa.nx = c.extent_x;
+    pa.box_size = c.box_size;
+    pa.q_over_m = c.pic_q_over_m;
+    pa.q_times_w = c.pic_q_times_w;
+    pa.dt = c.pic_dt;
+    pa.w_particle = c.w_particle;
+    pa.w_cell = c.w_cell;
+    pa.flags = c.cost_kind == LBX_COST_GPUCLOCK ? LBX_STEP_CLOCK : 0u;
+    pa.counts_out = d.counts;
+    pa.cost_out = d.cost;
+    pa.clk_out = d.clk;
+    pa.n_out = d.n;
+    pa.err_out = d.err;
+    int rc = lbx_pic_step(s->ctx, &pa, st);
+    if (rc) return rc;
+    if (s->timing) cudaEventRecord(s->t1[slot], st);
+    cudaError_t e = cudaEventRecord(s->ev[slot], st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    return LBX_OK;
+  }
   if (timers) {
     int rc = timers_prepare(s, kicked ? s->kvz : s->vz, kicked ? s->kvx : s->vx, st);
     if (rc) return rc;
@@ -511,6 +549,15 @@ int lbx_sim_set_particles(lbx_sim* s, double* z, double* x, double* vz, double* 
   return lbx_ctx_set_count(s->ctx, n, stream);
 }
 
+int lbx_sim_set_fields(lbx_sim* s, float* const* fields, float* const* current, double* uy) {
+  clear_error();
+  if (!s || !fields || !current || !uy) return set_error(LBX_EINVAL, "NULL argument");
+  for (int k = 0; k < 6; ++k) s->fields[k] = fields[k];
+  for (int k = 0; k < 3; ++k) s->current[k] = current[k];
+  s->uy = uy;
+  return LBX_OK;
+}
+
 int lbx_sim_run(lbx_sim* s, int64_t first, int64_t last, lbx_sim_outputs* o, void* stream) {
   clear_error();
   if (!s || !o) return set_error(LBX_EINVAL, "NULL argument");
@@ -519,6 +566,8 @@ int lbx_sim_run(lbx_sim* s, int64_t first, int64_t last, lbx_sim_outputs* o, voi
     return set_error(LBX_EINVAL, "step range [%lld, %lld) outside [0, %lld)", (long long)first,
                      (long long)last, (long long)c.total_steps);
   if (!s->z) return set_error(LBX_EINVAL, "particles not set");
+  if (c.physics == LBX_PHYSICS_PIC && !s->uy)
+    return set_error(LBX_EINVAL, "PIC physics needs lbx_sim_set_fields");
   if (first == 0) std::memcpy(s->lb->owner.data(), o->owner, 8 * (size_t)s->lb->nb);
   for (int b = 0; b < s->lb->nb; ++b)
     if (s->lb->owner[b] < 0 || s->lb->owner[b] >= c.n_ranks)

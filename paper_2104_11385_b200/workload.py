@@ -323,7 +323,11 @@ def policy_kind(policy: BalancePolicy, total_steps: int) -> str:
     return "static" if policy.static_step is not None else "none"
 
 
-def sim_config(cfg: ScenarioConfig, policy: BalancePolicy, provider: CostProvider):
+PIC_DEFAULTS = {"dt": 0.5, "q_over_m": -1.0, "q_times_w": -1e-4}
+
+
+def sim_config(cfg: ScenarioConfig, policy: BalancePolicy, provider: CostProvider,
+               physics: str = "surrogate", pic: dict | None = None):
     """Flatten (scenario, policy, provider) into lbx_sim_config."""
     if provider.device_kind < 0 or provider.device_kind > 4:
         raise ConfigError(f"provider {provider.kind!r} is not supported by the native loop")
@@ -347,18 +351,24 @@ def sim_config(cfg: ScenarioConfig, policy: BalancePolicy, provider: CostProvide
         comm_per_face=model.comm_per_face, gather=model.gather,
         redistribute_per_particle=model.redistribute_per_particle,
         redistribute_latency=model.redistribute_latency,
-        capacity_particles=-1 if cfg.capacity_particles is None else cfg.capacity_particles)
+        capacity_particles=-1 if cfg.capacity_particles is None else cfg.capacity_particles,
+        physics=0 if physics == "surrogate" else 1,
+        pic_dt=(pic or PIC_DEFAULTS)["dt"], pic_q_over_m=(pic or PIC_DEFAULTS)["q_over_m"],
+        pic_q_times_w=(pic or PIC_DEFAULTS)["q_times_w"])
 
 
 class Simulation:
     """Device-resident run: particles in HBM (SoA), native stepping loop.
 
     ``Simulation(cfg, policy, provider).run()`` == run_simulation(...);
-    ``run(first, last)`` runs a sub-range (benchmarks time a window)."""
+    ``run(first, last)`` runs a sub-range (benchmarks time a window).
+    ``physics="pic"`` replaces the reference's ballistic advance with the
+    2D3V PIC step (pic.py); the kick then sets momenta u = v_kick / dt."""
 
     def __init__(self, cfg: ScenarioConfig, policy: BalancePolicy, provider: CostProvider,
                  *, device="cuda:0", positions=None, kick=None, initial_owner=None,
-                 record_counts=False, record_clock=False, time_kernels=False):
+                 record_counts=False, record_clock=False, time_kernels=False,
+                 physics="surrogate", pic=None):
         import torch
 
         from . import device as D
@@ -393,7 +403,12 @@ class Simulation:
             self.kvx = torch.zeros(n + 2, dtype=torch.float64, device=self.dev)
             self.kvz[:n].copy_(kick[:, 0])
             self.kvx[:n].copy_(kick[:, 1])
-        self.conf = sim_config(cfg, policy, provider)
+        self.physics = physics
+        self.pic = dict(PIC_DEFAULTS, **(pic or {}))
+        if physics == "pic" and self.kvz is not None:   # momenta from the kick
+            self.kvz.div_(self.pic["dt"])
+            self.kvx.div_(self.pic["dt"])
+        self.conf = sim_config(cfg, policy, provider, physics, self.pic)
         h = C.c_void_p()
         _lib.check(_lib.lib.lbx_sim_create(C.byref(h), self.ctx.handle, C.byref(self.conf)))
         self.handle = h
@@ -401,6 +416,15 @@ class Simulation:
         _lib.check(_lib.lib.lbx_sim_set_particles(
             h, _lib.ptr(st.z), _lib.ptr(st.x), _lib.ptr(st.vz), _lib.ptr(st.vx),
             _lib.ptr(self.kvz), _lib.ptr(self.kvx), n, D._stream(self.dev)))
+        if physics == "pic":
+            from .pic import CURRENT_NAMES, FIELD_NAMES
+            nz, nx = cfg.domain_extent
+            self.fields = {k: torch.zeros((nz + 2, nx + 2), dtype=torch.float32,
+                                          device=self.dev) for k in FIELD_NAMES + CURRENT_NAMES}
+            self.uy = torch.zeros(n + 2, dtype=torch.float64, device=self.dev)
+            fa = (C.c_void_p * 6)(*(_lib.ptr(self.fields[k]) for k in FIELD_NAMES))
+            ca = (C.c_void_p * 3)(*(_lib.ptr(self.fields[k]) for k in CURRENT_NAMES))
+            _lib.check(_lib.lib.lbx_sim_set_fields(h, fa, ca, _lib.ptr(self.uy)))
         T, nb = cfg.total_steps, self.ba.n_boxes
         self.out = {k: np.zeros(T) for k in ("eff_before", "eff_after", "compute_max",
                                              "comm_max", "gather", "redistribute",

@@ -1,11 +1,9 @@
-"""2D3V PIC step (gather + Boris + deposit + Yee) vs the fp64/fp32 numpy
-oracle.  Parity unpinned by the reference (no PIC there); tolerances:
-  * step 1 from zero fields: particles bit-exact (no field contribution);
-  * currents / fields: max |GPU - oracle| <= 1e-5 * max|oracle| + 1e-7
-    (float32 atomics sum in a different order);
-  * particles after N steps: |dz|, |dx| <= 1e-6 cells, |du| <= 1e-6;
-  * per-box counts: exact while no particle sits within 1e-6 of a box edge.
-"""
+"""2D3V PIC step (gather + Boris + deposit + Yee) vs the numpy oracle.
+Parity unpinned by the reference (no PIC there).  The deposition quantises
+node contributions to fixed point and sums integers, so it is order
+independent; every other operation follows the oracle's IEEE evaluation
+order.  The bar is therefore BIT-EXACT: particles, currents, fields and
+per-box counts identical after several steps with the field solve."""
 import numpy as np
 import pytest
 
@@ -52,7 +50,7 @@ def close(a, b, rel=1e-5, abs_=1e-7):
     return np.max(np.abs(a - b)) <= rel * max(np.max(np.abs(b)), 1e-30) + abs_
 
 
-def test_first_step_particles_exact_and_currents_close():
+def test_first_step_particles_and_currents_exact():
     pos, u = setup(60_000, 64, 64, seed=1)
     st, f, p, outs = run_both(pos, u, 64, 64, steps=1, field_solve=False)
     g = st.particles()
@@ -60,7 +58,8 @@ def test_first_step_particles_exact_and_currents_close():
         assert np.array_equal(g[k], p[k]), k
     fa = st.field_arrays()
     for k in ("Jx", "Jy", "Jz"):
-        assert close(fa[k], outs[0][1][k]), k
+        assert np.array_equal(fa[k], outs[0][1][k]), k
+        assert np.abs(fa[k]).max() > 0
     c = LO.bin_particles(np.column_stack([p["z"], p["x"]]), 16.0, 4, 4)
     assert np.array_equal(outs[0][0]["counts"], c)
     assert ((outs[0][0]["clock"] > 0) == (c > 0)).all()
@@ -72,13 +71,13 @@ def test_multi_step_with_field_solve(clustered):
     st, f, p, outs = run_both(pos, u, 64, 96, steps=6, field_solve=True)
     g = st.particles()
     assert g["z"].shape == p["z"].shape
-    for k in ("z", "x"):
-        assert np.max(np.abs(g[k] - p[k])) <= 1e-6, k
-    for k in ("uz", "ux", "uy"):
-        assert np.max(np.abs(g[k] - p[k])) <= 1e-6, k
+    for k in ("z", "x", "uz", "ux", "uy"):
+        assert np.array_equal(g[k], p[k]), k
     fa = st.field_arrays()
     for k in PO.OFFSETS:
-        assert close(fa[k], f[k], rel=1e-4, abs_=1e-6), k
+        assert np.array_equal(fa[k], f[k]), k
+    for step, (out, _) in enumerate(outs):
+        assert out["n"] > 0
     assert np.max(np.abs(fa["Ey"])) > 0          # fields actually evolved
 
 
@@ -87,4 +86,46 @@ def test_absorption_and_compaction_keep_order():
     st, f, p, outs = run_both(pos, u, 32, 32, steps=4, field_solve=False)
     g = st.particles()
     assert st.n == p["z"].size < 30_000
-    assert np.max(np.abs(g["z"] - p["z"])) <= 1e-6
+    for k in ("z", "x", "uz", "ux", "uy"):
+        assert np.array_equal(g[k], p[k]), k
+
+
+def test_pic_physics_in_native_loop():
+    """Simulation(physics="pic"): the native LB loop driving lbx_pic_step,
+    against the oracle PIC run from the same sampled blob and kick."""
+    import json
+    from pathlib import Path
+
+    from paper_2104_11385_b200 import scenarios as S
+    from paper_2104_11385_b200.workload import Simulation, kick_velocities, sample_blob
+    doc = json.loads((Path(__file__).parent / "golden" / "runs.json").read_text())["_docs"]["small"]
+    spec = S.apply_overrides(S.spec_from_dict(doc), cost="gpuclock", steps=25)
+    cfg = spec.scenario
+    sim = Simulation(cfg, spec.policy, spec.build_provider(), physics="pic",
+                     record_counts=True)
+    sim.run()
+    res = sim.result()
+    pos = sample_blob(cfg)
+    kick = kick_velocities(pos, cfg)
+    nz, nx = cfg.domain_extent
+    dt = 0.5
+    f = PO.new_fields(nz, nx)
+    p = {"z": pos[:, 0].copy(), "x": pos[:, 1].copy(), "uz": np.zeros(len(pos)),
+         "ux": np.zeros(len(pos)), "uy": np.zeros(len(pos))}
+    mism = 0
+    for step in range(cfg.total_steps):
+        if step == cfg.kick.step:
+            p["uz"], p["ux"] = kick[:, 0] / dt, kick[:, 1] / dt
+        PO.particle_step(f, p, nz, nx, -1.0, -1e-4, dt)
+        PO.field_step(f, nz, nx, dt)
+        c = LO.bin_particles(np.column_stack([p["z"], p["x"]]), float(cfg.box_size),
+                             nz // cfg.box_size, nx // cfg.box_size)
+        mism += int(np.abs(res.count_trace[step] - c).sum())
+    assert mism == 0, mism
+    st = res.final_state
+    n = st.n
+    assert n == p["z"].size
+    assert np.array_equal(st.z[:n].cpu().numpy(), p["z"])
+    assert np.array_equal(st.vz[:n].cpu().numpy(), p["uz"])
+    assert np.array_equal(sim.uy[:n].cpu().numpy(), p["uy"])
+    assert (res.cost_trace[-1][res.count_trace[-1] > 0] > 0).all()   # GpuClock from PIC
