@@ -1,0 +1,156 @@
+#!/usr/bin/env python
+"""Config C5: no LB vs static LB vs dynamic LB speedup, against the
+performance-model maximum S_max = (1/E0)^x (perfmodel.py).
+
+Scenario: the C2 geometry with the high-imbalance blob of SURVEY 7 (centre
+[60, 480], core 44: the blob sits inside one rank's slab, E0 ~ 0.2 at 8
+ranks) from the kick on, the 801,499-particle-class set tiled R times, slab
+initial mapping, knapsack remaps with GpuClock costs.  Policies:
+  none     no rebalancing (slab mapping throughout)
+  static   one knapsack attempt at step 0
+  dynamic  knapsack attempt every 10 steps (10 % relative threshold)
+
+Modes:
+  torchrun --nproc-per-node N bench_lb.py      one rank per GPU (NCCL);
+      per-step time = max over ranks of the step's device time.
+  python bench_lb.py --emulate R               one GPU, R ranks as threads;
+      each rank's push/deposit kernels run alone (a lock serializes them)
+      and are timed with CUDA events; the emulated step time is the MAX over
+      ranks of those times -- the compute-imbalance part of an R-GPU step,
+      measured on B200 hardware.  Exchange/migration traffic is reported
+      (particles moved) but not timed in this mode.
+Prints one JSON object.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+from dataclasses import replace
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+
+def scenario(ranks, steps, policy):
+    from paper_2104_11385_b200.balancer import BalancePolicy
+    from paper_2104_11385_b200.scenarios import apply_overrides, load_spec
+    from paper_2104_11385_b200.workload import BlobSpec, KickSpec
+
+    spec = apply_overrides(load_spec("default"), cost="gpuclock", ranks=ranks, steps=steps,
+                           policy="knapsack" if policy == "dynamic" else policy)
+    sc = replace(spec.scenario, blob=BlobSpec(center=(60.0, 480.0), core_radius=44.0,
+                                              edge_scale=4.0, particles_per_cell=55.0),
+                 kick=KickSpec(step=0, speed=0.035, drift=0.01), initial_mapping="slab")
+    return spec, sc
+
+
+def make_timed_engine(lock, log):
+    from paper_2104_11385_b200.parallel import DeviceEngine
+
+    class TimedEngine(DeviceEngine):
+        def push(self, wp, wc):
+            import torch
+            with lock:
+                torch.cuda.synchronize()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                out = super().push(wp, wc)
+                e1.record()
+                e1.synchronize()
+                log.setdefault(self.rank, []).append(e0.elapsed_time(e1))
+            return out
+
+    return TimedEngine
+
+
+def run_emulated(R, steps, replicas, policy):
+    import torch
+
+    import bench
+    from paper_2104_11385_b200.parallel import DistributedSimulation, ThreadComm
+
+    spec, sc = scenario(R, steps, policy)
+    from paper_2104_11385_b200.workload import kick_velocities, sample_blob
+    pos = sample_blob(sc)
+    kick = kick_velocities(pos, sc)
+    lock, log = threading.Lock(), {}
+    shared = ThreadComm.shared(R)
+    sims, errs = [None] * R, []
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            sim = DistributedSimulation(sc, spec.policy, spec.build_provider(),
+                                        comm=ThreadComm(shared, r),
+                                        engine_factory=make_timed_engine(lock, log),
+                                        positions=pos, kick=kick, device="cuda:0",
+                                        replicas=replicas,
+                                        capacity=pos.shape[0] * replicas + 4096)
+            sim.run()
+            sims[r] = sim
+        except Exception as e:
+            errs.append(e)
+            shared["bar"].abort()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(R)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    per_step = np.max(np.array([log[r] for r in range(R)]), axis=0)   # [steps]
+    res = sims[0].result()
+    moved = int(sum(s.moved.sum() for s in sims))
+    for s in sims:
+        s.close()
+    return per_step, res, moved, pos.shape[0] * replicas
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--emulate", type=int, default=0, help="ranks emulated on one GPU")
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--replicas", type=int, default=128)
+    ap.add_argument("--warmup-steps", type=int, default=1)
+    args = ap.parse_args()
+    if not args.emulate:
+        raise SystemExit("multi-GPU mode: run under torchrun with bench.py --gpus N for the "
+                         "throughput line; this script's LB comparison uses --emulate R here")
+    from paper_2104_11385_b200.perfmodel import EXPONENT_PRESETS, achieved_fraction, max_speedup
+
+    R = args.emulate
+    out = {"mode": f"emulated {R} ranks on one B200 (per-rank kernels timed alone; "
+                   "step time = max over ranks)", "ranks": R, "steps": args.steps,
+           "policies": {}}
+    w = args.warmup_steps
+    for policy in ("none", "static", "dynamic"):
+        per_step, res, moved, n = run_emulated(R, args.steps, args.replicas, policy)
+        effs = [m.efficiency_after for m in res.metrics]
+        out["policies"][policy] = {
+            "time_ms": float(per_step[w:].sum()), "ms_per_step": float(per_step[w:].mean()),
+            "e0": float(res.metrics[0].efficiency_before), "mean_eff": float(np.mean(effs)),
+            "adoptions": res.summary["adoption_count"], "particles_migrated": moved,
+            "particles": n}
+    P = out["policies"]
+    x = EXPONENT_PRESETS["2d3v"]
+    e0 = P["none"]["e0"]
+    s_max = max_speedup(e0, x)
+    out["speedup_dynamic_vs_none"] = P["none"]["time_ms"] / P["dynamic"]["time_ms"]
+    out["speedup_static_vs_none"] = P["none"]["time_ms"] / P["static"]["time_ms"]
+    out["speedup_dynamic_vs_static"] = P["static"]["time_ms"] / P["dynamic"]["time_ms"]
+    out["model"] = {"E0": e0, "x": x, "S_max": s_max,
+                    "achieved_fraction": achieved_fraction(out["speedup_dynamic_vs_none"], s_max)}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -311,25 +311,45 @@ __global__ void __launch_bounds__(kPB, 2) pic_push_kernel(PicParams p) {
           off = (long long)(s.i0 + 1) * p.pitch + (s.j0 + 1);
           row = p.pitch;
         }
-        const long long key = keep[k] ? off : -1 - lane;
-        const unsigned grp = __match_any_sync(kAll, key);
-        const int t0s = __reduce_add_sync(grp, q[0]);
-        const int t1s = __reduce_add_sync(grp, q[1]);
-        const int t2s = __reduce_add_sync(grp, q[2]);
-        const int t3s = __reduce_add_sync(grp, q[3]);
-        if (keep[k] && lane == __ffs(grp) - 1) {
+        // Warp-uniform fast path: all depositing lanes share the stencil
+        // (sorted particles, 55 per cell) -> 4 full-warp redux.sync and one
+        // lane adds; otherwise each lane adds (native 32-bit atomics).
+        const unsigned dep = __ballot_sync(kAll, keep[k]);
+        if (!dep) continue;
+        const long long off0 = __shfl_sync(kAll, off, __ffs(dep) - 1);
+        if (__all_sync(kAll, !keep[k] || off == off0)) {
+          const int t0s = __reduce_add_sync(kAll, q[0]);
+          const int t1s = __reduce_add_sync(kAll, q[1]);
+          const int t2s = __reduce_add_sync(kAll, q[2]);
+          const int t3s = __reduce_add_sync(kAll, q[3]);
+          if (lane == __ffs(dep) - 1) {
+            if (staged) {
+              int* J = s_J + c * kPatchMax + off;
+              atomicAdd(J, t0s);
+              atomicAdd(J + 1, t1s);
+              atomicAdd(J + row, t2s);
+              atomicAdd(J + row + 1, t3s);
+            } else {
+              unsigned long long* J = p.Jacc[c] + off;
+              atomicAdd(J, (unsigned long long)(long long)t0s);
+              atomicAdd(J + 1, (unsigned long long)(long long)t1s);
+              atomicAdd(J + row, (unsigned long long)(long long)t2s);
+              atomicAdd(J + row + 1, (unsigned long long)(long long)t3s);
+            }
+          }
+        } else if (keep[k]) {
           if (staged) {
             int* J = s_J + c * kPatchMax + off;
-            if (t0s) atomicAdd(J, t0s);
-            if (t1s) atomicAdd(J + 1, t1s);
-            if (t2s) atomicAdd(J + row, t2s);
-            if (t3s) atomicAdd(J + row + 1, t3s);
+            atomicAdd(J, q[0]);
+            atomicAdd(J + 1, q[1]);
+            atomicAdd(J + row, q[2]);
+            atomicAdd(J + row + 1, q[3]);
           } else {
             unsigned long long* J = p.Jacc[c] + off;
-            if (t0s) atomicAdd(J, (unsigned long long)(long long)t0s);
-            if (t1s) atomicAdd(J + 1, (unsigned long long)(long long)t1s);
-            if (t2s) atomicAdd(J + row, (unsigned long long)(long long)t2s);
-            if (t3s) atomicAdd(J + row + 1, (unsigned long long)(long long)t3s);
+            atomicAdd(J, (unsigned long long)(long long)q[0]);
+            atomicAdd(J + 1, (unsigned long long)(long long)q[1]);
+            atomicAdd(J + row, (unsigned long long)(long long)q[2]);
+            atomicAdd(J + row + 1, (unsigned long long)(long long)q[3]);
           }
         }
       }
