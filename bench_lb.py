@@ -57,13 +57,14 @@ def make_timed_engine(lock, log):
     class TimedEngine(DeviceEngine):
         def push(self, wp, wc):
             import torch
+            st = torch.cuda.current_stream()   # this rank's own stream
             with lock:
-                torch.cuda.synchronize()
+                st.synchronize()
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
-                e0.record()
+                e0.record(st)
                 out = super().push(wp, wc)
-                e1.record()
+                e1.record(st)
                 e1.synchronize()
                 log.setdefault(self.rank, []).append(e0.elapsed_time(e1))
             return out
@@ -88,6 +89,7 @@ def run_emulated(R, steps, replicas, policy):
     def body(r):
         try:
             torch.cuda.set_device(0)
+            torch.cuda.set_stream(torch.cuda.Stream())   # per-rank stream (thread-local)
             sim = DistributedSimulation(sc, spec.policy, spec.build_provider(),
                                         comm=ThreadComm(shared, r),
                                         engine_factory=make_timed_engine(lock, log),

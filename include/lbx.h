@@ -343,6 +343,13 @@ typedef struct lbx_exchange_args {
   double* kick_vz;          /* pending kick velocities travelling with the
                                particles (NULL once the kick has happened)   */
   double* kick_vx;
+  /* Optional O(removed) compaction: when removed_list != NULL, the indices of
+   * every particle removed locally (absorbed or emigrated) are listed there
+   * (removed_cap entries) and NO stable compaction runs; the caller then
+   * calls lbx_fill_holes once it knows the count.  Local particle order is
+   * not preserved (the multi-GPU path does not need it). */
+  int64_t* removed_list;
+  int64_t removed_cap;
 } lbx_exchange_args;
 
 /* lbx_push_step + emigrant staging (per-step box-crossing exchange). */
@@ -355,6 +362,13 @@ int lbx_partition(lbx_ctx* ctx, double* z, double* x, double* vz, double* vx,
                   double extent_z, double extent_x, double box_size, int32_t nbz,
                   int32_t nbx, const lbx_exchange_args* ex, int64_t* n_out,
                   void* stream);
+/* Unstable O(removed) compaction: the n_removed listed indices (any order)
+ * are removed from [0, n_new + n_removed) by moving survivors from the tail
+ * [n_new, n_new + n_removed) into the holes below n_new.  kick_vz/kick_vx may
+ * be NULL.  Sets the context's live count to n_new. */
+int lbx_fill_holes(lbx_ctx* ctx, double* z, double* x, double* vz, double* vx,
+                   double* kick_vz, double* kick_vx, const int64_t* removed,
+                   int64_t n_removed, int64_t n_new, void* stream);
 /* Group `count` staged records by destination into `send` ([count][6]);
  * cursors[world] (device) holds each destination's first slot on entry. */
 int lbx_group_by_dest(const double* stage, const int32_t* stage_dest, int64_t count,

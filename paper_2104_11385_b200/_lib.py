@@ -94,7 +94,8 @@ class ExchangeArgs(C.Structure):
     """lbx_exchange_args (include/lbx.h)."""
     _fields_ = [("owner", vp), ("rank", i32), ("world", i32), ("stage", vp),
                 ("stage_dest", vp), ("stage_cap", i64), ("send_counts", vp),
-                ("kick_vz", vp), ("kick_vx", vp)]
+                ("kick_vz", vp), ("kick_vx", vp), ("removed_list", vp),
+                ("removed_cap", i64)]
 
 
 SIGNATURES.update({
@@ -107,6 +108,7 @@ SIGNATURES.update({
                             vp, vp]),
     "lbx_group_by_dest": (i32, [vp, vp, i64, i32, vp, vp, vp]),
     "lbx_unpack": (i32, [vp, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
+    "lbx_fill_holes": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, vp]),
     "lbx_advance_bin_host": (i32, [vp, vp, vp, i64, f64, f64, f64, i32, i32, f64, f64, vp, vp,
                                    vp, vp, P(i64)]),
 })

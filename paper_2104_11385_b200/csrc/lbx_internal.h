@@ -25,6 +25,9 @@ struct DevState {
   long long first_leaver;     // lowest index absorbed this step (LLONG_MAX: none)
   long long n_old;            // count before this step's push (compaction input)
   unsigned long long staged;  // emigrant records staged this call
+  unsigned long long removed_count;  // removed indices listed this call
+  unsigned long long holes;          // hole-fill cursors
+  unsigned long long movers;
 };
 
 // Host-side model of the particle state's pushed-and-binned step.
@@ -62,6 +65,8 @@ struct lbx_ctx {
   lbx::HostPipe* pipe = nullptr;      // lbx_advance_bin_host lanes (lazy)
   unsigned long long* pic_acc = nullptr;  // PIC fixed-point current [3][cells]
   int64_t pic_cells = 0;
+  long long* fill_scratch = nullptr;      // hole-fill: holes[cap] + tail flags[cap]
+  int64_t fill_cap = 0;
 };
 
 #include <vector>

@@ -89,6 +89,8 @@ struct StepParams {
   long long* send_counts;
   const double* kvz;
   const double* kvx;
+  long long* removed_list;  // non-NULL: list removed indices, no stable compaction
+  long long removed_cap;
 };
 
 struct ScanParams {
@@ -333,6 +335,24 @@ __global__ void __launch_bounds__(kBlock, 4) stream_kernel(StepParams p) {
       if (valid[2 * r + 1] && (!keep[2 * r + 1] || emig[2 * r + 1])) {
         ++removed;
         first_out = min(first_out, i0 + 1);
+      }
+    }
+    if (kExch && p.removed_list) {  // list removed indices (warp-aggregated)
+#pragma unroll
+      for (int k = 0; k < 2 * kPairs; ++k) {
+        const long long i = 2 * (q0 + (k >> 1) * kBlock + tid) + (k & 1);
+        const bool rm = valid[k] && (!keep[k] || emig[k]);
+        const unsigned m = __ballot_sync(kFull, rm);
+        if (!m) continue;
+        unsigned long long base = 0;
+        if (lane == __ffs(m) - 1)
+          base = atomicAdd(&p.st->removed_count, (unsigned long long)__popc(m));
+        base = __shfl_sync(kFull, base, __ffs(m) - 1);
+        if (rm) {
+          const long long slot = (long long)base + __popc(m & lanemask_lt());
+          if (slot < p.removed_cap) p.removed_list[slot] = i;
+          else atomicOr((unsigned long long*)&p.st->err, 1ull << 61);
+        }
       }
     }
     if (kExch) {
@@ -835,6 +855,51 @@ __global__ void timers_push_kernel(double* z, double* x, const double* __restric
   }
 }
 
+// Unstable O(removed) compaction (multi-GPU path): holes below n_new are
+// filled with the survivors found in the tail [n_new, n_new + L).
+__global__ void fill_mark_kernel(const long long* __restrict__ removed, long long L,
+                                 long long n_new, long long* holes, long long* tail_flag,
+                                 DevState* st) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < L; k += stride) {
+    const long long r = removed[k];
+    if (r >= n_new) tail_flag[r - n_new] = 1;
+    else holes[atomicAdd(&st->holes, 1ull)] = r;
+  }
+}
+
+__global__ void fill_move_kernel(long long L, long long n_new, const long long* __restrict__ holes,
+                                 long long* tail_flag, DevState* st, double* z, double* x,
+                                 double* vz, double* vx, double* kvz, double* kvx) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < L; j += stride) {
+    if (tail_flag[j]) {
+      tail_flag[j] = 0;
+      continue;
+    }
+    const long long src = n_new + j;
+    const long long dst = holes[atomicAdd(&st->movers, 1ull)];
+    z[dst] = z[src];
+    x[dst] = x[src];
+    vz[dst] = vz[src];
+    vx[dst] = vx[src];
+    if (kvz) {
+      kvz[dst] = kvz[src];
+      kvx[dst] = kvx[src];
+    }
+  }
+}
+
+__global__ void fill_done_kernel(DevState* st, long long n_new) {
+  st->n = n_new;
+  st->n_old = n_new;
+  st->holes = 0ull;
+  st->movers = 0ull;
+  st->removed_count = 0ull;
+  st->leavers = 0ull;
+  st->first_leaver = LLONG_MAX;
+}
+
 __global__ void counts_cost_kernel(const long long* __restrict__ counts, int nb, double wp,
                                    double wc, double cells, double* __restrict__ cost) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -850,6 +915,9 @@ __global__ void init_state_kernel(DevState* st, long long n) {
   st->leavers = 0ull;
   st->first_leaver = LLONG_MAX;
   st->staged = 0ull;
+  st->removed_count = 0ull;
+  st->holes = 0ull;
+  st->movers = 0ull;
 }
 
 __global__ void group_kernel(const double* __restrict__ stage, const int* __restrict__ dest,
@@ -1176,8 +1244,12 @@ int launch_push_step(lbx_ctx* ctx, const StepLaunch& a, void* stream,
     p.send_counts = reinterpret_cast<long long*>(ex->send_counts);
     p.kvz = ex->kick_vz;
     p.kvx = ex->kick_vx;
+    p.removed_list = reinterpret_cast<long long*>(ex->removed_list);
+    p.removed_cap = ex->removed_cap;
     rc = push ? launch_stream_any<true, true>(ctx, p, a.clock, pow2, s)
               : launch_stream_any<true, false>(ctx, p, false, pow2, s);
+    if (rc) return rc;
+    if (ex->removed_list) return LBX_OK;  // caller compacts with lbx_fill_holes
   } else {
     rc = launch_stream_any<false, true>(ctx, p, a.clock, pow2, s);
   }
@@ -1254,6 +1326,7 @@ int lbx_ctx_destroy(lbx_ctx* ctx) {
   if (ctx->host_scratch) cudaFreeHost(ctx->host_scratch);
   destroy_pipe(ctx->pipe);
   if (ctx->pic_acc) cudaFree(ctx->pic_acc);
+  if (ctx->fill_scratch) cudaFree(ctx->fill_scratch);
   delete ctx;
   return LBX_OK;
 }
@@ -1541,6 +1614,42 @@ int lbx_partition(lbx_ctx* ctx, double* z, double* x, double* vz, double* vx, do
   l.nbx = nbx;
   l.n_out = reinterpret_cast<long long*>(n_out);
   return launch_push_step(ctx, l, stream, ex, false);
+}
+
+int lbx_fill_holes(lbx_ctx* ctx, double* z, double* x, double* vz, double* vx, double* kick_vz,
+                   double* kick_vx, const int64_t* removed, int64_t n_removed, int64_t n_new,
+                   void* stream) {
+  clear_error();
+  if (!ctx || n_removed < 0 || n_new < 0) return set_error(LBX_EINVAL, "bad argument");
+  if ((kick_vz == nullptr) != (kick_vx == nullptr))
+    return set_error(LBX_EINVAL, "kick velocity buffers must be given together");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n_removed > 0) {
+    if (ctx->fill_cap < n_removed) {
+      if (ctx->fill_scratch) {
+        cudaStreamSynchronize(s);
+        cudaFree(ctx->fill_scratch);
+      }
+      ctx->fill_scratch = nullptr;
+      const int64_t cap = std::max<int64_t>(n_removed, 1 << 16);
+      if (cudaMalloc(&ctx->fill_scratch, (size_t)cap * 16) != cudaSuccess)
+        return set_error(LBX_EOOM, "hole-fill scratch");
+      cudaMemsetAsync(ctx->fill_scratch + cap, 0, (size_t)cap * 8, s);
+      ctx->fill_cap = cap;
+    }
+    long long* holes = ctx->fill_scratch;
+    long long* tail = ctx->fill_scratch + ctx->fill_cap;
+    const unsigned grid = (unsigned)std::max(1ll, std::min(4096ll, (long long)((n_removed + 255) / 256)));
+    fill_mark_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const long long*>(removed), n_removed,
+                                          n_new, holes, tail, ctx->st);
+    fill_move_kernel<<<grid, 256, 0, s>>>(n_removed, n_new, holes, tail, ctx->st, z, x, vz, vx,
+                                          kick_vz, kick_vx);
+  }
+  fill_done_kernel<<<1, 1, 0, s>>>(ctx->st, n_new);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "fill_holes launch");
+  ctx->n_upper = n_new;
+  return LBX_OK;
 }
 
 int lbx_group_by_dest(const double* stage, const int32_t* stage_dest, int64_t count,

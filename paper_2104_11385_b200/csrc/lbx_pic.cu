@@ -40,9 +40,12 @@
 namespace lbx {
 namespace {
 
+#ifndef LBX_PIC_PAIRS
+#define LBX_PIC_PAIRS 1
+#endif
 constexpr int kPB = 256;                  // threads per CTA
 constexpr int kPW = kPB / 32;
-constexpr int kPPairs = 2;                // particle pairs per thread per chunk
+constexpr int kPPairs = LBX_PIC_PAIRS;    // particle pairs per thread per chunk
 constexpr int kPItems = 2 * kPPairs;
 constexpr int kPChunk = kPB * kPItems;    // 1024 particles per chunk
 constexpr int kPatchMax = 1536;           // cells per staged patch
@@ -112,7 +115,10 @@ __device__ __forceinline__ double cic(const Stencil& s, double a, double b, doub
 }
 
 template <bool kClock>
-__global__ void __launch_bounds__(kPB, 2) pic_push_kernel(PicParams p) {
+#ifndef LBX_PIC_MINB
+#define LBX_PIC_MINB 3
+#endif
+__global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned* s_cnt = reinterpret_cast<unsigned*>(smem_raw);          // nb
   unsigned* s_clk = s_cnt + p.nb;                                    // nb

@@ -148,6 +148,7 @@ class DeviceEngine:
         self.capacity = int(capacity)
         self.stage = torch.empty((cap, REC), **f64)
         self.stage_dest = torch.empty(cap, dtype=torch.int32, device=self.dev)
+        self.removed = torch.empty(cap, dtype=torch.int64, device=self.dev)
         self.send_counts = torch.zeros(world, dtype=torch.int64, device=self.dev)
         self.owner = torch.zeros(self.nb, dtype=torch.int32, device=self.dev)
         self.counts = torch.zeros(self.nb, dtype=torch.int64, device=self.dev)
@@ -161,7 +162,7 @@ class DeviceEngine:
         return _lib.ExchangeArgs(
             _lib.ptr(self.owner), self.rank, self.world, _lib.ptr(self.stage),
             _lib.ptr(self.stage_dest), self.capacity + 2, _lib.ptr(self.send_counts),
-            _lib.ptr(self.kvz), _lib.ptr(self.kvx))
+            _lib.ptr(self.kvz), _lib.ptr(self.kvx), _lib.ptr(self.removed), self.capacity + 2)
 
     def set_owner(self, owner: np.ndarray):
         self.owner.copy_(torch.from_numpy(np.asarray(owner, dtype=np.int32)))
@@ -197,11 +198,18 @@ class DeviceEngine:
         return self.send_counts, self.nout
 
     def commit(self, nout_host):
-        """Adopt the local count left by push/partition (host copy of nout)."""
+        """Adopt the local count left by push/partition (host copy of nout)
+        and compact: O(removed) hole filling (local order is not kept)."""
         if int(nout_host[1]) != 0:
             raise ValueError("particles outside the box grid or staging overflow "
                              f"(code {int(nout_host[1])})")
-        self.n = int(nout_host[0])
+        n_new = int(nout_host[0])
+        _lib.check(_lib.lib.lbx_fill_holes(
+            self.ctx.handle, _lib.ptr(self.z), _lib.ptr(self.x), _lib.ptr(self.vz),
+            _lib.ptr(self.vx), _lib.ptr(self.kvz), _lib.ptr(self.kvx), _lib.ptr(self.removed),
+            self.n - n_new, n_new, self.D._stream(self.dev)))
+        self.launches += 3
+        self.n = n_new
 
     def pack(self, sc: list) -> torch.Tensor:
         total = int(sum(sc))
