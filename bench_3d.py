@@ -1,0 +1,113 @@
+#!/usr/bin/env python
+"""Config C4: 3D blob, 256 boxes, SFC vs knapsack (parity unpinned: the
+reference is 2D only).
+
+Workload: 256 x 256 x 128 cells, 32-cell boxes (8 x 8 x 4 = 256 boxes), a
+spherical blob (centre (128, 128, 64), core 40, skirt 4, 2 particles/cell,
+seed 1) from the kick (radial 0.035 + drift 0.01), tiled R times (default
+140 -> ~1e8 particles), GpuClock costs.  Measured on one B200:
+  * fused 3D step throughput (particle-pushes/s) and HBM roofline
+    (72 B/particle: read z,y,x,vz,vy,vx, write z,y,x);
+  * for R = 1, 2, 4, 8 ranks and each strategy (knapsack, SFC): the LB
+    efficiency of the proposed mapping on the measured GpuClock costs AND
+    under true work, the number of off-rank box faces (SFC's locality
+    advantage), and the modelled R-GPU step time = measured 1-GPU step x
+    (max rank work / total work) -- a strong-scaling estimate, labelled as
+    such (one GPU is available this round).
+Prints one JSON object.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--replicas", type=int, default=140)
+    ap.add_argument("--steps", type=int, default=12)
+    ap.add_argument("--warmup", type=int, default=3)
+    args = ap.parse_args()
+
+    import torch
+
+    import bench
+    from paper_2104_11385_b200.balancer import BalancePolicy, efficiency, knapsack_assign, sfc_assign
+    from paper_2104_11385_b200.cost import CostVector, make_provider
+    from paper_2104_11385_b200.decomposition import DistributionMapping, morton_order_3d
+    from paper_2104_11385_b200.three_d import (Scenario3D, Simulation3D, kick_velocities_3d,
+                                               sample_blob_3d)
+
+    total = args.warmup + args.steps
+    cfg = Scenario3D("c4-3d-blob", (256, 256, 128), 32, 1, (128.0, 128.0, 64.0), 40.0, 4.0,
+                     2.0, kick_step=0, kick_speed=0.035, kick_drift=0.01, total_steps=total)
+    pos0 = sample_blob_3d(cfg)
+    kick0 = kick_velocities_3d(pos0, cfg)
+    R = args.replicas
+    dev = torch.device("cuda:0")
+    pos = torch.from_numpy(pos0).to(dev).repeat(R, 1)
+    kick = torch.from_numpy(kick0).to(dev).repeat(R, 1)
+    sim = Simulation3D(cfg, BalancePolicy(interval=total + 1), make_provider("gpuclock"),
+                       device=dev, positions=pos, kick=kick, record_counts=True)
+    del pos, kick
+    n = sim.n_init
+    sim.run(0, args.warmup)
+    torch.cuda.synchronize()
+    ms = []
+    stream = torch.cuda.current_stream(dev)
+    for s in range(args.warmup, total):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sim.run(s, s + 1)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    step_ms = float(np.mean(ms))
+    peak, peak_src = bench.peaks()
+    achieved = 72 * n / (step_ms / 1e3) / 1e9
+    counts = sim.out["count_trace"][total - 1]
+    clk = sim.out["cost_trace"][total - 1]
+    work = cfg.work_weights[0] * counts + cfg.work_weights[1] * 32 ** 3
+    curve = morton_order_3d(cfg.grid)
+    g = cfg.grid
+    ids = np.arange(cfg.n_boxes).reshape(g)
+    fa = np.concatenate([ids[:-1].ravel(), ids[:, :-1].ravel(), ids[:, :, :-1].ravel()])
+    fb = np.concatenate([ids[1:].ravel(), ids[:, 1:].ravel(), ids[:, :, 1:].ravel()])
+    scaling = {}
+    for r in (1, 2, 4, 8):
+        row = {}
+        for name in ("knapsack", "sfc"):
+            cv = CostVector(values=clk)
+            own = (knapsack_assign(cv, r).owner if name == "knapsack"
+                   else sfc_assign(cv, curve, r).owner)
+            dm = DistributionMapping(owner=own, n_ranks=r)
+            e_clk = efficiency(cv, dm)
+            e_true = efficiency(CostVector(values=work), dm)
+            loads = np.bincount(own, weights=work, minlength=r)
+            row[name] = {"eff_gpuclock": e_clk, "eff_true_work": e_true,
+                         "offrank_faces": int((own[fa] != own[fb]).sum()),
+                         "model_step_ms": step_ms * loads.max() / loads.sum(),
+                         "model_speedup": float(loads.sum() / loads.max())}
+        scaling[str(r)] = row
+    out = {"workload": f"3D blob 256x256x128 cells, 256 boxes (8x8x4), {n} particles "
+                       f"({len(pos0)} x {R} replicas), GpuClock", "particles": n,
+           "step_ms": step_ms, "pushes_per_s": n / (step_ms / 1e3),
+           "roofline": {"bytes_per_particle": 72, "achieved_gbs": achieved, "peak_gbs": peak,
+                        "frac": achieved / peak, "peak_source": peak_src,
+                        "note": "whole step (fused 3D kernel + compaction launch + host LB step)"},
+           "strategies_by_ranks": scaling,
+           "note": "multi-rank step times are a model (measured 1-GPU step x max rank work share)"}
+    sim.close()
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -14,9 +14,9 @@ Modes:
   torchrun --nproc-per-node N bench_lb.py      one rank per GPU (NCCL);
       per-step time = max over ranks of the step's device time.
   python bench_lb.py --emulate R               one GPU, R ranks as threads;
-      each rank's push/deposit kernels run alone (a lock serializes them)
-      and are timed with CUDA events; the emulated step time is the MAX over
-      ranks of those times -- the compute-imbalance part of an R-GPU step,
+      each rank's fused step kernel runs alone (a lock serializes them) and
+      is timed with CUDA events recorded by libLBX immediately around its
+      launch; the emulated step time is the MAX over ranks of those times -- the compute-imbalance part of an R-GPU step,
       measured on B200 hardware.  Exchange/migration traffic is reported
       (particles moved) but not timed in this mode.
 Prints one JSON object.
@@ -56,17 +56,19 @@ def make_timed_engine(lock, log):
 
     class TimedEngine(DeviceEngine):
         def push(self, wp, wc):
+            import ctypes as C
+
             import torch
+
+            from paper_2104_11385_b200 import _lib
             st = torch.cuda.current_stream()   # this rank's own stream
-            with lock:
+            with lock:   # ranks' kernels run one at a time (no SM sharing)
                 st.synchronize()
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(st)
+                _lib.lib.lbx_ctx_enable_timing(self.ctx.handle, 1)
                 out = super().push(wp, wc)
-                e1.record(st)
-                e1.synchronize()
-                log.setdefault(self.rank, []).append(e0.elapsed_time(e1))
+                ms = C.c_float()
+                _lib.check(_lib.lib.lbx_ctx_last_kernel_ms(self.ctx.handle, C.byref(ms)))
+                log.setdefault(self.rank, []).append(ms.value)
             return out
 
     return TimedEngine

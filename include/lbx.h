@@ -57,6 +57,11 @@ int lbx_ctx_get_count(lbx_ctx* ctx, int64_t* n_host, void* stream); /* syncs */
 /* Persistent-grid size the step kernels launch with (0 = auto: resident
  * CTAs per SM x SMs). */
 int lbx_ctx_set_grid(lbx_ctx* ctx, int ctas);
+/* Kernel timing: when on, the main streaming kernel of each step call is
+ * bracketed by CUDA events recorded immediately around its launch;
+ * lbx_ctx_last_kernel_ms waits for the end event and returns milliseconds. */
+int lbx_ctx_enable_timing(lbx_ctx* ctx, int on);
+int lbx_ctx_last_kernel_ms(lbx_ctx* ctx, float* ms);
 
 /* ------------------------------------------------------------------------
  * Drop-in kernels (reference plugin point 1, kernels.py:10-25).
@@ -134,6 +139,24 @@ typedef struct lbx_step_args {
 } lbx_step_args;
 
 int lbx_push_step(lbx_ctx* ctx, const lbx_step_args* args, void* stream);
+
+/* 3D fused step (config C4, parity unpinned): SoA float64 z, y, x, vz, vy, vx
+ * in place (72 B/particle), absorbing box [0,Ez)x[0,Ey)x[0,Ex), per-box
+ * counts / heuristic cost / GpuClock into (nbz*nby*nbx) box vectors, stable
+ * compaction.  box_size must be a power of two dividing the extents. */
+typedef struct lbx_step3d_args {
+  double *z, *y, *x, *vz, *vy, *vx;
+  int32_t extent_z, extent_y, extent_x, box_size;
+  double w_particle, w_cell;
+  uint32_t flags;               /* LBX_STEP_CLOCK */
+  int64_t* counts_out;
+  double* cost_out;
+  uint64_t* clk_out;
+  int64_t* n_out;
+  int64_t* err_out;
+} lbx_step3d_args;
+
+int lbx_push_step_3d(lbx_ctx* ctx, const lbx_step3d_args* args, void* stream);
 
 /* Replaces cost.py:83-95 heuristic_cost on device vectors:
  * cost[i] = w_particle*particles[i] + w_cell*cells[i], two separately
@@ -222,6 +245,10 @@ typedef struct lbx_sim_config {
    * advance) or LBX_PHYSICS_PIC (lbx_pic_step; needs lbx_sim_set_fields) */
   int32_t physics;
   double pic_dt, pic_q_over_m, pic_q_times_w;
+  /* 3D box decomposition (config C4; the reference is 2D only): extent_y > 0
+   * makes the LB object 3D -- boxes (bz*nby + by)*nbx + bx, 3D Morton curve,
+   * interior faces along z, y, x, M^3 cells per box. */
+  int32_t extent_y;
 } lbx_sim_config;
 
 #define LBX_PHYSICS_SURROGATE 0

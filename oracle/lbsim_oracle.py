@@ -544,3 +544,39 @@ def run_simulation(cfg, *, record_counts=False, record_positions_at=()):
     if record_positions_at:
         out["positions"] = positions
     return out
+
+
+# ----------------------------------------------------------------------------
+# 3D extension (config C4) -- PARITY UNPINNED: the reference is 2D only
+# (SPEC.md:96).  Same rules carried to a third axis: boxes are
+# (bz*nby + by)*nbx + bx; Morton puts axis 0 on bits 0,3,6,...
+# ----------------------------------------------------------------------------
+
+def advance_particles_3d(pos, vel, extent):
+    new = pos + vel
+    alive = np.ones(pos.shape[0], dtype=bool)
+    for a in range(3):
+        alive &= (new[:, a] >= 0.0) & (new[:, a] < extent[a])
+    return np.ascontiguousarray(new[alive]), np.ascontiguousarray(vel[alive])
+
+
+def bin_particles_3d(pos, box_size, grid):
+    b = [np.trunc(pos[:, a] / box_size).astype(np.int64) for a in range(3)]
+    ids = (b[0] * grid[1] + b[1]) * grid[2] + b[2]
+    return np.bincount(ids, minlength=grid[0] * grid[1] * grid[2]).astype(np.int64)
+
+
+def morton_order_3d(grid):
+    def spread3(v):
+        out, s = 0, 0
+        while v:
+            out |= (v & 1) << (3 * s)
+            v >>= 1
+            s += 1
+        return out
+    n0, n1, n2 = grid
+    codes = []
+    for i in range(n0 * n1 * n2):
+        a, b, c = i // (n1 * n2), (i // n2) % n1, i % n2
+        codes.append(spread3(a) | (spread3(b) << 1) | (spread3(c) << 2))
+    return np.argsort(np.array(codes, dtype=np.int64), kind="stable").astype(np.int64)

@@ -45,7 +45,7 @@ class SimConfig(C.Structure):
                 ("comm_per_face", f64), ("gather", f64),
                 ("redistribute_per_particle", f64), ("redistribute_latency", f64),
                 ("capacity_particles", i64), ("physics", i32), ("pic_dt", f64),
-                ("pic_q_over_m", f64), ("pic_q_times_w", f64)]
+                ("pic_q_over_m", f64), ("pic_q_times_w", f64), ("extent_y", i32)]
 
 
 class SimOutputs(C.Structure):
@@ -69,6 +69,8 @@ SIGNATURES = {
     "lbx_ctx_set_count": (i32, [vp, i64, vp]),
     "lbx_ctx_get_count": (i32, [vp, P(i64), vp]),
     "lbx_ctx_set_grid": (i32, [vp, i32]),
+    "lbx_ctx_enable_timing": (i32, [vp, i32]),
+    "lbx_ctx_last_kernel_ms": (i32, [vp, P(C.c_float)]),
     "lbx_advance_particles": (i32, [vp, vp, vp, i64, f64, f64, vp, vp, vp, vp]),
     "lbx_bin_particles": (i32, [vp, i64, f64, i32, i32, vp, vp, vp]),
     "lbx_push_step": (i32, [vp, P(StepArgs), vp]),
@@ -128,6 +130,17 @@ class PicArgs(C.Structure):
 
 SIGNATURES["lbx_pic_step"] = (i32, [vp, P(PicArgs), vp])
 SIGNATURES["lbx_sim_set_fields"] = (i32, [vp, vp, vp, vp])
+
+
+class Step3DArgs(C.Structure):
+    """lbx_step3d_args (include/lbx.h)."""
+    _fields_ = [("z", vp), ("y", vp), ("x", vp), ("vz", vp), ("vy", vp), ("vx", vp),
+                ("extent_z", i32), ("extent_y", i32), ("extent_x", i32), ("box_size", i32),
+                ("w_particle", f64), ("w_cell", f64), ("flags", u32), ("counts_out", vp),
+                ("cost_out", vp), ("clk_out", vp), ("n_out", vp), ("err_out", vp)]
+
+
+SIGNATURES["lbx_push_step_3d"] = (i32, [vp, P(Step3DArgs), vp])
 
 
 class LBXError(RuntimeError):

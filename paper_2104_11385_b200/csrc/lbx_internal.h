@@ -67,6 +67,9 @@ struct lbx_ctx {
   int64_t pic_cells = 0;
   long long* fill_scratch = nullptr;      // hole-fill: holes[cap] + tail flags[cap]
   int64_t fill_cap = 0;
+  bool timing = false;                    // lbx_ctx_enable_timing
+  void* ev0 = nullptr;                    // cudaEvent_t
+  void* ev1 = nullptr;
 };
 
 #include <vector>

@@ -455,6 +455,199 @@ __global__ void __launch_bounds__(kBlock, 4) stream_kernel(StepParams p) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// stream3d_kernel: 3D push + absorb + per-box counts / GpuClock (config C4)
+// SoA z, y, x, vz, vy, vx in place; absorbed particles get z = -1 so the
+// stable compaction (which tests z, x) drops them.  Box size power of two.
+// ---------------------------------------------------------------------------
+struct Step3DParams {
+  double *z, *y, *x;
+  const double *vz, *vy, *vx;
+  double ez, ey, ex, inv_m;
+  int nbz, nby, nbx, nb;
+  int smem_hist;
+  DevState* st;
+  unsigned long long* g_cnt;
+  unsigned long long* g_clk;
+  long long* counts_out;
+  double* cost_out;
+  unsigned long long* clk_out;
+  long long* n_out;
+  long long* err_out;
+  double wp, wc, cells;
+};
+
+template <bool kClock>
+__global__ void __launch_bounds__(kBlock, 4) stream3d_kernel(Step3DParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned* s_cnt = reinterpret_cast<unsigned*>(smem_raw);
+  unsigned* s_clk = s_cnt + p.nb;
+  __shared__ long long s_n;
+  __shared__ int s_last;
+  __shared__ unsigned long long s_red[kWarps];
+  __shared__ long long s_min[kWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_n = *((volatile long long*)&p.st->n);
+  if (p.smem_hist)
+    for (int b = tid; b < p.nb; b += kBlock) {
+      s_cnt[b] = 0u;
+      if (kClock) s_clk[b] = 0u;
+    }
+  __syncthreads();
+  const long long n = s_n, npairs = (n + 1) >> 1;
+  const long long stride = (long long)gridDim.x * kBlock * kPairs;
+  double2* z2 = reinterpret_cast<double2*>(p.z);
+  double2* y2 = reinterpret_cast<double2*>(p.y);
+  double2* x2 = reinterpret_cast<double2*>(p.x);
+  const double2* vz2 = reinterpret_cast<const double2*>(p.vz);
+  const double2* vy2 = reinterpret_cast<const double2*>(p.vy);
+  const double2* vx2 = reinterpret_cast<const double2*>(p.vx);
+  unsigned long long removed = 0;
+  long long first_out = LLONG_MAX, err = 0;
+  int iter = 0;
+  for (long long q0 = (long long)blockIdx.x * kBlock * kPairs; q0 < npairs; q0 += stride) {
+    long long t0 = 0;
+    if (kClock) t0 = clock64();
+    int box[2 * kPairs];
+#pragma unroll
+    for (int r = 0; r < kPairs; ++r) {
+      const long long q = q0 + r * kBlock + tid;
+      const bool any = q < npairs;
+      double2 a = make_double2(-1.0, -1.0), b = a, c = a;
+      double2 d = make_double2(0.0, 0.0), e = d, f = d;
+      if (any) {
+        a = __ldcs(z2 + q);
+        b = __ldcs(y2 + q);
+        c = __ldcs(x2 + q);
+        d = __ldcs(vz2 + q);
+        e = __ldcs(vy2 + q);
+        f = __ldcs(vx2 + q);
+      }
+      double nz[2] = {__dadd_rn(a.x, d.x), __dadd_rn(a.y, d.y)};
+      const double ny[2] = {__dadd_rn(b.x, e.x), __dadd_rn(b.y, e.y)};
+      const double nx[2] = {__dadd_rn(c.x, f.x), __dadd_rn(c.y, f.y)};
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const long long i = 2 * q + t;
+        const bool valid = i < n;
+        const bool keep = valid && nz[t] >= 0.0 && nz[t] < p.ez && ny[t] >= 0.0 &&
+                          ny[t] < p.ey && nx[t] >= 0.0 && nx[t] < p.ex;
+        box[2 * r + t] = -1;
+        if (keep) {
+          const int bz = (int)__dmul_rn(nz[t], p.inv_m), by = (int)__dmul_rn(ny[t], p.inv_m),
+                    bx = (int)__dmul_rn(nx[t], p.inv_m);
+          if (bz < p.nbz && by < p.nby && bx < p.nbx) box[2 * r + t] = (bz * p.nby + by) * p.nbx + bx;
+          else ++err;
+        } else if (valid) {
+          ++removed;
+          first_out = min(first_out, i);
+          nz[t] = -1.0;  // compaction sentinel
+        }
+      }
+      if (any) {
+        __stcs(z2 + q, make_double2(nz[0], nz[1]));
+        __stcs(y2 + q, make_double2(ny[0], ny[1]));
+        __stcs(x2 + q, make_double2(nx[0], nx[1]));
+      }
+    }
+    unsigned dt = 0;
+    if (kClock) dt = (unsigned)min(clock64() - t0, (long long)(1 << 20)) >> kClockShift;
+    int cur = -1;
+    unsigned run = 0;
+#pragma unroll
+    for (int k = 0; k < 2 * kPairs; ++k) {
+      if (box[k] != cur) {
+        if (cur >= 0) {
+          if (p.smem_hist) {
+            atomicAdd(s_cnt + cur, run);
+            if (kClock) atomicAdd(s_clk + cur, dt * run);
+          } else {
+            atomicAdd(p.g_cnt + cur, (unsigned long long)run);
+            if (kClock) atomicAdd(p.g_clk + cur, (unsigned long long)(dt * run));
+          }
+        }
+        cur = box[k];
+        run = 0;
+      }
+      run += box[k] >= 0 ? 1u : 0u;
+    }
+    const int cur0 = __shfl_sync(kFull, cur, 0);
+    const bool uni = __all_sync(kFull, cur == cur0);
+    unsigned tot = run, clk = dt * run;
+    if (uni) {
+      tot = __reduce_add_sync(kFull, run);
+      clk = kClock ? __reduce_add_sync(kFull, dt * run) : 0u;
+    }
+    if ((uni ? lane == 0 && cur0 >= 0 : cur >= 0) && tot) {
+      const int b = uni ? cur0 : cur;
+      if (p.smem_hist) {
+        atomicAdd(s_cnt + b, tot);
+        if (kClock) atomicAdd(s_clk + b, clk);
+      } else {
+        atomicAdd(p.g_cnt + b, (unsigned long long)tot);
+        if (kClock) atomicAdd(p.g_clk + b, (unsigned long long)clk);
+      }
+    }
+    if (p.smem_hist && ++iter == kFlushIters) {
+      iter = 0;
+      __syncthreads();
+      for (int b = tid; b < p.nb; b += kBlock) {
+        if (s_cnt[b]) atomicAdd(p.g_cnt + b, (unsigned long long)s_cnt[b]), s_cnt[b] = 0u;
+        if (kClock && s_clk[b]) atomicAdd(p.g_clk + b, (unsigned long long)s_clk[b]), s_clk[b] = 0u;
+      }
+      __syncthreads();
+    }
+  }
+  const unsigned long long wa = (unsigned long long)warp_sum_ll((long long)removed);
+  const long long wm = warp_min_ll(first_out), we = warp_sum_ll(err);
+  if (lane == 0) {
+    s_red[warp] = wa;
+    s_min[warp] = wm;
+    if (we) atomicAdd((unsigned long long*)&p.st->err, (unsigned long long)we);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long ta = 0;
+    long long tm = LLONG_MAX;
+    for (int w = 0; w < kWarps; ++w) ta += s_red[w], tm = min(tm, s_min[w]);
+    if (ta) {
+      atomicAdd(&p.st->leavers, ta);
+      atomicMin(&p.st->first_leaver, tm);
+    }
+  }
+  if (p.smem_hist)
+    for (int b = tid; b < p.nb; b += kBlock) {
+      if (s_cnt[b]) atomicAdd(p.g_cnt + b, (unsigned long long)s_cnt[b]);
+      if (kClock && s_clk[b]) atomicAdd(p.g_clk + b, (unsigned long long)s_clk[b]);
+    }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(&p.st->done, 1u) == gridDim.x - 1) ? 1 : 0;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int b = tid; b < p.nb; b += kBlock) {
+    const unsigned long long c = atomicExch(p.g_cnt + b, 0ull);
+    if (p.counts_out) p.counts_out[b] = (long long)c;
+    if (p.cost_out)
+      p.cost_out[b] = __dadd_rn(__dmul_rn(p.wp, (double)(long long)c), __dmul_rn(p.wc, p.cells));
+    if (kClock) {
+      const unsigned long long k = atomicExch(p.g_clk + b, 0ull);
+      if (p.clk_out) p.clk_out[b] = k << kClockShift;
+    }
+  }
+  if (tid == 0) {
+    const long long n_new = n - (long long)*((volatile unsigned long long*)&p.st->leavers);
+    if (p.n_out) *p.n_out = n_new;
+    if (p.err_out) *p.err_out = *((volatile long long*)&p.st->err);
+    p.st->n_old = n;
+    p.st->n = n_new;
+    p.st->done = 0u;
+    __threadfence_system();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // scan_kernel (decoupled look-back stable compaction)
 // ---------------------------------------------------------------------------
@@ -978,7 +1171,9 @@ int launch_stream(lbx_ctx* ctx, const StepParams& p, cudaStream_t s) {
   const long long work = (ctx->n_upper + 2ll * kBlock * kPairs - 1) / (2ll * kBlock * kPairs);
   int rc = occupancy_grid(ctx, kern, smem, std::max(1ll, work), &grid);
   if (rc) return rc;
+  if (ctx->timing) cudaEventRecord((cudaEvent_t)ctx->ev0, s);
   kern<<<grid, kBlock, smem, s>>>(p);
+  if (ctx->timing) cudaEventRecord((cudaEvent_t)ctx->ev1, s);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "stream_kernel launch");
   return LBX_OK;
@@ -1327,6 +1522,7 @@ int lbx_ctx_destroy(lbx_ctx* ctx) {
   destroy_pipe(ctx->pipe);
   if (ctx->pic_acc) cudaFree(ctx->pic_acc);
   if (ctx->fill_scratch) cudaFree(ctx->fill_scratch);
+  if (ctx->ev0) cudaEventDestroy((cudaEvent_t)ctx->ev0), cudaEventDestroy((cudaEvent_t)ctx->ev1);
   delete ctx;
   return LBX_OK;
 }
@@ -1360,6 +1556,26 @@ int lbx_ctx_get_count(lbx_ctx* ctx, int64_t* n_host, void* stream) {
   if (e != cudaSuccess) return cuda_fail(e, "get_count");
   *n_host = ctx->host_scratch[0];
   ctx->n_upper = *n_host;
+  return LBX_OK;
+}
+
+int lbx_ctx_enable_timing(lbx_ctx* ctx, int on) {
+  clear_error();
+  if (!ctx) return set_error(LBX_EINVAL, "context is NULL");
+  if (on && !ctx->ev0) {
+    cudaEventCreate((cudaEvent_t*)&ctx->ev0);
+    cudaEventCreate((cudaEvent_t*)&ctx->ev1);
+  }
+  ctx->timing = on != 0;
+  return LBX_OK;
+}
+
+int lbx_ctx_last_kernel_ms(lbx_ctx* ctx, float* ms) {
+  clear_error();
+  if (!ctx || !ms || !ctx->ev0) return set_error(LBX_EINVAL, "timing not enabled");
+  cudaError_t e = cudaEventSynchronize((cudaEvent_t)ctx->ev1);
+  if (e == cudaSuccess) e = cudaEventElapsedTime(ms, (cudaEvent_t)ctx->ev0, (cudaEvent_t)ctx->ev1);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel timing");
   return LBX_OK;
 }
 
@@ -1614,6 +1830,67 @@ int lbx_partition(lbx_ctx* ctx, double* z, double* x, double* vz, double* vx, do
   l.nbx = nbx;
   l.n_out = reinterpret_cast<long long*>(n_out);
   return launch_push_step(ctx, l, stream, ex, false);
+}
+
+int lbx_push_step_3d(lbx_ctx* ctx, const lbx_step3d_args* a, void* stream) {
+  clear_error();
+  if (!ctx || !a) return set_error(LBX_EINVAL, "NULL argument");
+  const int M = a->box_size;
+  if (M < 1 || (M & (M - 1)) || a->extent_z % M || a->extent_y % M || a->extent_x % M)
+    return set_error(LBX_EINVAL, "3D box_size must be a power of two dividing the extents");
+  if (((uintptr_t)a->z | (uintptr_t)a->y | (uintptr_t)a->x | (uintptr_t)a->vz |
+       (uintptr_t)a->vy | (uintptr_t)a->vx) & 15u)
+    return set_error(LBX_EINVAL, "particle arrays must be 16-byte aligned");
+  const int nbz = a->extent_z / M, nby = a->extent_y / M, nbx = a->extent_x / M;
+  const long long nb = (long long)nbz * nby * nbx;
+  if (nb > (1ll << 30)) return set_error(LBX_EINVAL, "too many boxes");
+  int rc = ensure_accumulators(ctx, (int32_t)nb);
+  if (rc) return rc;
+  rc = reserve_status(ctx, ctx->n_upper);
+  if (rc) return rc;
+  Step3DParams p{};
+  p.z = a->z;
+  p.y = a->y;
+  p.x = a->x;
+  p.vz = a->vz;
+  p.vy = a->vy;
+  p.vx = a->vx;
+  p.ez = a->extent_z;
+  p.ey = a->extent_y;
+  p.ex = a->extent_x;
+  p.inv_m = 1.0 / M;
+  p.nbz = nbz;
+  p.nby = nby;
+  p.nbx = nbx;
+  p.nb = (int)nb;
+  p.smem_hist = nb <= kSmemBoxesMax ? 1 : 0;
+  p.st = ctx->st;
+  p.g_cnt = ctx->acc;
+  p.g_clk = ctx->acc + ctx->acc_boxes;
+  p.counts_out = reinterpret_cast<long long*>(a->counts_out);
+  p.cost_out = a->cost_out;
+  p.clk_out = reinterpret_cast<unsigned long long*>(a->clk_out);
+  p.n_out = reinterpret_cast<long long*>(a->n_out);
+  p.err_out = reinterpret_cast<long long*>(a->err_out);
+  p.wp = a->w_particle;
+  p.wc = a->w_cell;
+  p.cells = (double)M * M * M;
+  const bool clock = (a->flags & LBX_STEP_CLOCK) != 0;
+  auto kern = clock ? stream3d_kernel<true> : stream3d_kernel<false>;
+  const size_t smem = p.smem_hist ? (size_t)nb * 4 * (clock ? 2 : 1) : 0;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int grid = 0;
+  rc = occupancy_grid(ctx, kern, smem,
+                      std::max(1ll, (long long)((ctx->n_upper + 2ll * kBlock * kPairs - 1) /
+                                                (2ll * kBlock * kPairs))), &grid);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  kern<<<grid, kBlock, smem, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "stream3d_kernel launch");
+  return launch_compact(ctx, a->z, a->x, a->y, a->vz, a->vy, a->vx, (double)a->extent_z,
+                        (double)a->extent_x, stream);
 }
 
 int lbx_fill_holes(lbx_ctx* ctx, double* z, double* x, double* vz, double* vx, double* kick_vz,

@@ -30,6 +30,8 @@ using namespace lbx;
 struct lbx_lb {
   lbx_sim_config cfg{};
   int32_t nbz = 0, nbx = 0, nb = 0;
+  int32_t nby = 1;       // 3D (extent_y > 0)
+  double cells = 0.0;    // cells per box: M^2 (2D) or M^3 (3D)
   std::vector<int64_t> curve, face_a, face_b;
   std::vector<int64_t> owner, prop, prev;
   std::vector<double> work, scratch, rank_acc;
@@ -123,7 +125,7 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
   const lbx_sim_config& c = s->cfg;
   const int nb = s->nb;
   const int32_t R = c.n_ranks;
-  const double cells = (double)((int64_t)c.box_size * c.box_size);
+  const double cells = s->cells;
   for (int b = 0; b < nb; ++b) s->work[b] = c.work_wp * (double)counts[b] + c.work_wc * cells;
   double* cost = o->cost_trace + (size_t)step * nb;
   switch (c.cost_kind) {
@@ -385,20 +387,41 @@ int lbx_lb_create(lbx_lb** out, const lbx_sim_config* cfg, const int64_t* initia
   s->cfg = c;
   s->nbz = c.extent_z / c.box_size;
   s->nbx = c.extent_x / c.box_size;
-  s->nb = s->nbz * s->nbx;
+  const bool three_d = c.extent_y > 0;
+  if (three_d) {
+    if (c.extent_y % c.box_size) {
+      delete s;
+      return set_error(LBX_EINVAL, "box_size %d must divide the y-extent", c.box_size);
+    }
+    s->nby = c.extent_y / c.box_size;
+  }
+  s->nb = s->nbz * s->nby * s->nbx;
+  s->cells = three_d ? (double)c.box_size * c.box_size * c.box_size
+                     : (double)((int64_t)c.box_size * c.box_size);
   const int nb = s->nb;
   s->curve.resize(nb);
-  lbx_morton_order(s->nbz, s->nbx, s->curve.data());
-  for (int bz = 0; bz + 1 < s->nbz; ++bz)
-    for (int bx = 0; bx < s->nbx; ++bx) {
-      s->face_a.push_back(bz * s->nbx + bx);
-      s->face_b.push_back((bz + 1) * s->nbx + bx);
-    }
+  if (three_d) lbx_morton_order_3d(s->nbz, s->nby, s->nbx, s->curve.data());
+  else lbx_morton_order(s->nbz, s->nbx, s->curve.data());
+  const int NY = s->nby, NX = s->nbx;
+  auto id = [&](int bz, int by, int bx) { return ((int64_t)bz * NY + by) * NX + bx; };
+  for (int bz = 0; bz + 1 < s->nbz; ++bz)   // z-neighbours first, then y, then x
+    for (int by = 0; by < NY; ++by)
+      for (int bx = 0; bx < NX; ++bx) {
+        s->face_a.push_back(id(bz, by, bx));
+        s->face_b.push_back(id(bz + 1, by, bx));
+      }
   for (int bz = 0; bz < s->nbz; ++bz)
-    for (int bx = 0; bx + 1 < s->nbx; ++bx) {
-      s->face_a.push_back(bz * s->nbx + bx);
-      s->face_b.push_back(bz * s->nbx + bx + 1);
-    }
+    for (int by = 0; by + 1 < NY; ++by)
+      for (int bx = 0; bx < NX; ++bx) {
+        s->face_a.push_back(id(bz, by, bx));
+        s->face_b.push_back(id(bz, by + 1, bx));
+      }
+  for (int bz = 0; bz < s->nbz; ++bz)
+    for (int by = 0; by < NY; ++by)
+      for (int bx = 0; bx + 1 < NX; ++bx) {
+        s->face_a.push_back(id(bz, by, bx));
+        s->face_b.push_back(id(bz, by, bx + 1));
+      }
   s->owner.assign(nb, 0);
   if (initial_owner) {
     for (int b = 0; b < nb; ++b) {
@@ -447,6 +470,8 @@ int lbx_lb_owner(lbx_lb* lb, int64_t* owner) {
 int lbx_sim_create(lbx_sim** out, lbx_ctx* ctx, const lbx_sim_config* cfg) {
   clear_error();
   if (!out || !ctx || !cfg) return set_error(LBX_EINVAL, "NULL argument");
+  if (cfg->extent_y > 0)
+    return set_error(LBX_EINVAL, "3D runs use lbx_push_step_3d + lbx_lb (Simulation3D)");
   lbx_lb* lb = nullptr;
   int rc = lbx_lb_create(&lb, cfg, nullptr);
   if (rc) return rc;

@@ -137,3 +137,10 @@ def test_contract_errors(L):
         _ks(L, [1.0], 0, 1.5)
     with pytest.raises(ValueError, match="owner"):
         _eff(L, [1.0, 2.0], [0, 5], 2)
+
+
+def test_morton_3d_vs_oracle(L):
+    for g in ((1, 1, 1), (2, 2, 2), (8, 8, 4), (3, 5, 2)):
+        out = np.empty(g[0] * g[1] * g[2], dtype=np.int64)
+        L.check(L.lib.lbx_morton_order_3d(*g, L.ptr(out)))
+        assert np.array_equal(out, O.morton_order_3d(g)), g
