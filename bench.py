@@ -322,6 +322,9 @@ def run_lbx(args, rank, world, local_rank):
     tpp = traffic_per_push()
     effs = [m.efficiency_after for m in res.metrics]
 
+    # ---- the reference's own C2 size (801,499 particles, 1 replica) ----
+    c2n = c2_native(args, dev, spec, sc, pos0, kick0)
+
     # ---- e2e through the reference-facing C-ABI with host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -352,6 +355,7 @@ def run_lbx(args, rank, world, local_rank):
                      "kernel_ms": kernel_s * 1e3,
                      "traffic": None if tpp is None else tpp * per_launch},
         "clocks": clocks.summary(),
+        "c2_native": c2n,
     }
     if e2e is not None:
         line["e2e"] = e2e
@@ -361,6 +365,35 @@ def run_lbx(args, rank, world, local_rank):
     _lib.lib.lbx_sim_destroy(sim.handle)
     sim.handle = None
     del D
+
+
+def c2_native(args, dev, spec, sc, pos0, kick0, steps=400):
+    """The C2 workload at the reference's own size (one replica): a
+    latency-bound regime (38 MB of state, L2-resident); whole native loop
+    timed with CUDA events."""
+    from dataclasses import replace as _replace
+
+    import torch
+
+    from paper_2104_11385_b200.workload import Simulation
+
+    sc1 = _replace(sc, total_steps=steps + 20)
+    sim = Simulation(sc1, spec.policy, spec.build_provider(), device=dev,
+                     positions=torch.from_numpy(pos0).to(dev), kick=torch.from_numpy(kick0).to(dev))
+    sim.run(0, 20)
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    sim.run(20, steps + 20)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    n = pos0.shape[0]
+    sim.close()
+    return {"particles": n, "steps": steps, "us_per_step": 1e3 * ms / steps,
+            "pushes_per_s": n * steps / (ms / 1e3),
+            "note": "L2-resident, launch/latency bound; incl. host LB loop"}
 
 
 def run_lbx_dist(args, rank, world, dev):

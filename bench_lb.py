@@ -38,7 +38,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 
-def scenario(ranks, steps, policy):
+def scenario(ranks, steps, policy, speed=0.035, drift=0.01):
     from paper_2104_11385_b200.balancer import BalancePolicy
     from paper_2104_11385_b200.scenarios import apply_overrides, load_spec
     from paper_2104_11385_b200.workload import BlobSpec, KickSpec
@@ -47,7 +47,7 @@ def scenario(ranks, steps, policy):
                            policy="knapsack" if policy == "dynamic" else policy)
     sc = replace(spec.scenario, blob=BlobSpec(center=(60.0, 480.0), core_radius=44.0,
                                               edge_scale=4.0, particles_per_cell=55.0),
-                 kick=KickSpec(step=0, speed=0.035, drift=0.01), initial_mapping="slab")
+                 kick=KickSpec(step=0, speed=speed, drift=drift), initial_mapping="slab")
     return spec, sc
 
 
@@ -74,13 +74,13 @@ def make_timed_engine(lock, log):
     return TimedEngine
 
 
-def run_emulated(R, steps, replicas, policy):
+def run_emulated(R, steps, replicas, policy, speed=0.035, drift=0.01):
     import torch
 
     import bench
     from paper_2104_11385_b200.parallel import DistributedSimulation, ThreadComm
 
-    spec, sc = scenario(R, steps, policy)
+    spec, sc = scenario(R, steps, policy, speed, drift)
     from paper_2104_11385_b200.workload import kick_velocities, sample_blob
     pos = sample_blob(sc)
     kick = kick_velocities(pos, sc)
@@ -125,6 +125,8 @@ def main():
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--replicas", type=int, default=128)
     ap.add_argument("--warmup-steps", type=int, default=1)
+    ap.add_argument("--speed", type=float, default=0.035, help="kick speed (cells/step)")
+    ap.add_argument("--drift", type=float, default=0.01, help="axial drift (cells/step)")
     args = ap.parse_args()
     if not args.emulate:
         raise SystemExit("multi-GPU mode: run under torchrun with bench.py --gpus N for the "
@@ -134,10 +136,11 @@ def main():
     R = args.emulate
     out = {"mode": f"emulated {R} ranks on one B200 (per-rank kernels timed alone; "
                    "step time = max over ranks)", "ranks": R, "steps": args.steps,
-           "policies": {}}
+           "kick": {"speed": args.speed, "drift": args.drift}, "policies": {}}
     w = args.warmup_steps
     for policy in ("none", "static", "dynamic"):
-        per_step, res, moved, n = run_emulated(R, args.steps, args.replicas, policy)
+        per_step, res, moved, n = run_emulated(R, args.steps, args.replicas, policy,
+                                               args.speed, args.drift)
         effs = [m.efficiency_after for m in res.metrics]
         out["policies"][policy] = {
             "time_ms": float(per_step[w:].sum()), "ms_per_step": float(per_step[w:].mean()),

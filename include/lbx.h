@@ -154,6 +154,10 @@ typedef struct lbx_step3d_args {
   uint64_t* clk_out;
   int64_t* n_out;
   int64_t* err_out;
+  int64_t* removed_list;        /* optional: list removed indices and skip the
+                                   stable compaction (then lbx_fill_holes with
+                                   z, x, y, vz, vy, vx in the six slots) */
+  int64_t removed_cap;
 } lbx_step3d_args;
 
 int lbx_push_step_3d(lbx_ctx* ctx, const lbx_step3d_args* args, void* stream);

@@ -137,7 +137,8 @@ class Step3DArgs(C.Structure):
     _fields_ = [("z", vp), ("y", vp), ("x", vp), ("vz", vp), ("vy", vp), ("vx", vp),
                 ("extent_z", i32), ("extent_y", i32), ("extent_x", i32), ("box_size", i32),
                 ("w_particle", f64), ("w_cell", f64), ("flags", u32), ("counts_out", vp),
-                ("cost_out", vp), ("clk_out", vp), ("n_out", vp), ("err_out", vp)]
+                ("cost_out", vp), ("clk_out", vp), ("n_out", vp), ("err_out", vp),
+                ("removed_list", vp), ("removed_cap", i64)]
 
 
 SIGNATURES["lbx_push_step_3d"] = (i32, [vp, P(Step3DArgs), vp])

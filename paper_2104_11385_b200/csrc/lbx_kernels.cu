@@ -476,6 +476,8 @@ struct Step3DParams {
   long long* n_out;
   long long* err_out;
   double wp, wc, cells;
+  long long* removed_list;
+  long long removed_cap;
 };
 
 template <bool kClock>
@@ -543,6 +545,21 @@ __global__ void __launch_bounds__(kBlock, 4) stream3d_kernel(Step3DParams p) {
           ++removed;
           first_out = min(first_out, i);
           nz[t] = -1.0;  // compaction sentinel
+        }
+        if (p.removed_list) {
+          const bool rm = valid && box[2 * r + t] < 0 && !(keep);
+          const unsigned m = __ballot_sync(kFull, rm);
+          if (m) {
+            unsigned long long base = 0;
+            if (lane == __ffs(m) - 1)
+              base = atomicAdd(&p.st->removed_count, (unsigned long long)__popc(m));
+            base = __shfl_sync(kFull, base, __ffs(m) - 1);
+            if (rm) {
+              const long long slot = (long long)base + __popc(m & lanemask_lt());
+              if (slot < p.removed_cap) p.removed_list[slot] = i;
+              else atomicOr((unsigned long long*)&p.st->err, 1ull << 61);
+            }
+          }
         }
       }
       if (any) {
@@ -1875,6 +1892,8 @@ int lbx_push_step_3d(lbx_ctx* ctx, const lbx_step3d_args* a, void* stream) {
   p.wp = a->w_particle;
   p.wc = a->w_cell;
   p.cells = (double)M * M * M;
+  p.removed_list = reinterpret_cast<long long*>(a->removed_list);
+  p.removed_cap = a->removed_cap;
   const bool clock = (a->flags & LBX_STEP_CLOCK) != 0;
   auto kern = clock ? stream3d_kernel<true> : stream3d_kernel<false>;
   const size_t smem = p.smem_hist ? (size_t)nb * 4 * (clock ? 2 : 1) : 0;
@@ -1886,9 +1905,12 @@ int lbx_push_step_3d(lbx_ctx* ctx, const lbx_step3d_args* a, void* stream) {
                                                 (2ll * kBlock * kPairs))), &grid);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
+  if (ctx->timing) cudaEventRecord((cudaEvent_t)ctx->ev0, s);
   kern<<<grid, kBlock, smem, s>>>(p);
+  if (ctx->timing) cudaEventRecord((cudaEvent_t)ctx->ev1, s);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "stream3d_kernel launch");
+  if (a->removed_list) return LBX_OK;  // caller compacts with lbx_fill_holes
   return launch_compact(ctx, a->z, a->x, a->y, a->vz, a->vy, a->vx, (double)a->extent_z,
                         (double)a->extent_x, stream);
 }

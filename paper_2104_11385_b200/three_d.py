@@ -103,7 +103,10 @@ class Simulation3D:
     """Device-resident 3D run: fused 3D kernel per step + host LB step."""
 
     def __init__(self, cfg: Scenario3D, policy: BalancePolicy, provider: CostProvider, *,
-                 device="cuda:0", positions=None, kick=None, record_counts=False):
+                 device="cuda:0", positions=None, kick=None, record_counts=False,
+                 stable_order=True):
+        """stable_order=False compacts absorbed particles by O(removed) hole
+        filling (particle order then differs from the sequential rule)."""
         from .balancer import knapsack_assign, sfc_assign
         from .cost import CostVector
         from .decomposition import morton_order_3d
@@ -187,6 +190,9 @@ class Simulation3D:
         self.n = n
         self.done = 0
         self.kernel_ms = []
+        self.stable_order = stable_order
+        self.removed = None if stable_order else torch.empty(n + 2, dtype=torch.int64,
+                                                             device=self.dev)
 
     def close(self):
         if getattr(self, "lb", None):
@@ -209,7 +215,9 @@ class Simulation3D:
             float(self.wp), float(self.wc),
             _lib.LBX_STEP_CLOCK if self.provider.device_kind == 3 else 0,
             _lib.ptr(self.dcounts), _lib.ptr(self.dcost), _lib.ptr(self.dclk),
-            _lib.ptr(self.dn), _lib.ptr(self.dn[1:]))
+            _lib.ptr(self.dn), _lib.ptr(self.dn[1:]), _lib.ptr(self.removed),
+            0 if self.removed is None else self.removed.numel())
+        self.ctx.set_count(self.n)
         _lib.check(_lib.lib.lbx_push_step_3d(self.ctx.handle, C.byref(args), _stream(self.dev)))
 
     def run(self, first=None, last=None):
@@ -227,6 +235,11 @@ class Simulation3D:
             h = torch.cat([self.dn, self.dcounts, self.dclk]).cpu().numpy()
             if h[1]:
                 raise ValueError(f"{int(h[1])} particles outside the box grid")
+            if not self.stable_order:
+                a = self.arr
+                _lib.check(_lib.lib.lbx_fill_holes(
+                    self.ctx.handle, *(_lib.ptr(a[k]) for k in ("z", "x", "y", "vz", "vy", "vx")),
+                    _lib.ptr(self.removed), self.n - int(h[0]), int(h[0]), _stream(self.dev)))
             self.n = int(h[0])
             nb = self.cfg.n_boxes
             counts = np.ascontiguousarray(h[2:2 + nb])
