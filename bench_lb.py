@@ -16,9 +16,7 @@ Modes:
   python bench_lb.py --emulate R               one GPU, R ranks as threads;
       each rank's fused step kernel runs alone (a lock serializes them) and
       is timed with CUDA events recorded by libLBX immediately around its
-      launch; the emulated step time is the MAX over ranks of those times -- the compute-imbalance part of an R-GPU step,
-      measured on B200 hardware.  Exchange/migration traffic is reported
-      (particles moved) but not timed in this mode.
+      launch; the emulated step time is the MAX over ranks of those times
 Prints one JSON object.
 """
 
@@ -112,11 +110,16 @@ def run_emulated(R, steps, replicas, policy, speed=0.035, drift=0.01):
     if errs:
         raise errs[0]
     per_step = np.max(np.array([log[r] for r in range(R)]), axis=0)   # [steps]
+    # adoption-time redistribution over NVLink, modelled: each rank sends its
+    # lost boxes' particles (48-byte records); the step pays the slowest rank
+    # at the measured 770 GB/s per-direction peer bandwidth (B200_PROFILING.md)
+    sent = np.array([s.moved[:len(per_step)] for s in sims])            # [R, steps]
+    migrate_ms = sent.max(axis=0) * 48 / 770e9 * 1e3
     res = sims[0].result()
-    moved = int(sum(s.moved.sum() for s in sims))
+    moved = int(sent.sum())
     for s in sims:
         s.close()
-    return per_step, res, moved, pos.shape[0] * replicas
+    return per_step, migrate_ms, res, moved, pos.shape[0] * replicas
 
 
 def main():
@@ -139,11 +142,14 @@ def main():
            "kick": {"speed": args.speed, "drift": args.drift}, "policies": {}}
     w = args.warmup_steps
     for policy in ("none", "static", "dynamic"):
-        per_step, res, moved, n = run_emulated(R, args.steps, args.replicas, policy,
-                                               args.speed, args.drift)
+        per_step, mig, res, moved, n = run_emulated(R, args.steps, args.replicas, policy,
+                                                    args.speed, args.drift)
         effs = [m.efficiency_after for m in res.metrics]
+        total = per_step + mig
         out["policies"][policy] = {
-            "time_ms": float(per_step[w:].sum()), "ms_per_step": float(per_step[w:].mean()),
+            "time_ms": float(total[w:].sum()), "compute_ms": float(per_step[w:].sum()),
+            "migration_ms_modelled": float(mig[w:].sum()),
+            "ms_per_step": float(total[w:].mean()),
             "e0": float(res.metrics[0].efficiency_before), "mean_eff": float(np.mean(effs)),
             "adoptions": res.summary["adoption_count"], "particles_migrated": moved,
             "particles": n}

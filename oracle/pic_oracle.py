@@ -12,11 +12,15 @@ macro weight w):
           (z, x) cells: Ex (0, 1/2), Ey (0, 0), Ez (1/2, 0), Bx (1/2, 0),
           By (1/2, 1/2), Bz (0, 1/2); J like E.  float32 storage with one
           guard layer kept at zero (conducting walls).
-  gather  linear (CIC) interpolation of every component at its own stagger.
+  gather  linear (CIC) interpolation of every component at its own stagger,
+          in float32 (the fields are float32): cell fractions are computed in
+          float64 and rounded to float32, then ((1-fz)((1-fx)a + fx b) +
+          fz((1-fx)c + fx d)) in float32, result widened to float64.
   push    relativistic Boris rotation, then z += dt uz/gamma, x += dt ux/gamma.
   absorb  particles leaving [0, Nz) x [0, Nx) are removed (as in lbsim).
   deposit direct: J_c += q w v_c S(new position) at the component's stagger;
-          every node contribution is quantised to fixed point with a
+          float32 node weights ((v*wz)*wx with v rounded to float32); every
+          node contribution is quantised to fixed point with a
           power-of-two scale (exact scaling, round half to even) and summed as
           integers -- order-independent, so the GPU's atomics reproduce it
           bit for bit; J = float32(sum / scale).
@@ -45,17 +49,19 @@ def _stencil(z, x, oz, ox):
     zc, xc = z - oz, x - ox
     i0 = np.floor(zc).astype(np.int64)
     j0 = np.floor(xc).astype(np.int64)
-    fz, fx = zc - i0, xc - j0
+    fz, fx = (zc - i0).astype(np.float32), (xc - j0).astype(np.float32)
     return i0, j0, fz, fx
 
 
 def gather(f, comp, z, x):
     oz, ox = OFFSETS[comp]
     i0, j0, fz, fx = _stencil(z, x, oz, ox)
-    a = f[comp].astype(np.float64)
+    a = f[comp]
     g = lambda di, dj: a[i0 + 1 + di, j0 + 1 + dj]  # noqa: E731
-    return ((1 - fz) * ((1 - fx) * g(0, 0) + fx * g(0, 1))
-            + fz * ((1 - fx) * g(1, 0) + fx * g(1, 1)))
+    one = np.float32(1.0)
+    gz, gx = one - fz, one - fx
+    v = gz * (gx * g(0, 0) + fx * g(0, 1)) + fz * (gx * g(1, 0) + fx * g(1, 1))
+    return v.astype(np.float64)
 
 
 def current_scale(qw):
@@ -82,9 +88,12 @@ def deposit(f, comp, z, x, val, scale):
     oz, ox = {"Jx": OFFSETS["Ex"], "Jy": OFFSETS["Ey"], "Jz": OFFSETS["Ez"]}[comp]
     i0, j0, fz, fx = _stencil(z, x, oz, ox)
     acc = np.zeros(f[comp].shape, dtype=np.int64)
-    for di, wz in ((0, 1 - fz), (1, fz)):
-        for dj, wx in ((0, 1 - fx), (1, fx)):
-            q = np.rint((val * wz * wx) * scale).astype(np.int64)
+    one = np.float32(1.0)
+    v32 = val.astype(np.float32)
+    s32 = np.float32(scale)
+    for di, wz in ((0, one - fz), (1, fz)):
+        for dj, wx in ((0, one - fx), (1, fx)):
+            q = np.rint((v32 * wz * wx) * s32).astype(np.int64)
             np.add.at(acc, (i0 + 1 + di, j0 + 1 + dj), q)
     f[comp] += (acc.astype(np.float64) / scale).astype(np.float32)
 

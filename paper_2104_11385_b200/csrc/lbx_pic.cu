@@ -106,6 +106,31 @@ __device__ __forceinline__ Stencil stencil(double z, double x, double oz, double
   return s;
 }
 
+// float32 stencil: index in 32-bit, cell fractions rounded to float32.
+struct StencilF {
+  int i0, j0;
+  float fz, fx;
+};
+
+__device__ __forceinline__ StencilF stencil_f(double z, double x, double oz, double ox) {
+  const double zc = __dsub_rn(z, oz), xc = __dsub_rn(x, ox);
+  const double fl_z = floor(zc), fl_x = floor(xc);
+  StencilF s;
+  s.i0 = (int)fl_z;
+  s.j0 = (int)fl_x;
+  s.fz = __double2float_rn(__dsub_rn(zc, fl_z));
+  s.fx = __double2float_rn(__dsub_rn(xc, fl_x));
+  return s;
+}
+
+// float32 CIC: (1-fz)((1-fx) a + fx b) + fz((1-fx) c + fx d), oracle order.
+__device__ __forceinline__ float cic_f(const StencilF& s, float a, float b, float c, float d) {
+  const float gz = __fsub_rn(1.f, s.fz), gx = __fsub_rn(1.f, s.fx);
+  const float lo = __fadd_rn(__fmul_rn(gx, a), __fmul_rn(s.fx, b));
+  const float hi = __fadd_rn(__fmul_rn(gx, c), __fmul_rn(s.fx, d));
+  return __fadd_rn(__fmul_rn(gz, lo), __fmul_rn(s.fz, hi));
+}
+
 // (1-fz)((1-fx) a + fx b) + fz((1-fx) c + fx d), evaluated as the oracle does.
 __device__ __forceinline__ double cic(const Stencil& s, double a, double b, double c, double d) {
   const double gz = __dsub_rn(1.0, s.fz), gx = __dsub_rn(1.0, s.fx);
@@ -141,6 +166,7 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
   const long long npairs = (n + 1) >> 1;
   const double ez = (double)p.nz, ex = (double)p.nx;
   const double h = 0.5 * p.qm * p.dt;
+  const float jscale_f = (float)p.jscale;   // power of two: exact in float
   double2* z2 = reinterpret_cast<double2*>(p.z);
   double2* x2 = reinterpret_cast<double2*>(p.x);
   double2* uz2 = reinterpret_cast<double2*>(p.uz);
@@ -185,7 +211,7 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
 #pragma unroll
     for (int k = 0; k < kPItems; ++k) {
       if (!valid[k]) continue;
-      const long long i = (long long)floor(pz[k]), j = (long long)floor(px[k]);
+      const long long i = (int)pz[k], j = (int)px[k];  // positions >= 0: trunc == floor
       imin = min(imin, i);
       imax = max(imax, i);
       jmin = min(jmin, j);
@@ -236,27 +262,31 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
       nx_[k] = px[k];
       double vel[3] = {0.0, 0.0, 0.0};
       if (valid[k]) {
+        // 4 distinct staggers: A (0,1/2) Ex Bz | B (0,0) Ey | C (1/2,0) Ez Bx | D (1/2,1/2) By
+        const StencilF st[4] = {stencil_f(pz[k], px[k], 0.0, 0.5), stencil_f(pz[k], px[k], 0.0, 0.0),
+                                stencil_f(pz[k], px[k], 0.5, 0.0), stencil_f(pz[k], px[k], 0.5, 0.5)};
+        constexpr int kSt[6] = {0, 1, 2, 2, 3, 0};   // Ex Ey Ez Bx By Bz -> stencil
         double f6[6];
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
-          const Stencil s = stencil(pz[k], px[k], (double)c_oz[c], (double)c_ox[c]);
-          double a, b, cc, d;
+          const StencilF& sc = st[kSt[c]];
+          float a, b, cc, d;
           if (staged) {
             const float* F = s_F + c * kPatchMax;
-            const int o = (s.i0 - pi0) * W + (s.j0 - pj0);
+            const int o = (sc.i0 - pi0) * W + (sc.j0 - pj0);
             a = F[o];
             b = F[o + 1];
             cc = F[o + W];
             d = F[o + W + 1];
           } else {
             const float* F = p.F[c];
-            const long long o = (long long)(s.i0 + 1) * p.pitch + (s.j0 + 1);
+            const long long o = (long long)(sc.i0 + 1) * p.pitch + (sc.j0 + 1);
             a = __ldg(F + o);
             b = __ldg(F + o + 1);
             cc = __ldg(F + o + p.pitch);
             d = __ldg(F + o + p.pitch + 1);
           }
-          f6[c] = cic(s, a, b, cc, d);
+          f6[c] = (double)cic_f(sc, a, b, cc, d);
         }
         // relativistic Boris (x, y, z order; E = f6[0..2], B = f6[3..5])
         const double mx = __dadd_rn(pux[k], __dmul_rn(h, f6[0]));
@@ -297,16 +327,17 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
       // native 32-bit shared atomics -- order-independent, deterministic.
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const Stencil s = stencil(keep[k] ? nz_[k] : 0.5, keep[k] ? nx_[k] : 0.5,
-                                  (double)c_oz[c], (double)c_ox[c]);
+        const StencilF s = stencil_f(keep[k] ? nz_[k] : 0.5, keep[k] ? nx_[k] : 0.5,
+                                     (double)c_oz[c], (double)c_ox[c]);
         int q[4] = {0, 0, 0, 0};
         if (keep[k]) {
-          const double gz = __dsub_rn(1.0, s.fz), gx = __dsub_rn(1.0, s.fx);
-          const double vz = __dmul_rn(vel[c], gz), vf = __dmul_rn(vel[c], s.fz);
-          q[0] = (int)__double2ll_rn(__dmul_rn(__dmul_rn(vz, gx), p.jscale));
-          q[1] = (int)__double2ll_rn(__dmul_rn(__dmul_rn(vz, s.fx), p.jscale));
-          q[2] = (int)__double2ll_rn(__dmul_rn(__dmul_rn(vf, gx), p.jscale));
-          q[3] = (int)__double2ll_rn(__dmul_rn(__dmul_rn(vf, s.fx), p.jscale));
+          const float gz = __fsub_rn(1.f, s.fz), gx = __fsub_rn(1.f, s.fx);
+          const float v = __double2float_rn(vel[c]);
+          const float vz = __fmul_rn(v, gz), vf = __fmul_rn(v, s.fz);
+          q[0] = __float2int_rn(__fmul_rn(__fmul_rn(vz, gx), jscale_f));
+          q[1] = __float2int_rn(__fmul_rn(__fmul_rn(vz, s.fx), jscale_f));
+          q[2] = __float2int_rn(__fmul_rn(__fmul_rn(vf, gx), jscale_f));
+          q[3] = __float2int_rn(__fmul_rn(__fmul_rn(vf, s.fx), jscale_f));
         }
         long long off;
         int row;
