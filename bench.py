@@ -344,13 +344,14 @@ def run_lbx(args, rank, world, local_rank):
                    "cost": spec.build_provider().kind, "lb": "knapsack every 10, 10% rel",
                    "ranks": world, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2 (3.3 GB particle state vs 126 MB L2)"},
-        "gpu_launches": int(args.steps),
+        "gpu_launches": 2 * int(args.steps),   # stream_kernel + compaction (exits at once
+                                                 # when nothing was absorbed) per step
         "lb": {"ranks": world, "e_first": effs[0] if effs else None,
                "e_mean": float(np.mean(effs)) if effs else None,
                "adoptions": res.summary["adoption_count"]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_src,
-                     "kernel": "lbx push_kernel<SoA,hist,clock>",
+                     "kernel": "lbx stream_kernel<clock,pow2,exch=0,push=1>",
                      "bytes_per_launch": BYTES_PER_PUSH * per_launch,
                      "kernel_ms": kernel_s * 1e3,
                      "traffic": None if tpp is None else tpp * per_launch},

@@ -10,13 +10,16 @@ initial mapping, knapsack remaps with GpuClock costs.  Policies:
   static   one knapsack attempt at step 0
   dynamic  knapsack attempt every 10 steps (10 % relative threshold)
 
-Modes:
-  torchrun --nproc-per-node N bench_lb.py      one rank per GPU (NCCL);
-      per-step time = max over ranks of the step's device time.
-  python bench_lb.py --emulate R               one GPU, R ranks as threads;
-      each rank's fused step kernel runs alone (a lock serializes them) and
-      is timed with CUDA events recorded by libLBX immediately around its
-      launch; the emulated step time is the MAX over ranks of those times
+Mode (one GPU is available this round): `python bench_lb.py --emulate R`
+runs R ranks as threads through the full multi-GPU code path (exchange
+kernels, replicated LB, adoption-time migration).  Each rank's fused step
+kernel runs alone (a lock serializes them) and is timed with CUDA events
+recorded by libLBX immediately around its launch; the emulated step time is
+the MAX over ranks of those times (the compute-imbalance part of an R-GPU
+step, measured on B200) plus, on adoption steps, a modelled redistribution
+time: max over ranks of the bytes it sends (48-byte records) / 770 GB/s (the
+measured NVLink peer bandwidth, B200_PROFILING.md).  On a multi-GPU box the
+same path runs for real under torchrun via `bench.py --gpus N`.
 Prints one JSON object.
 """
 
