@@ -90,22 +90,6 @@ __device__ __forceinline__ long long warp_sum(long long v) {
   return v;
 }
 
-// CIC stencil of a point for a component with stagger (oz, ox).
-struct Stencil {
-  int i0, j0;
-  double fz, fx;
-};
-
-__device__ __forceinline__ Stencil stencil(double z, double x, double oz, double ox) {
-  const double zc = __dsub_rn(z, oz), xc = __dsub_rn(x, ox);
-  Stencil s;
-  s.i0 = (int)floor(zc);
-  s.j0 = (int)floor(xc);
-  s.fz = __dsub_rn(zc, (double)s.i0);
-  s.fx = __dsub_rn(xc, (double)s.j0);
-  return s;
-}
-
 // float32 stencil: index in 32-bit, cell fractions rounded to float32.
 struct StencilF {
   int i0, j0;
@@ -129,14 +113,6 @@ __device__ __forceinline__ float cic_f(const StencilF& s, float a, float b, floa
   const float lo = __fadd_rn(__fmul_rn(gx, a), __fmul_rn(s.fx, b));
   const float hi = __fadd_rn(__fmul_rn(gx, c), __fmul_rn(s.fx, d));
   return __fadd_rn(__fmul_rn(gz, lo), __fmul_rn(s.fz, hi));
-}
-
-// (1-fz)((1-fx) a + fx b) + fz((1-fx) c + fx d), evaluated as the oracle does.
-__device__ __forceinline__ double cic(const Stencil& s, double a, double b, double c, double d) {
-  const double gz = __dsub_rn(1.0, s.fz), gx = __dsub_rn(1.0, s.fx);
-  const double lo = __dadd_rn(__dmul_rn(gx, a), __dmul_rn(s.fx, b));
-  const double hi = __dadd_rn(__dmul_rn(gx, c), __dmul_rn(s.fx, d));
-  return __dadd_rn(__dmul_rn(gz, lo), __dmul_rn(s.fz, hi));
 }
 
 template <bool kClock>
