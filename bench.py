@@ -324,6 +324,7 @@ def run_lbx(args, rank, world, local_rank):
 
     # ---- the reference's own C2 size (801,499 particles, 1 replica) ----
     c2n = c2_native(args, dev, spec, sc, pos0, kick0)
+    c1 = c1_uniform(dev) if not args.no_cpu_baseline else None
 
     # ---- e2e through the reference-facing C-ABI with host buffers ----
     e2e = None
@@ -357,6 +358,7 @@ def run_lbx(args, rank, world, local_rank):
                      "traffic": None if tpp is None else tpp * per_launch},
         "clocks": clocks.summary(),
         "c2_native": c2n,
+        "c1_uniform": c1,
     }
     if e2e is not None:
         line["e2e"] = e2e
@@ -395,6 +397,65 @@ def c2_native(args, dev, spec, sc, pos0, kick0, steps=400):
     return {"particles": n, "steps": steps, "us_per_step": 1e3 * ms / steps,
             "pushes_per_s": n * steps / (ms / 1e3),
             "note": "L2-resident, launch/latency bound; incl. host LB loop"}
+
+
+C1_DOC = dict(scenario_id="c1-uniform", domain=dict(extent=[128, 128], box_size=32), ranks=8,
+              blob=dict(center=[64.0, 64.0], core_radius=91.0, edge_scale=0.0,
+                        particles_per_cell=8.0),
+              kick=dict(step=0, speed=0.0), steps=220, seed=1,
+              balance=dict(strategy="knapsack", interval=10, threshold=0.10))
+
+
+def c1_uniform(dev, steps=200, warm=20):
+    """Config C1: 128x128 uniform plasma, 16 boxes, 8 ppc,
+    Heuristic + knapsack, 8 ranks -- the case the CPU reference runs; GPU
+    native loop vs the reference's compiled kernels + cost/knapsack code on
+    one host core, same steps."""
+    import time as _t
+
+    import torch
+
+    from oracle import lbsim_oracle as O
+    from paper_2104_11385_b200.scenarios import spec_from_dict
+    from paper_2104_11385_b200.workload import Simulation
+
+    spec = spec_from_dict(C1_DOC)
+    sim = Simulation(spec.scenario, spec.policy, spec.build_provider(), device=dev)
+    n = sim.n_init
+    sim.run(0, warm)
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    sim.run(warm, warm + steps)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    gpu_ms = e0.elapsed_time(e1)
+    res = sim.result()
+    sim.close()
+    K, kind = _ref_kernels()
+    cfg = O.config_from_doc(C1_DOC)
+    pos, _ = O.init_scenario(cfg["extent"], 32, cfg["center"], 91.0, 0.0, 8.0, 1)
+    vel = np.zeros_like(pos)
+    owner = O.slab_mapping(16, 8)
+    cells = np.full(16, 1024, dtype=np.int64)
+    t0 = _t.perf_counter()
+    for s in range(steps):
+        pos, vel = K.advance_particles(pos, vel, 128.0, 128.0)
+        counts = K.bin_particles(pos, 32.0, 4, 4)
+        cost = O.heuristic_cost(counts, cells, 0.75, 0.25)
+        e, _ = O.efficiency_flagged(cost, owner, 8)
+        if s % 10 == 0:
+            prop = O.knapsack_assign(cost, 8)
+            if O.gate(e, O.efficiency_flagged(cost, prop, 8)[0], 0.10, "relative"):
+                owner = prop
+    cpu_s = _t.perf_counter() - t0
+    return {"particles": n, "steps": steps, "gpu_us_per_step": 1e3 * gpu_ms / steps,
+            "gpu_pushes_per_s": n * steps / (gpu_ms / 1e3),
+            "cpu_pushes_per_s": n * steps / cpu_s, "cpu_kind": kind, "cpu_cores": 1,
+            "mean_efficiency": res.summary["mean_efficiency"],
+            "adoptions": res.summary["adoption_count"],
+            "note": "L2-resident, latency bound; parity of this config: tests/test_gpu_runs.py::c1"}
 
 
 def run_lbx_dist(args, rank, world, dev):

@@ -39,13 +39,17 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 
-def scenario(ranks, steps, policy, speed=0.035, drift=0.01):
-    from paper_2104_11385_b200.balancer import BalancePolicy
+def scenario(ranks, steps, policy, speed=0.035, drift=0.01, strategy="knapsack",
+             migration_ratio=0.0):
+    from paper_2104_11385_b200.balancer import Strategy
     from paper_2104_11385_b200.scenarios import apply_overrides, load_spec
     from paper_2104_11385_b200.workload import BlobSpec, KickSpec
 
     spec = apply_overrides(load_spec("default"), cost="gpuclock", ranks=ranks, steps=steps,
-                           policy="knapsack" if policy == "dynamic" else policy)
+                           policy=strategy if policy == "dynamic" else policy)
+    if policy != "none":
+        spec = replace(spec, policy=replace(spec.policy, strategy=Strategy(strategy),
+                                            migration_ratio=migration_ratio))
     sc = replace(spec.scenario, blob=BlobSpec(center=(60.0, 480.0), core_radius=44.0,
                                               edge_scale=4.0, particles_per_cell=55.0),
                  kick=KickSpec(step=0, speed=speed, drift=drift), initial_mapping="slab")
@@ -75,13 +79,14 @@ def make_timed_engine(lock, log):
     return TimedEngine
 
 
-def run_emulated(R, steps, replicas, policy, speed=0.035, drift=0.01):
+def run_emulated(R, steps, replicas, policy, speed=0.035, drift=0.01, strategy="knapsack",
+                 migration_ratio=0.0):
     import torch
 
     import bench
     from paper_2104_11385_b200.parallel import DistributedSimulation, ThreadComm
 
-    spec, sc = scenario(R, steps, policy, speed, drift)
+    spec, sc = scenario(R, steps, policy, speed, drift, strategy, migration_ratio)
     from paper_2104_11385_b200.workload import kick_velocities, sample_blob
     pos = sample_blob(sc)
     kick = kick_velocities(pos, sc)
@@ -133,6 +138,9 @@ def main():
     ap.add_argument("--warmup-steps", type=int, default=1)
     ap.add_argument("--speed", type=float, default=0.035, help="kick speed (cells/step)")
     ap.add_argument("--drift", type=float, default=0.01, help="axial drift (cells/step)")
+    ap.add_argument("--strategy", default="knapsack", choices=["knapsack", "sfc"])
+    ap.add_argument("--migration-ratio", type=float, default=0.0,
+                    help=">0: migration-aware adoption gate (pushes per moved particle)")
     args = ap.parse_args()
     if not args.emulate:
         raise SystemExit("multi-GPU mode: run under torchrun with bench.py --gpus N for the "
@@ -142,11 +150,13 @@ def main():
     R = args.emulate
     out = {"mode": f"emulated {R} ranks on one B200 (per-rank kernels timed alone; "
                    "step time = max over ranks)", "ranks": R, "steps": args.steps,
-           "kick": {"speed": args.speed, "drift": args.drift}, "policies": {}}
+           "kick": {"speed": args.speed, "drift": args.drift}, "strategy": args.strategy,
+           "migration_ratio": args.migration_ratio, "policies": {}}
     w = args.warmup_steps
     for policy in ("none", "static", "dynamic"):
         per_step, mig, res, moved, n = run_emulated(R, args.steps, args.replicas, policy,
-                                                    args.speed, args.drift)
+                                                    args.speed, args.drift, args.strategy,
+                                                    args.migration_ratio)
         effs = [m.efficiency_after for m in res.metrics]
         total = per_step + mig
         out["policies"][policy] = {

@@ -253,6 +253,14 @@ typedef struct lbx_sim_config {
    * makes the LB object 3D -- boxes (bz*nby + by)*nbx + bx, 3D Morton curve,
    * interior faces along z, y, x, M^3 cells per box. */
   int32_t extent_y;
+  /* Migration-aware adoption (the paper's future work;
+   * 0 = the reference's gate only).  When > 0 a proposal that passes the
+   * efficiency gate is adopted only if the load it saves over one interval,
+   * interval * (max rank load now - max rank load proposed), exceeds the
+   * cost of moving the particles of every re-owned box, priced at
+   * migration_ratio particle-pushes each (cost per push = total cost /
+   * total particles of the step). */
+  double migration_ratio;
 } lbx_sim_config;
 
 #define LBX_PHYSICS_SURROGATE 0

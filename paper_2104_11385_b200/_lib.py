@@ -45,7 +45,8 @@ class SimConfig(C.Structure):
                 ("comm_per_face", f64), ("gather", f64),
                 ("redistribute_per_particle", f64), ("redistribute_latency", f64),
                 ("capacity_particles", i64), ("physics", i32), ("pic_dt", f64),
-                ("pic_q_over_m", f64), ("pic_q_times_w", f64), ("extent_y", i32)]
+                ("pic_q_over_m", f64), ("pic_q_times_w", f64), ("extent_y", i32),
+                ("migration_ratio", f64)]
 
 
 class SimOutputs(C.Structure):

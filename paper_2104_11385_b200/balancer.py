@@ -41,8 +41,14 @@ class BalancePolicy:
     knapsack_cap_factor: float = 1.5
     threshold_mode: str = "relative"
     static_step: int | None = None
+    # B200 extension: >0 also requires the load saved over
+    # one interval to exceed the migration cost (migration_ratio particle-
+    # pushes per moved particle).  0 = the reference's gate.
+    migration_ratio: float = 0.0
 
     def __post_init__(self):
+        if self.migration_ratio < 0:
+            raise ConfigError("migration_ratio must be >= 0")
         if self.interval < 1:
             raise ConfigError(f"interval must be >= 1, got {self.interval}")
         if self.improvement_threshold < 0:

@@ -173,6 +173,24 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
     const double need = c.threshold_relative ? e_cur * (1.0 + c.improvement_threshold)
                                              : e_cur + c.improvement_threshold;
     adopted = e_prop >= need && e_prop >= e_cur;
+    if (adopted && c.migration_ratio > 0.0) {
+      // price the redistribution against the load saved over one interval
+      std::vector<double> lc(R, 0.0), lp(R, 0.0);
+      double total_cost = 0.0;
+      int64_t total_n = 0, moved = 0;
+      for (int b = 0; b < nb; ++b) {
+        lc[s->owner[b]] += cost[b];
+        lp[s->prop[b]] += cost[b];
+        total_cost += cost[b];
+        total_n += counts[b];
+        if (s->prop[b] != s->owner[b]) moved += counts[b];
+      }
+      const double mc = *std::max_element(lc.begin(), lc.end());
+      const double mp = *std::max_element(lp.begin(), lp.end());
+      const double per_push = total_n > 0 ? total_cost / (double)total_n : 0.0;
+      const double saved = (double)c.interval * (mc - mp);
+      adopted = saved > c.migration_ratio * per_push * (double)moved;
+    }
     if (adopted) {
       s->owner = s->prop;
       e_after = e_prop;

@@ -144,3 +144,40 @@ def test_morton_3d_vs_oracle(L):
         out = np.empty(g[0] * g[1] * g[2], dtype=np.int64)
         L.check(L.lib.lbx_morton_order_3d(*g, L.ptr(out)))
         assert np.array_equal(out, O.morton_order_3d(g)), g
+
+
+def test_migration_aware_gate(L):
+    """B200 extension: a huge migration price blocks the
+    adoption the reference gate would make; zero restores the reference."""
+    import ctypes as C
+
+    from paper_2104_11385_b200.balancer import BalancePolicy
+    from paper_2104_11385_b200.cost import make_provider
+    from paper_2104_11385_b200.scenarios import load_spec
+    from paper_2104_11385_b200.workload import sim_config
+    sc = load_spec("mini").scenario
+    counts = np.zeros(225, dtype=np.int64)
+    counts[:20] = 1000            # all load on rank 0 of a slab mapping
+    owner = O.slab_mapping(225, 8)
+    res = {}
+    for ratio in (0.0, 1e9):
+        conf = sim_config(sc, BalancePolicy(migration_ratio=ratio), make_provider("heuristic"))
+        h = C.c_void_p()
+        L.check(L.lib.lbx_lb_create(C.byref(h), C.byref(conf), L.ptr(owner)))
+        T, nb = sc.total_steps, 225
+        arrs = {k: np.zeros(T) for k in ("eb", "ea", "cm", "co", "g", "r", "w")}
+        u8 = {k: np.zeros(T, dtype=np.uint8) for k in ("ad", "at", "oom")}
+        i64 = {k: np.zeros(T, dtype=np.int64) for k in ("mrp", "na", "as")}
+        trace = np.zeros((T, nb))
+        own_out = owner.copy()
+        so = L.SimOutputs(L.ptr(arrs["eb"]), L.ptr(arrs["ea"]), L.ptr(u8["ad"]), L.ptr(u8["at"]),
+                          L.ptr(arrs["cm"]), L.ptr(arrs["co"]), L.ptr(arrs["g"]), L.ptr(arrs["r"]),
+                          L.ptr(arrs["w"]), L.ptr(i64["mrp"]), L.ptr(u8["oom"]), L.ptr(i64["na"]),
+                          L.ptr(trace), None, None, L.ptr(own_out), L.ptr(i64["as"]), None, None,
+                          0, 0, 0)
+        ad, halt = C.c_int32(), C.c_int32()
+        L.check(L.lib.lbx_lb_step(h, 0, L.ptr(counts), None, int(counts.sum()), C.byref(so),
+                                  C.byref(ad), C.byref(halt)))
+        L.lib.lbx_lb_destroy(h)
+        res[ratio] = ad.value
+    assert res[0.0] == 1 and res[1e9] == 0
