@@ -4,11 +4,15 @@
 Workload: the C2 blob (default.yaml geometry: 960x960 cells, 32-cell boxes,
 801,499 particles sampled with the reference's stream) tiled R times
 (default 128 -> 102.6 M macro-particles), momenta from the C2 kick velocity
-(u = v/dt), electrons (q/m = -1), dt = 0.5, GpuClock tally on.  Timed with
-CUDA events on the launch stream:
-  push_deposit  lbx_pic_step with LBX_PIC_NO_FIELD_SOLVE (gather + Boris +
-                deposit + counts/clock + compaction), and
-  full_step     the same plus the Yee update.
+(u = v/dt), electrons (q/m = -1), dt = 0.5, GpuClock tally on.  Every mode
+starts from the same initial particles.  Timed with CUDA events on the
+launch stream:
+  push_deposit          lbx_pic_step, sorted mode (sort-on-write), with
+                        LBX_PIC_NO_FIELD_SOLVE: quad fields + gather + Boris +
+                        deposit + counts/clock + compaction + cell-slot scan;
+  push_deposit_inplace  the same in place (order kept, no sorting: the
+                        deposit's cell runs decay as particles drift);
+  full_step             sorted mode plus the Yee update.
 Roofline: HBM, algorithmic bytes = 80 B per particle (read z,x,uz,ux,uy +
 write them, float64) -- field patch and current flush traffic is counted
 separately from ncu (profiles/).  Prints one JSON object.
@@ -49,36 +53,44 @@ def main():
     R = args.replicas
     n = pos0.shape[0] * R
     nz, nx = sc.domain_extent
-    st = pic.PicState.create(pos0[:1], u0[:1], nz, nx, device=dev)
-    # tile on the device (host arrays of 100 M particles are not needed)
-    for name, col in (("z", pos0[:, 0]), ("x", pos0[:, 1]), ("uz", u0[:, 0]), ("ux", u0[:, 1]),
-                      ("uy", u0[:, 2])):
+    cols = (("z", pos0[:, 0]), ("x", pos0[:, 1]), ("uz", u0[:, 0]), ("ux", u0[:, 1]),
+            ("uy", u0[:, 2]))
+    init = {}
+    for name, col in cols:   # tile on the device (host arrays of 100 M particles are not needed)
         t = torch.zeros(n + 2, dtype=torch.float64, device=dev)
         t[:n].copy_(torch.from_numpy(np.ascontiguousarray(col)).to(dev).repeat(R))
-        setattr(st, name, t)
-    st.n = n
+        init[name] = t
     ctx = device.Context(dev, capacity=n)
     peak, peak_src = bench.peaks()
     out = {"workload": f"C2 blob x{R} replicas = {n} particles, 960x960 Yee grid, "
                        f"box 32, dt {dt}, q/m -1, GpuClock on", "particles": n}
     stream = torch.cuda.current_stream(dev)
-    for mode, solve in (("push_deposit", False), ("full_step", True)):
+    for mode, solve, sort in (("push_deposit", False, True), ("push_deposit_inplace", False, False),
+                              ("full_step", True, True)):
+        st = pic.PicState.create(pos0[:1], u0[:1], nz, nx, device=dev)
+        for name, t in init.items():
+            setattr(st, name, t.clone())
+        st.n = n
         for _ in range(args.warmup):
-            pic.pic_step(ctx, st, sc.box_size, -1.0, -1e-4, dt, clock=True, field_solve=solve)
+            pic.pic_step(ctx, st, sc.box_size, -1.0, -1e-4, dt, clock=True, field_solve=solve,
+                         sort=sort)
         times = []
         for _ in range(args.steps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             n_before = st.n
             e0.record(stream)
-            pic.pic_step(ctx, st, sc.box_size, -1.0, -1e-4, dt, clock=True, field_solve=solve)
+            pic.pic_step(ctx, st, sc.box_size, -1.0, -1e-4, dt, clock=True, field_solve=solve,
+                         sort=sort)
             e1.record(stream)
             torch.cuda.synchronize(dev)
             times.append((e0.elapsed_time(e1), n_before))
         ms = float(np.mean([t for t, _ in times]))
         nb = float(np.mean([k for _, k in times]))
         achieved = BYTES_PER_PARTICLE * nb / (ms / 1e3) / 1e9
-        out[mode] = {"ms": ms, "pushes_per_s": nb / (ms / 1e3), "achieved_gbs": achieved,
+        out[mode] = {"ms": ms, "ms_per_step": [round(t, 3) for t, _ in times],
+                     "pushes_per_s": nb / (ms / 1e3), "achieved_gbs": achieved,
                      "frac_of_hbm_peak": achieved / peak}
+        del st
     out["peak_gbs"] = peak
     out["peak_source"] = peak_src
     print(json.dumps(out))

@@ -324,17 +324,20 @@ int lbx_sim_particles(lbx_sim* sim, int64_t* n, void* stream);
 
 /* ------------------------------------------------------------------------
  * 2D3V electromagnetic PIC step (SURVEY 8a row a15 / north-star item 1; not
- * in the reference, parity unpinned -- checked against oracle/pic_oracle.py
- * at a stated tolerance).  Particles SoA float64 z, x, uz, ux, uy (u = gamma
- * v, c = 1, unit cells), 16-byte aligned, capacity >= n + 2, count in the
+ * in the reference, parity unpinned -- checked bit-exactly against
+ * oracle/pic_oracle.py).  Particles SoA float64 z, x, uz, ux, uy (u = gamma
+ * v, c = 1, unit cells), 32-byte aligned, capacity >= n + 2, count in the
  * context as for lbx_push_step.  Fields float32 on a Yee grid with one zero
  * guard layer: arrays of (nz+2) x (nx+2), cell (i, j) at [(i+1)*(nx+2) + j+1];
  * fields[] = {Ex, Ey, Ez, Bx, By, Bz}, current[] = {Jx, Jy, Jz} (zero on
- * entry, consumed).  One call: field gather + Boris push + absorb + current
- * deposition (shared-memory staged per 1024-particle tile) + per-box counts /
- * heuristic cost / GpuClock tally + stable compaction + Yee field update.
+ * entry, consumed).  One call: field gather (quad-expanded copy of the
+ * fields) + Boris push + absorb + current deposition (cell-relative
+ * fixed-point nodes accumulated per lane over cell runs, integer atomics:
+ * deterministic) + per-box counts / heuristic cost / GpuClock tally + stable
+ * compaction + Yee field update.
  * ---------------------------------------------------------------------- */
 #define LBX_PIC_NO_FIELD_SOLVE 2u  /* skip the Yee update (tests)         */
+#define LBX_PIC_RESYNC 4u          /* sorted mode: recount the input cells   */
 
 typedef struct lbx_pic_args {
   double* z;
@@ -355,6 +358,15 @@ typedef struct lbx_pic_args {
   uint64_t* clk_out;
   int64_t* n_out;
   int64_t* err_out;
+  /* Sorted mode (all five non-NULL): results are written to out[] = {z, x,
+   * uz, ux, uy} grouped by each particle's cell at the START of the step
+   * (sort-on-write, no extra pass), so the next step's particles of a cell
+   * are contiguous and their current is accumulated in registers.  The
+   * caller swaps in/out after the call.  The library keeps the next step's
+   * cell slots; passing any other input than the last call's out[] (or
+   * LBX_PIC_RESYNC) recounts them.  Order within a cell is not
+   * deterministic; every computed value is.  NULL: in place, order kept. */
+  double* out[5];
 } lbx_pic_args;
 
 int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* args, void* stream);

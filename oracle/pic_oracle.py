@@ -14,14 +14,15 @@ macro weight w):
           guard layer kept at zero (conducting walls).
   gather  linear (CIC) interpolation of every component at its own stagger,
           in float32 (the fields are float32): cell fractions are computed in
-          float64 and rounded to float32, then ((1-fz)((1-fx)a + fx b) +
+          float64 (half-staggered ones as f -/+ 1/2 from the cell fraction f,
+          see _axis) and rounded to float32, then ((1-fz)((1-fx)a + fx b) +
           fz((1-fx)c + fx d)) in float32, result widened to float64.
   push    relativistic Boris rotation, then z += dt uz/gamma, x += dt ux/gamma.
   absorb  particles leaving [0, Nz) x [0, Nx) are removed (as in lbsim).
   deposit direct: J_c += q w v_c S(new position) at the component's stagger;
-          float32 node weights ((v*wz)*wx with v rounded to float32); every
-          node contribution is quantised to fixed point with a
-          power-of-two scale (exact scaling, round half to even) and summed as
+          float32 node weights, contribution ((v*scale)*wz)*wx with v rounded
+          to float32 and a power-of-two scale; every node contribution is
+          rounded to an integer (round half to even) and summed as
           integers -- order-independent, so the GPU's atomics reproduce it
           bit for bit; J = float32(sum / scale).
   field   B -= dt curl E ; E += dt (curl B - J) on interior nodes.
@@ -45,11 +46,23 @@ def new_fields(nz, nx):
     return f
 
 
+def _axis(v, o):
+    """One axis of the stencil (lbx_pic.cu axis_of): cell i = floor(v) and the
+    exact fraction f = v - i; stagger 0 -> (i, f); stagger 1/2 -> the
+    half-shifted stencil, (i, f - 1/2) when f >= 1/2 (exact) else
+    (i - 1, f + 1/2).  Fractions are rounded to float32 last."""
+    fl = np.floor(v)
+    f = v - fl
+    i = fl.astype(np.int64)
+    if o == 0.0:
+        return i, f.astype(np.float32)
+    hi = f >= 0.5
+    return np.where(hi, i, i - 1), np.where(hi, f - 0.5, f + 0.5).astype(np.float32)
+
+
 def _stencil(z, x, oz, ox):
-    zc, xc = z - oz, x - ox
-    i0 = np.floor(zc).astype(np.int64)
-    j0 = np.floor(xc).astype(np.int64)
-    fz, fx = (zc - i0).astype(np.float32), (xc - j0).astype(np.float32)
+    i0, fz = _axis(z, oz)
+    j0, fx = _axis(x, ox)
     return i0, j0, fz, fx
 
 
@@ -93,7 +106,7 @@ def deposit(f, comp, z, x, val, scale):
     s32 = np.float32(scale)
     for di, wz in ((0, one - fz), (1, fz)):
         for dj, wx in ((0, one - fx), (1, fx)):
-            q = np.rint((v32 * wz * wx) * s32).astype(np.int64)
+            q = np.rint(((v32 * s32) * wz) * wx).astype(np.int64)
             np.add.at(acc, (i0 + 1 + di, j0 + 1 + dj), q)
     f[comp] += (acc.astype(np.float64) / scale).astype(np.float32)
 

@@ -8,11 +8,14 @@ how to build it.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from .errors import ConfigError  # noqa: F401  (re-exported for callers)
 
 LIB_PATH = Path(__file__).resolve().parent / "libLBX.so"
+if os.environ.get("LBX_VARIANT"):   # tuning experiments: an in-tree build variant libLBX.<v>.so
+    LIB_PATH = LIB_PATH.with_name(f"libLBX.{os.environ['LBX_VARIANT']}.so")
 
 LBX_OK, LBX_EINVAL, LBX_ECUDA, LBX_EOOM, LBX_ERANGE = 0, 1, 2, 3, 4
 LBX_STEP_CLOCK = 1
@@ -117,6 +120,7 @@ SIGNATURES.update({
 })
 RECORD_DOUBLES = 6
 LBX_PIC_NO_FIELD_SOLVE = 2
+LBX_PIC_RESYNC = 4
 
 
 class PicArgs(C.Structure):
@@ -126,7 +130,7 @@ class PicArgs(C.Structure):
                 ("box_size", i32), ("q_over_m", f64), ("q_times_w", f64), ("dt", f64),
                 ("w_particle", f64), ("w_cell", f64), ("flags", u32),
                 ("counts_out", vp), ("cost_out", vp), ("clk_out", vp), ("n_out", vp),
-                ("err_out", vp)]
+                ("err_out", vp), ("out", vp * 5)]
 
 
 SIGNATURES["lbx_pic_step"] = (i32, [vp, P(PicArgs), vp])

@@ -63,8 +63,13 @@ struct lbx_ctx {
   int grid_override = 0;
   int64_t* host_scratch = nullptr;    // pinned
   lbx::HostPipe* pipe = nullptr;      // lbx_advance_bin_host lanes (lazy)
-  unsigned long long* pic_acc = nullptr;  // PIC fixed-point current [3][cells]
-  int64_t pic_cells = 0;
+  unsigned long long* pic_acc = nullptr;  // PIC cell-centric fixed-point current [cells][16]
+  int64_t pic_cells = 0;                  //   + 4 ints: deposit bounding box
+  void* pic_quad = nullptr;               // PIC quad-expanded fields (float4) [6][quads]
+  int64_t pic_quads = 0;
+  unsigned* pic_sortbuf = nullptr;        // PIC sorted mode: cell counts, cursors, block sums
+  int64_t pic_sort_cells = 0;
+  const void* pic_sort_next = nullptr;    // z array whose cell slots are in the cursors
   long long* fill_scratch = nullptr;      // hole-fill: holes[cap] + tail flags[cap]
   int64_t fill_cap = 0;
   bool timing = false;                    // lbx_ctx_enable_timing

@@ -1538,6 +1538,8 @@ int lbx_ctx_destroy(lbx_ctx* ctx) {
   if (ctx->host_scratch) cudaFreeHost(ctx->host_scratch);
   destroy_pipe(ctx->pipe);
   if (ctx->pic_acc) cudaFree(ctx->pic_acc);
+  if (ctx->pic_quad) cudaFree(ctx->pic_quad);
+  if (ctx->pic_sortbuf) cudaFree(ctx->pic_sortbuf);
   if (ctx->fill_scratch) cudaFree(ctx->fill_scratch);
   if (ctx->ev0) cudaEventDestroy((cudaEvent_t)ctx->ev0), cudaEventDestroy((cudaEvent_t)ctx->ev1);
   delete ctx;

@@ -3,31 +3,36 @@
 // gather ... with vectorised SoA particle loads and shared-memory staging of
 // each tile's field and current patches").  The reference has no PIC (it
 // models the step as ballistic motion); the CPU restatement used
-// as the checker is oracle/pic_oracle.py (parity unpinned, tolerance tests).
+// as the checker is oracle/pic_oracle.py (parity unpinned, bit-exact tests).
 //
 // Particles: SoA float64 z, x, uz, ux, uy (u = gamma v, c = 1), uniform
 // charge q and macro weight w.  Fields: float32 Yee grid (2D in z, x; y
 // invariant) with one zero guard layer (conducting walls); offsets in cells
 // Ex (0,1/2) Ey (0,0) Ez (1/2,0) Bx (1/2,0) By (1/2,1/2) Bz (0,1/2), J as E.
 //
-// pic_push_kernel -- one pass per 1024-particle chunk (a "tile"):
-//   1. 16-byte pair loads of the chunk's particles (5 arrays);
-//   2. block-reduced bounding box of the chunk's cells; the chunk's field
-//      patch (bbox + 2-cell halo, <= kPatchMax cells) is staged into shared
-//      memory with coalesced loads, and a zeroed current patch is set up;
-//   3. CIC gather of the 6 components from shared memory, relativistic Boris
-//      push, move, absorbing test;
-//   4. direct current deposition into the shared current patch (shared-memory
-//      float atomics), then one flush of the patch to HBM (global atomics,
-//      nonzero cells only);
-//   5. z, x, u written back in place; per-box survivor counts + GpuClock
-//      tally (same run-length / warp-reduced histogram as the surrogate
-//      kernel); absorbed particles recorded for the compaction pass.
-//   Chunks whose patch would not fit fall back to direct global gather /
-//   atomics (uniform per CTA).
-// pic_b_kernel / pic_e_kernel -- Yee leapfrog (B -= dt curl E;
-//   E += dt (curl B - J)), fp64 arithmetic rounded to float32 (bit-identical
-//   to the oracle's), J consumed and zeroed.
+// One step = five stream-ordered launches (+ compaction on absorbing steps):
+//  pic_quad_kernel    fields -> quad-expanded copy Q[c][node] = float4 of the
+//                     2x2 nodes whose lower corner is `node` (HBM, L2/L1
+//                     resident for the blob), so a gather is ONE 16-byte load
+//                     per component instead of four scalar loads;
+//  pic_push_kernel    per warp unit of 64 particles = 2 slots of 32
+//                     CONSECUTIVE particles (coalesced 8-byte SoA loads):
+//                     gather (6 x LDG.128), relativistic Boris, move, absorb,
+//                     then the current of every kept particle as 16
+//                     cell-relative fixed-point node values (Jx 2x3, Jy 2x2,
+//                     Jz 3x2 nodes around its cell), summed over the slot's
+//                     (at most two) cells with full-warp redux.sync and added
+//                     with ONE 16-lane 128-byte RED per cell into the
+//                     cell-centric accumulator Jc[cell][16]; slots spanning
+//                     more cells (unsorted particles) add per lane.  Per-box
+//                     survivor counts + GpuClock tally as in the surrogate
+//                     kernel; no block barrier inside the particle loop;
+//  pic_current_kernel node gather Jc -> J (integer sums: order independent,
+//                     bit-identical to the oracle), over the deposit
+//                     bounding box only; pic_zero_kernel clears that box;
+//  pic_b_kernel / pic_e_kernel -- Yee leapfrog (B -= dt curl E;
+//                     E += dt (curl B - J)), fp64 arithmetic rounded to
+//                     float32 (bit-identical to the oracle's), J consumed.
 
 #include <cuda_runtime.h>
 
@@ -40,25 +45,32 @@
 namespace lbx {
 namespace {
 
-#ifndef LBX_PIC_PAIRS
-#define LBX_PIC_PAIRS 1
-#endif
 constexpr int kPB = 256;                  // threads per CTA
 constexpr int kPW = kPB / 32;
-constexpr int kPPairs = LBX_PIC_PAIRS;    // particle pairs per thread per chunk
-constexpr int kPItems = 2 * kPPairs;
-constexpr int kPChunk = kPB * kPItems;    // 1024 particles per chunk
-constexpr int kPatchMax = 1536;           // cells per staged patch
+#ifndef LBX_PIC_RUN
+#define LBX_PIC_RUN 64
+#endif
+constexpr int kRun = LBX_PIC_RUN;         // consecutive particles per lane per warp unit
+#ifndef LBX_PIC_G
+#define LBX_PIC_G 4
+#endif
+constexpr int kG = LBX_PIC_G;             // particles per vector load group (4: 256-bit)
+constexpr int kUnitP = 32 * kRun;         // particles per warp unit
+constexpr int kNodes = 16;                // cell-relative current nodes (Jx 6, Jy 4, Jz 6)
 constexpr unsigned kAll = 0xffffffffu;
 
 struct PicParams {
-  double *z, *x, *uz, *ux, *uy;
-  float* F[6];   // Ex Ey Ez Bx By Bz
-  unsigned long long* Jacc[3];  // fixed-point current accumulators (int64)
-  double jscale;                // power-of-two fixed-point scale
-  int nz, nx, pitch;
+  const double *z, *x, *uz, *ux, *uy;     // particles in
+  double *oz, *ox, *ouz, *oux, *ouy;      // particles out (== in unless sorting)
+  const float4* Q[6];           // quad-expanded Ex Ey Ez Bx By Bz, [(nz+1) x (nx+1)]
+  unsigned long long* Jc;       // cell-centric fixed-point node sums [nz*nx][16]
+  int* dep_box;                 // imin, imax, jmin, jmax of depositing cells
+  unsigned* cell_cnt;           // sorted mode: kept particles per new cell
+  unsigned* cursor;             // sorted mode: next free slot per old cell
+  float vscale;                 // power-of-two fixed-point scale (exact in float)
+  int nz, nx, qpitch;
   double qm, qw, dt;
-  double inv_m;  // box binning: power-of-two box size (checked on host)
+  int log2m;                    // box binning: power-of-two box size (checked on host)
   int nbz, nbx, nb;
   DevState* st;
   unsigned long long* g_cnt;
@@ -71,17 +83,9 @@ struct PicParams {
   double wp, wc, cells;
 };
 
-__constant__ float c_oz[6] = {0.f, 0.f, 0.5f, 0.5f, 0.5f, 0.f};
-__constant__ float c_ox[6] = {0.5f, 0.f, 0.f, 0.f, 0.5f, 0.5f};
-
 __device__ __forceinline__ long long warp_min(long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(kAll, v, o));
-  return v;
-}
-__device__ __forceinline__ long long warp_max(long long v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(kAll, v, o));
   return v;
 }
 __device__ __forceinline__ long long warp_sum(long long v) {
@@ -90,356 +94,385 @@ __device__ __forceinline__ long long warp_sum(long long v) {
   return v;
 }
 
-// float32 stencil: index in 32-bit, cell fractions rounded to float32.
-struct StencilF {
-  int i0, j0;
-  float fz, fx;
+// One axis of a position: its cell i and float32 fraction f (unstaggered
+// stencil), and the half-staggered stencil (base ih, fraction fh):
+// fh = f - 1/2 (exact, ih = i) when f >= 1/2, else f + 1/2 (ih = i - 1).
+// oracle/pic_oracle.py:_axis states the same arithmetic.
+struct Axis {
+  int i, ih;
+  float f, fh;
+  bool hi;
 };
 
-__device__ __forceinline__ StencilF stencil_f(double z, double x, double oz, double ox) {
-  const double zc = __dsub_rn(z, oz), xc = __dsub_rn(x, ox);
-  const double fl_z = floor(zc), fl_x = floor(xc);
-  StencilF s;
-  s.i0 = (int)fl_z;
-  s.j0 = (int)fl_x;
-  s.fz = __double2float_rn(__dsub_rn(zc, fl_z));
-  s.fx = __double2float_rn(__dsub_rn(xc, fl_x));
-  return s;
+__device__ __forceinline__ Axis axis_of(double v) {
+  const double fl = floor(v);
+  const double f = __dsub_rn(v, fl);
+  Axis a;
+  a.hi = f >= 0.5;
+  a.i = (int)fl;
+  a.ih = a.hi ? a.i : a.i - 1;
+  a.f = __double2float_rn(f);
+  a.fh = __double2float_rn(__dadd_rn(f, a.hi ? -0.5 : 0.5));
+  return a;
 }
 
-// float32 CIC: (1-fz)((1-fx) a + fx b) + fz((1-fx) c + fx d), oracle order.
-__device__ __forceinline__ float cic_f(const StencilF& s, float a, float b, float c, float d) {
-  const float gz = __fsub_rn(1.f, s.fz), gx = __fsub_rn(1.f, s.fx);
-  const float lo = __fadd_rn(__fmul_rn(gx, a), __fmul_rn(s.fx, b));
-  const float hi = __fadd_rn(__fmul_rn(gx, c), __fmul_rn(s.fx, d));
-  return __fadd_rn(__fmul_rn(gz, lo), __fmul_rn(s.fz, hi));
+// float32 CIC on a quad (a, b, c, d) = nodes (0,0) (0,1) (1,0) (1,1):
+// (1-fz)((1-fx) a + fx b) + fz((1-fx) c + fx d), the oracle's order.
+__device__ __forceinline__ float cic(const float4 q, float fz, float fx) {
+  const float gz = __fsub_rn(1.f, fz), gx = __fsub_rn(1.f, fx);
+  const float lo = __fadd_rn(__fmul_rn(gx, q.x), __fmul_rn(fx, q.y));
+  const float hi = __fadd_rn(__fmul_rn(gx, q.z), __fmul_rn(fx, q.w));
+  return __fadd_rn(__fmul_rn(gz, lo), __fmul_rn(fz, hi));
 }
 
-template <bool kClock>
+// Fire-and-forget adds (REDG; a plain atomicAdd may keep the returning ATOMG
+// form inside large kernels).
+__device__ __forceinline__ void red_add(unsigned long long* a, long long v) {
+  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(a), "l"((unsigned long long)v) : "memory");
+}
+__device__ __forceinline__ void red_add32(unsigned* a, unsigned v) {
+  asm volatile("red.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+
+// kG consecutive doubles [i, i+kG): one vector streaming load (256-bit for
+// kG = 4) when the group is complete, else clamped scalar loads (tail lanes
+// reload a live particle).
+__device__ __forceinline__ void ldg(const double* a, long long i, long long n, double v[kG]) {
+  if (i + kG <= n) {
+    if (kG % 4 == 0) {
+#pragma unroll
+      for (int c = 0; c < kG; c += 4)
+        asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];"
+                     : "=d"(v[c % kG]), "=d"(v[(c + 1) % kG]), "=d"(v[(c + 2) % kG]),
+                       "=d"(v[(c + 3) % kG])
+                     : "l"(a + i + c));
+    } else {
+      asm volatile("ld.global.cs.v2.f64 {%0,%1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "l"(a + i));
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kG; ++j) v[j] = __ldcs(a + min(i + j, n - 1));
+  }
+}
+__device__ __forceinline__ void stg(double* a, long long i, long long n, const double v[kG]) {
+  if (i + kG <= n) {
+    if (kG % 4 == 0) {
+#pragma unroll
+      for (int c = 0; c < kG; c += 4)
+        asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(a + i + c), "d"(v[c % kG]),
+                     "d"(v[(c + 1) % kG]), "d"(v[(c + 2) % kG]), "d"(v[(c + 3) % kG])
+                     : "memory");
+    } else {
+      asm volatile("st.global.cs.v2.f64 [%0], {%1,%2};" ::"l"(a + i), "d"(v[0]), "d"(v[1])
+                   : "memory");
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kG; ++j)
+      if (i + j < n) __stcs(a + i + j, v[j]);
+  }
+}
+
+__device__ __forceinline__ int qnode(float vs, float wz, float wx) {
+  return __float2int_rn(__fmul_rn(__fmul_rn(vs, wz), wx));
+}
+
+// The 16 cell-relative fixed-point node values of one deposit (v pre-scaled).
+__device__ __forceinline__ void node_values(const Axis& az, const Axis& ax, float vsx, float vsy,
+                                            float vsz, int q[kNodes]) {
+  const float z0 = __fsub_rn(1.f, az.f), z1 = az.f;
+  const float x0 = __fsub_rn(1.f, ax.f), x1 = ax.f;
+  const float zh = __fsub_rn(1.f, az.fh), xh = __fsub_rn(1.f, ax.fh);
+  const float zm = az.hi ? 0.f : zh, zc = az.hi ? zh : az.fh, zp = az.hi ? az.fh : 0.f;
+  const float xm = ax.hi ? 0.f : xh, xc = ax.hi ? xh : ax.fh, xp = ax.hi ? ax.fh : 0.f;
+  // Jx: rows {0,1} x cols {-1,0,1}
+  q[0] = qnode(vsx, z0, xm);
+  q[1] = qnode(vsx, z0, xc);
+  q[2] = qnode(vsx, z0, xp);
+  q[3] = qnode(vsx, z1, xm);
+  q[4] = qnode(vsx, z1, xc);
+  q[5] = qnode(vsx, z1, xp);
+  // Jy: rows {0,1} x cols {0,1}
+  q[6] = qnode(vsy, z0, x0);
+  q[7] = qnode(vsy, z0, x1);
+  q[8] = qnode(vsy, z1, x0);
+  q[9] = qnode(vsy, z1, x1);
+  // Jz: rows {-1,0,1} x cols {0,1}
+  q[10] = qnode(vsz, zm, x0);
+  q[11] = qnode(vsz, zm, x1);
+  q[12] = qnode(vsz, zc, x0);
+  q[13] = qnode(vsz, zc, x1);
+  q[14] = qnode(vsz, zp, x0);
+  q[15] = qnode(vsz, zp, x1);
+}
+
+template <bool kSort>
+__device__ __forceinline__ void flush_cell(const PicParams& p, int cell, const int acc[kNodes],
+                                           unsigned m) {
+  unsigned long long* d = p.Jc + (long long)cell * kNodes;
+#pragma unroll
+  for (int i = 0; i < kNodes; ++i)
+    if (acc[i]) red_add(d + i, acc[i]);
+  if (kSort) red_add32(p.cell_cnt + cell, m);
+}
+
 #ifndef LBX_PIC_MINB
-#define LBX_PIC_MINB 3
+#define LBX_PIC_MINB 2
 #endif
+template <bool kClock, bool kSort>
 __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  unsigned* s_cnt = reinterpret_cast<unsigned*>(smem_raw);          // nb
-  unsigned* s_clk = s_cnt + p.nb;                                    // nb
-  float* s_F = reinterpret_cast<float*>(s_clk + p.nb);               // 6 * kPatchMax
-  int* s_J = reinterpret_cast<int*>(s_F + 6 * kPatchMax);            // 3 * kPatchMax
+  extern __shared__ __align__(16) unsigned s_hist[];
+  unsigned* s_cnt = s_hist;           // nb
+  unsigned* s_clk = s_hist + p.nb;    // nb
   __shared__ long long s_n;
-  __shared__ int s_box[4];  // imin, imax, jmin, jmax
+  __shared__ int s_box[4];
   __shared__ int s_last;
   __shared__ unsigned long long s_red[kPW];
   __shared__ long long s_min[kPW];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_n = *((volatile long long*)&p.st->n);
+  if (tid == 0) {
+    s_n = *((volatile long long*)&p.st->n);
+    s_box[0] = INT_MAX;
+    s_box[1] = INT_MIN;
+    s_box[2] = INT_MAX;
+    s_box[3] = INT_MIN;
+  }
   for (int b = tid; b < p.nb; b += kPB) {
     s_cnt[b] = 0u;
     if (kClock) s_clk[b] = 0u;
   }
   __syncthreads();
   const long long n = s_n;
-  const long long npairs = (n + 1) >> 1;
+  const long long units = (n + kUnitP - 1) / kUnitP;
   const double ez = (double)p.nz, ex = (double)p.nx;
   const double h = 0.5 * p.qm * p.dt;
-  const float jscale_f = (float)p.jscale;   // power of two: exact in float
-  double2* z2 = reinterpret_cast<double2*>(p.z);
-  double2* x2 = reinterpret_cast<double2*>(p.x);
-  double2* uz2 = reinterpret_cast<double2*>(p.uz);
-  double2* ux2 = reinterpret_cast<double2*>(p.ux);
-  double2* uy2 = reinterpret_cast<double2*>(p.uy);
   unsigned long long removed = 0;
   long long first_out = LLONG_MAX, err = 0;
+  int bimin = INT_MAX, bimax = INT_MIN, bjmin = INT_MAX, bjmax = INT_MIN;
 
-  for (long long q0 = (long long)blockIdx.x * kPB * kPPairs; q0 < npairs;
-       q0 += (long long)gridDim.x * kPB * kPPairs) {
-    long long t0 = 0;
-    if (kClock) t0 = clock64();
-    double pz[kPItems], px[kPItems], puz[kPItems], pux[kPItems], puy[kPItems];
-    bool valid[kPItems];
+  for (long long u = (long long)blockIdx.x * kPW + warp; u < units;
+       u += (long long)gridDim.x * kPW) {
+    const long long run0 = u * kUnitP + (long long)lane * kRun;
+    // deposit accumulator (cell-relative node sums of the lane's current cell)
+    int acc[kNodes];
 #pragma unroll
-    for (int r = 0; r < kPPairs; ++r) {
-      const long long q = q0 + r * kPB + tid;
-      double2 a = make_double2(0.5, 0.5), b = a, c = make_double2(0.0, 0.0), d = c, e = c;
-      const bool any = q < npairs;
-      if (any) {
-        a = __ldcs(z2 + q);
-        b = __ldcs(x2 + q);
-        c = __ldcs(uz2 + q);
-        d = __ldcs(ux2 + q);
-        e = __ldcs(uy2 + q);
-      }
-      pz[2 * r] = a.x;
-      pz[2 * r + 1] = a.y;
-      px[2 * r] = b.x;
-      px[2 * r + 1] = b.y;
-      puz[2 * r] = c.x;
-      puz[2 * r + 1] = c.y;
-      pux[2 * r] = d.x;
-      pux[2 * r + 1] = d.y;
-      puy[2 * r] = e.x;
-      puy[2 * r + 1] = e.y;
-      valid[2 * r] = any;
-      valid[2 * r + 1] = 2 * q + 1 < n;
-    }
-    // ---- chunk bounding box (cells) ----
-    long long imin = LLONG_MAX, imax = LLONG_MIN, jmin = LLONG_MAX, jmax = LLONG_MIN;
+    for (int i = 0; i < kNodes; ++i) acc[i] = 0;
+    int cur = -1;
+    unsigned cur_m = 0;
+    // per-box survivor run (+ GpuClock: time since the last box flush)
+    int hb = -1;
+    unsigned hn = 0;
+    long long t_last = 0;
+    if (kClock) t_last = clock64();
+#pragma unroll 1
+    for (int g = 0; g < kRun / kG; ++g) {
+      const long long i0 = run0 + g * kG;
+      if (i0 >= n) break;
+      double pz[kG], px[kG], puz[kG], pux[kG], puy[kG];
+      ldg(p.z, i0, n, pz);
+      ldg(p.x, i0, n, px);
+      ldg(p.uz, i0, n, puz);
+      ldg(p.ux, i0, n, pux);
+      ldg(p.uy, i0, n, puy);
+      // ---- phase 0: old cells; sort-on-write destinations (one cursor
+      // atomic per run of equal old cells within the group) ----
+      // (the cursor atomics' results are consumed only at the store)
+      unsigned base[kG];
+      bool seg_start[kG];
+      if (kSort) {
+        int okey[kG];
 #pragma unroll
-    for (int k = 0; k < kPItems; ++k) {
-      if (!valid[k]) continue;
-      const long long i = (int)pz[k], j = (int)px[k];  // positions >= 0: trunc == floor
-      imin = min(imin, i);
-      imax = max(imax, i);
-      jmin = min(jmin, j);
-      jmax = max(jmax, j);
-    }
-    imin = warp_min(imin);
-    imax = warp_max(imax);
-    jmin = warp_min(jmin);
-    jmax = warp_max(jmax);
-    if (tid == 0) {
-      s_box[0] = INT_MAX;
-      s_box[1] = INT_MIN;
-      s_box[2] = INT_MAX;
-      s_box[3] = INT_MIN;
-    }
-    __syncthreads();
-    if (lane == 0 && imin <= imax) {
-      atomicMin(&s_box[0], (int)imin);
-      atomicMax(&s_box[1], (int)imax);
-      atomicMin(&s_box[2], (int)jmin);
-      atomicMax(&s_box[3], (int)jmax);
-    }
-    __syncthreads();
-    // patch rows/cols in cell units, clipped to the guarded grid [-1, n]
-    const int pi0 = max(s_box[0] - 2, -1), pi1 = min(s_box[1] + 2, p.nz);
-    const int pj0 = max(s_box[2] - 2, -1), pj1 = min(s_box[3] + 2, p.nx);
-    const int H = pi1 - pi0 + 1, W = pj1 - pj0 + 1;
-    const bool staged = s_box[0] <= s_box[1] && H * W <= kPatchMax;
-    if (staged) {
-      for (int idx = tid; idx < H * W; idx += kPB) {
-        const int li = idx / W, lj = idx - li * W;
-        const long long g = (long long)(pi0 + li + 1) * p.pitch + (pj0 + lj + 1);
+        for (int k = 0; k < kG; ++k) okey[k] = (int)pz[k] * p.nx + (int)px[k];   // z, x >= 0
 #pragma unroll
-        for (int c = 0; c < 6; ++c) s_F[c * kPatchMax + idx] = __ldg(p.F[c] + g);
+        for (int k = 0; k < kG; ++k) {
+          seg_start[k] = i0 + k < n && (k == 0 || okey[k] != okey[k - 1]);
+          int len = 0;
+          bool same = true;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) s_J[c * kPatchMax + idx] = 0;
-      }
-    }
-    __syncthreads();
-
-    // ---- gather, push, move, absorb (per lane), deposit (warp-collective) ----
-    double nz_[kPItems], nx_[kPItems];
-    bool keep[kPItems];
-#pragma unroll
-    for (int k = 0; k < kPItems; ++k) {
-      keep[k] = false;
-      nz_[k] = pz[k];
-      nx_[k] = px[k];
-      double vel[3] = {0.0, 0.0, 0.0};
-      if (valid[k]) {
-        // 4 distinct staggers: A (0,1/2) Ex Bz | B (0,0) Ey | C (1/2,0) Ez Bx | D (1/2,1/2) By
-        const StencilF st[4] = {stencil_f(pz[k], px[k], 0.0, 0.5), stencil_f(pz[k], px[k], 0.0, 0.0),
-                                stencil_f(pz[k], px[k], 0.5, 0.0), stencil_f(pz[k], px[k], 0.5, 0.5)};
-        constexpr int kSt[6] = {0, 1, 2, 2, 3, 0};   // Ex Ey Ez Bx By Bz -> stencil
-        double f6[6];
-#pragma unroll
-        for (int c = 0; c < 6; ++c) {
-          const StencilF& sc = st[kSt[c]];
-          float a, b, cc, d;
-          if (staged) {
-            const float* F = s_F + c * kPatchMax;
-            const int o = (sc.i0 - pi0) * W + (sc.j0 - pj0);
-            a = F[o];
-            b = F[o + 1];
-            cc = F[o + W];
-            d = F[o + W + 1];
-          } else {
-            const float* F = p.F[c];
-            const long long o = (long long)(sc.i0 + 1) * p.pitch + (sc.j0 + 1);
-            a = __ldg(F + o);
-            b = __ldg(F + o + 1);
-            cc = __ldg(F + o + p.pitch);
-            d = __ldg(F + o + p.pitch + 1);
+          for (int j = k; j < kG; ++j) {
+            same = same && i0 + j < n && okey[j] == okey[k];
+            len += same ? 1 : 0;
           }
-          f6[c] = (double)cic_f(sc, a, b, cc, d);
+          base[k] = seg_start[k] ? atomicAdd(p.cursor + okey[k], (unsigned)len) : 0u;
         }
-        // relativistic Boris (x, y, z order; E = f6[0..2], B = f6[3..5])
-        const double mx = __dadd_rn(pux[k], __dmul_rn(h, f6[0]));
-        const double my = __dadd_rn(puy[k], __dmul_rn(h, f6[1]));
-        const double mz = __dadd_rn(puz[k], __dmul_rn(h, f6[2]));
-        const double g = sqrt(__dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(mx, mx)),
-                                                  __dmul_rn(my, my)), __dmul_rn(mz, mz)));
-        const double ig = __ddiv_rn(1.0, g);
-        const double tx = __dmul_rn(__dmul_rn(h, f6[3]), ig);
-        const double ty = __dmul_rn(__dmul_rn(h, f6[4]), ig);
-        const double tz = __dmul_rn(__dmul_rn(h, f6[5]), ig);
-        const double s2 = __ddiv_rn(2.0, __dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(tx, tx)),
-                                                             __dmul_rn(ty, ty)),
-                                                   __dmul_rn(tz, tz)));
+      }
+      // ---- phase 1: gather, Boris, move, absorb ----
+      bool keep[kG];
+      int nkey[kG];
+      float vsx[kG], vsy[kG], vsz[kG];
+#pragma unroll
+      for (int k = 0; k < kG; ++k) {
+        const Axis az = axis_of(pz[k]), ax = axis_of(px[k]);
+        const int qp = p.qpitch;
+        const int oA = (az.i + 1) * qp + (ax.ih + 1);    // (0, 1/2)   Ex Bz
+        const int oB = (az.i + 1) * qp + (ax.i + 1);     // (0, 0)     Ey
+        const int oC = (az.ih + 1) * qp + (ax.i + 1);    // (1/2, 0)   Ez Bx
+        const int oD = (az.ih + 1) * qp + (ax.ih + 1);   // (1/2, 1/2) By
+        const float Ex = cic(__ldg(p.Q[0] + oA), az.f, ax.fh);
+        const float Ey = cic(__ldg(p.Q[1] + oB), az.f, ax.f);
+        const float Ez = cic(__ldg(p.Q[2] + oC), az.fh, ax.f);
+        const float Bx = cic(__ldg(p.Q[3] + oC), az.fh, ax.f);
+        const float By = cic(__ldg(p.Q[4] + oD), az.fh, ax.fh);
+        const float Bz = cic(__ldg(p.Q[5] + oA), az.f, ax.fh);
+        // relativistic Boris (x, y, z order; oracle boris())
+        const double hEx = __dmul_rn(h, (double)Ex), hEy = __dmul_rn(h, (double)Ey),
+                     hEz = __dmul_rn(h, (double)Ez);
+        const double mx = __dadd_rn(pux[k], hEx);
+        const double my = __dadd_rn(puy[k], hEy);
+        const double mz = __dadd_rn(puz[k], hEz);
+        const double gg = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(mx, mx)),
+                                                         __dmul_rn(my, my)), __dmul_rn(mz, mz)));
+        const double ig = __drcp_rn(gg);                 // == 1.0 / g (correctly rounded)
+        const double tx = __dmul_rn(__dmul_rn(h, (double)Bx), ig);
+        const double ty = __dmul_rn(__dmul_rn(h, (double)By), ig);
+        const double tz = __dmul_rn(__dmul_rn(h, (double)Bz), ig);
+        // 2 / d == 2 * RN(1/d) exactly (power-of-two scaling of a normal number)
+        const double s2 = __dmul_rn(2.0, __drcp_rn(__dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(tx, tx)),
+                                                                       __dmul_rn(ty, ty)),
+                                                             __dmul_rn(tz, tz))));
         const double qx = __dadd_rn(mx, __dsub_rn(__dmul_rn(my, tz), __dmul_rn(mz, ty)));
         const double qy = __dadd_rn(my, __dsub_rn(__dmul_rn(mz, tx), __dmul_rn(mx, tz)));
         const double qz = __dadd_rn(mz, __dsub_rn(__dmul_rn(mx, ty), __dmul_rn(my, tx)));
-        const double rx = __dadd_rn(mx, __dmul_rn(s2, __dsub_rn(__dmul_rn(qy, tz), __dmul_rn(qz, ty))));
-        const double ry = __dadd_rn(my, __dmul_rn(s2, __dsub_rn(__dmul_rn(qz, tx), __dmul_rn(qx, tz))));
-        const double rz = __dadd_rn(mz, __dmul_rn(s2, __dsub_rn(__dmul_rn(qx, ty), __dmul_rn(qy, tx))));
-        pux[k] = __dadd_rn(rx, __dmul_rn(h, f6[0]));
-        puy[k] = __dadd_rn(ry, __dmul_rn(h, f6[1]));
-        puz[k] = __dadd_rn(rz, __dmul_rn(h, f6[2]));
-        const double gam = sqrt(__dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(pux[k], pux[k])),
-                                                    __dmul_rn(puy[k], puy[k])),
-                                          __dmul_rn(puz[k], puz[k])));
-        const double igam = __ddiv_rn(1.0, gam);
-        nz_[k] = __dadd_rn(pz[k], __dmul_rn(__dmul_rn(p.dt, puz[k]), igam));
-        nx_[k] = __dadd_rn(px[k], __dmul_rn(__dmul_rn(p.dt, pux[k]), igam));
-        keep[k] = nz_[k] >= 0.0 && nz_[k] < ez && nx_[k] >= 0.0 && nx_[k] < ex;
-        vel[0] = __dmul_rn(__dmul_rn(p.qw, pux[k]), igam);
-        vel[1] = __dmul_rn(__dmul_rn(p.qw, puy[k]), igam);
-        vel[2] = __dmul_rn(__dmul_rn(p.qw, puz[k]), igam);
+        pux[k] = __dadd_rn(__dadd_rn(mx, __dmul_rn(s2, __dsub_rn(__dmul_rn(qy, tz), __dmul_rn(qz, ty)))), hEx);
+        puy[k] = __dadd_rn(__dadd_rn(my, __dmul_rn(s2, __dsub_rn(__dmul_rn(qz, tx), __dmul_rn(qx, tz)))), hEy);
+        puz[k] = __dadd_rn(__dadd_rn(mz, __dmul_rn(s2, __dsub_rn(__dmul_rn(qx, ty), __dmul_rn(qy, tx)))), hEz);
+        const double gam = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(pux[k], pux[k])),
+                                                          __dmul_rn(puy[k], puy[k])),
+                                                __dmul_rn(puz[k], puz[k])));
+        const double igam = __drcp_rn(gam);
+        pz[k] = __dadd_rn(pz[k], __dmul_rn(__dmul_rn(p.dt, puz[k]), igam));
+        px[k] = __dadd_rn(px[k], __dmul_rn(__dmul_rn(p.dt, pux[k]), igam));
+        keep[k] = i0 + k < n && pz[k] >= 0.0 && pz[k] < ez && px[k] >= 0.0 && px[k] < ex;
+        nkey[k] = keep[k] ? (int)pz[k] * p.nx + (int)px[k] : -1;   // positions >= 0: trunc == floor
+        const double qwg = keep[k] ? p.qw : 0.0;
+        vsx[k] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, pux[k]), igam)), p.vscale);
+        vsy[k] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, puy[k]), igam)), p.vscale);
+        vsz[k] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, puz[k]), igam)), p.vscale);
       }
-      // Deposition: node contributions quantised to fixed point (exact
-      // power-of-two scaling, round-to-nearest-even), pre-summed over lanes
-      // that share a stencil (__match_any_sync + redux.sync) and added with
-      // native 32-bit shared atomics -- order-independent, deterministic.
+      // ---- phase 3: store (in place, or scattered to the sorted slots) ----
+      long long dest[kG];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const StencilF s = stencil_f(keep[k] ? nz_[k] : 0.5, keep[k] ? nx_[k] : 0.5,
-                                     (double)c_oz[c], (double)c_ox[c]);
-        int q[4] = {0, 0, 0, 0};
-        if (keep[k]) {
-          const float gz = __fsub_rn(1.f, s.fz), gx = __fsub_rn(1.f, s.fx);
-          const float v = __double2float_rn(vel[c]);
-          const float vz = __fmul_rn(v, gz), vf = __fmul_rn(v, s.fz);
-          q[0] = __float2int_rn(__fmul_rn(__fmul_rn(vz, gx), jscale_f));
-          q[1] = __float2int_rn(__fmul_rn(__fmul_rn(vz, s.fx), jscale_f));
-          q[2] = __float2int_rn(__fmul_rn(__fmul_rn(vf, gx), jscale_f));
-          q[3] = __float2int_rn(__fmul_rn(__fmul_rn(vf, s.fx), jscale_f));
+      for (int k = 0; k < kG; ++k) {
+        if (kSort) dest[k] = seg_start[k] ? (long long)base[k] : (k ? dest[k - 1] + 1 : 0);
+        else dest[k] = i0 + k;
+        if (i0 + k < n && !keep[k]) {
+          ++removed;
+          first_out = min(first_out, dest[k]);
         }
-        long long off;
-        int row;
-        if (staged) {
-          off = (long long)(s.i0 - pi0) * W + (s.j0 - pj0);
-          row = W;
+      }
+      if (kSort) {
+#pragma unroll
+        for (int k = 0; k < kG; ++k) {
+          if (i0 + k >= n) continue;
+          const long long d = dest[k];
+          if (d >= n) {       // offsets inconsistent with the particles: refuse to scatter
+            ++err;
+            continue;
+          }
+          __stcs(p.oz + d, pz[k]);
+          __stcs(p.ox + d, px[k]);
+          __stcs(p.ouz + d, puz[k]);
+          __stcs(p.oux + d, pux[k]);
+          __stcs(p.ouy + d, puy[k]);
+        }
+      } else {
+        stg(p.oz, i0, n, pz);
+        stg(p.ox, i0, n, px);
+        stg(p.ouz, i0, n, puz);
+        stg(p.oux, i0, n, pux);
+        stg(p.ouy, i0, n, puy);
+      }
+      // ---- phase 2: current.  Accumulate in registers while consecutive
+      // particles share a cell; an isolated particle in another cell (drift)
+      // is added directly; otherwise switch cells.  One flush site (16 REDs)
+      // per particle. ----
+#pragma unroll
+      for (int k = 0; k < kG; ++k) {
+        if (nkey[k] < 0) continue;
+        const Axis az = axis_of(pz[k]), ax = axis_of(px[k]);
+        int q[kNodes];
+        node_values(az, ax, vsx[k], vsy[k], vsz[k], q);
+        bimin = min(bimin, az.i);
+        bimax = max(bimax, az.i);
+        bjmin = min(bjmin, ax.i);
+        bjmax = max(bjmax, ax.i);
+        const bool same = nkey[k] == cur;
+        const bool strag = !same && cur >= 0 && k + 1 < kG && nkey[k + 1] != nkey[k];
+        const bool swap = !same && !strag;
+        const int fcell = strag ? nkey[k] : (swap ? cur : -1);
+        if (fcell >= 0) {
+          unsigned long long* d = p.Jc + (long long)fcell * kNodes;
+#pragma unroll
+          for (int i = 0; i < kNodes; ++i) {
+            const int v = strag ? q[i] : acc[i];
+            if (v) red_add(d + i, v);
+          }
+          if (kSort) red_add32(p.cell_cnt + fcell, strag ? 1u : cur_m);
+        }
+        if (same) {
+#pragma unroll
+          for (int i = 0; i < kNodes; ++i) acc[i] += q[i];
+          ++cur_m;
+        } else if (swap) {
+#pragma unroll
+          for (int i = 0; i < kNodes; ++i) acc[i] = q[i];
+          cur = nkey[k];
+          cur_m = 1;
+        }
+        // per-box survivor counts (+ clock): run-length per lane
+        const int bz = az.i >> p.log2m, bx = ax.i >> p.log2m;
+        if (bz >= p.nbz || bx >= p.nbx) {
+          ++err;
+        } else if (bz * p.nbx + bx == hb) {
+          ++hn;
         } else {
-          off = (long long)(s.i0 + 1) * p.pitch + (s.j0 + 1);
-          row = p.pitch;
-        }
-        // Warp-uniform fast path: all depositing lanes share the stencil
-        // (sorted particles, 55 per cell) -> 4 full-warp redux.sync and one
-        // lane adds; otherwise each lane adds (native 32-bit atomics).
-        const unsigned dep = __ballot_sync(kAll, keep[k]);
-        if (!dep) continue;
-        const long long off0 = __shfl_sync(kAll, off, __ffs(dep) - 1);
-        if (__all_sync(kAll, !keep[k] || off == off0)) {
-          const int t0s = __reduce_add_sync(kAll, q[0]);
-          const int t1s = __reduce_add_sync(kAll, q[1]);
-          const int t2s = __reduce_add_sync(kAll, q[2]);
-          const int t3s = __reduce_add_sync(kAll, q[3]);
-          if (lane == __ffs(dep) - 1) {
-            if (staged) {
-              int* J = s_J + c * kPatchMax + off;
-              atomicAdd(J, t0s);
-              atomicAdd(J + 1, t1s);
-              atomicAdd(J + row, t2s);
-              atomicAdd(J + row + 1, t3s);
-            } else {
-              unsigned long long* J = p.Jacc[c] + off;
-              atomicAdd(J, (unsigned long long)(long long)t0s);
-              atomicAdd(J + 1, (unsigned long long)(long long)t1s);
-              atomicAdd(J + row, (unsigned long long)(long long)t2s);
-              atomicAdd(J + row + 1, (unsigned long long)(long long)t3s);
+          if (hb >= 0) {
+            atomicAdd(s_cnt + hb, hn);
+            if (kClock) {
+              const long long t = clock64();
+              atomicAdd(s_clk + hb, (unsigned)min((t - t_last) >> 4, (long long)(1u << 30)));
+              t_last = t;
             }
           }
-        } else if (keep[k]) {
-          if (staged) {
-            int* J = s_J + c * kPatchMax + off;
-            atomicAdd(J, q[0]);
-            atomicAdd(J + 1, q[1]);
-            atomicAdd(J + row, q[2]);
-            atomicAdd(J + row + 1, q[3]);
-          } else {
-            unsigned long long* J = p.Jacc[c] + off;
-            atomicAdd(J, (unsigned long long)(long long)q[0]);
-            atomicAdd(J + 1, (unsigned long long)(long long)q[1]);
-            atomicAdd(J + row, (unsigned long long)(long long)q[2]);
-            atomicAdd(J + row + 1, (unsigned long long)(long long)q[3]);
-          }
+          hb = bz * p.nbx + bx;
+          hn = 1;
         }
       }
     }
-    unsigned dt_clk = 0;
-    if (kClock) dt_clk = (unsigned)min(clock64() - t0, (long long)(1 << 20)) >> 4;
-    __syncthreads();
-    if (staged) {  // flush the current patch
-      for (int idx = tid; idx < H * W; idx += kPB) {
-        const int li = idx / W, lj = idx - li * W;
-        const long long g = (long long)(pi0 + li + 1) * p.pitch + (pj0 + lj + 1);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const int v = s_J[c * kPatchMax + idx];
-          if (v) atomicAdd(p.Jacc[c] + g, (unsigned long long)(long long)v);
-        }
+    if (cur >= 0) flush_cell<kSort>(p, cur, acc, cur_m);
+    // last box run of the lane: warp-uniform fast path (one shared atomic)
+    unsigned tclk = 0;
+    if (kClock && hb >= 0) tclk = (unsigned)min((clock64() - t_last) >> 4, (long long)(1u << 30));
+    const int hb0 = __shfl_sync(kAll, hb, 0);
+    if (__all_sync(kAll, hb == hb0)) {
+      const unsigned tot = __reduce_add_sync(kAll, hn);
+      const unsigned clk = kClock ? __reduce_add_sync(kAll, tclk) : 0u;
+      if (lane == 0 && hb0 >= 0 && tot) {
+        atomicAdd(s_cnt + hb0, tot);
+        if (kClock) atomicAdd(s_clk + hb0, clk);
       }
+    } else if (hb >= 0 && hn) {
+      atomicAdd(s_cnt + hb, hn);
+      if (kClock) atomicAdd(s_clk + hb, tclk);
     }
-    // ---- store, bin, account ----
-#pragma unroll
-    for (int r = 0; r < kPPairs; ++r) {
-      const long long q = q0 + r * kPB + tid;
-      if (!valid[2 * r]) continue;
-      __stcs(z2 + q, make_double2(nz_[2 * r], nz_[2 * r + 1]));
-      __stcs(x2 + q, make_double2(nx_[2 * r], nx_[2 * r + 1]));
-      __stcs(uz2 + q, make_double2(puz[2 * r], puz[2 * r + 1]));
-      __stcs(ux2 + q, make_double2(pux[2 * r], pux[2 * r + 1]));
-      __stcs(uy2 + q, make_double2(puy[2 * r], puy[2 * r + 1]));
-      for (int t = 0; t < 2; ++t) {
-        if (valid[2 * r + t] && !keep[2 * r + t]) {
-          ++removed;
-          first_out = min(first_out, 2 * q + t);
-        }
-      }
-    }
-    int cur = -1;
-    unsigned run = 0;
-#pragma unroll
-    for (int k = 0; k < kPItems; ++k) {
-      int b = -1;
-      if (keep[k]) {
-        const int bz = (int)__dmul_rn(nz_[k], p.inv_m), bx = (int)__dmul_rn(nx_[k], p.inv_m);
-        if (bz < p.nbz && bx < p.nbx) b = bz * p.nbx + bx;
-        else ++err;
-      }
-      if (b != cur) {
-        if (cur >= 0) {
-          atomicAdd(s_cnt + cur, run);
-          if (kClock) atomicAdd(s_clk + cur, dt_clk * run);
-        }
-        cur = b;
-        run = 0;
-      }
-      run += b >= 0 ? 1u : 0u;
-    }
-    const int cur0 = __shfl_sync(kAll, cur, 0);
-    if (__all_sync(kAll, cur == cur0)) {
-      const unsigned tot = __reduce_add_sync(kAll, run);
-      const unsigned clk = kClock ? __reduce_add_sync(kAll, dt_clk * run) : 0u;
-      if (lane == 0 && cur0 >= 0 && tot) {
-        atomicAdd(s_cnt + cur0, tot);
-        if (kClock) atomicAdd(s_clk + cur0, clk);
-      }
-    } else if (cur >= 0 && run) {
-      atomicAdd(s_cnt + cur, run);
-      if (kClock) atomicAdd(s_clk + cur, dt_clk * run);
-    }
-    __syncthreads();  // s_F / s_J / s_box reuse
   }
 
-  // ---- CTA totals, histogram flush, epilogue (as the surrogate kernel) ----
+  // ---- CTA totals, deposit box, histogram flush, epilogue ----
   const unsigned long long wa = (unsigned long long)warp_sum((long long)removed);
   const long long wm = warp_min(first_out), we = warp_sum(err);
+  const int wimin = __reduce_min_sync(kAll, bimin), wimax = __reduce_max_sync(kAll, bimax);
+  const int wjmin = __reduce_min_sync(kAll, bjmin), wjmax = __reduce_max_sync(kAll, bjmax);
   if (lane == 0) {
     s_red[warp] = wa;
     s_min[warp] = wm;
     if (we) atomicAdd((unsigned long long*)&p.st->err, (unsigned long long)we);
+    if (wimin <= wimax) {
+      atomicMin(&s_box[0], wimin);
+      atomicMax(&s_box[1], wimax);
+      atomicMin(&s_box[2], wjmin);
+      atomicMax(&s_box[3], wjmax);
+    }
   }
   __syncthreads();
   if (tid == 0) {
@@ -452,6 +485,12 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
     if (ta) {
       atomicAdd(&p.st->leavers, ta);
       atomicMin(&p.st->first_leaver, tm);
+    }
+    if (s_box[0] <= s_box[1]) {
+      atomicMin(p.dep_box + 0, s_box[0]);
+      atomicMax(p.dep_box + 1, s_box[1]);
+      atomicMin(p.dep_box + 2, s_box[2]);
+      atomicMax(p.dep_box + 3, s_box[3]);
     }
   }
   for (int b = tid; b < p.nb; b += kPB) {
@@ -485,22 +524,181 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
   }
 }
 
-// Fixed-point current -> float32 J (J += sum / scale), accumulators zeroed.
-__global__ void pic_current_kernel(unsigned long long* acc0, unsigned long long* acc1,
-                                   unsigned long long* acc2, float* J0, float* J1, float* J2,
-                                   long long cells, double inv_scale) {
-  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < cells;
-       o += (long long)gridDim.x * blockDim.x) {
-    unsigned long long* acc[3] = {acc0, acc1, acc2};
-    float* J[3] = {J0, J1, J2};
+// Sorted mode, resynchronisation: particles per cell of the current
+// positions (runs of equal cells per lane -> one RED each).
+__global__ void pic_count_kernel(const double* __restrict__ z, const double* __restrict__ x,
+                                 const DevState* st, unsigned* cell_cnt, int nx) {
+  const long long n = st->n;
+  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r * kRun < n;
+       r += (long long)gridDim.x * blockDim.x) {
+    int cur = -1;
+    unsigned m = 0;
+    for (long long i = r * kRun; i < min(n, (r + 1) * kRun); ++i) {
+      const int key = (int)__ldg(z + i) * nx + (int)__ldg(x + i);
+      if (key != cur) {
+        if (m) red_add32(cell_cnt + cur, m);
+        cur = key;
+        m = 0;
+      }
+      ++m;
+    }
+    if (m) red_add32(cell_cnt + cur, m);
+  }
+}
+
+// Exclusive scan of cell_cnt into cursor (the first slot of each cell), in
+// two launches over kScanBlocks contiguous segments; cell_cnt is zeroed.
+constexpr int kScanBlocks = 296;
+constexpr int kScanThreads = 1024;
+
+__global__ void pic_scan_reduce_kernel(const unsigned* __restrict__ cell_cnt, long long cells,
+                                       unsigned* block_sum) {
+  const long long seg = (cells + gridDim.x - 1) / gridDim.x;
+  const long long a = blockIdx.x * seg, b = min(cells, a + seg);
+  unsigned s = 0;
+  for (long long c = a + threadIdx.x; c < b; c += blockDim.x) s += cell_cnt[c];
+  s = __reduce_add_sync(kAll, s);
+  __shared__ unsigned w[32];
+  if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    unsigned v = threadIdx.x < (blockDim.x >> 5) ? w[threadIdx.x] : 0u;
+    v = __reduce_add_sync(kAll, v);
+    if (threadIdx.x == 0) block_sum[blockIdx.x] = v;
+  }
+}
+
+__global__ void pic_scan_apply_kernel(unsigned* cell_cnt, long long cells,
+                                      const unsigned* __restrict__ block_sum, unsigned* cursor) {
+  __shared__ unsigned w[32];
+  __shared__ unsigned s_base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // this segment's base: sum of the preceding segments' totals
+  unsigned pre = 0;
+  for (int i = threadIdx.x; i < (int)blockIdx.x; i += blockDim.x) pre += block_sum[i];
+  pre = __reduce_add_sync(kAll, pre);
+  if (lane == 0) w[warp] = pre;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += w[i];
+    s_base = t;
+  }
+  __syncthreads();
+  unsigned base = s_base;
+  const long long seg = (cells + gridDim.x - 1) / gridDim.x;
+  const long long a = blockIdx.x * seg, b = min(cells, a + seg);
+  for (long long c0 = a; c0 < b; c0 += blockDim.x) {
+    const long long c = c0 + threadIdx.x;
+    const unsigned v = c < b ? cell_cnt[c] : 0u;
+    // block-wide exclusive scan of v
+    unsigned incl = v;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const long long v = (long long)acc[c][o];
-      if (v) {
-        J[c][o] = __fadd_rn(J[c][o], (float)__dmul_rn((double)v, inv_scale));
-        acc[c][o] = 0ull;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned t = __shfl_up_sync(kAll, incl, o);
+      if (lane >= o) incl += t;
+    }
+    __syncthreads();
+    if (lane == 31) w[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      unsigned t = lane < (int)(blockDim.x >> 5) ? w[lane] : 0u;
+      unsigned ti = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(kAll, ti, o);
+        if (lane >= o) ti += y;
+      }
+      w[lane] = ti - t;   // exclusive warp offsets
+    }
+    __syncthreads();
+    const unsigned excl = base + w[warp] + incl - v;
+    if (c < b) {
+      cursor[c] = excl;
+      cell_cnt[c] = 0u;
+    }
+    // next chunk's base = excl of the last thread + its v
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_base = excl + v;
+    __syncthreads();
+    base = s_base;
+  }
+}
+
+// fields -> quads: Q[c][qi*(nx+1) + qj] = (F[qi][qj], F[qi][qj+1], F[qi+1][qj],
+// F[qi+1][qj+1]) in padded indices, qi in [0, nz], qj in [0, nx]; also resets
+// the deposit bounding box for this step's push.
+__global__ void pic_quad_kernel(const float* __restrict__ F0, const float* __restrict__ F1,
+                                const float* __restrict__ F2, const float* __restrict__ F3,
+                                const float* __restrict__ F4, const float* __restrict__ F5,
+                                float4* Q, long long quads, int qpitch, int pitch, int* dep_box) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    dep_box[0] = INT_MAX;
+    dep_box[1] = INT_MIN;
+    dep_box[2] = INT_MAX;
+    dep_box[3] = INT_MIN;
+  }
+  const float* F[6] = {F0, F1, F2, F3, F4, F5};
+  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < quads;
+       o += (long long)gridDim.x * blockDim.x) {
+    const int qi = (int)(o / qpitch), qj = (int)(o - (long long)qi * qpitch);
+    const long long g = (long long)qi * pitch + qj;
+#pragma unroll
+    for (int c = 0; c < 6; ++c)
+      __stcg(Q + c * quads + o, make_float4(__ldg(F[c] + g), __ldg(F[c] + g + 1),
+                                            __ldg(F[c] + g + pitch), __ldg(F[c] + g + pitch + 1)));
+  }
+}
+
+// Jc (cell-centric node sums) -> J: node (i, j) collects the slots of the
+// cells around it; J += float32(sum / scale) as the oracle's deposit.
+__global__ void pic_current_kernel(const unsigned long long* __restrict__ Jc, const int* dep_box,
+                                   float* Jx, float* Jy, float* Jz, int nz, int nx,
+                                   double inv_scale) {
+  const int bi0 = dep_box[0], bi1 = dep_box[1], bj0 = dep_box[2], bj1 = dep_box[3];
+  if (bi0 > bi1) return;
+  // receiving nodes: rows [bi0-1, bi1+1] x cols [bj0-1, bj1+1]
+  const int r0 = bi0 - 1, c0 = bj0 - 1, R = bi1 - bi0 + 3, C = bj1 - bj0 + 3;
+  const int pitch = nx + 2;
+  const long long all = (long long)R * C;
+  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < all;
+       o += (long long)gridDim.x * blockDim.x) {
+    const int i = r0 + (int)(o / C), j = c0 + (int)(o % C);
+    if (i < -1 || i > nz || j < -1 || j > nx) continue;
+    long long sx = 0, sy = 0, sz = 0;
+#pragma unroll
+    for (int r = -1; r <= 1; ++r) {
+      const int ci = i - r;
+      if (ci < 0 || ci >= nz) continue;
+#pragma unroll
+      for (int s = -1; s <= 1; ++s) {
+        const int cj = j - s;
+        if (cj < 0 || cj >= nx) continue;
+        const unsigned long long* cell = Jc + ((long long)ci * nx + cj) * kNodes;
+        if (r >= 0) sx += (long long)cell[r * 3 + s + 1];                       // Jx rows {0,1}
+        if (r >= 0 && s >= 0) sy += (long long)cell[6 + r * 2 + s];              // Jy
+        if (s >= 0) sz += (long long)cell[10 + (r + 1) * 2 + s];                 // Jz cols {0,1}
       }
     }
+    const long long o2 = (long long)(i + 1) * pitch + (j + 1);
+    if (sx) Jx[o2] = __fadd_rn(Jx[o2], (float)__dmul_rn((double)sx, inv_scale));
+    if (sy) Jy[o2] = __fadd_rn(Jy[o2], (float)__dmul_rn((double)sy, inv_scale));
+    if (sz) Jz[o2] = __fadd_rn(Jz[o2], (float)__dmul_rn((double)sz, inv_scale));
+  }
+}
+
+// Clears the deposit bounding box of Jc (after pic_current_kernel).
+__global__ void pic_zero_kernel(unsigned long long* Jc, const int* dep_box, int nx) {
+  const int bi0 = dep_box[0], bi1 = dep_box[1], bj0 = dep_box[2], bj1 = dep_box[3];
+  if (bi0 > bi1) return;
+  const int C = bj1 - bj0 + 1;
+  const long long all = (long long)(bi1 - bi0 + 1) * C * (kNodes / 2);
+  ulonglong2* J2 = reinterpret_cast<ulonglong2*>(Jc);
+  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < all;
+       o += (long long)gridDim.x * blockDim.x) {
+    const long long cell = o / (kNodes / 2);
+    const int i = bi0 + (int)(cell / C), j = bj0 + (int)(cell % C);
+    J2[((long long)i * nx + j) * (kNodes / 2) + (o % (kNodes / 2))] = make_ulonglong2(0ull, 0ull);
   }
 }
 
@@ -563,6 +761,8 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   clear_error();
   if (!ctx || !a) return set_error(LBX_EINVAL, "NULL argument");
   if (a->nz < 1 || a->nx < 1) return set_error(LBX_EINVAL, "grid must be at least 1x1");
+  if ((long long)(a->nz + 1) * (a->nx + 1) >= (1ll << 31) / 16)
+    return set_error(LBX_EINVAL, "PIC grid too large (quad index must fit 32 bits)");
   if (a->box_size < 1 || a->nz % a->box_size || a->nx % a->box_size ||
       (a->box_size & (a->box_size - 1)))
     return set_error(LBX_EINVAL, "PIC box_size must be a power of two dividing the grid");
@@ -572,9 +772,15 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
     if (!a->fields[c]) return set_error(LBX_EINVAL, "NULL field array");
   for (int c = 0; c < 3; ++c)
     if (!a->current[c]) return set_error(LBX_EINVAL, "NULL current array");
-  if (((uintptr_t)a->z | (uintptr_t)a->x | (uintptr_t)a->uz | (uintptr_t)a->ux |
-       (uintptr_t)a->uy) & 15u)
-    return set_error(LBX_EINVAL, "particle arrays must be 16-byte aligned");
+  const bool sorted = a->out[0] != nullptr;
+  uintptr_t al = (uintptr_t)a->z | (uintptr_t)a->x | (uintptr_t)a->uz | (uintptr_t)a->ux |
+                 (uintptr_t)a->uy;
+  for (int c = 0; c < 5; ++c) {
+    if (sorted && !a->out[c]) return set_error(LBX_EINVAL, "sorted mode needs all 5 output arrays");
+    al |= (uintptr_t)a->out[c];
+  }
+  if (al & 31u) return set_error(LBX_EINVAL, "particle arrays must be 32-byte aligned");
+  if (!(a->q_times_w != 0.0)) return set_error(LBX_EINVAL, "q_times_w must be nonzero");
   const int nbz = a->nz / a->box_size, nbx = a->nx / a->box_size, nb = nbz * nbx;
   if (nb > 4096) return set_error(LBX_EINVAL, "PIC step supports <= 4096 boxes");
   int rc = ensure_accumulators(ctx, nb);
@@ -582,37 +788,80 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   rc = reserve_status(ctx, ctx->n_upper);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
+  const long long cells = (long long)a->nz * a->nx;
+  const long long quads = (long long)(a->nz + 1) * (a->nx + 1);
+  if (!ctx->pic_acc || ctx->pic_cells < cells) {
+    if (ctx->pic_acc) {
+      cudaDeviceSynchronize();
+      cudaFree(ctx->pic_acc);
+    }
+    ctx->pic_acc = nullptr;
+    const size_t bytes = (size_t)cells * kNodes * 8 + 16;
+    if (cudaMalloc(&ctx->pic_acc, bytes) != cudaSuccess)
+      return set_error(LBX_EOOM, "PIC current accumulators");
+    cudaMemsetAsync(ctx->pic_acc, 0, bytes, s);
+    ctx->pic_cells = cells;
+  }
+  if (!ctx->pic_quad || ctx->pic_quads < quads) {
+    if (ctx->pic_quad) {
+      cudaDeviceSynchronize();
+      cudaFree(ctx->pic_quad);
+    }
+    ctx->pic_quad = nullptr;
+    if (cudaMalloc(&ctx->pic_quad, (size_t)quads * 6 * sizeof(float4)) != cudaSuccess)
+      return set_error(LBX_EOOM, "PIC quad field buffer");
+    ctx->pic_quads = quads;
+  }
+  if (sorted && (!ctx->pic_sortbuf || ctx->pic_sort_cells < cells)) {
+    if (ctx->pic_sortbuf) {
+      cudaDeviceSynchronize();
+      cudaFree(ctx->pic_sortbuf);
+    }
+    ctx->pic_sortbuf = nullptr;
+    const size_t bytes = ((size_t)cells * 2 + kScanBlocks) * sizeof(unsigned);
+    if (cudaMalloc(&ctx->pic_sortbuf, bytes) != cudaSuccess)
+      return set_error(LBX_EOOM, "PIC sort buffers");
+    cudaMemsetAsync(ctx->pic_sortbuf, 0, bytes, s);
+    ctx->pic_sort_cells = cells;
+    ctx->pic_sort_next = nullptr;
+  }
+  float4* Q = static_cast<float4*>(ctx->pic_quad);
+  unsigned* cell_cnt = sorted ? ctx->pic_sortbuf : nullptr;
+  unsigned* cursor = sorted ? ctx->pic_sortbuf + cells : nullptr;
+  unsigned* block_sum = sorted ? ctx->pic_sortbuf + 2 * cells : nullptr;
+  int* dep_box = reinterpret_cast<int*>(ctx->pic_acc + ctx->pic_cells * kNodes);
   PicParams p{};
   p.z = a->z;
   p.x = a->x;
   p.uz = a->uz;
   p.ux = a->ux;
   p.uy = a->uy;
-  for (int c = 0; c < 6; ++c) p.F[c] = a->fields[c];
-  const long long padded = (long long)(a->nz + 2) * (a->nx + 2);
-  if (!ctx->pic_acc || ctx->pic_cells < padded) {
-    if (ctx->pic_acc) {
-      cudaDeviceSynchronize();
-      cudaFree(ctx->pic_acc);
-    }
-    ctx->pic_acc = nullptr;
-    if (cudaMalloc(&ctx->pic_acc, (size_t)padded * 3 * 8) != cudaSuccess)
-      return set_error(LBX_EOOM, "PIC current accumulators");
-    cudaMemset(ctx->pic_acc, 0, (size_t)padded * 3 * 8);
-    ctx->pic_cells = padded;
-  }
-  for (int c = 0; c < 3; ++c) p.Jacc[c] = ctx->pic_acc + c * padded;
-  if (!(a->q_times_w != 0.0)) return set_error(LBX_EINVAL, "q_times_w must be nonzero");
+  double* out[5] = {a->z, a->x, a->uz, a->ux, a->uy};
+  if (sorted)
+    for (int c = 0; c < 5; ++c) out[c] = a->out[c];
+  p.oz = out[0];
+  p.ox = out[1];
+  p.ouz = out[2];
+  p.oux = out[3];
+  p.ouy = out[4];
+  p.cell_cnt = cell_cnt;
+  p.cursor = cursor;
+  for (int c = 0; c < 6; ++c) p.Q[c] = Q + c * quads;
+  p.Jc = ctx->pic_acc;
+  p.dep_box = dep_box;
   int e2 = 0;
   std::frexp(1048576.0 / std::fabs(a->q_times_w), &e2);  // scale = 2^floor(log2(2^20/|qw|))
-  p.jscale = std::ldexp(1.0, e2 - 1);
+  const double jscale = std::ldexp(1.0, e2 - 1);
+  p.vscale = (float)jscale;
   p.nz = a->nz;
   p.nx = a->nx;
-  p.pitch = a->nx + 2;
+  p.qpitch = a->nx + 1;
   p.qm = a->q_over_m;
   p.qw = a->q_times_w;
   p.dt = a->dt;
-  p.inv_m = 1.0 / (double)a->box_size;
+  int l2 = 0;
+  while ((1 << l2) < a->box_size) ++l2;
+  p.log2m = l2;
   p.nbz = nbz;
   p.nbx = nbx;
   p.nb = nb;
@@ -627,33 +876,53 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   p.wp = a->w_particle;
   p.wc = a->w_cell;
   p.cells = (double)a->box_size * (double)a->box_size;
-  const size_t smem = (size_t)nb * 8 + (size_t)kPatchMax * 9 * 4;
+  const int pitch = a->nx + 2;
+  const unsigned qg = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 8, (quads + 255) / 256));
+  if (sorted && (ctx->pic_sort_next != a->z || (a->flags & LBX_PIC_RESYNC))) {
+    // the slots of the input's cells are unknown: count them (cell_cnt is zero here)
+    const unsigned ng = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 8,
+                                                         (long long)(ctx->n_upper / kRun + 255) / 256));
+    pic_count_kernel<<<ng, 256, 0, s>>>(a->z, a->x, ctx->st, cell_cnt, a->nx);
+    pic_scan_reduce_kernel<<<kScanBlocks, kScanThreads, 0, s>>>(cell_cnt, cells, block_sum);
+    pic_scan_apply_kernel<<<kScanBlocks, kScanThreads, 0, s>>>(cell_cnt, cells, block_sum, cursor);
+  }
+  pic_quad_kernel<<<qg, 256, 0, s>>>(a->fields[0], a->fields[1], a->fields[2], a->fields[3],
+                                     a->fields[4], a->fields[5], Q, quads, p.qpitch, pitch,
+                                     dep_box);
+  const size_t smem = (size_t)nb * 8;
   const bool clock = (a->flags & LBX_STEP_CLOCK) != 0;
-  auto kern = clock ? pic_push_kernel<true> : pic_push_kernel<false>;
+  auto kern = clock ? (sorted ? pic_push_kernel<true, true> : pic_push_kernel<true, false>)
+                    : (sorted ? pic_push_kernel<false, true> : pic_push_kernel<false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(pic)");
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPB, smem);
   long long grid = (long long)std::max(per_sm, 1) * ctx->num_sms;
   if (ctx->grid_override > 0) grid = ctx->grid_override;
-  grid = std::max(1ll, std::min(grid, (long long)((ctx->n_upper + kPChunk - 1) / kPChunk)));
+  const long long units = (ctx->n_upper + kUnitP - 1) / kUnitP;
+  grid = std::max(1ll, std::min(grid, (units + kPW - 1) / kPW));
   kern<<<(unsigned)grid, kPB, smem, s>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "pic_push_kernel launch");
-  const unsigned cg = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 8, (padded + 255) / 256));
-  pic_current_kernel<<<cg, 256, 0, s>>>(p.Jacc[0], p.Jacc[1], p.Jacc[2], a->current[0],
-                                        a->current[1], a->current[2], padded, 1.0 / p.jscale);
-  rc = launch_compact(ctx, a->z, a->x, a->uz, a->ux, a->uy, nullptr, (double)a->nz,
+  const unsigned cg = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 8, (cells + 255) / 256));
+  pic_current_kernel<<<cg, 256, 0, s>>>(ctx->pic_acc, dep_box, a->current[0], a->current[1],
+                                        a->current[2], a->nz, a->nx, 1.0 / jscale);
+  pic_zero_kernel<<<cg, 256, 0, s>>>(ctx->pic_acc, dep_box, a->nx);
+  rc = launch_compact(ctx, out[0], out[1], out[2], out[3], out[4], nullptr, (double)a->nz,
                       (double)a->nx, stream);
   if (rc) return rc;
+  if (sorted) {   // next step's slots: exclusive scan of this step's kept particles per cell
+    pic_scan_reduce_kernel<<<kScanBlocks, kScanThreads, 0, s>>>(cell_cnt, cells, block_sum);
+    pic_scan_apply_kernel<<<kScanBlocks, kScanThreads, 0, s>>>(cell_cnt, cells, block_sum, cursor);
+    ctx->pic_sort_next = out[0];
+  }
   if (a->flags & LBX_PIC_NO_FIELD_SOLVE) return LBX_OK;
-  const long long cells = (long long)a->nz * a->nx;
   const unsigned fg = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 8, (cells + 255) / 256));
   pic_b_kernel<<<fg, 256, 0, s>>>(a->fields[0], a->fields[1], a->fields[2], a->fields[3],
-                                  a->fields[4], a->fields[5], a->nz, a->nx, p.pitch, a->dt);
+                                  a->fields[4], a->fields[5], a->nz, a->nx, pitch, a->dt);
   pic_e_kernel<<<fg, 256, 0, s>>>(a->fields[0], a->fields[1], a->fields[2], a->fields[3],
                                   a->fields[4], a->fields[5], a->current[0], a->current[1],
-                                  a->current[2], a->nz, a->nx, p.pitch, a->dt);
+                                  a->current[2], a->nz, a->nx, pitch, a->dt);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "field solve launch");
   return LBX_OK;

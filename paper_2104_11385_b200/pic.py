@@ -35,6 +35,8 @@ class PicState:
     nz: int
     nx: int
 
+    spare: tuple = None     # sorted mode: output buffers (z, x, uz, ux, uy), swapped each step
+
     @classmethod
     def create(cls, pos, u, nz, nx, device="cuda:0"):
         dev = require_cuda(device)
@@ -59,8 +61,13 @@ class PicState:
 
 
 def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times_w: float,
-             dt: float, weights=(0.75, 0.25), clock=False, field_solve=True):
-    """One PIC step in place; returns per-box counts / cost / clock and n."""
+             dt: float, weights=(0.75, 0.25), clock=False, field_solve=True, sort=False):
+    """One PIC step; returns per-box counts / cost / clock and n.
+
+    sort=False: in place, particle order kept (compaction is stable).
+    sort=True: sort-on-write -- results land in a second buffer set grouped by
+    each particle's cell at the start of the step, which the state then
+    swaps in (order within a cell is not deterministic; values are)."""
     dev = ctx.device
     nbz, nbx = st.nz // box_size, st.nx // box_size
     nb = nbz * nbx
@@ -82,7 +89,19 @@ def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times
                                                         _lib.LBX_PIC_NO_FIELD_SOLVE)
     a.counts_out, a.cost_out, a.clk_out = _lib.ptr(counts), _lib.ptr(cost), _lib.ptr(clk)
     a.n_out, a.err_out = _lib.ptr(nout), _lib.ptr(nout[1:])
+    names = ("z", "x", "uz", "ux", "uy")
+    if sort:
+        cap = st.z.numel()
+        if st.spare is None or st.spare[0].numel() != cap:
+            st.spare = tuple(torch.zeros(cap, dtype=torch.float64, device=dev) for _ in names)
+        for i, t in enumerate(st.spare):
+            a.out[i] = _lib.ptr(t)
     _lib.check(_lib.lib.lbx_pic_step(ctx.handle, C.byref(a), _stream(dev)))
+    if sort:
+        old = tuple(getattr(st, k) for k in names)
+        for k, t in zip(names, st.spare):
+            setattr(st, k, t)
+        st.spare = old
     h = nout.cpu().numpy()
     if h[1]:
         raise ValueError(f"{int(h[1])} particles fell outside the box grid")
