@@ -206,14 +206,42 @@ __device__ __forceinline__ void node_values(const Axis& az, const Axis& ax, floa
   q[15] = qnode(vsz, zp, x1);
 }
 
+// Per-warp flush queue in shared memory: a lane that must hand a cell's node
+// sums to HBM (cell change, isolated drifted particle, end of run) writes
+// them here with 4 vector stores inside the divergent branch; the warp then
+// drains the queue together, one 16-lane 128-byte RED per entry and two
+// entries per instruction -- instead of every lane issuing 16 predicated
+// REDs whenever any lane flushes.
+struct __align__(16) FlushEntry {
+  int4 v[kNodes / 4];
+  int cell;
+  unsigned m;
+  int pad[2];
+};
+constexpr int kQCap = 32 * kG;   // drained after every group and after the run's final entries
+
 template <bool kSort>
-__device__ __forceinline__ void flush_cell(const PicParams& p, int cell, const int acc[kNodes],
-                                           unsigned m) {
-  unsigned long long* d = p.Jc + (long long)cell * kNodes;
+__device__ __forceinline__ void drain_queue(const PicParams& p, const FlushEntry* q, int count,
+                                            int lane) {
+  __syncwarp();
+  const int node = lane & 15;
+  for (int e0 = 0; e0 < count; e0 += 2) {
+    const int e = e0 + (lane >> 4);
+    if (e < count) {
+      const int cell = q[e].cell;
+      const int v = reinterpret_cast<const int*>(q[e].v)[node];
+      if (v) red_add(p.Jc + (long long)cell * kNodes + node, v);
+      if (kSort && node == 0) red_add32(p.cell_cnt + cell, q[e].m);
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void enqueue(FlushEntry* e, const int v[kNodes], int cell, unsigned m) {
 #pragma unroll
-  for (int i = 0; i < kNodes; ++i)
-    if (acc[i]) red_add(d + i, acc[i]);
-  if (kSort) red_add32(p.cell_cnt + cell, m);
+  for (int i = 0; i < kNodes / 4; ++i) e->v[i] = make_int4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  e->cell = cell;
+  e->m = m;
 }
 
 #ifndef LBX_PIC_MINB
@@ -221,9 +249,10 @@ __device__ __forceinline__ void flush_cell(const PicParams& p, int cell, const i
 #endif
 template <bool kClock, bool kSort>
 __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p) {
-  extern __shared__ __align__(16) unsigned s_hist[];
-  unsigned* s_cnt = s_hist;           // nb
-  unsigned* s_clk = s_hist + p.nb;    // nb
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  FlushEntry* s_q = reinterpret_cast<FlushEntry*>(s_dyn) + (size_t)(threadIdx.x >> 5) * kQCap;
+  unsigned* s_cnt = reinterpret_cast<unsigned*>(s_dyn + (size_t)kPW * kQCap * sizeof(FlushEntry));  // nb
+  unsigned* s_clk = s_cnt + p.nb;                                                                   // nb
   __shared__ long long s_n;
   __shared__ int s_box[4];
   __shared__ int s_last;
@@ -268,7 +297,7 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
 #pragma unroll 1
     for (int g = 0; g < kRun / kG; ++g) {
       const long long i0 = run0 + g * kG;
-      if (i0 >= n) break;
+      if (__all_sync(kAll, i0 >= n)) break;     // warp-uniform: the queue below is warp-collective
       double pz[kG], px[kG], puz[kG], pux[kG], puy[kG];
       ldg(p.z, i0, n, pz);
       ldg(p.x, i0, n, px);
@@ -385,31 +414,25 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
       }
       // ---- phase 2: current.  Accumulate in registers while consecutive
       // particles share a cell; an isolated particle in another cell (drift)
-      // is added directly; otherwise switch cells.  One flush site (16 REDs)
-      // per particle. ----
+      // is queued directly; otherwise the finished cell is queued and the
+      // lane switches cells.  The queue drains once per group. ----
+      const unsigned lt = (1u << lane) - 1u;
+      int qn = 0;
 #pragma unroll
       for (int k = 0; k < kG; ++k) {
-        if (nkey[k] < 0) continue;
-        const Axis az = axis_of(pz[k]), ax = axis_of(px[k]);
+        const bool dep = nkey[k] >= 0;
+        const Axis az = axis_of(dep ? pz[k] : 0.5), ax = axis_of(dep ? px[k] : 0.5);
         int q[kNodes];
-        node_values(az, ax, vsx[k], vsy[k], vsz[k], q);
-        bimin = min(bimin, az.i);
-        bimax = max(bimax, az.i);
-        bjmin = min(bjmin, ax.i);
-        bjmax = max(bjmax, ax.i);
-        const bool same = nkey[k] == cur;
-        const bool strag = !same && cur >= 0 && k + 1 < kG && nkey[k + 1] != nkey[k];
-        const bool swap = !same && !strag;
-        const int fcell = strag ? nkey[k] : (swap ? cur : -1);
-        if (fcell >= 0) {
-          unsigned long long* d = p.Jc + (long long)fcell * kNodes;
-#pragma unroll
-          for (int i = 0; i < kNodes; ++i) {
-            const int v = strag ? q[i] : acc[i];
-            if (v) red_add(d + i, v);
-          }
-          if (kSort) red_add32(p.cell_cnt + fcell, strag ? 1u : cur_m);
-        }
+        node_values(az, ax, vsx[k], vsy[k], vsz[k], q);   // v = 0 -> q = 0 off-deposit
+        const bool same = dep && nkey[k] == cur;
+        const bool strag = dep && !same && cur >= 0 && k + 1 < kG && nkey[k + 1] != nkey[k];
+        const bool swap = dep && !same && !strag;
+        const bool need = strag || (swap && cur >= 0);
+        const unsigned fm = __ballot_sync(kAll, need);
+        if (need)
+          enqueue(s_q + qn + __popc(fm & lt), strag ? q : acc, strag ? nkey[k] : cur,
+                  strag ? 1u : cur_m);
+        qn += __popc(fm);
         if (same) {
 #pragma unroll
           for (int i = 0; i < kNodes; ++i) acc[i] += q[i];
@@ -420,6 +443,11 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
           cur = nkey[k];
           cur_m = 1;
         }
+        if (!dep) continue;
+        bimin = min(bimin, az.i);
+        bimax = max(bimax, az.i);
+        bjmin = min(bjmin, ax.i);
+        bjmax = max(bjmax, ax.i);
         // per-box survivor counts (+ clock): run-length per lane
         const int bz = az.i >> p.log2m, bx = ax.i >> p.log2m;
         if (bz >= p.nbz || bx >= p.nbx) {
@@ -439,8 +467,13 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
           hn = 1;
         }
       }
+      if (qn) drain_queue<kSort>(p, s_q, qn, lane);
     }
-    if (cur >= 0) flush_cell<kSort>(p, cur, acc, cur_m);
+    {   // end of the lane's run: queue its open cell, drain
+      const unsigned fm = __ballot_sync(kAll, cur >= 0);
+      if (cur >= 0) enqueue(s_q + __popc(fm & ((1u << lane) - 1u)), acc, cur, cur_m);
+      if (fm) drain_queue<kSort>(p, s_q, __popc(fm), lane);
+    }
     // last box run of the lane: warp-uniform fast path (one shared atomic)
     unsigned tclk = 0;
     if (kClock && hb >= 0) tclk = (unsigned)min((clock64() - t_last) >> 4, (long long)(1u << 30));
@@ -889,7 +922,7 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   pic_quad_kernel<<<qg, 256, 0, s>>>(a->fields[0], a->fields[1], a->fields[2], a->fields[3],
                                      a->fields[4], a->fields[5], Q, quads, p.qpitch, pitch,
                                      dep_box);
-  const size_t smem = (size_t)nb * 8;
+  const size_t smem = (size_t)kPW * kQCap * sizeof(FlushEntry) + (size_t)nb * 8;
   const bool clock = (a->flags & LBX_STEP_CLOCK) != 0;
   auto kern = clock ? (sorted ? pic_push_kernel<true, true> : pic_push_kernel<true, false>)
                     : (sorted ? pic_push_kernel<false, true> : pic_push_kernel<false, false>);
