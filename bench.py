@@ -541,7 +541,7 @@ def e2e_plugin(args, dev, pos0, kick0, R, sc):
     kernels.advance_particles / bin_particles for host arrays) on the
     particles in pinned host memory -- host->device copy of all particles,
     push + absorb + compaction + per-box counts + heuristic cost, and the
-    survivors, counts and costs copied back -- chunked over two streams so
+    survivors, counts and costs copied back -- chunked over three streams so
     both PCIe directions overlap the kernels."""
     import torch
 
@@ -581,7 +581,7 @@ def e2e_plugin(args, dev, pos0, kick0, R, sc):
             "d2h_bytes_per_step": io["d2h"] // args.e2e_steps,
             "steps": args.e2e_steps,
             "path": "lbx_advance_bin_host (reference AoS layout, pinned host buffers, "
-                    "4 Mi-particle chunks over 2 streams), copies in the timed region"}
+                    "4 Mi-particle chunks over 3 streams, no host round trip per chunk), copies in the timed region"}
 
 
 def main():

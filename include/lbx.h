@@ -89,11 +89,13 @@ int lbx_bin_particles(const double* pos, int64_t n, double box_size,
 /* The plugin path for HOST arrays (the reference calls advance_particles and
  * bin_particles on numpy arrays every step, workload.py:293-298): advance
  * [n][2] host pos/vel (pinned for full PCIe speed) into host out_pos/out_vel
- * (survivors, order kept, *m_out of them) and, when counts != NULL, the
- * per-box counts of the survivors and their heuristic cost (cost may be
- * NULL).  Chunks alternate over two streams with separate look-back state,
- * so host->device copies, kernels and device->host copies overlap (PCIe is
- * full duplex).  Synchronous. */
+ * (capacity n; survivors, order kept, *m_out of them) and, when counts !=
+ * NULL, the per-box counts of the survivors and their heuristic cost (cost
+ * may be NULL).  4 Mi-particle chunks rotate over three streams, each chunk
+ * stream-ordered end to end (copy in, advance, bin, copy out) with no host
+ * round trip, so both PCIe directions and the kernels overlap; a chunk's
+ * survivors land at its own offset and gaps left by absorbed particles are
+ * closed on the host afterwards.  Synchronous. */
 int lbx_advance_bin_host(lbx_ctx* ctx, const double* pos, const double* vel, int64_t n,
                          double extent_z, double extent_x, double box_size,
                          int32_t nbz, int32_t nbx, double w_particle, double w_cell,

@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -1246,16 +1247,20 @@ namespace {
 
 }  // namespace
 
-// Two-lane host-buffer pipeline state (lbx_advance_bin_host), cached in ctx.
+// Host-buffer pipeline state (lbx_advance_bin_host), cached in ctx: kLanes
+// streams, each with its own device chunk buffers and look-back state.
 struct HostPipe {
   static constexpr long long kChunk = 1ll << 22;  // 4 Mi particles per chunk
-  cudaStream_t s[2] = {};
-  cudaEvent_t done[2] = {}, ready = {};
-  DevState* st[2] = {};
-  unsigned long long* status[2] = {};
-  double *d_in_pos[2] = {}, *d_in_vel[2] = {}, *d_out_pos[2] = {}, *d_out_vel[2] = {};
-  long long* d_m[2] = {};
-  long long* h_m = nullptr;  // pinned [2]
+  static constexpr int kLanes = 3;
+  cudaStream_t s[kLanes] = {};
+  cudaEvent_t ready = {};
+  DevState* st[kLanes] = {};
+  unsigned long long* status[kLanes] = {};
+  double *d_in_pos[kLanes] = {}, *d_in_vel[kLanes] = {}, *d_out_pos[kLanes] = {},
+         *d_out_vel[kLanes] = {};
+  long long* d_m[kLanes] = {};
+  long long* h_m = nullptr;  // pinned [h_m_cap]: survivors per chunk (+1: error count)
+  long long h_m_cap = 0;
   long long* d_counts = nullptr;
   double* d_cost = nullptr;
   long long* d_err = nullptr;
@@ -1264,9 +1269,8 @@ struct HostPipe {
 
 void destroy_pipe(HostPipe* hp) {
   if (!hp) return;
-  for (int l = 0; l < 2; ++l) {
+  for (int l = 0; l < HostPipe::kLanes; ++l) {
     if (hp->s[l]) cudaStreamSynchronize(hp->s[l]), cudaStreamDestroy(hp->s[l]);
-    if (hp->done[l]) cudaEventDestroy(hp->done[l]);
     cudaFree(hp->st[l]);
     cudaFree(hp->status[l]);
     cudaFree(hp->d_in_pos[l]);
@@ -1285,8 +1289,19 @@ void destroy_pipe(HostPipe* hp) {
 
 namespace {
 
-int ensure_pipe(lbx_ctx* ctx, long long nb) {
-  if (ctx->pipe && ctx->pipe->nb >= nb) return LBX_OK;
+int ensure_pipe(lbx_ctx* ctx, long long nb, long long nchunks) {
+  if (ctx->pipe && ctx->pipe->nb >= nb) {
+    HostPipe* hp = ctx->pipe;
+    if (hp->h_m_cap < nchunks + 1) {
+      cudaFreeHost(hp->h_m);
+      hp->h_m = nullptr;
+      hp->h_m_cap = 0;
+      if (cudaHostAlloc(&hp->h_m, (size_t)(nchunks + 1) * 8, cudaHostAllocDefault) != cudaSuccess)
+        return set_error(LBX_EOOM, "host pipeline counters");
+      hp->h_m_cap = nchunks + 1;
+    }
+    return LBX_OK;
+  }
   if (ctx->pipe) {
     destroy_pipe(ctx->pipe);
     ctx->pipe = nullptr;
@@ -1294,10 +1309,10 @@ int ensure_pipe(lbx_ctx* ctx, long long nb) {
   HostPipe* hp = new HostPipe();
   const long long C = HostPipe::kChunk;
   const size_t tiles = (size_t)((C + kTile - 1) / kTile + 1);
-  bool ok = cudaHostAlloc(&hp->h_m, 16, cudaHostAllocDefault) == cudaSuccess;
-  for (int l = 0; l < 2 && ok; ++l) {
+  bool ok = cudaHostAlloc(&hp->h_m, (size_t)(nchunks + 1) * 8, cudaHostAllocDefault) == cudaSuccess;
+  hp->h_m_cap = nchunks + 1;
+  for (int l = 0; l < HostPipe::kLanes && ok; ++l) {
     ok = cudaStreamCreateWithFlags(&hp->s[l], cudaStreamNonBlocking) == cudaSuccess &&
-         cudaEventCreateWithFlags(&hp->done[l], cudaEventDisableTiming) == cudaSuccess &&
          cudaMalloc(&hp->st[l], sizeof(DevState)) == cudaSuccess &&
          cudaMalloc(&hp->status[l], tiles * 8) == cudaSuccess &&
          cudaMalloc(&hp->d_in_pos[l], (size_t)C * 16) == cudaSuccess &&
@@ -1711,41 +1726,28 @@ int lbx_advance_bin_host(lbx_ctx* ctx, const double* pos, const double* vel, int
   const long long nb = (long long)nbz * nbx;
   if (bin && nb < 1) return set_error(LBX_EINVAL, "box grid must be at least 1x1");
   cudaSetDevice(ctx->device);
-  int rc = ensure_pipe(ctx, bin ? nb : 0);
+  const long long C = HostPipe::kChunk;
+  const long long nchunks = (n + C - 1) / C;
+  int rc = ensure_pipe(ctx, bin ? nb : 0, nchunks);
   if (rc) return rc;
   HostPipe& hp = *ctx->pipe;
+  constexpr int L = HostPipe::kLanes;
   cudaError_t e = cudaSuccess;
   if (bin) e = cudaMemsetAsync(hp.d_counts, 0, (size_t)nb * 8, hp.s[0]);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
   cudaEventRecord(hp.ready, hp.s[0]);
-  cudaStreamWaitEvent(hp.s[1], hp.ready, 0);
-  const long long C = HostPipe::kChunk;
-  const long long nchunks = (n + C - 1) / C;
+  for (int l = 1; l < L; ++l) cudaStreamWaitEvent(hp.s[l], hp.ready, 0);
   const int smem_hist = (bin && nb <= kSmemBoxesMax) ? 1 : 0;
   const size_t bsmem = smem_hist ? (size_t)nb * 4 : 0;
   if (bsmem > 48 * 1024)
     cudaFuncSetAttribute(bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
-  long long written = 0;
-  auto drain = [&](long long i) -> int {
-    const int l = (int)(i & 1);
-    cudaError_t ee = cudaEventSynchronize(hp.done[l]);
-    if (ee != cudaSuccess) return cuda_fail(ee, "advance chunk");
-    const long long m = hp.h_m[l];
-    if (m > 0) {
-      cudaMemcpyAsync(out_pos + 2 * written, hp.d_out_pos[l], (size_t)m * 16,
-                      cudaMemcpyDeviceToHost, hp.s[l]);
-      cudaMemcpyAsync(out_vel + 2 * written, hp.d_out_vel[l], (size_t)m * 16,
-                      cudaMemcpyDeviceToHost, hp.s[l]);
-    }
-    written += m;
-    return LBX_OK;
-  };
+  // Every chunk is fully stream-ordered (copy in -> advance -> bin -> copy
+  // out -> survivor count) with no host round trip: its survivors land at the
+  // chunk's own offset i*C of the output (speculating that nothing is
+  // absorbed) and the host closes the gaps afterwards in the rare case that
+  // something was.  Lane l = i % L reuses its buffers in stream order.
   for (long long i = 0; i < nchunks; ++i) {
-    const int l = (int)(i & 1);
-    if (i >= 2) {  // lane l is reused: its previous chunk must be drained first
-      rc = drain(i - 2);
-      if (rc) return rc;
-    }
+    const int l = (int)(i % L);
     const long long k = std::min(C, n - i * C);
     cudaStream_t s = hp.s[l];
     cudaMemcpyAsync(hp.d_in_pos[l], pos + 2 * i * C, (size_t)k * 16, cudaMemcpyHostToDevice, s);
@@ -1771,30 +1773,37 @@ int lbx_advance_bin_host(lbx_ctx* ctx, const double* pos, const double* vel, int
           reinterpret_cast<unsigned long long*>(hp.d_counts),
           reinterpret_cast<unsigned long long*>(hp.d_err), hp.d_m[l]);
     }
-    cudaMemcpyAsync(&hp.h_m[l], hp.d_m[l], 8, cudaMemcpyDeviceToHost, s);
-    cudaEventRecord(hp.done[l], s);
+    cudaMemcpyAsync(out_pos + 2 * i * C, hp.d_out_pos[l], (size_t)k * 16, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(out_vel + 2 * i * C, hp.d_out_vel[l], (size_t)k * 16, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&hp.h_m[i], hp.d_m[l], 8, cudaMemcpyDeviceToHost, s);
   }
-  for (long long i = std::max(0ll, nchunks - 2); i < nchunks; ++i) {
-    rc = drain(i);
-    if (rc) return rc;
+  for (int l = 1; l < L; ++l) {
+    cudaEventRecord(hp.ready, hp.s[l]);
+    cudaStreamWaitEvent(hp.s[0], hp.ready, 0);
   }
-  cudaEventRecord(hp.ready, hp.s[1]);
-  cudaStreamWaitEvent(hp.s[0], hp.ready, 0);
   if (bin) {
     counts_cost_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, hp.s[0]>>>(
         hp.d_counts, (int)nb, w_particle, w_cell, box_size * box_size, hp.d_cost);
     cudaMemcpyAsync(counts, hp.d_counts, (size_t)nb * 8, cudaMemcpyDeviceToHost, hp.s[0]);
     if (cost) cudaMemcpyAsync(cost, hp.d_cost, (size_t)nb * 8, cudaMemcpyDeviceToHost, hp.s[0]);
-    cudaMemcpyAsync(&hp.h_m[0], hp.d_err, 8, cudaMemcpyDeviceToHost, hp.s[0]);
+    cudaMemcpyAsync(&hp.h_m[nchunks], hp.d_err, 8, cudaMemcpyDeviceToHost, hp.s[0]);
   }
-  e = cudaStreamSynchronize(hp.s[0]);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(hp.s[1]);
+  for (int l = 0; l < L && e == cudaSuccess; ++l) e = cudaStreamSynchronize(hp.s[l]);
   if (e != cudaSuccess) return cuda_fail(e, "host pipeline");
-  if (bin && hp.h_m[0] != 0) {
+  if (bin && hp.h_m[nchunks] != 0) {
     cudaMemsetAsync(hp.d_err, 0, 8, hp.s[0]);
     cudaStreamSynchronize(hp.s[0]);
     return set_error(LBX_ERANGE, "%lld survivors fall outside the box grid",
-                     (long long)hp.h_m[0]);
+                     (long long)hp.h_m[nchunks]);
+  }
+  long long written = 0;
+  for (long long i = 0; i < nchunks; ++i) {   // close the gaps left by absorbed particles
+    const long long m = hp.h_m[i];
+    if (written != i * C && m > 0) {
+      std::memmove(out_pos + 2 * written, out_pos + 2 * i * C, (size_t)m * 16);
+      std::memmove(out_vel + 2 * written, out_vel + 2 * i * C, (size_t)m * 16);
+    }
+    written += m;
   }
   *m_out = written;
   return LBX_OK;

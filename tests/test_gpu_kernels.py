@@ -118,7 +118,8 @@ def test_fused_sfc_weights_no_fma():
 
 @pytest.mark.parametrize("n", [0, 1, 5000, (1 << 22) + 17, 9_000_001])
 def test_host_pipeline_matches_oracle(K, n):
-    """lbx_advance_bin_host: chunked two-lane pipeline, host buffers."""
+    """lbx_advance_bin_host: chunked three-stream pipeline, host buffers (absorbing:
+    exercises the host-side gap closing across chunks)."""
     rng = np.random.default_rng(n + 7)
     pos = rng.uniform(0, 96.0, size=(n, 2))
     vel = rng.normal(0, 1.5, size=(n, 2))
