@@ -340,6 +340,9 @@ int lbx_sim_particles(lbx_sim* sim, int64_t* n, void* stream);
  * ---------------------------------------------------------------------- */
 #define LBX_PIC_NO_FIELD_SOLVE 2u  /* skip the Yee update (tests)         */
 #define LBX_PIC_RESYNC 4u          /* sorted mode: recount the input cells   */
+#define LBX_PIC_DEFER_CURRENT 8u   /* stop after push + compaction: the      */
+                                   /* cell accumulator stays for a cross-GPU */
+                                   /* reduction, then lbx_pic_finish         */
 
 typedef struct lbx_pic_args {
   double* z;
@@ -372,6 +375,17 @@ typedef struct lbx_pic_args {
 } lbx_pic_args;
 
 int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* args, void* stream);
+
+/* Multi-GPU PIC (guard-cell current sum): after a LBX_PIC_DEFER_CURRENT step
+ * the context holds the step's current as exact integers, cell-centric
+ * jc[cells][16] (16 cell-relative nodes, int64 two's complement) over the
+ * deposit box box[4] = {row_min, row_max, col_min, col_max} (device).  Ranks
+ * all-reduce(sum) jc over the union of their boxes (write the union into
+ * box) -- integer sums, so the result is bit-identical to one GPU -- and
+ * call lbx_pic_finish (node gather into current[], clear, Yee update with
+ * the same args; every rank keeps the full replicated field grid). */
+int lbx_pic_current_view(lbx_ctx* ctx, uint64_t** jc, int64_t* cells, int32_t** box);
+int lbx_pic_finish(lbx_ctx* ctx, const lbx_pic_args* args, void* stream);
 
 /* ------------------------------------------------------------------------
  * Multi-GPU: box ownership -> GPU.  Each rank holds the particles

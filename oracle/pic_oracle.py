@@ -97,10 +97,12 @@ def boris(uz, ux, uy, E, B, qm, dt):
     return qz + h * E["Ez"], qx + h * E["Ex"], qy + h * E["Ey"]
 
 
-def deposit(f, comp, z, x, val, scale):
+def deposit_acc(comp, z, x, val, scale, shape):
+    """Integer fixed-point node sums of one current component (the exact
+    quantity the GPU accumulates; summing these over ranks is exact)."""
     oz, ox = {"Jx": OFFSETS["Ex"], "Jy": OFFSETS["Ey"], "Jz": OFFSETS["Ez"]}[comp]
     i0, j0, fz, fx = _stencil(z, x, oz, ox)
-    acc = np.zeros(f[comp].shape, dtype=np.int64)
+    acc = np.zeros(shape, dtype=np.int64)
     one = np.float32(1.0)
     v32 = val.astype(np.float32)
     s32 = np.float32(scale)
@@ -108,12 +110,22 @@ def deposit(f, comp, z, x, val, scale):
         for dj, wx in ((0, one - fx), (1, fx)):
             q = np.rint(((v32 * s32) * wz) * wx).astype(np.int64)
             np.add.at(acc, (i0 + 1 + di, j0 + 1 + dj), q)
+    return acc
+
+
+def apply_current(f, comp, acc, scale):
+    """J += float32(acc / scale) (lbx_pic.cu pic_current_kernel)."""
     f[comp] += (acc.astype(np.float64) / scale).astype(np.float32)
 
 
-def particle_step(f, p, nz, nx, qm, qw, dt):
-    """Gather, Boris push, move, absorb, deposit.  p: dict of float64 arrays
-    z, x, uz, ux, uy (modified: survivors only, order kept)."""
+def deposit(f, comp, z, x, val, scale):
+    apply_current(f, comp, deposit_acc(comp, z, x, val, scale, f[comp].shape), scale)
+
+
+def push_particles(f, p, nz, nx, qm, dt):
+    """Gather, Boris push, move, absorb: p (dict of float64 arrays z, x, uz,
+    ux, uy) keeps the survivors in order; returns (keep mask, 1/gamma of the
+    survivors)."""
     z, x = p["z"], p["x"]
     E = {k: gather(f, k, z, x) for k in E_COMPS}
     B = {k: gather(f, k, z, x) for k in B_COMPS}
@@ -124,10 +136,23 @@ def particle_step(f, p, nz, nx, qm, qw, dt):
     keep = (zn >= 0) & (zn < nz) & (xn >= 0) & (xn < nx)
     for k, v in (("z", zn), ("x", xn), ("uz", uz), ("ux", ux), ("uy", uy)):
         p[k] = v[keep]
-    g = ig[keep]
+    return keep, ig[keep]
+
+
+def current_accs(p, ig, qw, shape):
+    """The three components' integer node sums of the particles p."""
     sc = current_scale(qw)
-    for comp, u in (("Jx", p["ux"]), ("Jy", p["uy"]), ("Jz", p["uz"])):
-        deposit(f, comp, p["z"], p["x"], qw * u * g, sc)
+    return {comp: deposit_acc(comp, p["z"], p["x"], qw * u * ig, sc, shape)
+            for comp, u in (("Jx", p["ux"]), ("Jy", p["uy"]), ("Jz", p["uz"]))}
+
+
+def particle_step(f, p, nz, nx, qm, qw, dt):
+    """Gather, Boris push, move, absorb, deposit.  p: dict of float64 arrays
+    z, x, uz, ux, uy (modified: survivors only, order kept)."""
+    keep, g = push_particles(f, p, nz, nx, qm, dt)
+    sc = current_scale(qw)
+    for comp, acc in current_accs(p, g, qw, f["Jx"].shape).items():
+        apply_current(f, comp, acc, sc)
     return keep
 
 

@@ -121,6 +121,7 @@ SIGNATURES.update({
 RECORD_DOUBLES = 6
 LBX_PIC_NO_FIELD_SOLVE = 2
 LBX_PIC_RESYNC = 4
+LBX_PIC_DEFER_CURRENT = 8
 
 
 class PicArgs(C.Structure):
@@ -134,6 +135,8 @@ class PicArgs(C.Structure):
 
 
 SIGNATURES["lbx_pic_step"] = (i32, [vp, P(PicArgs), vp])
+SIGNATURES["lbx_pic_finish"] = (i32, [vp, P(PicArgs), vp])
+SIGNATURES["lbx_pic_current_view"] = (i32, [vp, P(vp), P(i64), P(vp)])
 SIGNATURES["lbx_sim_set_fields"] = (i32, [vp, vp, vp, vp])
 
 

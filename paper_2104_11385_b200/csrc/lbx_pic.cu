@@ -785,6 +785,30 @@ int cuda_fail(cudaError_t e, const char* what) {
   return set_error(LBX_ECUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+// Jc -> J over the deposit box, clear Jc, Yee update (unless disabled).
+int pic_finish(lbx_ctx* ctx, const lbx_pic_args* a, cudaStream_t s, double jscale) {
+  const long long cells = (long long)a->nz * a->nx;
+  const int pitch = a->nx + 2;
+  int* dep_box = reinterpret_cast<int*>(ctx->pic_acc + ctx->pic_cells * kNodes);
+  const unsigned cg = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 8, (cells + 255) / 256));
+  pic_current_kernel<<<cg, 256, 0, s>>>(ctx->pic_acc, dep_box, a->current[0], a->current[1],
+                                        a->current[2], a->nz, a->nx, 1.0 / jscale);
+  pic_zero_kernel<<<cg, 256, 0, s>>>(ctx->pic_acc, dep_box, a->nx);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "current launch");
+  if (a->flags & LBX_PIC_NO_FIELD_SOLVE) return LBX_OK;
+  const unsigned fg = cg;
+  pic_b_kernel<<<fg, 256, 0, s>>>(a->fields[0], a->fields[1], a->fields[2], a->fields[3],
+                                  a->fields[4], a->fields[5], a->nz, a->nx, pitch, a->dt);
+  pic_e_kernel<<<fg, 256, 0, s>>>(a->fields[0], a->fields[1], a->fields[2], a->fields[3],
+                                  a->fields[4], a->fields[5], a->current[0], a->current[1],
+                                  a->current[2], a->nz, a->nx, pitch, a->dt);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "field solve launch");
+  return LBX_OK;
+}
+
+
 }  // namespace
 }  // namespace lbx
 
@@ -937,10 +961,6 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   kern<<<(unsigned)grid, kPB, smem, s>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "pic_push_kernel launch");
-  const unsigned cg = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 8, (cells + 255) / 256));
-  pic_current_kernel<<<cg, 256, 0, s>>>(ctx->pic_acc, dep_box, a->current[0], a->current[1],
-                                        a->current[2], a->nz, a->nx, 1.0 / jscale);
-  pic_zero_kernel<<<cg, 256, 0, s>>>(ctx->pic_acc, dep_box, a->nx);
   rc = launch_compact(ctx, out[0], out[1], out[2], out[3], out[4], nullptr, (double)a->nz,
                       (double)a->nx, stream);
   if (rc) return rc;
@@ -949,14 +969,28 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
     pic_scan_apply_kernel<<<kScanBlocks, kScanThreads, 0, s>>>(cell_cnt, cells, block_sum, cursor);
     ctx->pic_sort_next = out[0];
   }
-  if (a->flags & LBX_PIC_NO_FIELD_SOLVE) return LBX_OK;
-  const unsigned fg = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 8, (cells + 255) / 256));
-  pic_b_kernel<<<fg, 256, 0, s>>>(a->fields[0], a->fields[1], a->fields[2], a->fields[3],
-                                  a->fields[4], a->fields[5], a->nz, a->nx, pitch, a->dt);
-  pic_e_kernel<<<fg, 256, 0, s>>>(a->fields[0], a->fields[1], a->fields[2], a->fields[3],
-                                  a->fields[4], a->fields[5], a->current[0], a->current[1],
-                                  a->current[2], a->nz, a->nx, pitch, a->dt);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "field solve launch");
+  if (a->flags & LBX_PIC_DEFER_CURRENT) return LBX_OK;
+  return pic_finish(ctx, a, s, jscale);
+}
+
+
+extern "C" int lbx_pic_finish(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
+  clear_error();
+  if (!ctx || !a) return set_error(LBX_EINVAL, "NULL argument");
+  if (!ctx->pic_acc || ctx->pic_cells != (long long)a->nz * a->nx)
+    return set_error(LBX_EINVAL, "lbx_pic_finish without a deferred lbx_pic_step on this grid");
+  if (!(a->q_times_w != 0.0)) return set_error(LBX_EINVAL, "q_times_w must be nonzero");
+  int e2 = 0;
+  std::frexp(1048576.0 / std::fabs(a->q_times_w), &e2);
+  return pic_finish(ctx, a, (cudaStream_t)stream, std::ldexp(1.0, e2 - 1));
+}
+
+extern "C" int lbx_pic_current_view(lbx_ctx* ctx, uint64_t** jc, int64_t* cells, int32_t** box) {
+  clear_error();
+  if (!ctx || !jc || !cells || !box) return set_error(LBX_EINVAL, "NULL argument");
+  if (!ctx->pic_acc) return set_error(LBX_EINVAL, "no PIC step has run on this context");
+  *jc = reinterpret_cast<uint64_t*>(ctx->pic_acc);
+  *cells = ctx->pic_cells;
+  *box = reinterpret_cast<int32_t*>(ctx->pic_acc + ctx->pic_cells * kNodes);
   return LBX_OK;
 }

@@ -57,6 +57,9 @@ class TorchComm:
     def all_reduce_sum(self, t: torch.Tensor):
         self.dist.all_reduce(t, group=self.group)
 
+    def all_reduce_max(self, t: torch.Tensor):
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+
     def exchange_counts(self, send_counts: torch.Tensor) -> torch.Tensor:
         recv = torch.empty_like(send_counts)
         self.dist.all_to_all_single(recv, send_counts, group=self.group)
@@ -96,6 +99,13 @@ class ThreadComm:
         total = vals[0].clone()
         for v in vals[1:]:
             total += v
+        t.copy_(total.to(t.device))
+
+    def all_reduce_max(self, t: torch.Tensor):
+        vals = self._swap(t.detach().cpu().clone())
+        total = vals[0].clone()
+        for v in vals[1:]:
+            total = torch.maximum(total, v)
         t.copy_(total.to(t.device))
 
     def exchange_counts(self, send_counts: torch.Tensor) -> torch.Tensor:
@@ -244,6 +254,123 @@ class DeviceEngine:
         return pos, vel
 
 
+class _DevArray:
+    """A device pointer owned by libLBX, viewed as a torch tensor
+    (__cuda_array_interface__, no copy)."""
+
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3}
+
+
+class PicEngine(DeviceEngine):
+    """This rank's share of a box-decomposed PIC run (pic.py physics).
+
+    Particles: the rank's boxes (z, x, uz, ux, uy in HBM).  Fields: every rank
+    keeps the full Yee grid and runs the same field solve, so only the
+    current needs a cross-GPU sum -- the guard-cell exchange of a
+    box-decomposed PIC code.  The step's current stays on the device as
+    exact integers (LBX_PIC_DEFER_CURRENT); ranks all-reduce the rows of the
+    union of their deposit boxes and finish (node gather, Yee update): bit-
+    identical to one GPU, the order of the sums does not matter.  Emigrants
+    and adoption-time migration reuse the 6-double records: (z, x, uz, ux,
+    kick_z, kick_x) before the kick (uy is 0 then), (z, x, uz, ux, uy, 0)
+    after it."""
+
+    def __init__(self, cfg, rank, world, device, pos, kick, capacity, clock, pic=None):
+        from .pic import CURRENT_NAMES, FIELD_NAMES
+        from .workload import PIC_DEFAULTS
+        super().__init__(cfg, rank, world, device, pos, kick, capacity, clock)
+        self.pic = dict(PIC_DEFAULTS, **(pic or {}))
+        nz, nx = cfg.domain_extent
+        self.nz, self.nx = int(nz), int(nx)
+        cap = self.capacity + 2
+        f64 = dict(dtype=torch.float64, device=self.dev)
+        self.uy = torch.zeros(cap, **f64)
+        self.spare = torch.zeros(cap, **f64)
+        self.kicked = self.kvz is None
+        if self.kicked:
+            self.kvz, self.kvx = self.uy, self.spare
+        self.fields = {k: torch.zeros((nz + 2, nx + 2), dtype=torch.float32, device=self.dev)
+                       for k in FIELD_NAMES + CURRENT_NAMES}
+        self.field_names, self.current_names = FIELD_NAMES, CURRENT_NAMES
+        self.comm = None
+        self.nout2 = torch.zeros(2, dtype=torch.int64, device=self.dev)
+        self.ubox = torch.zeros(4, dtype=torch.int64, device=self.dev)
+
+    def attach_comm(self, comm):
+        self.comm = comm
+
+    def kick(self):
+        if not self.kicked:     # momenta u = v_kick / dt, as Simulation(physics="pic")
+            dt = self.pic["dt"]
+            self.vz, self.vx = self.kvz.div_(dt), self.kvx.div_(dt)
+            self.kvz, self.kvx = self.uy, self.spare
+            self.kicked = True
+
+    def _args(self, flags):
+        a = _lib.PicArgs()
+        a.z, a.x, a.uz, a.ux, a.uy = (_lib.ptr(t) for t in (self.z, self.x, self.vz, self.vx,
+                                                             self.uy))
+        for i, k in enumerate(self.field_names):
+            a.fields[i] = _lib.ptr(self.fields[k])
+        for i, k in enumerate(self.current_names):
+            a.current[i] = _lib.ptr(self.fields[k])
+        a.nz, a.nx, a.box_size = self.nz, self.nx, int(self.m)
+        a.q_over_m, a.q_times_w = float(self.pic["q_over_m"]), float(self.pic["q_times_w"])
+        a.dt = float(self.pic["dt"])
+        a.flags = flags
+        return a
+
+    def push(self, wp, wc):
+        stream = self.D._stream(self.dev)
+        self.ctx.set_count(self.n)
+        a = self._args((_lib.LBX_STEP_CLOCK if self.clock else 0) | _lib.LBX_PIC_DEFER_CURRENT)
+        a.w_particle, a.w_cell = float(wp), float(wc)
+        a.counts_out, a.cost_out, a.clk_out = (_lib.ptr(self.counts), _lib.ptr(self.cost),
+                                               _lib.ptr(self.clk))
+        a.n_out, a.err_out = _lib.ptr(self.nout2), _lib.ptr(self.nout2[1:])
+        _lib.check(_lib.lib.lbx_pic_step(self.ctx.handle, C.byref(a), stream))
+        self.launches += 6   # set_count, quad, push, compaction, (scan), current view
+        h = self.nout2.cpu().numpy()
+        if h[1]:
+            raise ValueError(f"{int(h[1])} particles fell outside the box grid")
+        self.n = int(h[0])
+        # guard-cell current: exact integer sum over the union of deposit boxes
+        jc_p, cells, box_p = C.c_void_p(), C.c_int64(), C.c_void_p()
+        _lib.check(_lib.lib.lbx_pic_current_view(self.ctx.handle, C.byref(jc_p), C.byref(cells),
+                                                 C.byref(box_p)))
+        box = torch.as_tensor(_DevArray(box_p.value, 4, "<i4"), device=self.dev)
+        b = box.to(torch.int64)
+        self.ubox.copy_(torch.stack([-b[0], b[1], -b[2], b[3]]))
+        self.comm.all_reduce_max(self.ubox)
+        u = self.ubox.cpu().numpy()
+        r0, r1, c0, c1 = -int(u[0]), int(u[1]), -int(u[2]), int(u[3])
+        if r0 <= r1:
+            box.copy_(torch.tensor([r0, r1, c0, c1], dtype=torch.int32, device=self.dev))
+            jc = torch.as_tensor(_DevArray(jc_p.value, cells.value * 16, "<i8"), device=self.dev)
+            band = jc[r0 * self.nx * 16:(r1 + 1) * self.nx * 16]
+            self.comm.all_reduce_sum(band)
+        _lib.check(_lib.lib.lbx_pic_finish(self.ctx.handle, C.byref(self._args(0)), stream))
+        self.launches += 4   # current, zero, B, E
+        send_counts, nout = self.partition()
+        return self.counts, self.clk, send_counts, nout
+
+    def unpack(self, recv: torch.Tensor):
+        n0 = self.n
+        super().unpack(recv)
+        if not self.kicked:     # uy is not carried before the kick: it is 0
+            self.uy[n0:self.n].zero_()
+
+    def state(self):
+        n = self.n
+        return {k: t[:n].cpu().numpy() for k, t in (("z", self.z), ("x", self.x), ("uz", self.vz),
+                                                    ("ux", self.vx), ("uy", self.uy))}
+
+    def field_arrays(self):
+        return {k: v.cpu().numpy() for k, v in self.fields.items()}
+
+
 # ---------------------------------------------------------------------------
 # driver
 # ---------------------------------------------------------------------------
@@ -260,7 +387,7 @@ class DistributedSimulation:
 
     def __init__(self, cfg, policy, provider, *, comm=None, engine_factory=None,
                  positions=None, kick=None, device=None, capacity=None,
-                 record_counts=False, replicas=1):
+                 record_counts=False, replicas=1, physics="surrogate", pic=None):
         self.comm = comm or TorchComm()
         self.rank, self.world = self.comm.rank, self.comm.world
         if cfg.n_ranks != self.world:
@@ -286,9 +413,16 @@ class DistributedSimulation:
             local = np.tile(local, (replicas, 1))
             kick_local = None if kick_local is None else np.tile(kick_local, (replicas, 1))
         cap = capacity if capacity is not None else self.n_init
-        factory = engine_factory or DeviceEngine
-        self.engine = factory(cfg, self.rank, self.world, device, local, kick_local, cap,
-                              provider.device_kind == 3)
+        if physics not in ("surrogate", "pic"):
+            raise ConfigError(f"unknown physics {physics!r}")
+        factory = engine_factory or (PicEngine if physics == "pic" else DeviceEngine)
+        if physics == "pic":
+            self.engine = factory(cfg, self.rank, self.world, device, local, kick_local, cap,
+                                  provider.device_kind == 3, pic=pic)
+            self.engine.attach_comm(self.comm)
+        else:
+            self.engine = factory(cfg, self.rank, self.world, device, local, kick_local, cap,
+                                  provider.device_kind == 3)
         self.engine.set_owner(self.initial_owner)
         self.conf = sim_config(cfg, policy, provider)
         h = C.c_void_p()

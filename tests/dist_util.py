@@ -132,3 +132,167 @@ def run_rank(rank, world, port, spec_kw, outdir, engine="numpy"):
         sim.close()
     finally:
         dist.destroy_process_group()
+
+
+class NumpyPicEngine:
+    """Test double for parallel.PicEngine: the same per-rank PIC protocol in
+    numpy (oracle/pic_oracle.py) -- push the local particles, all-reduce the
+    integer current of every rank, apply it and run the replicated field
+    solve, then stage emigrants as 6-double records."""
+
+    def __init__(self, cfg, rank, world, device, pos, kick, capacity, clock, pic=None):
+        from oracle import pic_oracle as PO
+        from paper_2104_11385_b200.workload import PIC_DEFAULTS
+        self.PO = PO
+        self.pic = dict(PIC_DEFAULTS, **(pic or {}))
+        self.rank, self.world = rank, world
+        self.nz, self.nx = cfg.domain_extent
+        self.m = float(cfg.box_size)
+        self.nbz, self.nbx = self.nz // cfg.box_size, self.nx // cfg.box_size
+        pos = np.array(pos, dtype=np.float64).reshape(-1, 2)
+        z0 = np.zeros(pos.shape[0])
+        self.p = {"z": pos[:, 0].copy(), "x": pos[:, 1].copy(), "uz": z0.copy(),
+                  "ux": z0.copy(), "uy": z0.copy()}
+        self.kick_v = None if kick is None else np.array(kick, dtype=np.float64).reshape(-1, 2)
+        self.f = PO.new_fields(self.nz, self.nx)
+        self.owner = None
+        self.staged = np.zeros((0, REC))
+        self.dest = np.zeros(0, dtype=np.int64)
+        self.comm = None
+
+    @property
+    def n(self):
+        return self.p["z"].size
+
+    def attach_comm(self, comm):
+        self.comm = comm
+
+    def set_owner(self, owner):
+        self.owner = np.asarray(owner, dtype=np.int64)
+
+    def kick(self):
+        if self.kick_v is not None:
+            self.p["uz"] = self.kick_v[:, 0] / self.pic["dt"]
+            self.p["ux"] = self.kick_v[:, 1] / self.pic["dt"]
+            self.kick_v = None
+
+    def _records(self, idx):
+        p = self.p
+        tail = (self.kick_v[idx] if self.kick_v is not None
+                else np.column_stack([p["uy"][idx], np.zeros(idx.size)]))
+        return np.column_stack([p["z"][idx], p["x"][idx], p["uz"][idx], p["ux"][idx], tail])
+
+    def _split(self):
+        p = self.p
+        box = (np.trunc(p["z"] / self.m).astype(np.int64) * self.nbx
+               + np.trunc(p["x"] / self.m).astype(np.int64))
+        emig = self.owner[box] != self.rank
+        idx = np.flatnonzero(emig)
+        self.staged = self._records(idx)
+        self.dest = self.owner[box[idx]]
+        stay = ~emig
+        self.p = {k: v[stay] for k, v in p.items()}
+        if self.kick_v is not None:
+            self.kick_v = self.kick_v[stay]
+        return box[stay]
+
+    def push(self, wp, wc):
+        PO, c = self.PO, self.pic
+        keep, ig = PO.push_particles(self.f, self.p, self.nz, self.nx, c["q_over_m"], c["dt"])
+        if self.kick_v is not None:
+            self.kick_v = self.kick_v[keep]
+        box = (np.trunc(self.p["z"] / self.m).astype(np.int64) * self.nbx
+               + np.trunc(self.p["x"] / self.m).astype(np.int64))
+        counts = np.bincount(box, minlength=self.nbz * self.nbx).astype(np.int64)
+        shape = self.f["Jx"].shape
+        sc = PO.current_scale(c["q_times_w"])
+        for comp, acc in PO.current_accs(self.p, ig, c["q_times_w"], shape).items():
+            t = torch.from_numpy(np.ascontiguousarray(acc).reshape(-1))
+            self.comm.all_reduce_sum(t)
+            PO.apply_current(self.f, comp, t.numpy().reshape(shape), sc)
+        PO.field_step(self.f, self.nz, self.nx, c["dt"])
+        self._split()
+        send = np.bincount(self.dest, minlength=self.world).astype(np.int64)
+        return (torch.from_numpy(counts), torch.zeros(counts.size, dtype=torch.int64),
+                torch.from_numpy(send), torch.tensor([self.n, 0], dtype=torch.int64))
+
+    def partition(self):
+        self._split()
+        return (torch.from_numpy(np.bincount(self.dest, minlength=self.world).astype(np.int64)),
+                torch.tensor([self.n, 0], dtype=torch.int64))
+
+    def commit(self, nout_host):
+        assert int(nout_host[0]) == self.n
+
+    def pack(self, sc):
+        order = np.argsort(self.dest, kind="stable")
+        return torch.from_numpy(np.ascontiguousarray(self.staged[order]).reshape(-1, REC))
+
+    def unpack(self, recv):
+        r = recv.numpy().reshape(-1, REC)
+        add = {"z": r[:, 0], "x": r[:, 1], "uz": r[:, 2], "ux": r[:, 3],
+               "uy": r[:, 4] if self.kick_v is None else np.zeros(r.shape[0])}
+        self.p = {k: np.concatenate([self.p[k], add[k]]) for k in self.p}
+        if self.kick_v is not None:
+            self.kick_v = np.concatenate([self.kick_v, r[:, 4:6]])
+
+    def state(self):
+        return {k: v.copy() for k, v in self.p.items()}
+
+    def field_arrays(self):
+        return {k: v.copy() for k, v in self.f.items()}
+
+
+def pic_reference(doc, steps):
+    """Single-process oracle PIC run of a scenario doc (kick -> u = v/dt):
+    per-step per-box counts, final particles and fields."""
+    from oracle import lbsim_oracle as LO
+    from oracle import pic_oracle as PO
+    from paper_2104_11385_b200 import scenarios as S
+    from paper_2104_11385_b200.workload import PIC_DEFAULTS, kick_velocities, sample_blob
+    spec = S.apply_overrides(S.spec_from_dict(doc), steps=steps)
+    cfg = spec.scenario
+    c = PIC_DEFAULTS
+    pos = sample_blob(cfg)
+    kick = kick_velocities(pos, cfg)
+    nz, nx = cfg.domain_extent
+    f = PO.new_fields(nz, nx)
+    z0 = np.zeros(len(pos))
+    p = {"z": pos[:, 0].copy(), "x": pos[:, 1].copy(), "uz": z0.copy(), "ux": z0.copy(),
+         "uy": z0.copy()}
+    counts = []
+    for step in range(cfg.total_steps):
+        if step == cfg.kick.step:
+            p["uz"], p["ux"] = kick[:, 0] / c["dt"], kick[:, 1] / c["dt"]
+        PO.particle_step(f, p, nz, nx, c["q_over_m"], c["q_times_w"], c["dt"])
+        PO.field_step(f, nz, nx, c["dt"])
+        counts.append(LO.bin_particles(np.column_stack([p["z"], p["x"]]), float(cfg.box_size),
+                                       nz // cfg.box_size, nx // cfg.box_size))
+    return np.array(counts), p, f
+
+
+def run_rank_pic(rank, world, port, doc, steps, outdir, overrides=None):
+    """mp.spawn target: one gloo rank of a distributed PIC run."""
+    import torch.distributed as dist
+
+    from paper_2104_11385_b200 import scenarios as S
+    from paper_2104_11385_b200.parallel import DistributedSimulation, TorchComm
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        spec = S.apply_overrides(S.spec_from_dict(doc), ranks=world, steps=steps,
+                                 **(overrides or {}))
+        sim = DistributedSimulation(spec.scenario, spec.policy, spec.build_provider(),
+                                    comm=TorchComm(), engine_factory=NumpyPicEngine,
+                                    record_counts=True, physics="pic")
+        sim.run()
+        res = sim.result()
+        st = sim.engine.state()
+        f = sim.engine.field_arrays()
+        np.savez(os.path.join(outdir, f"rank{rank}.npz"), count_trace=res.count_trace,
+                 adoptions=res.summary["adoption_count"], moved=sim.moved,
+                 **{f"p_{k}": v for k, v in st.items()}, **{f"f_{k}": v for k, v in f.items()})
+        sim.close()
+    finally:
+        dist.destroy_process_group()

@@ -83,3 +83,52 @@ def test_gpu_distributed_gpuclock_runs():
     ref = O.run_simulation(cfg, record_counts=True)
     assert np.array_equal(a.count_trace, ref["count_trace"])
     assert ((a.cost_trace > 0) == (ref["count_trace"] > 0)).all()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gpu_distributed_pic_matches_oracle(world):
+    """parallel.PicEngine on the GPU, ranks as threads: libLBX PIC step with
+    the current deferred, integer current all-reduce over the union of the
+    deposit boxes, lbx_pic_finish, emigrant exchange and adoption-time
+    migration -- bit-identical to the single-process oracle PIC run."""
+    from paper_2104_11385_b200 import scenarios as S
+    from paper_2104_11385_b200.parallel import DistributedSimulation, ThreadComm
+    from tests.dist_util import pic_reference
+    doc = json.loads((Path(__file__).parent / "golden" / "runs.json").read_text())["_docs"]["small"]
+    steps = 16
+    spec = S.apply_overrides(S.spec_from_dict(doc), ranks=world, steps=steps, interval=3,
+                             threshold=0.0)
+    shared = ThreadComm.shared(world)
+    outs, errs = [None] * world, []
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            sim = DistributedSimulation(spec.scenario, spec.policy, spec.build_provider(),
+                                        comm=ThreadComm(shared, r), device="cuda:0",
+                                        record_counts=True, physics="pic")
+            sim.run()
+            outs[r] = (sim.result(), sim.engine.state(), sim.engine.field_arrays(),
+                       sim.moved.copy())
+            sim.close()
+        except Exception as e:
+            errs.append(e)
+            shared["bar"].abort()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    counts, p, f = pic_reference(doc, steps)
+    keys = ("z", "x", "uz", "ux", "uy")
+    for res, _, fa, _ in outs:
+        assert np.array_equal(res.count_trace, counts)
+        for k in f:
+            assert np.array_equal(fa[k], f[k]), k
+    got = sorted_rows(np.column_stack([np.concatenate([o[1][k] for o in outs]) for k in keys]))
+    want = sorted_rows(np.column_stack([p[k] for k in keys]))
+    assert np.array_equal(got, want)
+    assert outs[0][0].summary["adoption_count"] > 0 and sum(o[3].sum() for o in outs) > 0
