@@ -516,7 +516,9 @@ def run_lbx_dist(args, rank, world, dev):
                                     f"{R} replicas = {n_total} particles, boxes owned by GPUs"),
                        "cost": spec.build_provider().kind,
                        "lb": "knapsack every 10, 10% rel, initial knapsack",
-                       "ranks": world, "parallelism": f"box ownership over {world} GPUs (NCCL)",
+                       "ranks": world, "parallelism": f"box ownership over {world} GPUs "
+                       f"(exchange: {sim.exchange}; p2p = emigrants written into the owner's "
+                       f"buffer by the push kernel over NVLink peer memory, NCCL all-reduce)",
                        "l2": "inputs larger than L2"},
             "gpu_launches": int(launches),
             "lb": {"ranks": world, "e_first": effs[0] if effs else None,

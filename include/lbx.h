@@ -417,6 +417,17 @@ typedef struct lbx_exchange_args {
    * not preserved (the multi-GPU path does not need it). */
   int64_t* removed_list;
   int64_t removed_cap;
+  /* Peer-memory exchange (fused push + exchange over NVLink / NVSwitch):
+   * when peer_recv != NULL the kernel writes each emigrant record straight
+   * into its destination's receive buffer, peer_recv[dest] (device array of
+   * `world` pointers to peer memory, lbx_peer_alloc / lbx_peer_open), at a
+   * slot reserved with one remote atomic per (warp, destination) on
+   * peer_cursor[dest] (u64 in the destination's memory); stage / stage_dest
+   * are not used.  The destination learns its count from its own cursor
+   * after any collective that orders it after the senders' kernels. */
+  double* const* peer_recv;
+  unsigned long long* const* peer_cursor;
+  int64_t peer_recv_cap;
 } lbx_exchange_args;
 
 /* lbx_push_step + emigrant staging (per-step box-crossing exchange). */
@@ -444,6 +455,17 @@ int lbx_group_by_dest(const double* stage, const int32_t* stage_dest, int64_t co
  * (kick_vz/kick_vx may be NULL). */
 int lbx_unpack(const double* recv, int64_t n_recv, int64_t offset, double* z, double* x,
                double* vz, double* vx, double* kick_vz, double* kick_vx, void* stream);
+
+/* Peer memory for the fused exchange.  lbx_peer_alloc: cudaMalloc'd device
+ * buffer (zeroed) and its 64-byte IPC handle; lbx_peer_open maps another
+ * process's buffer (NVLink / NVSwitch peer access enabled lazily; same-GPU
+ * processes also work); lbx_peer_close / lbx_peer_free release them.
+ * lbx_peer_can_access: 1 if device `dev` can access device `peer`. */
+int lbx_peer_alloc(int64_t bytes, void** ptr, unsigned char handle[64]);
+int lbx_peer_open(const unsigned char handle[64], void** ptr);
+int lbx_peer_close(void* ptr);
+int lbx_peer_free(void* ptr);
+int lbx_peer_can_access(int32_t dev, int32_t peer, int32_t* yes);
 
 #ifdef __cplusplus
 }

@@ -101,7 +101,8 @@ class ExchangeArgs(C.Structure):
     _fields_ = [("owner", vp), ("rank", i32), ("world", i32), ("stage", vp),
                 ("stage_dest", vp), ("stage_cap", i64), ("send_counts", vp),
                 ("kick_vz", vp), ("kick_vx", vp), ("removed_list", vp),
-                ("removed_cap", i64)]
+                ("removed_cap", i64), ("peer_recv", vp), ("peer_cursor", vp),
+                ("peer_recv_cap", i64)]
 
 
 SIGNATURES.update({
@@ -135,6 +136,11 @@ class PicArgs(C.Structure):
 
 
 SIGNATURES["lbx_pic_step"] = (i32, [vp, P(PicArgs), vp])
+SIGNATURES["lbx_peer_alloc"] = (i32, [i64, P(vp), vp])
+SIGNATURES["lbx_peer_open"] = (i32, [vp, P(vp)])
+SIGNATURES["lbx_peer_close"] = (i32, [vp])
+SIGNATURES["lbx_peer_free"] = (i32, [vp])
+SIGNATURES["lbx_peer_can_access"] = (i32, [i32, i32, P(i32)])
 SIGNATURES["lbx_pic_finish"] = (i32, [vp, P(PicArgs), vp])
 SIGNATURES["lbx_pic_current_view"] = (i32, [vp, P(vp), P(i64), P(vp)])
 SIGNATURES["lbx_sim_set_fields"] = (i32, [vp, vp, vp, vp])

@@ -92,6 +92,9 @@ struct StepParams {
   const double* kvx;
   long long* removed_list;  // non-NULL: list removed indices, no stable compaction
   long long removed_cap;
+  double* const* peer_recv;             // non-NULL: write emigrants into peers' buffers
+  unsigned long long* const* peer_cursor;
+  long long peer_cap;
 };
 
 struct ScanParams {
@@ -193,6 +196,30 @@ __device__ __forceinline__ void stage_emigrant(const StepParams& p, bool em, lon
   const unsigned mask = __ballot_sync(kFull, em);
   if (!mask) return;
   const int lane = threadIdx.x & 31;
+  if (p.peer_recv) {
+    // Fused exchange over peer memory: lanes going to the same rank reserve
+    // their slots with ONE remote atomic on that rank's cursor and write the
+    // records straight into its receive buffer (NVLink / NVSwitch stores).
+    const unsigned grp = __match_any_sync(mask, em ? dest : -1);
+    if (!em) return;
+    const int leader = __ffs(grp) - 1;
+    unsigned long long base = 0;
+    if (lane == leader)
+      base = atomicAdd(p.peer_cursor[dest], (unsigned long long)__popc(grp));
+    base = __shfl_sync(grp, base, leader);
+    const long long slot = (long long)base + __popc(grp & lanemask_lt());
+    atomicAdd((unsigned long long*)(p.send_counts + dest), 1ull);
+    if (slot >= p.peer_cap) {
+      atomicOr((unsigned long long*)&p.st->err, 1ull << 62);  // receive buffer overflow
+      return;
+    }
+    double2* r = reinterpret_cast<double2*>(p.peer_recv[dest] + slot * 6);
+    r[0] = make_double2(z, x);
+    r[1] = make_double2(vz, vx);
+    r[2] = make_double2(p.kvz ? p.kvz[i] : 0.0, p.kvx ? p.kvx[i] : 0.0);
+    __threadfence_system();   // visible to the destination once our kernel has completed
+    return;
+  }
   unsigned long long base = 0;
   if (lane == __ffs(mask) - 1) base = atomicAdd(&p.st->staged, (unsigned long long)__popc(mask));
   base = __shfl_sync(kFull, base, __ffs(mask) - 1);
@@ -1473,6 +1500,9 @@ int launch_push_step(lbx_ctx* ctx, const StepLaunch& a, void* stream,
     p.kvx = ex->kick_vx;
     p.removed_list = reinterpret_cast<long long*>(ex->removed_list);
     p.removed_cap = ex->removed_cap;
+    p.peer_recv = ex->peer_recv;
+    p.peer_cursor = ex->peer_cursor;
+    p.peer_cap = ex->peer_recv_cap;
     rc = push ? launch_stream_any<true, true>(ctx, p, a.clock, pow2, s)
               : launch_stream_any<true, false>(ctx, p, false, pow2, s);
     if (rc) return rc;
@@ -1815,7 +1845,8 @@ int lbx_push_step_exchange(lbx_ctx* ctx, const lbx_step_args* a, const lbx_excha
   if (!ctx || !a || !ex) return set_error(LBX_EINVAL, "NULL argument");
   if (ex->world < 1 || ex->world > 64 || ex->rank < 0 || ex->rank >= ex->world)
     return set_error(LBX_EINVAL, "rank %d / world %d out of range", ex->rank, ex->world);
-  if (!ex->owner || !ex->stage || !ex->stage_dest || !ex->send_counts)
+  if (!ex->owner || !ex->send_counts ||
+      (!ex->peer_recv && (!ex->stage || !ex->stage_dest)) || (ex->peer_recv && !ex->peer_cursor))
     return set_error(LBX_EINVAL, "NULL exchange buffer");
   StepLaunch l{};
   l.z = a->z;
@@ -1987,6 +2018,61 @@ int lbx_unpack(const double* recv, int64_t n_recv, int64_t offset, double* z, do
                                                          kick_vz, kick_vx);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "unpack_kernel launch");
+  return LBX_OK;
+}
+
+int lbx_peer_alloc(int64_t bytes, void** ptr, unsigned char handle[64]) {
+  clear_error();
+  if (!ptr || !handle || bytes <= 0) return set_error(LBX_EINVAL, "bad peer allocation request");
+  *ptr = nullptr;
+  cudaError_t e = cudaMalloc(ptr, (size_t)bytes);
+  if (e != cudaSuccess) return set_error(LBX_EOOM, "peer buffer: %s", cudaGetErrorString(e));
+  cudaMemset(*ptr, 0, (size_t)bytes);
+  cudaIpcMemHandle_t h;
+  e = cudaIpcGetMemHandle(&h, *ptr);
+  if (e != cudaSuccess) {
+    cudaFree(*ptr);
+    *ptr = nullptr;
+    return cuda_fail(e, "cudaIpcGetMemHandle");
+  }
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  std::memcpy(handle, &h, 64);
+  return LBX_OK;
+}
+
+int lbx_peer_open(const unsigned char handle[64], void** ptr) {
+  clear_error();
+  if (!ptr || !handle) return set_error(LBX_EINVAL, "NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  const cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  return LBX_OK;
+}
+
+int lbx_peer_close(void* ptr) {
+  clear_error();
+  const cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  return e == cudaSuccess ? LBX_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
+}
+
+int lbx_peer_free(void* ptr) {
+  clear_error();
+  const cudaError_t e = cudaFree(ptr);
+  return e == cudaSuccess ? LBX_OK : cuda_fail(e, "cudaFree(peer)");
+}
+
+int lbx_peer_can_access(int32_t dev, int32_t peer, int32_t* yes) {
+  clear_error();
+  if (!yes) return set_error(LBX_EINVAL, "NULL argument");
+  int v = 0;
+  if (dev == peer) {
+    *yes = 1;
+    return LBX_OK;
+  }
+  const cudaError_t e = cudaDeviceCanAccessPeer(&v, dev, peer);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceCanAccessPeer");
+  *yes = v;
   return LBX_OK;
 }
 

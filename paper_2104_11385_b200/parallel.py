@@ -73,6 +73,28 @@ class TorchComm:
     def barrier(self):
         self.dist.barrier(group=self.group)
 
+    def device_ids(self, dev: int) -> list:
+        out = [None] * self.world
+        self.dist.all_gather_object(out, int(dev), group=self.group)
+        return out
+
+    def share_peer(self, ptr: int, handle: bytes) -> tuple:
+        """Every rank's peer buffer mapped into this process: (pointers,
+        pointers this process opened and must close)."""
+        hs = [None] * self.world
+        self.dist.all_gather_object(hs, bytes(handle), group=self.group)
+        ptrs, opened = [], []
+        for r, h in enumerate(hs):
+            if r == self.rank:
+                ptrs.append(int(ptr))
+                continue
+            q = C.c_void_p()
+            buf = (C.c_ubyte * 64).from_buffer_copy(h)
+            _lib.check(_lib.lib.lbx_peer_open(buf, C.byref(q)))
+            ptrs.append(int(q.value))
+            opened.append(int(q.value))
+        return ptrs, opened
+
 
 class ThreadComm:
     """In-process communicator for `world` ranks run as threads (tests on a
@@ -121,6 +143,12 @@ class ThreadComm:
     def barrier(self):
         self.s["bar"].wait()
 
+    def device_ids(self, dev: int) -> list:
+        return self._swap(int(dev))
+
+    def share_peer(self, ptr: int, handle: bytes) -> tuple:
+        return self._swap(int(ptr)), []     # one address space: raw pointers
+
 
 # ---------------------------------------------------------------------------
 # device engine (libLBX)
@@ -167,12 +195,71 @@ class DeviceEngine:
         self.nout = torch.zeros(2, dtype=torch.int64, device=self.dev)
         self.ctx = D.Context(self.dev, capacity=cap)
         self.launches = 0   # libLBX kernel launches issued (for gpu_launches)
+        self.p2p = False
+        self.parity = 0
+
+    # -- fused exchange over peer memory ---------------------------------
+    def enable_p2p(self, comm):
+        """Peer-memory exchange: every rank exposes two receive buffers
+        (step parity) + two cursors; the push / partition kernels write
+        emigrant records straight into the destination's buffer (remote
+        atomics + stores over NVLink / NVSwitch), replacing staging, the
+        counts all-to-all, the grouping kernel and the record all-to-all."""
+        nrec = self.capacity + 2
+        per = nrec * REC * 8
+        total = 2 * per + 64
+        ptr, handle = C.c_void_p(), (C.c_ubyte * 64)()
+        _lib.check(_lib.lib.lbx_peer_alloc(total, C.byref(ptr), handle))
+        self._peer_own = int(ptr.value)
+        ptrs, self._peer_opened = comm.share_peer(self._peer_own, bytes(handle))
+        i64 = dict(dtype=torch.int64, device=self.dev)
+        self.peer_recv = [torch.tensor([b + par * per for b in ptrs], **i64) for par in (0, 1)]
+        self.peer_cursor = [torch.tensor([b + 2 * per + 8 * par for b in ptrs], **i64)
+                            for par in (0, 1)]
+        self.peer_cap = nrec
+        self.recv_base = [self._peer_own + par * per for par in (0, 1)]
+        self.cursor = [torch.as_tensor(_DevArray(self._peer_own + 2 * per + 8 * par, 1, "<i8"),
+                                       device=self.dev) for par in (0, 1)]
+        self.stage = torch.empty((1, REC), dtype=torch.float64, device=self.dev)
+        self.stage_dest = torch.empty(1, dtype=torch.int32, device=self.dev)
+        self.p2p = True
+
+    def close_p2p(self):
+        if not self.p2p:
+            return
+        torch.cuda.synchronize(self.dev)
+        for q in self._peer_opened:
+            _lib.lib.lbx_peer_close(C.c_void_p(q))
+        self._peer_opened = []
+        self.cursor = None
+        _lib.lib.lbx_peer_free(C.c_void_p(self._peer_own))
+        self.p2p = False
+
+    def unpack_peer(self, parity: int, m: int):
+        """Append the m records other ranks wrote into this rank's receive
+        buffer `parity`, then reset its cursor (stream-ordered)."""
+        if self.n + m > self.capacity:
+            raise MemoryError(f"rank {self.rank}: {self.n + m} particles exceed capacity "
+                              f"{self.capacity}")
+        if m:
+            _lib.check(_lib.lib.lbx_unpack(C.c_void_p(self.recv_base[parity]), m, self.n,
+                                           _lib.ptr(self.z), _lib.ptr(self.x), _lib.ptr(self.vz),
+                                           _lib.ptr(self.vx), _lib.ptr(self.kvz),
+                                           _lib.ptr(self.kvx), self.D._stream(self.dev)))
+            self.launches += 1
+        self.cursor[parity].zero_()
+        self.n += m
 
     def _ex(self):
-        return _lib.ExchangeArgs(
+        a = _lib.ExchangeArgs(
             _lib.ptr(self.owner), self.rank, self.world, _lib.ptr(self.stage),
             _lib.ptr(self.stage_dest), self.capacity + 2, _lib.ptr(self.send_counts),
             _lib.ptr(self.kvz), _lib.ptr(self.kvx), _lib.ptr(self.removed), self.capacity + 2)
+        if self.p2p:
+            a.peer_recv = _lib.ptr(self.peer_recv[self.parity])
+            a.peer_cursor = _lib.ptr(self.peer_cursor[self.parity])
+            a.peer_recv_cap = self.peer_cap
+        return a
 
     def set_owner(self, owner: np.ndarray):
         self.owner.copy_(torch.from_numpy(np.asarray(owner, dtype=np.int32)))
@@ -362,6 +449,12 @@ class PicEngine(DeviceEngine):
         if not self.kicked:     # uy is not carried before the kick: it is 0
             self.uy[n0:self.n].zero_()
 
+    def unpack_peer(self, parity: int, m: int):
+        n0 = self.n
+        super().unpack_peer(parity, m)
+        if not self.kicked:
+            self.uy[n0:self.n].zero_()
+
     def state(self):
         n = self.n
         return {k: t[:n].cpu().numpy() for k, t in (("z", self.z), ("x", self.x), ("uz", self.vz),
@@ -387,7 +480,8 @@ class DistributedSimulation:
 
     def __init__(self, cfg, policy, provider, *, comm=None, engine_factory=None,
                  positions=None, kick=None, device=None, capacity=None,
-                 record_counts=False, replicas=1, physics="surrogate", pic=None):
+                 record_counts=False, replicas=1, physics="surrogate", pic=None,
+                 exchange="auto"):
         self.comm = comm or TorchComm()
         self.rank, self.world = self.comm.rank, self.comm.world
         if cfg.n_ranks != self.world:
@@ -424,6 +518,9 @@ class DistributedSimulation:
             self.engine = factory(cfg, self.rank, self.world, device, local, kick_local, cap,
                                   provider.device_kind == 3)
         self.engine.set_owner(self.initial_owner)
+        self.exchange = self._choose_exchange(exchange)
+        if self.exchange == "p2p":
+            self.engine.enable_p2p(self.comm)
         self.conf = sim_config(cfg, policy, provider)
         h = C.c_void_p()
         own = np.ascontiguousarray(self.initial_owner, dtype=np.int64)
@@ -453,7 +550,35 @@ class DistributedSimulation:
         self.halted = False
         self.moved = np.zeros(T, dtype=np.int64)   # particles migrated on adoption
 
+    def _choose_exchange(self, exchange):
+        """p2p (fused exchange over peer memory) when the engine supports it
+        and every rank's GPU can access every other's; else collectives."""
+        if exchange not in ("auto", "p2p", "nccl"):
+            raise ConfigError(f"exchange must be auto, p2p or nccl; got {exchange!r}")
+        capable = (hasattr(self.engine, "enable_p2p") and hasattr(self.comm, "share_peer")
+                   and getattr(self.engine, "dev", None) is not None
+                   and self.engine.dev.type == "cuda")
+        ok = False
+        if capable and exchange != "nccl":
+            devs = self.comm.device_ids(self.engine.dev.index)
+            yes = C.c_int32()
+            ok = True
+            for d in devs:
+                _lib.check(_lib.lib.lbx_peer_can_access(int(self.engine.dev.index), int(d),
+                                                        C.byref(yes)))
+                ok = ok and bool(yes.value)
+            flags = torch.tensor([1 if ok else 0], dtype=torch.int64, device=self.engine.dev)
+            self.comm.all_reduce_sum(flags)     # every rank must agree
+            ok = int(flags.item()) == self.world
+        if exchange == "p2p" and not ok:
+            raise ConfigError("exchange='p2p' needs CUDA engines with peer access between all ranks")
+        return "p2p" if ok else "nccl"
+
     def close(self):
+        if getattr(self, "engine", None) is not None and getattr(self.engine, "p2p", False):
+            self.comm.barrier()        # peers may still map this rank's buffers
+            self.engine.close_p2p()
+            self.comm.barrier()
         if getattr(self, "lb", None):
             _lib.lib.lbx_lb_destroy(self.lb)
             self.lb = None
@@ -469,6 +594,23 @@ class DistributedSimulation:
         send = self.engine.pack(sc)
         recv = self.comm.exchange_records(send, sc, rc)
         self.engine.unpack(recv)
+
+    def _migrate_p2p(self, step):
+        """Adoption-time migration over peer memory: the partition kernel
+        writes the lost boxes' particles into their new owners' buffers (the
+        parity the next step does not use yet); the all-reduce orders every
+        sender before the reads; a barrier keeps the buffer quiet until all
+        ranks drained it."""
+        par = (step + 1) & 1
+        self.engine.parity = par
+        send_counts, nout = self.engine.partition()
+        total = send_counts.sum().reshape(1)
+        self.comm.all_reduce_sum(total)
+        h = torch.cat([nout, total, self.engine.cursor[par]]).cpu().numpy()
+        self.engine.commit(h[:2])
+        self.engine.unpack_peer(par, int(h[3]))
+        self.comm.barrier()
+        return int(send_counts.sum().item())
 
     def _migrate(self):
         """Adoption-time redistribution: stage the particles of lost boxes,
@@ -503,21 +645,30 @@ class DistributedSimulation:
                 break
             if step == cfg.kick.step:
                 self.engine.kick()
+            p2p = self.exchange == "p2p"
+            if p2p:
+                self.engine.parity = step & 1
             counts, clk, send_counts, nout = self.engine.push(wp, wc)
             parts = [counts, clk] if clock else [counts]
             red = torch.cat(parts + [send_counts.sum().reshape(1)])
-            self.comm.all_reduce_sum(red)
-            recv_counts = self.comm.exchange_counts(send_counts)
-            h = torch.cat([red, nout, send_counts, recv_counts]).cpu().numpy()
+            self.comm.all_reduce_sum(red)   # p2p: also orders every sender's kernel first
             k = len(parts) * nb
+            if p2p:
+                h = torch.cat([red, nout, self.engine.cursor[step & 1]]).cpu().numpy()
+            else:
+                recv_counts = self.comm.exchange_counts(send_counts)
+                h = torch.cat([red, nout, send_counts, recv_counts]).cpu().numpy()
             ch = np.ascontiguousarray(h[:nb], dtype=np.int64)
             kh = np.ascontiguousarray(h[nb:2 * nb]).view(np.uint64) if clock else None
             emigrants = int(h[k])
             self.engine.commit(h[k + 1:k + 3])
-            sc = [int(v) for v in h[k + 3:k + 3 + W]]
-            rc = [int(v) for v in h[k + 3 + W:k + 3 + 2 * W]]
-            if emigrants:
-                self._records(sc, rc)
+            if p2p:
+                self.engine.unpack_peer(step & 1, int(h[k + 3]))
+            else:
+                sc = [int(v) for v in h[k + 3:k + 3 + W]]
+                rc = [int(v) for v in h[k + 3 + W:k + 3 + 2 * W]]
+                if emigrants:
+                    self._records(sc, rc)
             _lib.check(_lib.lib.lbx_lb_step(self.lb, step, _lib.ptr(ch), _lib.ptr(kh),
                                             int(ch.sum()), C.byref(self.souts),
                                             C.byref(adopted), C.byref(halt)))
@@ -525,7 +676,7 @@ class DistributedSimulation:
                 owner = np.empty(nb, dtype=np.int64)
                 _lib.check(_lib.lib.lbx_lb_owner(self.lb, _lib.ptr(owner)))
                 self.engine.set_owner(owner)
-                self.moved[step] = self._migrate()
+                self.moved[step] = self._migrate_p2p(step) if p2p else self._migrate()
             self.done = step + 1
             if halt.value:
                 self.halted = True

@@ -17,20 +17,22 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-def run_threads(base, world, kw, doc):
+def run_threads(base, world, kw, doc, exchange="auto"):
     from paper_2104_11385_b200 import scenarios as S
     from paper_2104_11385_b200.parallel import DeviceEngine, DistributedSimulation, ThreadComm
     shared = ThreadComm.shared(world)
     spec = S.spec_from_dict(doc) if base == "leaky" else S.load_spec(base)
     spec = S.apply_overrides(spec, ranks=world, **kw)
     outs, errs = [None] * world, []
+    outs_mode = [None] * world
 
     def body(r):
         try:
             torch.cuda.set_device(0)
             sim = DistributedSimulation(spec.scenario, spec.policy, spec.build_provider(),
                                         comm=ThreadComm(shared, r), engine_factory=DeviceEngine,
-                                        device="cuda:0", record_counts=True)
+                                        device="cuda:0", record_counts=True, exchange=exchange)
+            outs_mode[r] = sim.exchange
             sim.run()
             outs[r] = (sim.result(), sim.local_state(), sim.moved.copy())
             sim.close()
@@ -45,16 +47,21 @@ def run_threads(base, world, kw, doc):
         t.join()
     if errs:
         raise errs[0]
+    assert all(m == ("nccl" if exchange == "nccl" else "p2p") for m in outs_mode), outs_mode
     return outs
 
 
+@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
 @pytest.mark.parametrize("base,world,kw", [("mini", 2, {"steps": 40}),
                                            ("mini", 3, {"steps": 40, "policy": "sfc"}),
                                            ("leaky", 3, {}),
                                            ("tight-memory", 2, {"steps": 60, "cost": "measured"})])
-def test_gpu_distributed_matches_oracle(base, world, kw):
+def test_gpu_distributed_matches_oracle(base, world, kw, exchange):
+    """exchange='p2p': the fused push + exchange writes emigrants straight
+    into the destination rank's receive buffer (peer memory; here the ranks
+    share one GPU); 'nccl': staged records + all-to-all collectives."""
     cfg, doc = oracle_cfg(base, world, kw)
-    outs = run_threads(base, world, kw, doc)
+    outs = run_threads(base, world, kw, doc, exchange)
     ref = O.run_simulation(cfg, record_counts=True)
     for res, _, _ in outs:
         m = res.metrics
