@@ -38,6 +38,10 @@ def main():
     ap.add_argument("--replicas", type=int, default=128)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c2", choices=["c2", "uniform"],
+                    help="c2: the C2 blob tiled (dense, ~7,000 particles per occupied cell); "
+                         "uniform: SURVEY 8d's roofline plasma, 4096x4096 cells x 8 ppc "
+                         "(134 M particles), thermal momenta")
     args = ap.parse_args()
 
     import torch
@@ -46,13 +50,28 @@ def main():
     from paper_2104_11385_b200 import device, pic
 
     dev = torch.device("cuda:0")
-    spec, sc = bench.c2_spec(1, 10, "gpuclock")
-    pos0, kick0 = bench.base_particles(spec)
     dt = 0.5
-    u0 = np.column_stack([kick0[:, 0] / dt, kick0[:, 1] / dt, np.zeros(len(kick0))])
-    R = args.replicas
+    if args.workload == "c2":
+        spec, sc = bench.c2_spec(1, 10, "gpuclock")
+        pos0, kick0 = bench.base_particles(spec)
+        u0 = np.column_stack([kick0[:, 0] / dt, kick0[:, 1] / dt, np.zeros(len(kick0))])
+        R = args.replicas
+        nz, nx = sc.domain_extent
+        box = sc.box_size
+        label = (f"C2 blob x{R} replicas = {pos0.shape[0] * R} particles, 960x960 Yee grid, "
+                 f"box 32, dt {dt}, q/m -1, GpuClock on")
+    else:   # uniform plasma, cell-sorted, 8 per cell, thermal u ~ N(0, 0.05)
+        nz = nx = 4096
+        ppc, R, box = 8, 1, 128
+        rng = np.random.default_rng(42)
+        cell = np.repeat(np.arange(nz * nx, dtype=np.int64), ppc)
+        off = rng.random((cell.size, 2))
+        pos0 = np.column_stack([(cell // nx) + off[:, 0], (cell % nx) + off[:, 1]])
+        u0 = rng.normal(0.0, 0.05, size=(cell.size, 3))
+        del cell, off
+        label = (f"uniform plasma 4096x4096 cells x {ppc} ppc = {pos0.shape[0]} particles, "
+                 f"box {box}, thermal u ~ N(0, 0.05), dt {dt}, q/m -1, GpuClock on")
     n = pos0.shape[0] * R
-    nz, nx = sc.domain_extent
     cols = (("z", pos0[:, 0]), ("x", pos0[:, 1]), ("uz", u0[:, 0]), ("ux", u0[:, 1]),
             ("uy", u0[:, 2]))
     init = {}
@@ -62,8 +81,7 @@ def main():
         init[name] = t
     ctx = device.Context(dev, capacity=n)
     peak, peak_src = bench.peaks()
-    out = {"workload": f"C2 blob x{R} replicas = {n} particles, 960x960 Yee grid, "
-                       f"box 32, dt {dt}, q/m -1, GpuClock on", "particles": n}
+    out = {"workload": label, "particles": n}
     stream = torch.cuda.current_stream(dev)
     for mode, solve, sort in (("push_deposit", False, True), ("push_deposit_inplace", False, False),
                               ("full_step", True, True)):
@@ -72,14 +90,14 @@ def main():
             setattr(st, name, t.clone())
         st.n = n
         for _ in range(args.warmup):
-            pic.pic_step(ctx, st, sc.box_size, -1.0, -1e-4, dt, clock=True, field_solve=solve,
+            pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=True, field_solve=solve,
                          sort=sort)
         times = []
         for _ in range(args.steps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             n_before = st.n
             e0.record(stream)
-            pic.pic_step(ctx, st, sc.box_size, -1.0, -1e-4, dt, clock=True, field_solve=solve,
+            pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=True, field_solve=solve,
                          sort=sort)
             e1.record(stream)
             torch.cuda.synchronize(dev)
