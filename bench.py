@@ -537,6 +537,41 @@ def run_lbx_dist(args, rank, world, dev):
     dist.destroy_process_group()
 
 
+def pcie_ceiling(dev, nbytes=1 << 30, reps=3):
+    """Measured pinned-host <-> HBM copy rates (GB/s): each direction alone
+    and both at once on two streams -- the ceiling of the host-buffer path."""
+    import torch
+    h = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    d = [torch.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(2)]
+    s = [torch.cuda.Stream(dev) for _ in range(2)]
+
+    def timed(fn):
+        best = 1e9
+        for _ in range(reps):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize(dev)
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    def h2d():
+        with torch.cuda.stream(s[0]):
+            d[0].copy_(h[0], non_blocking=True)
+
+    def d2h():
+        with torch.cuda.stream(s[1]):
+            h[1].copy_(d[1], non_blocking=True)
+
+    def both():
+        h2d()
+        d2h()
+
+    t_h, t_d, t_b = timed(h2d), timed(d2h), timed(both)
+    return {"h2d_gbs": nbytes / t_h / 1e9, "d2h_gbs": nbytes / t_d / 1e9,
+            "bidir_h2d_gbs": nbytes / t_b / 1e9, "bidir_d2h_gbs": nbytes / t_b / 1e9}
+
+
 def e2e_plugin(args, dev, pos0, kick0, R, sc):
     """Same workload through the reference-facing plugin boundary with HOST
     buffers: every step calls lbx_advance_bin_host (the C-ABI behind
@@ -578,10 +613,15 @@ def e2e_plugin(args, dev, pos0, kick0, R, sc):
     t0 = time.perf_counter()
     pushed = sum(step() for _ in range(args.e2e_steps))
     el = time.perf_counter() - t0
+    ceil = pcie_ceiling(dev)
+    h2d, d2h = io["h2d"] / args.e2e_steps, io["d2h"] / args.e2e_steps
+    # the e2e roofline: both directions at the measured concurrent copy rates
+    t_min = max(h2d / (ceil["bidir_h2d_gbs"] * 1e9), d2h / (ceil["bidir_d2h_gbs"] * 1e9))
+    bound = (pushed / args.e2e_steps) / t_min
     return {"value": pushed / el, "unit": UNIT,
-            "h2d_bytes_per_step": io["h2d"] // args.e2e_steps,
-            "d2h_bytes_per_step": io["d2h"] // args.e2e_steps,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "steps": args.e2e_steps,
+            "pcie": dict(ceil, bound_pushes_per_s=bound, frac_of_bound=(pushed / el) / bound),
             "path": "lbx_advance_bin_host (reference AoS layout, pinned host buffers, "
                     "4 Mi-particle chunks over 3 streams, no host round trip per chunk), copies in the timed region"}
 

@@ -56,8 +56,50 @@ def scenario(ranks, steps, policy, speed=0.035, drift=0.01, strategy="knapsack",
     return spec, sc
 
 
-def make_timed_engine(lock, log):
-    from paper_2104_11385_b200.parallel import DeviceEngine
+def make_timed_engine(lock, log, physics="surrogate"):
+    from paper_2104_11385_b200.parallel import DeviceEngine, PicEngine
+
+    if physics == "pic":
+        class TimedPic(PicEngine):
+            # A rank's step = its particle kernels + its (replicated) current
+            # gather / field solve + its emigrant partition.  Each part runs
+            # under the lock after a device-wide synchronize, so nothing else
+            # is on the GPU (the other ranks are either queued on the lock or
+            # parked in the next collective); the cross-rank sums are not timed.
+            def local_step(self, wp, wc):
+                import torch
+                with lock:
+                    torch.cuda.synchronize()
+                    self.time_step = True
+                    super().local_step(wp, wc)
+                    log.setdefault(self.rank, []).append(self.last_ms)
+
+            def finish(self):
+                import torch
+                with lock:
+                    torch.cuda.synchronize()
+                    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                    ev[0].record()
+                    super().finish()
+                    ev[1].record()
+                    ev[1].synchronize()
+                    log[self.rank][-1] += ev[0].elapsed_time(ev[1])
+
+            def push(self, wp, wc):
+                import torch
+                self.local_step(wp, wc)
+                self.current_sum()
+                self.finish()
+                with lock:
+                    torch.cuda.synchronize()
+                    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                    ev[0].record()
+                    send_counts, nout = self.partition()
+                    ev[1].record()
+                    ev[1].synchronize()
+                    log[self.rank][-1] += ev[0].elapsed_time(ev[1])
+                return self.counts, self.clk, send_counts, nout
+        return TimedPic
 
     class TimedEngine(DeviceEngine):
         def push(self, wp, wc):
@@ -66,9 +108,8 @@ def make_timed_engine(lock, log):
             import torch
 
             from paper_2104_11385_b200 import _lib
-            st = torch.cuda.current_stream()   # this rank's own stream
-            with lock:   # ranks' kernels run one at a time (no SM sharing)
-                st.synchronize()
+            with lock:   # ranks' kernels run one at a time, on an otherwise idle GPU
+                torch.cuda.synchronize()
                 _lib.lib.lbx_ctx_enable_timing(self.ctx.handle, 1)
                 out = super().push(wp, wc)
                 ms = C.c_float()
@@ -80,7 +121,7 @@ def make_timed_engine(lock, log):
 
 
 def run_emulated(R, steps, replicas, policy, speed=0.035, drift=0.01, strategy="knapsack",
-                 migration_ratio=0.0):
+                 migration_ratio=0.0, physics="surrogate", exchange="nccl"):
     import torch
 
     import bench
@@ -100,10 +141,11 @@ def run_emulated(R, steps, replicas, policy, speed=0.035, drift=0.01, strategy="
             torch.cuda.set_stream(torch.cuda.Stream())   # per-rank stream (thread-local)
             sim = DistributedSimulation(sc, spec.policy, spec.build_provider(),
                                         comm=ThreadComm(shared, r),
-                                        engine_factory=make_timed_engine(lock, log),
+                                        engine_factory=make_timed_engine(lock, log, physics),
                                         positions=pos, kick=kick, device="cuda:0",
                                         replicas=replicas,
-                                        capacity=pos.shape[0] * replicas + 4096)
+                                        capacity=pos.shape[0] * replicas + 4096,
+                                        physics=physics, exchange=exchange)
             sim.run()
             sims[r] = sim
         except Exception as e:
@@ -126,7 +168,7 @@ def run_emulated(R, steps, replicas, policy, speed=0.035, drift=0.01, strategy="
     res = sims[0].result()
     moved = int(sent.sum())
     for s in sims:
-        s.close()
+        s.close(collective=False)   # every rank thread has finished
     return per_step, migrate_ms, res, moved, pos.shape[0] * replicas
 
 
@@ -139,6 +181,11 @@ def main():
     ap.add_argument("--speed", type=float, default=0.035, help="kick speed (cells/step)")
     ap.add_argument("--drift", type=float, default=0.01, help="axial drift (cells/step)")
     ap.add_argument("--strategy", default="knapsack", choices=["knapsack", "sfc"])
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="emigrant exchange of the emulated ranks (p2p: fused peer writes)")
+    ap.add_argument("--physics", default="surrogate", choices=["surrogate", "pic"],
+                    help="pic: the 2D3V PIC step (pic.py) per rank, GpuClock from its "
+                         "kernel, integer current all-reduce + replicated field solve")
     ap.add_argument("--migration-ratio", type=float, default=0.0,
                     help=">0: migration-aware adoption gate (pushes per moved particle)")
     args = ap.parse_args()
@@ -151,12 +198,13 @@ def main():
     out = {"mode": f"emulated {R} ranks on one B200 (per-rank kernels timed alone; "
                    "step time = max over ranks)", "ranks": R, "steps": args.steps,
            "kick": {"speed": args.speed, "drift": args.drift}, "strategy": args.strategy,
-           "migration_ratio": args.migration_ratio, "policies": {}}
+           "migration_ratio": args.migration_ratio, "physics": args.physics, "policies": {}}
     w = args.warmup_steps
     for policy in ("none", "static", "dynamic"):
         per_step, mig, res, moved, n = run_emulated(R, args.steps, args.replicas, policy,
                                                     args.speed, args.drift, args.strategy,
-                                                    args.migration_ratio)
+                                                    args.migration_ratio, args.physics,
+                                                    args.exchange)
         effs = [m.efficiency_after for m in res.metrics]
         total = per_step + mig
         out["policies"][policy] = {
@@ -179,4 +227,7 @@ def main():
 
 
 if __name__ == "__main__":
+    if os.environ.get("LBX_DEBUG_HANG"):      # dump every thread's stack if stuck
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["LBX_DEBUG_HANG"]), exit=True)
     main()

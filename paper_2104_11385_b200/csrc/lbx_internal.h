@@ -70,6 +70,8 @@ struct lbx_ctx {
   unsigned* pic_sortbuf = nullptr;        // PIC sorted mode: cell counts, cursors, block sums
   int64_t pic_sort_cells = 0;
   const void* pic_sort_next = nullptr;    // z array whose cell slots are in the cursors
+  long long* pic_fill = nullptr;          // sorted mode: removed list, holes, tail flags [3][cap]
+  int64_t pic_fill_cap = 0;
   long long* fill_scratch = nullptr;      // hole-fill: holes[cap] + tail flags[cap]
   int64_t fill_cap = 0;
   bool timing = false;                    // lbx_ctx_enable_timing

@@ -200,8 +200,8 @@ __device__ __forceinline__ void stage_emigrant(const StepParams& p, bool em, lon
     // Fused exchange over peer memory: lanes going to the same rank reserve
     // their slots with ONE remote atomic on that rank's cursor and write the
     // records straight into its receive buffer (NVLink / NVSwitch stores).
-    const unsigned grp = __match_any_sync(mask, em ? dest : -1);
-    if (!em) return;
+    if (!em) return;                          // only the lanes in `mask` take part below
+    const unsigned grp = __match_any_sync(mask, dest);
     const int leader = __ffs(grp) - 1;
     unsigned long long base = 0;
     if (lane == leader)
@@ -1585,6 +1585,7 @@ int lbx_ctx_destroy(lbx_ctx* ctx) {
   if (ctx->pic_acc) cudaFree(ctx->pic_acc);
   if (ctx->pic_quad) cudaFree(ctx->pic_quad);
   if (ctx->pic_sortbuf) cudaFree(ctx->pic_sortbuf);
+  if (ctx->pic_fill) cudaFree(ctx->pic_fill);
   if (ctx->fill_scratch) cudaFree(ctx->fill_scratch);
   if (ctx->ev0) cudaEventDestroy((cudaEvent_t)ctx->ev0), cudaEventDestroy((cudaEvent_t)ctx->ev1);
   delete ctx;

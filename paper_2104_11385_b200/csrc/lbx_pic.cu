@@ -67,6 +67,8 @@ struct PicParams {
   int* dep_box;                 // imin, imax, jmin, jmax of depositing cells
   unsigned* cell_cnt;           // sorted mode: kept particles per new cell
   unsigned* cursor;             // sorted mode: next free slot per old cell
+  long long* removed_list;      // sorted mode: slots of absorbed particles (hole filling)
+  long long removed_cap;
   float vscale;                 // power-of-two fixed-point scale (exact in float)
   int nz, nx, qpitch;
   double qm, qw, dt;
@@ -388,6 +390,10 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
         if (i0 + k < n && !keep[k]) {
           ++removed;
           first_out = min(first_out, dest[k]);
+          if (kSort) {   // order is not kept in sorted mode: O(removed) hole filling
+            const unsigned long long slot = atomicAdd(&p.st->removed_count, 1ull);
+            if ((long long)slot < p.removed_cap) p.removed_list[slot] = dest[k];
+          }
         }
       }
       if (kSort) {
@@ -658,6 +664,55 @@ __global__ void pic_scan_apply_kernel(unsigned* cell_cnt, long long cells,
   }
 }
 
+// Sorted mode, O(removed) compaction of the absorbed slots: survivors from
+// the tail [n_new, n_new + L) move into the holes below n_new (order within a
+// cell is not kept anyway).  L = st->removed_count; when it exceeds the list
+// capacity these kernels do nothing and the stable compaction runs instead.
+__global__ void pic_fill_mark_kernel(DevState* st, const long long* __restrict__ removed,
+                                     long long cap, long long* holes, long long* tail_flag) {
+  const long long L = (long long)st->removed_count, n_new = st->n;
+  if (L == 0 || L > cap) return;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < L;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long r = removed[k];
+    if (r >= n_new) tail_flag[r - n_new] = 1;
+    else holes[atomicAdd(&st->holes, 1ull)] = r;
+  }
+}
+
+__global__ void pic_fill_move_kernel(DevState* st, long long cap, const long long* __restrict__ holes,
+                                     long long* tail_flag, double* z, double* x, double* uz,
+                                     double* ux, double* uy) {
+  const long long L = (long long)st->removed_count, n_new = st->n;
+  if (L == 0 || L > cap) return;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < L;
+       j += (long long)gridDim.x * blockDim.x) {
+    if (tail_flag[j]) {
+      tail_flag[j] = 0;
+      continue;
+    }
+    const long long src = n_new + j;
+    const long long dst = holes[atomicAdd(&st->movers, 1ull)];
+    z[dst] = z[src];
+    x[dst] = x[src];
+    uz[dst] = uz[src];
+    ux[dst] = ux[src];
+    uy[dst] = uy[src];
+  }
+}
+
+__global__ void pic_fill_done_kernel(DevState* st, long long cap) {
+  const long long L = (long long)st->removed_count;
+  if (L > 0 && L <= cap) {   // compacted: nothing left for the stable pass
+    st->leavers = 0ull;
+    st->first_leaver = LLONG_MAX;
+    st->n_old = st->n;
+  }
+  st->holes = 0ull;
+  st->movers = 0ull;
+  st->removed_count = 0ull;
+}
+
 // fields -> quads: Q[c][qi*(nx+1) + qj] = (F[qi][qj], F[qi][qj+1], F[qi+1][qj],
 // F[qi+1][qj+1]) in padded indices, qi in [0, nz], qj in [0, nx]; also resets
 // the deposit bounding box for this step's push.
@@ -882,6 +937,18 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
     ctx->pic_sort_cells = cells;
     ctx->pic_sort_next = nullptr;
   }
+  const long long rcap = std::max(1ll << 20, (long long)(ctx->n_upper / 64));
+  if (sorted && (!ctx->pic_fill || ctx->pic_fill_cap < rcap)) {
+    if (ctx->pic_fill) {
+      cudaDeviceSynchronize();
+      cudaFree(ctx->pic_fill);
+    }
+    ctx->pic_fill = nullptr;
+    if (cudaMalloc(&ctx->pic_fill, (size_t)rcap * 3 * 8) != cudaSuccess)
+      return set_error(LBX_EOOM, "PIC hole-filling lists");
+    cudaMemsetAsync(ctx->pic_fill, 0, (size_t)rcap * 3 * 8, s);
+    ctx->pic_fill_cap = rcap;
+  }
   float4* Q = static_cast<float4*>(ctx->pic_quad);
   unsigned* cell_cnt = sorted ? ctx->pic_sortbuf : nullptr;
   unsigned* cursor = sorted ? ctx->pic_sortbuf + cells : nullptr;
@@ -903,6 +970,8 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   p.ouy = out[4];
   p.cell_cnt = cell_cnt;
   p.cursor = cursor;
+  p.removed_list = sorted ? ctx->pic_fill : nullptr;
+  p.removed_cap = sorted ? ctx->pic_fill_cap : 0;
   for (int c = 0; c < 6; ++c) p.Q[c] = Q + c * quads;
   p.Jc = ctx->pic_acc;
   p.dep_box = dep_box;
@@ -961,6 +1030,15 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   kern<<<(unsigned)grid, kPB, smem, s>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "pic_push_kernel launch");
+  if (sorted) {
+    const long long fc = ctx->pic_fill_cap;
+    const unsigned fg2 = (unsigned)std::max(1, ctx->num_sms * 2);
+    pic_fill_mark_kernel<<<fg2, 256, 0, s>>>(ctx->st, ctx->pic_fill, fc, ctx->pic_fill + fc,
+                                             ctx->pic_fill + 2 * fc);
+    pic_fill_move_kernel<<<fg2, 256, 0, s>>>(ctx->st, fc, ctx->pic_fill + fc, ctx->pic_fill + 2 * fc,
+                                             out[0], out[1], out[2], out[3], out[4]);
+    pic_fill_done_kernel<<<1, 1, 0, s>>>(ctx->st, fc);
+  }
   rc = launch_compact(ctx, out[0], out[1], out[2], out[3], out[4], nullptr, (double)a->nz,
                       (double)a->nx, stream);
   if (rc) return rc;

@@ -382,6 +382,8 @@ class PicEngine(DeviceEngine):
                        for k in FIELD_NAMES + CURRENT_NAMES}
         self.field_names, self.current_names = FIELD_NAMES, CURRENT_NAMES
         self.comm = None
+        self.time_step = False      # bench_lb: CUDA events around the particle kernels
+        self.last_ms = 0.0
         self.nout2 = torch.zeros(2, dtype=torch.int64, device=self.dev)
         self.ubox = torch.zeros(4, dtype=torch.int64, device=self.dev)
 
@@ -410,6 +412,13 @@ class PicEngine(DeviceEngine):
         return a
 
     def push(self, wp, wc):
+        self.local_step(wp, wc)
+        self.current_sum_finish()
+        send_counts, nout = self.partition()
+        return self.counts, self.clk, send_counts, nout
+
+    def local_step(self, wp, wc):
+        """The rank's particle kernels: PIC step with the current deferred."""
         stream = self.D._stream(self.dev)
         self.ctx.set_count(self.n)
         a = self._args((_lib.LBX_STEP_CLOCK if self.clock else 0) | _lib.LBX_PIC_DEFER_CURRENT)
@@ -417,13 +426,32 @@ class PicEngine(DeviceEngine):
         a.counts_out, a.cost_out, a.clk_out = (_lib.ptr(self.counts), _lib.ptr(self.cost),
                                                _lib.ptr(self.clk))
         a.n_out, a.err_out = _lib.ptr(self.nout2), _lib.ptr(self.nout2[1:])
+        if self.time_step:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record()
         _lib.check(_lib.lib.lbx_pic_step(self.ctx.handle, C.byref(a), stream))
+        if self.time_step:
+            ev[1].record()
         self.launches += 6   # set_count, quad, push, compaction, (scan), current view
         h = self.nout2.cpu().numpy()
+        if self.time_step:
+            self.last_ms = ev[0].elapsed_time(ev[1])
         if h[1]:
             raise ValueError(f"{int(h[1])} particles fell outside the box grid")
         self.n = int(h[0])
-        # guard-cell current: exact integer sum over the union of deposit boxes
+
+    def current_sum_finish(self):
+        """Guard-cell current: exact integer sum over the union of the ranks'
+        deposit boxes, then node gather + Yee update."""
+        self.current_sum()
+        self.finish()
+
+    def finish(self):
+        _lib.check(_lib.lib.lbx_pic_finish(self.ctx.handle, C.byref(self._args(0)),
+                                           self.D._stream(self.dev)))
+        self.launches += 4   # current, zero, B, E
+
+    def current_sum(self):
         jc_p, cells, box_p = C.c_void_p(), C.c_int64(), C.c_void_p()
         _lib.check(_lib.lib.lbx_pic_current_view(self.ctx.handle, C.byref(jc_p), C.byref(cells),
                                                  C.byref(box_p)))
@@ -438,10 +466,6 @@ class PicEngine(DeviceEngine):
             jc = torch.as_tensor(_DevArray(jc_p.value, cells.value * 16, "<i8"), device=self.dev)
             band = jc[r0 * self.nx * 16:(r1 + 1) * self.nx * 16]
             self.comm.all_reduce_sum(band)
-        _lib.check(_lib.lib.lbx_pic_finish(self.ctx.handle, C.byref(self._args(0)), stream))
-        self.launches += 4   # current, zero, B, E
-        send_counts, nout = self.partition()
-        return self.counts, self.clk, send_counts, nout
 
     def unpack(self, recv: torch.Tensor):
         n0 = self.n
@@ -574,11 +598,17 @@ class DistributedSimulation:
             raise ConfigError("exchange='p2p' needs CUDA engines with peer access between all ranks")
         return "p2p" if ok else "nccl"
 
-    def close(self):
+    def close(self, collective=True):
+        """Release native state.  With the peer-memory exchange every rank's
+        buffers are mapped by the others, so by default close is collective
+        (all ranks call it together); collective=False when the caller knows
+        no rank runs any more (e.g. thread-ranks closed one after another)."""
         if getattr(self, "engine", None) is not None and getattr(self.engine, "p2p", False):
-            self.comm.barrier()        # peers may still map this rank's buffers
+            if collective:
+                self.comm.barrier()        # peers may still map this rank's buffers
             self.engine.close_p2p()
-            self.comm.barrier()
+            if collective:
+                self.comm.barrier()
         if getattr(self, "lb", None):
             _lib.lib.lbx_lb_destroy(self.lb)
             self.lb = None
