@@ -213,7 +213,7 @@ def main():
             "ms_per_step": float(total[w:].mean()),
             "e0": float(res.metrics[0].efficiency_before), "mean_eff": float(np.mean(effs)),
             "adoptions": res.summary["adoption_count"], "particles_migrated": moved,
-            "particles": n}
+            "particles": n, "step_ms": [round(float(t), 4) for t in total]}
     P = out["policies"]
     x = EXPONENT_PRESETS["2d3v"]
     e0 = P["none"]["e0"]

@@ -116,15 +116,20 @@ def test_fused_sfc_weights_no_fma():
     assert np.array_equal(out["cost"], O.heuristic_cost(c2, np.full(36, 256), 0.02, 0.98))
 
 
-@pytest.mark.parametrize("n", [0, 1, 5000, (1 << 22) + 17, 9_000_001])
-def test_host_pipeline_matches_oracle(K, n):
-    """lbx_advance_bin_host: chunked three-stream pipeline, host buffers (absorbing:
-    exercises the host-side gap closing across chunks)."""
+@pytest.mark.parametrize("n,sigma", [(0, 1.5), (1, 1.5), (5000, 1.5), ((1 << 22) + 17, 1.5),
+                                     (9_000_001, 1.5), (9_000_001, 0.0), (9_000_001, 0.004)])
+def test_host_pipeline_matches_oracle(K, n, sigma):
+    """lbx_advance_bin_host: chunked three-stream pipeline, host buffers.
+    sigma 1.5: many absorbed per chunk (velocities copied back from the
+    device, host gap closing); 0: none absorbed (host-side velocity copy);
+    0.004: a few per chunk (host copy skipping the listed absorbed indices)."""
     rng = np.random.default_rng(n + 7)
     pos = rng.uniform(0, 96.0, size=(n, 2))
-    vel = rng.normal(0, 1.5, size=(n, 2))
+    vel = rng.normal(0, sigma, size=(n, 2))
     p, v, counts, cost = K.advance_bin_host(pos, vel, 96.0, 96.0, 16.0, 6, 6)
     p2, v2 = O.advance_particles(pos, vel, 96.0, 96.0)
+    if sigma == 0.004:
+        assert 0 < n - p2.shape[0] < (n // (1 << 22) + 1) * 65536
     assert np.array_equal(p, p2) and np.array_equal(v, v2)
     c2 = O.bin_particles(p2, 16.0, 6, 6)
     assert np.array_equal(counts, c2)
