@@ -369,8 +369,10 @@ typedef struct lbx_pic_args {
    * are contiguous and their current is accumulated in registers.  The
    * caller swaps in/out after the call.  The library keeps the next step's
    * cell slots; passing any other input than the last call's out[] (or
-   * LBX_PIC_RESYNC) recounts them.  Order within a cell is not
-   * deterministic; every computed value is.  NULL: in place, order kept. */
+   * LBX_PIC_RESYNC) recounts them.  Absorbed particles' slots are filled
+   * from the tail (O(absorbed)).  Order within a cell is not deterministic;
+   * every computed value is.  NULL: in place, order kept (stable
+   * compaction). */
   double* out[5];
 } lbx_pic_args;
 
