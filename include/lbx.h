@@ -340,6 +340,9 @@ int lbx_sim_particles(lbx_sim* sim, int64_t* n, void* stream);
  * ---------------------------------------------------------------------- */
 #define LBX_PIC_NO_FIELD_SOLVE 2u  /* skip the Yee update (tests)         */
 #define LBX_PIC_RESYNC 4u          /* sorted mode: recount the input cells   */
+#define LBX_PIC_QUAD 16u           /* gather from the quad-expanded copy     */
+#define LBX_PIC_DIRECT 32u         /* gather from the fields (default: quad  */
+                                   /* when >= 16 particles per cell)         */
 #define LBX_PIC_DEFER_CURRENT 8u   /* stop after push + compaction: the      */
                                    /* cell accumulator stays for a cross-GPU */
                                    /* reduction, then lbx_pic_finish         */

@@ -123,6 +123,8 @@ RECORD_DOUBLES = 6
 LBX_PIC_NO_FIELD_SOLVE = 2
 LBX_PIC_RESYNC = 4
 LBX_PIC_DEFER_CURRENT = 8
+LBX_PIC_QUAD = 16
+LBX_PIC_DIRECT = 32
 
 
 class PicArgs(C.Structure):

@@ -63,6 +63,8 @@ struct PicParams {
   const double *z, *x, *uz, *ux, *uy;     // particles in
   double *oz, *ox, *ouz, *oux, *ouy;      // particles out (== in unless sorting)
   const float4* Q[6];           // quad-expanded Ex Ey Ez Bx By Bz, [(nz+1) x (nx+1)]
+  const float* F[6];            // the fields themselves (direct gather, sparse plasmas)
+  int pitch;                    // nx + 2
   unsigned long long* Jc;       // cell-centric fixed-point node sums [nz*nx][16]
   int* dep_box;                 // imin, imax, jmin, jmax of depositing cells
   unsigned* cell_cnt;           // sorted mode: kept particles per new cell
@@ -249,7 +251,20 @@ __device__ __forceinline__ void enqueue(FlushEntry* e, const int v[kNodes], int 
 #ifndef LBX_PIC_MINB
 #define LBX_PIC_MINB 2
 #endif
-template <bool kClock, bool kSort>
+// Gather of one component: from the quad copy (one 16-byte load) or, when
+// the particles are too sparse for the copy to pay (kQuad = false: each
+// node's quad would be fetched from HBM for a handful of particles), from
+// the field array itself (four 4-byte loads, 4x less gathered footprint).
+template <bool kQuad>
+__device__ __forceinline__ float gather_c(const PicParams& p, int c, int i0, int j0, float fz,
+                                          float fx) {
+  if (kQuad) return cic(__ldg(p.Q[c] + (i0 + 1) * p.qpitch + (j0 + 1)), fz, fx);
+  const float* F = p.F[c] + (i0 + 1) * p.pitch + (j0 + 1);
+  return cic(make_float4(__ldg(F), __ldg(F + 1), __ldg(F + p.pitch), __ldg(F + p.pitch + 1)), fz,
+             fx);
+}
+
+template <bool kClock, bool kSort, bool kQuad>
 __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p) {
   extern __shared__ __align__(16) unsigned char s_dyn[];
   FlushEntry* s_q = reinterpret_cast<FlushEntry*>(s_dyn) + (size_t)(threadIdx.x >> 5) * kQCap;
@@ -335,17 +350,13 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
 #pragma unroll
       for (int k = 0; k < kG; ++k) {
         const Axis az = axis_of(pz[k]), ax = axis_of(px[k]);
-        const int qp = p.qpitch;
-        const int oA = (az.i + 1) * qp + (ax.ih + 1);    // (0, 1/2)   Ex Bz
-        const int oB = (az.i + 1) * qp + (ax.i + 1);     // (0, 0)     Ey
-        const int oC = (az.ih + 1) * qp + (ax.i + 1);    // (1/2, 0)   Ez Bx
-        const int oD = (az.ih + 1) * qp + (ax.ih + 1);   // (1/2, 1/2) By
-        const float Ex = cic(__ldg(p.Q[0] + oA), az.f, ax.fh);
-        const float Ey = cic(__ldg(p.Q[1] + oB), az.f, ax.f);
-        const float Ez = cic(__ldg(p.Q[2] + oC), az.fh, ax.f);
-        const float Bx = cic(__ldg(p.Q[3] + oC), az.fh, ax.f);
-        const float By = cic(__ldg(p.Q[4] + oD), az.fh, ax.fh);
-        const float Bz = cic(__ldg(p.Q[5] + oA), az.f, ax.fh);
+        // staggers: (0, 1/2) Ex Bz | (0, 0) Ey | (1/2, 0) Ez Bx | (1/2, 1/2) By
+        const float Ex = gather_c<kQuad>(p, 0, az.i, ax.ih, az.f, ax.fh);
+        const float Ey = gather_c<kQuad>(p, 1, az.i, ax.i, az.f, ax.f);
+        const float Ez = gather_c<kQuad>(p, 2, az.ih, ax.i, az.fh, ax.f);
+        const float Bx = gather_c<kQuad>(p, 3, az.ih, ax.i, az.fh, ax.f);
+        const float By = gather_c<kQuad>(p, 4, az.ih, ax.ih, az.fh, ax.fh);
+        const float Bz = gather_c<kQuad>(p, 5, az.i, ax.ih, az.f, ax.fh);
         // relativistic Boris (x, y, z order; oracle boris())
         const double hEx = __dmul_rn(h, (double)Ex), hEy = __dmul_rn(h, (double)Ey),
                      hEz = __dmul_rn(h, (double)Ez);
@@ -973,6 +984,8 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   p.removed_list = sorted ? ctx->pic_fill : nullptr;
   p.removed_cap = sorted ? ctx->pic_fill_cap : 0;
   for (int c = 0; c < 6; ++c) p.Q[c] = Q + c * quads;
+  for (int c = 0; c < 6; ++c) p.F[c] = a->fields[c];
+  p.pitch = a->nx + 2;
   p.Jc = ctx->pic_acc;
   p.dep_box = dep_box;
   int e2 = 0;
@@ -1012,13 +1025,23 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
     pic_scan_reduce_kernel<<<kScanBlocks, kScanThreads, 0, s>>>(cell_cnt, cells, block_sum);
     pic_scan_apply_kernel<<<kScanBlocks, kScanThreads, 0, s>>>(cell_cnt, cells, block_sum, cursor);
   }
-  pic_quad_kernel<<<qg, 256, 0, s>>>(a->fields[0], a->fields[1], a->fields[2], a->fields[3],
-                                     a->fields[4], a->fields[5], Q, quads, p.qpitch, pitch,
-                                     dep_box);
+  // quad copy when nodes are shared by many particles (dense plasma), else
+  // direct gather (LBX_PIC_QUAD / LBX_PIC_DIRECT force either)
+  bool quad = ctx->n_upper >= 16 * cells;
+  if (a->flags & LBX_PIC_QUAD) quad = true;
+  if (a->flags & LBX_PIC_DIRECT) quad = false;
+  pic_quad_kernel<<<quad ? qg : 1, 256, 0, s>>>(a->fields[0], a->fields[1], a->fields[2],
+                                                 a->fields[3], a->fields[4], a->fields[5], Q,
+                                                 quad ? quads : 0, p.qpitch, pitch, dep_box);
   const size_t smem = (size_t)kPW * kQCap * sizeof(FlushEntry) + (size_t)nb * 8;
   const bool clock = (a->flags & LBX_STEP_CLOCK) != 0;
-  auto kern = clock ? (sorted ? pic_push_kernel<true, true> : pic_push_kernel<true, false>)
-                    : (sorted ? pic_push_kernel<false, true> : pic_push_kernel<false, false>);
+  void (*kern)(PicParams);
+  if (quad)
+    kern = clock ? (sorted ? pic_push_kernel<true, true, true> : pic_push_kernel<true, false, true>)
+                 : (sorted ? pic_push_kernel<false, true, true> : pic_push_kernel<false, false, true>);
+  else
+    kern = clock ? (sorted ? pic_push_kernel<true, true, false> : pic_push_kernel<true, false, false>)
+                 : (sorted ? pic_push_kernel<false, true, false> : pic_push_kernel<false, false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(pic)");
   int per_sm = 0;

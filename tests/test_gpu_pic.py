@@ -29,7 +29,7 @@ def setup(n, nz, nx, seed, speed=0.3, clustered=True):
 
 
 def run_both(pos, u, nz, nx, steps, field_solve=True, qm=-1.0, qw=-0.05, dt=0.5, M=16,
-             sort=False):
+             sort=False, gather=None):
     from paper_2104_11385_b200 import device, pic
     ctx = device.Context(capacity=pos.shape[0])
     st = pic.PicState.create(pos, u, nz, nx)
@@ -38,7 +38,8 @@ def run_both(pos, u, nz, nx, steps, field_solve=True, qm=-1.0, qw=-0.05, dt=0.5,
          "ux": u[:, 1].copy(), "uy": u[:, 2].copy()}
     outs = []
     for _ in range(steps):
-        out = pic.pic_step(ctx, st, M, qm, qw, dt, field_solve=field_solve, clock=True, sort=sort)
+        out = pic.pic_step(ctx, st, M, qm, qw, dt, field_solve=field_solve, clock=True, sort=sort,
+                           gather=gather)
         PO.particle_step(f, p, nz, nx, qm, qw, dt)
         fj = {k: f[k].copy() for k in ("Jx", "Jy", "Jz")}
         if field_solve:
@@ -73,10 +74,12 @@ def test_first_step_particles_and_currents_exact():
     assert ((outs[0][0]["clock"] > 0) == (c > 0)).all()
 
 
+@pytest.mark.parametrize("gather", ["quad", "direct"])
 @pytest.mark.parametrize("clustered", [True, False])
-def test_multi_step_with_field_solve(clustered):
+def test_multi_step_with_field_solve(clustered, gather):
+    """Both gather paths (quad-expanded copy / the fields directly)."""
     pos, u = setup(40_000, 64, 96, seed=2, clustered=clustered)
-    st, f, p, outs = run_both(pos, u, 64, 96, steps=6, field_solve=True)
+    st, f, p, outs = run_both(pos, u, 64, 96, steps=6, field_solve=True, gather=gather)
     g = st.particles()
     assert g["z"].shape == p["z"].shape
     for k in ("z", "x", "uz", "ux", "uy"):
