@@ -45,7 +45,10 @@
 namespace lbx {
 namespace {
 
-constexpr int kPB = 256;                  // threads per CTA
+#ifndef LBX_PIC_PB
+#define LBX_PIC_PB 256
+#endif
+constexpr int kPB = LBX_PIC_PB;           // threads per CTA
 constexpr int kPW = kPB / 32;
 #ifndef LBX_PIC_RUN
 #define LBX_PIC_RUN 64
@@ -222,7 +225,12 @@ struct __align__(16) FlushEntry {
   unsigned m;
   int pad[2];
 };
-constexpr int kQCap = 32 * kG;   // drained after every group and after the run's final entries
+#ifndef LBX_PIC_QCAP
+#define LBX_PIC_QCAP (32 * kG)
+#endif
+// Entries per warp queue: drained after every group, after the run's final
+// entries, and within a group whenever fewer than 32 free entries remain.
+constexpr int kQCap = LBX_PIC_QCAP;
 
 template <bool kSort>
 __device__ __forceinline__ void drain_queue(const PicParams& p, const FlushEntry* q, int count,
@@ -450,6 +458,10 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
           enqueue(s_q + qn + __popc(fm & lt), strag ? q : acc, strag ? nkey[k] : cur,
                   strag ? 1u : cur_m);
         qn += __popc(fm);
+        if (kQCap < 32 * kG && qn > kQCap - 32) {   // small queue: drain mid-group
+          drain_queue<kSort>(p, s_q, qn, lane);
+          qn = 0;
+        }
         if (same) {
 #pragma unroll
           for (int i = 0; i < kNodes; ++i) acc[i] += q[i];

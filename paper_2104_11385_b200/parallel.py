@@ -544,7 +544,7 @@ class DistributedSimulation:
         self.engine.set_owner(self.initial_owner)
         self.exchange = self._choose_exchange(exchange)
         if self.exchange == "p2p":
-            self.engine.enable_p2p(self.comm)
+            self._enable_p2p(exchange == "p2p")
         self.conf = sim_config(cfg, policy, provider)
         h = C.c_void_p()
         own = np.ascontiguousarray(self.initial_owner, dtype=np.int64)
@@ -597,6 +597,31 @@ class DistributedSimulation:
         if exchange == "p2p" and not ok:
             raise ConfigError("exchange='p2p' needs CUDA engines with peer access between all ranks")
         return "p2p" if ok else "nccl"
+
+    def _enable_p2p(self, required):
+        """Map the peers' receive buffers; if any rank fails (IPC not
+        permitted in the container, no peer mapping, out of memory) every
+        rank falls back to the collective exchange together."""
+        ok, err = 1, None
+        try:
+            self.engine.enable_p2p(self.comm)
+        except Exception as e:   # noqa: BLE001 -- reported below / re-raised if required
+            ok, err = 0, e
+        flag = torch.tensor([ok], dtype=torch.int64, device=self.engine.dev)
+        self.comm.all_reduce_sum(flag)
+        if int(flag.item()) == self.world:
+            return
+        if self.engine.p2p:
+            self.comm.barrier()
+            self.engine.close_p2p()
+        if required:
+            raise ConfigError(f"exchange='p2p' could not map peer memory: {err}")
+        self.exchange = "nccl"
+        self.p2p_error = str(err) if err else "a peer rank failed"
+        self.engine.stage = torch.empty((self.engine.capacity + 2, REC), dtype=torch.float64,
+                                        device=self.engine.dev)
+        self.engine.stage_dest = torch.empty(self.engine.capacity + 2, dtype=torch.int32,
+                                             device=self.engine.dev)
 
     def close(self, collective=True):
         """Release native state.  With the peer-memory exchange every rank's
