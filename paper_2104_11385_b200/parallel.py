@@ -90,7 +90,9 @@ class TorchComm:
                 continue
             q = C.c_void_p()
             buf = (C.c_ubyte * 64).from_buffer_copy(h)
-            _lib.check(_lib.lib.lbx_peer_open(buf, C.byref(q)))
+            if _lib.lib.lbx_peer_open(buf, C.byref(q)) != 0:
+                ptrs.append(None)          # the caller agrees on failure collectively
+                continue
             ptrs.append(int(q.value))
             opened.append(int(q.value))
         return ptrs, opened
@@ -204,14 +206,32 @@ class DeviceEngine:
         (step parity) + two cursors; the push / partition kernels write
         emigrant records straight into the destination's buffer (remote
         atomics + stores over NVLink / NVSwitch), replacing staging, the
-        counts all-to-all, the grouping kernel and the record all-to-all."""
+        counts all-to-all, the grouping kernel and the record all-to-all.
+        Single-rank convenience: DistributedSimulation runs the phases with
+        agreement between them (p2p_alloc / p2p_connect)."""
+        self.p2p_alloc()
+        ptrs, opened = comm.share_peer(self._peer_own, self._peer_handle)
+        if any(q is None for q in ptrs):
+            self._peer_opened = list(opened)
+            self.p2p_release()
+            raise RuntimeError("cudaIpcOpenMemHandle failed for a peer buffer")
+        self.p2p_connect(ptrs, opened)
+
+    def p2p_alloc(self):
+        """Local phase 1: this rank's receive buffers (may fail)."""
         nrec = self.capacity + 2
-        per = nrec * REC * 8
-        total = 2 * per + 64
+        self._peer_per = nrec * REC * 8
         ptr, handle = C.c_void_p(), (C.c_ubyte * 64)()
-        _lib.check(_lib.lib.lbx_peer_alloc(total, C.byref(ptr), handle))
+        _lib.check(_lib.lib.lbx_peer_alloc(2 * self._peer_per + 64, C.byref(ptr), handle))
         self._peer_own = int(ptr.value)
-        ptrs, self._peer_opened = comm.share_peer(self._peer_own, bytes(handle))
+        self._peer_handle = bytes(handle)
+        self._peer_opened = []
+
+    def p2p_connect(self, ptrs, opened):
+        """Local phase 2 (after the collective handle exchange): device tables
+        of every rank's buffers and cursors."""
+        per, nrec = self._peer_per, self.capacity + 2
+        self._peer_opened = list(opened)
         i64 = dict(dtype=torch.int64, device=self.dev)
         self.peer_recv = [torch.tensor([b + par * per for b in ptrs], **i64) for par in (0, 1)]
         self.peer_cursor = [torch.tensor([b + 2 * per + 8 * par for b in ptrs], **i64)
@@ -223,6 +243,15 @@ class DeviceEngine:
         self.stage = torch.empty((1, REC), dtype=torch.float64, device=self.dev)
         self.stage_dest = torch.empty(1, dtype=torch.int32, device=self.dev)
         self.p2p = True
+
+    def p2p_release(self):
+        """Undo p2p_alloc / an opened mapping (failure path, no kernels ran)."""
+        for q in getattr(self, "_peer_opened", []):
+            _lib.lib.lbx_peer_close(C.c_void_p(q))
+        self._peer_opened = []
+        if getattr(self, "_peer_own", None):
+            _lib.lib.lbx_peer_free(C.c_void_p(self._peer_own))
+            self._peer_own = None
 
     def close_p2p(self):
         if not self.p2p:
@@ -599,29 +628,36 @@ class DistributedSimulation:
         return "p2p" if ok else "nccl"
 
     def _enable_p2p(self, required):
-        """Map the peers' receive buffers; if any rank fails (IPC not
-        permitted in the container, no peer mapping, out of memory) every
-        rank falls back to the collective exchange together."""
-        ok, err = 1, None
+        """Map the peers' receive buffers in two phases with a collective
+        agreement after each (allocation; handle exchange + mapping): if any
+        rank fails (IPC not permitted in the container, no peer mapping, out
+        of memory) every rank falls back to the collective exchange."""
+        def agree(ok):
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int64, device=self.engine.dev)
+            self.comm.all_reduce_sum(flag)
+            return int(flag.item()) == self.world
+
+        err = None
         try:
-            self.engine.enable_p2p(self.comm)
-        except Exception as e:   # noqa: BLE001 -- reported below / re-raised if required
-            ok, err = 0, e
-        flag = torch.tensor([ok], dtype=torch.int64, device=self.engine.dev)
-        self.comm.all_reduce_sum(flag)
-        if int(flag.item()) == self.world:
-            return
-        if self.engine.p2p:
-            self.comm.barrier()
-            self.engine.close_p2p()
+            self.engine.p2p_alloc()
+            ok = True
+        except Exception as e:   # noqa: BLE001 -- agreed on below
+            ok, err = False, e
+        if agree(ok):
+            ptrs, opened = self.comm.share_peer(self.engine._peer_own, self.engine._peer_handle)
+            ok = all(q is not None for q in ptrs)
+            self.engine._peer_opened = list(opened)
+            if not ok:
+                err = RuntimeError("cudaIpcOpenMemHandle failed for a peer buffer")
+            if agree(ok):
+                self.engine.p2p_connect(ptrs, opened)
+                return
+        self.comm.barrier()
+        self.engine.p2p_release()
         if required:
             raise ConfigError(f"exchange='p2p' could not map peer memory: {err}")
         self.exchange = "nccl"
         self.p2p_error = str(err) if err else "a peer rank failed"
-        self.engine.stage = torch.empty((self.engine.capacity + 2, REC), dtype=torch.float64,
-                                        device=self.engine.dev)
-        self.engine.stage_dest = torch.empty(self.engine.capacity + 2, dtype=torch.int32,
-                                             device=self.engine.dev)
 
     def close(self, collective=True):
         """Release native state.  With the peer-memory exchange every rank's

@@ -134,3 +134,30 @@ def test_host_pipeline_matches_oracle(K, n, sigma):
     c2 = O.bin_particles(p2, 16.0, 6, 6)
     assert np.array_equal(counts, c2)
     assert np.array_equal(cost, O.heuristic_cost(c2, np.full(36, 256), 0.75, 0.25))
+
+
+@pytest.mark.parametrize("m", [15.0, 24.0, 7.0])
+def test_fused_step_non_power_of_two_boxes(m):
+    """Box sizes that are not powers of two take the IEEE-division binning
+    path ((int)(z / M), _kernels.pyx:45-46); include positions landing
+    exactly on box boundaries after the push."""
+    from paper_2104_11385_b200 import device
+    rng = np.random.default_rng(int(m))
+    nb1 = 6
+    ext = m * nb1
+    n = 400_003
+    pos = rng.uniform(0, ext, size=(n, 2))
+    vel = rng.normal(0, 0.7, size=(n, 2))
+    k = rng.integers(0, nb1, size=(n // 4, 2)).astype(np.float64)
+    pos[: n // 4] = k * m + 0.25          # lands exactly on k*m after a -0.25 push
+    vel[: n // 4] = -0.25
+    st = device.ParticleState.from_numpy(pos, vel)
+    ctx = device.Context(capacity=n)
+    out = device.push_step(ctx, st, ext, ext, m, nb1, nb1, (0.02, 0.98), clock=True)
+    p2, v2 = O.advance_particles(pos, vel, ext, ext)
+    c2 = O.bin_particles(p2, m, nb1, nb1)
+    assert out["n"] == p2.shape[0]
+    assert np.array_equal(out["counts"], c2)
+    assert np.array_equal(out["cost"], O.heuristic_cost(c2, np.full(nb1 * nb1, m * m), 0.02, 0.98))
+    gp, gv = st.to_numpy()
+    assert np.array_equal(gp, p2) and np.array_equal(gv, v2)
