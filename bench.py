@@ -532,8 +532,28 @@ def run_lbx_dist(args, rank, world, dev):
                          "traffic": None},
             "clocks": clocks.summary(),
         }
-        print(json.dumps(line), flush=True)
     sim.close()
+    del sim
+    torch.cuda.empty_cache()
+    if not args.no_e2e:
+        # e2e at N GPUs: every rank drives the host-buffer plugin path on its
+        # own C2 x R set (weak scaling, its own PCIe link), started together;
+        # value = all ranks' pushes / the slowest rank's wall time
+        dist.barrier()
+        e = e2e_plugin(args, dev, pos0, kick0, args.replicas, sc)
+        agg = torch.tensor([e["pushed"], e["seconds"], e["h2d_bytes_per_step"],
+                            e["d2h_bytes_per_step"]], dtype=torch.float64, device=dev)
+        mx = agg.clone()
+        dist.all_reduce(agg)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            line["e2e"] = {"value": float(agg[0].item() / mx[1].item()), "unit": UNIT,
+                           "h2d_bytes_per_step": int(agg[2].item()),
+                           "d2h_bytes_per_step": int(agg[3].item()),
+                           "steps": e["steps"], "per_rank": {k: e[k] for k in ("path", "pcie")},
+                           "note": "all ranks' host-buffer plugin calls, max wall time over ranks"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 
 
@@ -620,13 +640,17 @@ def e2e_plugin(args, dev, pos0, kick0, R, sc):
     bound = (pushed / args.e2e_steps) / t_min
     return {"value": pushed / el, "unit": UNIT,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "steps": args.e2e_steps,
+            "steps": args.e2e_steps, "seconds": el, "pushed": pushed,
             "pcie": dict(ceil, bound_pushes_per_s=bound, frac_of_bound=(pushed / el) / bound),
             "path": "lbx_advance_bin_host (reference AoS layout, pinned host buffers, "
                     "4 Mi-particle chunks over 3 streams, no host round trip per chunk), copies in the timed region"}
 
 
 def main():
+    # one JSON line on stdout: keep NCCL's version banner off it unless the
+    # user asked for NCCL debugging
+    if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+        os.environ["NCCL_DEBUG"] = "WARN"
     args = parse()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
