@@ -340,6 +340,10 @@ int lbx_sim_particles(lbx_sim* sim, int64_t* n, void* stream);
  * ---------------------------------------------------------------------- */
 #define LBX_PIC_NO_FIELD_SOLVE 2u  /* skip the Yee update (tests)         */
 #define LBX_PIC_RESYNC 4u          /* sorted mode: recount the input cells   */
+#define LBX_PIC_STABLE_ORDER 64u   /* in place: keep particle order (stable  */
+                                   /* compaction of absorbed particles);     */
+                                   /* default fills their slots from the     */
+                                   /* tail, O(absorbed)                      */
 #define LBX_PIC_QUAD 16u           /* gather from the quad-expanded copy     */
 #define LBX_PIC_DIRECT 32u         /* gather from the fields (default: quad  */
                                    /* when >= 16 particles per cell)         */
@@ -374,8 +378,8 @@ typedef struct lbx_pic_args {
    * cell slots; passing any other input than the last call's out[] (or
    * LBX_PIC_RESYNC) recounts them.  Absorbed particles' slots are filled
    * from the tail (O(absorbed)).  Order within a cell is not deterministic;
-   * every computed value is.  NULL: in place, order kept (stable
-   * compaction). */
+   * every computed value is.  NULL: in place (order kept with
+   * LBX_PIC_STABLE_ORDER, else absorbed slots filled from the tail). */
   double* out[5];
 } lbx_pic_args;
 

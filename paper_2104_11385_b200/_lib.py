@@ -124,6 +124,7 @@ LBX_PIC_NO_FIELD_SOLVE = 2
 LBX_PIC_RESYNC = 4
 LBX_PIC_DEFER_CURRENT = 8
 LBX_PIC_QUAD = 16
+LBX_PIC_STABLE_ORDER = 64
 LBX_PIC_DIRECT = 32
 
 

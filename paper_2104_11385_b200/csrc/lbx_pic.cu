@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
         if (i0 + k < n && !keep[k]) {
           ++removed;
           first_out = min(first_out, dest[k]);
-          if (kSort) {   // order is not kept in sorted mode: O(removed) hole filling
+          if (p.removed_list) {   // order not kept: O(removed) hole filling
             const unsigned long long slot = atomicAdd(&p.st->removed_count, 1ull);
             if ((long long)slot < p.removed_cap) p.removed_list[slot] = dest[k];
           }
@@ -961,7 +961,8 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
     ctx->pic_sort_next = nullptr;
   }
   const long long rcap = std::max(1ll << 20, (long long)(ctx->n_upper / 64));
-  if (sorted && (!ctx->pic_fill || ctx->pic_fill_cap < rcap)) {
+  const bool fill = sorted || !(a->flags & LBX_PIC_STABLE_ORDER);
+  if (fill && (!ctx->pic_fill || ctx->pic_fill_cap < rcap)) {
     if (ctx->pic_fill) {
       cudaDeviceSynchronize();
       cudaFree(ctx->pic_fill);
@@ -993,8 +994,8 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   p.ouy = out[4];
   p.cell_cnt = cell_cnt;
   p.cursor = cursor;
-  p.removed_list = sorted ? ctx->pic_fill : nullptr;
-  p.removed_cap = sorted ? ctx->pic_fill_cap : 0;
+  p.removed_list = fill ? ctx->pic_fill : nullptr;
+  p.removed_cap = fill ? ctx->pic_fill_cap : 0;
   for (int c = 0; c < 6; ++c) p.Q[c] = Q + c * quads;
   for (int c = 0; c < 6; ++c) p.F[c] = a->fields[c];
   p.pitch = a->nx + 2;
@@ -1065,7 +1066,7 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   kern<<<(unsigned)grid, kPB, smem, s>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "pic_push_kernel launch");
-  if (sorted) {
+  if (fill) {
     const long long fc = ctx->pic_fill_cap;
     const unsigned fg2 = (unsigned)std::max(1, ctx->num_sms * 2);
     pic_fill_mark_kernel<<<fg2, 256, 0, s>>>(ctx->st, ctx->pic_fill, fc, ctx->pic_fill + fc,

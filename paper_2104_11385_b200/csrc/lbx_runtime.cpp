@@ -316,7 +316,7 @@ int launch_step(lbx_sim* s, int64_t step, cudaStream_t st) {
     pa.dt = c.pic_dt;
     pa.w_particle = c.w_particle;
     pa.w_cell = c.w_cell;
-    pa.flags = c.cost_kind == LBX_COST_GPUCLOCK ? LBX_STEP_CLOCK : 0u;
+    pa.flags = (c.cost_kind == LBX_COST_GPUCLOCK ? LBX_STEP_CLOCK : 0u) | LBX_PIC_STABLE_ORDER;
     pa.counts_out = d.counts;
     pa.cost_out = d.cost;
     pa.clk_out = d.clk;

@@ -62,10 +62,11 @@ class PicState:
 
 def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times_w: float,
              dt: float, weights=(0.75, 0.25), clock=False, field_solve=True, sort=False,
-             gather=None):
+             gather=None, stable=False):
     """One PIC step; returns per-box counts / cost / clock and n.
 
-    sort=False: in place, particle order kept (compaction is stable).
+    sort=False: in place; absorbed particles' slots are filled from the tail
+    (O(absorbed)), or with stable=True the order is kept (stable compaction).
     sort=True: sort-on-write -- results land in a second buffer set grouped by
     each particle's cell at the start of the step, which the state then
     swaps in (order within a cell is not deterministic; values are)."""
@@ -88,6 +89,8 @@ def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times
     a.w_particle, a.w_cell = float(weights[0]), float(weights[1])
     a.flags = (_lib.LBX_STEP_CLOCK if clock else 0) | (0 if field_solve else
                                                         _lib.LBX_PIC_NO_FIELD_SOLVE)
+    if stable and not sort:
+        a.flags |= _lib.LBX_PIC_STABLE_ORDER
     if gather is not None:     # "quad" | "direct" (default: by particles per cell)
         a.flags |= {"quad": _lib.LBX_PIC_QUAD, "direct": _lib.LBX_PIC_DIRECT}[gather]
     a.counts_out, a.cost_out, a.clk_out = _lib.ptr(counts), _lib.ptr(cost), _lib.ptr(clk)
