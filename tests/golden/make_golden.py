@@ -196,7 +196,7 @@ def run_fixture():
     (OUT / "runs.json").write_text(json.dumps(out, indent=0, sort_keys=True))
 
 
-if __name__ == "__main__" and "--cli" not in sys.argv:
+if __name__ == "__main__" and not any(a.startswith("--cli") for a in sys.argv):
     print("reference lbsim", lbsim.__version__, "backend", lbsim.KERNEL_BACKEND)
     kernels_fixture()
     balancer_fixture()
@@ -232,5 +232,42 @@ def cli_fixture():
     (OUT / "cli.json").write_text(json.dumps(out, indent=1, sort_keys=True))
 
 
+FIT_POINTS = [(1, 812.5), (2, 431.0), (4, 239.25), (8, 137.75), (16, 84.0)]
+COMPARE_RUNS = {"dyn": ["--scenario", "mini", "--steps", "150"],
+                "sfc": ["--scenario", "mini", "--steps", "150", "--policy", "sfc"],
+                "none": ["--scenario", "mini", "--steps", "150", "--policy", "none"]}
+
+
+def cli_tools_fixture():
+    """Stdout of the reference CLI's `fit` and `compare` (lbsim/cli.py:328-371)
+    on fixed inputs: a nodes,walltime CSV and three mini runs."""
+    import contextlib
+    import io
+    import tempfile
+
+    from lbsim import cli
+    out = {"fit_points": FIT_POINTS, "compare_runs": list(COMPARE_RUNS.items())}
+    with tempfile.TemporaryDirectory() as d:
+        pts = Path(d) / "points.csv"
+        pts.write_text("nodes,walltime\n" + "".join(f"{n},{w}\n" for n, w in FIT_POINTS))
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            rc = cli.main(["fit", "--points", str(pts), "--e0", "0.3155", "--e0", "0.2"])
+        out["fit"] = {"rc": rc, "stdout": buf.getvalue()}
+        dirs = []
+        for name, argv in COMPARE_RUNS.items():
+            rd = Path(d) / name
+            cli.main(["run", *argv, "--out", str(rd)])
+            dirs.append(str(rd))
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            rc = cli.main(["compare", *dirs])
+        out["compare"] = {"rc": rc, "stdout": buf.getvalue()}
+    (OUT / "cli_tools.json").write_text(json.dumps(out, indent=1, sort_keys=True))
+
+
 if __name__ == "__main__" and "--cli" in sys.argv:
     cli_fixture()
+
+if __name__ == "__main__" and "--cli-tools" in sys.argv:
+    cli_tools_fixture()

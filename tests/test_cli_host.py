@@ -79,3 +79,30 @@ def test_cli_usage_errors(tmp_path):
     assert cli.main(["run", "--scenario", "nope", "--out", str(tmp_path)]) == 1
     assert cli.main(["replay"]) == 1
     assert cli.main(["bogus"]) == 1
+
+
+def test_fit_and_compare_match_reference_stdout(tmp_path, capsys):
+    """`fit` and `compare` (cli.py:328-371) print exactly what the reference
+    CLI printed on the same inputs (tests/golden/cli_tools.json); the run
+    directories come from our writers over oracle runs (byte-identical to the
+    reference's, test above)."""
+    from paper_2104_11385_b200 import cli
+    want = json.loads((G / "cli_tools.json").read_text())
+    pts = tmp_path / "points.csv"
+    pts.write_text("nodes,walltime\n" + "".join(f"{n},{w}\n" for n, w in want["fit_points"]))
+    capsys.readouterr()
+    assert cli.main(["fit", "--points", str(pts), "--e0", "0.3155", "--e0", "0.2"]) == 0
+    assert capsys.readouterr().out == want["fit"]["stdout"]
+    dirs = []
+    for name, argv in want["compare_runs"]:      # in the reference's order
+        cfg = O.config_from_doc(preset_doc("mini"))
+        cfg["steps"] = int(argv[argv.index("--steps") + 1])
+        if "--policy" in argv:
+            cfg = O.apply_policy(cfg, argv[argv.index("--policy") + 1])
+        d = tmp_path / name
+        cli.write_run_outputs(d, result_from_oracle(cfg, name))
+        dirs.append(str(d))
+    capsys.readouterr()
+    assert cli.main(["compare", *dirs]) == 0
+    assert capsys.readouterr().out == want["compare"]["stdout"]
+    assert cli.main(["compare", dirs[0]]) == 1          # needs two runs (usage error)
