@@ -14,6 +14,9 @@
 //     (load_other - c_b) + c_a exactly as balancer.py:163-164 does.
 
 #include <algorithm>
+#if defined(__AVX2__)
+#include <immintrin.h>
+#endif
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -63,13 +66,72 @@ void loads_of(const double* cost, const int64_t* owner, int64_t n, int32_t R, do
 // balancer.py:137-179.  Only swaps that involve the unique most-loaded rank
 // can lower the maximum; best strict improvement wins, ties to the lowest
 // own box id, then the lowest partner box id.
+// Best improving partner of box a (value ca) among `others`: the lowest j with
+// the smallest pair max max(here0 + cb_j, (L_j - cb_j) + ca) < top -- the
+// reference's per-box search (balancer.py:157-170, np.argmin = first index),
+// with d_j = L_j - cb_j precomputed exactly as the reference evaluates it.
+static inline int64_t best_partner(const double* cb, const double* d, int64_t no, double here0,
+                                   double ca, double top, double* pm_out) {
+  int64_t jbest = -1;
+  double pm_best = 0.0;
+  int64_t j0 = 0;
+#if defined(__AVX2__)
+  // 4 lanes, each keeping its FIRST minimum (strict <); merged by value then
+  // index -- the same j as the scalar scan.  max(here, there) of equal values
+  // may differ only in the sign of a zero, which no comparison sees.
+  if (no >= 8) {
+    const __m256d vh0 = _mm256_set1_pd(here0), vca = _mm256_set1_pd(ca);
+    const __m256d vtop = _mm256_set1_pd(top);
+    const __m256d vinf = _mm256_set1_pd(std::numeric_limits<double>::infinity());
+    __m256d vmin = vinf;
+    __m256i vidx = _mm256_set1_epi64x(-1);
+    __m256i vj = _mm256_setr_epi64x(0, 1, 2, 3);
+    const __m256i v4 = _mm256_set1_epi64x(4);
+    for (; j0 + 4 <= no; j0 += 4) {
+      const __m256d here = _mm256_add_pd(vh0, _mm256_loadu_pd(cb + j0));
+      const __m256d there = _mm256_add_pd(_mm256_loadu_pd(d + j0), vca);
+      __m256d pm = _mm256_max_pd(here, there);
+      pm = _mm256_blendv_pd(vinf, pm, _mm256_cmp_pd(pm, vtop, _CMP_LT_OQ));
+      const __m256d better = _mm256_cmp_pd(pm, vmin, _CMP_LT_OQ);
+      vmin = _mm256_blendv_pd(vmin, pm, better);
+      vidx = _mm256_castpd_si256(_mm256_blendv_pd(_mm256_castsi256_pd(vidx),
+                                                  _mm256_castsi256_pd(vj), better));
+      vj = _mm256_add_epi64(vj, v4);
+    }
+    alignas(32) double m[4];
+    alignas(32) long long ix[4];
+    _mm256_store_pd(m, vmin);
+    _mm256_store_si256(reinterpret_cast<__m256i*>(ix), vidx);
+    for (int l = 0; l < 4; ++l) {
+      if (ix[l] < 0) continue;
+      if (jbest < 0 || m[l] < pm_best || (m[l] == pm_best && ix[l] < jbest)) {
+        jbest = ix[l];
+        pm_best = m[l];
+      }
+    }
+  }
+#endif
+  for (int64_t j = j0; j < no; ++j) {   // tail (or everything without AVX2)
+    const double here = here0 + cb[j];
+    const double there = d[j] + ca;
+    const double pm = here >= there ? here : there;
+    if (pm < top && (jbest < 0 || pm < pm_best)) {
+      jbest = j;
+      pm_best = pm;
+    }
+  }
+  *pm_out = pm_best;
+  return jbest;
+}
+
 void refine_by_swaps(int64_t* owner, double* loads, const double* v, int64_t n, int32_t R) {
   if (R < 2 || n < 2) return;
   std::vector<int64_t> mine, others;
-  std::vector<double> other_load;
+  std::vector<double> cb, d;
   mine.reserve(n);
   others.reserve(n);
-  other_load.reserve(n);
+  cb.reserve(n);
+  d.reserve(n);
   while (true) {
     double top = loads[0];
     for (int32_t r = 1; r < R; ++r) top = std::max(top, loads[r]);
@@ -82,44 +144,38 @@ void refine_by_swaps(int64_t* owner, double* loads, const double* v, int64_t n, 
     if (at_top != 1) return;
     mine.clear();
     others.clear();
-    other_load.clear();
+    cb.clear();
+    d.clear();
     for (int64_t b = 0; b < n; ++b) {
       if (owner[b] == rmax) {
         mine.push_back(b);
       } else {
         others.push_back(b);
-        other_load.push_back(loads[owner[b]]);
+        cb.push_back(v[b]);
+        d.push_back(loads[owner[b]] - v[b]);
       }
     }
     if (mine.empty() || others.empty()) return;
-    bool have = false;
-    double best_pm = 0.0;
-    int64_t best_a = -1, best_b = -1;
-    const int64_t no = (int64_t)others.size();
-    for (int64_t a : mine) {
-      const double ca = v[a];
-      const double here0 = top - ca;
-      int64_t jbest = -1;
-      double pm_best = 0.0;
-      for (int64_t j = 0; j < no; ++j) {
-        const double cb = v[others[j]];
-        const double here = here0 + cb;
-        const double there = (other_load[j] - cb) + ca;
-        const double pm = here >= there ? here : there;
-        if (pm < top && (jbest < 0 || pm < pm_best)) {
-          jbest = j;
-          pm_best = pm;
-        }
-      }
-      if (jbest < 0) continue;
-      if (!have || pm_best < best_pm) {
-        have = true;
-        best_pm = pm_best;
-        best_a = a;
-        best_b = others[jbest];
+    const int64_t nm = (int64_t)mine.size(), no = (int64_t)others.size();
+    struct Best {
+      bool have = false;
+      double pm = 0.0;
+      int64_t ia = -1, j = -1;
+    } best;
+    for (int64_t ia = 0; ia < nm; ++ia) {
+      const double ca = v[mine[ia]];
+      double pm;
+      const int64_t j = best_partner(cb.data(), d.data(), no, top - ca, ca, top, &pm);
+      if (j < 0) continue;
+      if (!best.have || pm < best.pm) {
+        best.have = true;
+        best.pm = pm;
+        best.ia = ia;
+        best.j = j;
       }
     }
-    if (!have) return;
+    if (!best.have) return;
+    const int64_t best_a = mine[best.ia], best_b = others[best.j];
     const int64_t rb = owner[best_b];
     loads[rmax] += v[best_b] - v[best_a];
     loads[rb] += v[best_a] - v[best_b];
