@@ -1277,7 +1277,10 @@ namespace {
 // Host-buffer pipeline state (lbx_advance_bin_host), cached in ctx: kLanes
 // streams, each with its own device chunk buffers and look-back state.
 struct HostPipe {
-  static constexpr long long kChunk = 1ll << 22;  // 4 Mi particles per chunk
+#ifndef LBX_HOST_CHUNK_LOG2
+#define LBX_HOST_CHUNK_LOG2 22
+#endif
+  static constexpr long long kChunk = 1ll << LBX_HOST_CHUNK_LOG2;  // 4 Mi particles per chunk
   static constexpr int kLanes = 3;
   cudaStream_t s[kLanes] = {};
   cudaEvent_t ready = {};
