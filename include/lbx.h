@@ -53,6 +53,9 @@ int lbx_ctx_destroy(lbx_ctx* ctx);
 int lbx_ctx_reserve(lbx_ctx* ctx, int64_t capacity);
 /* Stream-ordered: set / read the device-resident live particle count. */
 int lbx_ctx_set_count(lbx_ctx* ctx, int64_t n, void* stream);
+/* Host-side upper bound on the live count (launch sizing) without touching
+ * the device count -- for loops whose count changes on the device only. */
+int lbx_ctx_set_upper(lbx_ctx* ctx, int64_t n_upper);
 int lbx_ctx_get_count(lbx_ctx* ctx, int64_t* n_host, void* stream); /* syncs */
 /* Persistent-grid size the step kernels launch with (0 = auto: resident
  * CTAs per SM x SMs). */
@@ -456,6 +459,19 @@ int lbx_partition(lbx_ctx* ctx, double* z, double* x, double* vz, double* vx,
 int lbx_fill_holes(lbx_ctx* ctx, double* z, double* x, double* vz, double* vx,
                    double* kick_vz, double* kick_vx, const int64_t* removed,
                    int64_t n_removed, int64_t n_new, void* stream);
+/* Device-count variants for a pipelined loop (no host round trip per step):
+ * lbx_fill_holes_dev takes L = removals listed by the preceding exchange
+ * push (<= removed_cap) and n_new from the device state, and recognises
+ * removed tail slots by their position (outside the domain, or the emigrant
+ * sentinel z = -1); lbx_unpack_peer_dev appends the records peers wrote
+ * into `recv` (count = the rank's own cursor, then reset to 0) at the
+ * device live count, bounded by `capacity` (overflow sets the error word). */
+int lbx_fill_holes_dev(lbx_ctx* ctx, double* z, double* x, double* vz, double* vx,
+                       double* kick_vz, double* kick_vx, const int64_t* removed,
+                       int64_t removed_cap, double extent_z, double extent_x, void* stream);
+int lbx_unpack_peer_dev(lbx_ctx* ctx, const double* recv, uint64_t* cursor, int64_t capacity,
+                        double* z, double* x, double* vz, double* vx, double* kick_vz,
+                        double* kick_vx, void* stream);
 /* Group `count` staged records by destination into `send` ([count][6]);
  * cursors[world] (device) holds each destination's first slot on entry. */
 int lbx_group_by_dest(const double* stage, const int32_t* stage_dest, int64_t count,

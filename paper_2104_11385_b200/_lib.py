@@ -140,6 +140,9 @@ class PicArgs(C.Structure):
 
 SIGNATURES["lbx_pic_step"] = (i32, [vp, P(PicArgs), vp])
 SIGNATURES["lbx_peer_alloc"] = (i32, [i64, P(vp), vp])
+SIGNATURES["lbx_ctx_set_upper"] = (i32, [vp, i64])
+SIGNATURES["lbx_fill_holes_dev"] = (i32, [vp, vp, vp, vp, vp, vp, vp, vp, i64, f64, f64, vp])
+SIGNATURES["lbx_unpack_peer_dev"] = (i32, [vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp])
 SIGNATURES["lbx_peer_open"] = (i32, [vp, P(vp)])
 SIGNATURES["lbx_peer_close"] = (i32, [vp])
 SIGNATURES["lbx_peer_free"] = (i32, [vp])

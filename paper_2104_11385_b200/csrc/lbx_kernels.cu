@@ -1138,6 +1138,86 @@ __global__ void fill_done_kernel(DevState* st, long long n_new) {
   st->first_leaver = LLONG_MAX;
 }
 
+// Device-count variants (pipelined multi-GPU loop: no host round trip).
+// The push epilogue left st->n = survivors kept in place and st->removed_count
+// = L listed removals; a tail slot in [n, n + L) is removed iff its position
+// is outside the domain (absorbed) or carries the emigrant sentinel z = -1.
+__global__ void fill_dev_mark_kernel(DevState* st, const long long* __restrict__ removed,
+                                     long long cap, long long* holes) {
+  const long long L = min((long long)st->removed_count, cap), n_new = st->n;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < L;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long r = removed[k];
+    if (r < n_new) holes[atomicAdd(&st->holes, 1ull)] = r;
+  }
+}
+
+__global__ void fill_dev_move_kernel(DevState* st, long long cap, const long long* __restrict__ holes,
+                                     double ez, double ex, double* z, double* x, double* vz,
+                                     double* vx, double* kvz, double* kvx) {
+  const long long L = min((long long)st->removed_count, cap), n_new = st->n;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < L;
+       j += (long long)gridDim.x * blockDim.x) {
+    const long long src = n_new + j;
+    if (!inside(z[src], x[src], ez, ex)) continue;   // removed tail slot
+    const long long dst = holes[atomicAdd(&st->movers, 1ull)];
+    z[dst] = z[src];
+    x[dst] = x[src];
+    vz[dst] = vz[src];
+    vx[dst] = vx[src];
+    if (kvz) {
+      kvz[dst] = kvz[src];
+      kvx[dst] = kvx[src];
+    }
+  }
+}
+
+__global__ void fill_dev_done_kernel(DevState* st, long long cap) {
+  if ((long long)st->removed_count > cap) st->err |= 1ll << 61;   // list overflowed
+  st->n_old = st->n;
+  st->holes = 0ull;
+  st->movers = 0ull;
+  st->removed_count = 0ull;
+  st->leavers = 0ull;
+  st->first_leaver = LLONG_MAX;
+}
+
+// Append the records peers wrote into this rank's receive buffer; the count
+// is the rank's own cursor (device), the offset the device live count.
+__global__ void unpack_dev_kernel(const double* __restrict__ recv,
+                                  const unsigned long long* cursor, const DevState* st,
+                                  long long capacity, double* z, double* x, double* vz,
+                                  double* vx, double* kvz, double* kvx) {
+  const long long off = st->n;
+  const long long m = min((long long)*cursor, capacity - off);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double2* r = reinterpret_cast<const double2*>(recv + i * 6);
+    const double2 a = r[0], b = r[1], c = r[2];
+    z[off + i] = a.x;
+    x[off + i] = a.y;
+    vz[off + i] = b.x;
+    vx[off + i] = b.y;
+    if (kvz) {
+      kvz[off + i] = c.x;
+      kvx[off + i] = c.y;
+    }
+  }
+}
+
+__global__ void unpack_dev_done_kernel(DevState* st, unsigned long long* cursor,
+                                       long long capacity) {
+  const long long m = (long long)*cursor;
+  long long n = st->n + m;
+  if (n > capacity) {
+    st->err |= 1ll << 60;   // more immigrants than capacity
+    n = capacity;
+  }
+  st->n = n;
+  st->n_old = n;
+  *cursor = 0ull;
+}
+
 __global__ void counts_cost_kernel(const long long* __restrict__ counts, int nb, double wp,
                                    double wc, double cells, double* __restrict__ cost) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1614,6 +1694,15 @@ int lbx_ctx_set_count(lbx_ctx* ctx, int64_t n, void* stream) {
   return LBX_OK;
 }
 
+int lbx_ctx_set_upper(lbx_ctx* ctx, int64_t n_upper) {
+  clear_error();
+  if (!ctx || n_upper < 0) return set_error(LBX_EINVAL, "bad argument");
+  int rc = reserve_status(ctx, n_upper);
+  if (rc) return rc;
+  ctx->n_upper = n_upper;
+  return LBX_OK;
+}
+
 int lbx_ctx_get_count(lbx_ctx* ctx, int64_t* n_host, void* stream) {
   clear_error();
   if (!ctx || !n_host) return set_error(LBX_EINVAL, "NULL argument");
@@ -1994,6 +2083,55 @@ int lbx_fill_holes(lbx_ctx* ctx, double* z, double* x, double* vz, double* vx, d
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "fill_holes launch");
   ctx->n_upper = n_new;
+  return LBX_OK;
+}
+
+int lbx_fill_holes_dev(lbx_ctx* ctx, double* z, double* x, double* vz, double* vx,
+                       double* kick_vz, double* kick_vx, const int64_t* removed,
+                       int64_t removed_cap, double extent_z, double extent_x, void* stream) {
+  clear_error();
+  if (!ctx || !removed || removed_cap < 0) return set_error(LBX_EINVAL, "bad argument");
+  if ((kick_vz == nullptr) != (kick_vx == nullptr))
+    return set_error(LBX_EINVAL, "kick velocity buffers must be given together");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (ctx->fill_cap < removed_cap) {
+    if (ctx->fill_scratch) {
+      cudaStreamSynchronize(s);
+      cudaFree(ctx->fill_scratch);
+    }
+    ctx->fill_scratch = nullptr;
+    const int64_t cap = std::max<int64_t>(removed_cap, 1 << 16);
+    if (cudaMalloc(&ctx->fill_scratch, (size_t)cap * 16) != cudaSuccess)
+      return set_error(LBX_EOOM, "hole-fill scratch");
+    cudaMemsetAsync(ctx->fill_scratch + cap, 0, (size_t)cap * 8, s);
+    ctx->fill_cap = cap;
+  }
+  const unsigned grid = (unsigned)std::max(1, ctx->num_sms * 4);
+  fill_dev_mark_kernel<<<grid, 256, 0, s>>>(ctx->st, reinterpret_cast<const long long*>(removed),
+                                            removed_cap, ctx->fill_scratch);
+  fill_dev_move_kernel<<<grid, 256, 0, s>>>(ctx->st, removed_cap, ctx->fill_scratch, extent_z,
+                                            extent_x, z, x, vz, vx, kick_vz, kick_vx);
+  fill_dev_done_kernel<<<1, 1, 0, s>>>(ctx->st, removed_cap);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "fill_holes_dev launch");
+  return LBX_OK;
+}
+
+int lbx_unpack_peer_dev(lbx_ctx* ctx, const double* recv, uint64_t* cursor, int64_t capacity,
+                        double* z, double* x, double* vz, double* vx, double* kick_vz,
+                        double* kick_vx, void* stream) {
+  clear_error();
+  if (!ctx || !recv || !cursor || capacity < 0) return set_error(LBX_EINVAL, "bad argument");
+  if ((kick_vz == nullptr) != (kick_vx == nullptr))
+    return set_error(LBX_EINVAL, "kick velocity buffers must be given together");
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned grid = (unsigned)std::max(1, ctx->num_sms * 2);
+  unpack_dev_kernel<<<grid, 256, 0, s>>>(recv, reinterpret_cast<unsigned long long*>(cursor),
+                                         ctx->st, capacity, z, x, vz, vx, kick_vz, kick_vx);
+  unpack_dev_done_kernel<<<1, 1, 0, s>>>(ctx->st, reinterpret_cast<unsigned long long*>(cursor),
+                                         capacity);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "unpack_dev launch");
   return LBX_OK;
 }
 

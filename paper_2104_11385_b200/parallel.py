@@ -279,6 +279,42 @@ class DeviceEngine:
         self.cursor[parity].zero_()
         self.n += m
 
+    # -- pipelined loop (device-resident counts, no host round trip) ----
+    def begin_async(self):
+        self.ctx.set_count(self.n)     # the device count takes over from here
+        _lib.check(_lib.lib.lbx_ctx_set_upper(self.ctx.handle, self.capacity + 2))
+
+    def end_async(self):
+        self.n = self.ctx.count()      # the device count is authoritative again
+
+    def push_async(self, wp, wc):
+        """The exchange push on the device live count (no set_count), then
+        the hole filling of the removed slots, all stream-ordered."""
+        self.send_counts.zero_()
+        args = _lib.StepArgs(
+            _lib.ptr(self.z), _lib.ptr(self.x), _lib.ptr(self.vz), _lib.ptr(self.vx),
+            self.ez, self.ex, self.m, self.nbz, self.nbx, float(wp), float(wc),
+            self.m * self.m, _lib.LBX_STEP_CLOCK if self.clock else 0,
+            _lib.ptr(self.counts), _lib.ptr(self.cost), _lib.ptr(self.clk),
+            _lib.ptr(self.nout), _lib.ptr(self.nout[1:]))
+        ex = self._ex()
+        st = self.D._stream(self.dev)
+        _lib.check(_lib.lib.lbx_push_step_exchange(self.ctx.handle, C.byref(args), C.byref(ex), st))
+        _lib.check(_lib.lib.lbx_fill_holes_dev(
+            self.ctx.handle, _lib.ptr(self.z), _lib.ptr(self.x), _lib.ptr(self.vz),
+            _lib.ptr(self.vx), _lib.ptr(self.kvz), _lib.ptr(self.kvx), _lib.ptr(self.removed),
+            self.capacity + 2, self.ez, self.ex, st))
+        self.launches += 5   # stream kernel, fill mark / move / done
+        return self.counts, self.clk, self.send_counts, self.nout
+
+    def unpack_peer_async(self, parity: int):
+        _lib.check(_lib.lib.lbx_unpack_peer_dev(
+            self.ctx.handle, C.c_void_p(self.recv_base[parity]),
+            C.c_void_p(int(self.cursor[parity].data_ptr())), self.capacity,
+            _lib.ptr(self.z), _lib.ptr(self.x), _lib.ptr(self.vz), _lib.ptr(self.vx),
+            _lib.ptr(self.kvz), _lib.ptr(self.kvx), self.D._stream(self.dev)))
+        self.launches += 2
+
     def _ex(self):
         a = _lib.ExchangeArgs(
             _lib.ptr(self.owner), self.rank, self.world, _lib.ptr(self.stage),
@@ -534,7 +570,7 @@ class DistributedSimulation:
     def __init__(self, cfg, policy, provider, *, comm=None, engine_factory=None,
                  positions=None, kick=None, device=None, capacity=None,
                  record_counts=False, replicas=1, physics="surrogate", pic=None,
-                 exchange="auto"):
+                 exchange="auto", pipeline=True):
         self.comm = comm or TorchComm()
         self.rank, self.world = self.comm.rank, self.comm.world
         if cfg.n_ranks != self.world:
@@ -574,6 +610,12 @@ class DistributedSimulation:
         self.exchange = self._choose_exchange(exchange)
         if self.exchange == "p2p":
             self._enable_p2p(exchange == "p2p")
+        # pipelined loop: the GPU runs the next step while the host does this
+        # step's LB bookkeeping; needs the fused exchange (device-resident
+        # counts) and no capacity model (an OOM halt must stop at its step)
+        self.pipeline = bool(pipeline and self.exchange == "p2p"
+                             and hasattr(self.engine, "push_async")
+                             and physics == "surrogate" and cfg.capacity_particles is None)
         self.conf = sim_config(cfg, policy, provider)
         h = C.c_void_p()
         own = np.ascontiguousarray(self.initial_owner, dtype=np.int64)
@@ -722,13 +764,17 @@ class DistributedSimulation:
         """Steps [first, last).  Per step: push (no host sync), one all-reduce
         of [counts, clock tally, global emigrant count], one all-to-all of
         per-destination counts, ONE device->host copy, then the record
-        all-to-all only if some rank has emigrants, then the host LB step."""
+        all-to-all only if some rank has emigrants, then the host LB step.
+        With the fused peer-memory exchange the loop is pipelined instead
+        (`_run_pipelined`)."""
         cfg = self.cfg
         first = self.done if first is None else first
         last = cfg.total_steps if last is None else last
         w = getattr(self.provider, "weights", None)
         wp, wc = (w.w_particle, w.w_cell) if w else (0.75, 0.25)
         clock = self.provider.device_kind == 3
+        if self.pipeline:
+            return self._run_pipelined(first, last, wp, wc, clock)
         nb, W = self.ba.n_boxes, self.world
         adopted, halt = C.c_int32(), C.c_int32()
         for step in range(first, last):
@@ -771,6 +817,72 @@ class DistributedSimulation:
             self.done = step + 1
             if halt.value:
                 self.halted = True
+        return self
+
+    def _run_pipelined(self, first, last, wp, wc, clock):
+        """Per step, all stream-ordered with no host round trip: fused push
+        (emigrants written into the owners' buffers, removed slots listed),
+        device-count hole filling, all-reduce of [counts, clock, emigrants]
+        (which also orders every sender's writes before the owner reads),
+        append of the received records at the device count, and an async
+        copy of the reduced vector to pinned memory.  The host runs the LB
+        step of step s while the GPU works on step s + 1; it catches up
+        before launching past an attempt step (an adoption changes the owner
+        table the next push uses) and migrates synchronously on adoption."""
+        from collections import deque
+
+        from .balancer import should_attempt
+
+        cfg, eng, nb = self.cfg, self.engine, self.ba.n_boxes
+        adopted, halt = C.c_int32(), C.c_int32()
+        eng.begin_async()
+        pend = deque()
+
+        def process(step, host, ev):
+            ev.synchronize()
+            h = host.numpy()
+            k = (2 if clock else 1) * nb
+            if int(h[k + 2]):
+                raise ValueError(f"rank {self.rank}: particles outside the box grid, staging "
+                                 f"or receive overflow (code {int(h[k + 2])})")
+            ch = np.ascontiguousarray(h[:nb], dtype=np.int64)
+            kh = np.ascontiguousarray(h[nb:2 * nb]).view(np.uint64) if clock else None
+            _lib.check(_lib.lib.lbx_lb_step(self.lb, step, _lib.ptr(ch), _lib.ptr(kh),
+                                            int(ch.sum()), C.byref(self.souts),
+                                            C.byref(adopted), C.byref(halt)))
+            if adopted.value:
+                owner = np.empty(nb, dtype=np.int64)
+                _lib.check(_lib.lib.lbx_lb_owner(self.lb, _lib.ptr(owner)))
+                eng.end_async()                       # host count for the sync migration
+                eng.set_owner(owner)
+                self.moved[step] = self._migrate_p2p(step)
+                eng.begin_async()
+            self.done = step + 1
+            if halt.value:
+                self.halted = True
+
+        for step in range(first, last):
+            if self.halted:
+                break
+            if step == cfg.kick.step:
+                eng.kick()
+            eng.parity = step & 1
+            counts, clk, send_counts, nout = eng.push_async(wp, wc)
+            parts = [counts, clk] if clock else [counts]
+            red = torch.cat(parts + [send_counts.sum().reshape(1)])
+            self.comm.all_reduce_sum(red)
+            eng.unpack_peer_async(step & 1)
+            host = torch.empty(red.numel() + 2, dtype=torch.int64, pin_memory=True)
+            host.copy_(torch.cat([red, nout]), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            pend.append((step, host, ev))
+            attempt = should_attempt(self.policy, step, cfg.total_steps)
+            while pend and (len(pend) > 1 or attempt):
+                process(*pend.popleft())
+        while pend:
+            process(*pend.popleft())
+        eng.end_async()
         return self
 
     def local_state(self):
