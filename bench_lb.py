@@ -145,7 +145,8 @@ def run_emulated(R, steps, replicas, policy, speed=0.035, drift=0.01, strategy="
                                         positions=pos, kick=kick, device="cuda:0",
                                         replicas=replicas,
                                         capacity=pos.shape[0] * replicas + 4096,
-                                        physics=physics, exchange=exchange)
+                                        physics=physics, exchange=exchange,
+                                        pipeline=False)   # ranks' pushes timed one by one
             sim.run()
             sims[r] = sim
         except Exception as e:
