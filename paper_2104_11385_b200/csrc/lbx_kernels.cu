@@ -49,7 +49,13 @@ constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 constexpr int kItems = 8;                 // particles per thread per scan tile
 constexpr int kTile = kBlock * kItems;    // 2048 particles per scan tile
-constexpr int kPairs = 2;                 // 16-byte pairs per thread per push iteration
+#ifndef LBX_PAIRS
+#define LBX_PAIRS 2
+#endif
+#ifndef LBX_STREAM_MINB
+#define LBX_STREAM_MINB 4
+#endif
+constexpr int kPairs = LBX_PAIRS;         // 16-byte pairs per thread per push iteration
 constexpr int kSmemBoxesMax = 12288;      // shared-memory histogram limit (96 KB)
 constexpr int kFlushIters = 128;          // push iterations between histogram flushes
 constexpr unsigned kFull = 0xffffffffu;
@@ -241,7 +247,7 @@ __device__ __forceinline__ void stage_emigrant(const StepParams& p, bool em, lon
 }
 
 template <bool kClock, bool kPow2, bool kExch, bool kPush>
-__global__ void __launch_bounds__(kBlock, 4) stream_kernel(StepParams p) {
+__global__ void __launch_bounds__(kBlock, LBX_STREAM_MINB) stream_kernel(StepParams p) {
   constexpr bool kHist = kPush;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned* s_cnt = reinterpret_cast<unsigned*>(smem_raw);
