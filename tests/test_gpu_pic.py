@@ -209,3 +209,32 @@ def test_in_place_hole_filling_matches_oracle_multiset():
     fa = st.field_arrays()
     for k in PO.OFFSETS:
         assert np.array_equal(fa[k], f[k]), k
+
+
+def test_pic_gpuclock_rank_correlates_with_work():
+    """GpuClock tallies of the PIC kernel are a work proxy: across boxes they
+    rank-correlate with the particle counts (Spearman > 0.9)."""
+    from paper_2104_11385_b200 import device, pic
+    rng = np.random.default_rng(8)
+    nz = nx = 128
+    # box densities spanning two orders of magnitude, spatially sorted
+    M = 16
+    dens = rng.integers(1, 200, size=(nz // M, nx // M))
+    parts = []
+    for bi in range(nz // M):
+        for bj in range(nx // M):
+            k = int(dens[bi, bj]) * 40
+            parts.append(np.column_stack([bi * M + rng.uniform(0, M, k), bj * M + rng.uniform(0, M, k)]))
+    pos = np.concatenate(parts)
+    pos = pos[np.lexsort((pos[:, 1], np.floor(pos[:, 0])))]
+    u = rng.normal(0, 0.05, size=(pos.shape[0], 3))
+    ctx = device.Context(capacity=pos.shape[0])
+    st = pic.PicState.create(pos, u, nz, nx)
+    rho = []
+    for _ in range(3):
+        out = pic.pic_step(ctx, st, M, -1.0, -1e-3, 0.5, clock=True)
+        c, k = out["counts"].astype(float), out["clock"].astype(float)
+        rc = np.argsort(np.argsort(c))
+        rk = np.argsort(np.argsort(k))
+        rho.append(np.corrcoef(rc, rk)[0, 1])
+    assert min(rho) > 0.9, rho
