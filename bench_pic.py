@@ -12,6 +12,8 @@ launch stream:
                         deposit + counts/clock + compaction + cell-slot scan;
   push_deposit_inplace  the same in place (order kept, no sorting: the
                         deposit's cell runs decay as particles drift);
+  push_deposit_noclock  sorted mode without the GpuClock tally (its overhead
+                        is gpuclock_overhead = push_deposit / this - 1);
   full_step             sorted mode plus the Yee update.
 Roofline: HBM, algorithmic bytes = 80 B per particle (read z,x,uz,ux,uy +
 write them, float64) -- field patch and current flush traffic is counted
@@ -83,21 +85,23 @@ def main():
     peak, peak_src = bench.peaks()
     out = {"workload": label, "particles": n}
     stream = torch.cuda.current_stream(dev)
-    for mode, solve, sort in (("push_deposit", False, True), ("push_deposit_inplace", False, False),
-                              ("full_step", True, True)):
+    for mode, solve, sort, clk in (("push_deposit", False, True, True),
+                                   ("push_deposit_inplace", False, False, True),
+                                   ("push_deposit_noclock", False, True, False),
+                                   ("full_step", True, True, True)):
         st = pic.PicState.create(pos0[:1], u0[:1], nz, nx, device=dev)
         for name, t in init.items():
             setattr(st, name, t.clone())
         st.n = n
         for _ in range(args.warmup):
-            pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=True, field_solve=solve,
+            pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=clk, field_solve=solve,
                          sort=sort)
         times = []
         for _ in range(args.steps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             n_before = st.n
             e0.record(stream)
-            pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=True, field_solve=solve,
+            pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=clk, field_solve=solve,
                          sort=sort)
             e1.record(stream)
             torch.cuda.synchronize(dev)
@@ -109,6 +113,7 @@ def main():
                      "pushes_per_s": nb / (ms / 1e3), "achieved_gbs": achieved,
                      "frac_of_hbm_peak": achieved / peak}
         del st
+    out["gpuclock_overhead"] = out["push_deposit"]["ms"] / out["push_deposit_noclock"]["ms"] - 1.0
     out["peak_gbs"] = peak
     out["peak_source"] = peak_src
     print(json.dumps(out))
