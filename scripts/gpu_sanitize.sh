@@ -1,0 +1,17 @@
+#!/bin/bash
+# compute-sanitizer (memcheck / racecheck / synccheck) over CI-sized cases of
+# every kernel family: fused push/bin/compaction, drop-in AoS path + host
+# pipeline, PIC (quad/direct, in place/sorted), multi-GPU exchange (p2p and
+# collectives, thread ranks).  Summaries -> gpurun_out/sanitize_*.log
+mkdir -p gpurun_out
+CASES_K='tests/test_gpu_kernels.py -k "fixture or known_answer or empty or (fused_step_matches_oracle and 300001) or non_power or (host_pipeline and 5000)"'
+CASES_P='tests/test_gpu_pic.py -k "first_step or (multi_step and clustered-quad) or sorted_mode_matches_oracle"'
+CASES_D='tests/test_gpu_dist.py -k "mini-2 and p2p"'
+for tool in memcheck racecheck synccheck; do
+  for grp in K P D; do
+    eval cases=\$CASES_$grp
+    eval timeout 1500 compute-sanitizer --tool $tool --error-exitcode 99 --target-processes all \
+      python -m pytest $cases -x -q -p no:cacheprovider > gpurun_out/sanitize_${tool}_$grp.log 2>&1
+    echo "$tool $grp rc=$?  $(grep -E 'ERROR SUMMARY|passed|failed' gpurun_out/sanitize_${tool}_$grp.log | tr '\n' ' ' | cut -c1-200)"
+  done
+done
