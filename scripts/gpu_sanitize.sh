@@ -9,7 +9,7 @@ CASES_P='tests/test_gpu_pic.py -k "first_step or (multi_step and clustered-quad)
 CASES_D='tests/test_gpu_dist.py -k "mini-2 and p2p"'
 CASES_E='tests/test_gpu_3d.py tests/test_gpu_pic.py -k "3d or hole_filling or (multi_step and direct) or gpuclock or timers"'
 CASES_R='tests/test_gpu_runs.py -k "timers or gpuclock"'
-for tool in memcheck racecheck synccheck; do
+for tool in ${SAN_TOOLS:-memcheck racecheck synccheck}; do
   for grp in ${SAN_GROUPS:-K P D E R}; do
     eval cases=\$CASES_$grp
     eval timeout 1500 compute-sanitizer --tool $tool --error-exitcode 99 --target-processes all \
