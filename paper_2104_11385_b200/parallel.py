@@ -825,63 +825,106 @@ class DistributedSimulation:
         device-count hole filling, all-reduce of [counts, clock, emigrants]
         (which also orders every sender's writes before the owner reads),
         append of the received records at the device count, and an async
-        copy of the reduced vector to pinned memory.  The host runs the LB
-        step of step s while the GPU works on step s + 1; it catches up
-        before launching past an attempt step (an adoption changes the owner
-        table the next push uses) and migrates synchronously on adoption."""
-        from collections import deque
+        copy of the reduced vector to pinned memory.
+
+        The host LB bookkeeping (cost vector, efficiency, knapsack / SFC
+        attempt, adoption gate, walltime model) runs in order on a worker
+        thread while this thread keeps the GPU fed, so even a multi-ms remap
+        never stalls the device.  An adoption decided at step s is applied
+        physically (owner table + particle migration) before step s + lag on
+        every rank -- a deterministic point, so the ranks' collectives stay
+        matched.  Ownership never changes a particle's push, and the per-box
+        counts are all-reduced over whichever ranks hold the particles, so
+        counts, costs, decisions and metrics are exactly those of the
+        synchronous loop (tests compare against the oracle)."""
+        import os
+        import queue
 
         from .balancer import should_attempt
 
         cfg, eng, nb = self.cfg, self.engine, self.ba.n_boxes
+        lag = max(1, int(os.environ.get("LBX_LB_LAG", "8")))
         adopted, halt = C.c_int32(), C.c_int32()
+        work = queue.Queue()
+        decided = {}                       # step -> adopted owner table
+        st = {"processed": first - 1, "err": None}
+        cv = threading.Condition()
+
+        def worker():
+            while True:
+                item = work.get()
+                if item is None:
+                    return
+                step, host, ev = item
+                try:
+                    ev.synchronize()
+                    h = host.numpy()
+                    k = (2 if clock else 1) * nb
+                    if int(h[k + 2]):
+                        raise ValueError(f"rank {self.rank}: particles outside the box grid, "
+                                         f"staging or receive overflow (code {int(h[k + 2])})")
+                    ch = np.ascontiguousarray(h[:nb], dtype=np.int64)
+                    kh = np.ascontiguousarray(h[nb:2 * nb]).view(np.uint64) if clock else None
+                    _lib.check(_lib.lib.lbx_lb_step(self.lb, step, _lib.ptr(ch), _lib.ptr(kh),
+                                                    int(ch.sum()), C.byref(self.souts),
+                                                    C.byref(adopted), C.byref(halt)))
+                    if adopted.value:
+                        owner = np.empty(nb, dtype=np.int64)
+                        _lib.check(_lib.lib.lbx_lb_owner(self.lb, _lib.ptr(owner)))
+                        decided[step] = owner
+                    self.done = step + 1
+                    if halt.value:
+                        self.halted = True
+                except Exception as e:  # noqa: BLE001 -- re-raised on the main thread
+                    st["err"] = e
+                with cv:
+                    st["processed"] = step
+                    cv.notify_all()
+
+        def wait_processed(step):
+            with cv:
+                cv.wait_for(lambda: st["processed"] >= step or st["err"] is not None)
+            if st["err"] is not None:
+                raise st["err"]
+
+        def apply(d, boundary):
+            """Adoption decided at step d, applied before step `boundary`."""
+            eng.end_async()                        # host count for the sync migration
+            eng.set_owner(decided.pop(d))
+            self.moved[d] = self._migrate_p2p(boundary - 1)
+            eng.begin_async()
+
+        th = threading.Thread(target=worker, name=f"lbx-lb-rank{self.rank}", daemon=True)
+        th.start()
         eng.begin_async()
-        pend = deque()
-
-        def process(step, host, ev):
-            ev.synchronize()
-            h = host.numpy()
-            k = (2 if clock else 1) * nb
-            if int(h[k + 2]):
-                raise ValueError(f"rank {self.rank}: particles outside the box grid, staging "
-                                 f"or receive overflow (code {int(h[k + 2])})")
-            ch = np.ascontiguousarray(h[:nb], dtype=np.int64)
-            kh = np.ascontiguousarray(h[nb:2 * nb]).view(np.uint64) if clock else None
-            _lib.check(_lib.lib.lbx_lb_step(self.lb, step, _lib.ptr(ch), _lib.ptr(kh),
-                                            int(ch.sum()), C.byref(self.souts),
-                                            C.byref(adopted), C.byref(halt)))
-            if adopted.value:
-                owner = np.empty(nb, dtype=np.int64)
-                _lib.check(_lib.lib.lbx_lb_owner(self.lb, _lib.ptr(owner)))
-                eng.end_async()                       # host count for the sync migration
-                eng.set_owner(owner)
-                self.moved[step] = self._migrate_p2p(step)
-                eng.begin_async()
-            self.done = step + 1
-            if halt.value:
-                self.halted = True
-
-        for step in range(first, last):
-            if self.halted:
-                break
-            if step == cfg.kick.step:
-                eng.kick()
-            eng.parity = step & 1
-            counts, clk, send_counts, nout = eng.push_async(wp, wc)
-            parts = [counts, clk] if clock else [counts]
-            red = torch.cat(parts + [send_counts.sum().reshape(1)])
-            self.comm.all_reduce_sum(red)
-            eng.unpack_peer_async(step & 1)
-            host = torch.empty(red.numel() + 2, dtype=torch.int64, pin_memory=True)
-            host.copy_(torch.cat([red, nout]), non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record()
-            pend.append((step, host, ev))
-            attempt = should_attempt(self.policy, step, cfg.total_steps)
-            while pend and (len(pend) > 1 or attempt):
-                process(*pend.popleft())
-        while pend:
-            process(*pend.popleft())
+        try:
+            for step in range(first, last):
+                if st["err"] is not None:
+                    raise st["err"]
+                d = step - lag
+                if d >= first and should_attempt(self.policy, d, cfg.total_steps):
+                    wait_processed(d)
+                    if d in decided:
+                        apply(d, step)
+                if step == cfg.kick.step:
+                    eng.kick()
+                eng.parity = step & 1
+                counts, clk, send_counts, nout = eng.push_async(wp, wc)
+                parts = [counts, clk] if clock else [counts]
+                red = torch.cat(parts + [send_counts.sum().reshape(1)])
+                self.comm.all_reduce_sum(red)
+                eng.unpack_peer_async(step & 1)
+                host = torch.empty(red.numel() + 2, dtype=torch.int64, pin_memory=True)
+                host.copy_(torch.cat([red, nout]), non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record()
+                work.put((step, host, ev))
+            wait_processed(last - 1)
+            for d in sorted(decided):              # adoptions of the last `lag` steps
+                apply(d, last)
+        finally:
+            work.put(None)
+            th.join()
         eng.end_async()
         return self
 
