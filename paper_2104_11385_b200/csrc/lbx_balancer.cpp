@@ -14,7 +14,7 @@
 //     (load_other - c_b) + c_a exactly as balancer.py:163-164 does.
 
 #include <algorithm>
-#if defined(__AVX2__)
+#if defined(__x86_64__)
 #include <immintrin.h>
 #endif
 #include <cmath>
@@ -70,56 +70,117 @@ void loads_of(const double* cost, const int64_t* owner, int64_t n, int32_t R, do
 // the smallest pair max max(here0 + cb_j, (L_j - cb_j) + ca) < top -- the
 // reference's per-box search (balancer.py:157-170, np.argmin = first index),
 // with d_j = L_j - cb_j precomputed exactly as the reference evaluates it.
-static inline int64_t best_partner(const double* cb, const double* d, int64_t no, double here0,
-                                   double ca, double top, double* pm_out) {
-  int64_t jbest = -1;
-  double pm_best = 0.0;
-  int64_t j0 = 0;
-#if defined(__AVX2__)
-  // 4 lanes, each keeping its FIRST minimum (strict <); merged by value then
-  // index -- the same j as the scalar scan.  max(here, there) of equal values
-  // may differ only in the sign of a zero, which no comparison sees.
-  if (no >= 8) {
-    const __m256d vh0 = _mm256_set1_pd(here0), vca = _mm256_set1_pd(ca);
-    const __m256d vtop = _mm256_set1_pd(top);
-    const __m256d vinf = _mm256_set1_pd(std::numeric_limits<double>::infinity());
-    __m256d vmin = vinf;
-    __m256i vidx = _mm256_set1_epi64x(-1);
-    __m256i vj = _mm256_setr_epi64x(0, 1, 2, 3);
-    const __m256i v4 = _mm256_set1_epi64x(4);
-    for (; j0 + 4 <= no; j0 += 4) {
-      const __m256d here = _mm256_add_pd(vh0, _mm256_loadu_pd(cb + j0));
-      const __m256d there = _mm256_add_pd(_mm256_loadu_pd(d + j0), vca);
-      __m256d pm = _mm256_max_pd(here, there);
-      pm = _mm256_blendv_pd(vinf, pm, _mm256_cmp_pd(pm, vtop, _CMP_LT_OQ));
-      const __m256d better = _mm256_cmp_pd(pm, vmin, _CMP_LT_OQ);
-      vmin = _mm256_blendv_pd(vmin, pm, better);
-      vidx = _mm256_castpd_si256(_mm256_blendv_pd(_mm256_castsi256_pd(vidx),
-                                                  _mm256_castsi256_pd(vj), better));
-      vj = _mm256_add_epi64(vj, v4);
-    }
-    alignas(32) double m[4];
-    alignas(32) long long ix[4];
-    _mm256_store_pd(m, vmin);
-    _mm256_store_si256(reinterpret_cast<__m256i*>(ix), vidx);
-    for (int l = 0; l < 4; ++l) {
-      if (ix[l] < 0) continue;
-      if (jbest < 0 || m[l] < pm_best || (m[l] == pm_best && ix[l] < jbest)) {
-        jbest = ix[l];
-        pm_best = m[l];
-      }
-    }
-  }
-#endif
-  for (int64_t j = j0; j < no; ++j) {   // tail (or everything without AVX2)
+static inline void partner_tail(const double* cb, const double* d, int64_t j0, int64_t no,
+                                double here0, double ca, double top, int64_t* jbest,
+                                double* pm_best) {
+  for (int64_t j = j0; j < no; ++j) {
     const double here = here0 + cb[j];
     const double there = d[j] + ca;
     const double pm = here >= there ? here : there;
-    if (pm < top && (jbest < 0 || pm < pm_best)) {
-      jbest = j;
-      pm_best = pm;
+    if (pm < top && (*jbest < 0 || pm < *pm_best)) {
+      *jbest = j;
+      *pm_best = pm;
     }
   }
+}
+
+// Merge per-lane first minima: smallest value, then smallest index -- the
+// scalar scan's first-index rule.  max(here, there) of equal values may
+// differ only in the sign of a zero, which no comparison sees.
+static inline void merge_lanes(const double* m, const long long* ix, int lanes, int64_t* jbest,
+                               double* pm_best) {
+  for (int l = 0; l < lanes; ++l) {
+    if (ix[l] < 0) continue;
+    if (*jbest < 0 || m[l] < *pm_best || (m[l] == *pm_best && ix[l] < *jbest)) {
+      *jbest = ix[l];
+      *pm_best = m[l];
+    }
+  }
+}
+
+#if defined(__x86_64__)
+__attribute__((target("avx512f"))) static int64_t best_partner_avx512(
+    const double* cb, const double* d, int64_t no, double here0, double ca, double top,
+    double* pm_out) {
+  int64_t jbest = -1;
+  double pm_best = 0.0;
+  int64_t j0 = 0;
+  const __m512d vh0 = _mm512_set1_pd(here0), vca = _mm512_set1_pd(ca), vtop = _mm512_set1_pd(top);
+  const __m512d vinf = _mm512_set1_pd(std::numeric_limits<double>::infinity());
+  __m512d vmin = vinf;
+  __m512i vidx = _mm512_set1_epi64(-1);
+  __m512i vj = _mm512_setr_epi64(0, 1, 2, 3, 4, 5, 6, 7);
+  const __m512i v8 = _mm512_set1_epi64(8);
+  for (; j0 + 8 <= no; j0 += 8) {
+    const __m512d here = _mm512_add_pd(vh0, _mm512_loadu_pd(cb + j0));
+    const __m512d there = _mm512_add_pd(_mm512_loadu_pd(d + j0), vca);
+    const __m512d pm = _mm512_max_pd(here, there);
+    const __mmask8 ok = _mm512_cmp_pd_mask(pm, vtop, _CMP_LT_OQ);
+    const __mmask8 better = _mm512_mask_cmp_pd_mask(ok, pm, vmin, _CMP_LT_OQ);
+    vmin = _mm512_mask_mov_pd(vmin, better, pm);
+    vidx = _mm512_mask_mov_epi64(vidx, better, vj);
+    vj = _mm512_add_epi64(vj, v8);
+  }
+  alignas(64) double m[8];
+  alignas(64) long long ix[8];
+  _mm512_store_pd(m, vmin);
+  _mm512_store_si512(reinterpret_cast<__m512i*>(ix), vidx);
+  merge_lanes(m, ix, 8, &jbest, &pm_best);
+  partner_tail(cb, d, j0, no, here0, ca, top, &jbest, &pm_best);
+  *pm_out = pm_best;
+  return jbest;
+}
+
+__attribute__((target("avx2"))) static int64_t best_partner_avx2(
+    const double* cb, const double* d, int64_t no, double here0, double ca, double top,
+    double* pm_out) {
+  int64_t jbest = -1;
+  double pm_best = 0.0;
+  int64_t j0 = 0;
+  const __m256d vh0 = _mm256_set1_pd(here0), vca = _mm256_set1_pd(ca), vtop = _mm256_set1_pd(top);
+  const __m256d vinf = _mm256_set1_pd(std::numeric_limits<double>::infinity());
+  __m256d vmin = vinf;
+  __m256i vidx = _mm256_set1_epi64x(-1);
+  __m256i vj = _mm256_setr_epi64x(0, 1, 2, 3);
+  const __m256i v4 = _mm256_set1_epi64x(4);
+  for (; j0 + 4 <= no; j0 += 4) {
+    const __m256d here = _mm256_add_pd(vh0, _mm256_loadu_pd(cb + j0));
+    const __m256d there = _mm256_add_pd(_mm256_loadu_pd(d + j0), vca);
+    __m256d pm = _mm256_max_pd(here, there);
+    pm = _mm256_blendv_pd(vinf, pm, _mm256_cmp_pd(pm, vtop, _CMP_LT_OQ));
+    const __m256d better = _mm256_cmp_pd(pm, vmin, _CMP_LT_OQ);
+    vmin = _mm256_blendv_pd(vmin, pm, better);
+    vidx = _mm256_castpd_si256(_mm256_blendv_pd(_mm256_castsi256_pd(vidx),
+                                                _mm256_castsi256_pd(vj), better));
+    vj = _mm256_add_epi64(vj, v4);
+  }
+  alignas(32) double m[4];
+  alignas(32) long long ix[4];
+  _mm256_store_pd(m, vmin);
+  _mm256_store_si256(reinterpret_cast<__m256i*>(ix), vidx);
+  merge_lanes(m, ix, 4, &jbest, &pm_best);
+  partner_tail(cb, d, j0, no, here0, ca, top, &jbest, &pm_best);
+  *pm_out = pm_best;
+  return jbest;
+}
+#endif
+
+// Best improving partner of box a (value ca) among `others`: the lowest j with
+// the smallest pair max max(here0 + cb_j, (L_j - cb_j) + ca) < top -- the
+// reference's per-box search (balancer.py:157-170, np.argmin = first index),
+// with d_j = L_j - cb_j precomputed exactly as the reference evaluates it.
+// Vectorised (AVX-512 or AVX2, chosen at run time) with per-lane first
+// minima merged by value then index: the same j as the scalar scan.
+static int64_t best_partner(const double* cb, const double* d, int64_t no, double here0,
+                            double ca, double top, double* pm_out) {
+#if defined(__x86_64__)
+  static const int isa = __builtin_cpu_supports("avx512f") ? 2 : __builtin_cpu_supports("avx2") ? 1 : 0;
+  if (isa == 2 && no >= 16) return best_partner_avx512(cb, d, no, here0, ca, top, pm_out);
+  if (isa == 1 && no >= 8) return best_partner_avx2(cb, d, no, here0, ca, top, pm_out);
+#endif
+  int64_t jbest = -1;
+  double pm_best = 0.0;
+  partner_tail(cb, d, 0, no, here0, ca, top, &jbest, &pm_best);
   *pm_out = pm_best;
   return jbest;
 }
