@@ -9,6 +9,8 @@ R-rank job, computed on one GPU).  For each strategy:
   gpuclock   the same kernel instantiated with the clock64 tally
   timers     per-box push launches timed with CUDA events (the paper's
              CUPTI-style strategy): box-sort + one launch per box
+  cupti      the same per-box launches timed by CUPTI kernel activity
+             records (the paper's actual mechanism)
   measured   the reference's simulated timer (true work x PCG64 jitter)
 
 Reported per strategy: mean fused-kernel time (CUDA events around each
@@ -44,7 +46,7 @@ def main():
     ap.add_argument("--ranks", type=int, default=8)
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--strategies", default="heuristic,gpuclock,timers,measured")
+    ap.add_argument("--strategies", default="heuristic,gpuclock,timers,cupti,measured")
     args = ap.parse_args()
 
     import torch
@@ -88,7 +90,7 @@ def main():
             work = true_work(res.count_trace[s], sc)
             e_true.append(efficiency(CostVector(values=work),
                                      DistributionMapping(owner=owner, n_ranks=args.ranks)))
-            if kind in ("gpuclock", "timers") and s % 10 == 0:
+            if kind in ("gpuclock", "timers", "cupti") and s % 10 == 0:
                 occ = res.count_trace[s] > 0
                 rho.append(spearman(res.cost_trace[s][occ], work[occ]))
         entry = {"step_ms_mean": step_ms,
@@ -110,6 +112,8 @@ def main():
         out["gpuclock_step_overhead"] = st["gpuclock"]["step_ms_mean"] / st["heuristic"]["step_ms_mean"] - 1
     if "heuristic" in st and "timers" in st:
         out["timers_step_overhead"] = st["timers"]["step_ms_mean"] / st["heuristic"]["step_ms_mean"] - 1
+    if "heuristic" in st and "cupti" in st:
+        out["cupti_step_overhead"] = st["cupti"]["step_ms_mean"] / st["heuristic"]["step_ms_mean"] - 1
     print(json.dumps(out))
 
 

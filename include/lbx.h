@@ -222,6 +222,11 @@ typedef struct lbx_sim lbx_sim;
 #define LBX_COST_TIMERS 4        /* per-box launches timed with CUDA events
                                     (the paper's CUPTI-style Timers); cost =
                                     microseconds per box                      */
+#define LBX_COST_CUPTI 5         /* the same per-box launches timed by CUPTI
+                                    kernel activity records (the paper's
+                                    actual Timers mechanism, PAPER.md:174-178;
+                                    libcupti is dlopen'ed on first use); cost
+                                    = microseconds per box                   */
 
 #define LBX_STRATEGY_KNAPSACK 0
 #define LBX_STRATEGY_SFC 1

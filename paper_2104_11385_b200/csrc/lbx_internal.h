@@ -108,4 +108,9 @@ int launch_timers_sort(const double* z, const double* x, long long n, double m, 
                        int phase);
 int launch_timers_push(double* z, double* x, const double* vz, const double* vx, const int* idx,
                        long long cnt, void* stream);
+// CUPTI activity-record timer (lbx_cupti.cpp).
+int cupti_acquire();
+void cupti_release();
+int cupti_stream(void* stream, uint32_t* id);
+int cupti_collect(uint32_t stream_id, int n, double* dur_ns);
 }  // namespace lbx

@@ -60,6 +60,10 @@ struct lbx_sim {
   unsigned long long* h_offsets = nullptr;  // pinned
   std::vector<cudaEvent_t> tb0, tb1;
   std::vector<double> timers;
+  // CUPTI strategy (cost_kind == LBX_COST_CUPTI): same per-box launches
+  bool cupti = false;
+  void* stream = nullptr;
+  std::vector<double> spans;
   // PIC physics
   float* fields[6] = {};
   float* current[3] = {};
@@ -102,12 +106,13 @@ int validate(const lbx_sim_config& c) {
   if (c.n_ranks < 1) return set_error(LBX_EINVAL, "n_ranks must be >= 1");
   if (c.total_steps < 1) return set_error(LBX_EINVAL, "total_steps must be >= 1");
   if (c.interval < 1) return set_error(LBX_EINVAL, "interval must be >= 1");
-  if (c.cost_kind < 0 || c.cost_kind > LBX_COST_TIMERS)
+  if (c.cost_kind < 0 || c.cost_kind > LBX_COST_CUPTI)
     return set_error(LBX_EINVAL, "unknown cost kind %d", c.cost_kind);
   if (c.physics != LBX_PHYSICS_SURROGATE && c.physics != LBX_PHYSICS_PIC)
     return set_error(LBX_EINVAL, "unknown physics %d", c.physics);
-  if (c.physics == LBX_PHYSICS_PIC && c.cost_kind == LBX_COST_TIMERS)
-    return set_error(LBX_EINVAL, "Timers strategy is implemented for the surrogate push only");
+  if (c.physics == LBX_PHYSICS_PIC &&
+      (c.cost_kind == LBX_COST_TIMERS || c.cost_kind == LBX_COST_CUPTI))
+    return set_error(LBX_EINVAL, "Timers strategies are implemented for the surrogate push only");
   return LBX_OK;
 }
 
@@ -145,7 +150,8 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
       for (int b = 0; b < nb; ++b) cost[b] = (double)clk[b];
       break;
     case LBX_COST_TIMERS:
-      if (!timers) return set_error(LBX_EINVAL, "Timers costs need per-box event timings");
+    case LBX_COST_CUPTI:
+      if (!timers) return set_error(LBX_EINVAL, "Timers costs need per-box kernel timings");
       std::memcpy(cost, timers, sizeof(double) * nb);
       break;
     default:
@@ -284,10 +290,10 @@ int timers_prepare(lbx_sim* s, const double* vz, const double* vx, cudaStream_t 
   for (int b = 0; b < nb; ++b) {
     const long long cnt = (long long)s->h_counts[b];
     if (!cnt) continue;
-    cudaEventRecord(s->tb0[b], st);
+    if (!s->cupti) cudaEventRecord(s->tb0[b], st);
     rc = launch_timers_push(s->z, s->x, vz, vx, s->perm + s->h_offsets[b], cnt, st);
     if (rc) return rc;
-    cudaEventRecord(s->tb1[b], st);
+    if (!s->cupti) cudaEventRecord(s->tb1[b], st);
   }
   return LBX_OK;
 }
@@ -298,7 +304,7 @@ int launch_step(lbx_sim* s, int64_t step, cudaStream_t st) {
   Rec d = rec_at(s->ring_d, s->rec_bytes, slot, s->lb->nb);
   const lbx_sim_config& c = s->lb->cfg;
   const bool kicked = step >= c.kick_step && s->kvz != nullptr;
-  const bool timers = c.cost_kind == LBX_COST_TIMERS;
+  const bool timers = c.cost_kind == LBX_COST_TIMERS || c.cost_kind == LBX_COST_CUPTI;
   if (c.physics == LBX_PHYSICS_PIC) {
     lbx_pic_args pa{};
     pa.z = s->z;
@@ -375,7 +381,20 @@ int process_step(lbx_sim* s, int64_t step, lbx_sim_outputs* o, int* halt) {
                      (long long)step, (long long)*h.err);
   const bool clock = s->lb->cfg.cost_kind == LBX_COST_GPUCLOCK;
   const double* timers = nullptr;
-  if (s->lb->cfg.cost_kind == LBX_COST_TIMERS) {
+  if (s->cupti) {
+    int busy = 0;
+    for (int b = 0; b < s->lb->nb; ++b) busy += s->h_counts[b] != 0;
+    uint32_t sid = 0;
+    int rc = cupti_stream(s->stream, &sid);
+    if (!rc) rc = cupti_collect(sid, busy, s->spans.data());
+    if (rc) return rc;
+    for (int b = 0, k = 0; b < s->lb->nb; ++b)
+      s->timers[b] = s->h_counts[b] ? s->spans[k++] / 1000.0 : 0.0;  // microseconds
+    timers = s->timers.data();
+    if (o->clock_trace)
+      for (int b = 0; b < s->lb->nb; ++b)
+        o->clock_trace[(size_t)step * s->lb->nb + b] = (uint64_t)(s->timers[b] * 1000.0);
+  } else if (s->lb->cfg.cost_kind == LBX_COST_TIMERS) {
     for (int b = 0; b < s->lb->nb; ++b) {
       float ms = 0.f;
       if (s->h_counts[b]) cudaEventElapsedTime(&ms, s->tb0[b], s->tb1[b]);
@@ -497,7 +516,19 @@ int lbx_sim_create(lbx_sim** out, lbx_ctx* ctx, const lbx_sim_config* cfg) {
   s->ctx = ctx;
   s->lb = lb;
   const int nb = lb->nb;
-  s->ring = (cfg->capacity_particles >= 0 || cfg->cost_kind == LBX_COST_TIMERS) ? 1 : 16;
+  s->ring = (cfg->capacity_particles >= 0 || cfg->cost_kind == LBX_COST_TIMERS ||
+             cfg->cost_kind == LBX_COST_CUPTI)
+                ? 1
+                : 16;
+  if (cfg->cost_kind == LBX_COST_CUPTI) {
+    rc = cupti_acquire();
+    if (rc) {
+      lbx_sim_destroy(s);
+      return rc;
+    }
+    s->cupti = true;
+    s->spans.assign(nb, 0.0);
+  }
   s->rec_bytes = ((size_t)24 * nb + 16 + 255) & ~(size_t)255;
   cudaError_t e = cudaHostAlloc(&s->ring_h, s->rec_bytes * s->ring, cudaHostAllocMapped);
   if (e != cudaSuccess) {
@@ -536,6 +567,7 @@ int lbx_sim_destroy(lbx_sim* s) {
   if (s->ring_h) cudaFreeHost(s->ring_h);
   for (auto& ev : s->tb0) cudaEventDestroy(ev);
   for (auto& ev : s->tb1) cudaEventDestroy(ev);
+  if (s->cupti) cupti_release();
   cudaFree(s->box);
   cudaFree(s->perm);
   cudaFree(s->zero_v);
@@ -562,7 +594,7 @@ int lbx_sim_set_particles(lbx_sim* s, double* z, double* x, double* vz, double* 
   s->kvz = kick_vz;
   s->kvx = kick_vx;
   s->n_host = n;
-  if (s->lb->cfg.cost_kind == LBX_COST_TIMERS) {
+  if (s->lb->cfg.cost_kind == LBX_COST_TIMERS || s->cupti) {
     if (n >= (1ll << 31)) return set_error(LBX_EINVAL, "Timers strategy supports < 2^31 particles");
     const int nb = s->lb->nb;
     cudaFree(s->box);
@@ -616,6 +648,7 @@ int lbx_sim_run(lbx_sim* s, int64_t first, int64_t last, lbx_sim_outputs* o, voi
     if (s->lb->owner[b] < 0 || s->lb->owner[b] >= c.n_ranks)
       return set_error(LBX_EINVAL, "owner entries must lie in [0, %d)", c.n_ranks);
   cudaStream_t st = (cudaStream_t)stream;
+  s->stream = stream;
   s->timing = o->kernel_ms != nullptr;
   int64_t launched = first, processed = first;
   int halt = 0;

@@ -329,7 +329,7 @@ PIC_DEFAULTS = {"dt": 0.5, "q_over_m": -1.0, "q_times_w": -1e-4}
 def sim_config(cfg: ScenarioConfig, policy: BalancePolicy, provider: CostProvider,
                physics: str = "surrogate", pic: dict | None = None):
     """Flatten (scenario, policy, provider) into lbx_sim_config."""
-    if provider.device_kind < 0 or provider.device_kind > 4:
+    if provider.device_kind < 0 or provider.device_kind > 5:
         raise ConfigError(f"provider {provider.kind!r} is not supported by the native loop")
     model = resolve_costs(cfg)
     w = getattr(provider, "weights", None)

@@ -83,9 +83,10 @@ def test_config_errors_name_the_field(P):
     with pytest.raises(P.ConfigError, match="box_size 7 does not divide the z-extent"):
         P.build_box_array((64, 64), 7)
     with pytest.raises(P.ConfigError):
-        P.make_provider("cupti")
+        P.make_provider("nvtx")
     assert P.make_provider("GpuClock").kind == "gpuclock"
     assert P.make_provider("Timers").kind == "timers"
+    assert P.make_provider("CUPTI").kind == "cupti" and P.make_provider("cupti").device_kind == 5
     s = P.apply_overrides(P.load_spec("mini"), policy="none")
     assert s.policy.interval == s.scenario.total_steps + 1
     s = P.apply_overrides(P.load_spec("mini"), policy="static", ranks=4)

@@ -87,13 +87,15 @@ def test_gpuclock_run_rank_correlates_with_true_work(runs):
         assert rho > 0.9, (s, rho)
 
 
-def test_timers_run_keeps_reference_state(runs):
-    """Timers strategy (per-box launches + events): particle state and counts
-    stay bit-exact with the reference (in-place push by index + stable
-    compaction); costs are positive exactly on occupied boxes."""
+@pytest.mark.parametrize("kind", ["timers", "cupti"])
+def test_timers_run_keeps_reference_state(runs, kind):
+    """Timers strategies (per-box launches timed by CUDA events, or by CUPTI
+    kernel activity records): particle state and counts stay bit-exact with
+    the reference (in-place push by index + stable compaction); costs are
+    positive exactly on occupied boxes."""
     from paper_2104_11385_b200 import scenarios as S
     from paper_2104_11385_b200.workload import run_simulation
-    spec = S.apply_overrides(S.load_spec("tight-memory"), cost="timers", steps=80)
+    spec = S.apply_overrides(S.load_spec("tight-memory"), cost=kind, steps=80)
     res = run_simulation(spec.scenario, spec.policy, spec.build_provider(),
                          record_counts=True)
     from oracle import lbsim_oracle as O
