@@ -44,6 +44,9 @@ def main():
                     help="c2: the C2 blob tiled (dense, ~7,000 particles per occupied cell); "
                          "uniform: SURVEY 8d's roofline plasma, 4096x4096 cells x 8 ppc "
                          "(134 M particles), thermal momenta")
+    ap.add_argument("--modes", default="push_deposit,push_deposit_inplace,push_deposit_noclock,"
+                                        "full_step",
+                    help="comma-separated subset of the modes")
     args = ap.parse_args()
 
     import torch
@@ -89,6 +92,8 @@ def main():
                                    ("push_deposit_inplace", False, False, True),
                                    ("push_deposit_noclock", False, True, False),
                                    ("full_step", True, True, True)):
+        if mode not in args.modes.split(","):
+            continue
         st = pic.PicState.create(pos0[:1], u0[:1], nz, nx, device=dev)
         for name, t in init.items():
             setattr(st, name, t.clone())
@@ -113,7 +118,8 @@ def main():
                      "pushes_per_s": nb / (ms / 1e3), "achieved_gbs": achieved,
                      "frac_of_hbm_peak": achieved / peak}
         del st
-    out["gpuclock_overhead"] = out["push_deposit"]["ms"] / out["push_deposit_noclock"]["ms"] - 1.0
+    if "push_deposit" in out and "push_deposit_noclock" in out:
+        out["gpuclock_overhead"] = out["push_deposit"]["ms"] / out["push_deposit_noclock"]["ms"] - 1.0
     out["peak_gbs"] = peak
     out["peak_source"] = peak_src
     print(json.dumps(out))

@@ -925,6 +925,7 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const long long cells = (long long)a->nz * a->nx;
   const long long quads = (long long)(a->nz + 1) * (a->nx + 1);
+  if (!sorted) ctx->pic_sort_next = nullptr;   // an in-place step invalidates the cell slots
   if (!ctx->pic_acc || ctx->pic_cells < cells) {
     if (ctx->pic_acc) {
       cudaDeviceSynchronize();

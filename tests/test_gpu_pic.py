@@ -165,6 +165,29 @@ def test_sorted_mode_matches_oracle(clustered):
     assert np.mean(np.diff(cell) >= 0) > 0.5
 
 
+def test_sorted_and_in_place_steps_share_a_state():
+    """An in-place step between sorted steps moves the particles without new
+    cell slots; the next sorted step must recount them (regression) and the
+    run stays exact."""
+    from paper_2104_11385_b200 import device, pic
+    pos, u = setup(20_000, 48, 48, seed=10, clustered=False, speed=0.8)
+    ctx = device.Context(capacity=pos.shape[0])
+    st = pic.PicState.create(pos, u, 48, 48)
+    f = PO.new_fields(48, 48)
+    p = {"z": pos[:, 0].copy(), "x": pos[:, 1].copy(), "uz": u[:, 0].copy(),
+         "ux": u[:, 1].copy(), "uy": u[:, 2].copy()}
+    for mode in ("sorted", "sorted", "inplace", "sorted", "inplace", "inplace", "sorted"):
+        pic.pic_step(ctx, st, 16, -1.0, -0.05, 0.5, field_solve=True, sort=mode == "sorted")
+        PO.particle_step(f, p, 48, 48, -1.0, -0.05, 0.5)
+        PO.field_step(f, 48, 48, 0.5)
+    g, o = canonical(st.particles()), canonical(p)
+    for k in g:
+        assert np.array_equal(g[k], o[k]), k
+    fa = st.field_arrays()
+    for k in PO.OFFSETS:
+        assert np.array_equal(fa[k], f[k]), k
+
+
 def test_sorted_mode_resync_and_absorption():
     """A new input (not the previous output) is recounted; absorbing steps
     compact the sorted output."""
