@@ -98,16 +98,22 @@ def main():
         for name, t in init.items():
             setattr(st, name, t.clone())
         st.n = n
-        for _ in range(args.warmup):
-            pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=clk, field_solve=solve,
-                         sort=sort)
+        for w in range(args.warmup):
+            try:
+                pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=clk, field_solve=solve,
+                             sort=sort)
+            except ValueError as e:
+                raise ValueError(f"mode {mode} warm-up step {w}: {e}") from None
         times = []
         for _ in range(args.steps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             n_before = st.n
             e0.record(stream)
-            pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=clk, field_solve=solve,
-                         sort=sort)
+            try:
+                pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=clk, field_solve=solve,
+                             sort=sort)
+            except ValueError as e:
+                raise ValueError(f"mode {mode} step {len(times)}: {e}") from None
             e1.record(stream)
             torch.cuda.synchronize(dev)
             times.append((e0.elapsed_time(e1), n_before))

@@ -11,6 +11,7 @@ See include/lbx.h (lbx_pic_step) for conventions.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -97,6 +98,13 @@ def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times
     a.n_out, a.err_out = _lib.ptr(nout), _lib.ptr(nout[1:])
     names = ("z", "x", "uz", "ux", "uy")
     if sort:
+        # The library keeps the cell slots of its last sorted output and
+        # recognises that output by address; a new state can reuse a freed
+        # buffer's address, so resynchronise unless this state (unmodified
+        # since: torch's version counter) produced the last sorted output.
+        last = getattr(ctx, "_pic_sorted", None)
+        if last is None or last[0]() is not st or last[1] != st.z._version:
+            a.flags |= _lib.LBX_PIC_RESYNC
         cap = st.z.numel()
         if st.spare is None or st.spare[0].numel() != cap:
             st.spare = tuple(torch.zeros(cap, dtype=torch.float64, device=dev) for _ in names)
@@ -108,6 +116,9 @@ def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times
         for k, t in zip(names, st.spare):
             setattr(st, k, t)
         st.spare = old
+        ctx._pic_sorted = (weakref.ref(st), st.z._version)
+    else:
+        ctx._pic_sorted = None
     h = nout.cpu().numpy()
     if h[1]:
         raise ValueError(f"{int(h[1])} particles fell outside the box grid")

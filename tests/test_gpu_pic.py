@@ -188,6 +188,34 @@ def test_sorted_and_in_place_steps_share_a_state():
         assert np.array_equal(fa[k], f[k]), k
 
 
+def test_sorted_mode_new_state_in_reused_buffers():
+    """A new state whose arrays sit at the addresses of the last sorted
+    output (what a caching allocator does after the old state is freed)
+    must not inherit that output's cell slots (regression)."""
+    from paper_2104_11385_b200 import device, pic
+    pos, u = setup(20_000, 48, 48, seed=11, clustered=True)
+    pos2, u2 = setup(20_000, 48, 48, seed=12, clustered=False)
+    ctx = device.Context(capacity=pos.shape[0])
+    a = pic.PicState.create(pos, u, 48, 48)
+    for _ in range(2):
+        pic.pic_step(ctx, a, 16, -1.0, -0.05, 0.5, field_solve=False, sort=True)
+    fresh = pic.PicState.create(pos2, u2, 48, 48)
+    for k in ("z", "x", "uz", "ux", "uy"):   # same buffers, new contents
+        getattr(a, k)[:pos2.shape[0]].copy_(getattr(fresh, k)[:pos2.shape[0]])
+    b = pic.PicState(z=a.z, x=a.x, uz=a.uz, ux=a.ux, uy=a.uy, n=pos2.shape[0],
+                     fields=fresh.fields, nz=48, nx=48, spare=a.spare)
+    f = PO.new_fields(48, 48)
+    p = {"z": pos2[:, 0].copy(), "x": pos2[:, 1].copy(), "uz": u2[:, 0].copy(),
+         "ux": u2[:, 1].copy(), "uy": u2[:, 2].copy()}
+    for _ in range(3):
+        pic.pic_step(ctx, b, 16, -1.0, -0.05, 0.5, field_solve=True, sort=True)
+        PO.particle_step(f, p, 48, 48, -1.0, -0.05, 0.5)
+        PO.field_step(f, 48, 48, 0.5)
+    g, o = canonical(b.particles()), canonical(p)
+    for k in g:
+        assert np.array_equal(g[k], o[k]), k
+
+
 def test_sorted_mode_resync_and_absorption():
     """A new input (not the previous output) is recounted; absorbing steps
     compact the sorted output."""
