@@ -384,7 +384,10 @@ typedef struct lbx_pic_args {
    * are contiguous and their current is accumulated in registers.  The
    * caller swaps in/out after the call.  The library keeps the next step's
    * cell slots; passing any other input than the last call's out[] (or
-   * LBX_PIC_RESYNC) recounts them.  Absorbed particles' slots are filled
+   * LBX_PIC_RESYNC) recounts them.  The last output is recognised by its
+   * address: a host that frees a state and may reuse its memory, or that
+   * edits the particles between calls, must pass LBX_PIC_RESYNC (the
+   * Python wrapper does, keyed on the state object and its version).  Absorbed particles' slots are filled
    * from the tail (O(absorbed)).  Order within a cell is not deterministic;
    * every computed value is.  NULL: in place (order kept with
    * LBX_PIC_STABLE_ORDER, else absorbed slots filled from the tail). */
