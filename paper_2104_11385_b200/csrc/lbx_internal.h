@@ -114,3 +114,43 @@ void cupti_release();
 int cupti_stream(void* stream, uint32_t* id);
 int cupti_collect(uint32_t stream_id, int n, double* dur_ns);
 }  // namespace lbx
+
+#ifdef __CUDACC__
+namespace lbx {
+// Last CTA of a step kernel: per-box totals -> the step record (counts,
+// heuristic cost w_p*count + w_c*cells, clock tally << clk_shift), and the
+// accumulators cleared for the next launch.  Every other CTA fenced its
+// atomics before taking the done ticket, so L2 loads (ld.cg) see the totals;
+// four loads per thread are in flight at once instead of one returning
+// atomic exchange per box (the serial tail of small steps).
+template <bool kClock>
+__device__ __forceinline__ void step_record(unsigned long long* g_cnt, unsigned long long* g_clk,
+                                            int nb, long long* counts_out, double* cost_out,
+                                            unsigned long long* clk_out, double wp, double wc,
+                                            double cells, int clk_shift) {
+  constexpr int kU = 4;
+  for (int b0 = threadIdx.x; b0 < nb; b0 += kU * blockDim.x) {
+    unsigned long long c[kU], k[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int b = b0 + u * (int)blockDim.x;
+      c[u] = b < nb ? __ldcg(g_cnt + b) : 0ull;
+      k[u] = (kClock && b < nb) ? __ldcg(g_clk + b) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int b = b0 + u * (int)blockDim.x;
+      if (b >= nb) break;
+      __stcg(g_cnt + b, 0ull);
+      if (counts_out) counts_out[b] = (long long)c[u];
+      if (cost_out)
+        cost_out[b] = __dadd_rn(__dmul_rn(wp, (double)(long long)c[u]), __dmul_rn(wc, cells));
+      if (kClock) {
+        __stcg(g_clk + b, 0ull);
+        if (clk_out) clk_out[b] = k[u] << clk_shift;
+      }
+    }
+  }
+}
+}  // namespace lbx
+#endif

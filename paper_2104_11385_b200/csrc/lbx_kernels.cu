@@ -462,20 +462,9 @@ __global__ void __launch_bounds__(kBlock, LBX_STREAM_MINB) stream_kernel(StepPar
 
   // ---- last CTA: step epilogue ----
   __threadfence();
-  if (kHist) {
-    for (int b = tid; b < p.nb; b += kBlock) {
-      const unsigned long long c = atomicExch(p.g_cnt + b, 0ull);
-      if (p.counts_out) p.counts_out[b] = (long long)c;
-      if (p.cost_out) {
-        p.cost_out[b] =
-            __dadd_rn(__dmul_rn(p.wp, (double)(long long)c), __dmul_rn(p.wc, p.cells));
-      }
-      if (kClock) {
-        const unsigned long long k = atomicExch(p.g_clk + b, 0ull);
-        if (p.clk_out) p.clk_out[b] = k << kClockShift;
-      }
-    }
-  }
+  if (kHist)
+    step_record<kClock>(p.g_cnt, p.g_clk, p.nb, p.counts_out, p.cost_out, p.clk_out, p.wp, p.wc,
+                        p.cells, kClockShift);
   if (tid == 0) {
     const unsigned long long lv = *((volatile unsigned long long*)&p.st->leavers);
     const long long n_new = n - (long long)lv;
@@ -678,16 +667,8 @@ __global__ void __launch_bounds__(kBlock, 4) stream3d_kernel(Step3DParams p) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int b = tid; b < p.nb; b += kBlock) {
-    const unsigned long long c = atomicExch(p.g_cnt + b, 0ull);
-    if (p.counts_out) p.counts_out[b] = (long long)c;
-    if (p.cost_out)
-      p.cost_out[b] = __dadd_rn(__dmul_rn(p.wp, (double)(long long)c), __dmul_rn(p.wc, p.cells));
-    if (kClock) {
-      const unsigned long long k = atomicExch(p.g_clk + b, 0ull);
-      if (p.clk_out) p.clk_out[b] = k << kClockShift;
-    }
-  }
+  step_record<kClock>(p.g_cnt, p.g_clk, p.nb, p.counts_out, p.cost_out, p.clk_out, p.wp, p.wc,
+                      p.cells, kClockShift);
   if (tid == 0) {
     const long long n_new = n - (long long)*((volatile unsigned long long*)&p.st->leavers);
     if (p.n_out) *p.n_out = n_new;

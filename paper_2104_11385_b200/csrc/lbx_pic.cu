@@ -565,16 +565,8 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int b = tid; b < p.nb; b += kPB) {
-    const unsigned long long c = atomicExch(p.g_cnt + b, 0ull);
-    if (p.counts_out) p.counts_out[b] = (long long)c;
-    if (p.cost_out)
-      p.cost_out[b] = __dadd_rn(__dmul_rn(p.wp, (double)(long long)c), __dmul_rn(p.wc, p.cells));
-    if (kClock) {
-      const unsigned long long k = atomicExch(p.g_clk + b, 0ull);
-      if (p.clk_out) p.clk_out[b] = k << 4;
-    }
-  }
+  step_record<kClock>(p.g_cnt, p.g_clk, p.nb, p.counts_out, p.cost_out, p.clk_out, p.wp, p.wc,
+                      p.cells, 4);
   if (tid == 0) {
     const long long n_new = n - (long long)*((volatile unsigned long long*)&p.st->leavers);
     if (p.n_out) *p.n_out = n_new;
