@@ -20,6 +20,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -64,6 +66,16 @@ struct lbx_sim {
   bool cupti = false;
   void* stream = nullptr;
   std::vector<double> spans;
+  // CUDA-graph replay of whole kCycle-step cycles (surrogate physics): the
+  // loop's own stream, one graph per (ring half, kicked, timing), captured
+  // on first use and replayed -- one launch per 16 steps instead of three.
+  cudaStream_t gs = nullptr;
+  cudaEvent_t join = nullptr;
+  cudaGraphExec_t gexec[2][2][2] = {};
+  bool graphs = false;   // eligible (ring of 2 cycles, surrogate, not disabled)
+  bool warm = false;     // a per-step launch has run (allocations are done)
+  bool capturing = false;
+  long long graph_cycles = 0;
   // PIC physics
   float* fields[6] = {};
   float* current[3] = {};
@@ -298,9 +310,16 @@ int timers_prepare(lbx_sim* s, const double* vz, const double* vx, cudaStream_t 
   return LBX_OK;
 }
 
+// Stream event record that, under graph capture, becomes an event-record
+// node the host can wait on (a plain record would be a capture-internal join).
+cudaError_t record(const lbx_sim* s, cudaEvent_t ev, cudaStream_t st) {
+  return s->capturing ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal)
+                      : cudaEventRecord(ev, st);
+}
+
 int launch_step(lbx_sim* s, int64_t step, cudaStream_t st) {
   const int slot = (int)(step % s->ring);
-  if (s->timing) cudaEventRecord(s->t0[slot], st);
+  if (s->timing) record(s, s->t0[slot], st);
   Rec d = rec_at(s->ring_d, s->rec_bytes, slot, s->lb->nb);
   const lbx_sim_config& c = s->lb->cfg;
   const bool kicked = step >= c.kick_step && s->kvz != nullptr;
@@ -330,8 +349,8 @@ int launch_step(lbx_sim* s, int64_t step, cudaStream_t st) {
     pa.err_out = d.err;
     int rc = lbx_pic_step(s->ctx, &pa, st);
     if (rc) return rc;
-    if (s->timing) cudaEventRecord(s->t1[slot], st);
-    cudaError_t e = cudaEventRecord(s->ev[slot], st);
+    if (s->timing) record(s, s->t1[slot], st);
+    cudaError_t e = record(s, s->ev[slot], st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
     return LBX_OK;
   }
@@ -360,10 +379,61 @@ int launch_step(lbx_sim* s, int64_t step, cudaStream_t st) {
   a.err_out = reinterpret_cast<long long*>(d.err);
   int rc = launch_push_step(s->ctx, a, st);
   if (rc) return rc;
-  if (s->timing) cudaEventRecord(s->t1[slot], st);
-  cudaError_t e = cudaEventRecord(s->ev[slot], st);
+  if (s->timing) record(s, s->t1[slot], st);
+  cudaError_t e = record(s, s->ev[slot], st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
   return LBX_OK;
+}
+
+constexpr int kCycle = 16;
+
+void drop_graphs(lbx_sim* s) {
+  for (auto& a : s->gexec)
+    for (auto& b : a)
+      for (auto& g : b)
+        if (g) cudaGraphExecDestroy(g), g = nullptr;
+}
+
+bool kicked_at(const lbx_sim* s, int64_t step) {
+  return step >= s->lb->cfg.kick_step && s->kvz != nullptr;
+}
+
+// Launches steps [step, step + kCycle) as one graph (captured the first time
+// this (half, kicked, timing) combination is seen).  Returns false -- with
+// nothing launched and graphs disabled for this sim -- if capture fails.
+bool launch_cycle(lbx_sim* s, int64_t step, cudaStream_t st) {
+  const int half = (int)((step / kCycle) & 1);
+  const int kick = kicked_at(s, step) ? 1 : 0;
+  cudaGraphExec_t& ge = s->gexec[half][kick][s->timing ? 1 : 0];
+  if (!ge) {
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    s->capturing = ok;
+    for (int j = 0; ok && j < kCycle; ++j) ok = launch_step(s, step + j, st) == LBX_OK;
+    s->capturing = false;
+    const cudaError_t ec = cudaStreamEndCapture(st, &g);
+    ok = ok && ec == cudaSuccess && g != nullptr &&
+         cudaGraphInstantiate(&ge, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (!ok) {
+      if (std::getenv("LBX_GRAPH_DEBUG"))
+        std::fprintf(stderr, "lbx: graph capture failed at step %lld: end=%s last=%s (%s)\n",
+                     (long long)step, cudaGetErrorString(ec), cudaGetErrorString(cudaGetLastError()),
+                     lbx_last_error());
+      ge = nullptr;
+      cudaGetLastError();   // clear the capture error; per-step launches from here on
+      clear_error();
+      s->graphs = false;
+      return false;
+    }
+  }
+  if (cudaGraphLaunch(ge, st) != cudaSuccess) {
+    cudaGetLastError();
+    s->graphs = false;
+    return false;
+  }
+  ++s->graph_cycles;
+  return true;
 }
 
 int process_step(lbx_sim* s, int64_t step, lbx_sim_outputs* o, int* halt) {
@@ -519,7 +589,12 @@ int lbx_sim_create(lbx_sim** out, lbx_ctx* ctx, const lbx_sim_config* cfg) {
   s->ring = (cfg->capacity_particles >= 0 || cfg->cost_kind == LBX_COST_TIMERS ||
              cfg->cost_kind == LBX_COST_CUPTI)
                 ? 1
-                : 16;
+                : 2 * kCycle;
+  if (s->ring > 1 && cfg->physics == LBX_PHYSICS_SURROGATE && !std::getenv("LBX_NO_GRAPHS")) {
+    s->graphs = cudaStreamCreateWithFlags(&s->gs, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming) == cudaSuccess;
+    if (!s->graphs) cudaGetLastError();
+  }
   if (cfg->cost_kind == LBX_COST_CUPTI) {
     rc = cupti_acquire();
     if (rc) {
@@ -567,6 +642,10 @@ int lbx_sim_destroy(lbx_sim* s) {
   if (s->ring_h) cudaFreeHost(s->ring_h);
   for (auto& ev : s->tb0) cudaEventDestroy(ev);
   for (auto& ev : s->tb1) cudaEventDestroy(ev);
+  if (s->gs) cudaStreamSynchronize(s->gs);
+  drop_graphs(s);
+  if (s->gs) cudaStreamDestroy(s->gs);
+  if (s->join) cudaEventDestroy(s->join);
   if (s->cupti) cupti_release();
   cudaFree(s->box);
   cudaFree(s->perm);
@@ -594,6 +673,7 @@ int lbx_sim_set_particles(lbx_sim* s, double* z, double* x, double* vz, double* 
   s->kvz = kick_vz;
   s->kvx = kick_vx;
   s->n_host = n;
+  drop_graphs(s);   // captured pointers and launch sizes change
   if (s->lb->cfg.cost_kind == LBX_COST_TIMERS || s->cupti) {
     if (n >= (1ll << 31)) return set_error(LBX_EINVAL, "Timers strategy supports < 2^31 particles");
     const int nb = s->lb->nb;
@@ -647,15 +727,32 @@ int lbx_sim_run(lbx_sim* s, int64_t first, int64_t last, lbx_sim_outputs* o, voi
   for (int b = 0; b < s->lb->nb; ++b)
     if (s->lb->owner[b] < 0 || s->lb->owner[b] >= c.n_ranks)
       return set_error(LBX_EINVAL, "owner entries must lie in [0, %d)", c.n_ranks);
-  cudaStream_t st = (cudaStream_t)stream;
-  s->stream = stream;
+  cudaStream_t caller = (cudaStream_t)stream;
+  cudaStream_t st = caller;
+  if (s->gs) {   // run on the loop's own (capturable) stream, ordered after the caller's work
+    cudaEventRecord(s->join, caller);
+    cudaStreamWaitEvent(s->gs, s->join, 0);
+    st = s->gs;
+  }
+  s->stream = st;
   s->timing = o->kernel_ms != nullptr;
   int64_t launched = first, processed = first;
   int halt = 0;
   while (processed < last && !halt) {
     while (launched < last && launched - processed < s->ring) {
+      // whole cycle as one graph: aligned, one side of the kick; wait for
+      // the ring half it writes to be processed
+      if (s->graphs && s->warm && launched % kCycle == 0 && launched + kCycle <= last &&
+          kicked_at(s, launched) == kicked_at(s, launched + kCycle - 1)) {
+        if (launched - processed + kCycle > s->ring) break;
+        if (launch_cycle(s, launched, st)) {
+          launched += kCycle;
+          continue;
+        }
+      }
       int rc = launch_step(s, launched, st);
       if (rc) return rc;
+      s->warm = true;
       ++launched;
     }
     int rc = process_step(s, processed, o, &halt);
@@ -665,7 +762,18 @@ int lbx_sim_run(lbx_sim* s, int64_t first, int64_t last, lbx_sim_outputs* o, voi
   // Capacity runs use ring=1, so no step past a halting step was launched.
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "stream sync");
+  if (s->gs) {
+    cudaEventRecord(s->join, s->gs);
+    cudaStreamWaitEvent(caller, s->join, 0);
+  }
   std::memcpy(o->owner, s->lb->owner.data(), 8 * (size_t)s->lb->nb);
+  return LBX_OK;
+}
+
+int lbx_sim_graph_cycles(lbx_sim* s, int64_t* cycles) {
+  clear_error();
+  if (!s || !cycles) return set_error(LBX_EINVAL, "NULL argument");
+  *cycles = s->graph_cycles;
   return LBX_OK;
 }
 

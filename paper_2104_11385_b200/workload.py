@@ -461,6 +461,13 @@ class Simulation:
         self.done = max(self.done, int(self.souts.completed_steps))
         return self
 
+    @property
+    def graph_cycles(self) -> int:
+        """16-step cycles the native loop has replayed as CUDA graphs."""
+        out = C.c_int64()
+        _lib.check(_lib.lib.lbx_sim_graph_cycles(self.handle, C.byref(out)))
+        return out.value
+
     def close(self):
         if getattr(self, "handle", None):
             _lib.lib.lbx_sim_destroy(self.handle)

@@ -67,6 +67,44 @@ def test_run_matches_reference(runs, name):
     assert sha(vel) == ref["final_vel_sha"], name
 
 
+@pytest.mark.parametrize("name", ["mini", "default_short"])
+def test_graph_replay_matches_per_step_launches(runs, name, monkeypatch):
+    """The native loop replays aligned 16-step cycles as CUDA graphs; with
+    graphs disabled (LBX_NO_GRAPHS) every output is the same.  Split runs
+    with unaligned boundaries mix graph cycles and per-step launches."""
+    from paper_2104_11385_b200.workload import Simulation
+    spec = spec_for(runs, name)
+    T = spec.scenario.total_steps
+    cuts = [0, 5, 37, 38, T // 2 + 3, T]
+
+    def run(graphs):
+        if graphs:
+            monkeypatch.delenv("LBX_NO_GRAPHS", raising=False)
+        else:
+            monkeypatch.setenv("LBX_NO_GRAPHS", "1")
+        sim = Simulation(spec.scenario, spec.policy, spec.build_provider(), device="cuda:0",
+                         record_counts=True)
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            sim.run(a, b)
+        cycles = sim.graph_cycles
+        res = sim.result()
+        sim.close()
+        return res, cycles
+
+    g, gc = run(True)
+    p, pc = run(False)
+    assert pc == 0 and gc >= (T - 48) // 16 - 2, (gc, pc)
+    assert np.array_equal(g.cost_trace, p.cost_trace)
+    assert np.array_equal(g.count_trace, p.count_trace)
+    assert [m.walltime for m in g.metrics] == [m.walltime for m in p.metrics]
+    assert [[s, o.tolist()] for s, o in g.adoption_snapshots] == \
+        [[s, o.tolist()] for s, o in p.adoption_snapshots]
+    gp, gv = g.final_state.to_numpy()
+    pp, pv = p.final_state.to_numpy()
+    assert np.array_equal(gp, pp) and np.array_equal(gv, pv)
+    assert sha(g.cost_trace) == runs[name]["cost_trace_sha"]
+
+
 def test_gpuclock_run_rank_correlates_with_true_work(runs):
     """GpuClock costs (real clock64 tallies) vs the reference's timer model:
     Spearman rank correlation with true work on every attempt step."""
