@@ -14,7 +14,9 @@ launch stream:
                         deposit's cell runs decay as particles drift);
   push_deposit_noclock  sorted mode without the GpuClock tally (its overhead
                         is gpuclock_overhead = push_deposit / this - 1);
-  full_step             sorted mode plus the Yee update.
+  full_step             sorted mode plus the Yee update;
+  push_deposit_resort   in place with lbx_pic_sort (cell counting sort)
+                        every --resort steps, its cost inside the timed step.
 Roofline: HBM, algorithmic bytes = 80 B per particle (read z,x,uz,ux,uy +
 write them, float64) -- field patch and current flush traffic is counted
 separately from ncu (profiles/).  Prints one JSON object.
@@ -44,8 +46,10 @@ def main():
                     help="c2: the C2 blob tiled (dense, ~7,000 particles per occupied cell); "
                          "uniform: SURVEY 8d's roofline plasma, 4096x4096 cells x 8 ppc "
                          "(134 M particles), thermal momenta")
+    ap.add_argument("--resort", type=int, default=25,
+                    help="push_deposit_resort: lbx_pic_sort every this many steps")
     ap.add_argument("--modes", default="push_deposit,push_deposit_inplace,push_deposit_noclock,"
-                                        "full_step",
+                                        "full_step,push_deposit_resort",
                     help="comma-separated subset of the modes")
     args = ap.parse_args()
 
@@ -91,13 +95,17 @@ def main():
     for mode, solve, sort, clk in (("push_deposit", False, True, True),
                                    ("push_deposit_inplace", False, False, True),
                                    ("push_deposit_noclock", False, True, False),
-                                   ("full_step", True, True, True)):
+                                   ("full_step", True, True, True),
+                                   ("push_deposit_resort", False, False, True)):
         if mode not in args.modes.split(","):
             continue
         st = pic.PicState.create(pos0[:1], u0[:1], nz, nx, device=dev)
         for name, t in init.items():
             setattr(st, name, t.clone())
         st.n = n
+        resort = mode == "push_deposit_resort"
+        if resort:   # start cell-ordered, like the other modes' first sorted step
+            pic.pic_sort(ctx, st)
         for w in range(args.warmup):
             try:
                 pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=clk, field_solve=solve,
@@ -109,6 +117,8 @@ def main():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             n_before = st.n
             e0.record(stream)
+            if resort and (len(times) + args.warmup) % args.resort == 0:
+                pic.pic_sort(ctx, st)
             try:
                 pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=clk, field_solve=solve,
                              sort=sort)

@@ -402,6 +402,14 @@ typedef struct lbx_pic_args {
 
 int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* args, void* stream);
 
+/* Counting sort of the particles (z, x, uz, ux, uy; the context's device
+ * count) by cell into out[] (order within a cell not kept; the caller swaps
+ * in/out).  Run every few steps it keeps an in-place run at the speed of a
+ * freshly cell-ordered input (the deposit's register runs follow cell
+ * order) without sort-on-write's per-step cost.  Fields, args' physics
+ * fields and flags are ignored. */
+int lbx_pic_sort(lbx_ctx* ctx, const lbx_pic_args* args, void* stream);
+
 /* Multi-GPU PIC (guard-cell current sum): after a LBX_PIC_DEFER_CURRENT step
  * the context holds the step's current as exact integers, cell-centric
  * jc[cells][16] (16 cell-relative nodes, int64 two's complement) over the

@@ -140,6 +140,7 @@ class PicArgs(C.Structure):
 
 
 SIGNATURES["lbx_pic_step"] = (i32, [vp, P(PicArgs), vp])
+SIGNATURES["lbx_pic_sort"] = (i32, [vp, P(PicArgs), vp])
 SIGNATURES["lbx_peer_alloc"] = (i32, [i64, P(vp), vp])
 SIGNATURES["lbx_ctx_set_upper"] = (i32, [vp, i64])
 SIGNATURES["lbx_fill_holes_dev"] = (i32, [vp, vp, vp, vp, vp, vp, vp, vp, i64, f64, f64, vp])

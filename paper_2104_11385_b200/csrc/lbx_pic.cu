@@ -600,6 +600,41 @@ __global__ void pic_count_kernel(const double* __restrict__ z, const double* __r
   }
 }
 
+// Periodic re-sort (lbx_pic_sort): scatter the particles to their cell's
+// slots.  A warp takes 32 consecutive particles (coalesced loads); lanes with
+// the same cell share one cursor atomic (__match_any_sync) and write
+// consecutive slots.
+__global__ void pic_sort_scatter_kernel(const double* __restrict__ z, const double* __restrict__ x,
+                                        const double* __restrict__ uz,
+                                        const double* __restrict__ ux,
+                                        const double* __restrict__ uy, double* oz, double* ox,
+                                        double* ouz, double* oux, double* ouy, const DevState* st,
+                                        unsigned* cursor, int nx) {
+  const long long n = st->n;
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w * 32 < n;
+       w += warps) {
+    const long long i = w * 32 + lane;
+    const bool live = i < n;
+    const unsigned act = __ballot_sync(kAll, live);
+    if (!live) continue;
+    const double zi = z[i], xi = x[i];
+    const int key = (int)zi * nx + (int)xi;
+    const unsigned grp = __match_any_sync(act, key);
+    const int leader = __ffs(grp) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(cursor + key, (unsigned)__popc(grp));
+    base = __shfl_sync(grp, base, leader);
+    const long long d = (long long)base + __popc(grp & ((1u << lane) - 1u));
+    oz[d] = zi;
+    ox[d] = xi;
+    ouz[d] = uz[i];
+    oux[d] = ux[i];
+    ouy[d] = uy[i];
+  }
+}
+
 // Exclusive scan of cell_cnt into cursor (the first slot of each cell), in
 // two launches over kScanBlocks contiguous segments; cell_cnt is zeroed.
 constexpr int kScanBlocks = 296;
@@ -1080,6 +1115,48 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   return pic_finish(ctx, a, s, jscale);
 }
 
+
+extern "C" int lbx_pic_sort(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
+  clear_error();
+  if (!ctx || !a) return set_error(LBX_EINVAL, "NULL argument");
+  if (a->nz < 1 || a->nx < 1) return set_error(LBX_EINVAL, "grid must be at least 1x1");
+  if ((long long)a->nz * a->nx >= (1ll << 31))
+    return set_error(LBX_EINVAL, "PIC grid too large (cell index must fit 32 bits)");
+  const double* in[5] = {a->z, a->x, a->uz, a->ux, a->uy};
+  for (int c = 0; c < 5; ++c)
+    if (!in[c] || !a->out[c]) return set_error(LBX_EINVAL, "lbx_pic_sort needs the 5 arrays and out[]");
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long cells = (long long)a->nz * a->nx;
+  if (!ctx->pic_sortbuf || ctx->pic_sort_cells < cells) {
+    if (ctx->pic_sortbuf) {
+      cudaDeviceSynchronize();
+      cudaFree(ctx->pic_sortbuf);
+    }
+    ctx->pic_sortbuf = nullptr;
+    const size_t bytes = ((size_t)cells * 2 + kScanBlocks) * sizeof(unsigned);
+    if (cudaMalloc(&ctx->pic_sortbuf, bytes) != cudaSuccess)
+      return set_error(LBX_EOOM, "PIC sort buffers");
+    cudaMemsetAsync(ctx->pic_sortbuf, 0, bytes, s);
+    ctx->pic_sort_cells = cells;
+  }
+  unsigned* cell_cnt = ctx->pic_sortbuf;
+  unsigned* cursor = ctx->pic_sortbuf + cells;
+  unsigned* block_sum = ctx->pic_sortbuf + 2 * cells;
+  const unsigned ng = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 8,
+                                                       (long long)(ctx->n_upper / kRun + 255) / 256));
+  pic_count_kernel<<<ng, 256, 0, s>>>(a->z, a->x, ctx->st, cell_cnt, a->nx);
+  pic_scan_reduce_kernel<<<kScanBlocks, kScanThreads, 0, s>>>(cell_cnt, cells, block_sum);
+  pic_scan_apply_kernel<<<kScanBlocks, kScanThreads, 0, s>>>(cell_cnt, cells, block_sum, cursor);
+  const unsigned sg = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 16,
+                                                       (long long)(ctx->n_upper + 255) / 256));
+  pic_sort_scatter_kernel<<<sg, 256, 0, s>>>(a->z, a->x, a->uz, a->ux, a->uy, a->out[0], a->out[1],
+                                             a->out[2], a->out[3], a->out[4], ctx->st, cursor,
+                                             a->nx);
+  ctx->pic_sort_next = nullptr;   // the cursors were consumed
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "pic sort launch");
+  return LBX_OK;
+}
 
 extern "C" int lbx_pic_finish(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   clear_error();

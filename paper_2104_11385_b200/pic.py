@@ -61,6 +61,29 @@ class PicState:
         return {k: v.cpu().numpy() for k, v in self.fields.items()}
 
 
+def pic_sort(ctx: Context, st: PicState):
+    """Counting sort of the particles by cell (lbx_pic_sort) into the spare
+    buffers, which the state then swaps in.  Every few in-place steps this
+    restores the cell order the deposit's register runs feed on."""
+    dev = ctx.device
+    names = ("z", "x", "uz", "ux", "uy")
+    ctx.set_count(st.n)
+    cap = st.z.numel()
+    if st.spare is None or st.spare[0].numel() != cap:
+        st.spare = tuple(torch.zeros(cap, dtype=torch.float64, device=dev) for _ in names)
+    a = _lib.PicArgs()
+    a.z, a.x, a.uz, a.ux, a.uy = (_lib.ptr(getattr(st, k)) for k in names)
+    a.nz, a.nx = st.nz, st.nx
+    for i, t in enumerate(st.spare):
+        a.out[i] = _lib.ptr(t)
+    _lib.check(_lib.lib.lbx_pic_sort(ctx.handle, C.byref(a), _stream(dev)))
+    old = tuple(getattr(st, k) for k in names)
+    for k, t in zip(names, st.spare):
+        setattr(st, k, t)
+    st.spare = old
+    ctx._pic_sorted = None
+
+
 def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times_w: float,
              dt: float, weights=(0.75, 0.25), clock=False, field_solve=True, sort=False,
              gather=None, stable=False):

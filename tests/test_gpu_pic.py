@@ -216,6 +216,38 @@ def test_sorted_mode_new_state_in_reused_buffers():
         assert np.array_equal(g[k], o[k]), k
 
 
+def test_periodic_cell_sort_keeps_results_exact():
+    """lbx_pic_sort between in-place steps: the particle multiset is kept,
+    the array ends up grouped by cell (non-decreasing cell index), and the
+    run stays identical to the oracle."""
+    from paper_2104_11385_b200 import device, pic
+    pos, u = setup(30_000, 48, 64, seed=13, clustered=False, speed=0.6)
+    ctx = device.Context(capacity=pos.shape[0])
+    st = pic.PicState.create(pos, u, 48, 64)
+    f = PO.new_fields(48, 64)
+    p = {"z": pos[:, 0].copy(), "x": pos[:, 1].copy(), "uz": u[:, 0].copy(),
+         "ux": u[:, 1].copy(), "uy": u[:, 2].copy()}
+    for step in range(6):
+        if step % 2 == 0:
+            before = canonical(st.particles())
+            pic.pic_sort(ctx, st)
+            after = st.particles()
+            cell = np.floor(after["z"]).astype(np.int64) * 64 + np.floor(after["x"]).astype(np.int64)
+            assert (np.diff(cell) >= 0).all()
+            ca = canonical(after)
+            for k in ca:
+                assert np.array_equal(ca[k], before[k]), k
+        pic.pic_step(ctx, st, 16, -1.0, -0.05, 0.5, field_solve=True)
+        PO.particle_step(f, p, 48, 64, -1.0, -0.05, 0.5)
+        PO.field_step(f, 48, 64, 0.5)
+    g, o = canonical(st.particles()), canonical(p)
+    for k in g:
+        assert np.array_equal(g[k], o[k]), k
+    fa = st.field_arrays()
+    for k in PO.OFFSETS:
+        assert np.array_equal(fa[k], f[k]), k
+
+
 def test_sorted_mode_resync_and_absorption():
     """A new input (not the previous output) is recounted; absorbing steps
     compact the sorted output."""
