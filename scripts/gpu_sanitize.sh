@@ -1,16 +1,17 @@
 #!/bin/bash
 # compute-sanitizer (memcheck / racecheck / synccheck) over CI-sized cases of
 # every kernel family: fused push/bin/compaction, drop-in AoS path + host
-# pipeline, PIC (quad/direct, in place/sorted), multi-GPU exchange (p2p and
+# pipeline, PIC (quad/direct, in place/sorted, cell sort), native loop graph replay, multi-GPU exchange (p2p and
 # collectives, thread ranks).  Summaries -> gpurun_out/sanitize_*.log
 mkdir -p gpurun_out
 CASES_K='tests/test_gpu_kernels.py -k "fixture or known_answer or empty or (fused_step_matches_oracle and 300001) or non_power or (host_pipeline and 5000)"'
 CASES_P='tests/test_gpu_pic.py -k "first_step or (multi_step and clustered-quad) or sorted_mode_matches_oracle"'
 CASES_D='tests/test_gpu_dist.py -k "mini-2 and p2p"'
 CASES_E='tests/test_gpu_3d.py tests/test_gpu_pic.py -k "3d or hole_filling or (multi_step and direct) or gpuclock or timers"'
-CASES_R='tests/test_gpu_runs.py -k "timers or gpuclock"'
+CASES_R='tests/test_gpu_runs.py -k "(timers and not cupti) or gpuclock or (graph_replay and mini)"'
+CASES_S='tests/test_gpu_pic.py -k "periodic_cell_sort or share_a_state or reused_buffers"'
 for tool in ${SAN_TOOLS:-memcheck racecheck synccheck}; do
-  for grp in ${SAN_GROUPS:-K P D E R}; do
+  for grp in ${SAN_GROUPS:-K P D E R S}; do
     eval cases=\$CASES_$grp
     eval timeout 1500 compute-sanitizer --tool $tool --error-exitcode 99 --target-processes all \
       python -m pytest $cases -x -q -p no:cacheprovider > gpurun_out/sanitize_${tool}_$grp.log 2>&1
