@@ -16,7 +16,9 @@ launch stream:
                         is gpuclock_overhead = push_deposit / this - 1);
   full_step             sorted mode plus the Yee update;
   push_deposit_resort   in place with lbx_pic_sort (cell counting sort)
-                        every --resort steps, its cost inside the timed step.
+                        every --resort steps, its cost inside the timed step;
+  push_deposit_tiled    the same with the tile-major sort and LBX_PIC_TILED
+                        steps (shared-memory patch and current).
 Roofline: HBM, algorithmic bytes = 80 B per particle (read z,x,uz,ux,uy +
 write them, float64) -- field patch and current flush traffic is counted
 separately from ncu (profiles/).  Prints one JSON object.
@@ -96,20 +98,22 @@ def main():
                                    ("push_deposit_inplace", False, False, True),
                                    ("push_deposit_noclock", False, True, False),
                                    ("full_step", True, True, True),
-                                   ("push_deposit_resort", False, False, True)):
+                                   ("push_deposit_resort", False, False, True),
+                                   ("push_deposit_tiled", False, False, True)):
         if mode not in args.modes.split(","):
             continue
         st = pic.PicState.create(pos0[:1], u0[:1], nz, nx, device=dev)
         for name, t in init.items():
             setattr(st, name, t.clone())
         st.n = n
-        resort = mode == "push_deposit_resort"
+        resort = mode in ("push_deposit_resort", "push_deposit_tiled")
+        tiled = mode == "push_deposit_tiled"
         if resort:   # start cell-ordered, like the other modes' first sorted step
-            pic.pic_sort(ctx, st)
+            pic.pic_sort(ctx, st, tiled=tiled)
         for w in range(args.warmup):
             try:
                 pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=clk, field_solve=solve,
-                             sort=sort)
+                             sort=sort, tiled=tiled)
             except ValueError as e:
                 raise ValueError(f"mode {mode} warm-up step {w}: {e}") from None
         times = []
@@ -118,10 +122,10 @@ def main():
             n_before = st.n
             e0.record(stream)
             if resort and (len(times) + args.warmup) % args.resort == 0:
-                pic.pic_sort(ctx, st)
+                pic.pic_sort(ctx, st, tiled=tiled)
             try:
                 pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=clk, field_solve=solve,
-                             sort=sort)
+                             sort=sort, tiled=tiled)
             except ValueError as e:
                 raise ValueError(f"mode {mode} step {len(times)}: {e}") from None
             e1.record(stream)

@@ -364,6 +364,14 @@ int lbx_sim_particles(lbx_sim* sim, int64_t* n, void* stream);
 #define LBX_PIC_DEFER_CURRENT 8u   /* stop after push + compaction: the      */
                                    /* cell accumulator stays for a cross-GPU */
                                    /* reduction, then lbx_pic_finish         */
+#define LBX_PIC_TILED 128u         /* in place, one CTA per 16x16-cell tile: */
+                                   /* field patch and current in shared      */
+                                   /* memory, node-centric int64 current.    */
+                                   /* Tile slot ranges come from the last    */
+                                   /* lbx_pic_sort with this flag (stale     */
+                                   /* ranges cost speed, never correctness). */
+                                   /* Sparse plasmas; not with sorted mode   */
+                                   /* or LBX_PIC_DEFER_CURRENT               */
 
 typedef struct lbx_pic_args {
   double* z;
@@ -406,8 +414,9 @@ int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* args, void* stream);
  * count) by cell into out[] (order within a cell not kept; the caller swaps
  * in/out).  Run every few steps it keeps an in-place run at the speed of a
  * freshly cell-ordered input (the deposit's register runs follow cell
- * order) without sort-on-write's per-step cost.  Fields, args' physics
- * fields and flags are ignored. */
+ * order) without sort-on-write's per-step cost.  With LBX_PIC_TILED in
+ * flags the key is tile-major (16x16-cell tiles) and the tiles' slot ranges
+ * are kept for LBX_PIC_TILED steps.  Fields and physics args are ignored. */
 int lbx_pic_sort(lbx_ctx* ctx, const lbx_pic_args* args, void* stream);
 
 /* Multi-GPU PIC (guard-cell current sum): after a LBX_PIC_DEFER_CURRENT step

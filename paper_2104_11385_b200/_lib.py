@@ -127,6 +127,7 @@ LBX_PIC_DEFER_CURRENT = 8
 LBX_PIC_QUAD = 16
 LBX_PIC_STABLE_ORDER = 64
 LBX_PIC_DIRECT = 32
+LBX_PIC_TILED = 128
 
 
 class PicArgs(C.Structure):

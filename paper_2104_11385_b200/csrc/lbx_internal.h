@@ -72,6 +72,11 @@ struct lbx_ctx {
   const void* pic_sort_next = nullptr;    // z array whose cell slots are in the cursors
   long long* pic_fill = nullptr;          // sorted mode: removed list, holes, tail flags [3][cap]
   int64_t pic_fill_cap = 0;
+  unsigned* pic_tiles = nullptr;          // tiled mode: slot ranges of the last tile-major sort
+  int64_t pic_tiles_cap = 0;
+  int pic_tiles_nz = 0, pic_tiles_nx = 0; //   grid they describe (0: none)
+  unsigned long long* pic_jn = nullptr;   // tiled mode: node-centric current [3][(nz+2)(nx+2)] + box
+  int64_t pic_jn_stride = 0;
   long long* fill_scratch = nullptr;      // hole-fill: holes[cap] + tail flags[cap]
   int64_t fill_cap = 0;
   bool timing = false;                    // lbx_ctx_enable_timing

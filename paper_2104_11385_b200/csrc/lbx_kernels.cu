@@ -1656,6 +1656,8 @@ int lbx_ctx_destroy(lbx_ctx* ctx) {
   if (ctx->pic_quad) cudaFree(ctx->pic_quad);
   if (ctx->pic_sortbuf) cudaFree(ctx->pic_sortbuf);
   if (ctx->pic_fill) cudaFree(ctx->pic_fill);
+  if (ctx->pic_tiles) cudaFree(ctx->pic_tiles);
+  if (ctx->pic_jn) cudaFree(ctx->pic_jn);
   if (ctx->fill_scratch) cudaFree(ctx->fill_scratch);
   if (ctx->ev0) cudaEventDestroy((cudaEvent_t)ctx->ev0), cudaEventDestroy((cudaEvent_t)ctx->ev1);
   delete ctx;

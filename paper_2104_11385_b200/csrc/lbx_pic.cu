@@ -88,6 +88,11 @@ struct PicParams {
   long long* n_out;
   long long* err_out;
   double wp, wc, cells;
+  // tiled mode (sparse plasmas): ranges of the last tile-major sort
+  const unsigned* tile_rd;      // first slot of each tile's particles [ntiles + 1]
+  unsigned long long* Jn;       // node-centric fixed-point current [3][(nz+2)(nx+2)]
+  long long jn_stride;
+  int ntx, ntiles;
 };
 
 __device__ __forceinline__ long long warp_min(long long v) {
@@ -578,17 +583,426 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
   }
 }
 
+// ---------------------------------------------------------------------------
+// Tiled in-place mode (LBX_PIC_TILED; sparse plasmas such as SURVEY 8d's
+// 8-ppc roofline case).  There the cell-centric accumulator costs 128 B per
+// cell per step and the direct gather waits on L2 for 24 scalar loads per
+// particle.  lbx_pic_sort with LBX_PIC_TILED orders the particles by a
+// tile-major cell key (16 x 16-cell tiles) and records each tile's slot range;
+// then, step after step in place, one CTA takes one tile's particles:
+//   * the tile's field patch (the tile plus kGd cells of drift margin and the
+//     stencil's nodes) is staged in shared memory: a gather is 4 LDS;
+//   * lane run sums go through the warp queue into a shared 64-bit node
+//     accumulator (lo/hi int32 pair: a 32-bit shared atomic plus a carry
+//     atomic -- exact for any count; 64-bit shared atomics are CAS loops),
+//     added to the node-centric int64 current Jn once per tile;
+//   * a particle outside the patch (drifted further since the sort, or moved
+//     in by hole filling) takes the global path: direct gather, RED into Jn.
+// Integer sums are order independent: J is bit-identical to the other modes.
+constexpr int kT = 16;                  // tile edge (cells)
+constexpr int kTileShift = 8;           // keys per tile
+constexpr int kGd = 3;                  // drift margin (cells) around the tile
+constexpr int kPP = kT + 2 * kGd + 2;   // patch edge in padded nodes
+constexpr int kPatch = kPP * kPP;
+constexpr int kQCapT = 64;              // flush-queue entries per warp (tiled kernel)
+
+__device__ __forceinline__ int tile_key(int i, int j, int ntx) {
+  return ((((i >> 4) * ntx) + (j >> 4)) << kTileShift) | ((i & 15) << 4) | (j & 15);
+}
+
+// cell-relative slot -> node (i + dr, j + ds) of component comp (the
+// pic_current_kernel mapping: Jx 2x3, Jy 2x2, Jz 3x2)
+__device__ __forceinline__ void slot_node(int sl, int& comp, int& dr, int& ds) {
+  if (sl < 6) {
+    comp = 0;
+    dr = sl >= 3 ? 1 : 0;
+    ds = sl - 3 * dr - 1;
+  } else if (sl < 10) {
+    comp = 1;
+    dr = (sl - 6) >> 1;
+    ds = (sl - 6) & 1;
+  } else {
+    comp = 2;
+    dr = ((sl - 10) >> 1) - 1;
+    ds = (sl - 10) & 1;
+  }
+}
+
+// every node a gather or deposit of cell (i, j) touches lies in the patch of
+// the tile with origin (tz, tx)
+__device__ __forceinline__ bool in_patch(int i, int j, int tz, int tx) {
+  return (unsigned)(i - tz + kGd) <= (unsigned)(kT - 1 + 2 * kGd) &&
+         (unsigned)(j - tx + kGd) <= (unsigned)(kT - 1 + 2 * kGd);
+}
+
+// local patch index of the padded node (P, Q)
+__device__ __forceinline__ int patch_at(int P, int Q, int tz, int tx) {
+  return (P - tz + kGd) * kPP + (Q - tx + kGd);
+}
+
+__device__ __forceinline__ float gather_s(const float* s_f, int c, int i0, int j0, float fz,
+                                          float fx, int tz, int tx) {
+  const float* F = s_f + c * kPatch + patch_at(i0 + 1, j0 + 1, tz, tx);
+  return cic(make_float4(F[0], F[1], F[kPP], F[kPP + 1]), fz, fx);
+}
+
+// exact 64-bit shared accumulation from 32-bit atomics
+__device__ __forceinline__ void sadd64(unsigned* lo, int* hi, int v) {
+  const unsigned old = atomicAdd(lo, (unsigned)v);
+  const unsigned nw = old + (unsigned)v;
+  const int d = (v < 0 ? -1 : 0) + (nw < old ? 1 : 0);
+  if (d) atomicAdd(hi, d);
+}
+
+__device__ __forceinline__ void enqueue_t(FlushEntry* e, const int v[kNodes], int i, int j) {
+#pragma unroll
+  for (int k = 0; k < kNodes / 4; ++k) e->v[k] = make_int4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  e->cell = i;
+  e->m = (unsigned)j;
+}
+
+__device__ __forceinline__ void drain_tile(const PicParams& p, const FlushEntry* q, int count,
+                                           int lane, unsigned* s_lo, int* s_hi, int tz, int tx) {
+  __syncwarp();
+  const int node = lane & 15;
+  int comp, dr, ds;
+  slot_node(node, comp, dr, ds);
+  for (int e0 = 0; e0 < count; e0 += 2) {
+    const int e = e0 + (lane >> 4);
+    if (e < count) {
+      const int i = q[e].cell, j = (int)q[e].m;
+      const int v = reinterpret_cast<const int*>(q[e].v)[node];
+      if (v) {
+        if (in_patch(i, j, tz, tx)) {
+          const int o = comp * kPatch + patch_at(i + dr + 1, j + ds + 1, tz, tx);
+          sadd64(s_lo + o, s_hi + o, v);
+        } else {
+          red_add(p.Jn + comp * p.jn_stride + (long long)(i + dr + 1) * p.pitch + (j + ds + 1), v);
+        }
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// kG consecutive doubles, stored back only for particles of this tile:
+// one vector store when the whole group is ours, else per particle.
+__device__ __forceinline__ void stg_mask(double* a, long long i, long long lo, long long hi,
+                                         const double v[kG]) {
+  if (i >= lo && i + kG <= hi) {
+    stg(a, i, hi, v);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kG; ++j)
+      if (i + j >= lo && i + j < hi) __stcs(a + i + j, v[j]);
+  }
+}
+
+template <bool kClock>
+__global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_tile_kernel(PicParams p) {
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  FlushEntry* s_q = reinterpret_cast<FlushEntry*>(s_dyn) + (size_t)(threadIdx.x >> 5) * kQCapT;
+  float* s_f = reinterpret_cast<float*>(s_dyn + (size_t)kPW * kQCapT * sizeof(FlushEntry));  // [6][kPatch]
+  unsigned* s_lo = reinterpret_cast<unsigned*>(s_f + 6 * kPatch);                            // [3][kPatch]
+  int* s_hi = reinterpret_cast<int*>(s_lo + 3 * kPatch);                                     // [3][kPatch]
+  unsigned* s_cnt = reinterpret_cast<unsigned*>(s_hi + 3 * kPatch);                          // nb
+  unsigned* s_clk = s_cnt + p.nb;                                                            // nb
+  __shared__ long long s_n;
+  __shared__ int s_box[4];
+  __shared__ int s_last;
+  __shared__ unsigned long long s_red[kPW];
+  __shared__ long long s_min[kPW];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    s_n = *((volatile long long*)&p.st->n);
+    s_box[0] = INT_MAX;
+    s_box[1] = INT_MIN;
+    s_box[2] = INT_MAX;
+    s_box[3] = INT_MIN;
+  }
+  for (int b = tid; b < p.nb; b += kPB) {
+    s_cnt[b] = 0u;
+    if (kClock) s_clk[b] = 0u;
+  }
+  __syncthreads();
+  const long long n = s_n;
+  const double ez = (double)p.nz, ex = (double)p.nx;
+  const double h = 0.5 * p.qm * p.dt;
+  unsigned long long removed = 0;
+  long long first_out = LLONG_MAX, err = 0;
+  int bimin = INT_MAX, bimax = INT_MIN, bjmin = INT_MAX, bjmax = INT_MIN;
+
+  for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+    // the ranges partition [0, n_sort); the last one is extended to n, so any
+    // input (even one the ranges do not describe) is processed exactly once
+    const long long lo = min((long long)p.tile_rd[tile], n);
+    const long long hi = tile == p.ntiles - 1 ? n : min((long long)p.tile_rd[tile + 1], n);
+    if (lo >= hi) continue;   // CTA-uniform
+    const int tz = (tile / p.ntx) * kT, tx = (tile % p.ntx) * kT;
+    const int P0 = tz - kGd, Q0 = tx - kGd;   // padded index of patch row / column 0
+    __syncthreads();                          // the previous tile's patch and sums are done
+    for (int o = tid; o < 6 * kPatch; o += kPB) {
+      const int c = o / kPatch, rr = (o - c * kPatch) / kPP, cc = o - c * kPatch - rr * kPP;
+      const int P = P0 + rr, Q = Q0 + cc;
+      s_f[o] = (P >= 0 && P < p.nz + 2 && Q >= 0 && Q < p.nx + 2)
+                   ? __ldg(p.F[c] + (long long)P * p.pitch + Q)
+                   : 0.f;
+    }
+    for (int o = tid; o < 3 * kPatch; o += kPB) {
+      s_lo[o] = 0u;
+      s_hi[o] = 0;
+    }
+    __syncthreads();
+    const long long a0 = lo & ~(long long)(kG - 1);   // group starts stay 32-byte aligned
+    const int run = min(kRun, (int)(((hi - a0 + kPB - 1) / kPB + kG - 1) / kG) * kG);
+    for (long long w = a0 + (long long)warp * 32 * run; w < hi; w += (long long)kPW * 32 * run) {
+      const long long run0 = w + (long long)lane * run;
+      int acc[kNodes];
+#pragma unroll
+      for (int i = 0; i < kNodes; ++i) acc[i] = 0;
+      int cur = -1, cur_i = 0, cur_j = 0;
+      int hb = -1;
+      unsigned hn = 0;
+      long long t_last = 0;
+      if (kClock) t_last = clock64();
+#pragma unroll 1
+      for (int g = 0; g < run / kG; ++g) {
+        const long long i0 = run0 + g * kG;
+        if (__all_sync(kAll, i0 >= hi)) break;
+        double pz[kG], px[kG], puz[kG], pux[kG], puy[kG];
+        ldg(p.z, i0, hi, pz);
+        ldg(p.x, i0, hi, px);
+        ldg(p.uz, i0, hi, puz);
+        ldg(p.ux, i0, hi, pux);
+        ldg(p.uy, i0, hi, puy);
+        bool keep[kG];
+        int nkey[kG];
+        float vsx[kG], vsy[kG], vsz[kG];
+#pragma unroll
+        for (int k = 0; k < kG; ++k) {
+          const bool valid = i0 + k >= lo && i0 + k < hi;
+          const Axis az = axis_of(pz[k]), ax = axis_of(px[k]);
+          float Ex, Ey, Ez, Bx, By, Bz;
+          if (in_patch(az.i, ax.i, tz, tx)) {
+            Ex = gather_s(s_f, 0, az.i, ax.ih, az.f, ax.fh, tz, tx);
+            Ey = gather_s(s_f, 1, az.i, ax.i, az.f, ax.f, tz, tx);
+            Ez = gather_s(s_f, 2, az.ih, ax.i, az.fh, ax.f, tz, tx);
+            Bx = gather_s(s_f, 3, az.ih, ax.i, az.fh, ax.f, tz, tx);
+            By = gather_s(s_f, 4, az.ih, ax.ih, az.fh, ax.fh, tz, tx);
+            Bz = gather_s(s_f, 5, az.i, ax.ih, az.f, ax.fh, tz, tx);
+          } else {
+            Ex = gather_c<false>(p, 0, az.i, ax.ih, az.f, ax.fh);
+            Ey = gather_c<false>(p, 1, az.i, ax.i, az.f, ax.f);
+            Ez = gather_c<false>(p, 2, az.ih, ax.i, az.fh, ax.f);
+            Bx = gather_c<false>(p, 3, az.ih, ax.i, az.fh, ax.f);
+            By = gather_c<false>(p, 4, az.ih, ax.ih, az.fh, ax.fh);
+            Bz = gather_c<false>(p, 5, az.i, ax.ih, az.f, ax.fh);
+          }
+          // relativistic Boris (x, y, z order; oracle boris())
+          const double hEx = __dmul_rn(h, (double)Ex), hEy = __dmul_rn(h, (double)Ey),
+                       hEz = __dmul_rn(h, (double)Ez);
+          const double mx = __dadd_rn(pux[k], hEx);
+          const double my = __dadd_rn(puy[k], hEy);
+          const double mz = __dadd_rn(puz[k], hEz);
+          const double gg = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(mx, mx)),
+                                                           __dmul_rn(my, my)), __dmul_rn(mz, mz)));
+          const double ig = __drcp_rn(gg);
+          const double tbx = __dmul_rn(__dmul_rn(h, (double)Bx), ig);
+          const double tby = __dmul_rn(__dmul_rn(h, (double)By), ig);
+          const double tbz = __dmul_rn(__dmul_rn(h, (double)Bz), ig);
+          const double s2 = __dmul_rn(2.0, __drcp_rn(__dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(tbx, tbx)),
+                                                                         __dmul_rn(tby, tby)),
+                                                               __dmul_rn(tbz, tbz))));
+          const double qx = __dadd_rn(mx, __dsub_rn(__dmul_rn(my, tbz), __dmul_rn(mz, tby)));
+          const double qy = __dadd_rn(my, __dsub_rn(__dmul_rn(mz, tbx), __dmul_rn(mx, tbz)));
+          const double qz = __dadd_rn(mz, __dsub_rn(__dmul_rn(mx, tby), __dmul_rn(my, tbx)));
+          pux[k] = __dadd_rn(__dadd_rn(mx, __dmul_rn(s2, __dsub_rn(__dmul_rn(qy, tbz), __dmul_rn(qz, tby)))), hEx);
+          puy[k] = __dadd_rn(__dadd_rn(my, __dmul_rn(s2, __dsub_rn(__dmul_rn(qz, tbx), __dmul_rn(qx, tbz)))), hEy);
+          puz[k] = __dadd_rn(__dadd_rn(mz, __dmul_rn(s2, __dsub_rn(__dmul_rn(qx, tby), __dmul_rn(qy, tbx)))), hEz);
+          const double gam = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(pux[k], pux[k])),
+                                                            __dmul_rn(puy[k], puy[k])),
+                                                  __dmul_rn(puz[k], puz[k])));
+          const double igam = __drcp_rn(gam);
+          pz[k] = __dadd_rn(pz[k], __dmul_rn(__dmul_rn(p.dt, puz[k]), igam));
+          px[k] = __dadd_rn(px[k], __dmul_rn(__dmul_rn(p.dt, pux[k]), igam));
+          keep[k] = valid && pz[k] >= 0.0 && pz[k] < ez && px[k] >= 0.0 && px[k] < ex;
+          nkey[k] = keep[k] ? (int)pz[k] * p.nx + (int)px[k] : -1;
+          const double qwg = keep[k] ? p.qw : 0.0;
+          vsx[k] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, pux[k]), igam)), p.vscale);
+          vsy[k] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, puy[k]), igam)), p.vscale);
+          vsz[k] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, puz[k]), igam)), p.vscale);
+          if (valid && !keep[k]) {
+            ++removed;
+            first_out = min(first_out, i0 + k);
+            if (p.removed_list) {
+              const unsigned long long slot = atomicAdd(&p.st->removed_count, 1ull);
+              if ((long long)slot < p.removed_cap) p.removed_list[slot] = i0 + k;
+            }
+          }
+        }
+        stg_mask(p.oz, i0, lo, hi, pz);
+        stg_mask(p.ox, i0, lo, hi, px);
+        stg_mask(p.ouz, i0, lo, hi, puz);
+        stg_mask(p.oux, i0, lo, hi, pux);
+        stg_mask(p.ouy, i0, lo, hi, puy);
+        // current: register runs -> warp queue -> shared (patch) / global
+        const unsigned lt = (1u << lane) - 1u;
+        int qn = 0;
+#pragma unroll
+        for (int k = 0; k < kG; ++k) {
+          const bool dep = nkey[k] >= 0;
+          const Axis az = axis_of(dep ? pz[k] : 0.5), ax = axis_of(dep ? px[k] : 0.5);
+          int q[kNodes];
+          node_values(az, ax, vsx[k], vsy[k], vsz[k], q);
+          const bool same = dep && nkey[k] == cur;
+          const bool strag = dep && !same && cur >= 0 && k + 1 < kG && nkey[k + 1] != nkey[k];
+          const bool swap = dep && !same && !strag;
+          const bool need = strag || (swap && cur >= 0);
+          const unsigned fm = __ballot_sync(kAll, need);
+          if (need) {
+            if (strag) enqueue_t(s_q + qn + __popc(fm & lt), q, az.i, ax.i);
+            else enqueue_t(s_q + qn + __popc(fm & lt), acc, cur_i, cur_j);
+          }
+          qn += __popc(fm);
+          if (kQCapT < 32 * kG && qn > kQCapT - 32) {
+            drain_tile(p, s_q, qn, lane, s_lo, s_hi, tz, tx);
+            qn = 0;
+          }
+          if (same) {
+#pragma unroll
+            for (int i = 0; i < kNodes; ++i) acc[i] += q[i];
+          } else if (swap) {
+#pragma unroll
+            for (int i = 0; i < kNodes; ++i) acc[i] = q[i];
+            cur = nkey[k];
+            cur_i = az.i;
+            cur_j = ax.i;
+          }
+          if (!dep) continue;
+          bimin = min(bimin, az.i);
+          bimax = max(bimax, az.i);
+          bjmin = min(bjmin, ax.i);
+          bjmax = max(bjmax, ax.i);
+          const int bz = az.i >> p.log2m, bx = ax.i >> p.log2m;
+          if (bz >= p.nbz || bx >= p.nbx) {
+            ++err;
+          } else if (bz * p.nbx + bx == hb) {
+            ++hn;
+          } else {
+            if (hb >= 0) {
+              atomicAdd(s_cnt + hb, hn);
+              if (kClock) {
+                const long long t = clock64();
+                atomicAdd(s_clk + hb, (unsigned)min((t - t_last) >> 4, (long long)(1u << 30)));
+                t_last = t;
+              }
+            }
+            hb = bz * p.nbx + bx;
+            hn = 1;
+          }
+        }
+        if (qn) drain_tile(p, s_q, qn, lane, s_lo, s_hi, tz, tx);
+      }
+      {
+        const unsigned fm = __ballot_sync(kAll, cur >= 0);
+        if (cur >= 0) enqueue_t(s_q + __popc(fm & ((1u << lane) - 1u)), acc, cur_i, cur_j);
+        if (fm) drain_tile(p, s_q, __popc(fm), lane, s_lo, s_hi, tz, tx);
+      }
+      unsigned tclk = 0;
+      if (kClock && hb >= 0) tclk = (unsigned)min((clock64() - t_last) >> 4, (long long)(1u << 30));
+      const int hb0 = __shfl_sync(kAll, hb, 0);
+      if (__all_sync(kAll, hb == hb0)) {
+        const unsigned tot = __reduce_add_sync(kAll, hn);
+        const unsigned clk = kClock ? __reduce_add_sync(kAll, tclk) : 0u;
+        if (lane == 0 && hb0 >= 0 && tot) {
+          atomicAdd(s_cnt + hb0, tot);
+          if (kClock) atomicAdd(s_clk + hb0, clk);
+        }
+      } else if (hb >= 0 && hn) {
+        atomicAdd(s_cnt + hb, hn);
+        if (kClock) atomicAdd(s_clk + hb, tclk);
+      }
+    }
+    __syncthreads();
+    for (int o = tid; o < 3 * kPatch; o += kPB) {   // the tile's node sums -> Jn
+      const long long v = (long long)(((unsigned long long)(unsigned)s_hi[o] << 32) | s_lo[o]);
+      if (!v) continue;
+      const int c = o / kPatch, rr = (o - c * kPatch) / kPP, cc = o - c * kPatch - rr * kPP;
+      red_add(p.Jn + c * p.jn_stride + (long long)(P0 + rr) * p.pitch + (Q0 + cc), v);
+    }
+  }
+
+  // ---- CTA totals, deposit box, histogram flush, epilogue (as pic_push_kernel) ----
+  const unsigned long long wa = (unsigned long long)warp_sum((long long)removed);
+  const long long wm = warp_min(first_out), we = warp_sum(err);
+  const int wimin = __reduce_min_sync(kAll, bimin), wimax = __reduce_max_sync(kAll, bimax);
+  const int wjmin = __reduce_min_sync(kAll, bjmin), wjmax = __reduce_max_sync(kAll, bjmax);
+  if (lane == 0) {
+    s_red[warp] = wa;
+    s_min[warp] = wm;
+    if (we) atomicAdd((unsigned long long*)&p.st->err, (unsigned long long)we);
+    if (wimin <= wimax) {
+      atomicMin(&s_box[0], wimin);
+      atomicMax(&s_box[1], wimax);
+      atomicMin(&s_box[2], wjmin);
+      atomicMax(&s_box[3], wjmax);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long ta = 0;
+    long long tm = LLONG_MAX;
+    for (int w2 = 0; w2 < kPW; ++w2) {
+      ta += s_red[w2];
+      tm = min(tm, s_min[w2]);
+    }
+    if (ta) {
+      atomicAdd(&p.st->leavers, ta);
+      atomicMin(&p.st->first_leaver, tm);
+    }
+    if (s_box[0] <= s_box[1]) {
+      atomicMin(p.dep_box + 0, s_box[0]);
+      atomicMax(p.dep_box + 1, s_box[1]);
+      atomicMin(p.dep_box + 2, s_box[2]);
+      atomicMax(p.dep_box + 3, s_box[3]);
+    }
+  }
+  for (int b = tid; b < p.nb; b += kPB) {
+    if (s_cnt[b]) atomicAdd(p.g_cnt + b, (unsigned long long)s_cnt[b]);
+    if (kClock && s_clk[b]) atomicAdd(p.g_clk + b, (unsigned long long)s_clk[b]);
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(&p.st->done, 1u) == gridDim.x - 1) ? 1 : 0;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  step_record<kClock>(p.g_cnt, p.g_clk, p.nb, p.counts_out, p.cost_out, p.clk_out, p.wp, p.wc,
+                      p.cells, 4);
+  if (tid == 0) {
+    const long long n_new = n - (long long)*((volatile unsigned long long*)&p.st->leavers);
+    if (p.n_out) *p.n_out = n_new;
+    if (p.err_out) *p.err_out = *((volatile long long*)&p.st->err);
+    p.st->n_old = n;
+    p.st->n = n_new;
+    p.st->done = 0u;
+    __threadfence_system();
+  }
+}
+
 // Sorted mode, resynchronisation: particles per cell of the current
 // positions (runs of equal cells per lane -> one RED each).
 __global__ void pic_count_kernel(const double* __restrict__ z, const double* __restrict__ x,
-                                 const DevState* st, unsigned* cell_cnt, int nx) {
+                                 const DevState* st, unsigned* cell_cnt, int nx, int ntx = 0) {
   const long long n = st->n;
   for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r * kRun < n;
        r += (long long)gridDim.x * blockDim.x) {
     int cur = -1;
     unsigned m = 0;
     for (long long i = r * kRun; i < min(n, (r + 1) * kRun); ++i) {
-      const int key = (int)__ldg(z + i) * nx + (int)__ldg(x + i);
+      const int iz = (int)__ldg(z + i), ix = (int)__ldg(x + i);
+      const int key = ntx ? tile_key(iz, ix, ntx) : iz * nx + ix;
       if (key != cur) {
         if (m) red_add32(cell_cnt + cur, m);
         cur = key;
@@ -609,7 +1023,7 @@ __global__ void pic_sort_scatter_kernel(const double* __restrict__ z, const doub
                                         const double* __restrict__ ux,
                                         const double* __restrict__ uy, double* oz, double* ox,
                                         double* ouz, double* oux, double* ouy, const DevState* st,
-                                        unsigned* cursor, int nx) {
+                                        unsigned* cursor, int nx, int ntx) {
   const long long n = st->n;
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
@@ -620,7 +1034,7 @@ __global__ void pic_sort_scatter_kernel(const double* __restrict__ z, const doub
     const unsigned act = __ballot_sync(kAll, live);
     if (!live) continue;
     const double zi = z[i], xi = x[i];
-    const int key = (int)zi * nx + (int)xi;
+    const int key = ntx ? tile_key((int)zi, (int)xi, ntx) : (int)zi * nx + (int)xi;
     const unsigned grp = __match_any_sync(act, key);
     const int leader = __ffs(grp) - 1;
     unsigned base = 0;
@@ -658,7 +1072,8 @@ __global__ void pic_scan_reduce_kernel(const unsigned* __restrict__ cell_cnt, lo
 }
 
 __global__ void pic_scan_apply_kernel(unsigned* cell_cnt, long long cells,
-                                      const unsigned* __restrict__ block_sum, unsigned* cursor) {
+                                      const unsigned* __restrict__ block_sum, unsigned* cursor,
+                                      unsigned* tile_start = nullptr) {
   __shared__ unsigned w[32];
   __shared__ unsigned s_base;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -705,6 +1120,10 @@ __global__ void pic_scan_apply_kernel(unsigned* cell_cnt, long long cells,
     if (c < b) {
       cursor[c] = excl;
       cell_cnt[c] = 0u;
+      if (tile_start) {   // tile-major keys: 2^kTileShift per tile; [ntiles] = total
+        if ((c & ((1 << kTileShift) - 1)) == 0) tile_start[c >> kTileShift] = excl;
+        if (c == cells - 1) tile_start[cells >> kTileShift] = excl + v;
+      }
     }
     // next chunk's base = excl of the last thread + its v
     __syncthreads();
@@ -840,6 +1259,33 @@ __global__ void pic_zero_kernel(unsigned long long* Jc, const int* dep_box, int 
   }
 }
 
+// Tiled mode: Jn (node-centric int64) -> J over the deposit box's nodes,
+// clearing Jn; the same float32 rounding of the same integer node sums as
+// pic_current_kernel.
+__global__ void pic_current_node_kernel(unsigned long long* Jn, long long stride,
+                                        const int* dep_box, float* Jx, float* Jy, float* Jz,
+                                        int nz, int nx, double inv_scale) {
+  const int bi0 = dep_box[0], bi1 = dep_box[1], bj0 = dep_box[2], bj1 = dep_box[3];
+  if (bi0 > bi1) return;
+  // nodes of cells [bi0, bi1] x [bj0, bj1]: padded rows bi0 .. bi1 + 2
+  const int r0 = max(bi0, 0), r1 = min(bi1 + 2, nz + 1), c0 = max(bj0, 0), c1 = min(bj1 + 2, nx + 1);
+  const int C = c1 - c0 + 1, pitch = nx + 2;
+  const long long all = (long long)(r1 - r0 + 1) * C;
+  float* J[3] = {Jx, Jy, Jz};
+  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < all;
+       o += (long long)gridDim.x * blockDim.x) {
+    const long long idx = (long long)(r0 + (int)(o / C)) * pitch + (c0 + (int)(o % C));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const long long v = (long long)Jn[c * stride + idx];
+      if (v) {
+        J[c][idx] = __fadd_rn(J[c][idx], (float)__dmul_rn((double)v, inv_scale));
+        Jn[c * stride + idx] = 0ull;
+      }
+    }
+  }
+}
+
 // Yee update, interior cells; float32 storage, float64 arithmetic in the
 // oracle's evaluation order.
 __global__ void pic_b_kernel(const float* __restrict__ Ex, const float* __restrict__ Ey,
@@ -891,14 +1337,22 @@ int cuda_fail(cudaError_t e, const char* what) {
 }
 
 // Jc -> J over the deposit box, clear Jc, Yee update (unless disabled).
-int pic_finish(lbx_ctx* ctx, const lbx_pic_args* a, cudaStream_t s, double jscale) {
+int pic_finish(lbx_ctx* ctx, const lbx_pic_args* a, cudaStream_t s, double jscale,
+               bool tiled = false) {
   const long long cells = (long long)a->nz * a->nx;
   const int pitch = a->nx + 2;
-  int* dep_box = reinterpret_cast<int*>(ctx->pic_acc + ctx->pic_cells * kNodes);
   const unsigned cg = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 8, (cells + 255) / 256));
-  pic_current_kernel<<<cg, 256, 0, s>>>(ctx->pic_acc, dep_box, a->current[0], a->current[1],
-                                        a->current[2], a->nz, a->nx, 1.0 / jscale);
-  pic_zero_kernel<<<cg, 256, 0, s>>>(ctx->pic_acc, dep_box, a->nx);
+  if (tiled) {
+    const int* box = reinterpret_cast<const int*>(ctx->pic_jn + 3 * ctx->pic_jn_stride);
+    pic_current_node_kernel<<<cg, 256, 0, s>>>(ctx->pic_jn, ctx->pic_jn_stride, box, a->current[0],
+                                               a->current[1], a->current[2], a->nz, a->nx,
+                                               1.0 / jscale);
+  } else {
+    int* dep_box = reinterpret_cast<int*>(ctx->pic_acc + ctx->pic_cells * kNodes);
+    pic_current_kernel<<<cg, 256, 0, s>>>(ctx->pic_acc, dep_box, a->current[0], a->current[1],
+                                          a->current[2], a->nz, a->nx, 1.0 / jscale);
+    pic_zero_kernel<<<cg, 256, 0, s>>>(ctx->pic_acc, dep_box, a->nx);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "current launch");
   if (a->flags & LBX_PIC_NO_FIELD_SOLVE) return LBX_OK;
@@ -943,6 +1397,12 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   }
   if (al & 31u) return set_error(LBX_EINVAL, "particle arrays must be 32-byte aligned");
   if (!(a->q_times_w != 0.0)) return set_error(LBX_EINVAL, "q_times_w must be nonzero");
+  const bool tiled = (a->flags & LBX_PIC_TILED) != 0;
+  if (tiled && sorted) return set_error(LBX_EINVAL, "LBX_PIC_TILED runs in place (no out[])");
+  if (tiled && (a->flags & LBX_PIC_DEFER_CURRENT))
+    return set_error(LBX_EINVAL, "LBX_PIC_TILED does not support LBX_PIC_DEFER_CURRENT");
+  if (tiled && (ctx->pic_tiles_nz != a->nz || ctx->pic_tiles_nx != a->nx))
+    return set_error(LBX_EINVAL, "LBX_PIC_TILED needs lbx_pic_sort with LBX_PIC_TILED on this grid first");
   const int nbz = a->nz / a->box_size, nbx = a->nx / a->box_size, nb = nbz * nbx;
   if (nb > 4096) return set_error(LBX_EINVAL, "PIC step supports <= 4096 boxes");
   int rc = ensure_accumulators(ctx, nb);
@@ -953,7 +1413,20 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   const long long cells = (long long)a->nz * a->nx;
   const long long quads = (long long)(a->nz + 1) * (a->nx + 1);
   if (!sorted) ctx->pic_sort_next = nullptr;   // an in-place step invalidates the cell slots
-  if (!ctx->pic_acc || ctx->pic_cells < cells) {
+  const long long jn_stride = (long long)(a->nz + 2) * (a->nx + 2);
+  if (tiled && (!ctx->pic_jn || ctx->pic_jn_stride != jn_stride)) {
+    if (ctx->pic_jn) {
+      cudaDeviceSynchronize();
+      cudaFree(ctx->pic_jn);
+    }
+    ctx->pic_jn = nullptr;
+    const size_t bytes = (size_t)jn_stride * 3 * 8 + 16;
+    if (cudaMalloc(&ctx->pic_jn, bytes) != cudaSuccess)
+      return set_error(LBX_EOOM, "PIC node current accumulators");
+    cudaMemsetAsync(ctx->pic_jn, 0, bytes, s);
+    ctx->pic_jn_stride = jn_stride;
+  }
+  if (!tiled && (!ctx->pic_acc || ctx->pic_cells < cells)) {
     if (ctx->pic_acc) {
       cudaDeviceSynchronize();
       cudaFree(ctx->pic_acc);
@@ -965,7 +1438,7 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
     cudaMemsetAsync(ctx->pic_acc, 0, bytes, s);
     ctx->pic_cells = cells;
   }
-  if (!ctx->pic_quad || ctx->pic_quads < quads) {
+  if (!tiled && (!ctx->pic_quad || ctx->pic_quads < quads)) {
     if (ctx->pic_quad) {
       cudaDeviceSynchronize();
       cudaFree(ctx->pic_quad);
@@ -1005,7 +1478,8 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   unsigned* cell_cnt = sorted ? ctx->pic_sortbuf : nullptr;
   unsigned* cursor = sorted ? ctx->pic_sortbuf + cells : nullptr;
   unsigned* block_sum = sorted ? ctx->pic_sortbuf + 2 * cells : nullptr;
-  int* dep_box = reinterpret_cast<int*>(ctx->pic_acc + ctx->pic_cells * kNodes);
+  int* dep_box = tiled ? reinterpret_cast<int*>(ctx->pic_jn + 3 * jn_stride)
+                       : reinterpret_cast<int*>(ctx->pic_acc + ctx->pic_cells * kNodes);
   PicParams p{};
   p.z = a->z;
   p.x = a->x;
@@ -1070,14 +1544,24 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   // direct gather (LBX_PIC_QUAD / LBX_PIC_DIRECT force either)
   bool quad = ctx->n_upper >= 16 * cells;
   if (a->flags & LBX_PIC_QUAD) quad = true;
-  if (a->flags & LBX_PIC_DIRECT) quad = false;
+  if ((a->flags & LBX_PIC_DIRECT) || tiled) quad = false;
   pic_quad_kernel<<<quad ? qg : 1, 256, 0, s>>>(a->fields[0], a->fields[1], a->fields[2],
                                                  a->fields[3], a->fields[4], a->fields[5], Q,
                                                  quad ? quads : 0, p.qpitch, pitch, dep_box);
-  const size_t smem = (size_t)kPW * kQCap * sizeof(FlushEntry) + (size_t)nb * 8;
   const bool clock = (a->flags & LBX_STEP_CLOCK) != 0;
+  size_t smem = (size_t)kPW * kQCap * sizeof(FlushEntry) + (size_t)nb * 8;
   void (*kern)(PicParams);
-  if (quad)
+  const int ntx = (a->nx + kT - 1) / kT, ntz = (a->nz + kT - 1) / kT;
+  if (tiled) {
+    smem = (size_t)kPW * kQCapT * sizeof(FlushEntry) + (size_t)6 * kPatch * 4 +
+           (size_t)6 * kPatch * 4 + (size_t)nb * 8;
+    kern = clock ? pic_tile_kernel<true> : pic_tile_kernel<false>;
+    p.tile_rd = ctx->pic_tiles;
+    p.Jn = ctx->pic_jn;
+    p.jn_stride = jn_stride;
+    p.ntx = ntx;
+    p.ntiles = ntz * ntx;
+  } else if (quad)
     kern = clock ? (sorted ? pic_push_kernel<true, true, true> : pic_push_kernel<true, false, true>)
                  : (sorted ? pic_push_kernel<false, true, true> : pic_push_kernel<false, false, true>);
   else
@@ -1090,7 +1574,7 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   long long grid = (long long)std::max(per_sm, 1) * ctx->num_sms;
   if (ctx->grid_override > 0) grid = ctx->grid_override;
   const long long units = (ctx->n_upper + kUnitP - 1) / kUnitP;
-  grid = std::max(1ll, std::min(grid, (units + kPW - 1) / kPW));
+  grid = std::max(1ll, std::min(grid, tiled ? (long long)ntz * ntx : (units + kPW - 1) / kPW));
   kern<<<(unsigned)grid, kPB, smem, s>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "pic_push_kernel launch");
@@ -1111,8 +1595,9 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
     pic_scan_apply_kernel<<<kScanBlocks, kScanThreads, 0, s>>>(cell_cnt, cells, block_sum, cursor);
     ctx->pic_sort_next = out[0];
   }
+  if (sorted) ctx->pic_tiles_nz = ctx->pic_tiles_nx = 0;   // sort-on-write moved the particles
   if (a->flags & LBX_PIC_DEFER_CURRENT) return LBX_OK;
-  return pic_finish(ctx, a, s, jscale);
+  return pic_finish(ctx, a, s, jscale, tiled);
 }
 
 
@@ -1126,33 +1611,53 @@ extern "C" int lbx_pic_sort(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   for (int c = 0; c < 5; ++c)
     if (!in[c] || !a->out[c]) return set_error(LBX_EINVAL, "lbx_pic_sort needs the 5 arrays and out[]");
   cudaStream_t s = (cudaStream_t)stream;
-  const long long cells = (long long)a->nz * a->nx;
-  if (!ctx->pic_sortbuf || ctx->pic_sort_cells < cells) {
+  const bool tiled = (a->flags & LBX_PIC_TILED) != 0;
+  const int ntx = (a->nx + kT - 1) / kT, ntz = (a->nz + kT - 1) / kT;
+  const long long ntiles = (long long)ntz * ntx;
+  // keys: row-major cells, or tile-major (2^kTileShift per tile, ragged tiles padded)
+  const long long keys = tiled ? ntiles << kTileShift : (long long)a->nz * a->nx;
+  if (!ctx->pic_sortbuf || ctx->pic_sort_cells < keys) {
     if (ctx->pic_sortbuf) {
       cudaDeviceSynchronize();
       cudaFree(ctx->pic_sortbuf);
     }
     ctx->pic_sortbuf = nullptr;
-    const size_t bytes = ((size_t)cells * 2 + kScanBlocks) * sizeof(unsigned);
+    const size_t bytes = ((size_t)keys * 2 + kScanBlocks) * sizeof(unsigned);
     if (cudaMalloc(&ctx->pic_sortbuf, bytes) != cudaSuccess)
       return set_error(LBX_EOOM, "PIC sort buffers");
     cudaMemsetAsync(ctx->pic_sortbuf, 0, bytes, s);
-    ctx->pic_sort_cells = cells;
+    ctx->pic_sort_cells = keys;
+  }
+  if (tiled && (!ctx->pic_tiles || ctx->pic_tiles_cap < ntiles + 1)) {
+    if (ctx->pic_tiles) {
+      cudaDeviceSynchronize();
+      cudaFree(ctx->pic_tiles);
+    }
+    ctx->pic_tiles = nullptr;
+    if (cudaMalloc(&ctx->pic_tiles, (size_t)(ntiles + 1) * sizeof(unsigned)) != cudaSuccess)
+      return set_error(LBX_EOOM, "PIC tile ranges");
+    ctx->pic_tiles_cap = ntiles + 1;
   }
   unsigned* cell_cnt = ctx->pic_sortbuf;
-  unsigned* cursor = ctx->pic_sortbuf + cells;
-  unsigned* block_sum = ctx->pic_sortbuf + 2 * cells;
+  unsigned* cursor = ctx->pic_sortbuf + keys;
+  unsigned* block_sum = ctx->pic_sortbuf + 2 * keys;
+  // sorted mode keeps its cursors in the same buffer at a row-major stride,
+  // which a padded tile-major count range can overlap
+  if (tiled) cudaMemsetAsync(cell_cnt, 0, (size_t)keys * sizeof(unsigned), s);
   const unsigned ng = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 8,
                                                        (long long)(ctx->n_upper / kRun + 255) / 256));
-  pic_count_kernel<<<ng, 256, 0, s>>>(a->z, a->x, ctx->st, cell_cnt, a->nx);
-  pic_scan_reduce_kernel<<<kScanBlocks, kScanThreads, 0, s>>>(cell_cnt, cells, block_sum);
-  pic_scan_apply_kernel<<<kScanBlocks, kScanThreads, 0, s>>>(cell_cnt, cells, block_sum, cursor);
+  pic_count_kernel<<<ng, 256, 0, s>>>(a->z, a->x, ctx->st, cell_cnt, a->nx, tiled ? ntx : 0);
+  pic_scan_reduce_kernel<<<kScanBlocks, kScanThreads, 0, s>>>(cell_cnt, keys, block_sum);
+  pic_scan_apply_kernel<<<kScanBlocks, kScanThreads, 0, s>>>(cell_cnt, keys, block_sum, cursor,
+                                                             tiled ? ctx->pic_tiles : nullptr);
   const unsigned sg = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 16,
                                                        (long long)(ctx->n_upper + 255) / 256));
   pic_sort_scatter_kernel<<<sg, 256, 0, s>>>(a->z, a->x, a->uz, a->ux, a->uy, a->out[0], a->out[1],
                                              a->out[2], a->out[3], a->out[4], ctx->st, cursor,
-                                             a->nx);
+                                             a->nx, tiled ? ntx : 0);
   ctx->pic_sort_next = nullptr;   // the cursors were consumed
+  ctx->pic_tiles_nz = tiled ? a->nz : 0;
+  ctx->pic_tiles_nx = tiled ? a->nx : 0;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "pic sort launch");
   return LBX_OK;

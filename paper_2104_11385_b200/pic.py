@@ -61,10 +61,12 @@ class PicState:
         return {k: v.cpu().numpy() for k, v in self.fields.items()}
 
 
-def pic_sort(ctx: Context, st: PicState):
+def pic_sort(ctx: Context, st: PicState, tiled: bool = False):
     """Counting sort of the particles by cell (lbx_pic_sort) into the spare
     buffers, which the state then swaps in.  Every few in-place steps this
-    restores the cell order the deposit's register runs feed on."""
+    restores the cell order the deposit's register runs feed on.  tiled=True
+    sorts by a tile-major key and records the tile ranges that
+    pic_step(tiled=True) works on."""
     dev = ctx.device
     names = ("z", "x", "uz", "ux", "uy")
     ctx.set_count(st.n)
@@ -74,6 +76,7 @@ def pic_sort(ctx: Context, st: PicState):
     a = _lib.PicArgs()
     a.z, a.x, a.uz, a.ux, a.uy = (_lib.ptr(getattr(st, k)) for k in names)
     a.nz, a.nx = st.nz, st.nx
+    a.flags = _lib.LBX_PIC_TILED if tiled else 0
     for i, t in enumerate(st.spare):
         a.out[i] = _lib.ptr(t)
     _lib.check(_lib.lib.lbx_pic_sort(ctx.handle, C.byref(a), _stream(dev)))
@@ -86,14 +89,17 @@ def pic_sort(ctx: Context, st: PicState):
 
 def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times_w: float,
              dt: float, weights=(0.75, 0.25), clock=False, field_solve=True, sort=False,
-             gather=None, stable=False):
+             gather=None, stable=False, tiled=False):
     """One PIC step; returns per-box counts / cost / clock and n.
 
     sort=False: in place; absorbed particles' slots are filled from the tail
     (O(absorbed)), or with stable=True the order is kept (stable compaction).
     sort=True: sort-on-write -- results land in a second buffer set grouped by
     each particle's cell at the start of the step, which the state then
-    swaps in (order within a cell is not deterministic; values are)."""
+    swaps in (order within a cell is not deterministic; values are).
+    tiled=True: in place, one CTA per 16x16-cell tile with the field patch
+    and the current in shared memory, on the tile ranges of the last
+    pic_sort(tiled=True) -- the sparse-plasma path."""
     dev = ctx.device
     nbz, nbx = st.nz // box_size, st.nx // box_size
     nb = nbz * nbx
@@ -117,6 +123,10 @@ def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times
         a.flags |= _lib.LBX_PIC_STABLE_ORDER
     if gather is not None:     # "quad" | "direct" (default: by particles per cell)
         a.flags |= {"quad": _lib.LBX_PIC_QUAD, "direct": _lib.LBX_PIC_DIRECT}[gather]
+    if tiled:
+        if sort:
+            raise ValueError("tiled steps run in place (sort=False)")
+        a.flags |= _lib.LBX_PIC_TILED
     a.counts_out, a.cost_out, a.clk_out = _lib.ptr(counts), _lib.ptr(cost), _lib.ptr(clk)
     a.n_out, a.err_out = _lib.ptr(nout), _lib.ptr(nout[1:])
     names = ("z", "x", "uz", "ux", "uy")
