@@ -9,7 +9,7 @@ CASES_P='tests/test_gpu_pic.py -k "first_step or (multi_step and clustered-quad)
 CASES_D='tests/test_gpu_dist.py -k "mini-2 and p2p"'
 CASES_E='tests/test_gpu_3d.py tests/test_gpu_pic.py -k "3d or hole_filling or (multi_step and direct) or gpuclock or timers"'
 CASES_R='tests/test_gpu_runs.py -k "(timers and not cupti) or gpuclock or (graph_replay and mini)"'
-CASES_S='tests/test_gpu_pic.py -k "periodic_cell_sort or share_a_state or reused_buffers"'
+CASES_S='tests/test_gpu_pic.py -k "periodic_cell_sort or share_a_state or reused_buffers or tiled"'
 for tool in ${SAN_TOOLS:-memcheck racecheck synccheck}; do
   for grp in ${SAN_GROUPS:-K P D E R S}; do
     eval cases=\$CASES_$grp
