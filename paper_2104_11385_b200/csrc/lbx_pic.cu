@@ -592,10 +592,11 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
 // then, step after step in place, one CTA takes one tile's particles:
 //   * the tile's field patch (the tile plus kGd cells of drift margin and the
 //     stencil's nodes) is staged in shared memory: a gather is 4 LDS;
-//   * lane run sums go through the warp queue into a shared 64-bit node
-//     accumulator (lo/hi int32 pair: a 32-bit shared atomic plus a carry
-//     atomic -- exact for any count; 64-bit shared atomics are CAS loops),
-//     added to the node-centric int64 current Jn once per tile;
+//   * lane run sums go through the warp queue into a shared node
+//     accumulator (16-bit halves summed by two fire-and-forget 32-bit shared
+//     atomics: exact below kSplitMax particles per tile; 64-bit shared
+//     atomics are CAS loops), added to the node-centric int64 current Jn
+//     once per tile; denser tiles add straight to Jn;
 //   * a particle outside the patch (drifted further since the sort, or moved
 //     in by hole filling) takes the global path: direct gather, RED into Jn.
 // Integer sums are order independent: J is bit-identical to the other modes.
@@ -646,12 +647,14 @@ __device__ __forceinline__ float gather_s(const float* s_f, int c, int i0, int j
   return cic(make_float4(F[0], F[1], F[kPP], F[kPP + 1]), fz, fx);
 }
 
-// exact 64-bit shared accumulation from 32-bit atomics
-__device__ __forceinline__ void sadd64(unsigned* lo, int* hi, int v) {
-  const unsigned old = atomicAdd(lo, (unsigned)v);
-  const unsigned nw = old + (unsigned)v;
-  const int d = (v < 0 ? -1 : 0) + (nw < old ? 1 : 0);
-  if (d) atomicAdd(hi, d);
+// Exact node sums from two fire-and-forget 32-bit shared atomics:
+// v = (v >> 16) * 2^16 + (v & 0xffff); the low halves (< 2^16 each) cannot
+// overflow int32 while a tile holds fewer than kSplitMax particles (each
+// particle adds to a node at most once); denser tiles go global.
+constexpr long long kSplitMax = 32768;
+__device__ __forceinline__ void sadd_split(unsigned* lo, int* hi, int v) {
+  atomicAdd(lo, (unsigned)(v & 0xffff));
+  atomicAdd(hi, v >> 16);
 }
 
 __device__ __forceinline__ void enqueue_t(FlushEntry* e, const int v[kNodes], int i, int j) {
@@ -662,7 +665,8 @@ __device__ __forceinline__ void enqueue_t(FlushEntry* e, const int v[kNodes], in
 }
 
 __device__ __forceinline__ void drain_tile(const PicParams& p, const FlushEntry* q, int count,
-                                           int lane, unsigned* s_lo, int* s_hi, int tz, int tx) {
+                                           int lane, unsigned* s_lo, int* s_hi, int tz, int tx,
+                                           bool dense) {
   __syncwarp();
   const int node = lane & 15;
   int comp, dr, ds;
@@ -673,9 +677,9 @@ __device__ __forceinline__ void drain_tile(const PicParams& p, const FlushEntry*
       const int i = q[e].cell, j = (int)q[e].m;
       const int v = reinterpret_cast<const int*>(q[e].v)[node];
       if (v) {
-        if (in_patch(i, j, tz, tx)) {
+        if (!dense && in_patch(i, j, tz, tx)) {
           const int o = comp * kPatch + patch_at(i + dr + 1, j + ds + 1, tz, tx);
-          sadd64(s_lo + o, s_hi + o, v);
+          sadd_split(s_lo + o, s_hi + o, v);
         } else {
           red_add(p.Jn + comp * p.jn_stride + (long long)(i + dr + 1) * p.pitch + (j + ds + 1), v);
         }
@@ -739,6 +743,7 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_tile_kernel(PicParams p
     const long long lo = min((long long)p.tile_rd[tile], n);
     const long long hi = tile == p.ntiles - 1 ? n : min((long long)p.tile_rd[tile + 1], n);
     if (lo >= hi) continue;   // CTA-uniform
+    const bool dense = hi - lo >= kSplitMax;
     const int tz = (tile / p.ntx) * kT, tx = (tile % p.ntx) * kT;
     const int P0 = tz - kGd, Q0 = tx - kGd;   // padded index of patch row / column 0
     __syncthreads();                          // the previous tile's patch and sums are done
@@ -866,7 +871,7 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_tile_kernel(PicParams p
           }
           qn += __popc(fm);
           if (kQCapT < 32 * kG && qn > kQCapT - 32) {
-            drain_tile(p, s_q, qn, lane, s_lo, s_hi, tz, tx);
+            drain_tile(p, s_q, qn, lane, s_lo, s_hi, tz, tx, dense);
             qn = 0;
           }
           if (same) {
@@ -902,12 +907,12 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_tile_kernel(PicParams p
             hn = 1;
           }
         }
-        if (qn) drain_tile(p, s_q, qn, lane, s_lo, s_hi, tz, tx);
+        if (qn) drain_tile(p, s_q, qn, lane, s_lo, s_hi, tz, tx, dense);
       }
       {
         const unsigned fm = __ballot_sync(kAll, cur >= 0);
         if (cur >= 0) enqueue_t(s_q + __popc(fm & ((1u << lane) - 1u)), acc, cur_i, cur_j);
-        if (fm) drain_tile(p, s_q, __popc(fm), lane, s_lo, s_hi, tz, tx);
+        if (fm) drain_tile(p, s_q, __popc(fm), lane, s_lo, s_hi, tz, tx, dense);
       }
       unsigned tclk = 0;
       if (kClock && hb >= 0) tclk = (unsigned)min((clock64() - t_last) >> 4, (long long)(1u << 30));
@@ -926,7 +931,7 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_tile_kernel(PicParams p
     }
     __syncthreads();
     for (int o = tid; o < 3 * kPatch; o += kPB) {   // the tile's node sums -> Jn
-      const long long v = (long long)(((unsigned long long)(unsigned)s_hi[o] << 32) | s_lo[o]);
+      const long long v = (long long)s_hi[o] * 65536 + (long long)s_lo[o];
       if (!v) continue;
       const int c = o / kPatch, rr = (o - c * kPatch) / kPP, cc = o - c * kPatch - rr * kPP;
       red_add(p.Jn + c * p.jn_stride + (long long)(P0 + rr) * p.pitch + (Q0 + cc), v);
