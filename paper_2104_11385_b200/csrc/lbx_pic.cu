@@ -600,15 +600,23 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
 //   * a particle outside the patch (drifted further since the sort, or moved
 //     in by hole filling) takes the global path: direct gather, RED into Jn.
 // Integer sums are order independent: J is bit-identical to the other modes.
-constexpr int kT = 16;                  // tile edge (cells)
-constexpr int kTileShift = 8;           // keys per tile
+#ifndef LBX_PIC_TILE_LOG2
+#define LBX_PIC_TILE_LOG2 4
+#endif
+constexpr int kTS = LBX_PIC_TILE_LOG2;  // tile edge 2^kTS cells
+constexpr int kT = 1 << kTS;
+constexpr int kTileShift = 2 * kTS;     // keys per tile
 constexpr int kGd = 3;                  // drift margin (cells) around the tile
 constexpr int kPP = kT + 2 * kGd + 2;   // patch edge in padded nodes
 constexpr int kPatch = kPP * kPP;
-constexpr int kQCapT = 64;              // flush-queue entries per warp (tiled kernel)
+#ifndef LBX_PIC_QCAPT
+#define LBX_PIC_QCAPT 64
+#endif
+constexpr int kQCapT = LBX_PIC_QCAPT;   // flush-queue entries per warp (tiled kernel)
 
 __device__ __forceinline__ int tile_key(int i, int j, int ntx) {
-  return ((((i >> 4) * ntx) + (j >> 4)) << kTileShift) | ((i & 15) << 4) | (j & 15);
+  return ((((i >> kTS) * ntx) + (j >> kTS)) << kTileShift) | ((i & (kT - 1)) << kTS) |
+         (j & (kT - 1));
 }
 
 // cell-relative slot -> node (i + dr, j + ds) of component comp (the
