@@ -181,3 +181,26 @@ def test_migration_aware_gate(L):
         L.lib.lbx_lb_destroy(h)
         res[ratio] = ad.value
     assert res[0.0] == 1 and res[1e9] == 0
+
+
+def test_integration_md_ctypes_binding():
+    """The raw ctypes binding INTEGRATION.md shows a reference maintainer
+    (no package import, plain CDLL + argtypes) gives the oracle's owners."""
+    import ctypes as C
+    from pathlib import Path
+
+    import numpy as np
+
+    from oracle import lbsim_oracle as O
+    so = Path(__file__).resolve().parent.parent / "paper_2104_11385_b200" / "libLBX.so"
+    lib = C.CDLL(str(so))
+    lib.lbx_knapsack.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_void_p]
+    lib.lbx_last_error.restype = C.c_char_p
+    rng = np.random.default_rng(7)
+    v = np.ascontiguousarray(rng.uniform(0, 100, 300))
+    owner = np.empty(v.size, dtype=np.int64)
+    assert lib.lbx_knapsack(v.ctypes.data, v.size, 8, 1.5, owner.ctypes.data) == 0
+    assert np.array_equal(owner, np.asarray(O.knapsack_assign(v, 8, 1.5)))
+    bad = np.ascontiguousarray(np.ones(10))
+    assert lib.lbx_knapsack(bad.ctypes.data, bad.size, 8, 0.5, owner.ctypes.data) != 0
+    assert b"cap" in lib.lbx_last_error()
