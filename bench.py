@@ -6,22 +6,32 @@ Workload (config C2, "2D laser-ion dense-slab target, GpuClock costs,
 dynamic LB every 10 steps"): the reference's default.yaml geometry -- 960x960
 cells, 32-cell boxes (900 boxes), dense blob (core 64, skirt 4, 55 ppc)
 sampled with the reference's own PCG64 stream -- from the kick step onward
-(radial kick, speed 0.035, drift 0.01), GpuClock costs, knapsack remap
-attempted every 10 steps with a 10% relative threshold.  To fill a B200 the
-801,499-particle set is tiled R times (default R=128 -> 102.6 M particles,
-3.3 GB of particle state): every replica evolves identically, so per-box
-counts are exactly R x the reference's (checked by tests/test_gpu_bench_parity).
+(radial kick, speed 0.035, drift 0.01), 8 virtual ranks (N > 1: one rank per
+GPU), initial slab mapping, knapsack remap attempted every 10 steps with a
+10 % relative threshold.  To fill a B200 the 801,499-particle set is tiled R
+times (default R=128 -> 102.6 M particles, 3.3 GB of particle state): every
+replica evolves identically, so per-box counts are exactly R x the
+reference's (tests/test_gpu_bench_parity).
 
-One step = the fused sm_100a kernel (push + absorb + stable compaction +
-per-box counts + heuristic cost + GpuClock tally) + the step record written
-to mapped host memory + the native host loop (cost vector, efficiency,
-knapsack attempt every 10 steps).  Inputs (3.3 GB) are larger than L2
-(126 MB), so no flush is needed between steps.
+Both arms print the SAME `config` dict (bench_config):
+* B200 arm: the fused sm_100a kernel (push + absorb + stable compaction +
+  per-box counts + heuristic cost + GpuClock clock64 tally) + the step record
+  written to mapped host memory + the native host loop (cost vector,
+  efficiency over the 8 ranks, knapsack attempt every 10 steps).  Inputs
+  (3.3 GB) are larger than L2 (126 MB), so no flush is needed between steps.
+* `e2e`: the same steps through the reference-facing plugin (C-ABI
+  lbx_advance_bin_host with pinned HOST buffers: H2D of every particle, D2H
+  of the survivors + counts every step) driving the package's public
+  balancer API (true_work -> measured_cost -> efficiency -> knapsack every
+  10), i.e. the reference's run loop with its kernels swapped.
+* --impl reference: the reference's own compiled Cython kernels
+  (oracle/_ref) + the oracle port of its numpy cost / balancer code, with
+  GpuClock costs modelled the way the reference models them (measured_cost,
+  cost.py:98-113) -- the package is NOT imported on this arm; one process per
+  host core, each on a bounded sample of the workload; rank 0 only.
 
---impl reference: the reference's own CPU implementation (its compiled
-Cython kernels from oracle/_ref, with the oracle port of its numpy cost and
-balancer code) on the same workload, one process per host core, each on a
-bounded sample; rank 0 only.
+--gpus N without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (NCCL INIT logging on).
 """
 
 from __future__ import annotations
@@ -54,7 +64,9 @@ def parse():
     ap.add_argument("--impl", default="lbx", choices=["lbx", "reference"])
     ap.add_argument("--replicas", type=int, default=128)
     ap.add_argument("--cost", default="gpuclock")
-    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--ranks", type=int, default=8,
+                    help="virtual ranks of the distribution mapping at N=1 (N>1: one per GPU)")
+    ap.add_argument("--e2e-steps", type=int, default=None, help="default: --steps")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -64,18 +76,66 @@ def parse():
 
 
 # ---------------------------------------------------------------------------
-# workload
+# workload (shared by both arms; nothing here imports the package)
 # ---------------------------------------------------------------------------
 
-def c2_spec(n_ranks: int, steps: int, cost: str):
-    from dataclasses import replace
+BASE_PARTICLES = 801_499   # the C2 set (default.yaml blob), tests/golden
 
-    from paper_2104_11385_b200.scenarios import apply_overrides, load_spec
 
-    spec = apply_overrides(load_spec("default"), cost=cost, ranks=n_ranks, steps=steps)
-    sc = spec.scenario
-    # bench starts at the kick (step 150 of the preset): kick applies at step 0
-    return spec, replace(sc, kick=replace(sc.kick, step=0))
+def c2_doc(provider: str, ranks: int, steps: int, initial_mapping: str = "slab") -> dict:
+    """default.yaml (reference pkg/src/lbsim/scenarios/default.yaml) with the
+    kick moved to step 0 (the bench starts at the kick), `ranks` virtual ranks
+    and the cost provider of the arm."""
+    return dict(scenario_id="c2-bench", domain=dict(extent=[960, 960], box_size=32),
+                ranks=int(ranks),
+                blob=dict(center=[480.0, 480.0], core_radius=64.0, edge_scale=4.0,
+                          particles_per_cell=55.0),
+                kick=dict(step=0, speed=0.035, drift=0.01), steps=int(steps),
+                compute_fraction=0.5, work_weights=[0.75, 0.25],
+                initial_mapping=initial_mapping, seed=7,
+                balance=dict(strategy="knapsack", interval=10, threshold=0.10,
+                             threshold_mode="relative", cap_factor=1.5),
+                provider=dict(kind=provider, weights="default", noise=0.05,
+                              instrumented_overhead=2.0))
+
+
+def dist_mode(args, world: int) -> bool:
+    return world > 1 or args.force_dist
+
+
+def bench_ranks(args, world: int) -> int:
+    return world if dist_mode(args, world) else args.ranks
+
+
+def bench_initial_mapping(args, world: int) -> str:
+    # N > 1: the ranks are real GPUs; a knapsack start keeps the first steps
+    # from piling the blob onto two GPUs (both arms use the same rule)
+    return "knapsack" if dist_mode(args, world) else "slab"
+
+
+def bench_config(args, world: int) -> dict:
+    """The `config` dict printed by BOTH arms (same workload, same mapping)."""
+    R = args.replicas
+    return {"workload": (f"C2: default.yaml geometry (960x960 cells, 32-cell boxes, 900 boxes, "
+                         f"blob core 64 / skirt 4 / 55 ppc, seed 7) from the kick, particle "
+                         f"set x{R} replicas = {BASE_PARTICLES * R} particles per GPU"),
+            "ranks": bench_ranks(args, world),
+            "cost": ("GpuClock: clock64 tally fused in the B200 push kernel; the CPU "
+                     "reference arm uses the reference's model of it (measured_cost, "
+                     "cost.py:98-113, noise 0.05)"),
+            "lb": (f"knapsack (cap 1.5) every 10 steps, 10% relative threshold, initial "
+                   f"{bench_initial_mapping(args, world)} mapping"),
+            "steps": args.steps, "warmup": args.warmup,
+            "l2": "inputs larger than L2 (3.3 GB particle state per GPU vs 126 MB L2)"}
+
+
+def c2_spec(args, world: int, steps: int):
+    """Package RunSpec + ScenarioConfig of the B200 arm."""
+    from paper_2104_11385_b200.scenarios import spec_from_dict
+
+    spec = spec_from_dict(c2_doc(args.cost, bench_ranks(args, world), steps,
+                                 bench_initial_mapping(args, world)))
+    return spec, spec.scenario
 
 
 def base_particles(spec):
@@ -83,6 +143,17 @@ def base_particles(spec):
 
     pos = sample_blob(spec.scenario)
     return pos, kick_velocities(pos, spec.scenario)
+
+
+def oracle_particles(cfg):
+    """The same C2 set from the oracle (reference arm: no package import)."""
+    from oracle import lbsim_oracle as O
+
+    pos, _ = O.init_scenario(cfg["extent"], cfg["box_size"], cfg["center"],
+                             cfg["core_radius"], cfg["edge_scale"], cfg["ppc"], cfg["seed"])
+    vel = O.kick_velocities(pos, cfg["center"], cfg["kick_speed"], cfg["kick_drift"],
+                            cfg["seed"])
+    return pos, vel
 
 
 def peaks():
@@ -170,48 +241,56 @@ def _ref_kernels():
     return O, "port"
 
 
-def _cpu_worker(args):
-    """One single-threaded reference loop over `reps` replicas of the base
-    set (its share of the benchmark workload), whole steps until `seconds`
-    elapse.  Returns (pushes, secs, steps)."""
-    seconds, cost_kind, reps = args
+def _cpu_worker(a):
+    """One single-threaded reference loop over `reps` replicas of the base set
+    (its sample of the benchmark workload), whole steps until `seconds`
+    elapse.  The workload is R identical replicas, so the full workload's
+    per-box counts are exactly (R / reps) x the sample's: the cost, efficiency
+    and knapsack steps run on that full vector, i.e. the same LB decisions as
+    the B200 arm's.  Returns (pushes, secs, steps, lb dict)."""
+    seconds, reps, R, ranks, init_map = a
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     from oracle import lbsim_oracle as O
     K, _ = _ref_kernels()
-    spec, sc = c2_spec(1, 10 ** 6, "measured")
-    pos, vel = base_particles(spec)
+    cfg = O.config_from_doc(c2_doc("measured", ranks, 10 ** 6, init_map))
+    pos, vel = oracle_particles(cfg)
     if reps > 1:
         pos = np.ascontiguousarray(np.tile(pos, (reps, 1)))
         vel = np.ascontiguousarray(np.tile(vel, (reps, 1)))
-    m = float(sc.box_size)
-    nbz = nbx = sc.domain_extent[0] // sc.box_size
-    cells = np.full(nbz * nbx, sc.box_size ** 2, dtype=np.int64)
-    owner = O.slab_mapping(nbz * nbx, 8)
-    pushes, step = 0, 0
+    scale = max(1, R // reps)
+    m, wts = cfg["box_size"], cfg["work_weights"]
+    ez, ex = (float(v) for v in cfg["extent"])
+    nbz, nbx = cfg["extent"][0] // m, cfg["extent"][1] // m
+    counts0 = K.bin_particles(pos, float(m), nbz, nbx) * scale
+    if init_map == "slab":
+        owner = O.slab_mapping(nbz * nbx, ranks)
+    else:
+        owner = O.knapsack_assign(O.true_work(counts0, m, wts), ranks)
+    pushes, step, effs, adoptions = 0, 0, [], 0
     t0 = time.perf_counter()
     while True:
         n = pos.shape[0]
-        pos, vel = K.advance_particles(pos, vel, float(sc.domain_extent[0]),
-                                       float(sc.domain_extent[1]))
-        counts = K.bin_particles(pos, m, nbz, nbx)
-        work = O.true_work(counts, sc.box_size, sc.work_weights)
-        if cost_kind == "heuristic":
-            cost = O.heuristic_cost(counts, cells, 0.75, 0.25)
-        else:
-            cost = O.measured_cost(work, 0.05, sc.seed, step)
-        e, _ = O.efficiency_flagged(cost, owner, 8)
-        if step % 10 == 0:
-            prop = O.knapsack_assign(cost, 8)
-            if O.gate(e, O.efficiency_flagged(cost, prop, 8)[0], 0.10, "relative"):
-                owner = prop
+        pos, vel = K.advance_particles(pos, vel, ez, ex)
+        counts = K.bin_particles(pos, float(m), nbz, nbx) * scale
+        work = O.true_work(counts, m, wts)
+        cost = O.measured_cost(work, cfg["noise"], cfg["seed"], step)
+        e, _ = O.efficiency_flagged(cost, owner, ranks)
+        if step % cfg["interval"] == 0:
+            prop = O.knapsack_assign(cost, ranks, cfg["cap_factor"])
+            ep = O.efficiency_flagged(cost, prop, ranks)[0]
+            if O.gate(e, ep, cfg["threshold"], cfg["threshold_mode"]):
+                owner, e = prop, ep
+                adoptions += 1
+        effs.append(e)
         pushes += n
         step += 1
         el = time.perf_counter() - t0
         if el >= seconds:
-            return pushes, el, step
+            return pushes, el, step, {"e_first": effs[0], "e_mean": float(np.mean(effs)),
+                                      "adoptions": adoptions, "steps": step}
 
 
-def cpu_baseline(seconds: float, processes: int, replicas: int):
+def cpu_baseline(seconds: float, processes: int, args, world: int):
     """The reference's CPU path on the benchmark workload: the R replicas of
     the C2 set are split over `processes` single-threaded processes (the
     reference itself is single-threaded), each running whole steps of its
@@ -219,40 +298,44 @@ def cpu_baseline(seconds: float, processes: int, replicas: int):
     import multiprocessing as mp
 
     _, kind = _ref_kernels()
-    processes = max(1, min(processes, replicas))
-    reps = max(1, replicas // processes)
+    R = args.replicas * (world if dist_mode(args, world) else 1)   # whole job
+    processes = max(1, min(processes, R))
+    reps = max(1, R // processes)
+    job = (seconds, reps, R, bench_ranks(args, world), bench_initial_mapping(args, world))
     if processes <= 1:
-        res = [_cpu_worker((seconds, "measured", reps))]
+        res = [_cpu_worker(job)]
     else:
         with mp.get_context("spawn").Pool(processes) as pool:
-            res = pool.map(_cpu_worker, [(seconds, "measured", reps)] * processes)
-    value = sum(p / s for p, s, _ in res)
-    steps = sum(k for _, _, k in res)
+            res = pool.map(_cpu_worker, [job] * processes)
+    value = sum(r[0] / r[1] for r in res)
+    steps = sum(r[2] for r in res)
     return {"value": value, "unit": UNIT, "cores": processes, "kind": kind,
-            "sample": (f"C2 set (801,499 particles, from the kick) x {reps} replicas per "
-                       f"process x {processes} single-threaded processes = "
-                       f"{801499 * reps * processes} particles; {steps} whole steps in "
+            "sample": (f"C2 set ({BASE_PARTICLES:,} particles, from the kick) x {reps} "
+                       f"replicas per process x {processes} single-threaded processes = "
+                       f"{BASE_PARTICLES * reps * processes} particles; {steps} whole steps in "
                        f"~{seconds:.0f} s: reference Cython advance_particles + "
-                       "bin_particles (oracle/_ref) + measured_cost / efficiency / "
-                       "knapsack every 10 (oracle numpy port)")}
+                       "bin_particles (oracle/_ref) + true_work / measured_cost / "
+                       "efficiency / knapsack every 10 on the full workload's per-box "
+                       "counts (oracle numpy port)"),
+            "lb": res[0][3]}
 
 
 # ---------------------------------------------------------------------------
 # arms
 # ---------------------------------------------------------------------------
 
-def run_reference(args, rank):
+def run_reference(args, rank, world):
+    """The reference arm: never imports paper_2104_11385_b200 (no libLBX)."""
     if rank != 0:
         return
     procs = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    cb = cpu_baseline(args.cpu_seconds, procs or 1, args.replicas)
+    cb = cpu_baseline(args.cpu_seconds, procs or 1, args, world)
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "impl": "reference",
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C2 default.yaml geometry from the kick, x"
-                                   f"{args.replicas} replicas (sampled: see cpu_baseline)",
-                       "cost": "measured (reference timer model)", "parallelism": "cpu"},
+            "config": bench_config(args, world),
+            "lb": cb.pop("lb"),
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -276,7 +359,7 @@ def run_lbx(args, rank, world, local_rank):
             dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
         return run_lbx_dist(args, rank, world, dev)
     total = args.warmup + args.steps
-    spec, sc = c2_spec(world, total, args.cost)
+    spec, sc = c2_spec(args, world, total)
     pos0, kick0 = base_particles(spec)
     R = args.replicas
     pos = torch.from_numpy(pos0).to(dev).repeat(R, 1)
@@ -287,13 +370,6 @@ def run_lbx(args, rank, world, local_rank):
     n0 = sim.n_init
     sim.run(0, args.warmup)
     torch.cuda.synchronize(dev)
-
-    def barrier():
-        if world > 1:
-            torch.distributed.barrier()
-
-    barrier()
-    torch.cuda.synchronize(dev)
     stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clocks:
@@ -301,19 +377,12 @@ def run_lbx(args, rank, world, local_rank):
         sim.run(args.warmup, total)
         e1.record(stream)
         torch.cuda.synchronize(dev)
-    barrier()
     ms = e0.elapsed_time(e1)
     n_alive = sim.out["n_alive"]
     n_before = np.concatenate(([n0], n_alive[:-1]))
     pushed = float(n_before[args.warmup:total].sum())
     kms = sim.out["kernel_ms"][args.warmup:total]
     res = sim.result()
-    if world > 1:
-        t = torch.tensor([ms, pushed], dtype=torch.float64, device=dev)
-        allt = [torch.zeros_like(t) for _ in range(world)]
-        torch.distributed.all_gather(allt, t)
-        ms = max(float(x[0]) for x in allt)
-        pushed = sum(float(x[1]) for x in allt)
     value = pushed / (ms / 1e3)
     kernel_s = float(np.mean(kms)) / 1e3
     per_launch = float(np.mean(n_before[args.warmup:total]))
@@ -321,6 +390,10 @@ def run_lbx(args, rank, world, local_rank):
     peak, peak_src = peaks()
     tpp = traffic_per_push()
     effs = [m.efficiency_after for m in res.metrics]
+    adopt_timed = int(sum(m.adopted for m in res.metrics[args.warmup:total]))
+    sim.close()
+    del sim
+    torch.cuda.empty_cache()
 
     # ---- the reference's own C2 size (801,499 particles, 1 replica) ----
     c2n = c2_native(args, dev, spec, sc, pos0, kick0)
@@ -329,27 +402,21 @@ def run_lbx(args, rank, world, local_rank):
     # ---- e2e through the reference-facing C-ABI with host buffers ----
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_plugin(args, dev, pos0, kick0, R, sc)
+        e2e = e2e_plugin(args, dev, pos0, kick0, R, spec)
 
-    if rank != 0:
-        return
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": (f"C2: default.yaml geometry (960x960 cells, 32-cell boxes, "
-                                f"900 boxes, blob core 64 / skirt 4 / 55 ppc, seed 7) from "
-                                f"the kick, particle set x{R} replicas = {n0} particles per "
-                                "GPU"),
-                   "cost": spec.build_provider().kind, "lb": "knapsack every 10, 10% rel",
-                   "ranks": world, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-                   "l2": "inputs larger than L2 (3.3 GB particle state vs 126 MB L2)"},
+        "config": bench_config(args, world),
+        "parallelism": "1 GPU, 8 virtual ranks (distribution mapping only)",
         "gpu_launches": 2 * int(args.steps),   # stream_kernel + compaction (exits at once
                                                  # when nothing was absorbed) per step
-        "lb": {"ranks": world, "e_first": effs[0] if effs else None,
+        "lb": {"ranks": sc.n_ranks, "e_first": effs[0] if effs else None,
                "e_mean": float(np.mean(effs)) if effs else None,
-               "adoptions": res.summary["adoption_count"]},
+               "e_mean_timed": float(np.mean(effs[args.warmup:total])) if effs else None,
+               "adoptions": res.summary["adoption_count"], "adoptions_timed": adopt_timed},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_src,
                      "kernel": "lbx stream_kernel<clock,pow2,exch=0,push=1>",
@@ -363,11 +430,10 @@ def run_lbx(args, rank, world, local_rank):
     if e2e is not None:
         line["e2e"] = e2e
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.cpu_seconds, 1, args.replicas)
+        line["cpu_baseline"] = cpu_baseline(args.cpu_seconds, 1, args, world)
+        line["cpu_baseline"].pop("lb", None)
     print(json.dumps(line), flush=True)
-    _lib.lib.lbx_sim_destroy(sim.handle)
-    sim.handle = None
-    del D
+    del D, _lib
 
 
 def c2_native(args, dev, spec, sc, pos0, kick0, steps=400):
@@ -464,16 +530,13 @@ def run_lbx_dist(args, rank, world, dev):
     initial knapsack mapping, GpuClock costs all-reduced every step, knapsack
     remap every 10 steps with real particle migration on adoption, per-step
     box-crossing exchange."""
-    from dataclasses import replace
-
     import torch
     import torch.distributed as dist
 
     from paper_2104_11385_b200.parallel import DistributedSimulation, TorchComm
 
     total = args.warmup + args.steps
-    spec, sc = c2_spec(world, total, args.cost)
-    sc = replace(sc, initial_mapping="knapsack")
+    spec, sc = c2_spec(args, world, total)
     pos0, kick0 = base_particles(spec)
     R = args.replicas * world
     n_total = pos0.shape[0] * R
@@ -512,14 +575,11 @@ def run_lbx_dist(args, rank, world, dev):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": (f"C2: default.yaml geometry from the kick, particle set x"
-                                    f"{R} replicas = {n_total} particles, boxes owned by GPUs"),
-                       "cost": spec.build_provider().kind,
-                       "lb": "knapsack every 10, 10% rel, initial knapsack",
-                       "ranks": world, "parallelism": f"box ownership over {world} GPUs "
-                       f"(exchange: {sim.exchange}; p2p = emigrants written into the owner's "
-                       f"buffer by the push kernel over NVLink peer memory, NCCL all-reduce)",
-                       "l2": "inputs larger than L2"},
+            "config": bench_config(args, world),
+            "parallelism": (f"box ownership over {world} GPUs, {n_total} particles in total "
+                            f"(exchange: {sim.exchange}; p2p = emigrants written into the "
+                            f"owner's buffer by the push kernel over NVLink peer memory, NCCL "
+                            f"all-reduce)"),
             "gpu_launches": int(launches),
             "lb": {"ranks": world, "e_first": effs[0] if effs else None,
                    "e_mean_timed": float(np.mean(effs[args.warmup:])) if effs else None,
@@ -540,7 +600,7 @@ def run_lbx_dist(args, rank, world, dev):
         # own C2 x R set (weak scaling, its own PCIe link), started together;
         # value = all ranks' pushes / the slowest rank's wall time
         dist.barrier()
-        e = e2e_plugin(args, dev, pos0, kick0, args.replicas, sc)
+        e = e2e_plugin(args, dev, pos0, kick0, args.replicas, spec)
         agg = torch.tensor([e["pushed"], e["seconds"], e["h2d_bytes_per_step"],
                             e["d2h_bytes_per_step"]], dtype=torch.float64, device=dev)
         mx = agg.clone()
@@ -592,24 +652,36 @@ def pcie_ceiling(dev, nbytes=1 << 30, reps=3):
             "bidir_h2d_gbs": nbytes / t_b / 1e9, "bidir_d2h_gbs": nbytes / t_b / 1e9}
 
 
-def e2e_plugin(args, dev, pos0, kick0, R, sc):
+def e2e_plugin(args, dev, pos0, kick0, R, spec):
     """Same workload through the reference-facing plugin boundary with HOST
-    buffers: every step calls lbx_advance_bin_host (the C-ABI behind
+    buffers -- the reference's run loop (workload.py:411-439) with its kernel
+    backend swapped: every step calls lbx_advance_bin_host (the C-ABI behind
     kernels.advance_particles / bin_particles for host arrays) on the
     particles in pinned host memory -- host->device copy of all particles,
-    push + absorb + compaction + per-box counts + heuristic cost, and the
-    survivors, counts and costs copied back -- chunked over three streams so
-    both PCIe directions overlap the kernels."""
+    push + absorb + compaction + per-box counts, survivors and counts copied
+    back, chunked over three streams so both PCIe directions overlap the
+    kernels -- then the package's public API on the host: true_work ->
+    measured_cost (the GpuClock model; no clock on host buffers) ->
+    efficiency -> knapsack attempt every 10 steps with the gate."""
     import torch
 
-    from paper_2104_11385_b200.kernels import advance_bin_host
+    from paper_2104_11385_b200.balancer import attempt_rebalance, efficiency
+    from paper_2104_11385_b200.cost import MeasurementConfig, measured_cost
+    from paper_2104_11385_b200.workload import box_array_for, initial_mapping, true_work
 
+    sc, policy = spec.scenario, spec.policy
+    steps = args.e2e_steps or args.steps
     n = pos0.shape[0] * R
     nbz = nbx = sc.domain_extent[0] // sc.box_size
     bufs = [torch.empty((n, 2), dtype=torch.float64, pin_memory=True).numpy() for _ in range(4)]
     bufs[0][:] = np.tile(pos0, (R, 1))
     bufs[1][:] = np.tile(kick0, (R, 1))
-    state = {"n": n, "inp": (bufs[0], bufs[1]), "out": (bufs[2], bufs[3])}
+    ba = box_array_for(sc)
+    from paper_2104_11385_b200.kernels import advance_bin_host, bin_particles
+    counts0 = bin_particles(bufs[0], float(sc.box_size), nbz, nbx)
+    state = {"n": n, "inp": (bufs[0], bufs[1]), "out": (bufs[2], bufs[3]),
+             "dm": initial_mapping(sc, ba, counts0), "step": 0, "adopt": 0, "eff": []}
+    mcfg = MeasurementConfig(noise_amplitude=0.05, seed=sc.seed)
     ez, ex = float(sc.domain_extent[0]), float(sc.domain_extent[1])
     io = {"h2d": 0, "d2h": 0}
 
@@ -617,13 +689,22 @@ def e2e_plugin(args, dev, pos0, kick0, R, sc):
         k = state["n"]
         ip, iv = state["inp"]
         op, ov = state["out"]
-        p, v, counts, cost = advance_bin_host(ip[:k], iv[:k], ez, ex, float(sc.box_size),
-                                              nbz, nbx, out=(op, ov), dev=dev)
+        p, v, counts, _ = advance_bin_host(ip[:k], iv[:k], ez, ex, float(sc.box_size),
+                                           nbz, nbx, out=(op, ov), dev=dev)
         m = p.shape[0]
         io["h2d"] += 32 * k
         io["d2h"] += 32 * m + 16 * nbz * nbx
         state["n"] = m
         state["inp"], state["out"] = state["out"], state["inp"]
+        s = state["step"]
+        cv = measured_cost(true_work(counts, sc), mcfg, s)
+        out = attempt_rebalance(cv, state["dm"], policy, s)
+        if out.adopted:
+            state["dm"] = out.proposed
+            state["adopt"] += 1
+        state["eff"].append(out.efficiency_proposed if out.adopted
+                            else out.efficiency_current)
+        state["step"] = s + 1
         return k
 
     for _ in range(2):
@@ -631,33 +712,68 @@ def e2e_plugin(args, dev, pos0, kick0, R, sc):
     io["h2d"] = io["d2h"] = 0
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
-    pushed = sum(step() for _ in range(args.e2e_steps))
+    pushed = sum(step() for _ in range(steps))
     el = time.perf_counter() - t0
     ceil = pcie_ceiling(dev)
-    h2d, d2h = io["h2d"] / args.e2e_steps, io["d2h"] / args.e2e_steps
+    h2d, d2h = io["h2d"] / steps, io["d2h"] / steps
     # the e2e roofline: both directions at the measured concurrent copy rates
     t_min = max(h2d / (ceil["bidir_h2d_gbs"] * 1e9), d2h / (ceil["bidir_d2h_gbs"] * 1e9))
-    bound = (pushed / args.e2e_steps) / t_min
+    bound = (pushed / steps) / t_min
     return {"value": pushed / el, "unit": UNIT,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "steps": args.e2e_steps, "seconds": el, "pushed": pushed,
+            "steps": steps, "seconds": el, "pushed": pushed,
+            "lb": {"e_first": state["eff"][0], "adoptions": state["adopt"]},
             "pcie": dict(ceil, bound_pushes_per_s=bound, frac_of_bound=(pushed / el) / bound),
-            "path": "lbx_advance_bin_host (reference AoS layout, pinned host buffers, "
-                    "4 Mi-particle chunks over 3 streams, no host round trip per chunk), copies in the timed region"}
+            "path": ("lbx_advance_bin_host (reference AoS layout, pinned host buffers, "
+                     "4 Mi-particle chunks over 3 streams) + the package's balancer API "
+                     "(true_work, measured_cost, efficiency, knapsack every 10) on the "
+                     "host; copies in the timed region")}
+
+
+def self_launch(args) -> int:
+    """`bench.py --gpus N` outside torchrun: re-exec under
+    torch.distributed.run with N ranks on this node (127.0.0.1)."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible",
+              file=sys.stderr, flush=True)
+        return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
-    # one JSON line on stdout: keep NCCL's version banner off it unless the
-    # user asked for NCCL debugging
+    # NCCL INIT logging on (communicator lines with nranks); the JSON line is
+    # printed last, after every NCCL init message
     if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
-        os.environ["NCCL_DEBUG"] = "WARN"
+        os.environ["NCCL_DEBUG"] = "INFO"
+    sub = os.environ.get("NCCL_DEBUG_SUBSYS", "")
+    if sub and "INIT" not in sub.upper() and sub.upper() != "ALL":
+        os.environ["NCCL_DEBUG_SUBSYS"] = sub + ",INIT"
+    elif not sub:
+        os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
     args = parse()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
-        run_reference(args, rank)
+        run_reference(args, rank, max(world, args.gpus))
         return
+    if "WORLD_SIZE" not in os.environ and (args.gpus > 1 or args.force_dist):
+        sys.exit(self_launch(args))
+    if world != args.gpus:
+        print(f"bench.py: launched with WORLD_SIZE={world} but --gpus {args.gpus}",
+              file=sys.stderr, flush=True)
+        sys.exit(2)
     run_lbx(args, rank, world, local_rank)
 
 

@@ -271,7 +271,21 @@ typedef struct lbx_sim_config {
    * migration_ratio particle-pushes each (cost per push = total cost /
    * total particles of the step). */
   double migration_ratio;
+  /* GpuClock cost form (cost_kind == LBX_COST_GPUCLOCK):
+   *   LBX_CLOCK_RAW        cost_b = clock tally_b (the paper's thread-summed
+   *                        cycles of the particle kernel);
+   *   LBX_CLOCK_CALIBRATED cost_b = clk_b * (w_particle * N / sum clk)
+   *                        + w_cell * cells_b: the measured tally carries
+   *                        the particle work's distribution over boxes,
+   *                        scaled to the heuristic's particle units (N =
+   *                        particles alive), plus the per-box field work,
+   *                        which no particle kernel measures and which is
+   *                        identical for equal-size boxes. */
+  int32_t clock_mode;
 } lbx_sim_config;
+
+#define LBX_CLOCK_RAW 0
+#define LBX_CLOCK_CALIBRATED 1
 
 #define LBX_PHYSICS_SURROGATE 0
 #define LBX_PHYSICS_PIC 1

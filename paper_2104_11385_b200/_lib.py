@@ -49,7 +49,7 @@ class SimConfig(C.Structure):
                 ("redistribute_per_particle", f64), ("redistribute_latency", f64),
                 ("capacity_particles", i64), ("physics", i32), ("pic_dt", f64),
                 ("pic_q_over_m", f64), ("pic_q_times_w", f64), ("extent_y", i32),
-                ("migration_ratio", f64)]
+                ("migration_ratio", f64), ("clock_mode", i32)]
 
 
 class SimOutputs(C.Structure):

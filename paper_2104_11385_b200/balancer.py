@@ -157,12 +157,42 @@ def gate(e_cur: float, e_prop: float, policy: BalancePolicy) -> bool:
     return bool(e_prop >= need and e_prop >= e_cur)
 
 
+def migration_worthwhile(costs: CostVector, current: DistributionMapping,
+                         proposed: DistributionMapping, counts, policy: BalancePolicy) -> bool:
+    """The migration-aware part of the gate (B200 extension, SURVEY 8f rank
+    3), the same arithmetic as lbx_runtime.cpp's lb_step: the max-rank load
+    saved over one interval must exceed migration_ratio x (cost per particle)
+    x (particles in boxes that change owner)."""
+    c = np.asarray(costs.values, dtype=np.float64)
+    n = np.asarray(counts, dtype=np.int64)
+    if n.shape != c.shape:
+        raise ValueError(f"counts length {n.size} != costs length {c.size}")
+    R = current.n_ranks
+    lc, lp = [0.0] * R, [0.0] * R
+    total_cost, total_n, moved = 0.0, 0, 0
+    for b in range(c.size):            # box order, as the C++ loop
+        lc[int(current.owner[b])] += float(c[b])
+        lp[int(proposed.owner[b])] += float(c[b])
+        total_cost += float(c[b])
+        total_n += int(n[b])
+        if proposed.owner[b] != current.owner[b]:
+            moved += int(n[b])
+    per_push = total_cost / float(total_n) if total_n > 0 else 0.0
+    saved = float(policy.interval) * (max(lc) - max(lp))
+    return saved > policy.migration_ratio * per_push * float(moved)
+
+
 def attempt_rebalance(costs: CostVector, current: DistributionMapping,
                       policy: BalancePolicy, step: int, *, curve=None,
-                      force: bool = False) -> BalanceOutcome:
-    """One pass of the balancing routine (balancer.py:258-292)."""
+                      force: bool = False, counts=None) -> BalanceOutcome:
+    """One pass of the balancing routine (balancer.py:258-292).  With
+    policy.migration_ratio > 0 the per-box particle `counts` are required
+    and the migration-aware check (migration_worthwhile) joins the gate,
+    exactly as in the native loop."""
     if step < 0:
         raise ValueError(f"step must be >= 0, got {step}")
+    if policy.migration_ratio > 0 and counts is None:
+        raise ValueError("migration_ratio > 0 needs the per-box particle counts")
     e_cur = efficiency(costs, current)
     if not force and step % policy.interval:
         return BalanceOutcome(current, e_cur, e_cur, adopted=False, attempted=False)
@@ -173,7 +203,10 @@ def attempt_rebalance(costs: CostVector, current: DistributionMapping,
             raise ValueError("sfc strategy requires the morton curve")
         prop = sfc_assign(costs, curve, current.n_ranks)
     e_prop = efficiency(costs, prop)
-    return BalanceOutcome(prop, e_cur, e_prop, adopted=gate(e_cur, e_prop, policy))
+    adopted = gate(e_cur, e_prop, policy)
+    if adopted and policy.migration_ratio > 0:
+        adopted = migration_worthwhile(costs, current, prop, counts, policy)
+    return BalanceOutcome(prop, e_cur, e_prop, adopted=adopted)
 
 
 def periodic_enabled(policy: BalancePolicy, total_steps: int) -> bool:

@@ -1272,12 +1272,12 @@ template <bool kClock, bool kPow2, bool kExch, bool kPush>
 int launch_stream(lbx_ctx* ctx, const StepParams& p, cudaStream_t s) {
   auto kern = stream_kernel<kClock, kPow2, kExch, kPush>;
   const size_t smem = p.smem_hist ? (size_t)p.nb * 4 * (1 + (kClock ? 1 : 0) + (kExch ? 1 : 0)) : 0;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  // per launch (a cheap host call): the attribute is per device context, and
+  // thread-ranks / several devices share this function
+  if (smem > 48 * 1024) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    configured = smem;
   }
   int grid = 0;
   const long long work = (ctx->n_upper + 2ll * kBlock * kPairs - 1) / (2ll * kBlock * kPairs);

@@ -122,6 +122,8 @@ int validate(const lbx_sim_config& c) {
     return set_error(LBX_EINVAL, "unknown cost kind %d", c.cost_kind);
   if (c.physics != LBX_PHYSICS_SURROGATE && c.physics != LBX_PHYSICS_PIC)
     return set_error(LBX_EINVAL, "unknown physics %d", c.physics);
+  if (c.clock_mode != LBX_CLOCK_RAW && c.clock_mode != LBX_CLOCK_CALIBRATED)
+    return set_error(LBX_EINVAL, "unknown clock mode %d", c.clock_mode);
   if (c.physics == LBX_PHYSICS_PIC &&
       (c.cost_kind == LBX_COST_TIMERS || c.cost_kind == LBX_COST_CUPTI))
     return set_error(LBX_EINVAL, "Timers strategies are implemented for the surrogate push only");
@@ -159,7 +161,21 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
       break;
     case LBX_COST_GPUCLOCK:
       if (!clk) return set_error(LBX_EINVAL, "GpuClock costs need the clock tally");
-      for (int b = 0; b < nb; ++b) cost[b] = (double)clk[b];
+      if (c.clock_mode == LBX_CLOCK_CALIBRATED) {
+        // cost.py GpuClockProvider.calibrated: the same operations in the
+        // same order (integer sums, one scale, mul then add)
+        uint64_t tot = 0;
+        int64_t np_ = 0;
+        for (int b = 0; b < nb; ++b) {
+          tot += clk[b];
+          np_ += counts[b];
+        }
+        const double scale = tot ? c.w_particle * (double)np_ / (double)tot : 0.0;
+        const double cell = c.w_cell * cells;
+        for (int b = 0; b < nb; ++b) cost[b] = (double)clk[b] * scale + cell;
+      } else {
+        for (int b = 0; b < nb; ++b) cost[b] = (double)clk[b];
+      }
       break;
     case LBX_COST_TIMERS:
     case LBX_COST_CUPTI:

@@ -143,6 +143,11 @@ class ThreadComm:
         return out.reshape(-1, REC).to(send.device)
 
     def barrier(self):
+        # A device barrier, as NCCL's is: this rank's queued work (e.g. the
+        # unpack of its receive buffer and the cursor reset) completes before
+        # any peer passes, so a peer's next push cannot race it.
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            torch.cuda.current_stream().synchronize()
         self.s["bar"].wait()
 
     def device_ids(self, dev: int) -> list:
@@ -730,10 +735,13 @@ class DistributedSimulation:
 
     def _migrate_p2p(self, step):
         """Adoption-time migration over peer memory: the partition kernel
-        writes the lost boxes' particles into their new owners' buffers (the
-        parity the next step does not use yet); the all-reduce orders every
-        sender before the reads; a barrier keeps the buffer quiet until all
-        ranks drained it."""
+        writes the lost boxes' particles into their new owners' buffers
+        (parity (step+1)&1 -- the buffer the NEXT step's push writes its
+        emigrants into); the all-reduce orders every sender before the reads;
+        the barrier (a device barrier on every communicator: NCCL's, and
+        ThreadComm's syncs the rank's stream first) keeps the next step's
+        pushes out until every rank has drained that buffer and reset its
+        cursor."""
         par = (step + 1) & 1
         self.engine.parity = par
         send_counts, nout = self.engine.partition()

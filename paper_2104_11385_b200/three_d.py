@@ -160,7 +160,8 @@ class Simulation3D:
             work_wc=cfg.work_weights[1], comm_per_face=0.0, gather=0.0,
             redistribute_per_particle=0.0, redistribute_latency=0.0, capacity_particles=-1,
             physics=0, pic_dt=0.5, pic_q_over_m=-1.0, pic_q_times_w=-1e-4,
-            extent_y=cfg.domain_extent[1], migration_ratio=policy.migration_ratio)
+            extent_y=cfg.domain_extent[1], migration_ratio=policy.migration_ratio,
+            clock_mode=getattr(provider, "clock_mode", 0))
         self.conf = conf
         h = C.c_void_p()
         _lib.check(_lib.lib.lbx_lb_create(C.byref(h), C.byref(conf), _lib.ptr(self.initial_owner)))

@@ -355,7 +355,8 @@ def sim_config(cfg: ScenarioConfig, policy: BalancePolicy, provider: CostProvide
         physics=0 if physics == "surrogate" else 1,
         pic_dt=(pic or PIC_DEFAULTS)["dt"], pic_q_over_m=(pic or PIC_DEFAULTS)["q_over_m"],
         pic_q_times_w=(pic or PIC_DEFAULTS)["q_times_w"], extent_y=0,
-        migration_ratio=getattr(policy, "migration_ratio", 0.0))
+        migration_ratio=getattr(policy, "migration_ratio", 0.0),
+        clock_mode=getattr(provider, "clock_mode", 0))
 
 
 class Simulation:

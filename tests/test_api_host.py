@@ -93,6 +93,28 @@ def test_config_errors_name_the_field(P):
     assert s.policy.static_step == 0 and s.scenario.n_ranks == 4
 
 
+def test_gpuclock_provider_forms(P):
+    """GpuClock cost forms: raw = the tally; calibrated = tally scaled to the
+    heuristic's particle units + the per-box cell work (the same operations
+    as lbx_runtime.cpp's lb_step)."""
+    clk = np.array([0, 1000, 3000, 0, 6000], dtype=np.uint64)
+    counts = np.array([0, 10, 30, 0, 60], dtype=np.int64)
+    cells = np.full(5, 1024.0)
+    raw = P.make_provider("gpuclock-raw")
+    assert raw.kind == "gpuclock-raw" and raw.clock_mode == 0
+    assert raw.assess(counts, cells, None, 0, clock=clk).values.tolist() == clk.tolist()
+    cal = P.make_provider("gpuclock")
+    assert cal.clock_mode == 1
+    v = cal.assess(counts, cells, None, 0, clock=clk).values
+    scale = 0.75 * 100.0 / 10000.0
+    assert v.tolist() == [c * scale + 0.25 * 1024.0 for c in clk.astype(float)]
+    assert abs(v.sum() - (0.75 * counts.sum() + 0.25 * cells.sum())) < 1e-9
+    with pytest.raises(ValueError, match="clock"):
+        cal.assess(counts, cells, None, 0)
+    with pytest.raises(P.ConfigError):
+        P.GpuClockProvider("fast")
+
+
 def test_perfmodel(P):
     assert abs(P.max_speedup(1 / 6.2, 0.91) - 5.261) < 1e-3
     m = P.fit_scaling([(n, 3.0 * n ** -0.9) for n in (1, 2, 4, 8)])

@@ -107,22 +107,68 @@ def test_graph_replay_matches_per_step_launches(runs, name, monkeypatch):
 
 def test_gpuclock_run_rank_correlates_with_true_work(runs):
     """GpuClock costs (real clock64 tallies) vs the reference's timer model:
-    Spearman rank correlation with true work on every attempt step."""
+    Spearman rank correlation with true work on every attempt step; the
+    calibrated cost vector is exactly GpuClockProvider.assess of the tally."""
     from paper_2104_11385_b200 import scenarios as S
     from paper_2104_11385_b200.workload import run_simulation
     spec = S.apply_overrides(S.load_spec("mini"), cost="gpuclock", steps=60)
-    res = run_simulation(spec.scenario, spec.policy, spec.build_provider(),
-                         record_counts=True)
+    prov = spec.build_provider()
+    res = run_simulation(spec.scenario, spec.policy, prov, record_counts=True,
+                         record_clock=True)
     assert res.summary["provider"] == "gpuclock"
+    cells = np.full(res.count_trace.shape[1], float(spec.scenario.box_size ** 2))
     for s in range(0, 60, 10):
         counts = res.count_trace[s]
-        clk = res.cost_trace[s]
+        clk = res.clock_trace[s]
         occ = counts > 0
         assert ((clk > 0) == occ).all()
         rc = np.argsort(np.argsort(clk[occ]))
         rw = np.argsort(np.argsort(counts[occ]))
         rho = np.corrcoef(rc, rw)[0, 1]
         assert rho > 0.9, (s, rho)
+        want = prov.assess(counts, cells, None, s, clock=clk).values
+        assert np.array_equal(res.cost_trace[s], want)
+
+
+def _true_work_efficiency(res, cfg):
+    """Mean over steps of efficiency(true work of the step, mapping in force
+    after the step's LB decision): how well a strategy's mappings balance
+    the reference's ground-truth work (workload.py:303-311)."""
+    from oracle import lbsim_oracle as O
+    owner = res.initial_owner.copy()
+    snaps = dict((s, o) for s, o in res.adoption_snapshots)
+    effs = []
+    for s in range(res.count_trace.shape[0]):
+        if s in snaps:
+            owner = snaps[s]
+        work = O.true_work(res.count_trace[s], cfg.box_size, cfg.work_weights)
+        effs.append(O.efficiency_flagged(work, owner, cfg.n_ranks)[0])
+    return float(np.mean(effs))
+
+
+def test_gpuclock_native_size_mapping_quality():
+    """at the reference's own C2 size (default.yaml,
+    801,499 particles, 24 ranks, 2000 steps, L2-resident) the GpuClock
+    mappings, judged by TRUE work, are within 5 % of Heuristic's (whose cost
+    is the true work itself), and the clock tally rank-correlates with the
+    particle work (Spearman > 0.9) on every attempt step after the kick."""
+    from paper_2104_11385_b200 import scenarios as S
+    from paper_2104_11385_b200.workload import run_simulation
+    e = {}
+    for kind in ("heuristic", "gpuclock"):
+        spec = S.apply_overrides(S.load_spec("default"), cost=kind)
+        res = run_simulation(spec.scenario, spec.policy, spec.build_provider(),
+                             record_counts=True, record_clock=kind == "gpuclock")
+        e[kind] = _true_work_efficiency(res, spec.scenario)
+        if kind == "gpuclock":
+            rhos = []
+            for s in range(0, spec.scenario.total_steps, 10):
+                occ = res.count_trace[s] > 0
+                rc = np.argsort(np.argsort(res.clock_trace[s][occ]))
+                rw = np.argsort(np.argsort(res.count_trace[s][occ]))
+                rhos.append(np.corrcoef(rc, rw)[0, 1])
+            assert min(rhos) > 0.9, min(rhos)
+    assert e["gpuclock"] >= 0.95 * e["heuristic"], e
 
 
 @pytest.mark.parametrize("kind", ["timers", "cupti"])

@@ -183,6 +183,58 @@ def test_migration_aware_gate(L):
     assert res[0.0] == 1 and res[1e9] == 0
 
 
+def _native_adopt(L, sc, owner, counts, ratio):
+    import ctypes as C
+
+    from paper_2104_11385_b200.balancer import BalancePolicy
+    from paper_2104_11385_b200.cost import make_provider
+    from paper_2104_11385_b200.workload import sim_config
+    conf = sim_config(sc, BalancePolicy(migration_ratio=ratio), make_provider("heuristic"))
+    h = C.c_void_p()
+    L.check(L.lib.lbx_lb_create(C.byref(h), C.byref(conf), L.ptr(owner)))
+    T, nb = sc.total_steps, owner.size
+    arrs = [np.zeros(T) for _ in range(7)]
+    u8 = [np.zeros(T, dtype=np.uint8) for _ in range(3)]
+    i64 = [np.zeros(T, dtype=np.int64) for _ in range(3)]
+    trace = np.zeros((T, nb))
+    own_out = owner.copy()
+    so = L.SimOutputs(*(L.ptr(a) for a in arrs[:2]), L.ptr(u8[0]), L.ptr(u8[1]),
+                      *(L.ptr(a) for a in arrs[2:7]), L.ptr(i64[0]), L.ptr(u8[2]),
+                      L.ptr(i64[1]), L.ptr(trace), None, None, L.ptr(own_out), L.ptr(i64[2]),
+                      None, None, 0, 0, 0)
+    ad, halt = C.c_int32(), C.c_int32()
+    L.check(L.lib.lbx_lb_step(h, 0, L.ptr(counts), None, int(counts.sum()), C.byref(so),
+                              C.byref(ad), C.byref(halt)))
+    L.lib.lbx_lb_destroy(h)
+    return bool(ad.value)
+
+
+def test_python_gate_applies_migration_ratio_like_native(L):
+    """the Python attempt_rebalance applies the same migration-
+    aware check as the native lb_step (same decision on both sides of the
+    break-even ratio), and refuses to run it without counts."""
+    from paper_2104_11385_b200.balancer import BalancePolicy, attempt_rebalance
+    from paper_2104_11385_b200.cost import CostVector
+    from paper_2104_11385_b200.decomposition import DistributionMapping
+    from paper_2104_11385_b200.scenarios import load_spec
+    sc = load_spec("mini").scenario
+    rng = np.random.default_rng(3)
+    for trial in range(6):
+        counts = np.zeros(225, dtype=np.int64)
+        k = int(rng.integers(5, 60))
+        counts[:k] = rng.integers(100, 5000, size=k)
+        owner = O.slab_mapping(225, 8)
+        cv = CostVector(values=O.heuristic_cost(counts, np.full(225, sc.box_size ** 2),
+                                                0.75, 0.25), step=0)
+        dm = DistributionMapping(owner=owner, n_ranks=8)
+        with pytest.raises(ValueError, match="counts"):
+            attempt_rebalance(cv, dm, BalancePolicy(migration_ratio=1.0), 0)
+        for ratio in (0.0, 0.5, 2.0, 8.0, 30.0, 1e3, 1e9):
+            py = attempt_rebalance(cv, dm, BalancePolicy(migration_ratio=ratio), 0,
+                                   counts=counts).adopted
+            assert py == _native_adopt(L, sc, owner, counts, ratio), (trial, ratio)
+
+
 def test_integration_md_ctypes_binding():
     """The raw ctypes binding INTEGRATION.md shows a reference maintainer
     (no package import, plain CDLL + argtypes) gives the oracle's owners."""
