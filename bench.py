@@ -129,13 +129,18 @@ def bench_config(args, world: int) -> dict:
             "l2": "inputs larger than L2 (3.3 GB particle state per GPU vs 126 MB L2)"}
 
 
-def c2_spec(args, world: int, steps: int):
-    """Package RunSpec + ScenarioConfig of the B200 arm."""
+def c2_spec(n_ranks: int, steps: int, cost: str, initial_mapping: str = "slab"):
+    """Package RunSpec + ScenarioConfig of the C2 bench workload."""
     from paper_2104_11385_b200.scenarios import spec_from_dict
 
-    spec = spec_from_dict(c2_doc(args.cost, bench_ranks(args, world), steps,
-                                 bench_initial_mapping(args, world)))
+    spec = spec_from_dict(c2_doc(cost, n_ranks, steps, initial_mapping))
     return spec, spec.scenario
+
+
+def arm_spec(args, world: int, steps: int):
+    """The B200 arm's spec (the config bench_config describes)."""
+    return c2_spec(bench_ranks(args, world), steps, args.cost,
+                   bench_initial_mapping(args, world))
 
 
 def base_particles(spec):
@@ -359,7 +364,7 @@ def run_lbx(args, rank, world, local_rank):
             dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
         return run_lbx_dist(args, rank, world, dev)
     total = args.warmup + args.steps
-    spec, sc = c2_spec(args, world, total)
+    spec, sc = arm_spec(args, world, total)
     pos0, kick0 = base_particles(spec)
     R = args.replicas
     pos = torch.from_numpy(pos0).to(dev).repeat(R, 1)
@@ -536,7 +541,7 @@ def run_lbx_dist(args, rank, world, dev):
     from paper_2104_11385_b200.parallel import DistributedSimulation, TorchComm
 
     total = args.warmup + args.steps
-    spec, sc = c2_spec(args, world, total)
+    spec, sc = arm_spec(args, world, total)
     pos0, kick0 = base_particles(spec)
     R = args.replicas * world
     n_total = pos0.shape[0] * R

@@ -274,13 +274,16 @@ typedef struct lbx_sim_config {
   /* GpuClock cost form (cost_kind == LBX_COST_GPUCLOCK):
    *   LBX_CLOCK_RAW        cost_b = clock tally_b (the paper's thread-summed
    *                        cycles of the particle kernel);
-   *   LBX_CLOCK_CALIBRATED cost_b = clk_b * (w_particle * N / sum clk)
-   *                        + w_cell * cells_b: the measured tally carries
-   *                        the particle work's distribution over boxes,
-   *                        scaled to the heuristic's particle units (N =
-   *                        particles alive), plus the per-box field work,
-   *                        which no particle kernel measures and which is
-   *                        identical for equal-size boxes. */
+   *   LBX_CLOCK_CALIBRATED cost_b = K_b * (w_particle * Nbar / sum K)
+   *                        + w_cell * cells_b, K = the tallies summed over
+   *                        the LB window (the steps since the previous
+   *                        attempt, reset after each attempt), Nbar = mean
+   *                        particles per step over the window: the measured
+   *                        tally carries the particle work's distribution
+   *                        over boxes, scaled to the heuristic's particle
+   *                        units, plus the per-box field work, which no
+   *                        particle kernel measures and which is identical
+   *                        for equal-size boxes. */
   int32_t clock_mode;
 } lbx_sim_config;
 

@@ -28,6 +28,7 @@ struct DevState {
   unsigned long long removed_count;  // removed indices listed this call
   unsigned long long holes;          // hole-fill cursors
   unsigned long long movers;
+  unsigned int rot;           // GpuClock chunk-rotation counter (stream_kernel)
 };
 
 // Host-side model of the particle state's pushed-and-binned step.

@@ -60,6 +60,11 @@ constexpr int kSmemBoxesMax = 12288;      // shared-memory histogram limit (96 K
 constexpr int kFlushIters = 128;          // push iterations between histogram flushes
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kClockShift = 4;            // GpuClock tally unit: 16 SM cycles
+#ifndef LBX_CLOCK_AFTER_LOADS
+#define LBX_CLOCK_AFTER_LOADS 1
+#endif
+constexpr bool kClockAfterLoads = LBX_CLOCK_AFTER_LOADS;
+
 
 constexpr int kEpochShift = 42;
 constexpr int kFlagShift = 40;
@@ -254,6 +259,7 @@ __global__ void __launch_bounds__(kBlock, LBX_STREAM_MINB) stream_kernel(StepPar
   unsigned* s_clk = s_cnt + p.nb;
   int* s_owner = reinterpret_cast<int*>(s_cnt + (kClock ? 2 : 1) * p.nb);
   __shared__ long long s_n;
+  __shared__ unsigned s_rot;
   __shared__ int s_last;
   __shared__ unsigned long long s_red[kWarps];
   __shared__ long long s_min[kWarps];
@@ -261,7 +267,10 @@ __global__ void __launch_bounds__(kBlock, LBX_STREAM_MINB) stream_kernel(StepPar
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  if (tid == 0) s_n = *((volatile long long*)&p.st->n);
+  if (tid == 0) {
+    s_n = *((volatile long long*)&p.st->n);
+    s_rot = *((volatile unsigned*)&p.st->rot);
+  }
   if (p.smem_hist) {
     for (int b = tid; b < p.nb; b += kBlock) {
       if (kHist) s_cnt[b] = 0u;
@@ -273,7 +282,6 @@ __global__ void __launch_bounds__(kBlock, LBX_STREAM_MINB) stream_kernel(StepPar
   const int* owner = p.smem_hist ? s_owner : p.owner;
   const long long n = s_n;
   const long long npairs = (n + 1) >> 1;
-  const long long stride = (long long)gridDim.x * kBlock * kPairs;
   double2* z2 = reinterpret_cast<double2*>(p.z);
   double2* x2 = reinterpret_cast<double2*>(p.x);
   const double2* vz2 = reinterpret_cast<const double2*>(p.vz);
@@ -285,9 +293,25 @@ __global__ void __launch_bounds__(kBlock, LBX_STREAM_MINB) stream_kernel(StepPar
   int iter = 0;
   // The loop trip count is uniform across the CTA (grid-stride over
   // CTA-sized chunks), so the periodic histogram flush can use barriers.
-  for (long long q0 = (long long)blockIdx.x * kBlock * kPairs; q0 < npairs; q0 += stride) {
+  // GpuClock: the chunk -> CTA assignment is rotated by a pseudo-random
+  // offset every step (DevState::rot), so a box's particles do not sit in the
+  // same CTA slot / wave step after step: at L2-resident sizes the thread
+  // time of a chunk depends on when it runs (full first wave vs draining
+  // tail), and the runtime sums the tally over the LB window, where the
+  // rotation averages that out.
+  const long long chunk = (long long)kBlock * kPairs;
+  const long long nchunks = (npairs + chunk - 1) / chunk;
+  // offset = nchunks x frac(rot x golden ratio): a Weyl sequence, so any
+  // window of consecutive steps spreads its offsets evenly over the chunks
+  const unsigned long long phase = ((unsigned long long)s_rot * 0x9E3779B97F4A7C15ull) >> 32;
+  const long long rot =
+      kClock && nchunks > 1 ? (long long)((phase * (unsigned long long)nchunks) >> 32) : 0;
+  for (long long k = blockIdx.x; k < nchunks; k += gridDim.x) {
+    long long c = k + rot;
+    if (c >= nchunks) c -= nchunks;
+    const long long q0 = c * chunk;
     long long t0 = 0;
-    if (kClock) t0 = clock64();
+    if (kClock && !kClockAfterLoads) t0 = clock64();
     double pz[2 * kPairs], px[2 * kPairs], pvz[2 * kPairs], pvx[2 * kPairs];
     bool keep[2 * kPairs], valid[2 * kPairs];
 #pragma unroll
@@ -321,6 +345,12 @@ __global__ void __launch_bounds__(kBlock, LBX_STREAM_MINB) stream_kernel(StepPar
       valid[2 * r] = any;
       valid[2 * r + 1] = 2 * q + 1 < n;
     }
+    // GpuClock window: opened after the pushed positions exist, i.e. after the
+    // loads landed (the CS2R issues behind the DADDs that consume them), so
+    // the tally is the thread's compute time on its particles -- not the
+    // memory latency, which at L2-resident sizes depends on WHEN a chunk runs
+    // (first or second wave) rather than on the box's work.
+    if (kClock && kClockAfterLoads) t0 = clock64();
 #pragma unroll
     for (int k = 0; k < 2 * kPairs; ++k) keep[k] = valid[k] && inside(pz[k], px[k], p.ez, p.ex);
 
@@ -474,6 +504,7 @@ __global__ void __launch_bounds__(kBlock, LBX_STREAM_MINB) stream_kernel(StepPar
     p.st->n = n_new;
     p.st->done = 0u;
     p.st->staged = 0ull;
+    if (kClock) p.st->rot += 1u;
     __threadfence_system();
   }
 }

@@ -38,6 +38,10 @@ struct lbx_lb {
   std::vector<int64_t> owner, prop, prev;
   std::vector<double> work, scratch, rank_acc;
   std::vector<int64_t> faces_per_rank;
+  // calibrated GpuClock: tallies summed over the LB window (the steps since
+  // the previous attempt), reset after every attempt
+  std::vector<uint64_t> clk_acc;
+  int64_t acc_n = 0, acc_steps = 0;
 };
 
 struct lbx_sim {
@@ -162,17 +166,22 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
     case LBX_COST_GPUCLOCK:
       if (!clk) return set_error(LBX_EINVAL, "GpuClock costs need the clock tally");
       if (c.clock_mode == LBX_CLOCK_CALIBRATED) {
-        // cost.py GpuClockProvider.calibrated: the same operations in the
-        // same order (integer sums, one scale, mul then add)
+        // cost.py calibrated_gpuclock_cost: the same operations in the same
+        // order (integer sums over the window, one scale, mul then add)
+        if ((int)s->clk_acc.size() != nb) s->clk_acc.assign(nb, 0);
         uint64_t tot = 0;
         int64_t np_ = 0;
         for (int b = 0; b < nb; ++b) {
-          tot += clk[b];
+          s->clk_acc[b] += clk[b];
+          tot += s->clk_acc[b];
           np_ += counts[b];
         }
-        const double scale = tot ? c.w_particle * (double)np_ / (double)tot : 0.0;
+        s->acc_n += np_;
+        s->acc_steps += 1;
+        const double mean_n = (double)s->acc_n / (double)s->acc_steps;
+        const double scale = tot ? c.w_particle * mean_n / (double)tot : 0.0;
         const double cell = c.w_cell * cells;
-        for (int b = 0; b < nb; ++b) cost[b] = (double)clk[b] * scale + cell;
+        for (int b = 0; b < nb; ++b) cost[b] = (double)s->clk_acc[b] * scale + cell;
       } else {
         for (int b = 0; b < nb; ++b) cost[b] = (double)clk[b];
       }
@@ -233,6 +242,10 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
         std::memcpy(o->adopt_owners + (size_t)o->n_adoptions * nb, s->owner.data(),
                     8 * (size_t)nb);
       o->n_adoptions += 1;
+    }
+    if (c.cost_kind == LBX_COST_GPUCLOCK && c.clock_mode == LBX_CLOCK_CALIBRATED) {
+      std::fill(s->clk_acc.begin(), s->clk_acc.end(), 0ull);   // new LB window
+      s->acc_n = s->acc_steps = 0;
     }
   }
 

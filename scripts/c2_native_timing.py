@@ -14,7 +14,7 @@ from paper_2104_11385_b200.workload import Simulation  # noqa: E402
 
 dev = torch.device("cuda:0")
 out = {}
-for cost in ("gpuclock", "heuristic"):
+for cost in sys.argv[2].split(",") if len(sys.argv) > 2 else ("gpuclock", "heuristic"):
     spec, sc = bench.c2_spec(int(sys.argv[1]) if len(sys.argv) > 1 else 1, 420, cost)
     pos0, kick0 = bench.base_particles(spec)
     for timed in (False, True):

@@ -94,9 +94,9 @@ def test_config_errors_name_the_field(P):
 
 
 def test_gpuclock_provider_forms(P):
-    """GpuClock cost forms: raw = the tally; calibrated = tally scaled to the
-    heuristic's particle units + the per-box cell work (the same operations
-    as lbx_runtime.cpp's lb_step)."""
+    """GpuClock cost forms: raw = the tally; calibrated = the tallies summed
+    over the LB window, scaled to the heuristic's particle units, + the
+    per-box cell work (the same operations as lbx_runtime.cpp's lb_step)."""
     clk = np.array([0, 1000, 3000, 0, 6000], dtype=np.uint64)
     counts = np.array([0, 10, 30, 0, 60], dtype=np.int64)
     cells = np.full(5, 1024.0)
@@ -109,6 +109,14 @@ def test_gpuclock_provider_forms(P):
     scale = 0.75 * 100.0 / 10000.0
     assert v.tolist() == [c * scale + 0.25 * 1024.0 for c in clk.astype(float)]
     assert abs(v.sum() - (0.75 * counts.sum() + 0.25 * cells.sum())) < 1e-9
+    # second step of the window: tallies and particles accumulate
+    clk2 = np.array([0, 3000, 1000, 0, 6000], dtype=np.uint64)
+    v2 = cal.assess(counts, cells, None, 1, clock=clk2).values
+    acc = (clk + clk2).astype(float)
+    scale2 = 0.75 * (200.0 / 2.0) / acc.sum()
+    assert v2.tolist() == [c * scale2 + 0.25 * 1024.0 for c in acc]
+    cal.reset_window()
+    assert cal.assess(counts, cells, None, 2, clock=clk).values.tolist() == v.tolist()
     with pytest.raises(ValueError, match="clock"):
         cal.assess(counts, cells, None, 0)
     with pytest.raises(P.ConfigError):

@@ -126,8 +126,18 @@ def test_gpuclock_run_rank_correlates_with_true_work(runs):
         rw = np.argsort(np.argsort(counts[occ]))
         rho = np.corrcoef(rc, rw)[0, 1]
         assert rho > 0.9, (s, rho)
-        want = prov.assess(counts, cells, None, s, clock=clk).values
-        assert np.array_equal(res.cost_trace[s], want)
+    # calibrated costs: the window's summed tallies (reset after every
+    # attempt step, interval 10) through calibrated_gpuclock_cost
+    from paper_2104_11385_b200.cost import calibrated_gpuclock_cost
+    lo = 0
+    for s in range(60):
+        win = slice(lo, s + 1)
+        want = calibrated_gpuclock_cost(res.clock_trace[win].sum(axis=0, dtype=np.uint64),
+                                        int(res.count_trace[win].sum()), s + 1 - lo, cells,
+                                        prov.weights, s).values
+        assert np.array_equal(res.cost_trace[s], want), s
+        if s % spec.policy.interval == 0:
+            lo = s + 1
 
 
 def _true_work_efficiency(res, cfg):
