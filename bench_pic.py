@@ -18,7 +18,10 @@ launch stream:
   push_deposit_resort   in place with lbx_pic_sort (cell counting sort)
                         every --resort steps, its cost inside the timed step;
   push_deposit_tiled    the same with the tile-major sort and LBX_PIC_TILED
-                        steps (shared-memory patch and current).
+                        steps (shared-memory patch and current);
+  push_deposit_fast     in place, tolerance mode (LBX_PIC_FAST: float32
+                        Boris increment, FMA gathers);
+  push_deposit_fast_resort  the same with lbx_pic_sort every --resort steps.
 Roofline: HBM, algorithmic bytes = 80 B per particle (read z,x,uz,ux,uy +
 write them, float64) -- field patch and current flush traffic is counted
 separately from ncu (profiles/).  Prints one JSON object.
@@ -99,21 +102,25 @@ def main():
                                    ("push_deposit_noclock", False, True, False),
                                    ("full_step", True, True, True),
                                    ("push_deposit_resort", False, False, True),
-                                   ("push_deposit_tiled", False, False, True)):
+                                   ("push_deposit_tiled", False, False, True),
+                                   ("push_deposit_fast", False, False, True),
+                                   ("push_deposit_fast_resort", False, False, True)):
         if mode not in args.modes.split(","):
             continue
         st = pic.PicState.create(pos0[:1], u0[:1], nz, nx, device=dev)
         for name, t in init.items():
             setattr(st, name, t.clone())
         st.n = n
-        resort = mode in ("push_deposit_resort", "push_deposit_tiled")
+        resort = mode in ("push_deposit_resort", "push_deposit_tiled",
+                          "push_deposit_fast_resort")
         tiled = mode == "push_deposit_tiled"
+        fast = mode.startswith("push_deposit_fast")
         if resort:   # start cell-ordered, like the other modes' first sorted step
             pic.pic_sort(ctx, st, tiled=tiled)
         for w in range(args.warmup):
             try:
                 pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=clk, field_solve=solve,
-                             sort=sort, tiled=tiled)
+                             sort=sort, tiled=tiled, fast=fast)
             except ValueError as e:
                 raise ValueError(f"mode {mode} warm-up step {w}: {e}") from None
         times = []
@@ -125,7 +132,7 @@ def main():
                 pic.pic_sort(ctx, st, tiled=tiled)
             try:
                 pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=clk, field_solve=solve,
-                             sort=sort, tiled=tiled)
+                             sort=sort, tiled=tiled, fast=fast)
             except ValueError as e:
                 raise ValueError(f"mode {mode} step {len(times)}: {e}") from None
             e1.record(stream)

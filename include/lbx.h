@@ -390,6 +390,11 @@ int lbx_sim_particles(lbx_sim* sim, int64_t* n, void* stream);
                                    /* Sparse plasmas; not with sorted mode   */
                                    /* or LBX_PIC_DEFER_CURRENT               */
 
+#define LBX_PIC_FAST 256u          /* tolerance mode (in place, untiled):   */
+                                   /* float32 Boris increment with FMA and  */
+                                   /* MUFU rsqrt/rcp, FMA gathers; checked  */
+                                   /* against the fp64 oracle at a stated   */
+                                   /* tolerance, not bit-exact              */
 typedef struct lbx_pic_args {
   double* z;
   double* x;

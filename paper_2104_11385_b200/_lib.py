@@ -128,6 +128,7 @@ LBX_PIC_QUAD = 16
 LBX_PIC_STABLE_ORDER = 64
 LBX_PIC_DIRECT = 32
 LBX_PIC_TILED = 128
+LBX_PIC_FAST = 256
 
 
 class PicArgs(C.Structure):

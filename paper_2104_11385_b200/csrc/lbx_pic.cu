@@ -137,6 +137,15 @@ __device__ __forceinline__ float cic(const float4 q, float fz, float fx) {
   return __fadd_rn(__fmul_rn(gz, lo), __fmul_rn(fz, hi));
 }
 
+// Tolerance mode (LBX_PIC_FAST): the same bilinear form with FMA
+// contraction, a + f (b - a) per axis.
+__device__ __forceinline__ float lerp_f(float a, float b, float f) {
+  return __fmaf_rn(f, __fsub_rn(b, a), a);
+}
+__device__ __forceinline__ float cic_fast(const float4 q, float fz, float fx) {
+  return lerp_f(lerp_f(q.x, q.y, fx), lerp_f(q.z, q.w, fx), fz);
+}
+
 // Fire-and-forget adds (REDG; a plain atomicAdd may keep the returning ATOMG
 // form inside large kernels).
 __device__ __forceinline__ void red_add(unsigned long long* a, long long v) {
@@ -268,41 +277,170 @@ __device__ __forceinline__ void enqueue(FlushEntry* e, const int v[kNodes], int 
 // the particles are too sparse for the copy to pay (kQuad = false: each
 // node's quad would be fetched from HBM for a handful of particles), from
 // the field array itself (four 4-byte loads, 4x less gathered footprint).
-template <bool kQuad>
+template <bool kQuad, bool kFast = false>
 __device__ __forceinline__ float gather_c(const PicParams& p, int c, int i0, int j0, float fz,
                                           float fx) {
-  if (kQuad) return cic(__ldg(p.Q[c] + (i0 + 1) * p.qpitch + (j0 + 1)), fz, fx);
-  const float* F = p.F[c] + (i0 + 1) * p.pitch + (j0 + 1);
-  return cic(make_float4(__ldg(F), __ldg(F + 1), __ldg(F + p.pitch), __ldg(F + p.pitch + 1)), fz,
-             fx);
+  float4 q;
+  if (kQuad) {
+    q = __ldg(p.Q[c] + (i0 + 1) * p.qpitch + (j0 + 1));
+  } else {
+    const float* F = p.F[c] + (i0 + 1) * p.pitch + (j0 + 1);
+    q = make_float4(__ldg(F), __ldg(F + 1), __ldg(F + p.pitch), __ldg(F + p.pitch + 1));
+  }
+  return kFast ? cic_fast(q, fz, fx) : cic(q, fz, fx);
 }
 
-template <bool kClock, bool kSort, bool kQuad>
-__global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p) {
-  extern __shared__ __align__(16) unsigned char s_dyn[];
-  FlushEntry* s_q = reinterpret_cast<FlushEntry*>(s_dyn) + (size_t)(threadIdx.x >> 5) * kQCap;
-  unsigned* s_cnt = reinterpret_cast<unsigned*>(s_dyn + (size_t)kPW * kQCap * sizeof(FlushEntry));  // nb
-  unsigned* s_clk = s_cnt + p.nb;                                                                   // nb
-  __shared__ long long s_n;
-  __shared__ int s_box[4];
-  __shared__ int s_last;
-  __shared__ unsigned long long s_red[kPW];
-  __shared__ long long s_min[kPW];
+// Tolerance-mode relativistic Boris (LBX_PIC_FAST).  The rotation is
+// evaluated in float32 (FMA, MUFU rsqrt / rcp) but only as the INCREMENT
+// du = u_new - u = 2 hE + (u- x t) + s (u' x t), which is added to the
+// float64 momenta; the new 1/gamma is float32 too.  Error: float32 rounding
+// of du (not of u) -- see oracle/pic_oracle.py boris_fast and the tolerance
+// tests.  Returns 1/gamma(u_new) in float32.
+__device__ __forceinline__ float boris_fast(double& ux, double& uy, double& uz, float hf,
+                                            float Ex, float Ey, float Ez, float Bx, float By,
+                                            float Bz) {
+  const float hEx = hf * Ex, hEy = hf * Ey, hEz = hf * Ez;
+  const float mx = __fadd_rn((float)ux, hEx), my = __fadd_rn((float)uy, hEy),
+              mz = __fadd_rn((float)uz, hEz);
+  const float ig = rsqrtf(__fmaf_rn(mz, mz, __fmaf_rn(my, my, __fmaf_rn(mx, mx, 1.f))));
+  const float tx = hf * Bx * ig, ty = hf * By * ig, tz = hf * Bz * ig;
+  const float sr = __frcp_rn(__fmaf_rn(tz, tz, __fmaf_rn(ty, ty, __fmaf_rn(tx, tx, 1.f))));
+  const float s2 = 2.f * sr;
+  // u' - u- = u- x t ; u+ - u- = s (u' x t)
+  const float cx = __fmaf_rn(my, tz, -mz * ty), cy = __fmaf_rn(mz, tx, -mx * tz),
+              cz = __fmaf_rn(mx, ty, -my * tx);
+  const float px = mx + cx, py = my + cy, pz = mz + cz;
+  const float rx = s2 * __fmaf_rn(py, tz, -pz * ty), ry = s2 * __fmaf_rn(pz, tx, -px * tz),
+              rz = s2 * __fmaf_rn(px, ty, -py * tx);
+  ux = __dadd_rn(ux, (double)(__fmaf_rn(2.f, hEx, rx)));
+  uy = __dadd_rn(uy, (double)(__fmaf_rn(2.f, hEy, ry)));
+  uz = __dadd_rn(uz, (double)(__fmaf_rn(2.f, hEz, rz)));
+  const float fx = (float)ux, fy = (float)uy, fz = (float)uz;
+  return rsqrtf(__fmaf_rn(fz, fz, __fmaf_rn(fy, fy, __fmaf_rn(fx, fx, 1.f))));
+}
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// Tolerance mode (LBX_PIC_FAST): cell by truncation, fraction rounded to
+// float32 once (the exact mode's axis_of floors in fp64 and rounds twice).
+__device__ __forceinline__ Axis fast_axis(double v) {
+  Axis a;
+  a.i = __double2int_rz(v);                       // v >= 0 inside the grid: trunc == floor
+  a.f = __double2float_rn(__dsub_rn(v, (double)a.i));
+  a.hi = a.f >= 0.5f;
+  a.ih = a.hi ? a.i : a.i - 1;
+  a.fh = __fadd_rn(a.f, a.hi ? -0.5f : 0.5f);
+  return a;
+}
+
+template <bool kFast>
+__device__ __forceinline__ Axis pic_axis(double v) {
+  return kFast ? fast_axis(v) : axis_of(v);
+}
+
+// Per-CTA state shared by the push kernels' prologue / epilogue.
+struct PushShared {
+  long long n;
+  int box[4];
+  int last;
+  unsigned long long red[kPW];
+  long long min[kPW];
+};
+
+template <bool kClock>
+__device__ __forceinline__ void push_prologue(const PicParams& p, PushShared& sh, unsigned* s_cnt,
+                                              unsigned* s_clk) {
+  const int tid = threadIdx.x;
   if (tid == 0) {
-    s_n = *((volatile long long*)&p.st->n);
-    s_box[0] = INT_MAX;
-    s_box[1] = INT_MIN;
-    s_box[2] = INT_MAX;
-    s_box[3] = INT_MIN;
+    sh.n = *((volatile long long*)&p.st->n);
+    sh.box[0] = INT_MAX;
+    sh.box[1] = INT_MIN;
+    sh.box[2] = INT_MAX;
+    sh.box[3] = INT_MIN;
   }
   for (int b = tid; b < p.nb; b += kPB) {
     s_cnt[b] = 0u;
     if (kClock) s_clk[b] = 0u;
   }
   __syncthreads();
-  const long long n = s_n;
+}
+
+// CTA totals (removed count, first removed slot, errors, deposit bounding
+// box), histogram flush, and the last CTA's step record.
+template <bool kClock>
+__device__ __forceinline__ void push_epilogue(const PicParams& p, PushShared& sh, long long n,
+                                              unsigned long long removed, long long first_out,
+                                              long long err, int bimin, int bimax, int bjmin,
+                                              int bjmax, const unsigned* s_cnt,
+                                              const unsigned* s_clk) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned long long wa = (unsigned long long)warp_sum((long long)removed);
+  const long long wm = warp_min(first_out), we = warp_sum(err);
+  const int wimin = __reduce_min_sync(kAll, bimin), wimax = __reduce_max_sync(kAll, bimax);
+  const int wjmin = __reduce_min_sync(kAll, bjmin), wjmax = __reduce_max_sync(kAll, bjmax);
+  if (lane == 0) {
+    sh.red[warp] = wa;
+    sh.min[warp] = wm;
+    if (we) atomicAdd((unsigned long long*)&p.st->err, (unsigned long long)we);
+    if (wimin <= wimax) {
+      atomicMin(&sh.box[0], wimin);
+      atomicMax(&sh.box[1], wimax);
+      atomicMin(&sh.box[2], wjmin);
+      atomicMax(&sh.box[3], wjmax);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long ta = 0;
+    long long tm = LLONG_MAX;
+    for (int w = 0; w < kPW; ++w) {
+      ta += sh.red[w];
+      tm = min(tm, sh.min[w]);
+    }
+    if (ta) {
+      atomicAdd(&p.st->leavers, ta);
+      atomicMin(&p.st->first_leaver, tm);
+    }
+    if (sh.box[0] <= sh.box[1]) {
+      atomicMin(p.dep_box + 0, sh.box[0]);
+      atomicMax(p.dep_box + 1, sh.box[1]);
+      atomicMin(p.dep_box + 2, sh.box[2]);
+      atomicMax(p.dep_box + 3, sh.box[3]);
+    }
+  }
+  for (int b = tid; b < p.nb; b += kPB) {
+    if (s_cnt[b]) atomicAdd(p.g_cnt + b, (unsigned long long)s_cnt[b]);
+    if (kClock && s_clk[b]) atomicAdd(p.g_clk + b, (unsigned long long)s_clk[b]);
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) sh.last = (atomicAdd(&p.st->done, 1u) == gridDim.x - 1) ? 1 : 0;
+  __syncthreads();
+  if (!sh.last) return;
+  __threadfence();
+  step_record<kClock>(p.g_cnt, p.g_clk, p.nb, p.counts_out, p.cost_out, p.clk_out, p.wp, p.wc,
+                      p.cells, 4);
+  if (tid == 0) {
+    const long long n_new = n - (long long)*((volatile unsigned long long*)&p.st->leavers);
+    if (p.n_out) *p.n_out = n_new;
+    if (p.err_out) *p.err_out = *((volatile long long*)&p.st->err);
+    p.st->n_old = n;
+    p.st->n = n_new;
+    p.st->done = 0u;
+    __threadfence_system();
+  }
+}
+
+// kFast: tolerance mode (LBX_PIC_FAST) -- fast_axis, FMA gathers, float32
+// Boris increment (boris_fast); same work structure, not bit-exact.
+template <bool kClock, bool kSort, bool kQuad, bool kFast = false>
+__global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p) {
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  FlushEntry* s_q = reinterpret_cast<FlushEntry*>(s_dyn) + (size_t)(threadIdx.x >> 5) * kQCap;
+  unsigned* s_cnt = reinterpret_cast<unsigned*>(s_dyn + (size_t)kPW * kQCap * sizeof(FlushEntry));  // nb
+  unsigned* s_clk = s_cnt + p.nb;                                                                   // nb
+  __shared__ PushShared sh;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  push_prologue<kClock>(p, sh, s_cnt, s_clk);
+  const long long n = sh.n;
   const long long units = (n + kUnitP - 1) / kUnitP;
   const double ez = (double)p.nz, ex = (double)p.nx;
   const double h = 0.5 * p.qm * p.dt;
@@ -362,14 +500,27 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
       float vsx[kG], vsy[kG], vsz[kG];
 #pragma unroll
       for (int k = 0; k < kG; ++k) {
-        const Axis az = axis_of(pz[k]), ax = axis_of(px[k]);
+        const Axis az = pic_axis<kFast>(pz[k]), ax = pic_axis<kFast>(px[k]);
         // staggers: (0, 1/2) Ex Bz | (0, 0) Ey | (1/2, 0) Ez Bx | (1/2, 1/2) By
-        const float Ex = gather_c<kQuad>(p, 0, az.i, ax.ih, az.f, ax.fh);
-        const float Ey = gather_c<kQuad>(p, 1, az.i, ax.i, az.f, ax.f);
-        const float Ez = gather_c<kQuad>(p, 2, az.ih, ax.i, az.fh, ax.f);
-        const float Bx = gather_c<kQuad>(p, 3, az.ih, ax.i, az.fh, ax.f);
-        const float By = gather_c<kQuad>(p, 4, az.ih, ax.ih, az.fh, ax.fh);
-        const float Bz = gather_c<kQuad>(p, 5, az.i, ax.ih, az.f, ax.fh);
+        const float Ex = gather_c<kQuad, kFast>(p, 0, az.i, ax.ih, az.f, ax.fh);
+        const float Ey = gather_c<kQuad, kFast>(p, 1, az.i, ax.i, az.f, ax.f);
+        const float Ez = gather_c<kQuad, kFast>(p, 2, az.ih, ax.i, az.fh, ax.f);
+        const float Bx = gather_c<kQuad, kFast>(p, 3, az.ih, ax.i, az.fh, ax.f);
+        const float By = gather_c<kQuad, kFast>(p, 4, az.ih, ax.ih, az.fh, ax.fh);
+        const float Bz = gather_c<kQuad, kFast>(p, 5, az.i, ax.ih, az.f, ax.fh);
+        if (kFast) {
+          const float ig = boris_fast(pux[k], puy[k], puz[k], (float)h, Ex, Ey, Ez, Bx, By, Bz);
+          const float dtg = (float)p.dt * ig;
+          pz[k] = __dadd_rn(pz[k], (double)__fmul_rn(dtg, (float)puz[k]));
+          px[k] = __dadd_rn(px[k], (double)__fmul_rn(dtg, (float)pux[k]));
+          keep[k] = i0 + k < n && pz[k] >= 0.0 && pz[k] < ez && px[k] >= 0.0 && px[k] < ex;
+          nkey[k] = keep[k] ? __double2int_rz(pz[k]) * p.nx + __double2int_rz(px[k]) : -1;
+          const float qv = keep[k] ? __fmul_rn((float)p.qw * p.vscale, ig) : 0.f;
+          vsx[k] = __fmul_rn(qv, (float)pux[k]);
+          vsy[k] = __fmul_rn(qv, (float)puy[k]);
+          vsz[k] = __fmul_rn(qv, (float)puz[k]);
+          continue;
+        }
         // relativistic Boris (x, y, z order; oracle boris())
         const double hEx = __dmul_rn(h, (double)Ex), hEy = __dmul_rn(h, (double)Ey),
                      hEz = __dmul_rn(h, (double)Ez);
@@ -451,7 +602,7 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
 #pragma unroll
       for (int k = 0; k < kG; ++k) {
         const bool dep = nkey[k] >= 0;
-        const Axis az = axis_of(dep ? pz[k] : 0.5), ax = axis_of(dep ? px[k] : 0.5);
+        const Axis az = pic_axis<kFast>(dep ? pz[k] : 0.5), ax = pic_axis<kFast>(dep ? px[k] : 0.5);
         int q[kNodes];
         node_values(az, ax, vsx[k], vsy[k], vsz[k], q);   // v = 0 -> q = 0 off-deposit
         const bool same = dep && nkey[k] == cur;
@@ -525,62 +676,8 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
     }
   }
 
-  // ---- CTA totals, deposit box, histogram flush, epilogue ----
-  const unsigned long long wa = (unsigned long long)warp_sum((long long)removed);
-  const long long wm = warp_min(first_out), we = warp_sum(err);
-  const int wimin = __reduce_min_sync(kAll, bimin), wimax = __reduce_max_sync(kAll, bimax);
-  const int wjmin = __reduce_min_sync(kAll, bjmin), wjmax = __reduce_max_sync(kAll, bjmax);
-  if (lane == 0) {
-    s_red[warp] = wa;
-    s_min[warp] = wm;
-    if (we) atomicAdd((unsigned long long*)&p.st->err, (unsigned long long)we);
-    if (wimin <= wimax) {
-      atomicMin(&s_box[0], wimin);
-      atomicMax(&s_box[1], wimax);
-      atomicMin(&s_box[2], wjmin);
-      atomicMax(&s_box[3], wjmax);
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    unsigned long long ta = 0;
-    long long tm = LLONG_MAX;
-    for (int w = 0; w < kPW; ++w) {
-      ta += s_red[w];
-      tm = min(tm, s_min[w]);
-    }
-    if (ta) {
-      atomicAdd(&p.st->leavers, ta);
-      atomicMin(&p.st->first_leaver, tm);
-    }
-    if (s_box[0] <= s_box[1]) {
-      atomicMin(p.dep_box + 0, s_box[0]);
-      atomicMax(p.dep_box + 1, s_box[1]);
-      atomicMin(p.dep_box + 2, s_box[2]);
-      atomicMax(p.dep_box + 3, s_box[3]);
-    }
-  }
-  for (int b = tid; b < p.nb; b += kPB) {
-    if (s_cnt[b]) atomicAdd(p.g_cnt + b, (unsigned long long)s_cnt[b]);
-    if (kClock && s_clk[b]) atomicAdd(p.g_clk + b, (unsigned long long)s_clk[b]);
-  }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(&p.st->done, 1u) == gridDim.x - 1) ? 1 : 0;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  step_record<kClock>(p.g_cnt, p.g_clk, p.nb, p.counts_out, p.cost_out, p.clk_out, p.wp, p.wc,
-                      p.cells, 4);
-  if (tid == 0) {
-    const long long n_new = n - (long long)*((volatile unsigned long long*)&p.st->leavers);
-    if (p.n_out) *p.n_out = n_new;
-    if (p.err_out) *p.err_out = *((volatile long long*)&p.st->err);
-    p.st->n_old = n;
-    p.st->n = n_new;
-    p.st->done = 0u;
-    __threadfence_system();
-  }
+  push_epilogue<kClock>(p, sh, n, removed, first_out, err, bimin, bimax, bjmin, bjmax, s_cnt,
+                        s_clk);
 }
 
 // ---------------------------------------------------------------------------
@@ -1412,6 +1509,8 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   if (!(a->q_times_w != 0.0)) return set_error(LBX_EINVAL, "q_times_w must be nonzero");
   const bool tiled = (a->flags & LBX_PIC_TILED) != 0;
   if (tiled && sorted) return set_error(LBX_EINVAL, "LBX_PIC_TILED runs in place (no out[])");
+  if ((a->flags & LBX_PIC_FAST) && (sorted || tiled))
+    return set_error(LBX_EINVAL, "LBX_PIC_FAST runs in place, untiled");
   if (tiled && (a->flags & LBX_PIC_DEFER_CURRENT))
     return set_error(LBX_EINVAL, "LBX_PIC_TILED does not support LBX_PIC_DEFER_CURRENT");
   if (tiled && (ctx->pic_tiles_nz != a->nz || ctx->pic_tiles_nx != a->nx))
@@ -1562,6 +1661,7 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
                                                  a->fields[3], a->fields[4], a->fields[5], Q,
                                                  quad ? quads : 0, p.qpitch, pitch, dep_box);
   const bool clock = (a->flags & LBX_STEP_CLOCK) != 0;
+  const bool fast = (a->flags & LBX_PIC_FAST) != 0;
   size_t smem = (size_t)kPW * kQCap * sizeof(FlushEntry) + (size_t)nb * 8;
   void (*kern)(PicParams);
   const int ntx = (a->nx + kT - 1) / kT, ntz = (a->nz + kT - 1) / kT;
@@ -1574,7 +1674,10 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
     p.jn_stride = jn_stride;
     p.ntx = ntx;
     p.ntiles = ntz * ntx;
-  } else if (quad)
+  } else if (fast)
+    kern = clock ? (quad ? pic_push_kernel<true, false, true, true> : pic_push_kernel<true, false, false, true>)
+                 : (quad ? pic_push_kernel<false, false, true, true> : pic_push_kernel<false, false, false, true>);
+  else if (quad)
     kern = clock ? (sorted ? pic_push_kernel<true, true, true> : pic_push_kernel<true, false, true>)
                  : (sorted ? pic_push_kernel<false, true, true> : pic_push_kernel<false, false, true>);
   else

@@ -89,7 +89,7 @@ def pic_sort(ctx: Context, st: PicState, tiled: bool = False):
 
 def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times_w: float,
              dt: float, weights=(0.75, 0.25), clock=False, field_solve=True, sort=False,
-             gather=None, stable=False, tiled=False):
+             gather=None, stable=False, tiled=False, fast=False):
     """One PIC step; returns per-box counts / cost / clock and n.
 
     sort=False: in place; absorbed particles' slots are filled from the tail
@@ -99,7 +99,11 @@ def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times
     swaps in (order within a cell is not deterministic; values are).
     tiled=True: in place, one CTA per 16x16-cell tile with the field patch
     and the current in shared memory, on the tile ranges of the last
-    pic_sort(tiled=True) -- the sparse-plasma path."""
+    pic_sort(tiled=True) -- the sparse-plasma path.
+    fast=True (in place, untiled): tolerance mode (LBX_PIC_FAST) -- float32
+    Boris increment with FMA and MUFU rsqrt/rcp, FMA gathers; agrees with
+    the fp64 oracle within the tolerances tests/test_gpu_pic_fast.py states,
+    not bit for bit."""
     dev = ctx.device
     nbz, nbx = st.nz // box_size, st.nx // box_size
     nb = nbz * nbx
@@ -127,6 +131,10 @@ def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times
         if sort:
             raise ValueError("tiled steps run in place (sort=False)")
         a.flags |= _lib.LBX_PIC_TILED
+    if fast:
+        if sort or tiled:
+            raise ValueError("fast (tolerance) steps run in place, untiled")
+        a.flags |= _lib.LBX_PIC_FAST
     a.counts_out, a.cost_out, a.clk_out = _lib.ptr(counts), _lib.ptr(cost), _lib.ptr(clk)
     a.n_out, a.err_out = _lib.ptr(nout), _lib.ptr(nout[1:])
     names = ("z", "x", "uz", "ux", "uy")
