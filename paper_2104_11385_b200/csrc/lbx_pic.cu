@@ -227,6 +227,37 @@ __device__ __forceinline__ void node_values(const Axis& az, const Axis& ax, floa
   q[15] = qnode(vsz, zp, x1);
 }
 
+// Tolerance mode: the 16 node contributions of one particle as float
+// products, FMA-accumulated into the lane's float run sums (rounded to
+// fixed point once per run, at the flush, instead of per particle).
+__device__ __forceinline__ void node_accum(const Axis& az, const Axis& ax, float vsx, float vsy,
+                                           float vsz, float acc[kNodes]) {
+  const float z0 = __fsub_rn(1.f, az.f), z1 = az.f;
+  const float x0 = __fsub_rn(1.f, ax.f), x1 = ax.f;
+  const float zh = __fsub_rn(1.f, az.fh), xh = __fsub_rn(1.f, ax.fh);
+  const float zm = az.hi ? 0.f : zh, zc = az.hi ? zh : az.fh, zp = az.hi ? az.fh : 0.f;
+  const float xm = ax.hi ? 0.f : xh, xc = ax.hi ? xh : ax.fh, xp = ax.hi ? ax.fh : 0.f;
+  const float a0 = __fmul_rn(vsx, z0), a1 = __fmul_rn(vsx, z1);
+  acc[0] = __fmaf_rn(a0, xm, acc[0]);
+  acc[1] = __fmaf_rn(a0, xc, acc[1]);
+  acc[2] = __fmaf_rn(a0, xp, acc[2]);
+  acc[3] = __fmaf_rn(a1, xm, acc[3]);
+  acc[4] = __fmaf_rn(a1, xc, acc[4]);
+  acc[5] = __fmaf_rn(a1, xp, acc[5]);
+  const float b0 = __fmul_rn(vsy, z0), b1 = __fmul_rn(vsy, z1);
+  acc[6] = __fmaf_rn(b0, x0, acc[6]);
+  acc[7] = __fmaf_rn(b0, x1, acc[7]);
+  acc[8] = __fmaf_rn(b1, x0, acc[8]);
+  acc[9] = __fmaf_rn(b1, x1, acc[9]);
+  const float c0 = __fmul_rn(vsz, x0), c1 = __fmul_rn(vsz, x1);
+  acc[10] = __fmaf_rn(zm, c0, acc[10]);
+  acc[11] = __fmaf_rn(zm, c1, acc[11]);
+  acc[12] = __fmaf_rn(zc, c0, acc[12]);
+  acc[13] = __fmaf_rn(zc, c1, acc[13]);
+  acc[14] = __fmaf_rn(zp, c0, acc[14]);
+  acc[15] = __fmaf_rn(zp, c1, acc[15]);
+}
+
 // Per-warp flush queue in shared memory: a lane that must hand a cell's node
 // sums to HBM (cell change, isolated drifted particle, end of run) writes
 // them here with 4 vector stores inside the divergent branch; the warp then
@@ -246,7 +277,7 @@ struct __align__(16) FlushEntry {
 // entries, and within a group whenever fewer than 32 free entries remain.
 constexpr int kQCap = LBX_PIC_QCAP;
 
-template <bool kSort>
+template <bool kSort, bool kFast = false>
 __device__ __forceinline__ void drain_queue(const PicParams& p, const FlushEntry* q, int count,
                                             int lane) {
   __syncwarp();
@@ -255,12 +286,24 @@ __device__ __forceinline__ void drain_queue(const PicParams& p, const FlushEntry
     const int e = e0 + (lane >> 4);
     if (e < count) {
       const int cell = q[e].cell;
-      const int v = reinterpret_cast<const int*>(q[e].v)[node];
+      const int raw = reinterpret_cast<const int*>(q[e].v)[node];
+      // tolerance mode queues float run sums: rounded to fixed point here
+      const int v = kFast ? __float2int_rn(__int_as_float(raw)) : raw;
       if (v) red_add(p.Jc + (long long)cell * kNodes + node, v);
       if (kSort && node == 0) red_add32(p.cell_cnt + cell, q[e].m);
     }
   }
   __syncwarp();
+}
+
+__device__ __forceinline__ void enqueue_f(FlushEntry* e, const float v[kNodes], int cell,
+                                          unsigned m) {
+#pragma unroll
+  for (int i = 0; i < kNodes / 4; ++i)
+    e->v[i] = make_int4(__float_as_int(v[4 * i]), __float_as_int(v[4 * i + 1]),
+                        __float_as_int(v[4 * i + 2]), __float_as_int(v[4 * i + 3]));
+  e->cell = cell;
+  e->m = m;
 }
 
 __device__ __forceinline__ void enqueue(FlushEntry* e, const int v[kNodes], int cell, unsigned m) {
@@ -334,6 +377,15 @@ __device__ __forceinline__ Axis fast_axis(double v) {
 template <bool kFast>
 __device__ __forceinline__ Axis pic_axis(double v) {
   return kFast ? fast_axis(v) : axis_of(v);
+}
+
+// One component's 2x2 node quad at a precomputed node offset (quad copy or
+// the field array itself).
+template <bool kQuad>
+__device__ __forceinline__ float4 quad_at(const PicParams& p, int c, int off) {
+  if (kQuad) return __ldg(p.Q[c] + off);
+  const float* F = p.F[c] + off;
+  return make_float4(__ldg(F), __ldg(F + 1), __ldg(F + p.pitch), __ldg(F + p.pitch + 1));
 }
 
 // Per-CTA state shared by the push kernels' prologue / epilogue.
@@ -451,10 +503,15 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
   for (long long u = (long long)blockIdx.x * kPW + warp; u < units;
        u += (long long)gridDim.x * kPW) {
     const long long run0 = u * kUnitP + (long long)lane * kRun;
-    // deposit accumulator (cell-relative node sums of the lane's current cell)
+    // deposit accumulator (cell-relative node sums of the lane's current cell;
+    // tolerance mode: float run sums)
     int acc[kNodes];
+    float accf[kNodes];
 #pragma unroll
-    for (int i = 0; i < kNodes; ++i) acc[i] = 0;
+    for (int i = 0; i < kNodes; ++i) {
+      acc[i] = 0;
+      accf[i] = 0.f;
+    }
     int cur = -1;
     unsigned cur_m = 0;
     // per-box survivor run (+ GpuClock: time since the last box flush)
@@ -501,14 +558,16 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
 #pragma unroll
       for (int k = 0; k < kG; ++k) {
         const Axis az = pic_axis<kFast>(pz[k]), ax = pic_axis<kFast>(px[k]);
-        // staggers: (0, 1/2) Ex Bz | (0, 0) Ey | (1/2, 0) Ez Bx | (1/2, 1/2) By
-        const float Ex = gather_c<kQuad, kFast>(p, 0, az.i, ax.ih, az.f, ax.fh);
-        const float Ey = gather_c<kQuad, kFast>(p, 1, az.i, ax.i, az.f, ax.f);
-        const float Ez = gather_c<kQuad, kFast>(p, 2, az.ih, ax.i, az.fh, ax.f);
-        const float Bx = gather_c<kQuad, kFast>(p, 3, az.ih, ax.i, az.fh, ax.f);
-        const float By = gather_c<kQuad, kFast>(p, 4, az.ih, ax.ih, az.fh, ax.fh);
-        const float Bz = gather_c<kQuad, kFast>(p, 5, az.i, ax.ih, az.f, ax.fh);
         if (kFast) {
+          // the four stagger combinations' node offsets, computed once
+          const int pit = kQuad ? p.qpitch : p.pitch;
+          const int rA = (az.i + 1) * pit, rH = (az.ih + 1) * pit, cA = ax.i + 1, cH = ax.ih + 1;
+          const float Ex = cic_fast(quad_at<kQuad>(p, 0, rA + cH), az.f, ax.fh);
+          const float Ey = cic_fast(quad_at<kQuad>(p, 1, rA + cA), az.f, ax.f);
+          const float Ez = cic_fast(quad_at<kQuad>(p, 2, rH + cA), az.fh, ax.f);
+          const float Bx = cic_fast(quad_at<kQuad>(p, 3, rH + cA), az.fh, ax.f);
+          const float By = cic_fast(quad_at<kQuad>(p, 4, rH + cH), az.fh, ax.fh);
+          const float Bz = cic_fast(quad_at<kQuad>(p, 5, rA + cH), az.f, ax.fh);
           const float ig = boris_fast(pux[k], puy[k], puz[k], (float)h, Ex, Ey, Ez, Bx, By, Bz);
           const float dtg = (float)p.dt * ig;
           pz[k] = __dadd_rn(pz[k], (double)__fmul_rn(dtg, (float)puz[k]));
@@ -521,6 +580,13 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
           vsz[k] = __fmul_rn(qv, (float)puz[k]);
           continue;
         }
+        // staggers: (0, 1/2) Ex Bz | (0, 0) Ey | (1/2, 0) Ez Bx | (1/2, 1/2) By
+        const float Ex = gather_c<kQuad>(p, 0, az.i, ax.ih, az.f, ax.fh);
+        const float Ey = gather_c<kQuad>(p, 1, az.i, ax.i, az.f, ax.f);
+        const float Ez = gather_c<kQuad>(p, 2, az.ih, ax.i, az.fh, ax.f);
+        const float Bx = gather_c<kQuad>(p, 3, az.ih, ax.i, az.fh, ax.f);
+        const float By = gather_c<kQuad>(p, 4, az.ih, ax.ih, az.fh, ax.fh);
+        const float Bz = gather_c<kQuad>(p, 5, az.i, ax.ih, az.f, ax.fh);
         // relativistic Boris (x, y, z order; oracle boris())
         const double hEx = __dmul_rn(h, (double)Ex), hEy = __dmul_rn(h, (double)Ey),
                      hEz = __dmul_rn(h, (double)Ez);
@@ -603,30 +669,60 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
       for (int k = 0; k < kG; ++k) {
         const bool dep = nkey[k] >= 0;
         const Axis az = pic_axis<kFast>(dep ? pz[k] : 0.5), ax = pic_axis<kFast>(dep ? px[k] : 0.5);
-        int q[kNodes];
-        node_values(az, ax, vsx[k], vsy[k], vsz[k], q);   // v = 0 -> q = 0 off-deposit
         const bool same = dep && nkey[k] == cur;
         const bool strag = dep && !same && cur >= 0 && k + 1 < kG && nkey[k + 1] != nkey[k];
         const bool swap = dep && !same && !strag;
         const bool need = strag || (swap && cur >= 0);
         const unsigned fm = __ballot_sync(kAll, need);
-        if (need)
-          enqueue(s_q + qn + __popc(fm & lt), strag ? q : acc, strag ? nkey[k] : cur,
-                  strag ? 1u : cur_m);
-        qn += __popc(fm);
-        if (kQCap < 32 * kG && qn > kQCap - 32) {   // small queue: drain mid-group
-          drain_queue<kSort>(p, s_q, qn, lane);
-          qn = 0;
-        }
-        if (same) {
+        if (kFast) {
+          if (need) {
+            FlushEntry* e = s_q + qn + __popc(fm & lt);
+            if (strag) {
+              float w[kNodes];
 #pragma unroll
-          for (int i = 0; i < kNodes; ++i) acc[i] += q[i];
-          ++cur_m;
-        } else if (swap) {
+              for (int i = 0; i < kNodes; ++i) w[i] = 0.f;
+              node_accum(az, ax, vsx[k], vsy[k], vsz[k], w);
+              enqueue_f(e, w, nkey[k], 1u);
+            } else {
+              enqueue_f(e, accf, cur, cur_m);
+            }
+          }
+          qn += __popc(fm);
+          if (kQCap < 32 * kG && qn > kQCap - 32) {
+            drain_queue<kSort, kFast>(p, s_q, qn, lane);
+            qn = 0;
+          }
+          if (swap) {
 #pragma unroll
-          for (int i = 0; i < kNodes; ++i) acc[i] = q[i];
-          cur = nkey[k];
-          cur_m = 1;
+            for (int i = 0; i < kNodes; ++i) accf[i] = 0.f;
+            cur = nkey[k];
+            cur_m = 0;
+          }
+          if (same || swap) {
+            node_accum(az, ax, vsx[k], vsy[k], vsz[k], accf);
+            ++cur_m;
+          }
+        } else {
+          int q[kNodes];
+          node_values(az, ax, vsx[k], vsy[k], vsz[k], q);   // v = 0 -> q = 0 off-deposit
+          if (need)
+            enqueue(s_q + qn + __popc(fm & lt), strag ? q : acc, strag ? nkey[k] : cur,
+                    strag ? 1u : cur_m);
+          qn += __popc(fm);
+          if (kQCap < 32 * kG && qn > kQCap - 32) {   // small queue: drain mid-group
+            drain_queue<kSort>(p, s_q, qn, lane);
+            qn = 0;
+          }
+          if (same) {
+#pragma unroll
+            for (int i = 0; i < kNodes; ++i) acc[i] += q[i];
+            ++cur_m;
+          } else if (swap) {
+#pragma unroll
+            for (int i = 0; i < kNodes; ++i) acc[i] = q[i];
+            cur = nkey[k];
+            cur_m = 1;
+          }
         }
         if (!dep) continue;
         bimin = min(bimin, az.i);
@@ -652,12 +748,16 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
           hn = 1;
         }
       }
-      if (qn) drain_queue<kSort>(p, s_q, qn, lane);
+      if (qn) drain_queue<kSort, kFast>(p, s_q, qn, lane);
     }
     {   // end of the lane's run: queue its open cell, drain
       const unsigned fm = __ballot_sync(kAll, cur >= 0);
-      if (cur >= 0) enqueue(s_q + __popc(fm & ((1u << lane) - 1u)), acc, cur, cur_m);
-      if (fm) drain_queue<kSort>(p, s_q, __popc(fm), lane);
+      if (cur >= 0) {
+        FlushEntry* e = s_q + __popc(fm & ((1u << lane) - 1u));
+        if (kFast) enqueue_f(e, accf, cur, cur_m);
+        else enqueue(e, acc, cur, cur_m);
+      }
+      if (fm) drain_queue<kSort, kFast>(p, s_q, __popc(fm), lane);
     }
     // last box run of the lane: warp-uniform fast path (one shared atomic)
     unsigned tclk = 0;
