@@ -21,7 +21,12 @@ launch stream:
                         steps (shared-memory patch and current);
   push_deposit_fast     in place, tolerance mode (LBX_PIC_FAST: float32
                         Boris increment, FMA gathers);
-  push_deposit_fast_resort  the same with lbx_pic_sort every --resort steps.
+  push_deposit_fast_resort  the same with lbx_pic_sort every --resort steps;
+  push_deposit_esk1/esk3  charge-conserving Esirkepov deposition with shape
+                        order 1 / 3 (the paper's order) and
+                        same-order gather, in place (+ _resort: cell sort
+                        every --resort steps; full_step_esk3_resort adds the
+                        Yee update).
 Roofline: HBM, algorithmic bytes = 80 B per particle (read z,x,uz,ux,uy +
 write them, float64) -- field patch and current flush traffic is counted
 separately from ncu (profiles/).  Prints one JSON object.
@@ -104,7 +109,11 @@ def main():
                                    ("push_deposit_resort", False, False, True),
                                    ("push_deposit_tiled", False, False, True),
                                    ("push_deposit_fast", False, False, True),
-                                   ("push_deposit_fast_resort", False, False, True)):
+                                   ("push_deposit_fast_resort", False, False, True),
+                                   ("push_deposit_esk1", False, False, True),
+                                   ("push_deposit_esk3", False, False, True),
+                                   ("push_deposit_esk3_resort", False, False, True),
+                                   ("full_step_esk3_resort", True, False, True)):
         if mode not in args.modes.split(","):
             continue
         st = pic.PicState.create(pos0[:1], u0[:1], nz, nx, device=dev)
@@ -112,7 +121,8 @@ def main():
             setattr(st, name, t.clone())
         st.n = n
         resort = mode in ("push_deposit_resort", "push_deposit_tiled",
-                          "push_deposit_fast_resort")
+                          "push_deposit_fast_resort") or mode.endswith("esk3_resort")
+        order = 3 if "esk3" in mode else (1 if "esk1" in mode else 0)
         tiled = mode == "push_deposit_tiled"
         fast = mode.startswith("push_deposit_fast")
         if resort:   # start cell-ordered, like the other modes' first sorted step
@@ -120,7 +130,7 @@ def main():
         for w in range(args.warmup):
             try:
                 pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=clk, field_solve=solve,
-                             sort=sort, tiled=tiled, fast=fast)
+                             sort=sort, tiled=tiled, fast=fast, shape_order=order)
             except ValueError as e:
                 raise ValueError(f"mode {mode} warm-up step {w}: {e}") from None
         times = []
@@ -132,7 +142,7 @@ def main():
                 pic.pic_sort(ctx, st, tiled=tiled)
             try:
                 pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=clk, field_solve=solve,
-                             sort=sort, tiled=tiled, fast=fast)
+                             sort=sort, tiled=tiled, fast=fast, shape_order=order)
             except ValueError as e:
                 raise ValueError(f"mode {mode} step {len(times)}: {e}") from None
             e1.record(stream)

@@ -428,6 +428,14 @@ typedef struct lbx_pic_args {
    * every computed value is.  NULL: in place (order kept with
    * LBX_PIC_STABLE_ORDER, else absorbed slots filled from the tail). */
   double* out[5];
+  /* 0: the CIC step above (direct deposit at the new position).  1, 2, 3:
+   * charge-conserving Esirkepov deposition with B-spline particle shapes of
+   * that order (CIC / TSC / PQS; the paper runs order 3) and
+   * the same-order gather at each component's stagger: in place, float32
+   * weights (tolerance mode, oracle/pic_oracle.py esirkepov_current), node
+   * current accumulated as int64 fixed point; not combinable with sorted /
+   * tiled / deferred-current modes. */
+  int32_t shape_order;
 } lbx_pic_args;
 
 int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* args, void* stream);

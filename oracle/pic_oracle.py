@@ -180,3 +180,156 @@ def field_step(f, nz, nx, dt):
         f[k][s] = a[s].astype(np.float32)
     for k in ("Jx", "Jy", "Jz"):
         f[k][:] = 0.0
+
+
+# ----------------------------------------------------------------------------
+# Charge-conserving (Esirkepov) deposition with shape order 1-3 (PAPER.md:235:
+# the paper's runs use third-order particle shapes; deposition is ~50 % of
+# the walltime).  Esirkepov, Comput. Phys. Commun. 135 (2001)
+# 144, restated for the 2D (z, x) Yee grid with y invariant:
+#   S0, S1   shape weights of the old / new position on a common window of
+#            order+2 nodes per axis, DS = S1 - S0;
+#   Wz = DSz (S0x + DSx/2),  Wx = DSx (S0z + DSz/2),
+#   Wy = S0z S0x + (DSz S0x + S0z DSx)/2 + DSz DSx/3;
+#   Jz(i+1/2, j) = -(q w / dt) sum_{i' <= i} Wz(i', j)   (Ez / Jz stagger),
+#   Jx(i, j+1/2) = -(q w / dt) sum_{j' <= j} Wx(i, j')   (Ex / Jx stagger),
+#   Jy(i, j)     = q w vy Wy.
+# Then (rho1 - rho0)/dt + div J = 0 exactly (rho = q w S S on the nodes):
+# Wz + Wx = S1z S1x - S0z S0x.  Fields are gathered with the same shape at
+# each component's stagger.  fp64 throughout (the GPU kernel computes in
+# float32 and is compared at a stated tolerance).
+# ----------------------------------------------------------------------------
+
+SHAPE_ORDERS = (1, 2, 3)
+
+
+def shape_fn(order, d):
+    """B-spline particle shape of the given order at node distance d."""
+    a = np.abs(d)
+    if order == 1:
+        return np.where(a < 1.0, 1.0 - a, 0.0)
+    if order == 2:
+        return np.where(a <= 0.5, 0.75 - a * a,
+                        np.where(a < 1.5, 0.5 * (1.5 - a) ** 2, 0.0))
+    if order == 3:
+        return np.where(a <= 1.0, 2.0 / 3.0 - a * a + 0.5 * a ** 3,
+                        np.where(a < 2.0, (2.0 - a) ** 3 / 6.0, 0.0))
+    raise ValueError(f"shape order must be 1, 2 or 3, got {order}")
+
+
+def shape_base(pos, order):
+    """Lowest node whose weight can be nonzero: floor(pos - (order+1)/2) + 1."""
+    return np.floor(pos - 0.5 * (order + 1)).astype(np.int64) + 1
+
+
+def window_weights(pos, base, order, width):
+    """Weights S(base + k - pos), k = 0..width-1, shape (n, width)."""
+    k = np.arange(width)
+    return shape_fn(order, (base[:, None] + k[None, :]) - pos[:, None])
+
+
+def gather_shaped(f, comp, z, x, order):
+    """Shape-`order` gather of one component at its stagger (zero outside the
+    stored nodes, i.e. beyond the one guard layer)."""
+    oz, ox = OFFSETS[comp]
+    zp, xp = z - oz, x - ox
+    bz, bx = shape_base(zp, order), shape_base(xp, order)
+    w = order + 1
+    sz, sx = window_weights(zp, bz, order, w), window_weights(xp, bx, order, w)
+    a = f[comp].astype(np.float64)
+    nzg, nxg = a.shape
+    out = np.zeros(z.shape[0])
+    for di in range(w):
+        ii = bz + di + 1
+        okz = (ii >= 0) & (ii < nzg)
+        for dj in range(w):
+            jj = bx + dj + 1
+            ok = okz & (jj >= 0) & (jj < nxg)
+            v = np.zeros(z.shape[0])
+            v[ok] = a[ii[ok], jj[ok]]
+            out += sz[:, di] * sx[:, dj] * v
+    return out
+
+
+def esirkepov_current(z0, x0, z1, x1, vy, qw, dt, order, shape, pad):
+    """fp64 Esirkepov current of particles moving (z0, x0) -> (z1, x1):
+    dict Jz, Jx, Jy on padded node arrays of `shape` = (nz + 2 pad, nx + 2
+    pad), index [i + pad, j + pad] <-> node (i, j) (Jz at i + 1/2, Jx at
+    j + 1/2).  Contributions outside the padded arrays are dropped."""
+    w = order + 2
+    bz = shape_base(np.minimum(z0, z1), order)
+    bx = shape_base(np.minimum(x0, x1), order)
+    s0z, s1z = window_weights(z0, bz, order, w), window_weights(z1, bz, order, w)
+    s0x, s1x = window_weights(x0, bx, order, w), window_weights(x1, bx, order, w)
+    dsz, dsx = s1z - s0z, s1x - s0x
+    wz = dsz[:, :, None] * (s0x + 0.5 * dsx)[:, None, :]
+    wx = (s0z + 0.5 * dsz)[:, :, None] * dsx[:, None, :]
+    wy = (s0z[:, :, None] * s0x[:, None, :] + 0.5 * dsz[:, :, None] * s0x[:, None, :]
+          + 0.5 * s0z[:, :, None] * dsx[:, None, :] + dsz[:, :, None] * dsx[:, None, :] / 3.0)
+    c = -(qw / dt)
+    jz = c * np.cumsum(wz, axis=1)
+    jx = c * np.cumsum(wx, axis=2)
+    jy = (qw * vy)[:, None, None] * wy
+    out = {k: np.zeros(shape) for k in ("Jz", "Jx", "Jy")}
+    for di in range(w):
+        ii = bz + di + pad
+        for dj in range(w):
+            jj = bx + dj + pad
+            ok = (ii >= 0) & (ii < shape[0]) & (jj >= 0) & (jj < shape[1])
+            for k, a in (("Jz", jz), ("Jx", jx), ("Jy", jy)):
+                np.add.at(out[k], (ii[ok], jj[ok]), a[ok, di, dj])
+    return out
+
+
+def deposit_rho(z, x, qw, order, shape, pad):
+    """Node charge density q w S(i - z) S(j - x) on the padded node arrays."""
+    w = order + 1
+    bz, bx = shape_base(z, order), shape_base(x, order)
+    sz, sx = window_weights(z, bz, order, w), window_weights(x, bx, order, w)
+    rho = np.zeros(shape)
+    for di in range(w):
+        ii = bz + di + pad
+        for dj in range(w):
+            jj = bx + dj + pad
+            ok = (ii >= 0) & (ii < shape[0]) & (jj >= 0) & (jj < shape[1])
+            np.add.at(rho, (ii[ok], jj[ok]), qw * sz[ok, di] * sx[ok, dj])
+    return rho
+
+
+def push_particles_shaped(f, p, nz, nx, qm, dt, order):
+    """Gather (shape `order`), Boris, move, absorb; returns (keep mask, old
+    z, old x of the survivors, 1/gamma of the survivors)."""
+    z, x = p["z"], p["x"]
+    E = {k: gather_shaped(f, k, z, x, order) for k in E_COMPS}
+    B = {k: gather_shaped(f, k, z, x, order) for k in B_COMPS}
+    uz, ux, uy = boris(p["uz"], p["ux"], p["uy"], E, B, qm, dt)
+    ig = 1.0 / np.sqrt(1.0 + ux * ux + uy * uy + uz * uz)
+    zn, xn = z + dt * uz * ig, x + dt * ux * ig
+    keep = (zn >= 0) & (zn < nz) & (xn >= 0) & (xn < nx)
+    z0, x0 = z[keep], x[keep]
+    for k, v in (("z", zn), ("x", xn), ("uz", uz), ("ux", ux), ("uy", uy)):
+        p[k] = v[keep]
+    return keep, z0, x0, ig[keep]
+
+
+def particle_step_esirkepov(f, p, nz, nx, qm, qw, dt, order):
+    """Shape-`order` gather, Boris, move, absorb, Esirkepov deposit of the
+    survivors into f's J arrays (one guard layer: contributions further out
+    are dropped).  Returns the keep mask."""
+    keep, z0, x0, ig = push_particles_shaped(f, p, nz, nx, qm, dt, order)
+    j = esirkepov_current(z0, x0, p["z"], p["x"], p["uy"] * ig, qw, dt, order,
+                          f["Jx"].shape, 1)
+    for k in ("Jx", "Jy", "Jz"):
+        f[k] += j[k].astype(np.float32)
+    return keep
+
+
+def field_energy(f):
+    """0.5 sum(E^2 + B^2) over the stored nodes (cell volume 1)."""
+    return 0.5 * sum(float(np.sum(f[k].astype(np.float64) ** 2)) for k in OFFSETS)
+
+
+def kinetic_energy(p, mass_w):
+    """sum w m (gamma - 1) (c = 1) for macro weight x mass `mass_w`."""
+    g = np.sqrt(1.0 + p["uz"] ** 2 + p["ux"] ** 2 + p["uy"] ** 2)
+    return float(mass_w * np.sum(g - 1.0))

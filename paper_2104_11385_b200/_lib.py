@@ -138,7 +138,7 @@ class PicArgs(C.Structure):
                 ("box_size", i32), ("q_over_m", f64), ("q_times_w", f64), ("dt", f64),
                 ("w_particle", f64), ("w_cell", f64), ("flags", u32),
                 ("counts_out", vp), ("cost_out", vp), ("clk_out", vp), ("n_out", vp),
-                ("err_out", vp), ("out", vp * 5)]
+                ("err_out", vp), ("out", vp * 5), ("shape_order", i32)]
 
 
 SIGNATURES["lbx_pic_step"] = (i32, [vp, P(PicArgs), vp])

@@ -78,6 +78,8 @@ struct lbx_ctx {
   int pic_tiles_nz = 0, pic_tiles_nx = 0; //   grid they describe (0: none)
   unsigned long long* pic_jn = nullptr;   // tiled mode: node-centric current [3][(nz+2)(nx+2)] + box
   int64_t pic_jn_stride = 0;
+  unsigned long long* pic_esk = nullptr;  // Esirkepov: padded node current [3][(nz+2G)(nx+2G)]
+  int64_t pic_esk_elems = 0;
   long long* fill_scratch = nullptr;      // hole-fill: holes[cap] + tail flags[cap]
   int64_t fill_cap = 0;
   bool timing = false;                    // lbx_ctx_enable_timing

@@ -1689,6 +1689,7 @@ int lbx_ctx_destroy(lbx_ctx* ctx) {
   if (ctx->pic_fill) cudaFree(ctx->pic_fill);
   if (ctx->pic_tiles) cudaFree(ctx->pic_tiles);
   if (ctx->pic_jn) cudaFree(ctx->pic_jn);
+  if (ctx->pic_esk) cudaFree(ctx->pic_esk);
   if (ctx->fill_scratch) cudaFree(ctx->fill_scratch);
   if (ctx->ev0) cudaEventDestroy((cudaEvent_t)ctx->ev0), cudaEventDestroy((cudaEvent_t)ctx->ev1);
   delete ctx;

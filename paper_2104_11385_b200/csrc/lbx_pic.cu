@@ -1547,6 +1547,294 @@ int cuda_fail(cudaError_t e, const char* what) {
 }
 
 // Jc -> J over the deposit box, clear Jc, Yee update (unless disabled).
+// ---------------------------------------------------------------------------
+// Charge-conserving PIC step (lbx_pic_args::shape_order K = 1..3): the
+// paper's deposition (PAPER.md:235 -- third-order shapes; ~50 % of the
+// walltime).  Per particle: K-order B-spline gather of every
+// component at its stagger, Boris (float32 increment, boris_fast), move,
+// absorb, then Esirkepov's decomposition on a common (K+2)^2 node window of
+// the old and new positions (oracle/pic_oracle.py esirkepov_current):
+// Jz / Jx as prefix sums of Wz / Wx along their axis, Jy from Wy; node
+// values rounded to fixed point and added as integers into a padded
+// node-centric int64 accumulator (kEskG guard nodes: every window of a
+// kept particle fits).  A warp whose 32 consecutive particles share one
+// window (dense, cell-sorted plasma) sums each node over the warp with
+// redux.sync and issues one RED per node; otherwise every lane adds its own.
+// pic_esk_current_kernel converts the sums (dropping nodes beyond the field
+// arrays' one guard layer) and clears them; the Yee update follows.
+constexpr int kEskG = 4;
+constexpr int kEB = 256;
+#ifndef LBX_ESK_RUN
+#define LBX_ESK_RUN 16
+#endif
+constexpr int kEskRun = LBX_ESK_RUN;     // 32-particle iterations per warp chunk
+
+// branchless: both pieces evaluated, selected (no divergence in the
+// unrolled window loops)
+template <int K>
+__device__ __forceinline__ float bspline(float d) {
+  const float a = fabsf(d);
+  if (K == 1) return fmaxf(__fsub_rn(1.f, a), 0.f);
+  if (K == 2) {
+    const float b = fmaxf(__fsub_rn(1.5f, a), 0.f);
+    return a <= 0.5f ? __fsub_rn(0.75f, a * a) : 0.5f * b * b;
+  }
+  const float b = fmaxf(__fsub_rn(2.f, a), 0.f);
+  const float inner = __fmaf_rn(a * a, __fmaf_rn(0.5f, a, -1.f), 2.f / 3.f);
+  return a <= 1.f ? inner : b * b * b * (1.f / 6.f);
+}
+
+// lowest node with a possibly nonzero weight: floor(v - (K+1)/2) + 1
+template <int K>
+__device__ __forceinline__ int shape_base(double v) {
+  return __double2int_rd(v - 0.5 * (K + 1)) + 1;
+}
+
+template <int K>
+__device__ __forceinline__ float gather_shaped(const float* __restrict__ F, int pitch, int nzg,
+                                               int nxg, double zp, double xp) {
+  const int bz = shape_base<K>(zp), bx = shape_base<K>(xp);
+  const float tz = __double2float_rn(zp - (double)bz), tx = __double2float_rn(xp - (double)bx);
+  float wx[K + 1];
+  int cx[K + 1];
+#pragma unroll
+  for (int l = 0; l <= K; ++l) {
+    const int c = bx + l + 1;
+    const bool ok = c >= 0 && c < nxg;
+    wx[l] = ok ? bspline<K>((float)l - tx) : 0.f;
+    cx[l] = ok ? c : 0;
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int k = 0; k <= K; ++k) {
+    const int r = bz + k + 1;
+    if (r < 0 || r >= nzg) continue;
+    const float wz = bspline<K>((float)k - tz);
+    const float* row = F + (long long)r * pitch;
+    float rs = 0.f;
+#pragma unroll
+    for (int l = 0; l <= K; ++l) rs = __fmaf_rn(wx[l], __ldg(row + cx[l]), rs);
+    acc = __fmaf_rn(wz, rs, acc);
+  }
+  return acc;
+}
+
+struct EskParams {
+  PicParams b;                  // particles, fields F[], grid, boxes, status, outputs
+  unsigned long long* J;        // [3][stride] padded node sums (Jx, Jy, Jz)
+  long long stride;
+  int apitch;                   // nx + 2 kEskG
+  float cz;                     // -(q w / dt) * scale  (Jz, Jx)
+  float cy;                     // q w * scale          (Jy, times vy)
+};
+
+template <int K, bool kClock>
+__global__ void __launch_bounds__(kEB, 2) pic_esk_kernel(EskParams e) {
+  constexpr int W = K + 2;                 // window nodes per axis
+  constexpr int NJ = (K + 1) * W;          // Jz (or Jx) nonzero prefix values
+  const PicParams& p = e.b;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  unsigned* s_cnt = reinterpret_cast<unsigned*>(s_dyn);
+  unsigned* s_clk = s_cnt + p.nb;
+  __shared__ PushShared sh;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  push_prologue<kClock>(p, sh, s_cnt, s_clk);
+  const long long n = sh.n;
+  const double ez = (double)p.nz, ex = (double)p.nx;
+  const float hf = (float)(0.5 * p.qm * p.dt), dtf = (float)p.dt;
+  const int nzg = p.nz + 2, nxg = p.nx + 2;
+  unsigned long long removed = 0;
+  long long first_out = LLONG_MAX, err = 0;
+  // A warp takes chunks of kEskRun x 32 consecutive particles.  While its
+  // 32-particle window stays the same (dense, cell-sorted plasma) the warp
+  // sums each node value over the warp (redux.sync) into registers -- lane l
+  // keeps values l, l+32, l+64 -- and adds them to HBM only when the window
+  // changes or the chunk ends: one RED per node per run instead of one per
+  // node per particle (hot nodes of a dense cell would serialise in L2).
+  constexpr int NS = (2 * NJ + W * W + 31) / 32;
+  int hold[NS];
+#pragma unroll
+  for (int q = 0; q < NS; ++q) hold[q] = 0;
+  int hbz = INT_MIN, hbx = 0;
+  auto flush = [&]() {
+    if (hbz == INT_MIN) return;
+    const long long h0 = (long long)(hbz + kEskG) * e.apitch + (hbx + kEskG);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      const int t = lane + 32 * q;
+      if (t < 2 * NJ + W * W && hold[q]) {
+        int comp, di, dj;
+        if (t < NJ) {
+          comp = 2;
+          di = t % (K + 1);
+          dj = t / (K + 1);
+        } else if (t < 2 * NJ) {
+          comp = 0;
+          di = (t - NJ) / (K + 1);
+          dj = (t - NJ) % (K + 1);
+        } else {
+          comp = 1;
+          di = (t - 2 * NJ) / W;
+          dj = (t - 2 * NJ) % W;
+        }
+        red_add(e.J + comp * e.stride + h0 + (long long)di * e.apitch + dj, hold[q]);
+      }
+      hold[q] = 0;
+    }
+    hbz = INT_MIN;
+  };
+  const long long chunk = (long long)kEskRun * 32;
+  for (long long c0 = ((long long)blockIdx.x * (kEB / 32) + warp) * chunk; c0 < n;
+       c0 += (long long)gridDim.x * (kEB / 32) * chunk)
+  for (long long w0 = c0; w0 < min(n, c0 + chunk); w0 += 32) {
+    const long long i = w0 + lane;
+    const bool valid = i < n;
+    long long t0 = 0;
+    if (kClock) t0 = clock64();
+    const long long ic = valid ? i : n - 1;
+    const double z0 = __ldcs(p.z + ic), x0 = __ldcs(p.x + ic);
+    double uz = __ldcs(p.uz + ic), ux = __ldcs(p.ux + ic), uy = __ldcs(p.uy + ic);
+    // staggers: (0, 1/2) Ex Bz | (0, 0) Ey | (1/2, 0) Ez Bx | (1/2, 1/2) By
+    const double zh = z0 - 0.5, xh = x0 - 0.5;
+    const float Ex = gather_shaped<K>(p.F[0], p.pitch, nzg, nxg, z0, xh);
+    const float Ey = gather_shaped<K>(p.F[1], p.pitch, nzg, nxg, z0, x0);
+    const float Ez = gather_shaped<K>(p.F[2], p.pitch, nzg, nxg, zh, x0);
+    const float Bx = gather_shaped<K>(p.F[3], p.pitch, nzg, nxg, zh, x0);
+    const float By = gather_shaped<K>(p.F[4], p.pitch, nzg, nxg, zh, xh);
+    const float Bz = gather_shaped<K>(p.F[5], p.pitch, nzg, nxg, z0, xh);
+    const float ig = boris_fast(ux, uy, uz, hf, Ex, Ey, Ez, Bx, By, Bz);
+    const float dtg = dtf * ig;
+    const double z1 = __dadd_rn(z0, (double)__fmul_rn(dtg, (float)uz));
+    const double x1 = __dadd_rn(x0, (double)__fmul_rn(dtg, (float)ux));
+    const bool keep = valid && z1 >= 0.0 && z1 < ez && x1 >= 0.0 && x1 < ex;
+    if (valid) {
+      __stcs(p.oz + i, z1);
+      __stcs(p.ox + i, x1);
+      __stcs(p.ouz + i, uz);
+      __stcs(p.oux + i, ux);
+      __stcs(p.ouy + i, uy);
+      if (!keep) {
+        ++removed;
+        first_out = min(first_out, i);
+        if (p.removed_list) {
+          const unsigned long long slot = atomicAdd(&p.st->removed_count, 1ull);
+          if ((long long)slot < p.removed_cap) p.removed_list[slot] = i;
+        }
+      }
+    }
+    // ---- Esirkepov weights on the common window ----
+    const int bz = shape_base<K>(fmin(z0, z1)), bx = shape_base<K>(fmin(x0, x1));
+    const float t0z = __double2float_rn(z0 - (double)bz), t1z = __double2float_rn(z1 - (double)bz);
+    const float t0x = __double2float_rn(x0 - (double)bx), t1x = __double2float_rn(x1 - (double)bx);
+    float s0z[W], dsz[W], s0x[W], dsx[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      s0z[k] = bspline<K>((float)k - t0z);
+      dsz[k] = __fsub_rn(bspline<K>((float)k - t1z), s0z[k]);
+      s0x[k] = bspline<K>((float)k - t0x);
+      dsx[k] = __fsub_rn(bspline<K>((float)k - t1x), s0x[k]);
+    }
+    const float cz = keep ? e.cz : 0.f;
+    const float cy = keep ? e.cy * __fmul_rn((float)uy, ig) : 0.f;
+    // ---- add: warp-uniform window -> each node summed over the warp
+    // (redux.sync) and added by one lane; otherwise per lane ----
+    const unsigned km = __ballot_sync(kAll, keep);
+    const int lead = km ? __ffs(km) - 1 : 0;
+    const int lbz = __shfl_sync(kAll, bz, lead), lbx = __shfl_sync(kAll, bx, lead);
+    const bool uni = __all_sync(kAll, !keep || (bz == lbz && bx == lbx));
+    const long long r0 = (long long)(bz + kEskG) * e.apitch + (bx + kEskG);
+    if (km && uni && (lbz != hbz || lbx != hbx)) {   // window change: add the held sums
+      flush();
+      hbz = lbz;
+      hbx = lbx;
+    }
+    auto emit = [&](int t, int comp, int di, int dj, int val) {
+      if (uni) {
+        const int r = __reduce_add_sync(kAll, val);
+        if (lane == (t & 31)) hold[t >> 5] += r;
+      } else if (val) {
+        red_add(e.J + comp * e.stride + r0 + (long long)di * e.apitch + dj, val);
+      }
+    };
+    if (km) {
+      // Jz at (bz + i + 1/2, bx + j): prefix over i of dsz_i (s0x_j + dsx_j / 2)
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        const float hx = __fmaf_rn(0.5f, dsx[j], s0x[j]);
+        float a = 0.f;
+#pragma unroll
+        for (int ii = 0; ii <= K; ++ii) {
+          a = __fmaf_rn(dsz[ii], hx, a);
+          emit(j * (K + 1) + ii, 2, ii, j, __float2int_rn(cz * a));
+        }
+      }
+      // Jx at (bz + i, bx + j + 1/2): prefix over j of dsx_j (s0z_i + dsz_i / 2)
+#pragma unroll
+      for (int ii = 0; ii < W; ++ii) {
+        const float hz = __fmaf_rn(0.5f, dsz[ii], s0z[ii]);
+        float a = 0.f;
+#pragma unroll
+        for (int j = 0; j <= K; ++j) {
+          a = __fmaf_rn(dsx[j], hz, a);
+          emit(NJ + ii * (K + 1) + j, 0, ii, j, __float2int_rn(cz * a));
+        }
+      }
+      // Jy at (bz + i, bx + j)
+#pragma unroll
+      for (int ii = 0; ii < W; ++ii) {
+        const float a0 = __fmaf_rn(0.5f, dsz[ii], s0z[ii]);               // s0z + dsz/2
+        const float a1 = __fmaf_rn(1.f / 3.f, dsz[ii], 0.5f * s0z[ii]);   // s0z/2 + dsz/3
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+          emit(2 * NJ + ii * W + j, 1, ii, j, __float2int_rn(cy * __fmaf_rn(a1, dsx[j], a0 * s0x[j])));
+      }
+    }
+    // ---- per-box survivor counts (+ GpuClock: the particle's whole work) ----
+    int box = -1;
+    if (keep) {
+      const int bzz = __double2int_rz(z1) >> p.log2m, bxx = __double2int_rz(x1) >> p.log2m;
+      if (bzz >= p.nbz || bxx >= p.nbx) ++err;
+      else box = bzz * p.nbx + bxx;
+    }
+    unsigned dt = 0;
+    if (kClock) dt = (unsigned)min((clock64() - t0) >> 4, (long long)(1 << 26));
+    const int b0 = __shfl_sync(kAll, box, lead);
+    if (__all_sync(kAll, box < 0 || box == b0)) {
+      const unsigned cnt = __popc(__ballot_sync(kAll, box >= 0));
+      const unsigned ck = kClock ? __reduce_add_sync(kAll, box >= 0 ? dt : 0u) : 0u;
+      if (lane == 0 && cnt) {
+        atomicAdd(s_cnt + b0, cnt);
+        if (kClock) atomicAdd(s_clk + b0, ck);
+      }
+    } else if (box >= 0) {
+      atomicAdd(s_cnt + box, 1u);
+      if (kClock) atomicAdd(s_clk + box, dt);
+    }
+  }
+  flush();
+  push_epilogue<kClock>(p, sh, n, removed, first_out, err, INT_MAX, INT_MIN, INT_MAX, INT_MIN,
+                        s_cnt, s_clk);
+}
+
+__global__ void pic_esk_current_kernel(unsigned long long* __restrict__ J, long long stride,
+                                       int apitch, float* __restrict__ jx, float* __restrict__ jy,
+                                       float* __restrict__ jz, int nz, int nx, double inv_scale) {
+  const int pitch = nx + 2;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < stride;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / apitch), c = (int)(idx - (long long)r * apitch);
+    const int i = r - kEskG, j = c - kEskG;                 // node (i, j)
+    const bool stored = i >= -1 && i <= nz && j >= -1 && j <= nx;
+    float* out[3] = {jx, jy, jz};
+#pragma unroll
+    for (int comp = 0; comp < 3; ++comp) {
+      const long long v = (long long)J[comp * stride + idx];
+      if (v) J[comp * stride + idx] = 0ull;
+      if (stored) out[comp][(i + 1) * pitch + (j + 1)] = (float)((double)v * inv_scale);
+    }
+  }
+}
+
 int pic_finish(lbx_ctx* ctx, const lbx_pic_args* a, cudaStream_t s, double jscale,
                bool tiled = false) {
   const long long cells = (long long)a->nz * a->nx;
@@ -1578,6 +1866,152 @@ int pic_finish(lbx_ctx* ctx, const lbx_pic_args* a, cudaStream_t s, double jscal
 }
 
 
+// Host side of the charge-conserving step (lbx_pic_args::shape_order > 0).
+int pic_step_esirkepov(lbx_ctx* ctx, const lbx_pic_args* a, cudaStream_t s) {
+  const int K = a->shape_order;
+  if (a->out[0]) return set_error(LBX_EINVAL, "shape_order > 0 runs in place (no out[])");
+  if (a->flags & (LBX_PIC_TILED | LBX_PIC_DEFER_CURRENT))
+    return set_error(LBX_EINVAL, "shape_order > 0 does not support tiled or deferred-current steps");
+  uintptr_t al = (uintptr_t)a->z | (uintptr_t)a->x | (uintptr_t)a->uz | (uintptr_t)a->ux |
+                 (uintptr_t)a->uy;
+  if (al & 7u) return set_error(LBX_EINVAL, "particle arrays must be 8-byte aligned");
+  const int nbz = a->nz / a->box_size, nbx = a->nx / a->box_size, nb = nbz * nbx;
+  if (nb > 4096) return set_error(LBX_EINVAL, "PIC step supports <= 4096 boxes");
+  int rc = ensure_accumulators(ctx, nb);
+  if (rc) return rc;
+  rc = reserve_status(ctx, ctx->n_upper);
+  if (rc) return rc;
+  ctx->pic_sort_next = nullptr;
+  ctx->pic_tiles_nz = ctx->pic_tiles_nx = 0;
+  const int apitch = a->nx + 2 * kEskG;
+  const long long stride = (long long)(a->nz + 2 * kEskG) * apitch;
+  if (!ctx->pic_esk || ctx->pic_esk_elems != stride) {
+    if (ctx->pic_esk) {
+      cudaDeviceSynchronize();
+      cudaFree(ctx->pic_esk);
+    }
+    ctx->pic_esk = nullptr;
+    const size_t bytes = (size_t)stride * 3 * 8 + 16;
+    if (cudaMalloc(&ctx->pic_esk, bytes) != cudaSuccess)
+      return set_error(LBX_EOOM, "PIC Esirkepov current accumulators");
+    cudaMemsetAsync(ctx->pic_esk, 0, bytes, s);
+    ctx->pic_esk_elems = stride;
+  }
+  const long long rcap = std::max(1ll << 20, (long long)(ctx->n_upper / 64));
+  const bool fill = !(a->flags & LBX_PIC_STABLE_ORDER);
+  if (fill && (!ctx->pic_fill || ctx->pic_fill_cap < rcap)) {
+    if (ctx->pic_fill) {
+      cudaDeviceSynchronize();
+      cudaFree(ctx->pic_fill);
+    }
+    ctx->pic_fill = nullptr;
+    if (cudaMalloc(&ctx->pic_fill, (size_t)rcap * 3 * 8) != cudaSuccess)
+      return set_error(LBX_EOOM, "PIC hole-filling lists");
+    cudaMemsetAsync(ctx->pic_fill, 0, (size_t)rcap * 3 * 8, s);
+    ctx->pic_fill_cap = rcap;
+  }
+  // fixed-point scale: a particle's largest node value, max(|q w| / dt, |q w|),
+  // maps to <= 2^20 (warp sums of 32 fit int32)
+  const double vmax = std::fabs(a->q_times_w) / std::min(a->dt, 1.0);
+  int e2 = 0;
+  std::frexp(1048576.0 / vmax, &e2);
+  const double jscale = std::ldexp(1.0, e2 - 1);
+  EskParams e{};
+  PicParams& p = e.b;
+  p.z = a->z;
+  p.x = a->x;
+  p.uz = a->uz;
+  p.ux = a->ux;
+  p.uy = a->uy;
+  p.oz = a->z;
+  p.ox = a->x;
+  p.ouz = a->uz;
+  p.oux = a->ux;
+  p.ouy = a->uy;
+  for (int c = 0; c < 6; ++c) p.F[c] = a->fields[c];
+  p.pitch = a->nx + 2;
+  p.dep_box = reinterpret_cast<int*>(ctx->pic_esk + 3 * stride);
+  p.removed_list = fill ? ctx->pic_fill : nullptr;
+  p.removed_cap = fill ? ctx->pic_fill_cap : 0;
+  p.nz = a->nz;
+  p.nx = a->nx;
+  p.qm = a->q_over_m;
+  p.qw = a->q_times_w;
+  p.dt = a->dt;
+  int l2 = 0;
+  while ((1 << l2) < a->box_size) ++l2;
+  p.log2m = l2;
+  p.nbz = nbz;
+  p.nbx = nbx;
+  p.nb = nb;
+  p.st = ctx->st;
+  p.g_cnt = ctx->acc;
+  p.g_clk = ctx->acc + ctx->acc_boxes;
+  p.counts_out = reinterpret_cast<long long*>(a->counts_out);
+  p.cost_out = a->cost_out;
+  p.clk_out = reinterpret_cast<unsigned long long*>(a->clk_out);
+  p.n_out = reinterpret_cast<long long*>(a->n_out);
+  p.err_out = reinterpret_cast<long long*>(a->err_out);
+  p.wp = a->w_particle;
+  p.wc = a->w_cell;
+  p.cells = (double)a->box_size * (double)a->box_size;
+  e.J = ctx->pic_esk;
+  e.stride = stride;
+  e.apitch = apitch;
+  e.cz = (float)(-(a->q_times_w / a->dt) * jscale);
+  e.cy = (float)(a->q_times_w * jscale);
+  const bool clock = (a->flags & LBX_STEP_CLOCK) != 0;
+  void (*kern)(EskParams) = nullptr;
+  switch (K) {
+    case 1: kern = clock ? pic_esk_kernel<1, true> : pic_esk_kernel<1, false>; break;
+    case 2: kern = clock ? pic_esk_kernel<2, true> : pic_esk_kernel<2, false>; break;
+    case 3: kern = clock ? pic_esk_kernel<3, true> : pic_esk_kernel<3, false>; break;
+    default: return set_error(LBX_EINVAL, "shape_order must be 0 (CIC direct) or 1, 2, 3");
+  }
+  const size_t smem = (size_t)nb * 8;
+  if (smem > 48 * 1024) {
+    cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ea != cudaSuccess) return cuda_fail(ea, "cudaFuncSetAttribute(esk)");
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEB, smem);
+  long long grid = (long long)std::max(per_sm, 1) * ctx->num_sms;
+  if (ctx->grid_override > 0) grid = ctx->grid_override;
+  grid = std::max(1ll, std::min(grid, (long long)((ctx->n_upper + kEB - 1) / kEB)));
+  kern<<<(unsigned)grid, kEB, smem, s>>>(e);
+  cudaError_t er = cudaGetLastError();
+  if (er != cudaSuccess) return cuda_fail(er, "pic_esk_kernel launch");
+  if (fill) {
+    const long long fc = ctx->pic_fill_cap;
+    const unsigned fg2 = (unsigned)std::max(1, ctx->num_sms * 2);
+    pic_fill_mark_kernel<<<fg2, 256, 0, s>>>(ctx->st, ctx->pic_fill, fc, ctx->pic_fill + fc,
+                                             ctx->pic_fill + 2 * fc);
+    pic_fill_move_kernel<<<fg2, 256, 0, s>>>(ctx->st, fc, ctx->pic_fill + fc, ctx->pic_fill + 2 * fc,
+                                             a->z, a->x, a->uz, a->ux, a->uy);
+    pic_fill_done_kernel<<<1, 1, 0, s>>>(ctx->st, fc);
+  }
+  rc = launch_compact(ctx, a->z, a->x, a->uz, a->ux, a->uy, nullptr, (double)a->nz, (double)a->nx, s);
+  if (rc) return rc;
+  const unsigned cg = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 8, (stride + 255) / 256));
+  pic_esk_current_kernel<<<cg, 256, 0, s>>>(ctx->pic_esk, stride, apitch, a->current[0],
+                                            a->current[1], a->current[2], a->nz, a->nx,
+                                            1.0 / jscale);
+  er = cudaGetLastError();
+  if (er != cudaSuccess) return cuda_fail(er, "current launch");
+  if (a->flags & LBX_PIC_NO_FIELD_SOLVE) return LBX_OK;
+  const int pitch = a->nx + 2;
+  const long long cells = (long long)a->nz * a->nx;
+  const unsigned fg = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 8, (cells + 255) / 256));
+  pic_b_kernel<<<fg, 256, 0, s>>>(a->fields[0], a->fields[1], a->fields[2], a->fields[3],
+                                  a->fields[4], a->fields[5], a->nz, a->nx, pitch, a->dt);
+  pic_e_kernel<<<fg, 256, 0, s>>>(a->fields[0], a->fields[1], a->fields[2], a->fields[3],
+                                  a->fields[4], a->fields[5], a->current[0], a->current[1],
+                                  a->current[2], a->nz, a->nx, pitch, a->dt);
+  er = cudaGetLastError();
+  if (er != cudaSuccess) return cuda_fail(er, "field solve launch");
+  return LBX_OK;
+}
+
 }  // namespace
 }  // namespace lbx
 
@@ -1598,6 +2032,8 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
     if (!a->fields[c]) return set_error(LBX_EINVAL, "NULL field array");
   for (int c = 0; c < 3; ++c)
     if (!a->current[c]) return set_error(LBX_EINVAL, "NULL current array");
+  if (!(a->q_times_w != 0.0)) return set_error(LBX_EINVAL, "q_times_w must be nonzero");
+  if (a->shape_order) return pic_step_esirkepov(ctx, a, (cudaStream_t)stream);
   const bool sorted = a->out[0] != nullptr;
   uintptr_t al = (uintptr_t)a->z | (uintptr_t)a->x | (uintptr_t)a->uz | (uintptr_t)a->ux |
                  (uintptr_t)a->uy;

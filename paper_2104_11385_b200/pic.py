@@ -89,7 +89,7 @@ def pic_sort(ctx: Context, st: PicState, tiled: bool = False):
 
 def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times_w: float,
              dt: float, weights=(0.75, 0.25), clock=False, field_solve=True, sort=False,
-             gather=None, stable=False, tiled=False, fast=False):
+             gather=None, stable=False, tiled=False, fast=False, shape_order=0):
     """One PIC step; returns per-box counts / cost / clock and n.
 
     sort=False: in place; absorbed particles' slots are filled from the tail
@@ -103,7 +103,11 @@ def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times
     fast=True (in place, untiled): tolerance mode (LBX_PIC_FAST) -- float32
     Boris increment with FMA and MUFU rsqrt/rcp, FMA gathers; agrees with
     the fp64 oracle within the tolerances tests/test_gpu_pic_fast.py states,
-    not bit for bit."""
+    not bit for bit.
+    shape_order=1..3 (in place): charge-conserving Esirkepov deposition
+    with B-spline shapes of that order and the same-order gather (the
+    paper's order 3); tolerance mode, checked against
+    oracle/pic_oracle.py esirkepov_current (tests/test_gpu_pic_esirkepov.py)."""
     dev = ctx.device
     nbz, nbx = st.nz // box_size, st.nx // box_size
     nb = nbz * nbx
@@ -135,6 +139,10 @@ def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times
         if sort or tiled:
             raise ValueError("fast (tolerance) steps run in place, untiled")
         a.flags |= _lib.LBX_PIC_FAST
+    if shape_order:
+        if sort or tiled:
+            raise ValueError("shape_order > 0 steps run in place, untiled")
+        a.shape_order = int(shape_order)
     a.counts_out, a.cost_out, a.clk_out = _lib.ptr(counts), _lib.ptr(cost), _lib.ptr(clk)
     a.n_out, a.err_out = _lib.ptr(nout), _lib.ptr(nout[1:])
     names = ("z", "x", "uz", "ux", "uy")
