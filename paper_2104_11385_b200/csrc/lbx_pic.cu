@@ -1738,10 +1738,19 @@ __global__ void __launch_bounds__(kEB, 2) pic_esk_kernel(EskParams e) {
     const float cy = keep ? e.cy * __fmul_rn((float)uy, ig) : 0.f;
     // ---- add: warp-uniform window -> each node summed over the warp
     // (redux.sync) and added by one lane; otherwise per lane ----
+    // the warp's most common window (match_any groups, largest wins): its
+    // lanes' values are summed over the warp into the held registers; the
+    // other lanes (particles that crossed a cell face downwards) add theirs
     const unsigned km = __ballot_sync(kAll, keep);
-    const int lead = km ? __ffs(km) - 1 : 0;
+    const unsigned key = keep ? ((unsigned)(bz + kEskG) << 16) | (unsigned)(bx + kEskG) : 0xffffffffu;
+    const unsigned grp = __match_any_sync(kAll, key);
+    const int gsize = keep ? __popc(grp) : 0;
+    const int gmax = __reduce_max_sync(kAll, gsize);
+    const unsigned cand = __ballot_sync(kAll, gsize == gmax && keep);
+    const int lead = cand ? __ffs(cand) - 1 : 0;
     const int lbz = __shfl_sync(kAll, bz, lead), lbx = __shfl_sync(kAll, bx, lead);
-    const bool uni = __all_sync(kAll, !keep || (bz == lbz && bx == lbx));
+    const bool ing = keep && bz == lbz && bx == lbx;
+    const bool uni = gmax > 1;                // warp-uniform decision
     const long long r0 = (long long)(bz + kEskG) * e.apitch + (bx + kEskG);
     if (km && uni && (lbz != hbz || lbx != hbx)) {   // window change: add the held sums
       flush();
@@ -1750,8 +1759,9 @@ __global__ void __launch_bounds__(kEB, 2) pic_esk_kernel(EskParams e) {
     }
     auto emit = [&](int t, int comp, int di, int dj, int val) {
       if (uni) {
-        const int r = __reduce_add_sync(kAll, val);
+        const int r = __reduce_add_sync(kAll, ing ? val : 0);
         if (lane == (t & 31)) hold[t >> 5] += r;
+        if (!ing && val) red_add(e.J + comp * e.stride + r0 + (long long)di * e.apitch + dj, val);
       } else if (val) {
         red_add(e.J + comp * e.stride + r0 + (long long)di * e.apitch + dj, val);
       }
