@@ -88,8 +88,7 @@ def make_timed_engine(lock, log, physics="surrogate"):
             def push(self, wp, wc):
                 import torch
                 self.local_step(wp, wc)
-                self.current_sum()
-                self.finish()
+                self.current_sum_finish()   # guard exchange + (timed) finish + field rings
                 with lock:
                     torch.cuda.synchronize()
                     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]

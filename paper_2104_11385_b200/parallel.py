@@ -70,6 +70,12 @@ class TorchComm:
         self.dist.all_to_all_single(recv, send, rc, sc, group=self.group)
         return recv
 
+    def exchange_values(self, send: torch.Tensor, sc: list, rc: list) -> torch.Tensor:
+        """All-to-all of a flat tensor with per-peer element counts."""
+        recv = torch.empty(sum(rc), dtype=send.dtype, device=send.device)
+        self.dist.all_to_all_single(recv, send, rc, sc, group=self.group)
+        return recv
+
     def barrier(self):
         self.dist.barrier(group=self.group)
 
@@ -141,6 +147,13 @@ class ThreadComm:
         vals = self._swap(chunks)
         out = torch.cat([v[self.rank] for v in vals]) if vals else send[:0].cpu()
         return out.reshape(-1, REC).to(send.device)
+
+    def exchange_values(self, send: torch.Tensor, sc: list, rc: list) -> torch.Tensor:
+        chunks = list(torch.split(send.detach().cpu(), sc))
+        vals = self._swap(chunks)
+        out = torch.cat([v[self.rank] for v in vals])
+        assert out.numel() == sum(rc)
+        return out.to(send.device)
 
     def barrier(self):
         # A device barrier, as NCCL's is: this rank's queued work (e.g. the
@@ -420,16 +433,116 @@ class _DevArray:
                                          "data": (int(ptr), False), "version": 3}
 
 
+# ---------------------------------------------------------------------------
+# guard-cell (halo) planning for the box-decomposed PIC
+# ---------------------------------------------------------------------------
+
+def cell_owner_map(owner, grid_shape, box_size: int) -> np.ndarray:
+    """Owner rank of every cell (nz, nx) from the per-box owner vector."""
+    nbz, nbx = grid_shape
+    o = np.asarray(owner, dtype=np.int64).reshape(nbz, nbx)
+    return np.repeat(np.repeat(o, box_size, axis=0), box_size, axis=1)
+
+
+def dilate(mask: np.ndarray, k: int) -> np.ndarray:
+    """Chebyshev dilation of a boolean cell mask by k cells (clipped to the grid)."""
+    out = mask
+    for _ in range(k):
+        g = out.copy()
+        g[1:, :] |= out[:-1, :]
+        g[:-1, :] |= out[1:, :]
+        h = g.copy()
+        h[:, 1:] |= g[:, :-1]
+        h[:, :-1] |= g[:, 1:]
+        out = h
+    return out
+
+
+def halo_plan(src_cells: np.ndarray, dst_cells: np.ndarray, rank: int, world: int,
+              src_grow: int, dst_grow: int):
+    """Cells this rank exchanges with every peer: send[q] = S(rank) & D(q),
+    recv[q] = S(q) & D(rank), with S(x) = own_src(x) grown by src_grow cells
+    and D(x) = own_dst(x) grown by dst_grow (flat row-major cell indices,
+    ascending, so both ends of a pair list the same cells in the same
+    order).  send[rank] = recv[rank] = empty."""
+    S = [dilate(src_cells == r, src_grow) for r in range(world)]
+    D = [dilate(dst_cells == r, dst_grow) for r in range(world)]
+    send, recv = [], []
+    for q in range(world):
+        if q == rank:
+            send.append(np.zeros(0, dtype=np.int64))
+            recv.append(np.zeros(0, dtype=np.int64))
+            continue
+        send.append(np.flatnonzero(S[rank] & D[q]).astype(np.int64))
+        recv.append(np.flatnonzero(S[q] & D[rank]).astype(np.int64))
+    return send, recv
+
+
+def bbox(mask: np.ndarray):
+    """(r0, r1, c0, c1) of the True cells, or an empty box."""
+    rows, cols = np.flatnonzero(mask.any(axis=1)), np.flatnonzero(mask.any(axis=0))
+    if rows.size == 0:
+        return (2 ** 31 - 1, -2 ** 31, 2 ** 31 - 1, -2 ** 31)
+    return (int(rows[0]), int(rows[-1]), int(cols[0]), int(cols[-1]))
+
+
+class PicHalo:
+    """One rank's exchange plan for an owner map (device index tensors):
+    current: the cell-centric int64 rows Jc[cell][16] of cells within one
+    cell of both ranks' boxes (a particle deposits at its new cell, at most
+    one cell outside its box; a node needs the rows of the cells around
+    it) -- summed into the receiver's rows;  fields: the owner's E, B
+    values of its cells within two cells of the receiver's boxes (the Yee
+    update of the owned cells reads one cell around them, the gather one) --
+    copied over the receiver's stale values.  Bytes per step scale with the
+    off-rank faces, not with the grid."""
+
+    def __init__(self, owner, grid_shape, box_size, nz, nx, rank, world, dev):
+        self.owner = np.asarray(owner, dtype=np.int64).copy()
+        cells = cell_owner_map(owner, grid_shape, box_size)
+        js, jr = halo_plan(cells, cells, rank, world, 1, 1)
+        fs, fr = halo_plan(cells, cells, rank, world, 0, 2)
+        self.j_send_n = [int(a.size) for a in js]
+        self.j_recv_n = [int(a.size) for a in jr]
+        self.f_send_n = [int(a.size) for a in fs]
+        self.f_recv_n = [int(a.size) for a in fr]
+        t = lambda a: torch.from_numpy(np.concatenate(a)).to(dev)  # noqa: E731
+        self.j_send, self.j_recv = t(js), t(jr)
+        pad = lambda c: (c // nx + 1) * (nx + 2) + (c % nx + 1)  # noqa: E731 (cell -> padded node)
+        self.f_send = t([pad(a) for a in fs])
+        self.f_recv = t([pad(a) for a in fr])
+        self.box = torch.tensor(bbox(dilate(cells == rank, 1)), dtype=torch.int32, device=dev)
+        self.bytes_j = 16 * 8 * sum(self.j_send_n)
+        self.bytes_f = 6 * 4 * sum(self.f_send_n)
+
+
+def field_sync_plan(old_owner, new_owner, grid_shape, box_size, nx, rank, world, dev):
+    """Adoption: every rank's new guard region (own_new grown by 2) from the
+    cells' previous owners (who hold their current values)."""
+    old = cell_owner_map(old_owner, grid_shape, box_size)
+    new = cell_owner_map(new_owner, grid_shape, box_size)
+    fs, fr = halo_plan(old, new, rank, world, 0, 2)
+    pad = lambda c: (c // nx + 1) * (nx + 2) + (c % nx + 1)  # noqa: E731
+    t = lambda a: torch.from_numpy(np.concatenate(a)).to(dev)  # noqa: E731
+    return (t([pad(a) for a in fs]), [int(a.size) for a in fs], t([pad(a) for a in fr]),
+            [int(a.size) for a in fr])
+
+
 class PicEngine(DeviceEngine):
     """This rank's share of a box-decomposed PIC run (pic.py physics).
 
-    Particles: the rank's boxes (z, x, uz, ux, uy in HBM).  Fields: every rank
-    keeps the full Yee grid and runs the same field solve, so only the
-    current needs a cross-GPU sum -- the guard-cell exchange of a
-    box-decomposed PIC code.  The step's current stays on the device as
-    exact integers (LBX_PIC_DEFER_CURRENT); ranks all-reduce the rows of the
-    union of their deposit boxes and finish (node gather, Yee update): bit-
-    identical to one GPU, the order of the sums does not matter.  Emigrants
+    Particles: the rank's boxes (z, x, uz, ux, uy in HBM).  Fields: each rank
+    keeps grid-sized arrays but only its own cells (and a two-cell guard
+    ring) are current: after the particle step (current deferred, exact
+    integers, LBX_PIC_DEFER_CURRENT) the ranks exchange the current rows of
+    the cells along their shared faces (PicHalo: one all-to-all, sizes known
+    from the owner map on every rank), finish (node gather over the rank's
+    region, Yee update), then exchange the owners' E, B values of the
+    two-cell guard rings.  Bytes per step scale with the off-rank faces
+    (the reference's face model, workload.py:324-327, decomposition.py:71-81).
+    Integer sums are order independent, so every rank's own cells are
+    bit-identical to one GPU.  On adoption the new owners first receive the
+    fields of their new guard regions from the previous owners.  Emigrants
     and adoption-time migration reuse the 6-double records: (z, x, uz, ux,
     kick_z, kick_x) before the kick (uy is 0 then), (z, x, uz, ux, uy, 0)
     after it."""
@@ -455,10 +568,36 @@ class PicEngine(DeviceEngine):
         self.time_step = False      # bench_lb: CUDA events around the particle kernels
         self.last_ms = 0.0
         self.nout2 = torch.zeros(2, dtype=torch.int64, device=self.dev)
-        self.ubox = torch.zeros(4, dtype=torch.int64, device=self.dev)
+        self.halo = None
+        self.halo_bytes = 0          # bytes sent by this rank's last step's exchanges
 
     def attach_comm(self, comm):
         self.comm = comm
+
+    def set_owner(self, owner: np.ndarray):
+        owner = np.asarray(owner, dtype=np.int64)
+        if self.halo is not None and not np.array_equal(owner, self.halo.owner):
+            self.field_sync(self.halo.owner, owner)
+        super().set_owner(owner)
+        if self.halo is None or not np.array_equal(owner, self.halo.owner):
+            self.halo = PicHalo(owner, (self.nbz, self.nbx), int(self.m), self.nz, self.nx,
+                                self.rank, self.world, self.dev)
+
+    def _field_exchange(self, send_idx, sc, recv_idx, rc):
+        names = self.field_names
+        send = torch.stack([self.fields[k].view(-1).index_select(0, send_idx) for k in names],
+                           1)
+        recv = self.comm.exchange_values(send.reshape(-1), [6 * k for k in sc],
+                                         [6 * k for k in rc]).view(-1, 6)
+        for c, k in enumerate(names):
+            self.fields[k].view(-1).index_copy_(0, recv_idx, recv[:, c].contiguous())
+        return 6 * 4 * sum(sc)
+
+    def field_sync(self, old_owner, new_owner):
+        """Adoption: the new guard regions' fields from the previous owners."""
+        plan = field_sync_plan(old_owner, new_owner, (self.nbz, self.nbx), int(self.m),
+                               self.nx, self.rank, self.world, self.dev)
+        self._field_exchange(*plan)
 
     def kick(self):
         if not self.kicked:     # momenta u = v_kick / dt, as Simulation(physics="pic")
@@ -511,10 +650,12 @@ class PicEngine(DeviceEngine):
         self.n = int(h[0])
 
     def current_sum_finish(self):
-        """Guard-cell current: exact integer sum over the union of the ranks'
-        deposit boxes, then node gather + Yee update."""
+        """Guard-cell exchange of the current, node gather + Yee update over
+        the rank's region, then the guard rings' fields from their owners."""
         self.current_sum()
         self.finish()
+        h = self.halo
+        self.halo_bytes += self._field_exchange(h.f_send, h.f_send_n, h.f_recv, h.f_recv_n)
 
     def finish(self):
         _lib.check(_lib.lib.lbx_pic_finish(self.ctx.handle, C.byref(self._args(0)),
@@ -522,20 +663,22 @@ class PicEngine(DeviceEngine):
         self.launches += 4   # current, zero, B, E
 
     def current_sum(self):
+        """Integer current rows of the shared-face cells, summed into each
+        receiver's rows; the node gather then covers the rank's cells grown
+        by one (every nonzero row lies there)."""
         jc_p, cells, box_p = C.c_void_p(), C.c_int64(), C.c_void_p()
         _lib.check(_lib.lib.lbx_pic_current_view(self.ctx.handle, C.byref(jc_p), C.byref(cells),
                                                  C.byref(box_p)))
+        h = self.halo
+        jc = torch.as_tensor(_DevArray(jc_p.value, cells.value * 16, "<i8"),
+                             device=self.dev).view(-1, 16)
+        send = jc.index_select(0, h.j_send)
+        recv = self.comm.exchange_values(send.reshape(-1), [16 * k for k in h.j_send_n],
+                                         [16 * k for k in h.j_recv_n])
+        jc.index_add_(0, h.j_recv, recv.view(-1, 16))
         box = torch.as_tensor(_DevArray(box_p.value, 4, "<i4"), device=self.dev)
-        b = box.to(torch.int64)
-        self.ubox.copy_(torch.stack([-b[0], b[1], -b[2], b[3]]))
-        self.comm.all_reduce_max(self.ubox)
-        u = self.ubox.cpu().numpy()
-        r0, r1, c0, c1 = -int(u[0]), int(u[1]), -int(u[2]), int(u[3])
-        if r0 <= r1:
-            box.copy_(torch.tensor([r0, r1, c0, c1], dtype=torch.int32, device=self.dev))
-            jc = torch.as_tensor(_DevArray(jc_p.value, cells.value * 16, "<i8"), device=self.dev)
-            band = jc[r0 * self.nx * 16:(r1 + 1) * self.nx * 16]
-            self.comm.all_reduce_sum(band)
+        box.copy_(h.box)
+        self.halo_bytes = 16 * 8 * sum(h.j_send_n)
 
     def unpack(self, recv: torch.Tensor):
         n0 = self.n

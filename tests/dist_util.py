@@ -136,9 +136,12 @@ def run_rank(rank, world, port, spec_kw, outdir, engine="numpy"):
 
 class NumpyPicEngine:
     """Test double for parallel.PicEngine: the same per-rank PIC protocol in
-    numpy (oracle/pic_oracle.py) -- push the local particles, all-reduce the
-    integer current of every rank, apply it and run the replicated field
-    solve, then stage emigrants as 6-double records."""
+    numpy (oracle/pic_oracle.py) -- push the local particles, exchange the
+    integer node current of the cells along shared faces (parallel.halo_plan:
+    node sums of the cells within two cells of the sender's boxes that the
+    receiver owns), apply it and run the field solve, exchange the owners'
+    E, B values of the two-cell guard rings, then stage emigrants as
+    6-double records.  Each rank's fields are current on its own cells."""
 
     def __init__(self, cfg, rank, world, device, pos, kick, capacity, clock, pic=None):
         from oracle import pic_oracle as PO
@@ -168,7 +171,39 @@ class NumpyPicEngine:
         self.comm = comm
 
     def set_owner(self, owner):
-        self.owner = np.asarray(owner, dtype=np.int64)
+        from paper_2104_11385_b200.parallel import cell_owner_map, halo_plan
+        owner = np.asarray(owner, dtype=np.int64)
+        grid = (self.nbz, self.nbx)
+        new = cell_owner_map(owner, grid, int(self.m))
+        if self.owner is not None and not np.array_equal(owner, self.owner):
+            old = cell_owner_map(self.owner, grid, int(self.m))
+            self._fields_exchange(*halo_plan(old, new, self.rank, self.world, 0, 2))
+        self.owner = owner
+        self.j_plan = halo_plan(new, new, self.rank, self.world, 2, 0)
+        self.f_plan = halo_plan(new, new, self.rank, self.world, 0, 2)
+
+    def _exchange(self, arrays, plan):
+        """Interior (cell) values of `arrays` at plan's send cells -> peers;
+        returns (received (m, k) values, the cells they belong to)."""
+        send_idx, recv_idx = plan
+        send = np.concatenate([np.column_stack([a.reshape(-1)[self._pad(ix)] for a in arrays])
+                               for ix in send_idx]) if sum(map(len, send_idx)) else \
+            np.zeros((0, len(arrays)), dtype=arrays[0].dtype)
+        k = len(arrays)
+        t = torch.from_numpy(np.ascontiguousarray(send).reshape(-1))
+        r = self.comm.exchange_values(t, [k * len(ix) for ix in send_idx],
+                                      [k * len(ix) for ix in recv_idx])
+        return r.numpy().reshape(-1, k), self._pad(np.concatenate(recv_idx))
+
+    def _pad(self, cells):
+        """flat cell index -> flat index of its node in the padded arrays"""
+        return (cells // self.nx + 1) * (self.nx + 2) + (cells % self.nx + 1)
+
+    def _fields_exchange(self, send_idx, recv_idx):
+        names = self.PO.E_COMPS + self.PO.B_COMPS
+        vals, cells = self._exchange([self.f[k] for k in names], (send_idx, recv_idx))
+        for c, k in enumerate(names):
+            self.f[k].reshape(-1)[cells] = vals[:, c]
 
     def kick(self):
         if self.kick_v is not None:
@@ -206,11 +241,14 @@ class NumpyPicEngine:
         counts = np.bincount(box, minlength=self.nbz * self.nbx).astype(np.int64)
         shape = self.f["Jx"].shape
         sc = PO.current_scale(c["q_times_w"])
-        for comp, acc in PO.current_accs(self.p, ig, c["q_times_w"], shape).items():
-            t = torch.from_numpy(np.ascontiguousarray(acc).reshape(-1))
-            self.comm.all_reduce_sum(t)
-            PO.apply_current(self.f, comp, t.numpy().reshape(shape), sc)
+        accs = PO.current_accs(self.p, ig, c["q_times_w"], shape)
+        comps = ("Jx", "Jy", "Jz")
+        vals, cells = self._exchange([accs[k] for k in comps], self.j_plan)
+        for i, k in enumerate(comps):
+            np.add.at(accs[k].reshape(-1), cells, vals[:, i])
+            PO.apply_current(self.f, k, accs[k], sc)
         PO.field_step(self.f, self.nz, self.nx, c["dt"])
+        self._fields_exchange(*self.f_plan)
         self._split()
         send = np.bincount(self.dest, minlength=self.world).astype(np.int64)
         return (torch.from_numpy(counts), torch.zeros(counts.size, dtype=torch.int64),
@@ -292,7 +330,18 @@ def run_rank_pic(rank, world, port, doc, steps, outdir, overrides=None):
         f = sim.engine.field_arrays()
         np.savez(os.path.join(outdir, f"rank{rank}.npz"), count_trace=res.count_trace,
                  adoptions=res.summary["adoption_count"], moved=sim.moved,
+                 owner=np.asarray(sim.engine.owner),
                  **{f"p_{k}": v for k, v in st.items()}, **{f"f_{k}": v for k, v in f.items()})
         sim.close()
     finally:
         dist.destroy_process_group()
+
+
+def own_cells_mask(owner, cfg_doc_or_shape, rank):
+    """Boolean (nz + 2, nx + 2) mask of the padded field nodes of `rank`'s cells."""
+    from paper_2104_11385_b200.parallel import cell_owner_map
+    grid, box, nz, nx = cfg_doc_or_shape
+    cells = cell_owner_map(owner, grid, box) == rank
+    m = np.zeros((nz + 2, nx + 2), dtype=bool)
+    m[1:-1, 1:-1] = cells
+    return m

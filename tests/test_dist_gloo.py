@@ -87,11 +87,13 @@ def test_distributed_matches_single_process_oracle(tmp_path, base, world, kw):
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_distributed_pic_matches_single_process_oracle(tmp_path, world):
-    """Box-decomposed PIC over gloo: per-rank particles, integer current
-    all-reduce (guard-cell sum), replicated field solve, emigrant exchange
-    and adoption-time migration reproduce the single-process oracle PIC run
-    bit for bit: per-step counts, particle multiset, fields on every rank."""
-    from tests.dist_util import pic_reference, run_rank_pic
+    """Box-decomposed PIC over gloo: per-rank particles, guard-cell exchange
+    of the integer current along shared faces, field solve, guard-ring field
+    exchange, emigrant exchange and adoption-time migration (with the new
+    owners' field sync) reproduce the single-process oracle PIC run bit for
+    bit: per-step counts, particle multiset, and every rank's fields on the
+    cells it owns (which together cover the grid)."""
+    from tests.dist_util import own_cells_mask, pic_reference, run_rank_pic
     doc = json.loads((G / "runs.json").read_text())["_docs"]["small"]
     steps = 16
     # frequent attempts, any non-worsening remap adopted: exercises migration
@@ -100,11 +102,36 @@ def test_distributed_pic_matches_single_process_oracle(tmp_path, world):
     counts, p, f = pic_reference(doc, steps)
     outs = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
     keys = ("z", "x", "uz", "ux", "uy")
-    for o in outs:
+    nz, nx = doc["domain"]["extent"]
+    box = doc["domain"]["box_size"]
+    cover = np.zeros((nz + 2, nx + 2), dtype=bool)
+    for r, o in enumerate(outs):
         assert np.array_equal(o["count_trace"], counts)
-        for k in f:
-            assert np.array_equal(o[f"f_{k}"], f[k]), k
+        mine = own_cells_mask(o["owner"], ((nz // box, nx // box), box, nz, nx), r)
+        cover |= mine
+        for k in ("Ex", "Ey", "Ez", "Bx", "By", "Bz"):
+            assert np.array_equal(o[f"f_{k}"][mine], f[k][mine]), (r, k)
+    assert cover[1:-1, 1:-1].all()
     got = sorted_rows(np.column_stack([np.concatenate([o[f"p_{k}"] for o in outs]) for k in keys]))
     want = sorted_rows(np.column_stack([p[k] for k in keys]))
     assert np.array_equal(got, want)
     assert int(outs[0]["adoptions"]) > 0 and sum(int(o["moved"].sum()) for o in outs) > 0
+
+
+def test_halo_plan_scales_with_off_rank_faces():
+    """PIC guard exchange sizes: for slabs of boxes, the current rows and
+    the field values crossing a rank boundary are two cell rows of the
+    boundary's length (one on each side / two on the owner's side), and
+    ranks that share no face exchange nothing."""
+    from paper_2104_11385_b200.parallel import cell_owner_map, halo_plan
+    nbz, nbx, M, R = 8, 6, 16, 4
+    owner = np.repeat(np.arange(R), nbz * nbx // R)     # slabs of 2 box rows
+    cells = cell_owner_map(owner, (nbz, nbx), M)
+    nx = nbx * M
+    for r in range(R):
+        js, jr = halo_plan(cells, cells, r, R, 1, 1)
+        fs, fr = halo_plan(cells, cells, r, R, 0, 2)
+        for q in range(R):
+            adj = abs(q - r) == 1
+            assert js[q].size == jr[q].size == (2 * nx if adj else 0), (r, q)
+            assert fs[q].size == fr[q].size == (2 * nx if adj else 0), (r, q)
