@@ -332,6 +332,10 @@ int lbx_lb_destroy(lbx_lb* lb);
 int lbx_lb_step(lbx_lb* lb, int64_t step, const int64_t* counts, const uint64_t* clk,
                 int64_t n_alive, lbx_sim_outputs* out, int32_t* adopted, int32_t* halt);
 int lbx_lb_owner(lbx_lb* lb, int64_t* owner);
+/* Replace the migration-aware gate's price (lbx_sim_config::migration_ratio,
+ * particle-pushes per moved particle) -- the distributed loop feeds it the
+ * MEASURED redistribution cost after every adoption. */
+int lbx_lb_set_migration_ratio(lbx_lb* lb, double ratio);
 
 int lbx_sim_create(lbx_sim** out, lbx_ctx* ctx, const lbx_sim_config* cfg);
 int lbx_sim_destroy(lbx_sim* sim);

@@ -142,6 +142,7 @@ class PicArgs(C.Structure):
 
 
 SIGNATURES["lbx_pic_step"] = (i32, [vp, P(PicArgs), vp])
+SIGNATURES["lbx_lb_set_migration_ratio"] = (i32, [vp, f64])
 SIGNATURES["lbx_pic_sort"] = (i32, [vp, P(PicArgs), vp])
 SIGNATURES["lbx_peer_alloc"] = (i32, [i64, P(vp), vp])
 SIGNATURES["lbx_ctx_set_upper"] = (i32, [vp, i64])

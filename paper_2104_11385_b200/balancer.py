@@ -45,6 +45,11 @@ class BalancePolicy:
     # one interval to exceed the migration cost (migration_ratio particle-
     # pushes per moved particle).  0 = the reference's gate.
     migration_ratio: float = 0.0
+    # B200 extension: the distributed loop MEASURES every adoption's
+    # redistribution (wall time of partition -> exchange -> unpack, max over
+    # ranks) and the step's push time, and sets migration_ratio to their
+    # per-particle ratio (pushes per moved particle) for later adoptions.
+    measured_migration: bool = False
 
     def __post_init__(self):
         if self.migration_ratio < 0:

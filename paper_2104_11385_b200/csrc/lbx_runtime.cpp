@@ -596,6 +596,14 @@ int lbx_lb_step(lbx_lb* lb, int64_t step, const int64_t* counts, const uint64_t*
   return rc;
 }
 
+int lbx_lb_set_migration_ratio(lbx_lb* lb, double ratio) {
+  clear_error();
+  if (!lb) return set_error(LBX_EINVAL, "NULL argument");
+  if (!(ratio >= 0.0)) return set_error(LBX_EINVAL, "migration ratio must be >= 0");
+  lb->cfg.migration_ratio = ratio;
+  return LBX_OK;
+}
+
 int lbx_lb_owner(lbx_lb* lb, int64_t* owner) {
   clear_error();
   if (!lb || !owner) return set_error(LBX_EINVAL, "NULL argument");

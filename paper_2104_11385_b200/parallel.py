@@ -792,6 +792,11 @@ class DistributedSimulation:
         self.done = 0
         self.halted = False
         self.moved = np.zeros(T, dtype=np.int64)   # particles migrated on adoption
+        # measured redistribution cost (policy.measured_migration)
+        self.measure_mig = bool(getattr(policy, "measured_migration", False))
+        self.mig_log = []            # per adoption: step, moved, migration ms, push ms, ratio
+        self.mig_ratio = float(getattr(policy, "migration_ratio", 0.0))
+        self._push_ev = None
 
     def _choose_exchange(self, exchange):
         """p2p (fused exchange over peer memory) when the engine supports it
@@ -870,6 +875,48 @@ class DistributedSimulation:
         except Exception:
             pass
 
+    def _push_events(self):
+        """CUDA events bracketing this step's push (measured migration)."""
+        if not self.measure_mig or not torch.cuda.is_available():
+            return None
+        return [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+
+    def _timed_migration(self, step, fn):
+        """Run a migration; with policy.measured_migration, time it (device
+        synchronised wall time, max over ranks) against the last push and
+        return the new per-particle price (pushes per moved particle) for
+        the adoption gate, else None."""
+        import time
+        if not self.measure_mig:
+            return fn(), None
+        dev = self.engine.dev
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        moved = fn()
+        torch.cuda.synchronize(dev)
+        mig_ms = 1e3 * (time.perf_counter() - t0)
+        ev = self._push_ev
+        push_ms = ev[0].elapsed_time(ev[1]) if ev is not None else 0.0
+        v = torch.tensor([mig_ms, push_ms, float(self.engine.n), float(moved)],
+                         dtype=torch.float64, device=dev)
+        tot = v.clone()
+        self.comm.all_reduce_max(v)
+        self.comm.all_reduce_sum(tot)
+        mig_ms, push_ms, n_max = float(v[0]), float(v[1]), float(v[2])
+        moved_all = int(tot[3])
+        ratio = None
+        if moved_all > 0 and push_ms > 0 and n_max > 0:
+            r = (mig_ms / moved_all) / (push_ms / n_max)
+            ratio = r if not self.mig_log else 0.5 * (self.mig_ratio + r)
+        self.mig_log.append({"step": int(step), "moved": moved_all, "migration_ms": mig_ms,
+                             "push_ms": push_ms, "ratio": ratio})
+        return moved, ratio
+
+    def _set_mig_ratio(self, ratio):
+        if ratio is not None:
+            self.mig_ratio = float(ratio)
+            _lib.check(_lib.lib.lbx_lb_set_migration_ratio(self.lb, self.mig_ratio))
+
     def _records(self, sc, rc):
         """All-to-all of the staged records given host split sizes."""
         send = self.engine.pack(sc)
@@ -936,7 +983,13 @@ class DistributedSimulation:
             p2p = self.exchange == "p2p"
             if p2p:
                 self.engine.parity = step & 1
+            ev = self._push_events()
+            if ev:
+                ev[0].record()
             counts, clk, send_counts, nout = self.engine.push(wp, wc)
+            if ev:
+                ev[1].record()
+                self._push_ev = ev
             parts = [counts, clk] if clock else [counts]
             red = torch.cat(parts + [send_counts.sum().reshape(1)])
             self.comm.all_reduce_sum(red)   # p2p: also orders every sender's kernel first
@@ -964,7 +1017,9 @@ class DistributedSimulation:
                 owner = np.empty(nb, dtype=np.int64)
                 _lib.check(_lib.lib.lbx_lb_owner(self.lb, _lib.ptr(owner)))
                 self.engine.set_owner(owner)
-                self.moved[step] = self._migrate_p2p(step) if p2p else self._migrate()
+                self.moved[step], ratio = self._timed_migration(
+                    step, (lambda: self._migrate_p2p(step)) if p2p else self._migrate)
+                self._set_mig_ratio(ratio)      # prices the next adoptions (same on every rank)
             self.done = step + 1
             if halt.value:
                 self.halted = True
@@ -1006,6 +1061,12 @@ class DistributedSimulation:
                 item = work.get()
                 if item is None:
                     return
+                if item[0] == "ratio":             # measured migration price, in step order
+                    try:
+                        self._set_mig_ratio(item[1])
+                    except Exception as e:  # noqa: BLE001
+                        st["err"] = e
+                    continue
                 step, host, ev = item
                 try:
                     ev.synchronize()
@@ -1042,7 +1103,10 @@ class DistributedSimulation:
             """Adoption decided at step d, applied before step `boundary`."""
             eng.end_async()                        # host count for the sync migration
             eng.set_owner(decided.pop(d))
-            self.moved[d] = self._migrate_p2p(boundary - 1)
+            self.moved[d], ratio = self._timed_migration(
+                d, lambda: self._migrate_p2p(boundary - 1))
+            if ratio is not None:                  # applied before step `boundary`'s LB
+                work.put(("ratio", ratio))
             eng.begin_async()
 
         th = threading.Thread(target=worker, name=f"lbx-lb-rank{self.rank}", daemon=True)
@@ -1060,7 +1124,13 @@ class DistributedSimulation:
                 if step == cfg.kick.step:
                     eng.kick()
                 eng.parity = step & 1
+                pev = self._push_events()
+                if pev:
+                    pev[0].record()
                 counts, clk, send_counts, nout = eng.push_async(wp, wc)
+                if pev:
+                    pev[1].record()
+                    self._push_ev = pev
                 parts = [counts, clk] if clock else [counts]
                 red = torch.cat(parts + [send_counts.sum().reshape(1)])
                 self.comm.all_reduce_sum(red)

@@ -176,3 +176,52 @@ def test_p2p_failure_on_one_rank_falls_back_to_collectives(monkeypatch):
     for res, _, _ in outs:
         assert np.array_equal(res.cost_trace, ref["cost_trace"])
         assert np.array_equal(res.count_trace, ref["count_trace"])
+
+
+def test_measured_migration_prices_the_gate():
+    """policy.measured_migration: every adoption's redistribution is timed
+    (max over ranks) against the push, the per-particle price is fed to the
+    native gate (lbx_lb_set_migration_ratio) identically on every rank, and
+    later adoptions must save more load than the measured move costs -- so
+    there are at most as many adoptions as with the reference gate."""
+    from dataclasses import replace
+
+    from paper_2104_11385_b200 import scenarios as S
+    from paper_2104_11385_b200.parallel import DistributedSimulation, ThreadComm
+    world = 2
+    res = {}
+    for measured in (False, True):
+        spec = S.apply_overrides(S.load_spec("mini"), ranks=world, steps=60, interval=3,
+                                 threshold=0.0)
+        policy = replace(spec.policy, measured_migration=measured)
+        shared = ThreadComm.shared(world)
+        outs, errs = [None] * world, []
+
+        def body(r):
+            try:
+                torch.cuda.set_device(0)
+                sim = DistributedSimulation(spec.scenario, policy, spec.build_provider(),
+                                            comm=ThreadComm(shared, r), device="cuda:0")
+                sim.run()
+                outs[r] = (sim.result(), list(sim.mig_log), sim.mig_ratio)
+                sim.close()
+            except Exception as e:
+                errs.append(e)
+                shared["bar"].abort()
+
+        th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        if errs:
+            raise errs[0]
+        a, b = outs
+        assert [m.adopted for m in a[0].metrics] == [m.adopted for m in b[0].metrics]
+        assert a[1] == b[1] and a[2] == b[2]      # same measurements, same price
+        res[measured] = outs[0]
+    base, meas = res[False], res[True]
+    assert meas[1], "no adoption was measured"
+    assert all(x["migration_ms"] > 0 and x["push_ms"] > 0 for x in meas[1])
+    assert meas[2] > 0
+    assert meas[0].summary["adoption_count"] <= base[0].summary["adoption_count"]
