@@ -55,6 +55,7 @@ void destroy_pipe(HostPipe* hp);
 struct lbx_ctx {
   int device = 0;
   int num_sms = 0;
+  int64_t l2_bytes = 0;               // cudaDevAttrL2CacheSize
   lbx::DevState* st = nullptr;        // device
   unsigned long long* status = nullptr;  // look-back tile status words
   int64_t status_tiles = 0;

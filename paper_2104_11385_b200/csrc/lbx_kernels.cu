@@ -106,6 +106,8 @@ struct StepParams {
   double* const* peer_recv;             // non-NULL: write emigrants into peers' buffers
   unsigned long long* const* peer_cursor;
   long long peer_cap;
+  int l2_keep;   // set by the launcher when the particle state fits in L2 (cache-global
+                 // loads / stores instead of evict-first streaming)
 };
 
 struct ScanParams {
@@ -320,11 +322,13 @@ __global__ void __launch_bounds__(kBlock, LBX_STREAM_MINB) stream_kernel(StepPar
       double2 a = make_double2(-1.0, -1.0), b = a, c = make_double2(0.0, 0.0), d = c;
       const bool any = q < npairs;
       if (any) {
-        a = __ldcs(z2 + q);
-        b = __ldcs(x2 + q);
+        // L2-resident steps (small sets, p.l2_keep) keep the particle state in
+        // L2 across steps; large ones stream it (evict-first)
+        a = p.l2_keep ? __ldcg(z2 + q) : __ldcs(z2 + q);
+        b = p.l2_keep ? __ldcg(x2 + q) : __ldcs(x2 + q);
         if (kPush || kExch) {
-          c = __ldcs(vz2 + q);
-          d = __ldcs(vx2 + q);
+          c = p.l2_keep ? __ldcg(vz2 + q) : __ldcs(vz2 + q);
+          d = p.l2_keep ? __ldcg(vx2 + q) : __ldcs(vx2 + q);
         }
       }
       pvz[2 * r] = c.x;
@@ -386,8 +390,13 @@ __global__ void __launch_bounds__(kBlock, LBX_STREAM_MINB) stream_kernel(StepPar
       const double z0 = emig[2 * r] ? -1.0 : pz[2 * r];
       const double z1 = emig[2 * r + 1] ? -1.0 : pz[2 * r + 1];
       if (kPush) {
-        __stcs(z2 + q, make_double2(z0, z1));
-        __stcs(x2 + q, make_double2(px[2 * r], px[2 * r + 1]));
+        if (p.l2_keep) {
+          __stcg(z2 + q, make_double2(z0, z1));
+          __stcg(x2 + q, make_double2(px[2 * r], px[2 * r + 1]));
+        } else {
+          __stcs(z2 + q, make_double2(z0, z1));
+          __stcs(x2 + q, make_double2(px[2 * r], px[2 * r + 1]));
+        }
       } else if (emig[2 * r] || emig[2 * r + 1]) {
         __stcs(z2 + q, make_double2(z0, z1));
       }
@@ -492,9 +501,11 @@ __global__ void __launch_bounds__(kBlock, LBX_STREAM_MINB) stream_kernel(StepPar
 
   // ---- last CTA: step epilogue ----
   __threadfence();
+#ifndef LBX_DIAG_NO_RECORD
   if (kHist)
     step_record<kClock>(p.g_cnt, p.g_clk, p.nb, p.counts_out, p.cost_out, p.clk_out, p.wp, p.wc,
                         p.cells, kClockShift);
+#endif
   if (tid == 0) {
     const unsigned long long lv = *((volatile unsigned long long*)&p.st->leavers);
     const long long n_new = n - (long long)lv;
@@ -1314,8 +1325,12 @@ int launch_stream(lbx_ctx* ctx, const StepParams& p, cudaStream_t s) {
   const long long work = (ctx->n_upper + 2ll * kBlock * kPairs - 1) / (2ll * kBlock * kPairs);
   int rc = occupancy_grid(ctx, kern, smem, std::max(1ll, work), &grid);
   if (rc) return rc;
+  StepParams pk = p;
+  // particle state (read 32 B + write 16 B per particle; 2x for the kick
+  // buffers) well inside L2: keep it resident across steps
+  pk.l2_keep = ctx->n_upper * 48ll < (long long)ctx->l2_bytes / 2 ? 1 : 0;
   if (ctx->timing) cudaEventRecord((cudaEvent_t)ctx->ev0, s);
-  kern<<<grid, kBlock, smem, s>>>(p);
+  kern<<<grid, kBlock, smem, s>>>(pk);
   if (ctx->timing) cudaEventRecord((cudaEvent_t)ctx->ev1, s);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "stream_kernel launch");
@@ -1646,6 +1661,8 @@ int lbx_ctx_create(lbx_ctx** out, int device, int64_t capacity) {
     delete c;
     return cuda_fail(e, "device query");
   }
+  int l2 = 0;
+  if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device) == cudaSuccess) c->l2_bytes = l2;
   e = cudaMalloc(&c->st, sizeof(DevState));
   if (e != cudaSuccess) {
     delete c;
