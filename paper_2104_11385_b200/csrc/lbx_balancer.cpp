@@ -23,7 +23,13 @@
 #include <numeric>
 #include <vector>
 
+#include <cstdlib>
+
 #include "lbx_internal.h"
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 namespace lbx {
 
@@ -49,6 +55,23 @@ double pairwise_sum(const double* a, int64_t n) {
 }
 
 namespace {
+
+// refine_by_swaps: partner-pair evaluations per iteration above which the
+// search is split over OpenMP threads (below, thread wake-up costs more)
+constexpr int64_t kParallelPairs = 16384;
+
+#ifdef _OPENMP
+// threads for the swap search: LBX_LB_THREADS, else up to 4 (one rank per
+// GPU shares the host's cores with the other ranks)
+int lb_threads() {
+  static const int n = [] {
+    const char* e = std::getenv("LBX_LB_THREADS");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? v : std::min(4, omp_get_max_threads());
+  }();
+  return n;
+}
+#endif
 
 int check_owner(const int64_t* owner, int64_t n, int32_t R) {
   for (int64_t i = 0; i < n; ++i)
@@ -223,17 +246,40 @@ void refine_by_swaps(int64_t* owner, double* loads, const double* v, int64_t n, 
       double pm = 0.0;
       int64_t ia = -1, j = -1;
     } best;
-    for (int64_t ia = 0; ia < nm; ++ia) {
-      const double ca = v[mine[ia]];
-      double pm;
-      const int64_t j = best_partner(cb.data(), d.data(), no, top - ca, ca, top, &pm);
-      if (j < 0) continue;
-      if (!best.have || pm < best.pm) {
-        best.have = true;
-        best.pm = pm;
-        best.ia = ia;
-        best.j = j;
+    // Partner searches of the max-rank's boxes are independent: large
+    // instances split them over OpenMP threads in contiguous chunks, and the
+    // per-chunk bests are merged in chunk order with the sequential loop's
+    // rule (strictly smaller pair max wins, so ties keep the lowest box) --
+    // the same swap as one thread.
+    const bool par = nm * no >= kParallelPairs;
+    int nt = 1;
+#ifdef _OPENMP
+    if (par) nt = std::min<int>(lb_threads(), (int)nm);
+#endif
+    std::vector<Best> part(nt);
+#ifdef _OPENMP
+#pragma omp parallel for num_threads(nt) schedule(static, 1) if (par)
+#endif
+    for (int t = 0; t < nt; ++t) {
+      const int64_t lo = nm * t / nt, hi = nm * (t + 1) / nt;
+      Best b;
+      for (int64_t ia = lo; ia < hi; ++ia) {
+        const double ca = v[mine[ia]];
+        double pm;
+        const int64_t j = best_partner(cb.data(), d.data(), no, top - ca, ca, top, &pm);
+        if (j < 0) continue;
+        if (!b.have || pm < b.pm) {
+          b.have = true;
+          b.pm = pm;
+          b.ia = ia;
+          b.j = j;
+        }
       }
+      part[t] = b;
+    }
+    for (int t = 0; t < nt; ++t) {
+      const Best& b = part[t];
+      if (b.have && (!best.have || b.pm < best.pm)) best = b;
     }
     if (!best.have) return;
     const int64_t best_a = mine[best.ia], best_b = others[best.j];
