@@ -349,13 +349,19 @@ int lbx_sim_set_particles(lbx_sim* sim, double* z, double* x, double* vz,
 int lbx_sim_set_fields(lbx_sim* sim, float* const* fields, float* const* current, double* uy);
 /* Run steps [first, last) of the loop; outputs indexed by absolute step.
  * The loop runs on its own stream, ordered after `stream`'s prior work and
- * before its later work.  Surrogate-physics runs replay each aligned
- * 16-step cycle as one CUDA graph (captured on first use; env LBX_NO_GRAPHS
- * disables), with per-step launches elsewhere -- identical results. */
+ * before its later work.  Surrogate-physics runs whose particle set fits the
+ * GPU's shared memory (~1 M particles on a B200; no capacity model, no
+ * per-step kernel timing, no Timers strategy) run as ONE resident
+ * cooperative kernel per call, the host following its per-step records
+ * (env LBX_NO_RESIDENT disables); others replay each aligned 16-step cycle
+ * as one CUDA graph (captured on first use; env LBX_NO_GRAPHS disables),
+ * with per-step launches elsewhere -- identical results. */
 int lbx_sim_run(lbx_sim* sim, int64_t first, int64_t last,
                 lbx_sim_outputs* out, void* stream);
 /* Number of 16-step cycles this sim has launched as CUDA graphs. */
 int lbx_sim_graph_cycles(lbx_sim* sim, int64_t* cycles);
+/* Number of lbx_sim_run calls this sim has run on the resident kernel. */
+int lbx_sim_resident_runs(lbx_sim* sim, int64_t* runs);
 /* Current device live count (syncs the stream). */
 int lbx_sim_particles(lbx_sim* sim, int64_t* n, void* stream);
 

@@ -94,6 +94,7 @@ SIGNATURES = {
     "lbx_sim_run": (i32, [vp, i64, i64, P(SimOutputs), vp]),
     "lbx_sim_particles": (i32, [vp, P(i64), vp]),
     "lbx_sim_graph_cycles": (i32, [vp, P(i64)]),
+    "lbx_sim_resident_runs": (i32, [vp, P(i64)]),
 }
 
 

@@ -17,6 +17,7 @@
 #if defined(__x86_64__)
 #include <immintrin.h>
 #endif
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -57,8 +58,10 @@ double pairwise_sum(const double* a, int64_t n) {
 namespace {
 
 // refine_by_swaps: partner-pair evaluations per iteration above which the
-// search is split over OpenMP threads (below, thread wake-up costs more)
-constexpr int64_t kParallelPairs = 16384;
+// search is split over OpenMP threads (below, waking the threads costs more
+// than the search: a C2 pass -- 112 x 788 pairs at 8 ranks -- is ~10 us on
+// one core, a thread wake-up tens of microseconds)
+constexpr int64_t kParallelPairs = 1 << 21;
 
 #ifdef _OPENMP
 // threads for the swap search: LBX_LB_THREADS, else up to 4 (one rank per
@@ -130,25 +133,43 @@ __attribute__((target("avx512f"))) static int64_t best_partner_avx512(
   int64_t j0 = 0;
   const __m512d vh0 = _mm512_set1_pd(here0), vca = _mm512_set1_pd(ca), vtop = _mm512_set1_pd(top);
   const __m512d vinf = _mm512_set1_pd(std::numeric_limits<double>::infinity());
-  __m512d vmin = vinf;
-  __m512i vidx = _mm512_set1_epi64(-1);
-  __m512i vj = _mm512_setr_epi64(0, 1, 2, 3, 4, 5, 6, 7);
-  const __m512i v8 = _mm512_set1_epi64(8);
-  for (; j0 + 8 <= no; j0 += 8) {
-    const __m512d here = _mm512_add_pd(vh0, _mm512_loadu_pd(cb + j0));
-    const __m512d there = _mm512_add_pd(_mm512_loadu_pd(d + j0), vca);
-    const __m512d pm = _mm512_max_pd(here, there);
-    const __mmask8 ok = _mm512_cmp_pd_mask(pm, vtop, _CMP_LT_OQ);
-    const __mmask8 better = _mm512_mask_cmp_pd_mask(ok, pm, vmin, _CMP_LT_OQ);
-    vmin = _mm512_mask_mov_pd(vmin, better, pm);
-    vidx = _mm512_mask_mov_epi64(vidx, better, vj);
-    vj = _mm512_add_epi64(vj, v8);
+  // four independent (min, index) accumulators over interleaved 8-wide
+  // groups: the masked compare / move chain is four times shorter
+  __m512d vmin[4] = {vinf, vinf, vinf, vinf};
+  __m512i vidx[4];
+  __m512i vj[4];
+  for (int u = 0; u < 4; ++u) {
+    vidx[u] = _mm512_set1_epi64(-1);
+    vj[u] = _mm512_add_epi64(_mm512_setr_epi64(0, 1, 2, 3, 4, 5, 6, 7), _mm512_set1_epi64(8 * u));
   }
-  alignas(64) double m[8];
-  alignas(64) long long ix[8];
-  _mm512_store_pd(m, vmin);
-  _mm512_store_si512(reinterpret_cast<__m512i*>(ix), vidx);
-  merge_lanes(m, ix, 8, &jbest, &pm_best);
+  const __m512i v32 = _mm512_set1_epi64(32);
+  for (; j0 + 32 <= no; j0 += 32) {
+#pragma GCC unroll 4
+    for (int u = 0; u < 4; ++u) {
+      const __m512d here = _mm512_add_pd(vh0, _mm512_loadu_pd(cb + j0 + 8 * u));
+      const __m512d there = _mm512_add_pd(_mm512_loadu_pd(d + j0 + 8 * u), vca);
+      const __m512d pm = _mm512_max_pd(here, there);
+      const __mmask8 ok = _mm512_cmp_pd_mask(pm, vtop, _CMP_LT_OQ);
+      const __mmask8 better = _mm512_mask_cmp_pd_mask(ok, pm, vmin[u], _CMP_LT_OQ);
+      vmin[u] = _mm512_mask_mov_pd(vmin[u], better, pm);
+      vidx[u] = _mm512_mask_mov_epi64(vidx[u], better, vj[u]);
+      vj[u] = _mm512_add_epi64(vj[u], v32);
+    }
+  }
+  // first minimum over the 32 lanes: smallest value, then smallest index
+  const __m512d m01 = _mm512_min_pd(vmin[0], vmin[1]), m23 = _mm512_min_pd(vmin[2], vmin[3]);
+  const double mv = _mm512_reduce_min_pd(_mm512_min_pd(m01, m23));
+  if (mv < std::numeric_limits<double>::infinity()) {
+    const __m512d vm = _mm512_set1_pd(mv);
+    const __m512i big = _mm512_set1_epi64(LLONG_MAX);
+    __m512i best = big;
+    for (int u = 0; u < 4; ++u) {
+      const __mmask8 eq = _mm512_cmp_pd_mask(vmin[u], vm, _CMP_EQ_OQ);
+      best = _mm512_min_epi64(best, _mm512_mask_mov_epi64(big, eq, vidx[u]));
+    }
+    jbest = _mm512_reduce_min_epi64(best);
+    pm_best = mv;
+  }
   partner_tail(cb, d, j0, no, here0, ca, top, &jbest, &pm_best);
   *pm_out = pm_best;
   return jbest;
@@ -198,7 +219,7 @@ static int64_t best_partner(const double* cb, const double* d, int64_t no, doubl
                             double ca, double top, double* pm_out) {
 #if defined(__x86_64__)
   static const int isa = __builtin_cpu_supports("avx512f") ? 2 : __builtin_cpu_supports("avx2") ? 1 : 0;
-  if (isa == 2 && no >= 16) return best_partner_avx512(cb, d, no, here0, ca, top, pm_out);
+  if (isa == 2 && no >= 64) return best_partner_avx512(cb, d, no, here0, ca, top, pm_out);
   if (isa == 1 && no >= 8) return best_partner_avx2(cb, d, no, here0, ca, top, pm_out);
 #endif
   int64_t jbest = -1;
@@ -241,6 +262,13 @@ void refine_by_swaps(int64_t* owner, double* loads, const double* v, int64_t n, 
     }
     if (mine.empty() || others.empty()) return;
     const int64_t nm = (int64_t)mine.size(), no = (int64_t)others.size();
+    // pad the partner arrays to whole 32-wide vector groups with entries that
+    // never qualify (pair max = inf), so the search has no scalar tail
+    for (int64_t k = no; k % 32; ++k) {
+      cb.push_back(std::numeric_limits<double>::infinity());
+      d.push_back(std::numeric_limits<double>::infinity());
+    }
+    const int64_t no_pad = (int64_t)cb.size();
     struct Best {
       bool have = false;
       double pm = 0.0;
@@ -266,7 +294,7 @@ void refine_by_swaps(int64_t* owner, double* loads, const double* v, int64_t n, 
       for (int64_t ia = lo; ia < hi; ++ia) {
         const double ca = v[mine[ia]];
         double pm;
-        const int64_t j = best_partner(cb.data(), d.data(), no, top - ca, ca, top, &pm);
+        const int64_t j = best_partner(cb.data(), d.data(), no_pad, top - ca, ca, top, &pm);
         if (j < 0) continue;
         if (!b.have || pm < b.pm) {
           b.have = true;
@@ -429,6 +457,48 @@ int efficiency(const double* cost, const int64_t* owner, int64_t n, int32_t R, d
   return LBX_OK;
 }
 
+// Box order of the greedy pass: descending cost, ties to the lower box id
+// (np.lexsort((arange(n), -values))).  LSD radix sort of an order-reversing
+// integer image of the cost (stable, so equal costs keep ascending ids);
+// -0.0 and 0.0 are one key, as the comparison sees them.  NaN-free input.
+static void lpt_order(const double* v, int64_t n, std::vector<int64_t>& order) {
+  std::vector<uint64_t> key(n), key2(n);
+  std::vector<int64_t> tmp(n);
+  order.resize(n);
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t u;
+    const double x = v[i] == 0.0 ? 0.0 : v[i];
+    std::memcpy(&u, &x, 8);
+    u = (u >> 63) ? ~u : (u | (1ull << 63));   // ascending image of x
+    key[i] = ~u;                                // descending
+    order[i] = i;
+  }
+  int64_t* src = order.data();
+  int64_t* dst = tmp.data();
+  uint64_t* ks = key.data();
+  uint64_t* kd = key2.data();
+  uint64_t all_or = 0, all_and = ~0ull;
+  for (int64_t i = 0; i < n; ++i) {
+    all_or |= ks[i];
+    all_and &= ks[i];
+  }
+  const uint64_t varies = all_or ^ all_and;   // bits that differ between keys
+  for (int shift = 0; shift < 64; shift += 8) {
+    if (((varies >> shift) & 255u) == 0) continue;   // one digit for all: order unchanged
+    int64_t cnt[257] = {0};
+    for (int64_t i = 0; i < n; ++i) ++cnt[((ks[i] >> shift) & 255) + 1];
+    for (int k = 0; k < 256; ++k) cnt[k + 1] += cnt[k];
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t at = cnt[(ks[i] >> shift) & 255]++;
+      dst[at] = src[i];
+      kd[at] = ks[i];
+    }
+    std::swap(src, dst);
+    std::swap(ks, kd);
+  }
+  if (src != order.data()) std::memcpy(order.data(), src, 8 * (size_t)n);
+}
+
 int knapsack(const double* v, int64_t n, int32_t R, double cap_factor, int64_t* owner) {
   if (R < 1) return set_error(LBX_EINVAL, "n_ranks must be >= 1, got %d", R);
   const int64_t cap = n ? (int64_t)std::ceil(cap_factor * (double)n / (double)R) : 0;
@@ -437,29 +507,38 @@ int knapsack(const double* v, int64_t n, int32_t R, double cap_factor, int64_t* 
                      "box cap %lld per rank cannot place %lld boxes on %d ranks "
                      "(cap_factor %g too tight)",
                      (long long)cap, (long long)n, R, cap_factor);
-  std::vector<int64_t> order(n);
-  std::iota(order.begin(), order.end(), 0);
-  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-    if (v[a] > v[b]) return true;
-    if (v[b] > v[a]) return false;
-    return a < b;
-  });
+  std::vector<int64_t> order;
+  lpt_order(v, n, order);
   std::vector<double> loads(R, 0.0);
   std::vector<int64_t> count(R, 0);
-  const double inf = std::numeric_limits<double>::infinity();
-  for (int64_t b : order) {
-    int32_t r = 0;
-    double best = count[0] < cap ? loads[0] : inf;
-    for (int32_t k = 1; k < R; ++k) {
-      const double m = count[k] < cap ? loads[k] : inf;
-      if (m < best) {
-        best = m;
-        r = k;
-      }
+  // least-loaded rank with room, ties to the lower rank (np.argmin over the
+  // loads masked to inf at the cap): a binary min-heap of (load, rank);
+  // a rank that reaches the cap leaves the heap
+  std::vector<int32_t> heap(R);
+  std::iota(heap.begin(), heap.end(), 0);   // all loads 0: rank order is a heap
+  int32_t hn = cap > 0 ? R : 0;
+  auto less = [&](int32_t a, int32_t b) {
+    return loads[a] < loads[b] || (!(loads[b] < loads[a]) && a < b);
+  };
+  auto sift_down = [&](int32_t i) {
+    const int32_t x = heap[i];
+    while (true) {
+      int32_t c = 2 * i + 1;
+      if (c >= hn) break;
+      if (c + 1 < hn && less(heap[c + 1], heap[c])) ++c;
+      if (!less(heap[c], x)) break;
+      heap[i] = heap[c];
+      i = c;
     }
+    heap[i] = x;
+  };
+  for (int64_t b : order) {
+    const int32_t r = heap[0];
     owner[b] = r;
     loads[r] += v[b];
     count[r] += 1;
+    if (count[r] >= cap) heap[0] = heap[--hn];   // full: drop it
+    if (hn > 0) sift_down(0);
   }
   refine_by_swaps(owner, loads.data(), v, n, R);
   return LBX_OK;

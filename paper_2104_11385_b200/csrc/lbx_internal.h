@@ -109,6 +109,38 @@ int ensure_accumulators(lbx_ctx* ctx, int32_t nboxes);
 int launch_compact(lbx_ctx* ctx, double* z, double* x, double* a, double* b, double* c,
                    double* d, double ez, double ex, void* stream);
 int reserve_status(lbx_ctx* ctx, int64_t capacity);
+// Resident multi-step kernel (lbx_resident.cu): device control block and
+// launch description.  kResSlots must match the kernel's accumulator ring.
+constexpr int kResSlots = 8;
+struct ResCtl {
+  unsigned long long recorded;              // steps recorded (last + 1)
+  unsigned long long n_acc[kResSlots];      // live particles of the slot's step
+  unsigned long long err_acc;               // out-of-grid survivors this run
+  unsigned long long n_final;
+  unsigned int arrive[kResSlots];           // CTAs done with the slot's step
+  unsigned int done;
+  unsigned int abort;
+};
+struct ResidentLaunch {
+  double *z, *x, *vz, *vx, *kvz, *kvx;
+  long long n, first, last, kick_step;
+  double ez, ex, m;
+  int pow2, nbz, nbx;
+  double wp, wc, cells;
+  bool clock;
+  ResCtl* ctl;                              // device
+  unsigned long long* acc;                  // device [kResSlots][2 * nb]
+  unsigned char* rec;                       // mapped host record ring (device pointer)
+  size_t rec_bytes;
+  int H;
+  unsigned long long* flags;                // mapped [H] (device pointer)
+  const volatile unsigned long long* consumed;
+  const volatile unsigned* abort_h;
+  unsigned long long* trace;                // NULL, or [3][last - first] timestamps
+};
+// Largest particle count the resident kernel holds for nb boxes, and its grid.
+int resident_capacity(lbx_ctx* ctx, int nb, long long* max_particles, int* grid);
+int launch_resident(lbx_ctx* ctx, const ResidentLaunch& a, void* stream);
 // Timers strategy helpers (lbx_kernels.cu): phase 0 = box ids + counts,
 // phase 1 = scatter indices into per-box segments (offsets from the host).
 int launch_timers_sort(const double* z, const double* x, long long n, double m, int nbz, int nbx,

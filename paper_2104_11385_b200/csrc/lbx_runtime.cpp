@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -38,6 +40,9 @@ struct lbx_lb {
   std::vector<int64_t> owner, prop, prev;
   std::vector<double> work, scratch, rank_acc;
   std::vector<int64_t> faces_per_rank;
+  std::vector<double> rank3;   // per-rank cost / work / particle sums [3][R]
+  int64_t fmax = 0;            // most off-rank faces of a rank under `owner`
+  bool faces_dirty = true;     // owner changed since fmax was counted
   // calibrated GpuClock: tallies summed over the LB window (the steps since
   // the previous attempt), reset after every attempt
   std::vector<uint64_t> clk_acc;
@@ -80,6 +85,15 @@ struct lbx_sim {
   bool warm = false;     // a per-step launch has run (allocations are done)
   bool capturing = false;
   long long graph_cycles = 0;
+  // resident multi-step kernel (lbx_resident.cu): surrogate physics, particle
+  // set within shared-memory capacity, no per-step kernel timing
+  bool resident = false;            // eligible configuration
+  long long resident_max = 0;       // particle capacity for this box grid
+  ResCtl* rctl = nullptr;           // device
+  unsigned long long* racc = nullptr;      // device [kResSlots][2 * nb]
+  unsigned char* rctl_h = nullptr;         // mapped: flags[ring], consumed, abort
+  unsigned char* rctl_d = nullptr;
+  long long resident_runs = 0;
   // PIC physics
   float* fields[6] = {};
   float* current[3] = {};
@@ -198,13 +212,44 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
   if (o->clock_trace && clk) std::memcpy(o->clock_trace + (size_t)step * nb, clk, 8 * (size_t)nb);
   if (o->n_alive) o->n_alive[step] = n_alive;
 
-  // balance (balancer.py:258-304)
+  // One pass over the boxes: per-rank cost (efficiency), true work (compute
+  // max) and particles (occupancy) under the current mapping.  Each rank's
+  // sums still run in box order (numpy's bincount / add order), three
+  // independent chains instead of three passes.
+  if ((int32_t)s->rank3.size() != 3 * R) s->rank3.assign(3 * (size_t)R, 0.0);
+  double* lc = s->rank3.data();
+  double* lw = lc + R;
+  double* ln = lw + R;
+  auto rank_sums = [&](const int64_t* own, bool with_cost) {
+    std::fill(s->rank3.begin(), s->rank3.end(), 0.0);
+    if (with_cost) {
+      for (int b = 0; b < nb; ++b) {
+        const int64_t r = own[b];
+        lc[r] += cost[b];
+        lw[r] += s->work[b];
+        ln[r] += (double)counts[b];
+      }
+    } else {
+      for (int b = 0; b < nb; ++b) {
+        const int64_t r = own[b];
+        lw[r] += s->work[b];
+        ln[r] += (double)counts[b];
+      }
+    }
+  };
+  rank_sums(s->owner.data(), true);
+
+  // balance (balancer.py:258-304); efficiency as lbx::efficiency (mean / max)
   double e_cur = 1.0;
-  efficiency(cost, s->owner.data(), nb, R, &e_cur, nullptr, s->scratch);
+  {
+    double top = lc[0];
+    for (int32_t r = 1; r < R; ++r) top = std::max(top, lc[r]);
+    if (top != 0.0) e_cur = (pairwise_sum(lc, R) / (double)R) / top;
+  }
   double e_after = e_cur;
   const bool attempted = should_attempt(c, step);
   bool adopted = false;
-  s->prev = s->owner;
+  int64_t moved_particles = 0;
   if (attempted) {
     o->n_attempts += 1;
     int rc = c.strategy == LBX_STRATEGY_KNAPSACK
@@ -218,24 +263,28 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
     adopted = e_prop >= need && e_prop >= e_cur;
     if (adopted && c.migration_ratio > 0.0) {
       // price the redistribution against the load saved over one interval
-      std::vector<double> lc(R, 0.0), lp(R, 0.0);
+      std::vector<double> lpc(R, 0.0), lpp(R, 0.0);
       double total_cost = 0.0;
       int64_t total_n = 0, moved = 0;
       for (int b = 0; b < nb; ++b) {
-        lc[s->owner[b]] += cost[b];
-        lp[s->prop[b]] += cost[b];
+        lpc[s->owner[b]] += cost[b];
+        lpp[s->prop[b]] += cost[b];
         total_cost += cost[b];
         total_n += counts[b];
         if (s->prop[b] != s->owner[b]) moved += counts[b];
       }
-      const double mc = *std::max_element(lc.begin(), lc.end());
-      const double mp = *std::max_element(lp.begin(), lp.end());
+      const double mc = *std::max_element(lpc.begin(), lpc.end());
+      const double mp = *std::max_element(lpp.begin(), lpp.end());
       const double per_push = total_n > 0 ? total_cost / (double)total_n : 0.0;
       const double saved = (double)c.interval * (mc - mp);
       adopted = saved > c.migration_ratio * per_push * (double)moved;
     }
     if (adopted) {
-      s->owner = s->prop;
+      for (int b = 0; b < nb; ++b)
+        if (s->prop[b] != s->owner[b]) moved_particles += counts[b];
+      s->owner.swap(s->prop);
+      s->faces_dirty = true;
+      rank_sums(s->owner.data(), false);   // walltime under the adopted mapping
       e_after = e_prop;
       if (o->adopt_steps) o->adopt_steps[o->n_adoptions] = step;
       if (o->adopt_owners)
@@ -250,33 +299,28 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
   }
 
   // walltime model (workload.py:314-363)
-  std::fill(s->rank_acc.begin(), s->rank_acc.end(), 0.0);
-  for (int b = 0; b < nb; ++b) s->rank_acc[s->owner[b]] += s->work[b];
-  double compute_max = s->rank_acc[0];
-  for (int r = 1; r < R; ++r) compute_max = std::max(compute_max, s->rank_acc[r]);
-  std::fill(s->faces_per_rank.begin(), s->faces_per_rank.end(), 0);
-  for (size_t f = 0; f < s->face_a.size(); ++f) {
-    const int64_t ra = s->owner[s->face_a[f]], rb = s->owner[s->face_b[f]];
-    if (ra != rb) {
-      s->faces_per_rank[ra] += 1;
-      s->faces_per_rank[rb] += 1;
+  double compute_max = lw[0];
+  for (int r = 1; r < R; ++r) compute_max = std::max(compute_max, lw[r]);
+  if (s->faces_dirty) {   // off-rank faces change only with the mapping
+    std::fill(s->faces_per_rank.begin(), s->faces_per_rank.end(), 0);
+    for (size_t f = 0; f < s->face_a.size(); ++f) {
+      const int64_t ra = s->owner[s->face_a[f]], rb = s->owner[s->face_b[f]];
+      if (ra != rb) {
+        s->faces_per_rank[ra] += 1;
+        s->faces_per_rank[rb] += 1;
+      }
     }
+    s->fmax = s->faces_per_rank[0];
+    for (int r = 1; r < R; ++r) s->fmax = std::max(s->fmax, s->faces_per_rank[r]);
+    s->faces_dirty = false;
   }
-  int64_t fmax = s->faces_per_rank[0];
-  for (int r = 1; r < R; ++r) fmax = std::max(fmax, s->faces_per_rank[r]);
-  double comm_max = (double)fmax * c.comm_per_face;
+  double comm_max = (double)s->fmax * c.comm_per_face;
   double gather = attempted ? c.gather : 0.0;
   double redis = 0.0;
-  if (adopted) {
-    int64_t moved = 0;
-    for (int b = 0; b < nb; ++b)
-      if (s->owner[b] != s->prev[b]) moved += counts[b];
-    redis = c.redistribute_latency + c.redistribute_per_particle * (double)moved;
-  }
-  std::fill(s->rank_acc.begin(), s->rank_acc.end(), 0.0);
-  for (int b = 0; b < nb; ++b) s->rank_acc[s->owner[b]] += (double)counts[b];
-  double occ = s->rank_acc[0];
-  for (int r = 1; r < R; ++r) occ = std::max(occ, s->rank_acc[r]);
+  if (adopted)
+    redis = c.redistribute_latency + c.redistribute_per_particle * (double)moved_particles;
+  double occ = ln[0];
+  for (int r = 1; r < R; ++r) occ = std::max(occ, ln[r]);
   const int64_t mrp = (int64_t)occ;
   const bool oom = c.capacity_particles >= 0 && mrp > c.capacity_particles;
   const double ov = c.overhead_factor;
@@ -509,6 +553,120 @@ int process_step(lbx_sim* s, int64_t step, lbx_sim_outputs* o, int* halt) {
                  timers);
 }
 
+// Resident path (lbx_resident.cu): one cooperative launch runs steps
+// [first, last); the host follows the per-step ready flags the kernel raises
+// in mapped memory, runs the host LB step on each record and reports its
+// progress back (the kernel waits only when H steps ahead of the host).  The
+// run ends with the look-back compaction of the CTA ranges' holes.
+int run_resident(lbx_sim* s, int64_t first, int64_t last, lbx_sim_outputs* o, cudaStream_t st,
+                 int* halt) {
+  const lbx_sim_config& c = s->lb->cfg;
+  const int nb = s->lb->nb;
+  const int H = s->ring;
+  volatile unsigned long long* flags = reinterpret_cast<unsigned long long*>(s->rctl_h);
+  volatile unsigned long long* consumed = flags + H;
+  volatile unsigned* abort_h = reinterpret_cast<volatile unsigned*>(flags + H + 1);
+  for (int i = 0; i < H; ++i) flags[i] = 0ull;
+  *consumed = (unsigned long long)first;
+  *abort_h = 0u;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  const bool kick = s->kvz != nullptr;
+  ResidentLaunch a{};
+  a.z = s->z;
+  a.x = s->x;
+  a.vz = s->vz;
+  a.vx = s->vx;
+  a.kvz = s->kvz;
+  a.kvx = s->kvx;
+  a.n = s->n_host;
+  a.first = first;
+  a.last = last;
+  a.kick_step = kick ? c.kick_step : LLONG_MAX;
+  a.ez = (double)c.extent_z;
+  a.ex = (double)c.extent_x;
+  a.m = (double)c.box_size;
+  a.pow2 = (c.box_size & (c.box_size - 1)) == 0;
+  a.nbz = s->lb->nbz;
+  a.nbx = s->lb->nbx;
+  a.wp = c.w_particle;
+  a.wc = c.w_cell;
+  a.cells = (double)c.box_size * (double)c.box_size;
+  a.clock = c.cost_kind == LBX_COST_GPUCLOCK;
+  a.ctl = s->rctl;
+  a.acc = s->racc;
+  a.rec = s->ring_d;
+  a.rec_bytes = s->rec_bytes;
+  a.H = H;
+  a.flags = reinterpret_cast<unsigned long long*>(s->rctl_d);
+  a.consumed = reinterpret_cast<unsigned long long*>(s->rctl_d) + H;
+  a.abort_h = reinterpret_cast<const unsigned*>(reinterpret_cast<unsigned long long*>(s->rctl_d) + H + 1);
+#ifdef LBX_RES_TRACE
+  unsigned long long* trace_d = nullptr;
+  cudaMalloc(&trace_d, 3 * sizeof(unsigned long long) * (last - first));
+  cudaMemset(trace_d, 0, 3 * sizeof(unsigned long long) * (last - first));
+  a.trace = trace_d;
+#endif
+  int rc = launch_resident(s->ctx, a, st);
+  if (rc) return rc;
+  ++s->resident_runs;
+  auto fail = [&](int code) {   // stop the kernel, reset its control state
+    *abort_h = 1u;
+    cudaStreamSynchronize(st);
+    cudaGetLastError();
+    cudaMemsetAsync(s->rctl, 0, sizeof(ResCtl), st);
+    cudaMemsetAsync(s->racc, 0, sizeof(unsigned long long) * 2 * kResSlots * nb, st);
+    cudaStreamSynchronize(st);
+    return code;
+  };
+  for (int64_t step = first; step < last; ++step) {
+    const int slot = (int)(step % H);
+    unsigned spins = 0;
+    while (flags[slot] != (unsigned long long)(step + 1)) {
+      if ((++spins & 4095u) == 0u) {
+        const cudaError_t q = cudaStreamQuery(st);
+        if (q != cudaErrorNotReady && flags[slot] != (unsigned long long)(step + 1)) {
+          return fail(q == cudaSuccess ? set_error(LBX_ECUDA, "resident kernel ended before step %lld",
+                                                   (long long)step)
+                                       : cuda_fail(q, "resident kernel"));
+        }
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    Rec h = rec_at(s->ring_h, s->rec_bytes, slot, nb);
+    if (*h.err != 0)
+      return fail(set_error(LBX_ERANGE, "step %lld: %lld survivors fall outside the box grid",
+                            (long long)step, (long long)*h.err));
+    s->n_host = *h.n;
+    rc = lb_step(s->lb, step, h.counts, nullptr, a.clock ? h.clk : nullptr, *h.n, o, nullptr, halt);
+    if (rc) return fail(rc);
+    std::atomic_thread_fence(std::memory_order_release);
+    *consumed = (unsigned long long)(step + 1);
+  }
+  // holes -> stable compaction; velocities live in the kick arrays once kicked
+  const bool kicked = kick && last > c.kick_step;
+  rc = launch_compact(s->ctx, s->z, s->x, kicked ? s->kvz : s->vz, kicked ? s->kvx : s->vx,
+                      (kick && !kicked) ? s->kvz : nullptr, (kick && !kicked) ? s->kvx : nullptr,
+                      (double)c.extent_z, (double)c.extent_x, st);
+  if (rc) return rc;
+#ifdef LBX_RES_TRACE
+  {
+    const int64_t T = last - first;
+    std::vector<unsigned long long> tr(3 * T);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(tr.data(), trace_d, tr.size() * 8, cudaMemcpyDeviceToHost);
+    cudaFree(trace_d);
+    double per = T > 1 ? (double)(tr[T - 1] - tr[0]) / (T - 1) : 0, rec = 0, lag = 0;
+    for (int64_t i = 0; i < T; ++i) {
+      rec += (double)(tr[2 * T + i] - tr[T + i]);
+      lag += (double)(tr[T + i] - tr[i]);
+    }
+    std::fprintf(stderr, "lbx resident trace: %lld steps, CTA0 step period %.0f ns, courier %.0f ns, "
+                 "step start -> record start %.0f ns\n", (long long)T, per, rec / T, lag / T);
+  }
+#endif
+  return LBX_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -666,6 +824,31 @@ int lbx_sim_create(lbx_sim** out, lbx_ctx* ctx, const lbx_sim_config* cfg) {
     lbx_sim_destroy(s);
     return rc;
   }
+  // resident multi-step kernel: the reference's surrogate step with an
+  // on-device cost form (no Timers launches), no capacity halting (ring > 1)
+  int coop = 0;
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
+  if (coop && s->ring > 1 && cfg->physics == LBX_PHYSICS_SURROGATE &&
+      cfg->cost_kind != LBX_COST_TIMERS && cfg->cost_kind != LBX_COST_CUPTI && nb <= 8192 &&
+      !std::getenv("LBX_NO_RESIDENT")) {
+    int grid = 0;
+    rc = resident_capacity(ctx, nb, &s->resident_max, &grid);
+    const size_t ctl_bytes = sizeof(unsigned long long) * (s->ring + 2);
+    bool ok = rc == LBX_OK &&
+              cudaMalloc(&s->rctl, sizeof(ResCtl)) == cudaSuccess &&
+              cudaMalloc(&s->racc, sizeof(unsigned long long) * 2 * kResSlots * nb) == cudaSuccess &&
+              cudaHostAlloc(&s->rctl_h, ctl_bytes, cudaHostAllocMapped) == cudaSuccess &&
+              cudaHostGetDevicePointer((void**)&s->rctl_d, s->rctl_h, 0) == cudaSuccess;
+    if (ok) {
+      cudaMemset(s->rctl, 0, sizeof(ResCtl));
+      cudaMemset(s->racc, 0, sizeof(unsigned long long) * 2 * kResSlots * nb);
+      std::memset(s->rctl_h, 0, ctl_bytes);
+      s->resident = true;
+    } else {
+      cudaGetLastError();
+      clear_error();
+    }
+  }
   *out = s;
   return LBX_OK;
 }
@@ -684,6 +867,9 @@ int lbx_sim_destroy(lbx_sim* s) {
   if (s->gs) cudaStreamDestroy(s->gs);
   if (s->join) cudaEventDestroy(s->join);
   if (s->cupti) cupti_release();
+  cudaFree(s->rctl);
+  cudaFree(s->racc);
+  if (s->rctl_h) cudaFreeHost(s->rctl_h);
   cudaFree(s->box);
   cudaFree(s->perm);
   cudaFree(s->zero_v);
@@ -760,7 +946,10 @@ int lbx_sim_run(lbx_sim* s, int64_t first, int64_t last, lbx_sim_outputs* o, voi
   if (!s->z) return set_error(LBX_EINVAL, "particles not set");
   if (c.physics == LBX_PHYSICS_PIC && !s->uy)
     return set_error(LBX_EINVAL, "PIC physics needs lbx_sim_set_fields");
-  if (first == 0) std::memcpy(s->lb->owner.data(), o->owner, 8 * (size_t)s->lb->nb);
+  if (first == 0) {
+    std::memcpy(s->lb->owner.data(), o->owner, 8 * (size_t)s->lb->nb);
+    s->lb->faces_dirty = true;
+  }
   for (int b = 0; b < s->lb->nb; ++b)
     if (s->lb->owner[b] < 0 || s->lb->owner[b] >= c.n_ranks)
       return set_error(LBX_EINVAL, "owner entries must lie in [0, %d)", c.n_ranks);
@@ -775,6 +964,12 @@ int lbx_sim_run(lbx_sim* s, int64_t first, int64_t last, lbx_sim_outputs* o, voi
   s->timing = o->kernel_ms != nullptr;
   int64_t launched = first, processed = first;
   int halt = 0;
+  if (s->resident && !s->timing && last - first >= 2 && s->n_host > 0 &&
+      s->n_host <= s->resident_max) {
+    int rc = run_resident(s, first, last, o, st, &halt);
+    if (rc) return rc;
+    processed = launched = last;
+  }
   while (processed < last && !halt) {
     while (launched < last && launched - processed < s->ring) {
       // whole cycle as one graph: aligned, one side of the kick; wait for
@@ -811,6 +1006,13 @@ int lbx_sim_graph_cycles(lbx_sim* s, int64_t* cycles) {
   clear_error();
   if (!s || !cycles) return set_error(LBX_EINVAL, "NULL argument");
   *cycles = s->graph_cycles;
+  return LBX_OK;
+}
+
+int lbx_sim_resident_runs(lbx_sim* s, int64_t* runs) {
+  clear_error();
+  if (!s || !runs) return set_error(LBX_EINVAL, "NULL argument");
+  *runs = s->resident_runs;
   return LBX_OK;
 }
 

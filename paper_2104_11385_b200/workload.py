@@ -441,6 +441,10 @@ class Simulation:
         self.out["owner"] = self.initial_owner.copy()
         self.out["adopt_steps"] = np.zeros(T, dtype=np.int64)
         self.out["adopt_owners"] = np.zeros((T, nb), dtype=np.int64)
+        for v in self.out.values():   # fault the pages in now, not inside the native loop
+            if v is not None:
+                v.fill(0)
+        self.out["owner"][:] = self.initial_owner
         self.time_kernels = time_kernels
         o = self.out
         self.souts = _lib.SimOutputs(
@@ -467,6 +471,13 @@ class Simulation:
         """16-step cycles the native loop has replayed as CUDA graphs."""
         out = C.c_int64()
         _lib.check(_lib.lib.lbx_sim_graph_cycles(self.handle, C.byref(out)))
+        return out.value
+
+    @property
+    def resident_runs(self) -> int:
+        """run() calls the native loop executed on the resident kernel."""
+        out = C.c_int64()
+        _lib.check(_lib.lib.lbx_sim_resident_runs(self.handle, C.byref(out)))
         return out.value
 
     def close(self):

@@ -77,6 +77,8 @@ def test_graph_replay_matches_per_step_launches(runs, name, monkeypatch):
     T = spec.scenario.total_steps
     cuts = [0, 5, 37, 38, T // 2 + 3, T]
 
+    monkeypatch.setenv("LBX_NO_RESIDENT", "1")   # the per-step path (small sets run resident)
+
     def run(graphs):
         if graphs:
             monkeypatch.delenv("LBX_NO_GRAPHS", raising=False)
