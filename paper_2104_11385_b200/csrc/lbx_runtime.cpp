@@ -20,6 +20,11 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
+#include <string>
+#include <thread>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -48,6 +53,8 @@ struct lbx_lb {
   std::vector<uint64_t> clk_acc;
   int64_t acc_n = 0, acc_steps = 0;
 };
+
+struct ProposalPool;
 
 struct lbx_sim {
   lbx_ctx* ctx = nullptr;
@@ -94,6 +101,7 @@ struct lbx_sim {
   unsigned char* rctl_h = nullptr;         // mapped: flags[ring], consumed, abort
   unsigned char* rctl_d = nullptr;
   long long resident_runs = 0;
+  ProposalPool* pool = nullptr;            // resident loop: remap proposals off-thread
   // PIC physics
   float* fields[6] = {};
   float* current[3] = {};
@@ -152,18 +160,22 @@ int validate(const lbx_sim_config& c) {
 
 namespace lbx {
 
-// Host half of one step (see file comment).  `device_cost` is the heuristic
-// cost formed on the device (NULL: form it here from counts -- same
-// separately rounded products).  `clk` is the GpuClock tally (NULL unless
-// cost_kind is GPUCLOCK).
-int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device_cost,
-            const uint64_t* clk, int64_t n_alive, lbx_sim_outputs* o, int* adopted_out,
-            int* halt, const double* timers = nullptr) {
+// Host half of one step (see file comment), in two stages:
+//  lb_cost    the step's cost row (o->cost_trace) and traces -- a function of
+//             the step's record and of earlier records only (the GpuClock
+//             window restarts at every attempt step, adopted or not), never
+//             of the mapping, so a pipelined caller may run it ahead;
+//  lb_decide  efficiency under the current mapping, the remap attempt
+//             (proposal computed here, or handed in by a caller that ran the
+//             knapsack / SFC ahead on the same cost row), gate, walltime.
+// `device_cost` is the heuristic cost formed on the device (NULL: form it
+// here from counts -- same separately rounded products).  `clk` is the
+// GpuClock tally (NULL unless cost_kind is GPUCLOCK).
+int lb_cost(lbx_lb* s, int64_t step, const int64_t* counts, const double* device_cost,
+            const uint64_t* clk, lbx_sim_outputs* o, const double* timers = nullptr) {
   const lbx_sim_config& c = s->cfg;
   const int nb = s->nb;
-  const int32_t R = c.n_ranks;
   const double cells = s->cells;
-  for (int b = 0; b < nb; ++b) s->work[b] = c.work_wp * (double)counts[b] + c.work_wc * cells;
   double* cost = o->cost_trace + (size_t)step * nb;
   switch (c.cost_kind) {
     case LBX_COST_HEURISTIC:
@@ -175,6 +187,7 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
       break;
     case LBX_COST_MEASURED:
     case LBX_COST_INSTRUMENTED:
+      for (int b = 0; b < nb; ++b) s->work[b] = c.work_wp * (double)counts[b] + c.work_wc * cells;
       measured_cost(s->work.data(), nb, c.noise_amplitude, c.noise_seed, (uint64_t)step, cost);
       break;
     case LBX_COST_GPUCLOCK:
@@ -196,6 +209,10 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
         const double scale = tot ? c.w_particle * mean_n / (double)tot : 0.0;
         const double cell = c.w_cell * cells;
         for (int b = 0; b < nb; ++b) cost[b] = (double)s->clk_acc[b] * scale + cell;
+        if (should_attempt(c, step)) {   // new LB window after every attempt
+          std::fill(s->clk_acc.begin(), s->clk_acc.end(), 0ull);
+          s->acc_n = s->acc_steps = 0;
+        }
       } else {
         for (int b = 0; b < nb; ++b) cost[b] = (double)clk[b];
       }
@@ -210,6 +227,24 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
   }
   if (o->count_trace) std::memcpy(o->count_trace + (size_t)step * nb, counts, 8 * (size_t)nb);
   if (o->clock_trace && clk) std::memcpy(o->clock_trace + (size_t)step * nb, clk, 8 * (size_t)nb);
+  return LBX_OK;
+}
+
+// Remap proposal for one cost row (knapsack or SFC, as configured).
+int lb_propose(const lbx_lb* s, const double* cost, int64_t* prop) {
+  const lbx_sim_config& c = s->cfg;
+  return c.strategy == LBX_STRATEGY_KNAPSACK ? knapsack(cost, s->nb, c.n_ranks, c.cap_factor, prop)
+                                             : sfc(cost, s->curve.data(), s->nb, c.n_ranks, prop);
+}
+
+int lb_decide(lbx_lb* s, int64_t step, const int64_t* counts, int64_t n_alive,
+              lbx_sim_outputs* o, int* adopted_out, int* halt, const int64_t* ready_prop) {
+  const lbx_sim_config& c = s->cfg;
+  const int nb = s->nb;
+  const int32_t R = c.n_ranks;
+  const double cells = s->cells;
+  const double* cost = o->cost_trace + (size_t)step * nb;
+  for (int b = 0; b < nb; ++b) s->work[b] = c.work_wp * (double)counts[b] + c.work_wc * cells;
   if (o->n_alive) o->n_alive[step] = n_alive;
 
   // One pass over the boxes: per-rank cost (efficiency), true work (compute
@@ -252,10 +287,12 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
   int64_t moved_particles = 0;
   if (attempted) {
     o->n_attempts += 1;
-    int rc = c.strategy == LBX_STRATEGY_KNAPSACK
-                 ? knapsack(cost, nb, R, c.cap_factor, s->prop.data())
-                 : sfc(cost, s->curve.data(), nb, R, s->prop.data());
-    if (rc) return rc;
+    if (ready_prop) {
+      std::memcpy(s->prop.data(), ready_prop, 8 * (size_t)nb);
+    } else {
+      int rc = lb_propose(s, cost, s->prop.data());
+      if (rc) return rc;
+    }
     double e_prop = 1.0;
     efficiency(cost, s->prop.data(), nb, R, &e_prop, nullptr, s->scratch);
     const double need = c.threshold_relative ? e_cur * (1.0 + c.improvement_threshold)
@@ -291,10 +328,6 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
         std::memcpy(o->adopt_owners + (size_t)o->n_adoptions * nb, s->owner.data(),
                     8 * (size_t)nb);
       o->n_adoptions += 1;
-    }
-    if (c.cost_kind == LBX_COST_GPUCLOCK && c.clock_mode == LBX_CLOCK_CALIBRATED) {
-      std::fill(s->clk_acc.begin(), s->clk_acc.end(), 0ull);   // new LB window
-      s->acc_n = s->acc_steps = 0;
     }
   }
 
@@ -343,6 +376,14 @@ int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device
   if (adopted_out) *adopted_out = adopted ? 1 : 0;
   *halt = oom ? 1 : 0;
   return LBX_OK;
+}
+
+int lb_step(lbx_lb* s, int64_t step, const int64_t* counts, const double* device_cost,
+            const uint64_t* clk, int64_t n_alive, lbx_sim_outputs* o, int* adopted_out,
+            int* halt, const double* timers = nullptr) {
+  int rc = lb_cost(s, step, counts, device_cost, clk, o, timers);
+  if (rc) return rc;
+  return lb_decide(s, step, counts, n_alive, o, adopted_out, halt, nullptr);
 }
 
 }  // namespace lbx
@@ -553,6 +594,88 @@ int process_step(lbx_sim* s, int64_t step, lbx_sim_outputs* o, int* halt) {
                  timers);
 }
 
+}  // namespace
+
+// Proposal pool of the resident loop: worker threads run the remap proposal
+// (knapsack / SFC) of attempt steps whose cost rows the cost stage formed
+// ahead of the decide stage.  One job per attempt step, at most H steps
+// ahead (slot = step % H); the proposal is a pure function of the cost row,
+// so it is the same mapping lb_decide would compute itself.
+struct ProposalPool {
+  struct Job {
+    int64_t step = -1;
+    const double* cost = nullptr;
+    std::vector<int64_t> prop;
+    int rc = 0;
+    std::string err;
+    std::atomic<int> state{0};   // 0 free, 1 queued / running, 2 done
+  };
+  const lbx_lb* lb;
+  std::vector<Job> jobs;
+  std::deque<Job*> queue;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::vector<std::thread> th;
+  bool stop = false;
+
+  ProposalPool(const lbx_lb* l, int slots, int workers) : lb(l), jobs(slots) {
+    for (auto& j : jobs) j.prop.assign(l->nb, 0);
+    for (int w = 0; w < workers; ++w) th.emplace_back([this] { run(); });
+  }
+  ~ProposalPool() {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& t : th) t.join();
+  }
+  void run() {
+    while (true) {
+      Job* j = nullptr;
+      {
+        std::unique_lock<std::mutex> g(mu);
+        cv.wait(g, [this] { return stop || !queue.empty(); });
+        if (stop && queue.empty()) return;
+        j = queue.front();
+        queue.pop_front();
+      }
+      j->rc = lb_propose(lb, j->cost, j->prop.data());
+      if (j->rc) j->err = lbx_last_error();
+      j->state.store(2, std::memory_order_release);
+    }
+  }
+  void submit(int64_t step, const double* cost) {
+    Job& j = jobs[step % (int64_t)jobs.size()];
+    j.step = step;
+    j.cost = cost;
+    j.rc = 0;
+    j.state.store(1, std::memory_order_relaxed);
+    {
+      std::lock_guard<std::mutex> g(mu);
+      queue.push_back(&j);
+    }
+    cv.notify_one();
+  }
+  int wait(int64_t step, const int64_t** prop) {
+    Job& j = jobs[step % (int64_t)jobs.size()];
+    if (j.step != step || j.state.load(std::memory_order_relaxed) == 0)
+      return set_error(LBX_EINVAL, "no proposal queued for step %lld", (long long)step);
+    while (j.state.load(std::memory_order_acquire) != 2) std::this_thread::yield();
+    j.state.store(0, std::memory_order_relaxed);
+    if (j.rc) return set_error(j.rc, "%s", j.err.c_str());
+    *prop = j.prop.data();
+    return LBX_OK;
+  }
+  void drain() {   // let queued / running jobs finish (their cost rows stay valid)
+    for (auto& j : jobs)
+      while (j.state.load(std::memory_order_acquire) == 1) std::this_thread::yield();
+    for (auto& j : jobs) j.state.store(0, std::memory_order_relaxed);
+  }
+};
+
+namespace {
+
 // Resident path (lbx_resident.cu): one cooperative launch runs steps
 // [first, last); the host follows the per-step ready flags the kernel raises
 // in mapped memory, runs the host LB step on each record and reports its
@@ -610,6 +733,7 @@ int run_resident(lbx_sim* s, int64_t first, int64_t last, lbx_sim_outputs* o, cu
   if (rc) return rc;
   ++s->resident_runs;
   auto fail = [&](int code) {   // stop the kernel, reset its control state
+    if (s->pool) s->pool->drain();
     *abort_h = 1u;
     cudaStreamSynchronize(st);
     cudaGetLastError();
@@ -618,13 +742,20 @@ int run_resident(lbx_sim* s, int64_t first, int64_t last, lbx_sim_outputs* o, cu
     cudaStreamSynchronize(st);
     return code;
   };
+  // Records are taken in two passes: the cost stage (lb_cost) runs ahead on
+  // every record that has arrived, and hands each attempt step's cost row to
+  // the proposal pool (the knapsack / SFC of the step, off this thread); the
+  // decide stage (lb_decide) follows in step order and collects the proposal.
+  ProposalPool* pool = s->pool;
+  auto ready = [&](int64_t t) { return flags[t % H] == (unsigned long long)(t + 1); };
+  int64_t ahead = first;   // next step for the cost stage
   for (int64_t step = first; step < last; ++step) {
     const int slot = (int)(step % H);
     unsigned spins = 0;
-    while (flags[slot] != (unsigned long long)(step + 1)) {
+    while (!ready(step)) {
       if ((++spins & 4095u) == 0u) {
         const cudaError_t q = cudaStreamQuery(st);
-        if (q != cudaErrorNotReady && flags[slot] != (unsigned long long)(step + 1)) {
+        if (q != cudaErrorNotReady && !ready(step)) {
           return fail(q == cudaSuccess ? set_error(LBX_ECUDA, "resident kernel ended before step %lld",
                                                    (long long)step)
                                        : cuda_fail(q, "resident kernel"));
@@ -632,12 +763,26 @@ int run_resident(lbx_sim* s, int64_t first, int64_t last, lbx_sim_outputs* o, cu
       }
     }
     std::atomic_thread_fence(std::memory_order_acquire);
+    while (ahead < last && ahead < step + H && (ahead == step || ready(ahead))) {
+      std::atomic_thread_fence(std::memory_order_acquire);
+      Rec r = rec_at(s->ring_h, s->rec_bytes, (int)(ahead % H), nb);
+      if (*r.err != 0)
+        return fail(set_error(LBX_ERANGE, "step %lld: %lld survivors fall outside the box grid",
+                              (long long)ahead, (long long)*r.err));
+      rc = lb_cost(s->lb, ahead, r.counts, nullptr, a.clock ? r.clk : nullptr, o);
+      if (rc) return fail(rc);
+      if (pool && should_attempt(c, ahead))
+        pool->submit(ahead, o->cost_trace + (size_t)ahead * nb);
+      ++ahead;
+    }
     Rec h = rec_at(s->ring_h, s->rec_bytes, slot, nb);
-    if (*h.err != 0)
-      return fail(set_error(LBX_ERANGE, "step %lld: %lld survivors fall outside the box grid",
-                            (long long)step, (long long)*h.err));
     s->n_host = *h.n;
-    rc = lb_step(s->lb, step, h.counts, nullptr, a.clock ? h.clk : nullptr, *h.n, o, nullptr, halt);
+    const int64_t* prop = nullptr;
+    if (pool && should_attempt(c, step)) {
+      rc = pool->wait(step, &prop);
+      if (rc) return fail(rc);
+    }
+    rc = lb_decide(s->lb, step, h.counts, *h.n, o, nullptr, halt, prop);
     if (rc) return fail(rc);
     std::atomic_thread_fence(std::memory_order_release);
     *consumed = (unsigned long long)(step + 1);
@@ -844,6 +989,11 @@ int lbx_sim_create(lbx_sim** out, lbx_ctx* ctx, const lbx_sim_config* cfg) {
       cudaMemset(s->racc, 0, sizeof(unsigned long long) * 2 * kResSlots * nb);
       std::memset(s->rctl_h, 0, ctl_bytes);
       s->resident = true;
+      if (cfg->interval <= cfg->total_steps || cfg->static_step >= 0) {
+        const char* e = std::getenv("LBX_LB_WORKERS");
+        const int workers = e ? std::atoi(e) : 4;
+        if (workers > 0) s->pool = new ProposalPool(lb, s->ring, workers);
+      }
     } else {
       cudaGetLastError();
       clear_error();
@@ -867,6 +1017,7 @@ int lbx_sim_destroy(lbx_sim* s) {
   if (s->gs) cudaStreamDestroy(s->gs);
   if (s->join) cudaEventDestroy(s->join);
   if (s->cupti) cupti_release();
+  delete s->pool;
   cudaFree(s->rctl);
   cudaFree(s->racc);
   if (s->rctl_h) cudaFreeHost(s->rctl_h);
