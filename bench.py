@@ -466,10 +466,13 @@ def c2_native(args, dev, spec, sc, pos0, kick0, steps=400):
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
     n = pos0.shape[0]
+    resident = sim.resident_runs
     sim.close()
     return {"particles": n, "steps": steps, "us_per_step": 1e3 * ms / steps,
             "pushes_per_s": n * steps / (ms / 1e3),
-            "note": "L2-resident, launch/latency bound; incl. host LB loop"}
+            "resident_runs": resident,
+            "note": "resident kernel (particles in shared memory across steps, lbx_resident.cu); "
+                    "incl. the host LB loop (8-rank GpuClock knapsack every 10)"}
 
 
 C1_DOC = dict(scenario_id="c1-uniform", domain=dict(extent=[128, 128], box_size=32), ranks=8,
@@ -505,6 +508,7 @@ def c1_uniform(dev, steps=200, warm=20):
     torch.cuda.synchronize(dev)
     gpu_ms = e0.elapsed_time(e1)
     res = sim.result()
+    resident = sim.resident_runs
     sim.close()
     K, kind = _ref_kernels()
     cfg = O.config_from_doc(C1_DOC)
@@ -528,7 +532,9 @@ def c1_uniform(dev, steps=200, warm=20):
             "cpu_pushes_per_s": n * steps / cpu_s, "cpu_kind": kind, "cpu_cores": 1,
             "mean_efficiency": res.summary["mean_efficiency"],
             "adoptions": res.summary["adoption_count"],
-            "note": "L2-resident, latency bound; parity of this config: tests/test_gpu_runs.py::c1"}
+            "resident_runs": resident,
+            "note": "resident kernel (lbx_resident.cu); parity of this config: "
+                    "tests/test_gpu_runs.py::c1, tests/test_gpu_resident.py"}
 
 
 def compaction_leavers(dev, n=100_000_000, steps=3, ext=960.0, box=32.0):
