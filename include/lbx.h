@@ -167,6 +167,7 @@ typedef struct lbx_step3d_args {
 
 int lbx_push_step_3d(lbx_ctx* ctx, const lbx_step3d_args* args, void* stream);
 
+
 /* Replaces cost.py:83-95 heuristic_cost on device vectors:
  * cost[i] = w_particle*particles[i] + w_cell*cells[i], two separately
  * rounded products then one add (no FMA). */
@@ -523,6 +524,23 @@ int lbx_partition(lbx_ctx* ctx, double* z, double* x, double* vz, double* vx,
                   double extent_z, double extent_x, double box_size, int32_t nbz,
                   int32_t nbx, const lbx_exchange_args* ex, int64_t* n_out,
                   void* stream);
+/* Multi-GPU 3D (Distributed3D; the 3D analogue of lbx_push_step_exchange,
+ * not fused over peer memory): the same fused 3D step, and survivors in
+ * boxes another rank owns (ex->owner, int32 [nbz*nby*nbx]) are staged as
+ * 6-double (z, y, x, vz, vy, vx) records with their destination (still
+ * counted in their box: per-rank counts sum to the global bin counts) and
+ * removed locally.  ex->removed_list is required (lbx_fill_holes with z, y,
+ * x, vz, vy, vx in the six slots compacts); no pending kick arrays, no peer
+ * buffers.  lbx_group_by_dest / lbx_unpack (same six slots) move the records. */
+int lbx_push_step_3d_exchange(lbx_ctx* ctx, const lbx_step3d_args* args,
+                              const lbx_exchange_args* ex, void* stream);
+/* Adoption-time 3D migration: stage and list every particle whose box
+ * ex->owner gives to another rank (no push).  n_out (device int64[2]) =
+ * {particles kept, error code}. */
+int lbx_partition_3d(lbx_ctx* ctx, double* z, double* y, double* x, double* vz,
+                     double* vy, double* vx, int32_t extent_z, int32_t extent_y,
+                     int32_t extent_x, int32_t box_size, const lbx_exchange_args* ex,
+                     int64_t* n_out, void* stream);
 /* Unstable O(removed) compaction: the n_removed listed indices (any order)
  * are removed from [0, n_new + n_removed) by moving survivors from the tail
  * [n_new, n_new + n_removed) into the holes below n_new.  kick_vz/kick_vx may

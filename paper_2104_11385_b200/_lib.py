@@ -168,6 +168,9 @@ class Step3DArgs(C.Structure):
 
 
 SIGNATURES["lbx_push_step_3d"] = (i32, [vp, P(Step3DArgs), vp])
+SIGNATURES["lbx_push_step_3d_exchange"] = (i32, [vp, P(Step3DArgs), P(ExchangeArgs), vp])
+SIGNATURES["lbx_partition_3d"] = (i32, [vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32,
+                                        P(ExchangeArgs), vp, vp])
 
 
 class LBXError(RuntimeError):

@@ -543,7 +543,41 @@ struct Step3DParams {
   double wp, wc, cells;
   long long* removed_list;
   long long removed_cap;
+  // multi-GPU 3D exchange (Distributed3D): survivors in boxes another rank
+  // owns are staged as (z, y, x, vz, vy, vx) records and removed locally
+  const int* owner;   // NULL: no exchange
+  int me;
+  double* stage;
+  int* stage_dest;
+  long long stage_cap;
+  long long* send_counts;
 };
+
+// Stage one 3D emigrant record (warp-collective: every lane calls it).
+__device__ __forceinline__ void stage3d(const Step3DParams& p, bool em, double z, double y,
+                                        double x, double vz, double vy, double vx, int dest) {
+  const unsigned mask = __ballot_sync(kFull, em);
+  if (!mask) return;
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == __ffs(mask) - 1) base = atomicAdd(&p.st->staged, (unsigned long long)__popc(mask));
+  base = __shfl_sync(kFull, base, __ffs(mask) - 1);
+  if (!em) return;
+  const long long slot = (long long)base + __popc(mask & lanemask_lt());
+  if (slot >= p.stage_cap) {
+    atomicOr((unsigned long long*)&p.st->err, 1ull << 62);  // staging overflow
+    return;
+  }
+  double* r = p.stage + slot * 6;
+  r[0] = z;
+  r[1] = y;
+  r[2] = x;
+  r[3] = vz;
+  r[4] = vy;
+  r[5] = vx;
+  p.stage_dest[slot] = dest;
+  atomicAdd((unsigned long long*)(p.send_counts + dest), 1ull);
+}
 
 template <bool kClock>
 __global__ void __launch_bounds__(kBlock, 4) stream3d_kernel(Step3DParams p) {
@@ -601,18 +635,35 @@ __global__ void __launch_bounds__(kBlock, 4) stream3d_kernel(Step3DParams p) {
         const bool keep = valid && nz[t] >= 0.0 && nz[t] < p.ez && ny[t] >= 0.0 &&
                           ny[t] < p.ey && nx[t] >= 0.0 && nx[t] < p.ex;
         box[2 * r + t] = -1;
+        bool emig = false;
+        int dest = 0;
         if (keep) {
           const int bz = (int)__dmul_rn(nz[t], p.inv_m), by = (int)__dmul_rn(ny[t], p.inv_m),
                     bx = (int)__dmul_rn(nx[t], p.inv_m);
-          if (bz < p.nbz && by < p.nby && bx < p.nbx) box[2 * r + t] = (bz * p.nby + by) * p.nbx + bx;
-          else ++err;
+          if (bz < p.nbz && by < p.nby && bx < p.nbx) {
+            box[2 * r + t] = (bz * p.nby + by) * p.nbx + bx;
+            if (p.owner) {
+              dest = __ldg(p.owner + box[2 * r + t]);
+              emig = dest != p.me;
+            }
+          } else {
+            ++err;
+          }
         } else if (valid) {
           ++removed;
           first_out = min(first_out, i);
-          nz[t] = -1.0;  // compaction sentinel
         }
+        if (p.owner) {   // counted in its box above; leaves this rank's arrays
+          const double vz0 = t ? d.y : d.x, vy0 = t ? e.y : e.x, vx0 = t ? f.y : f.x;
+          stage3d(p, emig, nz[t], ny[t], nx[t], vz0, vy0, vx0, dest);
+          if (emig) {
+            ++removed;
+            first_out = min(first_out, i);
+          }
+        }
+        if (valid && (!keep || emig)) nz[t] = -1.0;  // compaction sentinel
         if (p.removed_list) {
-          const bool rm = valid && box[2 * r + t] < 0 && !(keep);
+          const bool rm = valid && (!keep || emig);
           const unsigned m = __ballot_sync(kFull, rm);
           if (m) {
             unsigned long long base = 0;
@@ -720,6 +771,60 @@ __global__ void __launch_bounds__(kBlock, 4) stream3d_kernel(Step3DParams p) {
     p.st->done = 0u;
     __threadfence_system();
   }
+}
+
+// Adoption-time 3D migration: particles in boxes another rank now owns are
+// staged (as stream3d_kernel's emigrants) and listed as removed; no push.
+__global__ void __launch_bounds__(kBlock) partition3d_kernel(Step3DParams p) {
+  const long long n = *((volatile long long*)&p.st->n);
+  const int lane = threadIdx.x & 31;
+  const long long stride = (long long)gridDim.x * kBlock;
+  const long long end = (n + kBlock - 1) / kBlock * kBlock;   // whole warps: collectives
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < end; i += stride) {
+    const bool valid = i < n;
+    double z = 0, y = 0, x = 0, vz = 0, vy = 0, vx = 0;
+    bool em = false;
+    int dest = 0;
+    if (valid) {
+      z = p.z[i];
+      y = p.y[i];
+      x = p.x[i];
+      const int bz = (int)__dmul_rn(z, p.inv_m), by = (int)__dmul_rn(y, p.inv_m),
+                bx = (int)__dmul_rn(x, p.inv_m);
+      if (z >= 0.0 && bz < p.nbz && y >= 0.0 && by < p.nby && x >= 0.0 && bx < p.nbx) {
+        dest = __ldg(p.owner + (bz * p.nby + by) * p.nbx + bx);
+        em = dest != p.me;
+      } else {
+        atomicAdd((unsigned long long*)&p.st->err, 1ull);
+      }
+      if (em) {
+        vz = p.vz[i];
+        vy = p.vy[i];
+        vx = p.vx[i];
+      }
+    }
+    stage3d(p, em, z, y, x, vz, vy, vx, dest);
+    const unsigned m = __ballot_sync(kFull, em);
+    if (m) {
+      unsigned long long base = 0;
+      if (lane == __ffs(m) - 1) base = atomicAdd(&p.st->removed_count, (unsigned long long)__popc(m));
+      base = __shfl_sync(kFull, base, __ffs(m) - 1);
+      if (em) {
+        const long long slot = (long long)base + __popc(m & lanemask_lt());
+        if (slot < p.removed_cap) p.removed_list[slot] = i;
+        else atomicOr((unsigned long long*)&p.st->err, 1ull << 61);
+        p.z[i] = -1.0;
+      }
+    }
+  }
+}
+
+// n_out = {survivors kept in place, error code} after partition3d_kernel.
+__global__ void partition_done_kernel(DevState* st, long long* n_out) {
+  const long long L = (long long)st->removed_count;
+  n_out[0] = st->n - L;
+  n_out[1] = st->err;
+  st->n -= L;
 }
 
 // ---------------------------------------------------------------------------
@@ -2022,8 +2127,30 @@ int lbx_partition(lbx_ctx* ctx, double* z, double* x, double* vz, double* vx, do
   return launch_push_step(ctx, l, stream, ex, false);
 }
 
+static int push_step_3d(lbx_ctx* ctx, const lbx_step3d_args* a, const lbx_exchange_args* ex,
+                        void* stream);
+
 int lbx_push_step_3d(lbx_ctx* ctx, const lbx_step3d_args* a, void* stream) {
   clear_error();
+  return push_step_3d(ctx, a, nullptr, stream);
+}
+
+int lbx_push_step_3d_exchange(lbx_ctx* ctx, const lbx_step3d_args* a,
+                              const lbx_exchange_args* ex, void* stream) {
+  clear_error();
+  if (!ex) return set_error(LBX_EINVAL, "NULL argument");
+  if (ex->world < 1 || ex->world > 64 || ex->rank < 0 || ex->rank >= ex->world)
+    return set_error(LBX_EINVAL, "rank %d / world %d out of range", ex->rank, ex->world);
+  if (!ex->owner || !ex->stage || !ex->stage_dest || !ex->send_counts || !ex->removed_list)
+    return set_error(LBX_EINVAL, "3D exchange needs owner, stage, stage_dest, send_counts "
+                                 "and removed_list");
+  if (ex->kick_vz || ex->kick_vx || ex->peer_recv)
+    return set_error(LBX_EINVAL, "3D exchange: no pending kick arrays, no peer buffers");
+  return push_step_3d(ctx, a, ex, stream);
+}
+
+static int push_step_3d(lbx_ctx* ctx, const lbx_step3d_args* a, const lbx_exchange_args* ex,
+                        void* stream) {
   if (!ctx || !a) return set_error(LBX_EINVAL, "NULL argument");
   const int M = a->box_size;
   if (M < 1 || (M & (M - 1)) || a->extent_z % M || a->extent_y % M || a->extent_x % M)
@@ -2067,6 +2194,16 @@ int lbx_push_step_3d(lbx_ctx* ctx, const lbx_step3d_args* a, void* stream) {
   p.cells = (double)M * M * M;
   p.removed_list = reinterpret_cast<long long*>(a->removed_list);
   p.removed_cap = a->removed_cap;
+  if (ex) {
+    p.owner = ex->owner;
+    p.me = ex->rank;
+    p.stage = ex->stage;
+    p.stage_dest = ex->stage_dest;
+    p.stage_cap = ex->stage_cap;
+    p.send_counts = reinterpret_cast<long long*>(ex->send_counts);
+    p.removed_list = reinterpret_cast<long long*>(ex->removed_list);
+    p.removed_cap = ex->removed_cap;
+  }
   const bool clock = (a->flags & LBX_STEP_CLOCK) != 0;
   auto kern = clock ? stream3d_kernel<true> : stream3d_kernel<false>;
   const size_t smem = p.smem_hist ? (size_t)nb * 4 * (clock ? 2 : 1) : 0;
@@ -2083,9 +2220,53 @@ int lbx_push_step_3d(lbx_ctx* ctx, const lbx_step3d_args* a, void* stream) {
   if (ctx->timing) cudaEventRecord((cudaEvent_t)ctx->ev1, s);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "stream3d_kernel launch");
-  if (a->removed_list) return LBX_OK;  // caller compacts with lbx_fill_holes
+  if (p.removed_list) return LBX_OK;  // caller compacts with lbx_fill_holes
   return launch_compact(ctx, a->z, a->x, a->y, a->vz, a->vy, a->vx, (double)a->extent_z,
                         (double)a->extent_x, stream);
+}
+
+int lbx_partition_3d(lbx_ctx* ctx, double* z, double* y, double* x, double* vz, double* vy,
+                     double* vx, int32_t extent_z, int32_t extent_y, int32_t extent_x,
+                     int32_t box_size, const lbx_exchange_args* ex, int64_t* n_out,
+                     void* stream) {
+  clear_error();
+  if (!ctx || !ex || !n_out) return set_error(LBX_EINVAL, "NULL argument");
+  const int M = box_size;
+  if (M < 1 || (M & (M - 1)) || extent_z % M || extent_y % M || extent_x % M)
+    return set_error(LBX_EINVAL, "3D box_size must be a power of two dividing the extents");
+  if (ex->world < 1 || ex->world > 64 || ex->rank < 0 || ex->rank >= ex->world)
+    return set_error(LBX_EINVAL, "rank %d / world %d out of range", ex->rank, ex->world);
+  if (!ex->owner || !ex->stage || !ex->stage_dest || !ex->send_counts || !ex->removed_list)
+    return set_error(LBX_EINVAL, "3D partition needs owner, stage, stage_dest, send_counts "
+                                 "and removed_list");
+  Step3DParams p{};
+  p.z = z;
+  p.y = y;
+  p.x = x;
+  p.vz = vz;
+  p.vy = vy;
+  p.vx = vx;
+  p.inv_m = 1.0 / M;
+  p.nbz = extent_z / M;
+  p.nby = extent_y / M;
+  p.nbx = extent_x / M;
+  p.st = ctx->st;
+  p.owner = ex->owner;
+  p.me = ex->rank;
+  p.stage = ex->stage;
+  p.stage_dest = ex->stage_dest;
+  p.stage_cap = ex->stage_cap;
+  p.send_counts = reinterpret_cast<long long*>(ex->send_counts);
+  p.removed_list = reinterpret_cast<long long*>(ex->removed_list);
+  p.removed_cap = ex->removed_cap;
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long blocks = std::max(1ll, std::min((long long)(ctx->n_upper + kBlock - 1) / kBlock,
+                                                  (long long)ctx->num_sms * 8));
+  partition3d_kernel<<<(unsigned)blocks, kBlock, 0, s>>>(p);
+  partition_done_kernel<<<1, 1, 0, s>>>(ctx->st, reinterpret_cast<long long*>(n_out));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "partition3d_kernel launch");
+  return LBX_OK;
 }
 
 int lbx_fill_holes(lbx_ctx* ctx, double* z, double* x, double* vz, double* vx, double* kick_vz,
