@@ -15,6 +15,13 @@ seed 1) from the kick (radial 0.035 + drift 0.01), tiled R times (default
     (max rank work / total work) -- a strong-scaling estimate, labelled as
     such (one GPU is available this round).
 Prints one JSON object.
+
+`--distributed` (under torchrun, one rank per GPU, NCCL): the real
+multi-GPU path instead -- three_d.Distributed3D with the scenario's
+particles split by box ownership (strong scaling: the total is fixed), the
+fused 3D exchange push, all-reduced counts, record all-to-all, replicated
+LB and adoption-time migration; device-timed (CUDA events, barrier, max
+over ranks) pushes/s of the whole job.
 """
 
 from __future__ import annotations
@@ -35,7 +42,13 @@ def main():
     ap.add_argument("--replicas", type=int, default=140)
     ap.add_argument("--steps", type=int, default=12)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--distributed", action="store_true",
+                    help="real multi-GPU run (torchrun, NCCL): Distributed3D strong scaling")
+    ap.add_argument("--strategy", default="knapsack", choices=["knapsack", "sfc"])
+    ap.add_argument("--interval", type=int, default=10)
     args = ap.parse_args()
+    if args.distributed:
+        return distributed_main(args)
 
     import torch
 
@@ -161,6 +174,66 @@ def main():
                    "included; model_*: 1-GPU step x max rank work share"}
     sim.close()
     print(json.dumps(out))
+
+
+def distributed_main(args):
+    """Config C4 on WORLD_SIZE GPUs through Distributed3D (see module doc)."""
+    import os
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2104_11385_b200.balancer import BalancePolicy, Strategy
+    from paper_2104_11385_b200.cost import make_provider
+    from paper_2104_11385_b200.parallel import TorchComm
+    from paper_2104_11385_b200.three_d import (Distributed3D, Scenario3D, kick_velocities_3d,
+                                               sample_blob_3d)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    total = args.warmup + args.steps
+    cfg = Scenario3D("c4-3d-blob", (256, 256, 128), 32, world, (128.0, 128.0, 64.0), 40.0, 4.0,
+                     2.0, kick_step=0, kick_speed=0.035, kick_drift=0.01, total_steps=total,
+                     initial_mapping="sfc" if args.strategy == "sfc" else "knapsack")
+    pos0 = sample_blob_3d(cfg)
+    kick0 = kick_velocities_3d(pos0, cfg)
+    pol = BalancePolicy(strategy=Strategy(args.strategy), interval=args.interval)
+    sim = Distributed3D(cfg, pol, make_provider("gpuclock"), comm=TorchComm(), device=dev,
+                        positions=pos0, kick=kick0, replicas=args.replicas,
+                        capacity=int(len(pos0) * args.replicas * min(1.0, 2.5 / world)) + 4096)
+    sim.run(0, args.warmup)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    sim.run(args.warmup, total)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    wall = time.perf_counter() - t0
+    ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    n_total = sim.n_total
+    if rank == 0:
+        print(json.dumps({
+            "workload": "C4 3D blob 256x256x128, 256 boxes, GpuClock, "
+                        f"{args.strategy} every {args.interval} (Distributed3D)",
+            "n_gpus": world, "particles": n_total, "steps": args.steps,
+            "ms_per_step": float(ms.item()) / args.steps,
+            "pushes_per_s": n_total * args.steps / (float(ms.item()) / 1e3),
+            "wall_s": wall, "scaling": "strong", "adoptions": int(sim.souts.n_adoptions),
+            "emigrated_per_step": float(sim.emigrated[args.warmup:total].mean()),
+            "migrated": int(sim.moved.sum())}), flush=True)
+    sim.close()
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":
