@@ -145,6 +145,11 @@ __device__ __forceinline__ float lerp_f(float a, float b, float f) {
 __device__ __forceinline__ float cic_fast(const float4 q, float fz, float fx) {
   return lerp_f(lerp_f(q.x, q.y, fx), lerp_f(q.z, q.w, fx), fz);
 }
+// Tolerance mode on a difference quad (a, b - a, c - a, a - b - c + d), as
+// pic_quad_kernel writes it for LBX_PIC_FAST: the bilinear form in 3 FMAs.
+__device__ __forceinline__ float cic_diff(const float4 q, float fz, float fx) {
+  return __fmaf_rn(fz, __fmaf_rn(fx, q.w, q.z), __fmaf_rn(fx, q.y, q.x));
+}
 
 // Fire-and-forget adds (REDG; a plain atomicAdd may keep the returning ATOMG
 // form inside large kernels).
@@ -155,6 +160,13 @@ __device__ __forceinline__ void red_add32(unsigned* a, unsigned v) {
   asm volatile("red.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
 }
 
+// Streaming particle loads do not allocate in L1, which the quad gathers of
+// the blob's few hot cells share (an L2::evict_first hint on top doubled the
+// DRAM reads: the second 32-byte sector of a 64-byte DRAM atom is read by
+// the next group, after eviction).
+#ifndef LBX_PIC_LDQ
+#define LBX_PIC_LDQ ".L1::no_allocate"
+#endif
 // kG consecutive doubles [i, i+kG): one vector streaming load (256-bit for
 // kG = 4) when the group is complete, else clamped scalar loads (tail lanes
 // reload a live particle).
@@ -163,7 +175,7 @@ __device__ __forceinline__ void ldg(const double* a, long long i, long long n, d
     if (kG % 4 == 0) {
 #pragma unroll
       for (int c = 0; c < kG; c += 4)
-        asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];"
+        asm volatile("ld.global" LBX_PIC_LDQ ".v4.f64 {%0,%1,%2,%3}, [%4];"
                      : "=d"(v[c % kG]), "=d"(v[(c + 1) % kG]), "=d"(v[(c + 2) % kG]),
                        "=d"(v[(c + 3) % kG])
                      : "l"(a + i + c));
@@ -333,6 +345,20 @@ __device__ __forceinline__ float gather_c(const PicParams& p, int c, int i0, int
   return kFast ? cic_fast(q, fz, fx) : cic(q, fz, fx);
 }
 
+// MUFU approximations (<= 2 ulp; arguments are >= 1 here, so flushing
+// denormals never applies): one instruction each instead of the IEEE
+// sequences of rsqrtf / __frcp_rn.
+__device__ __forceinline__ float rsqrt_approx(float v) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ float rcp_approx(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
 // Tolerance-mode relativistic Boris (LBX_PIC_FAST).  The rotation is
 // evaluated in float32 (FMA, MUFU rsqrt / rcp) but only as the INCREMENT
 // du = u_new - u = 2 hE + (u- x t) + s (u' x t), which is added to the
@@ -345,9 +371,9 @@ __device__ __forceinline__ float boris_fast(double& ux, double& uy, double& uz, 
   const float hEx = hf * Ex, hEy = hf * Ey, hEz = hf * Ez;
   const float mx = __fadd_rn((float)ux, hEx), my = __fadd_rn((float)uy, hEy),
               mz = __fadd_rn((float)uz, hEz);
-  const float ig = rsqrtf(__fmaf_rn(mz, mz, __fmaf_rn(my, my, __fmaf_rn(mx, mx, 1.f))));
+  const float ig = rsqrt_approx(__fmaf_rn(mz, mz, __fmaf_rn(my, my, __fmaf_rn(mx, mx, 1.f))));
   const float tx = hf * Bx * ig, ty = hf * By * ig, tz = hf * Bz * ig;
-  const float sr = __frcp_rn(__fmaf_rn(tz, tz, __fmaf_rn(ty, ty, __fmaf_rn(tx, tx, 1.f))));
+  const float sr = rcp_approx(__fmaf_rn(tz, tz, __fmaf_rn(ty, ty, __fmaf_rn(tx, tx, 1.f))));
   const float s2 = 2.f * sr;
   // u' - u- = u- x t ; u+ - u- = s (u' x t)
   const float cx = __fmaf_rn(my, tz, -mz * ty), cy = __fmaf_rn(mz, tx, -mx * tz),
@@ -359,7 +385,7 @@ __device__ __forceinline__ float boris_fast(double& ux, double& uy, double& uz, 
   uy = __dadd_rn(uy, (double)(__fmaf_rn(2.f, hEy, ry)));
   uz = __dadd_rn(uz, (double)(__fmaf_rn(2.f, hEz, rz)));
   const float fx = (float)ux, fy = (float)uy, fz = (float)uz;
-  return rsqrtf(__fmaf_rn(fz, fz, __fmaf_rn(fy, fy, __fmaf_rn(fx, fx, 1.f))));
+  return rsqrt_approx(__fmaf_rn(fz, fz, __fmaf_rn(fy, fy, __fmaf_rn(fx, fx, 1.f))));
 }
 
 // Tolerance mode (LBX_PIC_FAST): cell by truncation, fraction rounded to
@@ -377,6 +403,11 @@ __device__ __forceinline__ Axis fast_axis(double v) {
 template <bool kFast>
 __device__ __forceinline__ Axis pic_axis(double v) {
   return kFast ? fast_axis(v) : axis_of(v);
+}
+
+template <bool kQuad>
+__device__ __forceinline__ float fast_gather(const float4 q, float fz, float fx) {
+  return kQuad ? cic_diff(q, fz, fx) : cic_fast(q, fz, fx);
 }
 
 // One component's 2x2 node quad at a precomputed node offset (quad copy or
@@ -562,12 +593,12 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
           // the four stagger combinations' node offsets, computed once
           const int pit = kQuad ? p.qpitch : p.pitch;
           const int rA = (az.i + 1) * pit, rH = (az.ih + 1) * pit, cA = ax.i + 1, cH = ax.ih + 1;
-          const float Ex = cic_fast(quad_at<kQuad>(p, 0, rA + cH), az.f, ax.fh);
-          const float Ey = cic_fast(quad_at<kQuad>(p, 1, rA + cA), az.f, ax.f);
-          const float Ez = cic_fast(quad_at<kQuad>(p, 2, rH + cA), az.fh, ax.f);
-          const float Bx = cic_fast(quad_at<kQuad>(p, 3, rH + cA), az.fh, ax.f);
-          const float By = cic_fast(quad_at<kQuad>(p, 4, rH + cH), az.fh, ax.fh);
-          const float Bz = cic_fast(quad_at<kQuad>(p, 5, rA + cH), az.f, ax.fh);
+          const float Ex = fast_gather<kQuad>(quad_at<kQuad>(p, 0, rA + cH), az.f, ax.fh);
+          const float Ey = fast_gather<kQuad>(quad_at<kQuad>(p, 1, rA + cA), az.f, ax.f);
+          const float Ez = fast_gather<kQuad>(quad_at<kQuad>(p, 2, rH + cA), az.fh, ax.f);
+          const float Bx = fast_gather<kQuad>(quad_at<kQuad>(p, 3, rH + cA), az.fh, ax.f);
+          const float By = fast_gather<kQuad>(quad_at<kQuad>(p, 4, rH + cH), az.fh, ax.fh);
+          const float Bz = fast_gather<kQuad>(quad_at<kQuad>(p, 5, rA + cH), az.f, ax.fh);
           const float ig = boris_fast(pux[k], puy[k], puz[k], (float)h, Ex, Ey, Ez, Bx, By, Bz);
           const float dtg = (float)p.dt * ig;
           pz[k] = __dadd_rn(pz[k], (double)__fmul_rn(dtg, (float)puz[k]));
@@ -692,11 +723,13 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
             drain_queue<kSort, kFast>(p, s_q, qn, lane);
             qn = 0;
           }
-          if (swap) {
+          if (__any_sync(kAll, swap)) {   // rare (cell changes): keep the 16 resets off the common path
+            if (swap) {
 #pragma unroll
-            for (int i = 0; i < kNodes; ++i) accf[i] = 0.f;
-            cur = nkey[k];
-            cur_m = 0;
+              for (int i = 0; i < kNodes; ++i) accf[i] = 0.f;
+              cur = nkey[k];
+              cur_m = 0;
+            }
           }
           if (same || swap) {
             node_accum(az, ax, vsx[k], vsy[k], vsz[k], accf);
@@ -760,6 +793,333 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
       if (fm) drain_queue<kSort, kFast>(p, s_q, __popc(fm), lane);
     }
     // last box run of the lane: warp-uniform fast path (one shared atomic)
+    unsigned tclk = 0;
+    if (kClock && hb >= 0) tclk = (unsigned)min((clock64() - t_last) >> 4, (long long)(1u << 30));
+    const int hb0 = __shfl_sync(kAll, hb, 0);
+    if (__all_sync(kAll, hb == hb0)) {
+      const unsigned tot = __reduce_add_sync(kAll, hn);
+      const unsigned clk = kClock ? __reduce_add_sync(kAll, tclk) : 0u;
+      if (lane == 0 && hb0 >= 0 && tot) {
+        atomicAdd(s_cnt + hb0, tot);
+        if (kClock) atomicAdd(s_clk + hb0, clk);
+      }
+    } else if (hb >= 0 && hn) {
+      atomicAdd(s_cnt + hb, hn);
+      if (kClock) atomicAdd(s_clk + hb, tclk);
+    }
+  }
+
+  push_epilogue<kClock>(p, sh, n, removed, first_out, err, bimin, bimax, bjmin, bjmax, s_cnt,
+                        s_clk);
+}
+
+// ---------------------------------------------------------------------------
+// Pipelined tolerance-mode kernel (LBX_PIC_FAST with the quad copy, the dense
+// plasma path).  Same arithmetic as pic_push_kernel<.., kFast = true> (the
+// tolerance tests hold both), restructured for latency:
+//  * particle loads are bulk copies (cp.async.bulk, one mbarrier per warp)
+//    of 128-particle chunks into a per-warp shared-memory stage; the warp
+//    reads its chunk into registers, then immediately issues the NEXT chunk's
+//    copy, so the HBM latency overlaps the chunk's arithmetic instead of
+//    stalling the first use of the data (ncu, pic_push_kernel fast mode:
+//    11 % of stall samples waiting for the particle loads);
+//  * a per-warp quad window in shared memory: the 6 components' quads of a
+//    4 x 5 block of nodes around the warp's current cell (1.9 KB), reloaded
+//    only when a particle of the warp falls outside it -- a gather is one
+//    LDS.128 per component instead of an LDG that misses L1 15 % of the
+//    time (22 % of stall samples at the interpolation);
+//  * the flush queue is drained after every particle slot (32 entries per
+//    warp instead of 128): the smem budget goes to the stage and the window
+//    while keeping 2 CTAs x 8 warps per SM.
+// Lane L of a chunk owns particles {2L, 2L+1, 64+2L, 64+2L+1}: conflict-free
+// LDS.128 / coalesced STG.128; a lane's run state (current cell, float node
+// sums, box run, clock) persists across the chunks of a unit as before.
+#ifndef LBX_PIC_PIPE
+#define LBX_PIC_PIPE 1                         // 0: fast mode runs pic_push_kernel (A/B builds)
+#endif
+constexpr int kChunk = 128;                    // particles per warp chunk
+constexpr int kChunks = kUnitP / kChunk;       // chunks per warp unit
+constexpr int kQCapP = 64;                     // flush entries per warp (drained every 2 slots)
+constexpr int kWinR = 4, kWinC = 5;            // quad window: rows wi-2..wi+1, cols wj-2..wj+2
+constexpr int kWin = kWinR * kWinC;
+
+struct __align__(16) PipeWarp {
+  double stage[5][kChunk];                     // z x uz ux uy
+  FlushEntry q[kQCapP];
+  float4 win[6][kWin];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// Lane 0: bulk-copy particles [base, base + cnt) of the five arrays into the
+// warp's stage (sizes rounded up to whole 16-byte pairs: arrays have n + 2
+// slots), completion counted on the warp's mbarrier.
+__device__ __forceinline__ void pipe_issue(const PicParams& p, PipeWarp* w, unsigned long long* bar,
+                                           long long base, long long n) {
+  const long long cnt = min((long long)kChunk, n - base);
+  const unsigned bytes = (unsigned)((cnt + 1) & ~1ll) * 8u;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(5u * bytes) : "memory");
+  const double* src[5] = {p.z, p.x, p.uz, p.ux, p.uy};
+#pragma unroll
+  for (int a = 0; a < 5; ++a)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(w->stage[a])), "l"(src[a] + base), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Reload the warp's quad window around cell (ci, cj).
+__device__ __forceinline__ void pipe_window(const PicParams& p, PipeWarp* w, int ci, int cj,
+                                            int lane) {
+  __syncwarp();
+  for (int t = lane; t < 6 * kWin; t += 32) {
+    const int c = t / kWin, r = (t % kWin) / kWinC, k = t % kWinC;
+    const int row = min(max(ci - 2 + r, -1), p.nz - 1), col = min(max(cj - 2 + k, -1), p.nx - 1);
+    w->win[c][r * kWinC + k] = __ldg(p.Q[c] + (row + 1) * p.qpitch + (col + 1));
+  }
+  __syncwarp();
+}
+
+template <bool kClock>
+__global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p) {
+  extern __shared__ __align__(128) unsigned char s_dyn[];
+  PipeWarp* w = reinterpret_cast<PipeWarp*>(s_dyn) + (threadIdx.x >> 5);
+  unsigned* s_cnt = reinterpret_cast<unsigned*>(s_dyn + (size_t)kPW * sizeof(PipeWarp));  // nb
+  unsigned* s_clk = s_cnt + p.nb;                                                         // nb
+  __shared__ PushShared sh;
+  __shared__ unsigned long long s_bar[kPW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long* bar = s_bar + warp;
+  if (lane == 0) mbar_init(bar);
+  push_prologue<kClock>(p, sh, s_cnt, s_clk);     // (its barrier publishes the mbarrier init)
+  const long long n = sh.n;
+  const long long units = (n + kUnitP - 1) / kUnitP;
+  const long long ustride = (long long)gridDim.x * kPW;
+  const float hf = (float)(0.5 * p.qm * p.dt), dtf = (float)p.dt;
+  const float qws = (float)p.qw * p.vscale;
+  unsigned long long removed = 0;
+  long long first_out = LLONG_MAX, err = 0;
+  int bimin = INT_MAX, bimax = INT_MIN, bjmin = INT_MAX, bjmax = INT_MIN;
+  int wi = INT_MIN / 2, wj = INT_MIN / 2;        // window centre (none loaded)
+  unsigned phase = 0;
+  const unsigned lt = (1u << lane) - 1u;
+  // my four slots in a chunk
+  const int slot0 = kG * lane;                  // my slots: kG consecutive particles
+
+  long long u = (long long)blockIdx.x * kPW + warp;
+  if (u < units && lane == 0) pipe_issue(p, w, bar, u * kUnitP, n);
+  for (; u < units; u += ustride) {
+    float accf[kNodes];
+#pragma unroll
+    for (int i = 0; i < kNodes; ++i) accf[i] = 0.f;
+    int cur = -1;
+    unsigned cur_m = 0;
+    int hb = -1;
+    unsigned hn = 0;
+    long long t_last = 0;
+    if (kClock) t_last = clock64();
+#pragma unroll 1
+    for (int c = 0; c < kChunks; ++c) {
+      const long long base = u * kUnitP + (long long)c * kChunk;
+      if (base >= n) break;                      // warp-uniform
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+      double pz[kG], px[kG], puz[kG], pux[kG], puy[kG];
+      {
+        const double2* s2[5];
+#pragma unroll
+        for (int a = 0; a < 5; ++a) s2[a] = reinterpret_cast<const double2*>(w->stage[a]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int o = 2 * lane + h;            // pair index: slots 2o, 2o + 1 (2-way bank conflict)
+          const double2 a0 = s2[0][o], a1 = s2[1][o], a2 = s2[2][o], a3 = s2[3][o], a4 = s2[4][o];
+          pz[2 * h] = a0.x; pz[2 * h + 1] = a0.y;
+          px[2 * h] = a1.x; px[2 * h + 1] = a1.y;
+          puz[2 * h] = a2.x; puz[2 * h + 1] = a2.y;
+          pux[2 * h] = a3.x; pux[2 * h + 1] = a3.y;
+          puy[2 * h] = a4.x; puy[2 * h + 1] = a4.y;
+        }
+      }
+      __syncwarp();                              // stage consumed: refill it now
+      if (lane == 0) {
+        long long nb2 = base + kChunk;
+        if (c + 1 == kChunks || nb2 >= n) nb2 = (u + ustride) * kUnitP;
+        if (nb2 < n) pipe_issue(p, w, bar, nb2, n);
+      }
+      const bool full = base + kChunk <= n;      // warp-uniform: every slot live
+      const int lim = full ? kChunk : (int)(n - base);
+      bool valid[kG], keep[kG];
+      int nkey[kG];
+      float vsx[kG], vsy[kG], vsz[kG];
+#pragma unroll
+      for (int k = 0; k < kG; ++k) {
+        valid[k] = slot0 + k < lim;
+        const Axis az = fast_axis(valid[k] ? pz[k] : 0.5), ax = fast_axis(valid[k] ? px[k] : 0.5);
+        // the window: rows wi-2..wi+1 and cols wj-2..wj+2 hold every quad of
+        // a particle in cells [wi-1, wi+1] x [wj-1, wj+2]
+        const bool hit = !valid[k] || ((unsigned)(az.i - wi + 1) <= 2u && (unsigned)(ax.i - wj + 1) <= 3u);
+        unsigned miss = __ballot_sync(kAll, !hit);
+        if (miss) {   // recentre so the window starts at the warp's lowest row / column, if it then covers the warp
+          const int ci = __reduce_min_sync(kAll, valid[k] ? az.i : INT_MAX) + 1;
+          const int cj = __reduce_min_sync(kAll, valid[k] ? ax.i : INT_MAX) + 1;
+          const bool h2 = !valid[k] || ((unsigned)(az.i - ci + 1) <= 2u && (unsigned)(ax.i - cj + 1) <= 3u);
+          if (__all_sync(kAll, h2)) {
+            wi = ci;
+            wj = cj;
+            pipe_window(p, w, wi, wj, lane);
+            miss = 0u;
+          }
+        }
+        float Ex, Ey, Ez, Bx, By, Bz;
+        if (!miss) {
+          const int rA = (az.i - wi + 2) * kWinC, rH = (az.ih - wi + 2) * kWinC;
+          const int cA = ax.i - wj + 2, cH = ax.ih - wj + 2;
+          Ex = cic_diff(w->win[0][rA + cH], az.f, ax.fh);
+          Ey = cic_diff(w->win[1][rA + cA], az.f, ax.f);
+          Ez = cic_diff(w->win[2][rH + cA], az.fh, ax.f);
+          Bx = cic_diff(w->win[3][rH + cA], az.fh, ax.f);
+          By = cic_diff(w->win[4][rH + cH], az.fh, ax.fh);
+          Bz = cic_diff(w->win[5][rA + cH], az.f, ax.fh);
+        } else {                                 // lanes span more than the window
+          const int pit = p.qpitch;
+          const int rA = (az.i + 1) * pit, rH = (az.ih + 1) * pit, cA = ax.i + 1, cH = ax.ih + 1;
+          Ex = cic_diff(__ldg(p.Q[0] + rA + cH), az.f, ax.fh);
+          Ey = cic_diff(__ldg(p.Q[1] + rA + cA), az.f, ax.f);
+          Ez = cic_diff(__ldg(p.Q[2] + rH + cA), az.fh, ax.f);
+          Bx = cic_diff(__ldg(p.Q[3] + rH + cA), az.fh, ax.f);
+          By = cic_diff(__ldg(p.Q[4] + rH + cH), az.fh, ax.fh);
+          Bz = cic_diff(__ldg(p.Q[5] + rA + cH), az.f, ax.fh);
+        }
+        const float ig = boris_fast(pux[k], puy[k], puz[k], hf, Ex, Ey, Ez, Bx, By, Bz);
+        const float dtg = dtf * ig;
+        pz[k] = __dadd_rn(pz[k], (double)__fmul_rn(dtg, (float)puz[k]));
+        px[k] = __dadd_rn(px[k], (double)__fmul_rn(dtg, (float)pux[k]));
+        // inside iff z, x >= 0 and trunc(z) < nz, trunc(x) < nx (integer extents)
+        const int iz = __double2int_rz(pz[k]), ix = __double2int_rz(px[k]);
+        keep[k] = valid[k] && pz[k] >= 0.0 && px[k] >= 0.0 && iz < p.nz && ix < p.nx;
+        nkey[k] = keep[k] ? iz * p.nx + ix : -1;
+        const float qv = keep[k] ? __fmul_rn(qws, ig) : 0.f;
+        vsx[k] = __fmul_rn(qv, (float)pux[k]);
+        vsy[k] = __fmul_rn(qv, (float)puy[k]);
+        vsz[k] = __fmul_rn(qv, (float)puz[k]);
+      }
+      // store in place (one 32-byte group per array), removed bookkeeping
+      {
+        const long long i = base + slot0;
+        if (full) {
+          stg(p.oz, i, n, pz);
+          stg(p.ox, i, n, px);
+          stg(p.ouz, i, n, puz);
+          stg(p.oux, i, n, pux);
+          stg(p.ouy, i, n, puy);
+        } else if (i < n) {
+          double* dst[5] = {p.oz, p.ox, p.ouz, p.oux, p.ouy};
+          const double* v[5] = {pz, px, puz, pux, puy};
+#pragma unroll
+          for (int a = 0; a < 5; ++a)
+#pragma unroll
+            for (int k = 0; k < kG; ++k)
+              if (i + k < n) __stcs(dst[a] + i + k, v[a][k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kG; ++k) {
+        if (valid[k] && !keep[k]) {
+          const long long d = base + slot0 + k;
+          ++removed;
+          first_out = min(first_out, d);
+          if (p.removed_list) {
+            const unsigned long long s = atomicAdd(&p.st->removed_count, 1ull);
+            if ((long long)s < p.removed_cap) p.removed_list[s] = d;
+          }
+        }
+      }
+      // current: register runs per lane, queue drained after every 2 slots.
+      // A particle in another cell than the lane's run is queued alone unless
+      // the next slot is in that cell too (then the run moves); the chunk's
+      // last slot has no look-ahead and always counts as a straggler, so a
+      // particle that drifted across a face does not flip the run twice.
+      int qn = 0;
+#pragma unroll
+      for (int k = 0; k < kG; ++k) {
+        const bool dep = nkey[k] >= 0;
+        const Axis az = fast_axis(dep ? pz[k] : 0.5), ax = fast_axis(dep ? px[k] : 0.5);
+        const bool same = dep && nkey[k] == cur;
+        const bool strag = dep && !same && cur >= 0 && (k + 1 == kG || nkey[k + 1] != nkey[k]);
+        const bool swap = dep && !same && !strag;
+        const bool need = strag || (swap && cur >= 0);
+        const unsigned fm = __ballot_sync(kAll, need);
+        if (fm) {
+          if (need) {
+            FlushEntry* e = w->q + qn + __popc(fm & lt);
+            if (strag) {
+              float t[kNodes];
+#pragma unroll
+              for (int i = 0; i < kNodes; ++i) t[i] = 0.f;
+              node_accum(az, ax, vsx[k], vsy[k], vsz[k], t);
+              enqueue_f(e, t, nkey[k], 1u);
+            } else {
+              enqueue_f(e, accf, cur, cur_m);
+            }
+          }
+          qn += __popc(fm);
+        }
+        if ((k & 1) && qn) {
+          drain_queue<false, true>(p, w->q, qn, lane);
+          qn = 0;
+        }
+        if (__any_sync(kAll, swap)) {
+          if (swap) {
+#pragma unroll
+            for (int i = 0; i < kNodes; ++i) accf[i] = 0.f;
+            cur = nkey[k];
+            cur_m = 0;
+          }
+        }
+        if (same || swap) {
+          node_accum(az, ax, vsx[k], vsy[k], vsz[k], accf);
+          ++cur_m;
+        }
+        if (!dep) continue;
+        bimin = min(bimin, az.i);
+        bimax = max(bimax, az.i);
+        bjmin = min(bjmin, ax.i);
+        bjmax = max(bjmax, ax.i);
+        const int bz = az.i >> p.log2m, bx = ax.i >> p.log2m;
+        if (bz >= p.nbz || bx >= p.nbx) {
+          ++err;
+        } else if (bz * p.nbx + bx == hb) {
+          ++hn;
+        } else {
+          if (hb >= 0) {
+            atomicAdd(s_cnt + hb, hn);
+            if (kClock) {
+              const long long t = clock64();
+              atomicAdd(s_clk + hb, (unsigned)min((t - t_last) >> 4, (long long)(1u << 30)));
+              t_last = t;
+            }
+          }
+          hb = bz * p.nbx + bx;
+          hn = 1;
+        }
+      }
+    }
+    {   // end of the unit: queue the lane's open cell, drain
+      const unsigned fm = __ballot_sync(kAll, cur >= 0);
+      if (cur >= 0) enqueue_f(w->q + __popc(fm & lt), accf, cur, cur_m);
+      if (fm) drain_queue<false, true>(p, w->q, __popc(fm), lane);
+    }
     unsigned tclk = 0;
     if (kClock && hb >= 0) tclk = (unsigned)min((clock64() - t_last) >> 4, (long long)(1u << 30));
     const int hb0 = __shfl_sync(kAll, hb, 0);
@@ -1398,7 +1758,8 @@ __global__ void pic_fill_done_kernel(DevState* st, long long cap) {
 __global__ void pic_quad_kernel(const float* __restrict__ F0, const float* __restrict__ F1,
                                 const float* __restrict__ F2, const float* __restrict__ F3,
                                 const float* __restrict__ F4, const float* __restrict__ F5,
-                                float4* Q, long long quads, int qpitch, int pitch, int* dep_box) {
+                                float4* Q, long long quads, int qpitch, int pitch, int* dep_box,
+                                int diff) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     dep_box[0] = INT_MAX;
     dep_box[1] = INT_MIN;
@@ -1411,9 +1772,15 @@ __global__ void pic_quad_kernel(const float* __restrict__ F0, const float* __res
     const int qi = (int)(o / qpitch), qj = (int)(o - (long long)qi * qpitch);
     const long long g = (long long)qi * pitch + qj;
 #pragma unroll
-    for (int c = 0; c < 6; ++c)
-      __stcg(Q + c * quads + o, make_float4(__ldg(F[c] + g), __ldg(F[c] + g + 1),
-                                            __ldg(F[c] + g + pitch), __ldg(F[c] + g + pitch + 1)));
+    for (int c = 0; c < 6; ++c) {
+      const float a = __ldg(F[c] + g), b = __ldg(F[c] + g + 1), d0 = __ldg(F[c] + g + pitch),
+                  d1 = __ldg(F[c] + g + pitch + 1);
+      // diff (LBX_PIC_FAST): (a, b - a, c - a, a - b - c + d) for cic_diff
+      __stcg(Q + c * quads + o,
+             diff ? make_float4(a, __fsub_rn(b, a), __fsub_rn(d0, a),
+                                __fadd_rn(__fsub_rn(a, b), __fsub_rn(d1, d0)))
+                  : make_float4(a, b, d0, d1));
+    }
   }
 }
 
@@ -2205,7 +2572,8 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   if ((a->flags & LBX_PIC_DIRECT) || tiled) quad = false;
   pic_quad_kernel<<<quad ? qg : 1, 256, 0, s>>>(a->fields[0], a->fields[1], a->fields[2],
                                                  a->fields[3], a->fields[4], a->fields[5], Q,
-                                                 quad ? quads : 0, p.qpitch, pitch, dep_box);
+                                                 quad ? quads : 0, p.qpitch, pitch, dep_box,
+                                                 (a->flags & LBX_PIC_FAST) ? 1 : 0);
   const bool clock = (a->flags & LBX_STEP_CLOCK) != 0;
   const bool fast = (a->flags & LBX_PIC_FAST) != 0;
   size_t smem = (size_t)kPW * kQCap * sizeof(FlushEntry) + (size_t)nb * 8;
@@ -2220,6 +2588,9 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
     p.jn_stride = jn_stride;
     p.ntx = ntx;
     p.ntiles = ntz * ntx;
+  } else if (fast && quad && LBX_PIC_PIPE) {
+    smem = (size_t)kPW * sizeof(PipeWarp) + (size_t)nb * 8;
+    kern = clock ? pic_pipe_kernel<true> : pic_pipe_kernel<false>;
   } else if (fast)
     kern = clock ? (quad ? pic_push_kernel<true, false, true, true> : pic_push_kernel<true, false, false, true>)
                  : (quad ? pic_push_kernel<false, false, true, true> : pic_push_kernel<false, false, false, true>);

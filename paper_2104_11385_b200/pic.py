@@ -61,15 +61,23 @@ class PicState:
         return {k: v.cpu().numpy() for k, v in self.fields.items()}
 
 
-def pic_sort(ctx: Context, st: PicState, tiled: bool = False):
+def pic_sync(ctx: Context, st: PicState) -> int:
+    """After steps / sorts run with sync=False: wait for the device and read
+    the particle count back into st.n."""
+    st.n = ctx.count()
+    return st.n
+
+
+def pic_sort(ctx: Context, st: PicState, tiled: bool = False, sync: bool = True):
     """Counting sort of the particles by cell (lbx_pic_sort) into the spare
     buffers, which the state then swaps in.  Every few in-place steps this
     restores the cell order the deposit's register runs feed on.  tiled=True
     sorts by a tile-major key and records the tile ranges that
-    pic_step(tiled=True) works on."""
+    pic_step(tiled=True) works on.  sync=False: as pic_step(sync=False)."""
     dev = ctx.device
     names = ("z", "x", "uz", "ux", "uy")
-    ctx.set_count(st.n)
+    if sync:
+        ctx.set_count(st.n)
     cap = st.z.numel()
     if st.spare is None or st.spare[0].numel() != cap:
         st.spare = tuple(torch.zeros(cap, dtype=torch.float64, device=dev) for _ in names)
@@ -89,7 +97,7 @@ def pic_sort(ctx: Context, st: PicState, tiled: bool = False):
 
 def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times_w: float,
              dt: float, weights=(0.75, 0.25), clock=False, field_solve=True, sort=False,
-             gather=None, stable=False, tiled=False, fast=False, shape_order=0):
+             gather=None, stable=False, tiled=False, fast=False, shape_order=0, sync=True):
     """One PIC step; returns per-box counts / cost / clock and n.
 
     sort=False: in place; absorbed particles' slots are filled from the tail
@@ -107,7 +115,11 @@ def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times
     shape_order=1..3 (in place): charge-conserving Esirkepov deposition
     with B-spline shapes of that order and the same-order gather (the
     paper's order 3); tolerance mode, checked against
-    oracle/pic_oracle.py esirkepov_current (tests/test_gpu_pic_esirkepov.py)."""
+    oracle/pic_oracle.py esirkepov_current (tests/test_gpu_pic_esirkepov.py).
+    sync=False: no host round trip -- the device keeps the particle count
+    from the previous step / sort on this context (st.n stays an upper
+    bound), nothing is read back and None is returned; pic_sync() ends such
+    a sequence.  Back-to-back steps then time the device alone."""
     dev = ctx.device
     nbz, nbx = st.nz // box_size, st.nx // box_size
     nb = nbz * nbx
@@ -115,7 +127,8 @@ def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times
     cost = torch.empty(nb, dtype=torch.float64, device=dev)
     clk = torch.zeros(nb, dtype=torch.int64, device=dev)
     nout = torch.zeros(2, dtype=torch.int64, device=dev)
-    ctx.set_count(st.n)
+    if sync:
+        ctx.set_count(st.n)
     a = _lib.PicArgs()
     a.z, a.x, a.uz, a.ux, a.uy = (_lib.ptr(getattr(st, k)) for k in ("z", "x", "uz", "ux", "uy"))
     for i, k in enumerate(FIELD_NAMES):
@@ -168,6 +181,8 @@ def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times
         ctx._pic_sorted = (weakref.ref(st), st.z._version)
     else:
         ctx._pic_sorted = None
+    if not sync:
+        return None
     h = nout.cpu().numpy()
     if h[1]:
         raise ValueError(f"{int(h[1])} particles fell outside the box grid")
