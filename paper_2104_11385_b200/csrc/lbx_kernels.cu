@@ -1083,6 +1083,230 @@ __global__ void __launch_bounds__(kBlock, kMode == kCompactSoA ? 2 : 3) scan_ker
 }
 
 // ---------------------------------------------------------------------------
+// Stable compaction without a look-back chain (COMPACT_SOA, the default):
+//   compact_count_kernel  survivors per 2,048-particle tile from the first
+//                         absorbed tile on (reads z, x: 16 B / particle);
+//   compact_scan_kernel   one CTA: exclusive scan of the tile counts -> each
+//                         tile's first output slot;
+//   compact_move_kernel   tiles in ticket order: load (8-byte lane-consecutive
+//                         loads), rank survivors by ballot, store them at the
+//                         tile's slot (consecutive survivors -> coalesced
+//                         stores).  In place: a tile's output range lies in
+//                         the input of the same or earlier tiles, so it first
+//                         waits for those tiles' "loaded" flags (status words,
+//                         epoch-tagged like the look-back's).
+// ncu of the look-back kernel on a leaver-heavy step (100 M particles, 0.33 %
+// absorbed anywhere): 2.19 ms, warps stalled at the CTA barrier 23 per issue
+// while warp 0 walked the look-back -- no loads in flight meanwhile.
+// 80 B / particle instead of 64, all of it streaming.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool compact_range(const DevState* st, long long* n, long long* tile0) {
+  const unsigned long long lv = *((volatile const unsigned long long*)&st->leavers);
+  if (!lv) return false;
+  *n = *((volatile const long long*)&st->n_old);
+  *tile0 = (*((volatile const long long*)&st->first_leaver)) / kTile;
+  return true;
+}
+
+// CTA c counts the survivors of a contiguous tile range and writes each
+// tile's exclusive prefix within the range plus the range total.
+__global__ void __launch_bounds__(kBlock) compact_count_kernel(ScanParams p,
+                                                               unsigned long long* tile_cnt,
+                                                               unsigned long long* cta_tot) {
+  long long n, tile0;
+  if (!compact_range(p.st, &n, &tile0)) return;
+  const long long m = (n + kTile - 1) / kTile - tile0;
+  const long long per = (m + gridDim.x - 1) / gridDim.x;
+  const long long a = min(m, (long long)blockIdx.x * per), b = min(m, a + per);
+  __shared__ int s_w[2][kWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned long long run = 0;
+  for (long long j = a; j < b; ++j) {
+    const long long base = (tile0 + j) * kTile;
+    int c = 0;
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+      const long long i = base + r * kBlock + tid;
+      if (i < n) c += inside(__ldcg(p.z + i), __ldcg(p.x + i), p.ez, p.ex) ? 1 : 0;
+    }
+    c = __reduce_add_sync(kFull, c);
+    if (lane == 0) s_w[j & 1][warp] = c;
+    __syncthreads();   // (double-buffered s_w: one barrier per tile)
+    int tot = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) tot += s_w[j & 1][w];
+    if (tid == 0) tile_cnt[j] = run;
+    run += (unsigned long long)tot;
+  }
+  if (tid == 0) cta_tot[blockIdx.x] = run;
+}
+
+// One CTA: exclusive scan of the CTA range totals (in place, <= kScanT
+// entries) plus tile0's slot, and the grand total in cta_tot[G].
+constexpr int kScanT = 1024;
+__global__ void __launch_bounds__(kScanT) compact_scan_kernel(const DevState* st,
+                                                               unsigned long long* cta_tot,
+                                                               int g) {
+  long long n, tile0;
+  if (!compact_range(st, &n, &tile0)) return;
+  __shared__ unsigned long long s_ws[kScanT / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned long long v = threadIdx.x < g ? cta_tot[threadIdx.x] : 0ull;
+  unsigned long long inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_ws[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long wv = s_ws[lane];
+    unsigned long long w = wv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(kFull, w, o);
+      if (lane >= o) w += y;
+    }
+    s_ws[lane] = w - wv;
+  }
+  __syncthreads();
+  const unsigned long long excl = s_ws[warp] + inc - v;
+  if (threadIdx.x < g) cta_tot[threadIdx.x] = (unsigned long long)(tile0 * kTile) + excl;
+  if (threadIdx.x == g - 1) cta_tot[g] = (unsigned long long)(tile0 * kTile) + excl + v;  // survivors
+}
+
+// 512 threads x 4 rows per tile: ~64 registers, 2 CTAs = 32 warps per SM
+// (256 x 8 at 128 registers left 16 warps, mostly parked at the barriers).
+constexpr int kMB = 512, kMW = kMB / 32, kMI = kTile / kMB;
+template <int kKick>   // extra arrays moved along: 0, 1 (kvz) or 2 (kvz, kvx)
+__global__ void __launch_bounds__(kMB, 2) compact_move_kernel(ScanParams p,
+                                                                 const unsigned long long* tile_cnt,
+                                                                 const unsigned long long* cta_base,
+                                                                 int g) {
+  __shared__ long long s_tile;
+  __shared__ int s_last;
+  __shared__ int s_off[kMI * kMW];
+  long long n, tile0;
+  if (!compact_range(p.st, &n, &tile0)) return;
+  const unsigned epoch = *((volatile unsigned*)&p.st->epoch);
+  const long long ntiles = (n + kTile - 1) / kTile;
+  const long long per = (ntiles - tile0 + g - 1) / g;   // compact_count_kernel's ranges
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = lanemask_lt();
+  while (true) {
+    if (tid == 0) s_tile = tile0 + (long long)atomicAdd(&p.st->ticket, 1ull);
+    __syncthreads();
+    const long long t = s_tile;
+    if (t >= ntiles) break;
+    const long long base = t * kTile;
+    double z[kMI], x[kMI], vz[kMI], vx[kMI], kz[kKick ? kMI : 1], kx[kKick > 1 ? kMI : 1];
+    bool keep[kMI];
+    unsigned long long dep = 0;
+#pragma unroll
+    for (int r = 0; r < kMI; ++r) {
+      const long long i = base + r * kMB + tid;
+      z[r] = -1.0;
+      x[r] = -1.0;
+      vz[r] = vx[r] = 0.0;
+      if (kKick) kz[r] = 0.0;
+      if (kKick > 1) kx[r] = 0.0;
+      if (i < n) {
+        z[r] = __ldcs(p.z + i);
+        x[r] = __ldcs(p.x + i);
+        vz[r] = __ldcs(p.vz + i);
+        vx[r] = __ldcs(p.vx + i);
+        if (kKick) kz[r] = __ldcs(p.kvz + i);
+        if (kKick > 1) kx[r] = __ldcs(p.kvx + i);
+      }
+      keep[r] = inside(z[r], x[r], p.ez, p.ex);
+      dep ^= (unsigned long long)__double_as_longlong(vz[r]) ^
+             (unsigned long long)__double_as_longlong(vx[r]);
+      if (kKick) dep ^= (unsigned long long)__double_as_longlong(kz[r]);
+      if (kKick > 1) dep ^= (unsigned long long)__double_as_longlong(kx[r]);
+      const unsigned b = __ballot_sync(kFull, keep[r]);
+      if (lane == 0) s_off[r * kMW + warp] = __popc(b);
+    }
+    // every load of this tile has landed (the barrier's predicate consumes
+    // them all): publish "loaded" so later tiles may overwrite this input
+    const int any = __syncthreads_or((int)(dep == 0x9e3779b97f4a7c15ull));
+    if (tid == 0) {
+      __threadfence();
+      st_release(p.status + t, pack_status(epoch, kFlagAgg, (unsigned long long)(any & 1)));
+    }
+    const long long out = (long long)(cta_base[(t - tile0) / per] + tile_cnt[t - tile0]);
+    if (warp == 0) {
+      // exclusive offsets of the (row, warp) survivor groups, row-major
+      constexpr int kPer = kMI * kMW / 32;
+      int v[kPer], sum = 0;
+#pragma unroll
+      for (int e = 0; e < kPer; ++e) {
+        v[e] = s_off[lane * kPer + e];
+        sum += v[e];
+      }
+      int inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += y;
+      }
+      int off = inc - sum;
+#pragma unroll
+      for (int e = 0; e < kPer; ++e) {
+        s_off[lane * kPer + e] = off;
+        off += v[e];
+      }
+      // wait until every earlier tile whose input this tile's output covers
+      // has loaded (tiles before tile0 are never rewritten)
+      const long long first = max(tile0, out / kTile);
+      for (long long w0 = first; w0 < t; w0 += 32) {
+        const long long w = w0 + lane;
+        if (w < t) {
+          unsigned long long s;
+          do {
+            s = ld_acquire(p.status + w);
+          } while ((unsigned)(s >> kEpochShift) != epoch);
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kMI; ++r) {
+      const unsigned b = __ballot_sync(kFull, keep[r]);
+      if (keep[r]) {
+        const long long d = out + s_off[r * kMW + warp] + __popc(b & lt);
+        if (d != base + r * kMB + tid) {   // in place where nothing moved
+          __stcs(p.z + d, z[r]);
+          __stcs(p.x + d, x[r]);
+          __stcs(p.vz + d, vz[r]);
+          __stcs(p.vx + d, vx[r]);
+          if (kKick) __stcs(p.kvz + d, kz[r]);
+          if (kKick > 1) __stcs(p.kvx + d, kx[r]);
+        }
+      }
+    }
+    __syncthreads();   // s_off / s_tile reuse
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(&p.st->done, 1u) == gridDim.x - 1) ? 1 : 0;
+  __syncthreads();
+  if (!s_last || tid != 0) return;
+  __threadfence();
+  // invariant: the tiles' survivors add up to the push's count
+  const long long n_new = (long long)cta_base[g];
+  p.st->leavers = 0ull;
+  p.st->first_leaver = LLONG_MAX;
+  if (*((volatile long long*)&p.st->n) != n_new) p.st->err += 1ll << 40;
+  p.st->ticket = 0ull;
+  p.st->done = 0u;
+  const unsigned ne = (epoch + 1u) & kEpochMask;
+  p.st->epoch = ne ? ne : 1u;
+  __threadfence();
+}
+
+// ---------------------------------------------------------------------------
 // drop-in bin_particles, heuristic cost, state init
 // ---------------------------------------------------------------------------
 
@@ -1452,6 +1676,33 @@ int launch_stream_any(lbx_ctx* ctx, const StepParams& p, bool clock, bool pow2, 
               : launch_stream<false, false, kExch, kPush>(ctx, p, s);
 }
 
+#ifndef LBX_COMPACT_LOOKBACK
+#define LBX_COMPACT_LOOKBACK 0   // 1: the single-pass look-back compaction (A/B)
+#endif
+// count -> scan -> move (each kernel exits at once when nothing was absorbed)
+int launch_compact3(lbx_ctx* ctx, const ScanParams& p, cudaStream_t s) {
+  unsigned long long* tiles = ctx->status + ctx->status_tiles;
+  const long long ntiles = std::max(1ll, (long long)((ctx->n_upper + kTile - 1) / kTile));
+  // count CTAs: <= kScanT - 1 ranges (one scan CTA), a few per SM
+  const int cg = (int)std::max(1ll, std::min({(long long)ctx->num_sms * 4, ntiles,
+                                              (long long)kScanT - 1}));
+  unsigned long long* cta = tiles + ctx->status_tiles;   // [cg + 1]
+  compact_count_kernel<<<cg, kBlock, 0, s>>>(p, tiles, cta);
+  compact_scan_kernel<<<1, kScanT, 0, s>>>(p.st, cta, cg);
+  if (!p.kvz && p.kvx) return set_error(LBX_EINVAL, "compaction: kvx without kvz");
+  auto kern = p.kvx ? compact_move_kernel<2> : (p.kvz ? compact_move_kernel<1> : compact_move_kernel<0>);
+  int per_sm = 0;
+  cudaError_t e0 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMB, 0);
+  if (e0 != cudaSuccess) return cuda_fail(e0, "occupancy query");
+  long long grid = (long long)std::max(per_sm, 1) * ctx->num_sms;
+  if (ctx->grid_override > 0) grid = ctx->grid_override;
+  grid = std::max(1ll, std::min(grid, ntiles));
+  kern<<<(unsigned)grid, kMB, 0, s>>>(p, tiles, cta, cg);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "compaction launch");
+  return LBX_OK;
+}
+
 template <int kMode>
 int launch_scan(lbx_ctx* ctx, const ScanParams& p, long long n_upper, cudaStream_t s) {
   auto kern = scan_kernel<kMode>;
@@ -1470,11 +1721,13 @@ int reserve_status(lbx_ctx* ctx, int64_t capacity) {
   const int64_t tiles = (capacity + kTile - 1) / kTile + 1;
   if (tiles <= ctx->status_tiles) return LBX_OK;
   unsigned long long* s = nullptr;
-  cudaError_t e = cudaMalloc(&s, (size_t)tiles * sizeof(unsigned long long));
+  // [tiles] status words, [tiles] compaction tile prefixes, [kScanT] range totals
+  const size_t words = (size_t)tiles * 2 + 1024;
+  cudaError_t e = cudaMalloc(&s, words * sizeof(unsigned long long));
   if (e != cudaSuccess)
     return set_error(LBX_EOOM, "look-back workspace: %s", cudaGetErrorString(e));
   // Epoch 0 is never current, so zeroed words read as "not yet published".
-  e = cudaMemset(s, 0, (size_t)tiles * sizeof(unsigned long long));
+  e = cudaMemset(s, 0, words * sizeof(unsigned long long));
   if (e != cudaSuccess) {
     cudaFree(s);
     return cuda_fail(e, "cudaMemset");
@@ -1611,7 +1864,11 @@ int launch_compact(lbx_ctx* ctx, double* z, double* x, double* a, double* b, dou
   p.ex = ex;
   p.st = ctx->st;
   p.status = ctx->status;
+#if LBX_COMPACT_LOOKBACK
   return launch_scan<kCompactSoA>(ctx, p, ctx->n_upper, (cudaStream_t)stream);
+#else
+  return launch_compact3(ctx, p, (cudaStream_t)stream);
+#endif
 }
 
 int launch_timers_sort(const double* z, const double* x, long long n, double m, int nbz, int nbx,
@@ -1744,7 +2001,11 @@ int launch_push_step(lbx_ctx* ctx, const StepLaunch& a, void* stream,
   c.ex = a.ex;
   c.st = ctx->st;
   c.status = ctx->status;
+#if LBX_COMPACT_LOOKBACK
   return launch_scan<kCompactSoA>(ctx, c, ctx->n_upper, s);
+#else
+  return launch_compact3(ctx, c, s);
+#endif
 }
 
 }  // namespace lbx

@@ -161,3 +161,29 @@ def test_fused_step_non_power_of_two_boxes(m):
     assert np.array_equal(out["cost"], O.heuristic_cost(c2, np.full(nb1 * nb1, m * m), 0.02, 0.98))
     gp, gv = st.to_numpy()
     assert np.array_equal(gp, p2) and np.array_equal(gv, v2)
+
+
+@pytest.mark.parametrize("ctas", [0, 3])
+def test_compaction_large_shift_and_late_first_leaver(ctas):
+    """Stable compaction (count -> scan -> move, in place): nothing absorbed
+    before index 1.2 M (first absorbed tile > 0), a block of 300 k absorbed
+    particles (every later tile's output lands ~146 tiles back, so tiles wait
+    for those tiles' "loaded" flags), then sparse absorption; with the
+    occupancy grid and with 3 CTAs cycling through the tickets."""
+    from paper_2104_11385_b200 import device
+    n, ext, m = 3_000_000, 96.0, 16.0
+    rng = np.random.default_rng(11)
+    pos = rng.uniform(1.0, ext - 1.0, size=(n, 2))
+    vel = np.zeros((n, 2))
+    vel[1_200_000:1_500_000, 0] = 200.0
+    tail = 1_500_000 + np.flatnonzero(rng.random(n - 1_500_000) < 0.01)
+    vel[tail, 1] = -200.0
+    st = device.ParticleState.from_numpy(pos, vel)
+    ctx = device.Context(capacity=n)
+    if ctas:
+        ctx.set_grid(ctas)
+    out = device.push_step(ctx, st, ext, ext, m, 6, 6, (0.75, 0.25))
+    p2, v2 = O.advance_particles(pos, vel, ext, ext)
+    assert out["n"] == p2.shape[0] == n - 300_000 - tail.size
+    gp, gv = st.to_numpy()
+    assert np.array_equal(gp, p2) and np.array_equal(gv, v2)
