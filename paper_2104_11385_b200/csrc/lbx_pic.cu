@@ -167,6 +167,11 @@ __device__ __forceinline__ void red_add32(unsigned* a, unsigned v) {
 #ifndef LBX_PIC_LDQ
 #define LBX_PIC_LDQ ".L1::no_allocate"
 #endif
+__device__ __forceinline__ double ld_na(const double* a) {
+  double v;
+  asm volatile("ld.global" LBX_PIC_LDQ ".f64 %0, [%1];" : "=d"(v) : "l"(a));
+  return v;
+}
 // kG consecutive doubles [i, i+kG): one vector streaming load (256-bit for
 // kG = 4) when the group is complete, else clamped scalar loads (tail lanes
 // reload a live particle).
@@ -900,7 +905,7 @@ __device__ __forceinline__ void pipe_window(const PicParams& p, PipeWarp* w, int
 
 template <bool kClock>
 __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p) {
-  extern __shared__ __align__(128) unsigned char s_dyn[];
+  extern __shared__ __align__(16) unsigned char s_dyn[];
   // warp index and count through a shuffle: warp-uniform for the compiler,
   // so the bulk copies' operands live in uniform registers
   const int warp = __shfl_sync(kAll, (int)(threadIdx.x >> 5), 0);
@@ -1946,58 +1951,99 @@ constexpr int kEB = 256;
 #endif
 constexpr int kEskRun = LBX_ESK_RUN;     // 32-particle iterations per warp chunk
 
-// branchless: both pieces evaluated, selected (no divergence in the
-// unrolled window loops)
-template <int K>
-__device__ __forceinline__ float bspline(float d) {
-  const float a = fabsf(d);
-  if (K == 1) return fmaxf(__fsub_rn(1.f, a), 0.f);
-  if (K == 2) {
-    const float b = fmaxf(__fsub_rn(1.5f, a), 0.f);
-    return a <= 0.5f ? __fsub_rn(0.75f, a * a) : 0.5f * b * b;
-  }
-  const float b = fmaxf(__fsub_rn(2.f, a), 0.f);
-  const float inner = __fmaf_rn(a * a, __fmaf_rn(0.5f, a, -1.f), 2.f / 3.f);
-  return a <= 1.f ? inner : b * b * b * (1.f / 6.f);
-}
-
 // lowest node with a possibly nonzero weight: floor(v - (K+1)/2) + 1
 template <int K>
 __device__ __forceinline__ int shape_base(double v) {
   return __double2int_rd(v - 0.5 * (K + 1)) + 1;
 }
 
+// The K+1 nonzero weights of a position v, closed form: base = the lowest
+// node (shape_base), u = frac(v - (K+1)/2) in [0, 1); w[k] = S_K(base + k - v)
+// (K = 3: (1-u)^3/6, (3u^3 - 6u^2 + 4)/6, 1 - the others, u^3/6).  One
+// evaluation per axis instead of one branchless piecewise polynomial per node.
 template <int K>
-__device__ __forceinline__ float gather_shaped(const float* __restrict__ F, int pitch, int nzg,
-                                               int nxg, double zp, double xp) {
-  const int bz = shape_base<K>(zp), bx = shape_base<K>(xp);
-  const float tz = __double2float_rn(zp - (double)bz), tx = __double2float_rn(xp - (double)bx);
-  float wx[K + 1];
-  int cx[K + 1];
-#pragma unroll
-  for (int l = 0; l <= K; ++l) {
-    const int c = bx + l + 1;
-    const bool ok = c >= 0 && c < nxg;
-    wx[l] = ok ? bspline<K>((float)l - tx) : 0.f;
-    cx[l] = ok ? c : 0;
+__device__ __forceinline__ int bweights(double v, float w[K + 1]) {
+  const double q = v - 0.5 * (K + 1);
+  const double fl = floor(q);
+  const float u = __double2float_rn(q - fl);
+  if (K == 1) {
+    w[0] = __fsub_rn(1.f, u);
+    w[1] = u;
+  } else if (K == 2) {
+    const float h = __fsub_rn(u, 0.5f);
+    w[0] = 0.5f * __fsub_rn(1.f, u) * __fsub_rn(1.f, u);
+    w[1] = __fmaf_rn(-h, h, 0.75f);
+    w[2] = 0.5f * u * u;
+  } else {
+    const float v1 = __fsub_rn(1.f, u), u2 = u * u, u3 = u2 * u;
+    w[0] = v1 * v1 * v1 * (1.f / 6.f);
+    w[1] = __fmaf_rn(u2, __fmaf_rn(0.5f, u, -1.f), 2.f / 3.f);
+    w[3] = u3 * (1.f / 6.f);
+    w[2] = __fsub_rn(__fsub_rn(__fsub_rn(1.f, w[0]), w[1]), w[3]);
   }
+  return (int)fl + 1;
+}
+
+// Row-quad gather: R[(r + 1) * rpitch + (c + 1)] = the padded field values
+// (r, c .. c + 3) (zeros outside the array), so a shape-K gather is K + 1
+// 16-byte loads instead of (K + 1)^2 scalar loads.
+template <int K>
+__device__ __forceinline__ float gather_rows(const float4* __restrict__ R, int rpitch, int bz,
+                                             const float wz[K + 1], int bx,
+                                             const float wx[K + 1]) {
+  const float4* q = R + (long long)(bz + 2) * rpitch + (bx + 2);   // padded row bz + 1, col bx + 1
   float acc = 0.f;
 #pragma unroll
   for (int k = 0; k <= K; ++k) {
-    const int r = bz + k + 1;
-    if (r < 0 || r >= nzg) continue;
-    const float wz = bspline<K>((float)k - tz);
-    const float* row = F + (long long)r * pitch;
-    float rs = 0.f;
-#pragma unroll
-    for (int l = 0; l <= K; ++l) rs = __fmaf_rn(wx[l], __ldg(row + cx[l]), rs);
-    acc = __fmaf_rn(wz, rs, acc);
+    const float4 v = __ldg(q + (long long)k * rpitch);
+    float rs = wx[0] * v.x;
+    rs = __fmaf_rn(wx[1], v.y, rs);
+    if (K >= 2) rs = __fmaf_rn(wx[2], v.z, rs);
+    if (K >= 3) rs = __fmaf_rn(wx[3], v.w, rs);
+    acc = __fmaf_rn(wz[k], rs, acc);
   }
   return acc;
 }
 
+// Esirkepov's common-window shape of one position: its K+1 weights placed
+// at window nodes o .. o + K (o = its base - the window base, 0 or 1).
+template <int K>
+__device__ __forceinline__ void window_shape(double v, int wbase, float S[K + 2]) {
+  float w[K + 1];
+  const int o = bweights<K>(v, w) - wbase;
+#pragma unroll
+  for (int k = 0; k < K + 2; ++k)
+    S[k] = o ? (k >= 1 ? w[k - 1] : 0.f) : (k <= K ? w[k] : 0.f);
+}
+
+__global__ void esk_rows_kernel(const float* __restrict__ F0, const float* __restrict__ F1,
+                                const float* __restrict__ F2, const float* __restrict__ F3,
+                                const float* __restrict__ F4, const float* __restrict__ F5,
+                                float4* R, int nz, int nx) {
+  const int rp = nx + 5, pitch = nx + 2;
+  const long long rows = (long long)(nz + 5) * rp;
+  const float* F[6] = {F0, F1, F2, F3, F4, F5};
+  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < rows;
+       o += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(o / rp) - 1, c = (int)(o % rp) - 1;   // padded field indices
+    const bool rok = r >= 0 && r <= nz + 1;
+#pragma unroll
+    for (int comp = 0; comp < 6; ++comp) {
+      float v[4];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        const int cc = c + l;
+        v[l] = (rok && cc >= 0 && cc <= nx + 1) ? __ldg(F[comp] + (long long)r * pitch + cc) : 0.f;
+      }
+      __stcg(R + comp * rows + o, make_float4(v[0], v[1], v[2], v[3]));
+    }
+  }
+}
+
 struct EskParams {
   PicParams b;                  // particles, fields F[], grid, boxes, status, outputs
+  const float4* R[6];           // row-quad field copies [(nz+5) x (nx+5)]
+  int rpitch;
   unsigned long long* J;        // [3][stride] padded node sums (Jx, Jy, Jz)
   long long stride;
   int apitch;                   // nx + 2 kEskG
@@ -2005,10 +2051,77 @@ struct EskParams {
   float cy;                     // q w * scale          (Jy, times vy)
 };
 
+// Add a warp's held block (pic_esk_kernel): node t's 32 lane sums (read
+// rotated: conflict-free), zeroed, rounded to fixed point, one RED each.
+// Out of line: the rare path keeps its registers off the particle loop.
+template <int K>
+__device__ __noinline__ void esk_flush(const EskParams& e, float* acc, int hbz, int hbx, int lane) {
+  constexpr int W = K + 2, W1 = W + 1, NZE = (K + 2) * W1, NE = 2 * NZE + W1 * W1;
+  __syncwarp();
+  const long long h0 = (long long)(hbz - 1 + kEskG) * e.apitch + (hbx - 1 + kEskG);
+  for (int t = lane; t < NE; t += 32) {
+    float sum = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      float* a = acc + t * 32 + ((k + lane) & 31);
+      sum += *a;
+      *a = 0.f;
+    }
+    int comp, di, dj;
+    float scale;
+    if (t < NZE) {
+      comp = 2; di = t / W1; dj = t % W1; scale = e.cz;
+    } else if (t < 2 * NZE) {
+      comp = 0; di = (t - NZE) / (K + 2); dj = (t - NZE) % (K + 2); scale = e.cz;
+    } else {
+      comp = 1; di = (t - 2 * NZE) / W1; dj = (t - 2 * NZE) % W1; scale = e.cy;
+    }
+    const long long v = __float2ll_rn(sum * scale);
+    if (v) red_add(e.J + comp * e.stride + h0 + (long long)di * e.apitch + dj, v);
+  }
+  __syncwarp();
+}
+
+// One particle's fixed-point Esirkepov values straight to HBM (a lane
+// outside its warp's held block).
+template <int K>
+__device__ __noinline__ void esk_direct(const EskParams& e, int bz, int bx, const float* s0z,
+                                        const float* dsz, const float* s0x, const float* dsx,
+                                        float uyg) {
+  constexpr int W = K + 2;
+  const long long r0 = (long long)(bz + kEskG) * e.apitch + (bx + kEskG);
+  const float cz = e.cz, cy = e.cy * uyg;
+  for (int j = 0; j < W; ++j) {
+    const float hx = __fmaf_rn(0.5f, dsx[j], s0x[j]);
+    float a = 0.f;
+    for (int ii = 0; ii <= K; ++ii) {
+      a = __fmaf_rn(dsz[ii], hx, a);
+      const int v = __float2int_rn(cz * a);
+      if (v) red_add(e.J + 2 * e.stride + r0 + (long long)ii * e.apitch + j, v);
+    }
+  }
+  for (int ii = 0; ii < W; ++ii) {
+    const float hz = __fmaf_rn(0.5f, dsz[ii], s0z[ii]);
+    float a = 0.f;
+    for (int j = 0; j <= K; ++j) {
+      a = __fmaf_rn(dsx[j], hz, a);
+      const int v = __float2int_rn(cz * a);
+      if (v) red_add(e.J + r0 + (long long)ii * e.apitch + j, v);
+    }
+  }
+  for (int ii = 0; ii < W; ++ii) {
+    const float a0 = __fmaf_rn(0.5f, dsz[ii], s0z[ii]);
+    const float a1 = __fmaf_rn(1.f / 3.f, dsz[ii], 0.5f * s0z[ii]);
+    for (int j = 0; j < W; ++j) {
+      const int v = __float2int_rn(cy * __fmaf_rn(a1, dsx[j], a0 * s0x[j]));
+      if (v) red_add(e.J + e.stride + r0 + (long long)ii * e.apitch + j, v);
+    }
+  }
+}
+
 template <int K, bool kClock>
 __global__ void __launch_bounds__(kEB, 2) pic_esk_kernel(EskParams e) {
   constexpr int W = K + 2;                 // window nodes per axis
-  constexpr int NJ = (K + 1) * W;          // Jz (or Jx) nonzero prefix values
   const PicParams& p = e.b;
   extern __shared__ __align__(16) unsigned char s_dyn[];
   unsigned* s_cnt = reinterpret_cast<unsigned*>(s_dyn);
@@ -2019,46 +2132,27 @@ __global__ void __launch_bounds__(kEB, 2) pic_esk_kernel(EskParams e) {
   const long long n = sh.n;
   const double ez = (double)p.nz, ex = (double)p.nx;
   const float hf = (float)(0.5 * p.qm * p.dt), dtf = (float)p.dt;
-  const int nzg = p.nz + 2, nxg = p.nx + 2;
   unsigned long long removed = 0;
   long long first_out = LLONG_MAX, err = 0;
-  // A warp takes chunks of kEskRun x 32 consecutive particles.  While its
-  // 32-particle window stays the same (dense, cell-sorted plasma) the warp
-  // sums each node value over the warp (redux.sync) into registers -- lane l
-  // keeps values l, l+32, l+64 -- and adds them to HBM only when the window
-  // changes or the chunk ends: one RED per node per run instead of one per
-  // node per particle (hot nodes of a dense cell would serialise in L2).
-  constexpr int NS = (2 * NJ + W * W + 31) / 32;
-  int hold[NS];
-#pragma unroll
-  for (int q = 0; q < NS; ++q) hold[q] = 0;
-  int hbz = INT_MIN, hbx = 0;
+  // A warp takes chunks of kEskRun x 32 consecutive particles and holds a
+  // node block in shared memory: every lane keeps its own float sums
+  // (acc[node][lane], conflict-free) of the Esirkepov values of its
+  // particles whose window base lies within one node below the held window
+  // (the particles of a dense, cell-sorted plasma, incl. those that moved a
+  // face down); the block is summed over the lanes, rounded to fixed point
+  // and added to HBM only when most of the warp's particles leave it
+  // (recentre) and at the end of the chunk.  Lanes outside it add their own
+  // fixed-point values directly.  (Round 2; replaces a redux.sync per node
+  // per particle: 1,000 of 1,600 instructions per particle, ncu.)
+  constexpr int W1 = W + 1;
+  constexpr int NZE = (K + 2) * W1;        // Jz (and Jx) extended block
+  constexpr int NE = 2 * NZE + W1 * W1;    // + Jy
+  float* acc = reinterpret_cast<float*>(s_dyn + (size_t)p.nb * 8) + (size_t)warp * NE * 32;
+  for (int t = lane; t < NE * 32; t += 32) acc[t] = 0.f;
+  __syncwarp();
+  int hbz = INT_MIN / 2, hbx = INT_MIN / 2;   // held window (block origin: hbz - 1, hbx - 1)
   auto flush = [&]() {
-    if (hbz == INT_MIN) return;
-    const long long h0 = (long long)(hbz + kEskG) * e.apitch + (hbx + kEskG);
-#pragma unroll
-    for (int q = 0; q < NS; ++q) {
-      const int t = lane + 32 * q;
-      if (t < 2 * NJ + W * W && hold[q]) {
-        int comp, di, dj;
-        if (t < NJ) {
-          comp = 2;
-          di = t % (K + 1);
-          dj = t / (K + 1);
-        } else if (t < 2 * NJ) {
-          comp = 0;
-          di = (t - NJ) / (K + 1);
-          dj = (t - NJ) % (K + 1);
-        } else {
-          comp = 1;
-          di = (t - 2 * NJ) / W;
-          dj = (t - 2 * NJ) % W;
-        }
-        red_add(e.J + comp * e.stride + h0 + (long long)di * e.apitch + dj, hold[q]);
-      }
-      hold[q] = 0;
-    }
-    hbz = INT_MIN;
+    if (hbz != INT_MIN / 2) esk_flush<K>(e, acc, hbz, hbx, lane);
   };
   const long long chunk = (long long)kEskRun * 32;
   for (long long c0 = ((long long)blockIdx.x * (kEB / 32) + warp) * chunk; c0 < n;
@@ -2069,16 +2163,21 @@ __global__ void __launch_bounds__(kEB, 2) pic_esk_kernel(EskParams e) {
     long long t0 = 0;
     if (kClock) t0 = clock64();
     const long long ic = valid ? i : n - 1;
-    const double z0 = __ldcs(p.z + ic), x0 = __ldcs(p.x + ic);
-    double uz = __ldcs(p.uz + ic), ux = __ldcs(p.ux + ic), uy = __ldcs(p.uy + ic);
+    // particle loads bypass L1 (the row-quad gathers live there)
+    const double z0 = ld_na(p.z + ic), x0 = ld_na(p.x + ic);
+    double uz = ld_na(p.uz + ic), ux = ld_na(p.ux + ic), uy = ld_na(p.uy + ic);
     // staggers: (0, 1/2) Ex Bz | (0, 0) Ey | (1/2, 0) Ez Bx | (1/2, 1/2) By
-    const double zh = z0 - 0.5, xh = x0 - 0.5;
-    const float Ex = gather_shaped<K>(p.F[0], p.pitch, nzg, nxg, z0, xh);
-    const float Ey = gather_shaped<K>(p.F[1], p.pitch, nzg, nxg, z0, x0);
-    const float Ez = gather_shaped<K>(p.F[2], p.pitch, nzg, nxg, zh, x0);
-    const float Bx = gather_shaped<K>(p.F[3], p.pitch, nzg, nxg, zh, x0);
-    const float By = gather_shaped<K>(p.F[4], p.pitch, nzg, nxg, zh, xh);
-    const float Bz = gather_shaped<K>(p.F[5], p.pitch, nzg, nxg, z0, xh);
+    // weights of the four stagger positions, once each
+    float wz0[K + 1], wzh[K + 1], wx0[K + 1], wxh[K + 1];
+    const int bz0 = bweights<K>(z0, wz0), bzh = bweights<K>(z0 - 0.5, wzh);
+    const int bx0 = bweights<K>(x0, wx0), bxh = bweights<K>(x0 - 0.5, wxh);
+    const int rp = e.rpitch;
+    const float Ex = gather_rows<K>(e.R[0], rp, bz0, wz0, bxh, wxh);
+    const float Ey = gather_rows<K>(e.R[1], rp, bz0, wz0, bx0, wx0);
+    const float Ez = gather_rows<K>(e.R[2], rp, bzh, wzh, bx0, wx0);
+    const float Bx = gather_rows<K>(e.R[3], rp, bzh, wzh, bx0, wx0);
+    const float By = gather_rows<K>(e.R[4], rp, bzh, wzh, bxh, wxh);
+    const float Bz = gather_rows<K>(e.R[5], rp, bz0, wz0, bxh, wxh);
     const float ig = boris_fast(ux, uy, uz, hf, Ex, Ey, Ez, Bx, By, Bz);
     const float dtg = dtf * ig;
     const double z1 = __dadd_rn(z0, (double)__fmul_rn(dtg, (float)uz));
@@ -2101,50 +2200,34 @@ __global__ void __launch_bounds__(kEB, 2) pic_esk_kernel(EskParams e) {
     }
     // ---- Esirkepov weights on the common window ----
     const int bz = shape_base<K>(fmin(z0, z1)), bx = shape_base<K>(fmin(x0, x1));
-    const float t0z = __double2float_rn(z0 - (double)bz), t1z = __double2float_rn(z1 - (double)bz);
-    const float t0x = __double2float_rn(x0 - (double)bx), t1x = __double2float_rn(x1 - (double)bx);
     float s0z[W], dsz[W], s0x[W], dsx[W];
+    window_shape<K>(z0, bz, s0z);
+    window_shape<K>(z1, bz, dsz);
+    window_shape<K>(x0, bx, s0x);
+    window_shape<K>(x1, bx, dsx);
 #pragma unroll
     for (int k = 0; k < W; ++k) {
-      s0z[k] = bspline<K>((float)k - t0z);
-      dsz[k] = __fsub_rn(bspline<K>((float)k - t1z), s0z[k]);
-      s0x[k] = bspline<K>((float)k - t0x);
-      dsx[k] = __fsub_rn(bspline<K>((float)k - t1x), s0x[k]);
+      dsz[k] = __fsub_rn(dsz[k], s0z[k]);
+      dsx[k] = __fsub_rn(dsx[k], s0x[k]);
     }
-    const float cz = keep ? e.cz : 0.f;
-    const float cy = keep ? e.cy * __fmul_rn((float)uy, ig) : 0.f;
-    // ---- add: warp-uniform window -> each node summed over the warp
-    // (redux.sync) and added by one lane; otherwise per lane ----
-    // the warp's most common window (match_any groups, largest wins): its
-    // lanes' values are summed over the warp into the held registers; the
-    // other lanes (particles that crossed a cell face downwards) add theirs
+    const float uyg = __fmul_rn((float)uy, ig);     // Jy's velocity factor
     const unsigned km = __ballot_sync(kAll, keep);
-    const unsigned key = keep ? ((unsigned)(bz + kEskG) << 16) | (unsigned)(bx + kEskG) : 0xffffffffu;
-    const unsigned grp = __match_any_sync(kAll, key);
-    const int gsize = keep ? __popc(grp) : 0;
-    const int gmax = __reduce_max_sync(kAll, gsize);
-    const unsigned cand = __ballot_sync(kAll, gsize == gmax && keep);
-    const int lead = cand ? __ffs(cand) - 1 : 0;
-    const int lbz = __shfl_sync(kAll, bz, lead), lbx = __shfl_sync(kAll, bx, lead);
-    const bool ing = keep && bz == lbz && bx == lbx;
-    const bool uni = gmax > 1;                // warp-uniform decision
-    const long long r0 = (long long)(bz + kEskG) * e.apitch + (bx + kEskG);
-    if (km && uni && (lbz != hbz || lbx != hbx)) {   // window change: add the held sums
+    const int lead = km ? __ffs(km) - 1 : 0;
+    bool inb = keep && (unsigned)(bz - hbz + 1) <= 1u && (unsigned)(bx - hbx + 1) <= 1u;
+    if (km && 2 * __popc(__ballot_sync(kAll, inb)) < __popc(km)) {
+      // most kept particles outside the held block: add it, hold the block
+      // whose upper window is the warp's highest (covers that and one below)
       flush();
-      hbz = lbz;
-      hbx = lbx;
+      hbz = __reduce_max_sync(kAll, keep ? bz : INT_MIN);
+      hbx = __reduce_max_sync(kAll, keep ? bx : INT_MIN);
+      inb = keep && (unsigned)(bz - hbz + 1) <= 1u && (unsigned)(bx - hbx + 1) <= 1u;
     }
-    auto emit = [&](int t, int comp, int di, int dj, int val) {
-      if (uni) {
-        const int r = __reduce_add_sync(kAll, ing ? val : 0);
-        if (lane == (t & 31)) hold[t >> 5] += r;
-        if (!ing && val) red_add(e.J + comp * e.stride + r0 + (long long)di * e.apitch + dj, val);
-      } else if (val) {
-        red_add(e.J + comp * e.stride + r0 + (long long)di * e.apitch + dj, val);
-      }
-    };
-    if (km) {
-      // Jz at (bz + i + 1/2, bx + j): prefix over i of dsz_i (s0x_j + dsx_j / 2)
+    if (inb) {
+      // unscaled values into this lane's slots at the block offset (oz, ox)
+      const int oz = bz - hbz + 1, ox = bx - hbx + 1;
+      float* az = acc + (oz * W1 + ox) * 32 + lane;
+      float* ax = acc + (NZE + oz * (K + 2) + ox) * 32 + lane;
+      float* ay = acc + (2 * NZE + oz * W1 + ox) * 32 + lane;
 #pragma unroll
       for (int j = 0; j < W; ++j) {
         const float hx = __fmaf_rn(0.5f, dsx[j], s0x[j]);
@@ -2152,10 +2235,9 @@ __global__ void __launch_bounds__(kEB, 2) pic_esk_kernel(EskParams e) {
 #pragma unroll
         for (int ii = 0; ii <= K; ++ii) {
           a = __fmaf_rn(dsz[ii], hx, a);
-          emit(j * (K + 1) + ii, 2, ii, j, __float2int_rn(cz * a));
+          az[(ii * W1 + j) * 32] += a;
         }
       }
-      // Jx at (bz + i, bx + j + 1/2): prefix over j of dsx_j (s0z_i + dsz_i / 2)
 #pragma unroll
       for (int ii = 0; ii < W; ++ii) {
         const float hz = __fmaf_rn(0.5f, dsz[ii], s0z[ii]);
@@ -2163,18 +2245,18 @@ __global__ void __launch_bounds__(kEB, 2) pic_esk_kernel(EskParams e) {
 #pragma unroll
         for (int j = 0; j <= K; ++j) {
           a = __fmaf_rn(dsx[j], hz, a);
-          emit(NJ + ii * (K + 1) + j, 0, ii, j, __float2int_rn(cz * a));
+          ax[(ii * (K + 2) + j) * 32] += a;
         }
       }
-      // Jy at (bz + i, bx + j)
 #pragma unroll
       for (int ii = 0; ii < W; ++ii) {
-        const float a0 = __fmaf_rn(0.5f, dsz[ii], s0z[ii]);               // s0z + dsz/2
-        const float a1 = __fmaf_rn(1.f / 3.f, dsz[ii], 0.5f * s0z[ii]);   // s0z/2 + dsz/3
+        const float a0 = __fmul_rn(uyg, __fmaf_rn(0.5f, dsz[ii], s0z[ii]));             // s0z + dsz/2
+        const float a1 = __fmul_rn(uyg, __fmaf_rn(1.f / 3.f, dsz[ii], 0.5f * s0z[ii])); // s0z/2 + dsz/3
 #pragma unroll
-        for (int j = 0; j < W; ++j)
-          emit(2 * NJ + ii * W + j, 1, ii, j, __float2int_rn(cy * __fmaf_rn(a1, dsx[j], a0 * s0x[j])));
+        for (int j = 0; j < W; ++j) ay[(ii * W1 + j) * 32] += __fmaf_rn(a1, dsx[j], a0 * s0x[j]);
       }
+    } else if (keep) {   // outside the block: this particle's values straight to HBM
+      esk_direct<K>(e, bz, bx, s0z, dsz, s0x, dsx, uyg);
     }
     // ---- per-box survivor counts (+ GpuClock: the particle's whole work) ----
     int box = -1;
@@ -2342,6 +2424,25 @@ int pic_step_esirkepov(lbx_ctx* ctx, const lbx_pic_args* a, cudaStream_t s) {
   p.wp = a->w_particle;
   p.wc = a->w_cell;
   p.cells = (double)a->box_size * (double)a->box_size;
+  const long long rows = (long long)(a->nz + 5) * (a->nx + 5);
+  if (!ctx->pic_quad || ctx->pic_quads < rows) {
+    if (ctx->pic_quad) {
+      cudaDeviceSynchronize();
+      cudaFree(ctx->pic_quad);
+    }
+    ctx->pic_quad = nullptr;
+    if (cudaMalloc(&ctx->pic_quad, (size_t)rows * 6 * sizeof(float4)) != cudaSuccess)
+      return set_error(LBX_EOOM, "PIC row-quad field buffer");
+    ctx->pic_quads = rows;
+  }
+  float4* R = static_cast<float4*>(ctx->pic_quad);
+  for (int c = 0; c < 6; ++c) e.R[c] = R + c * rows;
+  e.rpitch = a->nx + 5;
+  {
+    const unsigned rg = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 8, (rows + 255) / 256));
+    esk_rows_kernel<<<rg, 256, 0, s>>>(a->fields[0], a->fields[1], a->fields[2], a->fields[3],
+                                       a->fields[4], a->fields[5], R, a->nz, a->nx);
+  }
   e.J = ctx->pic_esk;
   e.stride = stride;
   e.apitch = apitch;
@@ -2355,7 +2456,8 @@ int pic_step_esirkepov(lbx_ctx* ctx, const lbx_pic_args* a, cudaStream_t s) {
     case 3: kern = clock ? pic_esk_kernel<3, true> : pic_esk_kernel<3, false>; break;
     default: return set_error(LBX_EINVAL, "shape_order must be 0 (CIC direct) or 1, 2, 3");
   }
-  const size_t smem = (size_t)nb * 8;
+  const int W1 = K + 3, NE = 2 * (K + 2) * W1 + W1 * W1;   // pic_esk_kernel's per-warp block
+  const size_t smem = (size_t)nb * 8 + (size_t)(kEB / 32) * NE * 32 * sizeof(float);
   if (smem > 48 * 1024) {
     cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ea != cudaSuccess) return cuda_fail(ea, "cudaFuncSetAttribute(esk)");
