@@ -10,8 +10,12 @@ CASES_D='tests/test_gpu_dist.py -k "mini-2 and p2p"'
 CASES_E='tests/test_gpu_3d.py tests/test_gpu_pic.py -k "3d or hole_filling or (multi_step and direct) or gpuclock or timers"'
 CASES_R='tests/test_gpu_runs.py -k "(timers and not cupti) or gpuclock or (graph_replay and mini)"'
 CASES_S='tests/test_gpu_pic.py -k "periodic_cell_sort or share_a_state or reused_buffers or tiled"'
+# round 2: pipelined tolerance kernel, Esirkepov, count/scan/move compaction
+CASES_F='tests/test_gpu_pic_fast.py -k "quad"'
+CASES_Q='tests/test_gpu_pic_esirkepov.py -k "first_step or absorbing"'
+CASES_C='tests/test_gpu_kernels.py -k "compaction_large_shift or (fused_step_matches_oracle and 300001)"'
 for tool in ${SAN_TOOLS:-memcheck racecheck synccheck}; do
-  for grp in ${SAN_GROUPS:-K P D E R S}; do
+  for grp in ${SAN_GROUPS:-K P D E R S F Q C}; do
     eval cases=\$CASES_$grp
     eval timeout 1500 compute-sanitizer --tool $tool --error-exitcode 99 --target-processes all \
       python -m pytest $cases -x -q -p no:cacheprovider > gpurun_out/sanitize_${tool}_$grp.log 2>&1
