@@ -22,6 +22,8 @@ launch stream:
   push_deposit_fast     in place, tolerance mode (LBX_PIC_FAST: float32
                         Boris increment, FMA gathers);
   push_deposit_fast_resort  the same with lbx_pic_sort every --resort steps;
+  push_deposit_fast_tiled   tolerance mode on the tiled path (tile-major sort
+                        every --resort steps; sparse plasmas);
   push_deposit_esk1/esk3  charge-conserving Esirkepov deposition with shape
                         order 1 / 3 (the paper's order) and
                         same-order gather, in place (+ _resort: cell sort
@@ -110,6 +112,7 @@ def main():
                                    ("push_deposit_tiled", False, False, True),
                                    ("push_deposit_fast", False, False, True),
                                    ("push_deposit_fast_resort", False, False, True),
+                                   ("push_deposit_fast_tiled", False, False, True),
                                    ("push_deposit_esk1", False, False, True),
                                    ("push_deposit_esk3", False, False, True),
                                    ("push_deposit_esk3_resort", False, False, True),
@@ -120,10 +123,10 @@ def main():
         for name, t in init.items():
             setattr(st, name, t.clone())
         st.n = n
-        resort = mode in ("push_deposit_resort", "push_deposit_tiled",
+        resort = mode in ("push_deposit_resort", "push_deposit_tiled", "push_deposit_fast_tiled",
                           "push_deposit_fast_resort") or mode.endswith("esk3_resort")
         order = 3 if "esk3" in mode else (1 if "esk1" in mode else 0)
-        tiled = mode == "push_deposit_tiled"
+        tiled = mode in ("push_deposit_tiled", "push_deposit_fast_tiled")
         fast = mode.startswith("push_deposit_fast")
         if resort:   # start cell-ordered, like the other modes' first sorted step
             pic.pic_sort(ctx, st, tiled=tiled)

@@ -1221,10 +1221,12 @@ __device__ __forceinline__ int patch_at(int P, int Q, int tz, int tx) {
   return (P - tz + kGd) * kPP + (Q - tx + kGd);
 }
 
+template <bool kFast = false>
 __device__ __forceinline__ float gather_s(const float* s_f, int c, int i0, int j0, float fz,
                                           float fx, int tz, int tx) {
   const float* F = s_f + c * kPatch + patch_at(i0 + 1, j0 + 1, tz, tx);
-  return cic(make_float4(F[0], F[1], F[kPP], F[kPP + 1]), fz, fx);
+  const float4 q = make_float4(F[0], F[1], F[kPP], F[kPP + 1]);
+  return kFast ? cic_fast(q, fz, fx) : cic(q, fz, fx);
 }
 
 // Exact node sums from two fire-and-forget 32-bit shared atomics:
@@ -1282,7 +1284,9 @@ __device__ __forceinline__ void stg_mask(double* a, long long i, long long lo, l
   }
 }
 
-template <bool kClock>
+// kFast: tolerance mode (LBX_PIC_FAST | LBX_PIC_TILED): fast_axis, FMA gathers,
+// float32 Boris increment, float run sums (rounded to fixed point at the queue).
+template <bool kClock, bool kFast = false>
 __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_tile_kernel(PicParams p) {
   extern __shared__ __align__(16) unsigned char s_dyn[];
   FlushEntry* s_q = reinterpret_cast<FlushEntry*>(s_dyn) + (size_t)(threadIdx.x >> 5) * kQCapT;
@@ -1344,8 +1348,12 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_tile_kernel(PicParams p
     for (long long w = a0 + (long long)warp * 32 * run; w < hi; w += (long long)kPW * 32 * run) {
       const long long run0 = w + (long long)lane * run;
       int acc[kNodes];
+      float accf[kNodes];
 #pragma unroll
-      for (int i = 0; i < kNodes; ++i) acc[i] = 0;
+      for (int i = 0; i < kNodes; ++i) {
+        acc[i] = 0;
+        accf[i] = 0.f;
+      }
       int cur = -1, cur_i = 0, cur_j = 0;
       int hb = -1;
       unsigned hn = 0;
@@ -1367,23 +1375,36 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_tile_kernel(PicParams p
 #pragma unroll
         for (int k = 0; k < kG; ++k) {
           const bool valid = i0 + k >= lo && i0 + k < hi;
-          const Axis az = axis_of(pz[k]), ax = axis_of(px[k]);
+          const Axis az = pic_axis<kFast>(pz[k]), ax = pic_axis<kFast>(px[k]);
           float Ex, Ey, Ez, Bx, By, Bz;
           if (in_patch(az.i, ax.i, tz, tx)) {
-            Ex = gather_s(s_f, 0, az.i, ax.ih, az.f, ax.fh, tz, tx);
-            Ey = gather_s(s_f, 1, az.i, ax.i, az.f, ax.f, tz, tx);
-            Ez = gather_s(s_f, 2, az.ih, ax.i, az.fh, ax.f, tz, tx);
-            Bx = gather_s(s_f, 3, az.ih, ax.i, az.fh, ax.f, tz, tx);
-            By = gather_s(s_f, 4, az.ih, ax.ih, az.fh, ax.fh, tz, tx);
-            Bz = gather_s(s_f, 5, az.i, ax.ih, az.f, ax.fh, tz, tx);
+            Ex = gather_s<kFast>(s_f, 0, az.i, ax.ih, az.f, ax.fh, tz, tx);
+            Ey = gather_s<kFast>(s_f, 1, az.i, ax.i, az.f, ax.f, tz, tx);
+            Ez = gather_s<kFast>(s_f, 2, az.ih, ax.i, az.fh, ax.f, tz, tx);
+            Bx = gather_s<kFast>(s_f, 3, az.ih, ax.i, az.fh, ax.f, tz, tx);
+            By = gather_s<kFast>(s_f, 4, az.ih, ax.ih, az.fh, ax.fh, tz, tx);
+            Bz = gather_s<kFast>(s_f, 5, az.i, ax.ih, az.f, ax.fh, tz, tx);
           } else {
-            Ex = gather_c<false>(p, 0, az.i, ax.ih, az.f, ax.fh);
-            Ey = gather_c<false>(p, 1, az.i, ax.i, az.f, ax.f);
-            Ez = gather_c<false>(p, 2, az.ih, ax.i, az.fh, ax.f);
-            Bx = gather_c<false>(p, 3, az.ih, ax.i, az.fh, ax.f);
-            By = gather_c<false>(p, 4, az.ih, ax.ih, az.fh, ax.fh);
-            Bz = gather_c<false>(p, 5, az.i, ax.ih, az.f, ax.fh);
+            Ex = gather_c<false, kFast>(p, 0, az.i, ax.ih, az.f, ax.fh);
+            Ey = gather_c<false, kFast>(p, 1, az.i, ax.i, az.f, ax.f);
+            Ez = gather_c<false, kFast>(p, 2, az.ih, ax.i, az.fh, ax.f);
+            Bx = gather_c<false, kFast>(p, 3, az.ih, ax.i, az.fh, ax.f);
+            By = gather_c<false, kFast>(p, 4, az.ih, ax.ih, az.fh, ax.fh);
+            Bz = gather_c<false, kFast>(p, 5, az.i, ax.ih, az.f, ax.fh);
           }
+          if (kFast) {
+            const float ig = boris_fast(pux[k], puy[k], puz[k], (float)h, Ex, Ey, Ez, Bx, By, Bz);
+            const float dtg = (float)p.dt * ig;
+            pz[k] = __dadd_rn(pz[k], (double)__fmul_rn(dtg, (float)puz[k]));
+            px[k] = __dadd_rn(px[k], (double)__fmul_rn(dtg, (float)pux[k]));
+            const int iz = __double2int_rz(pz[k]), ix = __double2int_rz(px[k]);
+            keep[k] = valid && pz[k] >= 0.0 && px[k] >= 0.0 && iz < p.nz && ix < p.nx;
+            nkey[k] = keep[k] ? iz * p.nx + ix : -1;
+            const float qv = keep[k] ? __fmul_rn((float)p.qw * p.vscale, ig) : 0.f;
+            vsx[k] = __fmul_rn(qv, (float)pux[k]);
+            vsy[k] = __fmul_rn(qv, (float)puy[k]);
+            vsz[k] = __fmul_rn(qv, (float)puz[k]);
+          } else {
           // relativistic Boris (x, y, z order; oracle boris())
           const double hEx = __dmul_rn(h, (double)Ex), hEy = __dmul_rn(h, (double)Ey),
                        hEz = __dmul_rn(h, (double)Ez);
@@ -1417,6 +1438,7 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_tile_kernel(PicParams p
           vsx[k] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, pux[k]), igam)), p.vscale);
           vsy[k] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, puy[k]), igam)), p.vscale);
           vsz[k] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, puz[k]), igam)), p.vscale);
+          }
           if (valid && !keep[k]) {
             ++removed;
             first_out = min(first_out, i0 + k);
@@ -1437,14 +1459,48 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_tile_kernel(PicParams p
 #pragma unroll
         for (int k = 0; k < kG; ++k) {
           const bool dep = nkey[k] >= 0;
-          const Axis az = axis_of(dep ? pz[k] : 0.5), ax = axis_of(dep ? px[k] : 0.5);
-          int q[kNodes];
-          node_values(az, ax, vsx[k], vsy[k], vsz[k], q);
+          const Axis az = pic_axis<kFast>(dep ? pz[k] : 0.5), ax = pic_axis<kFast>(dep ? px[k] : 0.5);
           const bool same = dep && nkey[k] == cur;
           const bool strag = dep && !same && cur >= 0 && k + 1 < kG && nkey[k + 1] != nkey[k];
           const bool swap = dep && !same && !strag;
           const bool need = strag || (swap && cur >= 0);
           const unsigned fm = __ballot_sync(kAll, need);
+          if (kFast) {
+            // float run sums, rounded to fixed point when queued
+            if (need) {
+              int qi[kNodes];
+              if (strag) {
+                float w[kNodes];
+#pragma unroll
+                for (int i = 0; i < kNodes; ++i) w[i] = 0.f;
+                node_accum(az, ax, vsx[k], vsy[k], vsz[k], w);
+#pragma unroll
+                for (int i = 0; i < kNodes; ++i) qi[i] = __float2int_rn(w[i]);
+                enqueue_t(s_q + qn + __popc(fm & lt), qi, az.i, ax.i);
+              } else {
+#pragma unroll
+                for (int i = 0; i < kNodes; ++i) qi[i] = __float2int_rn(accf[i]);
+                enqueue_t(s_q + qn + __popc(fm & lt), qi, cur_i, cur_j);
+              }
+            }
+            qn += __popc(fm);
+            if (kQCapT < 32 * kG && qn > kQCapT - 32) {
+              drain_tile(p, s_q, qn, lane, s_lo, s_hi, tz, tx, dense);
+              qn = 0;
+            }
+            if (__any_sync(kAll, swap)) {
+              if (swap) {
+#pragma unroll
+                for (int i = 0; i < kNodes; ++i) accf[i] = 0.f;
+                cur = nkey[k];
+                cur_i = az.i;
+                cur_j = ax.i;
+              }
+            }
+            if (same || swap) node_accum(az, ax, vsx[k], vsy[k], vsz[k], accf);
+          } else {
+          int q[kNodes];
+          node_values(az, ax, vsx[k], vsy[k], vsz[k], q);
           if (need) {
             if (strag) enqueue_t(s_q + qn + __popc(fm & lt), q, az.i, ax.i);
             else enqueue_t(s_q + qn + __popc(fm & lt), acc, cur_i, cur_j);
@@ -1463,6 +1519,7 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_tile_kernel(PicParams p
             cur = nkey[k];
             cur_i = az.i;
             cur_j = ax.i;
+          }
           }
           if (!dep) continue;
           bimin = min(bimin, az.i);
@@ -1491,6 +1548,10 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_tile_kernel(PicParams p
       }
       {
         const unsigned fm = __ballot_sync(kAll, cur >= 0);
+        if (kFast) {
+#pragma unroll
+          for (int i = 0; i < kNodes; ++i) acc[i] = __float2int_rn(accf[i]);
+        }
         if (cur >= 0) enqueue_t(s_q + __popc(fm & ((1u << lane) - 1u)), acc, cur_i, cur_j);
         if (fm) drain_tile(p, s_q, __popc(fm), lane, s_lo, s_hi, tz, tx, dense);
       }
@@ -2534,8 +2595,8 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   if (!(a->q_times_w != 0.0)) return set_error(LBX_EINVAL, "q_times_w must be nonzero");
   const bool tiled = (a->flags & LBX_PIC_TILED) != 0;
   if (tiled && sorted) return set_error(LBX_EINVAL, "LBX_PIC_TILED runs in place (no out[])");
-  if ((a->flags & LBX_PIC_FAST) && (sorted || tiled))
-    return set_error(LBX_EINVAL, "LBX_PIC_FAST runs in place, untiled");
+  if ((a->flags & LBX_PIC_FAST) && sorted)
+    return set_error(LBX_EINVAL, "LBX_PIC_FAST runs in place");
   if (tiled && (a->flags & LBX_PIC_DEFER_CURRENT))
     return set_error(LBX_EINVAL, "LBX_PIC_TILED does not support LBX_PIC_DEFER_CURRENT");
   if (tiled && (ctx->pic_tiles_nz != a->nz || ctx->pic_tiles_nx != a->nx))
@@ -2694,7 +2755,8 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   if (tiled) {
     smem = (size_t)kPW * kQCapT * sizeof(FlushEntry) + (size_t)6 * kPatch * 4 +
            (size_t)6 * kPatch * 4 + (size_t)nb * 8;
-    kern = clock ? pic_tile_kernel<true> : pic_tile_kernel<false>;
+    kern = fast ? (clock ? pic_tile_kernel<true, true> : pic_tile_kernel<false, true>)
+                : (clock ? pic_tile_kernel<true> : pic_tile_kernel<false>);
     p.tile_rd = ctx->pic_tiles;
     p.Jn = ctx->pic_jn;
     p.jn_stride = jn_stride;

@@ -108,7 +108,7 @@ def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times
     tiled=True: in place, one CTA per 16x16-cell tile with the field patch
     and the current in shared memory, on the tile ranges of the last
     pic_sort(tiled=True) -- the sparse-plasma path.
-    fast=True (in place, untiled): tolerance mode (LBX_PIC_FAST) -- float32
+    fast=True (in place, also tiled): tolerance mode (LBX_PIC_FAST) -- float32
     Boris increment with FMA and MUFU rsqrt/rcp, FMA gathers; agrees with
     the fp64 oracle within the tolerances tests/test_gpu_pic_fast.py states,
     not bit for bit.
@@ -149,8 +149,8 @@ def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times
             raise ValueError("tiled steps run in place (sort=False)")
         a.flags |= _lib.LBX_PIC_TILED
     if fast:
-        if sort or tiled:
-            raise ValueError("fast (tolerance) steps run in place, untiled")
+        if sort:
+            raise ValueError("fast (tolerance) steps run in place")
         a.flags |= _lib.LBX_PIC_FAST
     if shape_order:
         if sort or tiled:
