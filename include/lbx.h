@@ -460,15 +460,23 @@ int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* args, void* stream);
  * are kept for LBX_PIC_TILED steps.  Fields and physics args are ignored. */
 int lbx_pic_sort(lbx_ctx* ctx, const lbx_pic_args* args, void* stream);
 
-/* Multi-GPU PIC (guard-cell current sum): after a LBX_PIC_DEFER_CURRENT step
- * the context holds the step's current as exact integers, cell-centric
+/* Multi-GPU PIC (guard-cell current exchange): after a LBX_PIC_DEFER_CURRENT
+ * step the context holds the step's current as exact integers, cell-centric
  * jc[cells][16] (16 cell-relative nodes, int64 two's complement) over the
  * deposit box box[4] = {row_min, row_max, col_min, col_max} (device).  Ranks
- * all-reduce(sum) jc over the union of their boxes (write the union into
- * box) -- integer sums, so the result is bit-identical to one GPU -- and
- * call lbx_pic_finish (node gather into current[], clear, Yee update with
- * the same args; every rank keeps the full replicated field grid). */
+ * sum the rows of the cells along their shared faces into each other's rows
+ * (integer sums: bit-identical to one GPU in any order), set box to their
+ * region and call lbx_pic_finish (node gather into current[], clear, Yee
+ * update with the same args). */
 int lbx_pic_current_view(lbx_ctx* ctx, uint64_t** jc, int64_t* cells, int32_t** box);
+/* The same for a deferred Esirkepov step (shape_order > 0): node-centric
+ * fixed-point sums j[3][stride], stride = (nz + 2 guard) (nx + 2 guard),
+ * node (i, j) of component c at j[c * stride + (i + guard) (nx + 2 guard)
+ * + (j + guard)]; lbx_pic_finish with shape_order set converts them (all
+ * nodes, cleared) and runs the Yee update.  Replaces the reference's
+ * modelled guard-cell communication (workload.py:324-327) for the paper's
+ * order-3 deposition. */
+int lbx_pic_esk_current_view(lbx_ctx* ctx, uint64_t** j, int64_t* stride, int32_t* guard);
 int lbx_pic_finish(lbx_ctx* ctx, const lbx_pic_args* args, void* stream);
 
 /* ------------------------------------------------------------------------

@@ -155,6 +155,7 @@ SIGNATURES["lbx_peer_free"] = (i32, [vp])
 SIGNATURES["lbx_peer_can_access"] = (i32, [i32, i32, P(i32)])
 SIGNATURES["lbx_pic_finish"] = (i32, [vp, P(PicArgs), vp])
 SIGNATURES["lbx_pic_current_view"] = (i32, [vp, P(vp), P(i64), P(vp)])
+SIGNATURES["lbx_pic_esk_current_view"] = (i32, [vp, P(vp), P(i64), P(i32)])
 SIGNATURES["lbx_sim_set_fields"] = (i32, [vp, vp, vp, vp])
 
 

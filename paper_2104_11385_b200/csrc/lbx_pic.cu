@@ -2396,12 +2396,14 @@ int pic_finish(lbx_ctx* ctx, const lbx_pic_args* a, cudaStream_t s, double jscal
 }
 
 
+int esk_finish(lbx_ctx* ctx, const lbx_pic_args* a, cudaStream_t s);
+
 // Host side of the charge-conserving step (lbx_pic_args::shape_order > 0).
 int pic_step_esirkepov(lbx_ctx* ctx, const lbx_pic_args* a, cudaStream_t s) {
   const int K = a->shape_order;
   if (a->out[0]) return set_error(LBX_EINVAL, "shape_order > 0 runs in place (no out[])");
-  if (a->flags & (LBX_PIC_TILED | LBX_PIC_DEFER_CURRENT))
-    return set_error(LBX_EINVAL, "shape_order > 0 does not support tiled or deferred-current steps");
+  if (a->flags & LBX_PIC_TILED)
+    return set_error(LBX_EINVAL, "shape_order > 0 does not support tiled steps");
   uintptr_t al = (uintptr_t)a->z | (uintptr_t)a->x | (uintptr_t)a->uz | (uintptr_t)a->ux |
                  (uintptr_t)a->uy;
   if (al & 7u) return set_error(LBX_EINVAL, "particle arrays must be 8-byte aligned");
@@ -2542,11 +2544,25 @@ int pic_step_esirkepov(lbx_ctx* ctx, const lbx_pic_args* a, cudaStream_t s) {
   }
   rc = launch_compact(ctx, a->z, a->x, a->uz, a->ux, a->uy, nullptr, (double)a->nz, (double)a->nx, s);
   if (rc) return rc;
+  if (a->flags & LBX_PIC_DEFER_CURRENT) return LBX_OK;   // multi-GPU: sums exchanged first
+  return esk_finish(ctx, a, s);
+}
+
+// Esirkepov node sums -> current arrays (cleared), then the Yee update.
+int esk_finish(lbx_ctx* ctx, const lbx_pic_args* a, cudaStream_t s) {
+  const int apitch = a->nx + 2 * kEskG;
+  const long long stride = (long long)(a->nz + 2 * kEskG) * apitch;
+  if (!ctx->pic_esk || ctx->pic_esk_elems != stride)
+    return set_error(LBX_EINVAL, "lbx_pic_finish without a deferred Esirkepov step on this grid");
+  const double vmax = std::fabs(a->q_times_w) / std::min(a->dt, 1.0);
+  int e2 = 0;
+  std::frexp(1048576.0 / vmax, &e2);
+  const double jscale = std::ldexp(1.0, e2 - 1);
   const unsigned cg = (unsigned)std::max(1ll, std::min((long long)ctx->num_sms * 8, (stride + 255) / 256));
   pic_esk_current_kernel<<<cg, 256, 0, s>>>(ctx->pic_esk, stride, apitch, a->current[0],
                                             a->current[1], a->current[2], a->nz, a->nx,
                                             1.0 / jscale);
-  er = cudaGetLastError();
+  cudaError_t er = cudaGetLastError();
   if (er != cudaSuccess) return cuda_fail(er, "current launch");
   if (a->flags & LBX_PIC_NO_FIELD_SOLVE) return LBX_OK;
   const int pitch = a->nx + 2;
@@ -2873,12 +2889,27 @@ extern "C" int lbx_pic_sort(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
 extern "C" int lbx_pic_finish(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
   clear_error();
   if (!ctx || !a) return set_error(LBX_EINVAL, "NULL argument");
+  if (a->shape_order) {
+    if (!(a->q_times_w != 0.0)) return set_error(LBX_EINVAL, "q_times_w must be nonzero");
+    return esk_finish(ctx, a, (cudaStream_t)stream);
+  }
   if (!ctx->pic_acc || ctx->pic_cells != (long long)a->nz * a->nx)
     return set_error(LBX_EINVAL, "lbx_pic_finish without a deferred lbx_pic_step on this grid");
   if (!(a->q_times_w != 0.0)) return set_error(LBX_EINVAL, "q_times_w must be nonzero");
   int e2 = 0;
   std::frexp(1048576.0 / std::fabs(a->q_times_w), &e2);
   return pic_finish(ctx, a, (cudaStream_t)stream, std::ldexp(1.0, e2 - 1));
+}
+
+extern "C" int lbx_pic_esk_current_view(lbx_ctx* ctx, uint64_t** j, int64_t* stride,
+                                        int32_t* guard) {
+  clear_error();
+  if (!ctx || !j || !stride || !guard) return set_error(LBX_EINVAL, "NULL argument");
+  if (!ctx->pic_esk) return set_error(LBX_EINVAL, "no Esirkepov PIC step has run on this context");
+  *j = reinterpret_cast<uint64_t*>(ctx->pic_esk);
+  *stride = ctx->pic_esk_elems;
+  *guard = kEskG;
+  return LBX_OK;
 }
 
 extern "C" int lbx_pic_current_view(lbx_ctx* ctx, uint64_t** jc, int64_t* cells, int32_t** box) {

@@ -497,11 +497,26 @@ class PicHalo:
     copied over the receiver's stale values.  Bytes per step scale with the
     off-rank faces, not with the grid."""
 
-    def __init__(self, owner, grid_shape, box_size, nz, nx, rank, world, dev):
+    def __init__(self, owner, grid_shape, box_size, nz, nx, rank, world, dev, order=0):
         self.owner = np.asarray(owner, dtype=np.int64).copy()
+        self.order = int(order)
         cells = cell_owner_map(owner, grid_shape, box_size)
-        js, jr = halo_plan(cells, cells, rank, world, 1, 1)
-        fs, fr = halo_plan(cells, cells, rank, world, 0, 2)
+        # field guard ring: the gather reaches one cell (CIC) or `order` - 1
+        # cells (B-spline order K) beyond the particle's cell, the Yee update
+        # of the owned cells one
+        self.guard = max(2, self.order)
+        if self.order:
+            # Esirkepov: node-centric sums on the padded node grid of
+            # lbx_pic_esk_current_view (guard G nodes around the cells; a
+            # padding node belongs to its nearest cell's owner).  A rank's
+            # particles deposit within 4 nodes of their boxes (window base
+            # one node below the cell after a downward move, K + 2 nodes up).
+            G = ESK_GUARD
+            padded = np.pad(cells, G, mode="edge")
+            js, jr = halo_plan(padded, padded, rank, world, self.order + 1, 1)
+        else:
+            js, jr = halo_plan(cells, cells, rank, world, 1, 1)
+        fs, fr = halo_plan(cells, cells, rank, world, 0, self.guard)
         self.j_send_n = [int(a.size) for a in js]
         self.j_recv_n = [int(a.size) for a in jr]
         self.f_send_n = [int(a.size) for a in fs]
@@ -512,16 +527,20 @@ class PicHalo:
         self.f_send = t([pad(a) for a in fs])
         self.f_recv = t([pad(a) for a in fr])
         self.box = torch.tensor(bbox(dilate(cells == rank, 1)), dtype=torch.int32, device=dev)
-        self.bytes_j = 16 * 8 * sum(self.j_send_n)
+        self.bytes_j = (3 if self.order else 16) * 8 * sum(self.j_send_n)
         self.bytes_f = 6 * 4 * sum(self.f_send_n)
 
 
-def field_sync_plan(old_owner, new_owner, grid_shape, box_size, nx, rank, world, dev):
-    """Adoption: every rank's new guard region (own_new grown by 2) from the
-    cells' previous owners (who hold their current values)."""
+ESK_GUARD = 4   # lbx_pic_esk_current_view's guard nodes (kEskG in lbx_pic.cu)
+
+
+def field_sync_plan(old_owner, new_owner, grid_shape, box_size, nx, rank, world, dev,
+                    guard=2):
+    """Adoption: every rank's new guard region (own_new grown by `guard`) from
+    the cells' previous owners (who hold their current values)."""
     old = cell_owner_map(old_owner, grid_shape, box_size)
     new = cell_owner_map(new_owner, grid_shape, box_size)
-    fs, fr = halo_plan(old, new, rank, world, 0, 2)
+    fs, fr = halo_plan(old, new, rank, world, 0, guard)
     pad = lambda c: (c // nx + 1) * (nx + 2) + (c % nx + 1)  # noqa: E731
     t = lambda a: torch.from_numpy(np.concatenate(a)).to(dev)  # noqa: E731
     return (t([pad(a) for a in fs]), [int(a.size) for a in fs], t([pad(a) for a in fr]),
@@ -552,6 +571,13 @@ class PicEngine(DeviceEngine):
         from .workload import PIC_DEFAULTS
         super().__init__(cfg, rank, world, device, pos, kick, capacity, clock)
         self.pic = dict(PIC_DEFAULTS, **(pic or {}))
+        self.order = int(self.pic.get("shape_order", 0))   # 0: CIC; 1-3: Esirkepov
+        # cell-sort the rank's particles every `resort` steps after the kick
+        # (lbx_pic_sort: the deposit's runs / held blocks follow cell order;
+        # emigrant unpacking and hole filling scramble it) -- 0: never
+        self.resort = int(self.pic.get("resort", 0))
+        self._sortbuf = None
+        self._steps = 0
         nz, nx = cfg.domain_extent
         self.nz, self.nx = int(nz), int(nx)
         cap = self.capacity + 2
@@ -581,7 +607,7 @@ class PicEngine(DeviceEngine):
         super().set_owner(owner)
         if self.halo is None or not np.array_equal(owner, self.halo.owner):
             self.halo = PicHalo(owner, (self.nbz, self.nbx), int(self.m), self.nz, self.nx,
-                                self.rank, self.world, self.dev)
+                                self.rank, self.world, self.dev, order=self.order)
 
     def _field_exchange(self, send_idx, sc, recv_idx, rc):
         names = self.field_names
@@ -596,7 +622,8 @@ class PicEngine(DeviceEngine):
     def field_sync(self, old_owner, new_owner):
         """Adoption: the new guard regions' fields from the previous owners."""
         plan = field_sync_plan(old_owner, new_owner, (self.nbz, self.nbx), int(self.m),
-                               self.nx, self.rank, self.world, self.dev)
+                               self.nx, self.rank, self.world, self.dev,
+                               guard=max(2, self.order))
         self._field_exchange(*plan)
 
     def kick(self):
@@ -618,6 +645,7 @@ class PicEngine(DeviceEngine):
         a.q_over_m, a.q_times_w = float(self.pic["q_over_m"]), float(self.pic["q_times_w"])
         a.dt = float(self.pic["dt"])
         a.flags = flags
+        a.shape_order = self.order
         return a
 
     def push(self, wp, wc):
@@ -626,10 +654,33 @@ class PicEngine(DeviceEngine):
         send_counts, nout = self.partition()
         return self.counts, self.clk, send_counts, nout
 
+    def _resort(self, stream):
+        """Counting sort of the rank's particles by cell into the spare
+        buffers, then swap (after the kick: (z, x, uz, ux, uy) is the whole
+        particle record; kvz aliases uy from then on)."""
+        names = ("z", "x", "vz", "vx", "uy")
+        cap = self.z.numel()
+        if self._sortbuf is None or self._sortbuf[0].numel() != cap:
+            self._sortbuf = [torch.zeros(cap, dtype=torch.float64, device=self.dev)
+                             for _ in names]
+        a = self._args(0)
+        for i, t in enumerate(self._sortbuf):
+            a.out[i] = _lib.ptr(t)
+        _lib.check(_lib.lib.lbx_pic_sort(self.ctx.handle, C.byref(a), stream))
+        old = [getattr(self, k) for k in names]
+        for k, t in zip(names, self._sortbuf):
+            setattr(self, k, t)
+        self._sortbuf = old
+        self.kvz = self.uy
+        self.launches += 4   # count, scan reduce, scan apply, scatter
+
     def local_step(self, wp, wc):
         """The rank's particle kernels: PIC step with the current deferred."""
         stream = self.D._stream(self.dev)
         self.ctx.set_count(self.n)
+        if self.resort and self.kicked and self._steps % self.resort == 0 and self.n:
+            self._resort(stream)
+        self._steps += 1
         a = self._args((_lib.LBX_STEP_CLOCK if self.clock else 0) | _lib.LBX_PIC_DEFER_CURRENT)
         a.w_particle, a.w_cell = float(wp), float(wc)
         a.counts_out, a.cost_out, a.clk_out = (_lib.ptr(self.counts), _lib.ptr(self.cost),
@@ -665,7 +716,10 @@ class PicEngine(DeviceEngine):
     def current_sum(self):
         """Integer current rows of the shared-face cells, summed into each
         receiver's rows; the node gather then covers the rank's cells grown
-        by one (every nonzero row lies there)."""
+        by one (every nonzero row lies there).  Esirkepov (shape_order > 0):
+        the node sums near the shared faces, summed into the receivers'."""
+        if self.order:
+            return self._esk_current_sum()
         jc_p, cells, box_p = C.c_void_p(), C.c_int64(), C.c_void_p()
         _lib.check(_lib.lib.lbx_pic_current_view(self.ctx.handle, C.byref(jc_p), C.byref(cells),
                                                  C.byref(box_p)))
@@ -679,6 +733,21 @@ class PicEngine(DeviceEngine):
         box = torch.as_tensor(_DevArray(box_p.value, 4, "<i4"), device=self.dev)
         box.copy_(h.box)
         self.halo_bytes = 16 * 8 * sum(h.j_send_n)
+
+    def _esk_current_sum(self):
+        j_p, stride, guard = C.c_void_p(), C.c_int64(), C.c_int32()
+        _lib.check(_lib.lib.lbx_pic_esk_current_view(self.ctx.handle, C.byref(j_p),
+                                                     C.byref(stride), C.byref(guard)))
+        if guard.value != ESK_GUARD:
+            raise RuntimeError(f"libLBX Esirkepov guard {guard.value} != {ESK_GUARD}")
+        h = self.halo
+        j = torch.as_tensor(_DevArray(j_p.value, 3 * stride.value, "<i8"),
+                            device=self.dev).view(3, -1)
+        send = j.index_select(1, h.j_send).t().contiguous()          # [k, 3]
+        recv = self.comm.exchange_values(send.reshape(-1), [3 * k for k in h.j_send_n],
+                                         [3 * k for k in h.j_recv_n])
+        j.index_add_(1, h.j_recv, recv.view(-1, 3).t())
+        self.halo_bytes = 3 * 8 * sum(h.j_send_n)
 
     def unpack(self, recv: torch.Tensor):
         n0 = self.n

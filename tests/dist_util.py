@@ -281,9 +281,10 @@ class NumpyPicEngine:
         return {k: v.copy() for k, v in self.f.items()}
 
 
-def pic_reference(doc, steps):
+def pic_reference(doc, steps, order=0):
     """Single-process oracle PIC run of a scenario doc (kick -> u = v/dt):
-    per-step per-box counts, final particles and fields."""
+    per-step per-box counts, final particles and fields.  order > 0: the
+    Esirkepov step with B-spline shapes of that order."""
     from oracle import lbsim_oracle as LO
     from oracle import pic_oracle as PO
     from paper_2104_11385_b200 import scenarios as S
@@ -302,7 +303,10 @@ def pic_reference(doc, steps):
     for step in range(cfg.total_steps):
         if step == cfg.kick.step:
             p["uz"], p["ux"] = kick[:, 0] / c["dt"], kick[:, 1] / c["dt"]
-        PO.particle_step(f, p, nz, nx, c["q_over_m"], c["q_times_w"], c["dt"])
+        if order:
+            PO.particle_step_esirkepov(f, p, nz, nx, c["q_over_m"], c["q_times_w"], c["dt"], order)
+        else:
+            PO.particle_step(f, p, nz, nx, c["q_over_m"], c["q_times_w"], c["dt"])
         PO.field_step(f, nz, nx, c["dt"])
         counts.append(LO.bin_particles(np.column_stack([p["z"], p["x"]]), float(cfg.box_size),
                                        nz // cfg.box_size, nx // cfg.box_size))

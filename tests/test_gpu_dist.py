@@ -158,6 +158,68 @@ def test_gpu_distributed_pic_matches_oracle(world):
     assert outs[0][0].summary["adoption_count"] > 0 and sum(o[3].sum() for o in outs) > 0
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_gpu_distributed_pic_esirkepov(world):
+    """Distributed PIC with the paper's order-3 charge-conserving deposition
+    (shape_order 3, ranks cell-sort their particles every 4 steps): each rank defers its node-centric Esirkepov sums, the
+    sums near shared faces are exchanged and added (PicHalo order 3), every
+    rank finishes its region and the guard rings (3 cells) come from their
+    owners.  Against the single-process oracle Esirkepov run (tolerance
+    mode): per-box counts exact, fields on every rank's own cells and the
+    particle multiset within tests/test_gpu_pic_esirkepov.py's tolerances."""
+    from paper_2104_11385_b200 import scenarios as S
+    from paper_2104_11385_b200.parallel import DistributedSimulation, ThreadComm
+    from tests.dist_util import own_cells_mask, pic_reference
+    from tests.test_gpu_pic_esirkepov import F_TOL, U_TOL, X_TOL
+    doc = json.loads((Path(__file__).parent / "golden" / "runs.json").read_text())["_docs"]["small"]
+    steps = 12
+    spec = S.apply_overrides(S.spec_from_dict(doc), ranks=world, steps=steps, interval=3,
+                             threshold=0.0)
+    shared = ThreadComm.shared(world)
+    outs, errs = [None] * world, []
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            sim = DistributedSimulation(spec.scenario, spec.policy, spec.build_provider(),
+                                        comm=ThreadComm(shared, r), device="cuda:0",
+                                        record_counts=True, physics="pic",
+                                        pic={"shape_order": 3, "resort": 4})
+            sim.run()
+            assert sim.engine.order == 3 and sim.engine.halo.guard == 3
+            outs[r] = (sim.result(), sim.engine.state(), sim.engine.field_arrays(),
+                       sim.engine.halo.owner.copy(), sim.engine.halo.bytes_j)
+            sim.close()
+        except Exception as e:
+            errs.append(e)
+            shared["bar"].abort()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    counts, p, f = pic_reference(doc, steps, order=3)
+    nz, nx = doc["domain"]["extent"]
+    box = doc["domain"]["box_size"]
+    for r, (res, _, fa, owner, nbytes) in enumerate(outs):
+        assert np.array_equal(res.count_trace, counts)
+        mine = own_cells_mask(owner, ((nz // box, nx // box), box, nz, nx), r)
+        for k in ("Ex", "Ey", "Ez", "Bx", "By", "Bz"):
+            scale = max(float(np.abs(f[k]).max()), 1e-30)
+            assert np.abs(fa[k][mine] - f[k][mine]).max() / scale <= F_TOL, (r, k)
+        assert 0 < nbytes < 3 * 8 * nz * nx
+    umax = max(float(np.abs(p[k]).max()) for k in ("uz", "ux", "uy"))
+    for k, tol in (("z", X_TOL), ("x", X_TOL), ("uz", U_TOL * umax), ("ux", U_TOL * umax),
+                   ("uy", U_TOL * umax)):
+        got = np.sort(np.concatenate([o[1][k] for o in outs]))
+        assert got.shape == p[k].shape
+        assert np.abs(got - np.sort(p[k])).max() <= tol, k
+    assert outs[0][0].summary["adoption_count"] > 0
+
+
 def test_p2p_failure_on_one_rank_falls_back_to_collectives(monkeypatch):
     """If any rank cannot map peer memory, every rank switches to the
     collective exchange together and the run stays exact."""
