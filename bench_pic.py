@@ -22,6 +22,9 @@ launch stream:
   push_deposit_fast     in place, tolerance mode (LBX_PIC_FAST: float32
                         Boris increment, FMA gathers);
   push_deposit_fast_resort  the same with lbx_pic_sort every --resort steps;
+  push_deposit_fast_resort_noclock / push_deposit_esk3_resort_noclock
+                        the same without the GpuClock tally (overhead =
+                        gpuclock_overhead_<mode>, pipelined step times);
   push_deposit_fast_tiled   tolerance mode on the tiled path (tile-major sort
                         every --resort steps; sparse plasmas);
   push_deposit_esk1/esk3  charge-conserving Esirkepov deposition with shape
@@ -112,10 +115,12 @@ def main():
                                    ("push_deposit_tiled", False, False, True),
                                    ("push_deposit_fast", False, False, True),
                                    ("push_deposit_fast_resort", False, False, True),
+                                   ("push_deposit_fast_resort_noclock", False, False, False),
                                    ("push_deposit_fast_tiled", False, False, True),
                                    ("push_deposit_esk1", False, False, True),
                                    ("push_deposit_esk3", False, False, True),
                                    ("push_deposit_esk3_resort", False, False, True),
+                                   ("push_deposit_esk3_resort_noclock", False, False, False),
                                    ("full_step_esk3_resort", True, False, True)):
         if mode not in args.modes.split(","):
             continue
@@ -124,7 +129,8 @@ def main():
             setattr(st, name, t.clone())
         st.n = n
         resort = mode in ("push_deposit_resort", "push_deposit_tiled", "push_deposit_fast_tiled",
-                          "push_deposit_fast_resort") or mode.endswith("esk3_resort")
+                          "push_deposit_fast_resort", "push_deposit_fast_resort_noclock",
+                          "push_deposit_esk3_resort_noclock") or mode.endswith("esk3_resort")
         order = 3 if "esk3" in mode else (1 if "esk1" in mode else 0)
         tiled = mode in ("push_deposit_tiled", "push_deposit_fast_tiled")
         fast = mode.startswith("push_deposit_fast")
@@ -184,8 +190,11 @@ def main():
         out[mode]["ms_pipelined"] = msp
         out[mode]["frac_of_hbm_peak_pipelined"] = BYTES_PER_PARTICLE * nb2 / (msp / 1e3) / 1e9 / peak
         del st
-    if "push_deposit" in out and "push_deposit_noclock" in out:
-        out["gpuclock_overhead"] = out["push_deposit"]["ms"] / out["push_deposit_noclock"]["ms"] - 1.0
+    for a, b in (("push_deposit", "push_deposit_noclock"),
+                 ("push_deposit_fast_resort", "push_deposit_fast_resort_noclock"),
+                 ("push_deposit_esk3_resort", "push_deposit_esk3_resort_noclock")):
+        if a in out and b in out:   # GpuClock tally in that kernel vs the same kernel without it
+            out[f"gpuclock_overhead_{a}"] = out[a]["ms_pipelined"] / out[b]["ms_pipelined"] - 1.0
     out["peak_gbs"] = peak
     out["peak_source"] = peak_src
     print(json.dumps(out))
