@@ -2181,7 +2181,10 @@ __device__ __noinline__ void esk_direct(const EskParams& e, int bz, int bx, cons
 }
 
 template <int K, bool kClock>
-__global__ void __launch_bounds__(kEB, 2) pic_esk_kernel(EskParams e) {
+#ifndef LBX_ESK_MINB
+#define LBX_ESK_MINB 2
+#endif
+__global__ void __launch_bounds__(kEB, LBX_ESK_MINB) pic_esk_kernel(EskParams e) {
   constexpr int W = K + 2;                 // window nodes per axis
   const PicParams& p = e.b;
   extern __shared__ __align__(16) unsigned char s_dyn[];
