@@ -70,6 +70,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-native", action="store_true",
+                    help="skip the native-size lines (resident multi-step kernel): "
+                         "profiling runs (ncu serialises the kernel's host handshake)")
     ap.add_argument("--force-dist", action="store_true",
                     help="use the multi-GPU box-ownership path even at N=1 (testing)")
     return ap.parse_args()
@@ -401,8 +404,8 @@ def run_lbx(args, rank, world, local_rank):
     torch.cuda.empty_cache()
 
     # ---- the reference's own C2 size (801,499 particles, 1 replica) ----
-    c2n = c2_native(args, dev, spec, sc, pos0, kick0)
-    c1 = c1_uniform(dev) if not args.no_cpu_baseline else None
+    c2n = c2_native(args, dev, spec, sc, pos0, kick0) if not args.no_native else None
+    c1 = c1_uniform(dev) if not (args.no_cpu_baseline or args.no_native) else None
     comp = compaction_leavers(dev) if not args.no_e2e else None
 
     # ---- e2e through the reference-facing C-ABI with host buffers ----
