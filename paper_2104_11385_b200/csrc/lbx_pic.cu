@@ -848,6 +848,42 @@ constexpr int kQCapP = 64;                     // flush entries per warp (draine
 constexpr int kWinR = 4, kWinC = 5;            // quad window: rows wi-2..wi+1, cols wj-2..wj+2
 constexpr int kWin = kWinR * kWinC;
 
+template <bool kFast>
+__device__ __forceinline__ float pipe_cic(const float4 q, float fz, float fx) {
+  return kFast ? cic_diff(q, fz, fx) : cic(q, fz, fx);   // difference quads / raw quads
+}
+
+// The exact relativistic Boris of pic_push_kernel (x, y, z order; oracle
+// boris()): updates u in place, returns 1/gamma(u_new) correctly rounded.
+__device__ __forceinline__ double boris_exact(double& ux, double& uy, double& uz, double h,
+                                              float Ex, float Ey, float Ez, float Bx, float By,
+                                              float Bz) {
+  const double hEx = __dmul_rn(h, (double)Ex), hEy = __dmul_rn(h, (double)Ey),
+               hEz = __dmul_rn(h, (double)Ez);
+  const double mx = __dadd_rn(ux, hEx);
+  const double my = __dadd_rn(uy, hEy);
+  const double mz = __dadd_rn(uz, hEz);
+  const double gg = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(mx, mx)),
+                                                   __dmul_rn(my, my)), __dmul_rn(mz, mz)));
+  const double ig = __drcp_rn(gg);
+  const double tx = __dmul_rn(__dmul_rn(h, (double)Bx), ig);
+  const double ty = __dmul_rn(__dmul_rn(h, (double)By), ig);
+  const double tz = __dmul_rn(__dmul_rn(h, (double)Bz), ig);
+  const double s2 = __dmul_rn(2.0, __drcp_rn(__dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(tx, tx)),
+                                                                 __dmul_rn(ty, ty)),
+                                                       __dmul_rn(tz, tz))));
+  const double qx = __dadd_rn(mx, __dsub_rn(__dmul_rn(my, tz), __dmul_rn(mz, ty)));
+  const double qy = __dadd_rn(my, __dsub_rn(__dmul_rn(mz, tx), __dmul_rn(mx, tz)));
+  const double qz = __dadd_rn(mz, __dsub_rn(__dmul_rn(mx, ty), __dmul_rn(my, tx)));
+  ux = __dadd_rn(__dadd_rn(mx, __dmul_rn(s2, __dsub_rn(__dmul_rn(qy, tz), __dmul_rn(qz, ty)))), hEx);
+  uy = __dadd_rn(__dadd_rn(my, __dmul_rn(s2, __dsub_rn(__dmul_rn(qz, tx), __dmul_rn(qx, tz)))), hEy);
+  uz = __dadd_rn(__dadd_rn(mz, __dmul_rn(s2, __dsub_rn(__dmul_rn(qx, ty), __dmul_rn(qy, tx)))), hEz);
+  const double gam = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(1.0, __dmul_rn(ux, ux)),
+                                                    __dmul_rn(uy, uy)),
+                                          __dmul_rn(uz, uz)));
+  return __drcp_rn(gam);
+}
+
 struct __align__(16) PipeWarp {
   double stage[5][kChunk];                     // z x uz ux uy
   FlushEntry q[kQCapP];
@@ -903,7 +939,9 @@ __device__ __forceinline__ void pipe_window(const PicParams& p, PipeWarp* w, int
   __syncwarp();
 }
 
-template <bool kClock>
+// kFast = false: the exact (bit-exact) step with the same pipeline -- fp64
+// Boris, floor axes, float32 CIC on raw quads, integer node values.
+template <bool kClock, bool kFast = true>
 __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p) {
   extern __shared__ __align__(16) unsigned char s_dyn[];
   // warp index and count through a shuffle: warp-uniform for the compiler,
@@ -923,6 +961,7 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
   const long long ustride = (long long)gridDim.x * kPW;
   const float hf = (float)(0.5 * p.qm * p.dt), dtf = (float)p.dt;
   const float qws = (float)p.qw * p.vscale;
+  const double h = 0.5 * p.qm * p.dt;
   unsigned long long removed = 0;
   long long first_out = LLONG_MAX, err = 0;
   int bimin = INT_MAX, bimax = INT_MIN, bjmin = INT_MAX, bjmax = INT_MIN;
@@ -936,8 +975,12 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
   if (u < units) pipe_issue(p, w, bar, u * kUnitP, n);
   for (; u < units; u += ustride) {
     float accf[kNodes];
+    int acc[kNodes];
 #pragma unroll
-    for (int i = 0; i < kNodes; ++i) accf[i] = 0.f;
+    for (int i = 0; i < kNodes; ++i) {
+      accf[i] = 0.f;
+      acc[i] = 0;
+    }
     int cur = -1;
     unsigned cur_m = 0;
     int hb = -1;
@@ -980,7 +1023,8 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
 #pragma unroll
       for (int k = 0; k < kG; ++k) {
         valid[k] = slot0 + k < lim;
-        const Axis az = fast_axis(valid[k] ? pz[k] : 0.5), ax = fast_axis(valid[k] ? px[k] : 0.5);
+        const Axis az = pic_axis<kFast>(valid[k] ? pz[k] : 0.5),
+                   ax = pic_axis<kFast>(valid[k] ? px[k] : 0.5);
         // the window: rows wi-2..wi+1 and cols wj-2..wj+2 hold every quad of
         // a particle in cells [wi-1, wi+1] x [wj-1, wj+2]
         const bool hit = !valid[k] || ((unsigned)(az.i - wi + 1) <= 2u && (unsigned)(ax.i - wj + 1) <= 3u);
@@ -1000,34 +1044,47 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
         if (!miss) {
           const int rA = (az.i - wi + 2) * kWinC, rH = (az.ih - wi + 2) * kWinC;
           const int cA = ax.i - wj + 2, cH = ax.ih - wj + 2;
-          Ex = cic_diff(w->win[0][rA + cH], az.f, ax.fh);
-          Ey = cic_diff(w->win[1][rA + cA], az.f, ax.f);
-          Ez = cic_diff(w->win[2][rH + cA], az.fh, ax.f);
-          Bx = cic_diff(w->win[3][rH + cA], az.fh, ax.f);
-          By = cic_diff(w->win[4][rH + cH], az.fh, ax.fh);
-          Bz = cic_diff(w->win[5][rA + cH], az.f, ax.fh);
+          Ex = pipe_cic<kFast>(w->win[0][rA + cH], az.f, ax.fh);
+          Ey = pipe_cic<kFast>(w->win[1][rA + cA], az.f, ax.f);
+          Ez = pipe_cic<kFast>(w->win[2][rH + cA], az.fh, ax.f);
+          Bx = pipe_cic<kFast>(w->win[3][rH + cA], az.fh, ax.f);
+          By = pipe_cic<kFast>(w->win[4][rH + cH], az.fh, ax.fh);
+          Bz = pipe_cic<kFast>(w->win[5][rA + cH], az.f, ax.fh);
         } else {                                 // lanes span more than the window
           const int pit = p.qpitch;
           const int rA = (az.i + 1) * pit, rH = (az.ih + 1) * pit, cA = ax.i + 1, cH = ax.ih + 1;
-          Ex = cic_diff(__ldg(p.Q[0] + rA + cH), az.f, ax.fh);
-          Ey = cic_diff(__ldg(p.Q[1] + rA + cA), az.f, ax.f);
-          Ez = cic_diff(__ldg(p.Q[2] + rH + cA), az.fh, ax.f);
-          Bx = cic_diff(__ldg(p.Q[3] + rH + cA), az.fh, ax.f);
-          By = cic_diff(__ldg(p.Q[4] + rH + cH), az.fh, ax.fh);
-          Bz = cic_diff(__ldg(p.Q[5] + rA + cH), az.f, ax.fh);
+          Ex = pipe_cic<kFast>(__ldg(p.Q[0] + rA + cH), az.f, ax.fh);
+          Ey = pipe_cic<kFast>(__ldg(p.Q[1] + rA + cA), az.f, ax.f);
+          Ez = pipe_cic<kFast>(__ldg(p.Q[2] + rH + cA), az.fh, ax.f);
+          Bx = pipe_cic<kFast>(__ldg(p.Q[3] + rH + cA), az.fh, ax.f);
+          By = pipe_cic<kFast>(__ldg(p.Q[4] + rH + cH), az.fh, ax.fh);
+          Bz = pipe_cic<kFast>(__ldg(p.Q[5] + rA + cH), az.f, ax.fh);
         }
-        const float ig = boris_fast(pux[k], puy[k], puz[k], hf, Ex, Ey, Ez, Bx, By, Bz);
-        const float dtg = dtf * ig;
-        pz[k] = __dadd_rn(pz[k], (double)__fmul_rn(dtg, (float)puz[k]));
-        px[k] = __dadd_rn(px[k], (double)__fmul_rn(dtg, (float)pux[k]));
-        // inside iff z, x >= 0 and trunc(z) < nz, trunc(x) < nx (integer extents)
-        const int iz = __double2int_rz(pz[k]), ix = __double2int_rz(px[k]);
-        keep[k] = valid[k] && pz[k] >= 0.0 && px[k] >= 0.0 && iz < p.nz && ix < p.nx;
-        nkey[k] = keep[k] ? iz * p.nx + ix : -1;
-        const float qv = keep[k] ? __fmul_rn(qws, ig) : 0.f;
-        vsx[k] = __fmul_rn(qv, (float)pux[k]);
-        vsy[k] = __fmul_rn(qv, (float)puy[k]);
-        vsz[k] = __fmul_rn(qv, (float)puz[k]);
+        if (kFast) {
+          const float ig = boris_fast(pux[k], puy[k], puz[k], hf, Ex, Ey, Ez, Bx, By, Bz);
+          const float dtg = dtf * ig;
+          pz[k] = __dadd_rn(pz[k], (double)__fmul_rn(dtg, (float)puz[k]));
+          px[k] = __dadd_rn(px[k], (double)__fmul_rn(dtg, (float)pux[k]));
+          // inside iff z, x >= 0 and trunc(z) < nz, trunc(x) < nx (integer extents)
+          const int iz = __double2int_rz(pz[k]), ix = __double2int_rz(px[k]);
+          keep[k] = valid[k] && pz[k] >= 0.0 && px[k] >= 0.0 && iz < p.nz && ix < p.nx;
+          nkey[k] = keep[k] ? iz * p.nx + ix : -1;
+          const float qv = keep[k] ? __fmul_rn(qws, ig) : 0.f;
+          vsx[k] = __fmul_rn(qv, (float)pux[k]);
+          vsy[k] = __fmul_rn(qv, (float)puy[k]);
+          vsz[k] = __fmul_rn(qv, (float)puz[k]);
+        } else {
+          const double igam = boris_exact(pux[k], puy[k], puz[k], h, Ex, Ey, Ez, Bx, By, Bz);
+          pz[k] = __dadd_rn(pz[k], __dmul_rn(__dmul_rn(p.dt, puz[k]), igam));
+          px[k] = __dadd_rn(px[k], __dmul_rn(__dmul_rn(p.dt, pux[k]), igam));
+          const int iz = __double2int_rz(pz[k]), ix = __double2int_rz(px[k]);
+          keep[k] = valid[k] && pz[k] >= 0.0 && px[k] >= 0.0 && iz < p.nz && ix < p.nx;
+          nkey[k] = keep[k] ? iz * p.nx + ix : -1;
+          const double qwg = keep[k] ? p.qw : 0.0;
+          vsx[k] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, pux[k]), igam)), p.vscale);
+          vsy[k] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, puy[k]), igam)), p.vscale);
+          vsz[k] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, puz[k]), igam)), p.vscale);
+        }
       }
       // store in place (one 32-byte group per array), removed bookkeeping
       {
@@ -1069,7 +1126,9 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
 #pragma unroll
       for (int k = 0; k < kG; ++k) {
         const bool dep = nkey[k] >= 0;
-        const Axis az = fast_axis(dep ? pz[k] : 0.5), ax = fast_axis(dep ? px[k] : 0.5);
+        const Axis az = pic_axis<kFast>(dep ? pz[k] : 0.5), ax = pic_axis<kFast>(dep ? px[k] : 0.5);
+        int qv[kNodes];
+        if (!kFast) node_values(az, ax, vsx[k], vsy[k], vsz[k], qv);   // v = 0 -> q = 0 off-deposit
         const bool same = dep && nkey[k] == cur;
         const bool strag = dep && !same && cur >= 0 && (k + 1 == kG || nkey[k + 1] != nkey[k]);
         const bool swap = dep && !same && !strag;
@@ -1078,7 +1137,9 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
         if (fm) {
           if (need) {
             FlushEntry* e = w->q + qn + __popc(fm & lt);
-            if (strag) {
+            if (!kFast) {
+              enqueue(e, strag ? qv : acc, strag ? nkey[k] : cur, strag ? 1u : cur_m);
+            } else if (strag) {
               float t[kNodes];
 #pragma unroll
               for (int i = 0; i < kNodes; ++i) t[i] = 0.f;
@@ -1091,20 +1152,31 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
           qn += __popc(fm);
         }
         if ((k & 1) && qn) {
-          drain_queue<false, true>(p, w->q, qn, lane);
+          drain_queue<false, kFast>(p, w->q, qn, lane);
           qn = 0;
         }
-        if (__any_sync(kAll, swap)) {
-          if (swap) {
+        if (kFast) {
+          if (__any_sync(kAll, swap)) {
+            if (swap) {
 #pragma unroll
-            for (int i = 0; i < kNodes; ++i) accf[i] = 0.f;
-            cur = nkey[k];
-            cur_m = 0;
+              for (int i = 0; i < kNodes; ++i) accf[i] = 0.f;
+              cur = nkey[k];
+              cur_m = 0;
+            }
           }
-        }
-        if (same || swap) {
-          node_accum(az, ax, vsx[k], vsy[k], vsz[k], accf);
+          if (same || swap) {
+            node_accum(az, ax, vsx[k], vsy[k], vsz[k], accf);
+            ++cur_m;
+          }
+        } else if (same) {
+#pragma unroll
+          for (int i = 0; i < kNodes; ++i) acc[i] += qv[i];
           ++cur_m;
+        } else if (swap) {
+#pragma unroll
+          for (int i = 0; i < kNodes; ++i) acc[i] = qv[i];
+          cur = nkey[k];
+          cur_m = 1;
         }
         if (!dep) continue;
         bimin = min(bimin, az.i);
@@ -1132,8 +1204,11 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
     }
     {   // end of the unit: queue the lane's open cell, drain
       const unsigned fm = __ballot_sync(kAll, cur >= 0);
-      if (cur >= 0) enqueue_f(w->q + __popc(fm & lt), accf, cur, cur_m);
-      if (fm) drain_queue<false, true>(p, w->q, __popc(fm), lane);
+      if (cur >= 0) {
+        if (kFast) enqueue_f(w->q + __popc(fm & lt), accf, cur, cur_m);
+        else enqueue(w->q + __popc(fm & lt), acc, cur, cur_m);
+      }
+      if (fm) drain_queue<false, kFast>(p, w->q, __popc(fm), lane);
     }
     unsigned tclk = 0;
     if (kClock && hb >= 0) tclk = (unsigned)min((clock64() - t_last) >> 4, (long long)(1u << 30));
@@ -2781,9 +2856,10 @@ extern "C" int lbx_pic_step(lbx_ctx* ctx, const lbx_pic_args* a, void* stream) {
     p.jn_stride = jn_stride;
     p.ntx = ntx;
     p.ntiles = ntz * ntx;
-  } else if (fast && quad && LBX_PIC_PIPE) {
+  } else if (quad && !sorted && LBX_PIC_PIPE) {
     smem = (size_t)kPW * sizeof(PipeWarp) + (size_t)nb * 8;
-    kern = clock ? pic_pipe_kernel<true> : pic_pipe_kernel<false>;
+    kern = fast ? (clock ? pic_pipe_kernel<true, true> : pic_pipe_kernel<false, true>)
+                : (clock ? pic_pipe_kernel<true, false> : pic_pipe_kernel<false, false>);
   } else if (fast)
     kern = clock ? (quad ? pic_push_kernel<true, false, true, true> : pic_push_kernel<true, false, false, true>)
                  : (quad ? pic_push_kernel<false, false, true, true> : pic_push_kernel<false, false, false, true>);
