@@ -11,11 +11,13 @@ CASES_E='tests/test_gpu_3d.py tests/test_gpu_pic.py -k "3d or hole_filling or (m
 CASES_R='tests/test_gpu_runs.py -k "(timers and not cupti) or gpuclock or (graph_replay and mini)"'
 CASES_S='tests/test_gpu_pic.py -k "periodic_cell_sort or share_a_state or reused_buffers or tiled"'
 # round 2: pipelined tolerance kernel, Esirkepov, count/scan/move compaction
-CASES_F='tests/test_gpu_pic_fast.py -k "quad"'
+CASES_F='tests/test_gpu_pic_fast.py -k "quad or tiled"'
 CASES_Q='tests/test_gpu_pic_esirkepov.py -k "first_step or absorbing"'
 CASES_C='tests/test_gpu_kernels.py -k "compaction_large_shift or (fused_step_matches_oracle and 300001)"'
+CASES_X='tests/test_gpu_pic.py -k "quad and not sorted"'
+CASES_Y='tests/test_gpu_dist.py -k "esirkepov"'
 for tool in ${SAN_TOOLS:-memcheck racecheck synccheck}; do
-  for grp in ${SAN_GROUPS:-K P D E R S F Q C}; do
+  for grp in ${SAN_GROUPS:-K P D E R S F Q C X}; do   # (Y: memcheck / synccheck only; racecheck of thread ranks stalls the tool)
     eval cases=\$CASES_$grp
     eval timeout 1500 compute-sanitizer --tool $tool --error-exitcode 99 --target-processes all \
       python -m pytest $cases -x -q -p no:cacheprovider > gpurun_out/sanitize_${tool}_$grp.log 2>&1
