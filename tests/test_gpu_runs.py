@@ -204,3 +204,31 @@ def test_timers_run_keeps_reference_state(runs, kind):
     if res.summary["completed_steps"] == 80:
         pos, vel = res.final_state.to_numpy()
         assert np.array_equal(pos, ref["final_pos"]) and np.array_equal(vel, ref["final_vel"])
+
+
+@pytest.mark.parametrize("name", ["default_full", "default_full_measured", "default_full_sfc"])
+def test_long_run_matches_reference(name):
+    """The reference's own full `default` scenario (2,000 steps, 801,499
+    particles, 24 ranks) through the native loop (resident kernel), against
+    the REAL reference run in this container (tests/golden/make_golden_long.py):
+    every per-step metric column, the cost and count traces, the adoption
+    snapshots, the summary and the final particle state -- bit-identical."""
+    from paper_2104_11385_b200 import scenarios as S
+    from paper_2104_11385_b200.workload import run_simulation
+    ref = json.loads((G / "runs_long.json").read_text())[name]
+    spec = S.apply_overrides(S.load_spec("default"), **ref["overrides"])
+    res = run_simulation(spec.scenario, spec.policy, spec.build_provider(), record_counts=True)
+    assert len(res.metrics) == ref["steps"]
+    for c, want in ref["metrics_sha"].items():
+        v = [getattr(m, c) for m in res.metrics]
+        dt = np.bool_ if c in ("adopted", "oom") else (
+            np.int64 if c == "max_rank_particles" else np.float64)
+        assert sha(np.array(v, dtype=dt)) == want, (name, c)
+    assert sha(res.cost_trace) == ref["cost_trace_sha"], name
+    assert sha(res.count_trace.astype(np.int64)) == ref["count_trace_sha"], name
+    assert [[s, o.tolist()] for s, o in res.adoption_snapshots] == ref["snapshots"]
+    for k, v in ref["summary"].items():
+        assert res.summary[k] == v, (name, k)
+    pos, vel = res.final_state.to_numpy()
+    assert sha(pos) == ref["final_pos_sha"], name
+    assert sha(vel) == ref["final_vel_sha"], name
