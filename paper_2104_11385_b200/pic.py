@@ -68,6 +68,17 @@ def pic_sync(ctx: Context, st: PicState) -> int:
     return st.n
 
 
+def _device_count(ctx: Context, st: PicState, sync: bool):
+    """The context's device count must be this state's before a kernel runs:
+    set from st.n unless (sync=False) this state's own previous step / sort
+    left it there (then st.n is only an upper bound).  Call pic_sync before
+    running another state on the same context."""
+    live = getattr(ctx, "_pic_live", None)
+    if sync or live is None or live() is not st:
+        ctx.set_count(st.n)
+    ctx._pic_live = weakref.ref(st)
+
+
 def pic_sort(ctx: Context, st: PicState, tiled: bool = False, sync: bool = True):
     """Counting sort of the particles by cell (lbx_pic_sort) into the spare
     buffers, which the state then swaps in.  Every few in-place steps this
@@ -76,8 +87,7 @@ def pic_sort(ctx: Context, st: PicState, tiled: bool = False, sync: bool = True)
     pic_step(tiled=True) works on.  sync=False: as pic_step(sync=False)."""
     dev = ctx.device
     names = ("z", "x", "uz", "ux", "uy")
-    if sync:
-        ctx.set_count(st.n)
+    _device_count(ctx, st, sync)
     cap = st.z.numel()
     if st.spare is None or st.spare[0].numel() != cap:
         st.spare = tuple(torch.zeros(cap, dtype=torch.float64, device=dev) for _ in names)
@@ -117,9 +127,10 @@ def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times
     paper's order 3); tolerance mode, checked against
     oracle/pic_oracle.py esirkepov_current (tests/test_gpu_pic_esirkepov.py).
     sync=False: no host round trip -- the device keeps the particle count
-    from the previous step / sort on this context (st.n stays an upper
-    bound), nothing is read back and None is returned; pic_sync() ends such
-    a sequence.  Back-to-back steps then time the device alone."""
+    from this state's previous step / sort on this context (set from st.n
+    on the first call; st.n stays an upper bound), nothing is read back and
+    None is returned; pic_sync() ends such a sequence.  Back-to-back steps
+    then time the device alone."""
     dev = ctx.device
     nbz, nbx = st.nz // box_size, st.nx // box_size
     nb = nbz * nbx
@@ -127,8 +138,7 @@ def pic_step(ctx: Context, st: PicState, box_size: int, q_over_m: float, q_times
     cost = torch.empty(nb, dtype=torch.float64, device=dev)
     clk = torch.zeros(nb, dtype=torch.int64, device=dev)
     nout = torch.zeros(2, dtype=torch.int64, device=dev)
-    if sync:
-        ctx.set_count(st.n)
+    _device_count(ctx, st, sync)
     a = _lib.PicArgs()
     a.z, a.x, a.uz, a.ux, a.uy = (_lib.ptr(getattr(st, k)) for k in ("z", "x", "uz", "ux", "uy"))
     for i, k in enumerate(FIELD_NAMES):

@@ -248,6 +248,34 @@ def test_periodic_cell_sort_keeps_results_exact():
         assert np.array_equal(fa[k], f[k]), k
 
 
+def test_steps_without_host_round_trip_match_oracle():
+    """pic_step(sync=False) / pic_sort(sync=False): no per-step readback, the
+    device keeps the count (bench_pic's back-to-back timing); with absorbing
+    walls and a sort in between, the state after pic_sync() equals the
+    oracle's (quad gather forced: the pipelined kernel's exact path)."""
+    from paper_2104_11385_b200 import device, pic
+    pos, u = setup(40_000, 32, 48, seed=21, clustered=False, speed=2.0)
+    ctx = device.Context(capacity=pos.shape[0])
+    st = pic.PicState.create(pos, u, 32, 48)
+    f = PO.new_fields(32, 48)
+    p = {"z": pos[:, 0].copy(), "x": pos[:, 1].copy(), "uz": u[:, 0].copy(),
+         "ux": u[:, 1].copy(), "uy": u[:, 2].copy()}
+    for step in range(5):
+        if step == 2:
+            pic.pic_sort(ctx, st, sync=False)
+        assert pic.pic_step(ctx, st, 16, -1.0, -0.05, 0.5, field_solve=True,
+                            gather="quad", sync=False) is None
+        PO.particle_step(f, p, 32, 48, -1.0, -0.05, 0.5)
+        PO.field_step(f, 32, 48, 0.5)
+    assert pic.pic_sync(ctx, st) == p["z"].size < pos.shape[0]
+    g, o = canonical(st.particles()), canonical(p)
+    for k in g:
+        assert np.array_equal(g[k], o[k]), k
+    fa = st.field_arrays()
+    for k in PO.OFFSETS:
+        assert np.array_equal(fa[k], f[k]), k
+
+
 @pytest.mark.parametrize("case", ["sparse", "dense", "ragged"])
 def test_tiled_mode_matches_oracle(case):
     """Tiled in-place steps (shared-memory field patch and exact 64-bit
