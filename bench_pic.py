@@ -25,6 +25,8 @@ launch stream:
   push_deposit_fast_resort_noclock / push_deposit_esk3_resort_noclock
                         the same without the GpuClock tally (overhead =
                         gpuclock_overhead_<mode>, pipelined step times);
+  push_deposit_fast_resort_quad  push_deposit_fast_resort with the quad copy
+                        forced (the pipelined kernel on a sparse plasma);
   push_deposit_fast_tiled   tolerance mode on the tiled path (tile-major sort
                         every --resort steps; sparse plasmas);
   push_deposit_esk1/esk3  charge-conserving Esirkepov deposition with shape
@@ -117,6 +119,7 @@ def main():
                                    ("push_deposit_fast_resort", False, False, True),
                                    ("push_deposit_fast_resort_noclock", False, False, False),
                                    ("push_deposit_fast_tiled", False, False, True),
+                                   ("push_deposit_fast_resort_quad", False, False, True),
                                    ("push_deposit_esk1", False, False, True),
                                    ("push_deposit_esk3", False, False, True),
                                    ("push_deposit_esk3_resort", False, False, True),
@@ -130,6 +133,7 @@ def main():
         st.n = n
         resort = mode in ("push_deposit_resort", "push_deposit_tiled", "push_deposit_fast_tiled",
                           "push_deposit_fast_resort", "push_deposit_fast_resort_noclock",
+                          "push_deposit_fast_resort_quad",
                           "push_deposit_esk3_resort_noclock") or mode.endswith("esk3_resort")
         order = 3 if "esk3" in mode else (1 if "esk1" in mode else 0)
         tiled = mode in ("push_deposit_tiled", "push_deposit_fast_tiled")
@@ -139,7 +143,8 @@ def main():
         for w in range(args.warmup):
             try:
                 pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=clk, field_solve=solve,
-                             sort=sort, tiled=tiled, fast=fast, shape_order=order)
+                             sort=sort, tiled=tiled, fast=fast, shape_order=order,
+                             gather="quad" if mode.endswith("_quad") else None)
             except ValueError as e:
                 raise ValueError(f"mode {mode} warm-up step {w}: {e}") from None
         times = []
@@ -151,7 +156,8 @@ def main():
                 pic.pic_sort(ctx, st, tiled=tiled)
             try:
                 pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, clock=clk, field_solve=solve,
-                             sort=sort, tiled=tiled, fast=fast, shape_order=order)
+                             sort=sort, tiled=tiled, fast=fast, shape_order=order,
+                             gather="quad" if mode.endswith("_quad") else None)
             except ValueError as e:
                 raise ValueError(f"mode {mode} step {len(times)}: {e}") from None
             e1.record(stream)
@@ -173,8 +179,9 @@ def main():
         st.n = n
         if resort:
             pic.pic_sort(ctx, st, tiled=tiled)
+        gather = "quad" if mode.endswith("_quad") else None
         kw = dict(clock=clk, field_solve=solve, sort=sort, tiled=tiled, fast=fast,
-                  shape_order=order)
+                  shape_order=order, gather=gather)
         for w in range(args.warmup):
             pic.pic_step(ctx, st, box, -1.0, -1e-4, dt, **kw)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

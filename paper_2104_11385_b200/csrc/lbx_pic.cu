@@ -1009,7 +1009,15 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
           puy[2 * h] = a4.x; puy[2 * h + 1] = a4.y;
         }
       }
-      __syncwarp();                              // stage consumed: refill it now
+      // stage consumed: refill it now.  The lanes' shared-memory reads
+      // (generic proxy) must be performed before the bulk copy (async proxy)
+      // overwrites the stage: proxy fence per lane, then the warp barrier
+      // orders every lane's reads before the elected lane's copy (without
+      // it a copy could land before a read -- garbage particles, seen as an
+      // illegal address on a 2048^2 sparse plasma).
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
       {
         long long nb2 = base + kChunk;
         if (c + 1 == kChunks || nb2 >= n) nb2 = (u + ustride) * kUnitP;
@@ -1042,8 +1050,11 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
         }
         float Ex, Ey, Ez, Bx, By, Bz;
         if (!miss) {
-          const int rA = (az.i - wi + 2) * kWinC, rH = (az.ih - wi + 2) * kWinC;
-          const int cA = ax.i - wj + 2, cH = ax.ih - wj + 2;
+          // (a slot past the end of the array reads entry 0: its cell is not
+          // in the window, and a shared read outside the CTA faults)
+          const int rA = valid[k] ? (az.i - wi + 2) * kWinC : 0;
+          const int rH = valid[k] ? (az.ih - wi + 2) * kWinC : 0;
+          const int cA = valid[k] ? ax.i - wj + 2 : 0, cH = valid[k] ? ax.ih - wj + 2 : 0;
           Ex = pipe_cic<kFast>(w->win[0][rA + cH], az.f, ax.fh);
           Ey = pipe_cic<kFast>(w->win[1][rA + cA], az.f, ax.f);
           Ez = pipe_cic<kFast>(w->win[2][rH + cA], az.fh, ax.f);

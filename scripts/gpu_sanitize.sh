@@ -11,7 +11,7 @@ CASES_E='tests/test_gpu_3d.py tests/test_gpu_pic.py -k "3d or hole_filling or (m
 CASES_R='tests/test_gpu_runs.py -k "(timers and not cupti) or gpuclock or (graph_replay and mini)"'
 CASES_S='tests/test_gpu_pic.py -k "periodic_cell_sort or share_a_state or reused_buffers or tiled"'
 # round 2: pipelined tolerance kernel, Esirkepov, count/scan/move compaction
-CASES_F='tests/test_gpu_pic_fast.py -k "quad or tiled"'
+CASES_F='tests/test_gpu_pic_fast.py -k "quad or tiled or large_sparse"'
 CASES_Q='tests/test_gpu_pic_esirkepov.py -k "first_step or absorbing"'
 CASES_C='tests/test_gpu_kernels.py -k "compaction_large_shift or (fused_step_matches_oracle and 300001)"'
 CASES_X='tests/test_gpu_pic.py -k "quad and not sorted"'

@@ -163,3 +163,39 @@ def test_fast_tiled_within_tolerance(clustered):
     for k in PO.OFFSETS:
         e = rel_err(fa[k], f[k])
         assert e <= F_TOL, (k, e)
+
+
+def test_pipelined_kernel_on_a_large_sparse_grid():
+    """Regression (round 2): in the last, partial chunk of pic_pipe_kernel the
+    slots past the end of the array read the shared quad window at an index
+    computed from cell 0 -- outside the CTA's shared memory when the window
+    sits at large cell indices (an illegal-address fault on a 2048^2 grid).
+    A uniform 2048^2 x 8 ppc plasma (33.5 M particles) through the pipelined
+    kernel (quad gather forced) in the exact mode: per-box counts and the
+    particle count agree with the exact tiled path on the same input."""
+    from paper_2104_11385_b200 import device, pic
+    nz = nx = 2048
+    rng = np.random.default_rng(42)
+    cell = np.repeat(np.arange(nz * nx, dtype=np.int64), 8)
+    off = rng.random((cell.size, 2))
+    pos = np.column_stack([(cell // nx) + off[:, 0], (cell % nx) + off[:, 1]])
+    u = rng.normal(0.0, 0.05, size=(cell.size, 3))
+    del cell, off
+    outs = {}
+    for mode in ("pipe", "tiled"):
+        ctx = device.Context(capacity=pos.shape[0])
+        st = pic.PicState.create(pos, u, nz, nx)
+        pic.pic_sort(ctx, st, tiled=mode == "tiled")
+        res = []
+        for _ in range(2):
+            if mode == "pipe":
+                out = pic.pic_step(ctx, st, 128, -1.0, -1e-4, 0.5, gather="quad")
+            else:
+                out = pic.pic_step(ctx, st, 128, -1.0, -1e-4, 0.5, tiled=True)
+            res.append((out["n"], out["counts"].copy()))
+        outs[mode] = res
+        del st, ctx
+        torch.cuda.empty_cache()
+    for (na, ca), (nb, cb) in zip(outs["pipe"], outs["tiled"]):
+        assert na == nb < pos.shape[0]
+        assert np.array_equal(ca, cb)
