@@ -2229,14 +2229,31 @@ struct EskParams {
   float cy;                     // q w * scale          (Jy, times vy)
 };
 
+// The held block of pic_esk_kernel: the window of the block origin plus one
+// node below in x (always) and in z (kEskZE = 1): Jz (K+1+ZE) x (W+1),
+// Jx (W+ZE) x (K+2), Jy (W+ZE) x (W+1) nodes, each [node][lane] floats.
+#ifndef LBX_ESK_ZEXT
+#define LBX_ESK_ZEXT 1
+#endif
+constexpr int kEskZE = LBX_ESK_ZEXT;
+template <int K>
+struct EskBlock {
+  static constexpr int W = K + 2;
+  static constexpr int ZC = W + 1, ZR = K + 1 + kEskZE;   // Jz
+  static constexpr int XC = K + 2, XR = W + kEskZE;       // Jx
+  static constexpr int YC = W + 1, YR = W + kEskZE;       // Jy
+  static constexpr int NZ = ZR * ZC, NX = XR * XC, NY = YR * YC, NE = NZ + NX + NY;
+};
+
 // Add a warp's held block (pic_esk_kernel): node t's 32 lane sums (read
 // rotated: conflict-free), zeroed, rounded to fixed point, one RED each.
 // Out of line: the rare path keeps its registers off the particle loop.
 template <int K>
 __device__ __noinline__ void esk_flush(const EskParams& e, float* acc, int hbz, int hbx, int lane) {
-  constexpr int W = K + 2, W1 = W + 1, NZE = (K + 2) * W1, NE = 2 * NZE + W1 * W1;
+  using B = EskBlock<K>;
+  constexpr int NE = B::NE;
   __syncwarp();
-  const long long h0 = (long long)(hbz - 1 + kEskG) * e.apitch + (hbx - 1 + kEskG);
+  const long long h0 = (long long)(hbz - kEskZE + kEskG) * e.apitch + (hbx - 1 + kEskG);
   for (int t = lane; t < NE; t += 32) {
     float sum = 0.f;
 #pragma unroll 8
@@ -2247,12 +2264,12 @@ __device__ __noinline__ void esk_flush(const EskParams& e, float* acc, int hbz, 
     }
     int comp, di, dj;
     float scale;
-    if (t < NZE) {
-      comp = 2; di = t / W1; dj = t % W1; scale = e.cz;
-    } else if (t < 2 * NZE) {
-      comp = 0; di = (t - NZE) / (K + 2); dj = (t - NZE) % (K + 2); scale = e.cz;
+    if (t < B::NZ) {
+      comp = 2; di = t / B::ZC; dj = t % B::ZC; scale = e.cz;
+    } else if (t < B::NZ + B::NX) {
+      comp = 0; di = (t - B::NZ) / B::XC; dj = (t - B::NZ) % B::XC; scale = e.cz;
     } else {
-      comp = 1; di = (t - 2 * NZE) / W1; dj = (t - 2 * NZE) % W1; scale = e.cy;
+      comp = 1; di = (t - B::NZ - B::NX) / B::YC; dj = (t - B::NZ - B::NX) % B::YC; scale = e.cy;
     }
     const long long v = __float2ll_rn(sum * scale);
     if (v) red_add(e.J + comp * e.stride + h0 + (long long)di * e.apitch + dj, v);
@@ -2325,9 +2342,8 @@ __global__ void __launch_bounds__(kEB, LBX_ESK_MINB) pic_esk_kernel(EskParams e)
   // (recentre) and at the end of the chunk.  Lanes outside it add their own
   // fixed-point values directly.  (Round 2; replaces a redux.sync per node
   // per particle: 1,000 of 1,600 instructions per particle, ncu.)
-  constexpr int W1 = W + 1;
-  constexpr int NZE = (K + 2) * W1;        // Jz (and Jx) extended block
-  constexpr int NE = 2 * NZE + W1 * W1;    // + Jy
+  using Blk = EskBlock<K>;
+  constexpr int NE = Blk::NE;
   float* acc = reinterpret_cast<float*>(s_dyn + (size_t)p.nb * 8) + (size_t)warp * NE * 32;
   for (int t = lane; t < NE * 32; t += 32) acc[t] = 0.f;
   __syncwarp();
@@ -2394,21 +2410,23 @@ __global__ void __launch_bounds__(kEB, LBX_ESK_MINB) pic_esk_kernel(EskParams e)
     const float uyg = __fmul_rn((float)uy, ig);     // Jy's velocity factor
     const unsigned km = __ballot_sync(kAll, keep);
     const int lead = km ? __ffs(km) - 1 : 0;
-    bool inb = keep && (unsigned)(bz - hbz + 1) <= 1u && (unsigned)(bx - hbx + 1) <= 1u;
+    bool inb = keep && (unsigned)(bz - hbz + kEskZE) <= (unsigned)kEskZE &&
+               (unsigned)(bx - hbx + 1) <= 1u;
     if (km && 2 * __popc(__ballot_sync(kAll, inb)) < __popc(km)) {
       // most kept particles outside the held block: add it, hold the block
       // whose upper window is the warp's highest (covers that and one below)
       flush();
       hbz = __reduce_max_sync(kAll, keep ? bz : INT_MIN);
       hbx = __reduce_max_sync(kAll, keep ? bx : INT_MIN);
-      inb = keep && (unsigned)(bz - hbz + 1) <= 1u && (unsigned)(bx - hbx + 1) <= 1u;
+      inb = keep && (unsigned)(bz - hbz + kEskZE) <= (unsigned)kEskZE &&
+            (unsigned)(bx - hbx + 1) <= 1u;
     }
     if (inb) {
       // unscaled values into this lane's slots at the block offset (oz, ox)
-      const int oz = bz - hbz + 1, ox = bx - hbx + 1;
-      float* az = acc + (oz * W1 + ox) * 32 + lane;
-      float* ax = acc + (NZE + oz * (K + 2) + ox) * 32 + lane;
-      float* ay = acc + (2 * NZE + oz * W1 + ox) * 32 + lane;
+      const int oz = bz - hbz + kEskZE, ox = bx - hbx + 1;
+      float* az = acc + (oz * Blk::ZC + ox) * 32 + lane;
+      float* ax = acc + (Blk::NZ + oz * Blk::XC + ox) * 32 + lane;
+      float* ay = acc + (Blk::NZ + Blk::NX + oz * Blk::YC + ox) * 32 + lane;
 #pragma unroll
       for (int j = 0; j < W; ++j) {
         const float hx = __fmaf_rn(0.5f, dsx[j], s0x[j]);
@@ -2416,7 +2434,7 @@ __global__ void __launch_bounds__(kEB, LBX_ESK_MINB) pic_esk_kernel(EskParams e)
 #pragma unroll
         for (int ii = 0; ii <= K; ++ii) {
           a = __fmaf_rn(dsz[ii], hx, a);
-          az[(ii * W1 + j) * 32] += a;
+          az[(ii * Blk::ZC + j) * 32] += a;
         }
       }
 #pragma unroll
@@ -2426,7 +2444,7 @@ __global__ void __launch_bounds__(kEB, LBX_ESK_MINB) pic_esk_kernel(EskParams e)
 #pragma unroll
         for (int j = 0; j <= K; ++j) {
           a = __fmaf_rn(dsx[j], hz, a);
-          ax[(ii * (K + 2) + j) * 32] += a;
+          ax[(ii * Blk::XC + j) * 32] += a;
         }
       }
 #pragma unroll
@@ -2434,7 +2452,7 @@ __global__ void __launch_bounds__(kEB, LBX_ESK_MINB) pic_esk_kernel(EskParams e)
         const float a0 = __fmul_rn(uyg, __fmaf_rn(0.5f, dsz[ii], s0z[ii]));             // s0z + dsz/2
         const float a1 = __fmul_rn(uyg, __fmaf_rn(1.f / 3.f, dsz[ii], 0.5f * s0z[ii])); // s0z/2 + dsz/3
 #pragma unroll
-        for (int j = 0; j < W; ++j) ay[(ii * W1 + j) * 32] += __fmaf_rn(a1, dsx[j], a0 * s0x[j]);
+        for (int j = 0; j < W; ++j) ay[(ii * Blk::YC + j) * 32] += __fmaf_rn(a1, dsx[j], a0 * s0x[j]);
       }
     } else if (keep) {   // outside the block: this particle's values straight to HBM
       esk_direct<K>(e, bz, bx, s0z, dsz, s0x, dsx, uyg);
@@ -2639,7 +2657,7 @@ int pic_step_esirkepov(lbx_ctx* ctx, const lbx_pic_args* a, cudaStream_t s) {
     case 3: kern = clock ? pic_esk_kernel<3, true> : pic_esk_kernel<3, false>; break;
     default: return set_error(LBX_EINVAL, "shape_order must be 0 (CIC direct) or 1, 2, 3");
   }
-  const int W1 = K + 3, NE = 2 * (K + 2) * W1 + W1 * W1;   // pic_esk_kernel's per-warp block
+  const int NE = K == 1 ? EskBlock<1>::NE : (K == 2 ? EskBlock<2>::NE : EskBlock<3>::NE);
   const size_t smem = (size_t)nb * 8 + (size_t)(kEB / 32) * NE * 32 * sizeof(float);
   if (smem > 48 * 1024) {
     cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
