@@ -1,6 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
-for v in "" z0; do
+for v in ""; do
 LBX_VARIANT=$v timeout 600 python -m pytest tests/test_gpu_pic_esirkepov.py -q -x 2>&1 | tail -1
 LBX_VARIANT=$v timeout 900 python bench_pic.py --steps 10 --warmup 3 --resort 10 --modes push_deposit_esk3_resort,push_deposit_esk1 > gpurun_out/ez_$v.json 2>&1
 python -c "
