@@ -70,6 +70,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-pic", action="store_true", help="skip the PIC (north-star item 1) line")
     ap.add_argument("--no-native", action="store_true",
                     help="skip the native-size lines (resident multi-step kernel): "
                          "profiling runs (ncu serialises the kernel's host handshake)")
@@ -407,6 +408,7 @@ def run_lbx(args, rank, world, local_rank):
     c2n = c2_native(args, dev, spec, sc, pos0, kick0) if not args.no_native else None
     c1 = c1_uniform(dev) if not (args.no_cpu_baseline or args.no_native) else None
     comp = compaction_leavers(dev) if not args.no_e2e else None
+    picl = pic_line(dev, pos0, kick0, R, sc) if not args.no_pic else None
 
     # ---- e2e through the reference-facing C-ABI with host buffers ----
     e2e = None
@@ -436,6 +438,7 @@ def run_lbx(args, rank, world, local_rank):
         "c2_native": c2n,
         "c1_uniform": c1,
         "compaction": comp,
+        "pic": picl,
     }
     if e2e is not None:
         line["e2e"] = e2e
@@ -538,6 +541,64 @@ def c1_uniform(dev, steps=200, warm=20):
             "resident_runs": resident,
             "note": "resident kernel (lbx_resident.cu); parity of this config: "
                     "tests/test_gpu_runs.py::c1, tests/test_gpu_resident.py"}
+
+
+def pic_line(dev, pos0, kick0, R, sc, steps=10, warmup=3, resort=10):
+    """North-star item 1 (SURVEY 8d "PIC extension"): the same C2 particle set
+    (x R) through the 2D3V PIC push + deposit, tolerance mode (pic_pipe_kernel,
+    the fields of a 960^2 Yee grid; bench_pic.py has every mode).  `steps`
+    steps run back to back (no host round trip) with a cell sort every
+    `resort` steps, the sorts inside the timed region; the first step after
+    a sort is also timed alone.  80 B per push (5 fp64 read + write)."""
+    import torch
+
+    from paper_2104_11385_b200 import device, pic
+
+    dt = 0.5
+    n = pos0.shape[0] * R
+    u0 = np.column_stack([kick0[:, 0] / dt, kick0[:, 1] / dt, np.zeros(len(kick0))])
+    nz, nx = sc.domain_extent
+    st = pic.PicState.create(pos0[:1], u0[:1], nz, nx, device=dev)
+    cols = (pos0[:, 0], pos0[:, 1], u0[:, 0], u0[:, 1], u0[:, 2])
+    for name, col in zip(("z", "x", "uz", "ux", "uy"), cols):
+        t = torch.zeros(n + 2, dtype=torch.float64, device=dev)
+        t[:n].copy_(torch.from_numpy(np.ascontiguousarray(col)).to(dev).repeat(R))
+        setattr(st, name, t)
+    st.n = n
+    ctx = device.Context(dev, capacity=n)
+    kw = dict(clock=True, field_solve=False, fast=True, sync=False)
+    stream = torch.cuda.current_stream(dev)
+    pic.pic_sort(ctx, st)
+    for _ in range(warmup):
+        pic.pic_step(ctx, st, sc.box_size, -1.0, -1e-4, dt, **kw)
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    e[0].record(stream)
+    for i in range(steps):
+        if i % resort == 0:
+            pic.pic_sort(ctx, st, sync=False)   # inside the timed region
+        if i == 0:
+            e[1].record(stream)
+        pic.pic_step(ctx, st, sc.box_size, -1.0, -1e-4, dt, **kw)
+        if i == 0:
+            e[2].record(stream)
+    e[3].record(stream)
+    torch.cuda.synchronize(dev)
+    n1 = pic.pic_sync(ctx, st)
+    peak, _ = peaks()
+    first_ms = e[1].elapsed_time(e[2])   # the first step after the sort
+    ms = e[0].elapsed_time(e[3]) / steps
+    del st, ctx
+    torch.cuda.empty_cache()
+    return {"workload": f"C2 set x{R} = {n} particles, 2D3V PIC push + deposit, {nz}x{nx} "
+                        "Yee grid, tolerance mode (LBX_PIC_FAST), GpuClock on",
+            "bytes_per_particle": 80, "steps": steps, "resort_every": resort,
+            "ms_per_step": ms, "pushes_per_s": n / (ms / 1e3),
+            "frac_of_hbm": 80.0 * n / (ms / 1e3) / 1e9 / peak,
+            "first_step_after_sort_ms": first_ms,
+            "first_step_frac_of_hbm": 80.0 * n / (first_ms / 1e3) / 1e9 / peak,
+            "survivors": n1, "kernel": "pic_pipe_kernel<clock, fast> (+ quad copy, current "
+                                      "gather, hole filling per step; cell sort every "
+                                      f"{resort} steps)"}
 
 
 def compaction_leavers(dev, n=100_000_000, steps=3, ext=960.0, box=32.0):
