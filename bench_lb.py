@@ -120,7 +120,8 @@ def make_timed_engine(lock, log, physics="surrogate"):
 
 
 def run_emulated(R, steps, replicas, policy, speed=0.035, drift=0.01, strategy="knapsack",
-                 migration_ratio=0.0, physics="surrogate", exchange="nccl", shape_order=0):
+                 migration_ratio=0.0, physics="surrogate", exchange="nccl", shape_order=0,
+                 pic_fast=False):
     import torch
 
     import bench
@@ -145,7 +146,8 @@ def run_emulated(R, steps, replicas, policy, speed=0.035, drift=0.01, strategy="
                                         replicas=replicas,
                                         capacity=pos.shape[0] * replicas + 4096,
                                         physics=physics, exchange=exchange,
-                                        pic={"shape_order": shape_order, "resort": 10}
+                                        pic={"shape_order": shape_order, "resort": 10,
+                                             "fast": pic_fast}
                                         if physics == "pic" else None,
                                         pipeline=False)   # ranks' pushes timed one by one
             sim.run()
@@ -193,6 +195,8 @@ def main():
                     help="pic: 0 = CIC deposit, 1-3 = charge-conserving Esirkepov deposit "
                          "with that B-spline order (the paper's 3) -- its GpuClock tally "
                          "drives the remap")
+    ap.add_argument("--pic-fast", action="store_true",
+                    help="pic with shape order 0: tolerance mode (LBX_PIC_FAST)")
     ap.add_argument("--migration-ratio", type=float, default=0.0,
                     help=">0: migration-aware adoption gate (pushes per moved particle)")
     args = ap.parse_args()
@@ -207,13 +211,14 @@ def main():
                    "model, not a multi-GPU measurement", "ranks": R, "steps": args.steps,
            "kick": {"speed": args.speed, "drift": args.drift}, "strategy": args.strategy,
            "migration_ratio": args.migration_ratio, "physics": args.physics,
-           "shape_order": args.shape_order, "policies": {}}
+           "shape_order": args.shape_order, "pic_fast": args.pic_fast, "policies": {}}
     w = args.warmup_steps
     for policy in ("none", "static", "dynamic"):
         per_step, mig, res, moved, n = run_emulated(R, args.steps, args.replicas, policy,
                                                     args.speed, args.drift, args.strategy,
                                                     args.migration_ratio, args.physics,
-                                                    args.exchange, args.shape_order)
+                                                    args.exchange, args.shape_order,
+                                                    args.pic_fast)
         effs = [m.efficiency_after for m in res.metrics]
         # speedups use the raw (unclipped) step times; only the compute of
         # the first `w` steps (lazy allocations, graph capture) is dropped,

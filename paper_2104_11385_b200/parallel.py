@@ -576,6 +576,8 @@ class PicEngine(DeviceEngine):
         # (lbx_pic_sort: the deposit's runs / held blocks follow cell order;
         # emigrant unpacking and hole filling scramble it) -- 0: never
         self.resort = int(self.pic.get("resort", 0))
+        # tolerance mode (LBX_PIC_FAST, the pipelined kernel on dense plasmas)
+        self.fast = bool(self.pic.get("fast", False))
         self._sortbuf = None
         self._steps = 0
         nz, nx = cfg.domain_extent
@@ -681,7 +683,8 @@ class PicEngine(DeviceEngine):
         if self.resort and self.kicked and self._steps % self.resort == 0 and self.n:
             self._resort(stream)
         self._steps += 1
-        a = self._args((_lib.LBX_STEP_CLOCK if self.clock else 0) | _lib.LBX_PIC_DEFER_CURRENT)
+        a = self._args((_lib.LBX_STEP_CLOCK if self.clock else 0) | _lib.LBX_PIC_DEFER_CURRENT
+                       | (_lib.LBX_PIC_FAST if self.fast and not self.order else 0))
         a.w_particle, a.w_cell = float(wp), float(wc)
         a.counts_out, a.cost_out, a.clk_out = (_lib.ptr(self.counts), _lib.ptr(self.cost),
                                                _lib.ptr(self.clk))

@@ -220,6 +220,62 @@ def test_gpu_distributed_pic_esirkepov(world):
     assert outs[0][0].summary["adoption_count"] > 0
 
 
+def test_gpu_distributed_pic_tolerance_mode():
+    """Distributed PIC in tolerance mode (pic={"fast": True}: LBX_PIC_FAST,
+    the pipelined kernel where the quad copy pays) on 2 thread ranks with the
+    current deferred and the face-band exchange: per-box counts exact, the
+    particle multiset and the fields of every rank's own cells within
+    tests/test_gpu_pic_fast.py's tolerances of the single-process oracle."""
+    from paper_2104_11385_b200 import scenarios as S
+    from paper_2104_11385_b200.parallel import DistributedSimulation, ThreadComm
+    from tests.dist_util import own_cells_mask, pic_reference
+    from tests.test_gpu_pic_fast import F_TOL, U_TOL, X_TOL
+    doc = json.loads((Path(__file__).parent / "golden" / "runs.json").read_text())["_docs"]["small"]
+    steps, world = 12, 2
+    spec = S.apply_overrides(S.spec_from_dict(doc), ranks=world, steps=steps, interval=3,
+                             threshold=0.0)
+    shared = ThreadComm.shared(world)
+    outs, errs = [None] * world, []
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            sim = DistributedSimulation(spec.scenario, spec.policy, spec.build_provider(),
+                                        comm=ThreadComm(shared, r), device="cuda:0",
+                                        record_counts=True, physics="pic",
+                                        pic={"fast": True, "resort": 4})
+            sim.run()
+            assert sim.engine.fast
+            outs[r] = (sim.result(), sim.engine.state(), sim.engine.field_arrays(),
+                       sim.engine.halo.owner.copy())
+            sim.close()
+        except Exception as e:
+            errs.append(e)
+            shared["bar"].abort()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    counts, p, f = pic_reference(doc, steps)
+    nz, nx = doc["domain"]["extent"]
+    box = doc["domain"]["box_size"]
+    for r, (res, _, fa, owner) in enumerate(outs):
+        assert np.array_equal(res.count_trace, counts)
+        mine = own_cells_mask(owner, ((nz // box, nx // box), box, nz, nx), r)
+        for k in ("Ex", "Ey", "Ez", "Bx", "By", "Bz"):
+            scale = max(float(np.abs(f[k]).max()), 1e-30)
+            assert np.abs(fa[k][mine] - f[k][mine]).max() / scale <= F_TOL, (r, k)
+    umax = max(float(np.abs(p[k]).max()) for k in ("uz", "ux", "uy"))
+    for k, tol in (("z", X_TOL), ("x", X_TOL), ("uz", U_TOL * umax), ("ux", U_TOL * umax),
+                   ("uy", U_TOL * umax)):
+        got = np.sort(np.concatenate([o[1][k] for o in outs]))
+        assert np.abs(got - np.sort(p[k])).max() <= tol, k
+
+
 def test_p2p_failure_on_one_rank_falls_back_to_collectives(monkeypatch):
     """If any rank cannot map peer memory, every rank switches to the
     collective exchange together and the run stays exact."""
