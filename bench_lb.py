@@ -211,7 +211,8 @@ def main():
                    "model, not a multi-GPU measurement", "ranks": R, "steps": args.steps,
            "kick": {"speed": args.speed, "drift": args.drift}, "strategy": args.strategy,
            "migration_ratio": args.migration_ratio, "physics": args.physics,
-           "shape_order": args.shape_order, "pic_fast": args.pic_fast, "policies": {}}
+           "shape_order": args.shape_order, "pic_fast": args.pic_fast,
+           "warmup_steps_dropped": args.warmup_steps, "policies": {}}
     w = args.warmup_steps
     for policy in ("none", "static", "dynamic"):
         per_step, mig, res, moved, n = run_emulated(R, args.steps, args.replicas, policy,
