@@ -408,7 +408,13 @@ def run_lbx(args, rank, world, local_rank):
     c2n = c2_native(args, dev, spec, sc, pos0, kick0) if not args.no_native else None
     c1 = c1_uniform(dev) if not (args.no_cpu_baseline or args.no_native) else None
     comp = compaction_leavers(dev) if not args.no_e2e else None
-    picl = pic_line(dev, pos0, kick0, R, sc) if not args.no_pic else None
+    picl = None
+    if not args.no_pic:
+        try:   # an extra line: never let it take the headline line down
+            picl = pic_line(dev, pos0, kick0, R, sc)
+        except Exception as e:   # noqa: BLE001
+            picl = {"error": f"{type(e).__name__}: {e}"}
+            torch.cuda.empty_cache()
 
     # ---- e2e through the reference-facing C-ABI with host buffers ----
     e2e = None
