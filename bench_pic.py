@@ -22,7 +22,8 @@ launch stream:
   push_deposit_fast     in place, tolerance mode (LBX_PIC_FAST: float32
                         Boris increment, FMA gathers);
   push_deposit_fast_resort  the same with lbx_pic_sort every --resort steps;
-  push_deposit_fast_resort_noclock / push_deposit_esk3_resort_noclock
+  push_deposit_resort_noclock / push_deposit_fast_resort_noclock /
+  push_deposit_esk3_resort_noclock
                         the same without the GpuClock tally (overhead =
                         gpuclock_overhead_<mode>, pipelined step times);
   push_deposit_fast_resort_quad  push_deposit_fast_resort with the quad copy
@@ -114,6 +115,7 @@ def main():
                                    ("push_deposit_noclock", False, True, False),
                                    ("full_step", True, True, True),
                                    ("push_deposit_resort", False, False, True),
+                                   ("push_deposit_resort_noclock", False, False, False),
                                    ("push_deposit_tiled", False, False, True),
                                    ("push_deposit_fast", False, False, True),
                                    ("push_deposit_fast_resort", False, False, True),
@@ -131,7 +133,7 @@ def main():
         for name, t in init.items():
             setattr(st, name, t.clone())
         st.n = n
-        resort = mode in ("push_deposit_resort", "push_deposit_tiled", "push_deposit_fast_tiled",
+        resort = mode in ("push_deposit_resort", "push_deposit_resort_noclock", "push_deposit_tiled", "push_deposit_fast_tiled",
                           "push_deposit_fast_resort", "push_deposit_fast_resort_noclock",
                           "push_deposit_fast_resort_quad",
                           "push_deposit_esk3_resort_noclock") or mode.endswith("esk3_resort")
@@ -198,6 +200,7 @@ def main():
         out[mode]["frac_of_hbm_peak_pipelined"] = BYTES_PER_PARTICLE * nb2 / (msp / 1e3) / 1e9 / peak
         del st
     for a, b in (("push_deposit", "push_deposit_noclock"),
+                 ("push_deposit_resort", "push_deposit_resort_noclock"),
                  ("push_deposit_fast_resort", "push_deposit_fast_resort_noclock"),
                  ("push_deposit_esk3_resort", "push_deposit_esk3_resort_noclock")):
         if a in out and b in out:   # GpuClock tally in that kernel vs the same kernel without it

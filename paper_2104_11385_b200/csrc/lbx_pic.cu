@@ -939,6 +939,20 @@ __device__ __forceinline__ void pipe_window(const PicParams& p, PipeWarp* w, int
   __syncwarp();
 }
 
+#ifndef LBX_PIPE_ROLL
+#define LBX_PIPE_ROLL 1   // exact pipe kernel: rolled slot loop (see below)
+#endif
+#ifndef LBX_PIPE_ROLL_FAST
+#define LBX_PIPE_ROLL_FAST 0
+#endif
+template <typename T, int N>
+__device__ __forceinline__ void rot(T (&a)[N]) {
+  const T t = a[0];
+#pragma unroll
+  for (int i = 0; i + 1 < N; ++i) a[i] = a[i + 1];
+  a[N - 1] = t;
+}
+
 // kFast = false: the exact (bit-exact) step with the same pipeline -- fp64
 // Boris, floor axes, float32 CIC on raw quads, integer node values.
 template <bool kClock, bool kFast = true>
@@ -970,6 +984,8 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
   const unsigned lt = (1u << lane) - 1u;
   // my four slots in a chunk
   const int slot0 = kG * lane;                  // my slots: kG consecutive particles
+  constexpr bool kRoll = LBX_PIPE_ROLL && (!kFast || LBX_PIPE_ROLL_FAST);
+  constexpr bool kRoll2 = LBX_PIPE_ROLL >= 2 && (!kFast || LBX_PIPE_ROLL_FAST);   // the deposit loop too
 
   long long u = (long long)blockIdx.x * kPW + warp;
   if (u < units) pipe_issue(p, w, bar, u * kUnitP, n);
@@ -1028,19 +1044,21 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
       bool valid[kG], keep[kG];
       int nkey[kG];
       float vsx[kG], vsy[kG], vsz[kG];
-#pragma unroll
-      for (int k = 0; k < kG; ++k) {
-        valid[k] = slot0 + k < lim;
-        const Axis az = pic_axis<kFast>(valid[k] ? pz[k] : 0.5),
-                   ax = pic_axis<kFast>(valid[k] ? px[k] : 0.5);
+      // gather + push + move of one slot.  kRoll (exact mode): one copy of
+      // the body in a rolled loop over slot 0, the slot arrays rotated after
+      // each pass, so the kernel's hot loop fits the instruction cache.
+      auto slot = [&](const int k, const int K) {
+        valid[K] = slot0 + k < lim;
+        const Axis az = pic_axis<kFast>(valid[K] ? pz[K] : 0.5),
+                   ax = pic_axis<kFast>(valid[K] ? px[K] : 0.5);
         // the window: rows wi-2..wi+1 and cols wj-2..wj+2 hold every quad of
         // a particle in cells [wi-1, wi+1] x [wj-1, wj+2]
-        const bool hit = !valid[k] || ((unsigned)(az.i - wi + 1) <= 2u && (unsigned)(ax.i - wj + 1) <= 3u);
+        const bool hit = !valid[K] || ((unsigned)(az.i - wi + 1) <= 2u && (unsigned)(ax.i - wj + 1) <= 3u);
         unsigned miss = __ballot_sync(kAll, !hit);
         if (miss) {   // recentre so the window starts at the warp's lowest row / column, if it then covers the warp
-          const int ci = __reduce_min_sync(kAll, valid[k] ? az.i : INT_MAX) + 1;
-          const int cj = __reduce_min_sync(kAll, valid[k] ? ax.i : INT_MAX) + 1;
-          const bool h2 = !valid[k] || ((unsigned)(az.i - ci + 1) <= 2u && (unsigned)(ax.i - cj + 1) <= 3u);
+          const int ci = __reduce_min_sync(kAll, valid[K] ? az.i : INT_MAX) + 1;
+          const int cj = __reduce_min_sync(kAll, valid[K] ? ax.i : INT_MAX) + 1;
+          const bool h2 = !valid[K] || ((unsigned)(az.i - ci + 1) <= 2u && (unsigned)(ax.i - cj + 1) <= 3u);
           if (__all_sync(kAll, h2)) {
             wi = ci;
             wj = cj;
@@ -1052,9 +1070,9 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
         if (!miss) {
           // (a slot past the end of the array reads entry 0: its cell is not
           // in the window, and a shared read outside the CTA faults)
-          const int rA = valid[k] ? (az.i - wi + 2) * kWinC : 0;
-          const int rH = valid[k] ? (az.ih - wi + 2) * kWinC : 0;
-          const int cA = valid[k] ? ax.i - wj + 2 : 0, cH = valid[k] ? ax.ih - wj + 2 : 0;
+          const int rA = valid[K] ? (az.i - wi + 2) * kWinC : 0;
+          const int rH = valid[K] ? (az.ih - wi + 2) * kWinC : 0;
+          const int cA = valid[K] ? ax.i - wj + 2 : 0, cH = valid[K] ? ax.ih - wj + 2 : 0;
           Ex = pipe_cic<kFast>(w->win[0][rA + cH], az.f, ax.fh);
           Ey = pipe_cic<kFast>(w->win[1][rA + cA], az.f, ax.f);
           Ez = pipe_cic<kFast>(w->win[2][rH + cA], az.fh, ax.f);
@@ -1072,30 +1090,41 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
           Bz = pipe_cic<kFast>(__ldg(p.Q[5] + rA + cH), az.f, ax.fh);
         }
         if (kFast) {
-          const float ig = boris_fast(pux[k], puy[k], puz[k], hf, Ex, Ey, Ez, Bx, By, Bz);
+          const float ig = boris_fast(pux[K], puy[K], puz[K], hf, Ex, Ey, Ez, Bx, By, Bz);
           const float dtg = dtf * ig;
-          pz[k] = __dadd_rn(pz[k], (double)__fmul_rn(dtg, (float)puz[k]));
-          px[k] = __dadd_rn(px[k], (double)__fmul_rn(dtg, (float)pux[k]));
+          pz[K] = __dadd_rn(pz[K], (double)__fmul_rn(dtg, (float)puz[K]));
+          px[K] = __dadd_rn(px[K], (double)__fmul_rn(dtg, (float)pux[K]));
           // inside iff z, x >= 0 and trunc(z) < nz, trunc(x) < nx (integer extents)
-          const int iz = __double2int_rz(pz[k]), ix = __double2int_rz(px[k]);
-          keep[k] = valid[k] && pz[k] >= 0.0 && px[k] >= 0.0 && iz < p.nz && ix < p.nx;
-          nkey[k] = keep[k] ? iz * p.nx + ix : -1;
-          const float qv = keep[k] ? __fmul_rn(qws, ig) : 0.f;
-          vsx[k] = __fmul_rn(qv, (float)pux[k]);
-          vsy[k] = __fmul_rn(qv, (float)puy[k]);
-          vsz[k] = __fmul_rn(qv, (float)puz[k]);
+          const int iz = __double2int_rz(pz[K]), ix = __double2int_rz(px[K]);
+          keep[K] = valid[K] && pz[K] >= 0.0 && px[K] >= 0.0 && iz < p.nz && ix < p.nx;
+          nkey[K] = keep[K] ? iz * p.nx + ix : -1;
+          const float qv = keep[K] ? __fmul_rn(qws, ig) : 0.f;
+          vsx[K] = __fmul_rn(qv, (float)pux[K]);
+          vsy[K] = __fmul_rn(qv, (float)puy[K]);
+          vsz[K] = __fmul_rn(qv, (float)puz[K]);
         } else {
-          const double igam = boris_exact(pux[k], puy[k], puz[k], h, Ex, Ey, Ez, Bx, By, Bz);
-          pz[k] = __dadd_rn(pz[k], __dmul_rn(__dmul_rn(p.dt, puz[k]), igam));
-          px[k] = __dadd_rn(px[k], __dmul_rn(__dmul_rn(p.dt, pux[k]), igam));
-          const int iz = __double2int_rz(pz[k]), ix = __double2int_rz(px[k]);
-          keep[k] = valid[k] && pz[k] >= 0.0 && px[k] >= 0.0 && iz < p.nz && ix < p.nx;
-          nkey[k] = keep[k] ? iz * p.nx + ix : -1;
-          const double qwg = keep[k] ? p.qw : 0.0;
-          vsx[k] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, pux[k]), igam)), p.vscale);
-          vsy[k] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, puy[k]), igam)), p.vscale);
-          vsz[k] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, puz[k]), igam)), p.vscale);
+          const double igam = boris_exact(pux[K], puy[K], puz[K], h, Ex, Ey, Ez, Bx, By, Bz);
+          pz[K] = __dadd_rn(pz[K], __dmul_rn(__dmul_rn(p.dt, puz[K]), igam));
+          px[K] = __dadd_rn(px[K], __dmul_rn(__dmul_rn(p.dt, pux[K]), igam));
+          const int iz = __double2int_rz(pz[K]), ix = __double2int_rz(px[K]);
+          keep[K] = valid[K] && pz[K] >= 0.0 && px[K] >= 0.0 && iz < p.nz && ix < p.nx;
+          nkey[K] = keep[K] ? iz * p.nx + ix : -1;
+          const double qwg = keep[K] ? p.qw : 0.0;
+          vsx[K] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, pux[K]), igam)), p.vscale);
+          vsy[K] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, puy[K]), igam)), p.vscale);
+          vsz[K] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, puz[K]), igam)), p.vscale);
         }
+      };
+      if (kRoll) {
+#pragma unroll 1
+        for (int k = 0; k < kG; ++k) {
+          slot(k, 0);
+          rot(pz); rot(px); rot(puz); rot(pux); rot(puy);
+          rot(valid); rot(keep); rot(nkey); rot(vsx); rot(vsy); rot(vsz);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < kG; ++k) slot(k, k);
       }
       // store in place (one 32-byte group per array), removed bookkeeping
       {
@@ -1134,14 +1163,13 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
       // last slot has no look-ahead and always counts as a straggler, so a
       // particle that drifted across a face does not flip the run twice.
       int qn = 0;
-#pragma unroll
-      for (int k = 0; k < kG; ++k) {
-        const bool dep = nkey[k] >= 0;
-        const Axis az = pic_axis<kFast>(dep ? pz[k] : 0.5), ax = pic_axis<kFast>(dep ? px[k] : 0.5);
+      auto deposit = [&](const int k, const int K) {
+        const bool dep = nkey[K] >= 0;
+        const Axis az = pic_axis<kFast>(dep ? pz[K] : 0.5), ax = pic_axis<kFast>(dep ? px[K] : 0.5);
         int qv[kNodes];
-        if (!kFast) node_values(az, ax, vsx[k], vsy[k], vsz[k], qv);   // v = 0 -> q = 0 off-deposit
-        const bool same = dep && nkey[k] == cur;
-        const bool strag = dep && !same && cur >= 0 && (k + 1 == kG || nkey[k + 1] != nkey[k]);
+        if (!kFast) node_values(az, ax, vsx[K], vsy[K], vsz[K], qv);   // v = 0 -> q = 0 off-deposit
+        const bool same = dep && nkey[K] == cur;
+        const bool strag = dep && !same && cur >= 0 && (k + 1 == kG || nkey[K + 1] != nkey[K]);
         const bool swap = dep && !same && !strag;
         const bool need = strag || (swap && cur >= 0);
         const unsigned fm = __ballot_sync(kAll, need);
@@ -1149,13 +1177,13 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
           if (need) {
             FlushEntry* e = w->q + qn + __popc(fm & lt);
             if (!kFast) {
-              enqueue(e, strag ? qv : acc, strag ? nkey[k] : cur, strag ? 1u : cur_m);
+              enqueue(e, strag ? qv : acc, strag ? nkey[K] : cur, strag ? 1u : cur_m);
             } else if (strag) {
               float t[kNodes];
 #pragma unroll
               for (int i = 0; i < kNodes; ++i) t[i] = 0.f;
-              node_accum(az, ax, vsx[k], vsy[k], vsz[k], t);
-              enqueue_f(e, t, nkey[k], 1u);
+              node_accum(az, ax, vsx[K], vsy[K], vsz[K], t);
+              enqueue_f(e, t, nkey[K], 1u);
             } else {
               enqueue_f(e, accf, cur, cur_m);
             }
@@ -1171,12 +1199,12 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
             if (swap) {
 #pragma unroll
               for (int i = 0; i < kNodes; ++i) accf[i] = 0.f;
-              cur = nkey[k];
+              cur = nkey[K];
               cur_m = 0;
             }
           }
           if (same || swap) {
-            node_accum(az, ax, vsx[k], vsy[k], vsz[k], accf);
+            node_accum(az, ax, vsx[K], vsy[K], vsz[K], accf);
             ++cur_m;
           }
         } else if (same) {
@@ -1186,10 +1214,10 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
         } else if (swap) {
 #pragma unroll
           for (int i = 0; i < kNodes; ++i) acc[i] = qv[i];
-          cur = nkey[k];
+          cur = nkey[K];
           cur_m = 1;
         }
-        if (!dep) continue;
+        if (!dep) return;
         bimin = min(bimin, az.i);
         bimax = max(bimax, az.i);
         bjmin = min(bjmin, ax.i);
@@ -1211,6 +1239,16 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
           hb = bz * p.nbx + bx;
           hn = 1;
         }
+      };
+      if (kRoll2) {
+#pragma unroll 1
+        for (int k = 0; k < kG; ++k) {
+          deposit(k, 0);
+          rot(pz); rot(px); rot(nkey); rot(vsx); rot(vsy); rot(vsz);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < kG; ++k) deposit(k, k);
       }
     }
     {   // end of the unit: queue the lane's open cell, drain
