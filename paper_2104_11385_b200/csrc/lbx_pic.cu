@@ -976,8 +976,9 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
   const float hf = (float)(0.5 * p.qm * p.dt), dtf = (float)p.dt;
   const float qws = (float)p.qw * p.vscale;
   const double h = 0.5 * p.qm * p.dt;
-  unsigned long long removed = 0;
-  long long first_out = LLONG_MAX, err = 0;
+  unsigned removed = 0;                          // per lane: 32 bits (register pressure)
+  long long first_out = LLONG_MAX;
+  int err = 0;
   int bimin = INT_MAX, bimax = INT_MIN, bjmin = INT_MAX, bjmax = INT_MIN;
   int wi = INT_MIN / 2, wj = INT_MIN / 2;        // window centre (none loaded)
   unsigned phase = 0;
@@ -1041,24 +1042,23 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
       }
       const bool full = base + kChunk <= n;      // warp-uniform: every slot live
       const int lim = full ? kChunk : (int)(n - base);
-      bool valid[kG], keep[kG];
       int nkey[kG];
       float vsx[kG], vsy[kG], vsz[kG];
       // gather + push + move of one slot.  kRoll (exact mode): one copy of
       // the body in a rolled loop over slot 0, the slot arrays rotated after
       // each pass, so the kernel's hot loop fits the instruction cache.
       auto slot = [&](const int k, const int K) {
-        valid[K] = slot0 + k < lim;
-        const Axis az = pic_axis<kFast>(valid[K] ? pz[K] : 0.5),
-                   ax = pic_axis<kFast>(valid[K] ? px[K] : 0.5);
+        const bool vk = slot0 + k < lim;
+        const Axis az = pic_axis<kFast>(vk ? pz[K] : 0.5),
+                   ax = pic_axis<kFast>(vk ? px[K] : 0.5);
         // the window: rows wi-2..wi+1 and cols wj-2..wj+2 hold every quad of
         // a particle in cells [wi-1, wi+1] x [wj-1, wj+2]
-        const bool hit = !valid[K] || ((unsigned)(az.i - wi + 1) <= 2u && (unsigned)(ax.i - wj + 1) <= 3u);
+        const bool hit = !vk || ((unsigned)(az.i - wi + 1) <= 2u && (unsigned)(ax.i - wj + 1) <= 3u);
         unsigned miss = __ballot_sync(kAll, !hit);
         if (miss) {   // recentre so the window starts at the warp's lowest row / column, if it then covers the warp
-          const int ci = __reduce_min_sync(kAll, valid[K] ? az.i : INT_MAX) + 1;
-          const int cj = __reduce_min_sync(kAll, valid[K] ? ax.i : INT_MAX) + 1;
-          const bool h2 = !valid[K] || ((unsigned)(az.i - ci + 1) <= 2u && (unsigned)(ax.i - cj + 1) <= 3u);
+          const int ci = __reduce_min_sync(kAll, vk ? az.i : INT_MAX) + 1;
+          const int cj = __reduce_min_sync(kAll, vk ? ax.i : INT_MAX) + 1;
+          const bool h2 = !vk || ((unsigned)(az.i - ci + 1) <= 2u && (unsigned)(ax.i - cj + 1) <= 3u);
           if (__all_sync(kAll, h2)) {
             wi = ci;
             wj = cj;
@@ -1070,9 +1070,9 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
         if (!miss) {
           // (a slot past the end of the array reads entry 0: its cell is not
           // in the window, and a shared read outside the CTA faults)
-          const int rA = valid[K] ? (az.i - wi + 2) * kWinC : 0;
-          const int rH = valid[K] ? (az.ih - wi + 2) * kWinC : 0;
-          const int cA = valid[K] ? ax.i - wj + 2 : 0, cH = valid[K] ? ax.ih - wj + 2 : 0;
+          const int rA = vk ? (az.i - wi + 2) * kWinC : 0;
+          const int rH = vk ? (az.ih - wi + 2) * kWinC : 0;
+          const int cA = vk ? ax.i - wj + 2 : 0, cH = vk ? ax.ih - wj + 2 : 0;
           Ex = pipe_cic<kFast>(w->win[0][rA + cH], az.f, ax.fh);
           Ey = pipe_cic<kFast>(w->win[1][rA + cA], az.f, ax.f);
           Ez = pipe_cic<kFast>(w->win[2][rH + cA], az.fh, ax.f);
@@ -1096,9 +1096,9 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
           px[K] = __dadd_rn(px[K], (double)__fmul_rn(dtg, (float)pux[K]));
           // inside iff z, x >= 0 and trunc(z) < nz, trunc(x) < nx (integer extents)
           const int iz = __double2int_rz(pz[K]), ix = __double2int_rz(px[K]);
-          keep[K] = valid[K] && pz[K] >= 0.0 && px[K] >= 0.0 && iz < p.nz && ix < p.nx;
-          nkey[K] = keep[K] ? iz * p.nx + ix : -1;
-          const float qv = keep[K] ? __fmul_rn(qws, ig) : 0.f;
+          const bool kp = vk && pz[K] >= 0.0 && px[K] >= 0.0 && iz < p.nz && ix < p.nx;
+          nkey[K] = kp ? iz * p.nx + ix : -1;
+          const float qv = kp ? __fmul_rn(qws, ig) : 0.f;
           vsx[K] = __fmul_rn(qv, (float)pux[K]);
           vsy[K] = __fmul_rn(qv, (float)puy[K]);
           vsz[K] = __fmul_rn(qv, (float)puz[K]);
@@ -1107,9 +1107,9 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
           pz[K] = __dadd_rn(pz[K], __dmul_rn(__dmul_rn(p.dt, puz[K]), igam));
           px[K] = __dadd_rn(px[K], __dmul_rn(__dmul_rn(p.dt, pux[K]), igam));
           const int iz = __double2int_rz(pz[K]), ix = __double2int_rz(px[K]);
-          keep[K] = valid[K] && pz[K] >= 0.0 && px[K] >= 0.0 && iz < p.nz && ix < p.nx;
-          nkey[K] = keep[K] ? iz * p.nx + ix : -1;
-          const double qwg = keep[K] ? p.qw : 0.0;
+          const bool kp = vk && pz[K] >= 0.0 && px[K] >= 0.0 && iz < p.nz && ix < p.nx;
+          nkey[K] = kp ? iz * p.nx + ix : -1;
+          const double qwg = kp ? p.qw : 0.0;
           vsx[K] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, pux[K]), igam)), p.vscale);
           vsy[K] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, puy[K]), igam)), p.vscale);
           vsz[K] = __fmul_rn(__double2float_rn(__dmul_rn(__dmul_rn(qwg, puz[K]), igam)), p.vscale);
@@ -1120,7 +1120,7 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
         for (int k = 0; k < kG; ++k) {
           slot(k, 0);
           rot(pz); rot(px); rot(puz); rot(pux); rot(puy);
-          rot(valid); rot(keep); rot(nkey); rot(vsx); rot(vsy); rot(vsz);
+          rot(nkey); rot(vsx); rot(vsy); rot(vsz);
         }
       } else {
 #pragma unroll
@@ -1147,7 +1147,7 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_pipe_kernel(PicParams p
       }
 #pragma unroll
       for (int k = 0; k < kG; ++k) {
-        if (valid[k] && !keep[k]) {
+        if (slot0 + k < lim && nkey[k] < 0) {   // a live slot that left the grid
           const long long d = base + slot0 + k;
           ++removed;
           first_out = min(first_out, d);
