@@ -2256,15 +2256,22 @@ __global__ void esk_rows_kernel(const float* __restrict__ F0, const float* __res
   }
 }
 
-struct EskParams {
-  PicParams b;                  // particles, fields F[], grid, boxes, status, outputs
-  const float4* R[6];           // row-quad field copies [(nz+5) x (nx+5)]
-  int rpitch;
+// Where a deposit goes: passed BY VALUE to the out-of-line flush / direct
+// paths (a reference to the kernel parameter would copy all of EskParams to
+// the stack).
+struct EskOut {
   unsigned long long* J;        // [3][stride] padded node sums (Jx, Jy, Jz)
   long long stride;
   int apitch;                   // nx + 2 kEskG
   float cz;                     // -(q w / dt) * scale  (Jz, Jx)
   float cy;                     // q w * scale          (Jy, times vy)
+};
+
+struct EskParams {
+  PicParams b;                  // particles, fields F[], grid, boxes, status, outputs
+  const float4* R[6];           // row-quad field copies [(nz+5) x (nx+5)]
+  int rpitch;
+  EskOut o;                     // the current sums (by value into the out-of-line paths)
 };
 
 // The held block of pic_esk_kernel: the window of the block origin plus one
@@ -2287,7 +2294,7 @@ struct EskBlock {
 // rotated: conflict-free), zeroed, rounded to fixed point, one RED each.
 // Out of line: the rare path keeps its registers off the particle loop.
 template <int K>
-__device__ __noinline__ void esk_flush(const EskParams& e, float* acc, int hbz, int hbx, int lane) {
+__device__ __noinline__ void esk_flush(const EskOut e, float* acc, int hbz, int hbx, int lane) {
   using B = EskBlock<K>;
   constexpr int NE = B::NE;
   __syncwarp();
@@ -2318,7 +2325,7 @@ __device__ __noinline__ void esk_flush(const EskParams& e, float* acc, int hbz, 
 // One particle's fixed-point Esirkepov values straight to HBM (a lane
 // outside its warp's held block).
 template <int K>
-__device__ __noinline__ void esk_direct(const EskParams& e, int bz, int bx, const float* s0z,
+__device__ __noinline__ void esk_direct(const EskOut e, int bz, int bx, const float* s0z,
                                         const float* dsz, const float* s0x, const float* dsx,
                                         float uyg) {
   constexpr int W = K + 2;
@@ -2356,6 +2363,9 @@ template <int K, bool kClock>
 #ifndef LBX_ESK_MINB
 #define LBX_ESK_MINB 2
 #endif
+#ifndef LBX_ESK_PREFETCH
+#define LBX_ESK_PREFETCH 1
+#endif
 __global__ void __launch_bounds__(kEB, LBX_ESK_MINB) pic_esk_kernel(EskParams e) {
   constexpr int W = K + 2;                 // window nodes per axis
   const PicParams& p = e.b;
@@ -2368,8 +2378,9 @@ __global__ void __launch_bounds__(kEB, LBX_ESK_MINB) pic_esk_kernel(EskParams e)
   const long long n = sh.n;
   const double ez = (double)p.nz, ex = (double)p.nx;
   const float hf = (float)(0.5 * p.qm * p.dt), dtf = (float)p.dt;
-  unsigned long long removed = 0;
-  long long first_out = LLONG_MAX, err = 0;
+  unsigned removed = 0;                          // per lane: 32 bits (register pressure)
+  long long first_out = LLONG_MAX;
+  int err = 0;
   // A warp takes chunks of kEskRun x 32 consecutive particles and holds a
   // node block in shared memory: every lane keeps its own float sums
   // (acc[node][lane], conflict-free) of the Esirkepov values of its
@@ -2387,20 +2398,34 @@ __global__ void __launch_bounds__(kEB, LBX_ESK_MINB) pic_esk_kernel(EskParams e)
   __syncwarp();
   int hbz = INT_MIN / 2, hbx = INT_MIN / 2;   // held window (block origin: hbz - 1, hbx - 1)
   auto flush = [&]() {
-    if (hbz != INT_MIN / 2) esk_flush<K>(e, acc, hbz, hbx, lane);
+    if (hbz != INT_MIN / 2) esk_flush<K>(e.o, acc, hbz, hbx, lane);
   };
   const long long chunk = (long long)kEskRun * 32;
+  // the next 32 particles' loads are issued before this iteration's work
+  // (LBX_ESK_PREFETCH): their HBM latency hides behind the gather / deposit
+  double nz0 = 0.0, nx0 = 0.0, nuz = 0.0, nux = 0.0, nuy = 0.0;
+  auto load = [&](long long w) {
+    // particle loads bypass L1 (the row-quad gathers live there)
+    const long long ic = min(w + lane, n - 1);
+    nz0 = ld_na(p.z + ic);
+    nx0 = ld_na(p.x + ic);
+    nuz = ld_na(p.uz + ic);
+    nux = ld_na(p.ux + ic);
+    nuy = ld_na(p.uy + ic);
+  };
   for (long long c0 = ((long long)blockIdx.x * (kEB / 32) + warp) * chunk; c0 < n;
-       c0 += (long long)gridDim.x * (kEB / 32) * chunk)
-  for (long long w0 = c0; w0 < min(n, c0 + chunk); w0 += 32) {
+       c0 += (long long)gridDim.x * (kEB / 32) * chunk) {
+  const long long wend = min(n, c0 + chunk);
+  if (LBX_ESK_PREFETCH) load(c0);
+  for (long long w0 = c0; w0 < wend; w0 += 32) {
     const long long i = w0 + lane;
     const bool valid = i < n;
     long long t0 = 0;
     if (kClock) t0 = clock64();
-    const long long ic = valid ? i : n - 1;
-    // particle loads bypass L1 (the row-quad gathers live there)
-    const double z0 = ld_na(p.z + ic), x0 = ld_na(p.x + ic);
-    double uz = ld_na(p.uz + ic), ux = ld_na(p.ux + ic), uy = ld_na(p.uy + ic);
+    if (!LBX_ESK_PREFETCH) load(w0);
+    const double z0 = nz0, x0 = nx0;
+    double uz = nuz, ux = nux, uy = nuy;
+    if (LBX_ESK_PREFETCH && w0 + 32 < wend) load(w0 + 32);
     // staggers: (0, 1/2) Ex Bz | (0, 0) Ey | (1/2, 0) Ez Bx | (1/2, 1/2) By
     // weights of the four stagger positions, once each
     float wz0[K + 1], wzh[K + 1], wx0[K + 1], wxh[K + 1];
@@ -2493,7 +2518,7 @@ __global__ void __launch_bounds__(kEB, LBX_ESK_MINB) pic_esk_kernel(EskParams e)
         for (int j = 0; j < W; ++j) ay[(ii * Blk::YC + j) * 32] += __fmaf_rn(a1, dsx[j], a0 * s0x[j]);
       }
     } else if (keep) {   // outside the block: this particle's values straight to HBM
-      esk_direct<K>(e, bz, bx, s0z, dsz, s0x, dsx, uyg);
+      esk_direct<K>(e.o, bz, bx, s0z, dsz, s0x, dsx, uyg);
     }
     // ---- per-box survivor counts (+ GpuClock: the particle's whole work) ----
     int box = -1;
@@ -2516,6 +2541,7 @@ __global__ void __launch_bounds__(kEB, LBX_ESK_MINB) pic_esk_kernel(EskParams e)
       atomicAdd(s_cnt + box, 1u);
       if (kClock) atomicAdd(s_clk + box, dt);
     }
+  }
   }
   flush();
   push_epilogue<kClock>(p, sh, n, removed, first_out, err, INT_MAX, INT_MIN, INT_MAX, INT_MIN,
@@ -2682,11 +2708,11 @@ int pic_step_esirkepov(lbx_ctx* ctx, const lbx_pic_args* a, cudaStream_t s) {
     esk_rows_kernel<<<rg, 256, 0, s>>>(a->fields[0], a->fields[1], a->fields[2], a->fields[3],
                                        a->fields[4], a->fields[5], R, a->nz, a->nx);
   }
-  e.J = ctx->pic_esk;
-  e.stride = stride;
-  e.apitch = apitch;
-  e.cz = (float)(-(a->q_times_w / a->dt) * jscale);
-  e.cy = (float)(a->q_times_w * jscale);
+  e.o.J = ctx->pic_esk;
+  e.o.stride = stride;
+  e.o.apitch = apitch;
+  e.o.cz = (float)(-(a->q_times_w / a->dt) * jscale);
+  e.o.cy = (float)(a->q_times_w * jscale);
   const bool clock = (a->flags & LBX_STEP_CLOCK) != 0;
   void (*kern)(EskParams) = nullptr;
   switch (K) {
