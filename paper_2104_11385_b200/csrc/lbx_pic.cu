@@ -461,7 +461,7 @@ __device__ __forceinline__ void push_epilogue(const PicParams& p, PushShared& sh
                                               const unsigned* s_clk) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned long long wa = (unsigned long long)warp_sum((long long)removed);
-  const long long wm = warp_min(first_out), we = warp_sum(err);
+  const long long wm = warp_min(first_out), we = warp_sum((long long)err);
   const int wimin = __reduce_min_sync(kAll, bimin), wimax = __reduce_max_sync(kAll, bimax);
   const int wjmin = __reduce_min_sync(kAll, bjmin), wjmax = __reduce_max_sync(kAll, bjmax);
   if (lane == 0) {
@@ -532,8 +532,9 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_push_kernel(PicParams p
   const long long units = (n + kUnitP - 1) / kUnitP;
   const double ez = (double)p.nz, ex = (double)p.nx;
   const double h = 0.5 * p.qm * p.dt;
-  unsigned long long removed = 0;
-  long long first_out = LLONG_MAX, err = 0;
+  unsigned removed = 0;                          // per lane: 32 bits (register pressure)
+  long long first_out = LLONG_MAX;
+  int err = 0;
   int bimin = INT_MAX, bimax = INT_MIN, bjmin = INT_MAX, bjmax = INT_MIN;
 
   for (long long u = (long long)blockIdx.x * kPW + warp; u < units;
@@ -1441,8 +1442,9 @@ __global__ void __launch_bounds__(kPB, LBX_PIC_MINB) pic_tile_kernel(PicParams p
   const long long n = s_n;
   const double ez = (double)p.nz, ex = (double)p.nx;
   const double h = 0.5 * p.qm * p.dt;
-  unsigned long long removed = 0;
-  long long first_out = LLONG_MAX, err = 0;
+  unsigned removed = 0;                          // per lane: 32 bits (register pressure)
+  long long first_out = LLONG_MAX;
+  int err = 0;
   int bimin = INT_MAX, bimax = INT_MIN, bjmin = INT_MAX, bjmax = INT_MIN;
 
   for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
