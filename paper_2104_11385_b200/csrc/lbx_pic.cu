@@ -2202,6 +2202,16 @@ __device__ __forceinline__ int bweights(double v, float w[K + 1]) {
   return (int)fl + 1;
 }
 
+#ifndef LBX_ESK_F2
+#define LBX_ESK_F2 0   // 1: Esirkepov gather / deposit arithmetic in packed f32x2 ops (measured slower per step, off)
+#endif
+// shared-memory adds of two nodes' values: two LDS, one FADD2, two STS
+__device__ __forceinline__ void sadd2(float* a, int o1, float2 v) {
+  const float2 t = __fadd2_rn(make_float2(a[0], a[o1]), v);
+  a[0] = t.x;
+  a[o1] = t.y;
+}
+
 // Row-quad gather: R[(r + 1) * rpitch + (c + 1)] = the padded field values
 // (r, c .. c + 3) (zeros outside the array), so a shape-K gather is K + 1
 // 16-byte loads instead of (K + 1)^2 scalar loads.
@@ -2211,14 +2221,29 @@ __device__ __forceinline__ float gather_rows(const float4* __restrict__ R, int r
                                              const float wx[K + 1]) {
   const float4* q = R + (long long)(bz + 2) * rpitch + (bx + 2);   // padded row bz + 1, col bx + 1
   float acc = 0.f;
+  if constexpr (LBX_ESK_F2 && K % 2 == 1) {
+    // two rows' sums per packed f32x2 op; each lane of an FFMA2 rounds as
+    // the scalar FFMA does, and the row chain keeps its order: same bits
 #pragma unroll
-  for (int k = 0; k <= K; ++k) {
-    const float4 v = __ldg(q + (long long)k * rpitch);
-    float rs = wx[0] * v.x;
-    rs = __fmaf_rn(wx[1], v.y, rs);
-    if (K >= 2) rs = __fmaf_rn(wx[2], v.z, rs);
-    if (K >= 3) rs = __fmaf_rn(wx[3], v.w, rs);
-    acc = __fmaf_rn(wz[k], rs, acc);
+    for (int k = 0; k <= K; k += 2) {
+      const float4 v = __ldg(q + (long long)k * rpitch), u = __ldg(q + (long long)(k + 1) * rpitch);
+      float2 rs = __fmul2_rn(make_float2(wx[0], wx[0]), make_float2(v.x, u.x));
+      rs = __ffma2_rn(make_float2(wx[1], wx[1]), make_float2(v.y, u.y), rs);
+      if (K >= 2) rs = __ffma2_rn(make_float2(wx[2], wx[2]), make_float2(v.z, u.z), rs);
+      if (K >= 3) rs = __ffma2_rn(make_float2(wx[3], wx[3]), make_float2(v.w, u.w), rs);
+      acc = __fmaf_rn(wz[k], rs.x, acc);
+      acc = __fmaf_rn(wz[k + 1], rs.y, acc);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k <= K; ++k) {
+      const float4 v = __ldg(q + (long long)k * rpitch);
+      float rs = wx[0] * v.x;
+      rs = __fmaf_rn(wx[1], v.y, rs);
+      if (K >= 2) rs = __fmaf_rn(wx[2], v.z, rs);
+      if (K >= 3) rs = __fmaf_rn(wx[3], v.w, rs);
+      acc = __fmaf_rn(wz[k], rs, acc);
+    }
   }
   return acc;
 }
@@ -2492,6 +2517,70 @@ __global__ void __launch_bounds__(kEB, LBX_ESK_MINB) pic_esk_kernel(EskParams e)
       float* az = acc + (oz * Blk::ZC + ox) * 32 + lane;
       float* ax = acc + (Blk::NZ + oz * Blk::XC + ox) * 32 + lane;
       float* ay = acc + (Blk::NZ + Blk::NX + oz * Blk::YC + ox) * 32 + lane;
+      if (LBX_ESK_F2) {
+        // the same values, two window nodes per packed op (j pairs for Jz /
+        // Jy, ii pairs for Jx); each lane of a pair rounds as before
+        constexpr int WP = W & ~1;             // paired part; node W-1 alone when W is odd
+#pragma unroll
+        for (int j = 0; j < WP; j += 2) {
+          const float2 hx = __ffma2_rn(make_float2(0.5f, 0.5f), make_float2(dsx[j], dsx[j + 1]),
+                                       make_float2(s0x[j], s0x[j + 1]));
+          float2 a = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int ii = 0; ii <= K; ++ii) {
+            a = __ffma2_rn(make_float2(dsz[ii], dsz[ii]), hx, a);
+            sadd2(az + (ii * Blk::ZC + j) * 32, 32, a);
+          }
+        }
+        if (W & 1) {
+          const int j = W - 1;
+          const float hx = __fmaf_rn(0.5f, dsx[j], s0x[j]);
+          float a = 0.f;
+#pragma unroll
+          for (int ii = 0; ii <= K; ++ii) {
+            a = __fmaf_rn(dsz[ii], hx, a);
+            az[(ii * Blk::ZC + j) * 32] += a;
+          }
+        }
+#pragma unroll
+        for (int ii = 0; ii < WP; ii += 2) {
+          const float2 hz = __ffma2_rn(make_float2(0.5f, 0.5f), make_float2(dsz[ii], dsz[ii + 1]),
+                                       make_float2(s0z[ii], s0z[ii + 1]));
+          float2 a = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int j = 0; j <= K; ++j) {
+            a = __ffma2_rn(make_float2(dsx[j], dsx[j]), hz, a);
+            sadd2(ax + (ii * Blk::XC + j) * 32, Blk::XC * 32, a);
+          }
+        }
+        if (W & 1) {
+          const int ii = W - 1;
+          const float hz = __fmaf_rn(0.5f, dsz[ii], s0z[ii]);
+          float a = 0.f;
+#pragma unroll
+          for (int j = 0; j <= K; ++j) {
+            a = __fmaf_rn(dsx[j], hz, a);
+            ax[(ii * Blk::XC + j) * 32] += a;
+          }
+        }
+#pragma unroll
+        for (int ii = 0; ii < W; ++ii) {
+          // (a0, a1) = uyg * (s0z + dsz/2, s0z/2 + dsz/3)
+          const float2 a01 = __fmul2_rn(make_float2(uyg, uyg),
+                                        __ffma2_rn(make_float2(0.5f, 1.f / 3.f), make_float2(dsz[ii], dsz[ii]),
+                                                   make_float2(s0z[ii], 0.5f * s0z[ii])));
+#pragma unroll
+          for (int j = 0; j < WP; j += 2) {
+            const float2 t = __fmul2_rn(make_float2(a01.x, a01.x), make_float2(s0x[j], s0x[j + 1]));
+            sadd2(ay + (ii * Blk::YC + j) * 32, 32,
+                  __ffma2_rn(make_float2(a01.y, a01.y), make_float2(dsx[j], dsx[j + 1]), t));
+          }
+          if (W & 1) {
+            const int j = W - 1;
+            ay[(ii * Blk::YC + j) * 32] += __fmaf_rn(a01.y, dsx[j], a01.x * s0x[j]);
+          }
+        }
+      } else {
 #pragma unroll
       for (int j = 0; j < W; ++j) {
         const float hx = __fmaf_rn(0.5f, dsx[j], s0x[j]);
@@ -2518,6 +2607,7 @@ __global__ void __launch_bounds__(kEB, LBX_ESK_MINB) pic_esk_kernel(EskParams e)
         const float a1 = __fmul_rn(uyg, __fmaf_rn(1.f / 3.f, dsz[ii], 0.5f * s0z[ii])); // s0z/2 + dsz/3
 #pragma unroll
         for (int j = 0; j < W; ++j) ay[(ii * Blk::YC + j) * 32] += __fmaf_rn(a1, dsx[j], a0 * s0x[j]);
+      }
       }
     } else if (keep) {   // outside the block: this particle's values straight to HBM
       esk_direct<K>(e.o, bz, bx, s0z, dsz, s0x, dsx, uyg);
